@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: GPT-2 block-stack training step (fwd + bwd + Adam) on 1..8 B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config small] [--impl nnt|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: NCCL, one rank per GPU)
+
+Metric (BASELINE.json): GPT-2 train tokens/s (+ model TFLOP/s, % of bf16 peak).
+A step = one pass of the whole hot path over one synthetic batch per GPU: L
+pre-LN GPT-2 blocks forward, the linear-probe loss, L blocks backward, the DP
+gradient all-reduce (N > 1) and Adam on every parameter.  Weak scaling: each
+GPU holds B = 8 sequences of S = 1024 tokens.  The per-step working set
+(activations of 12 layers, several GB) is far larger than the 126 MB L2, so no
+explicit flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, fp64 NumPy) on the box's host
+cores on a bounded sample of the same workload (one block, one sequence).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {  # name -> (L, E, H, S, B per GPU)
+    "tiny": (1, 64, 2, 32, 2),
+    "small": (12, 768, 12, 1024, 8),
+    "large": (36, 1280, 20, 1024, 8),
+    "xl": (48, 1600, 25, 1024, 8),
+    "wide": (1, 8192, 128, 1024, 8),
+}
+METRIC = "GPT-2 train tokens/s & model TFLOP/s at 1/2/4/8 B200; % of bf16 peak"
+
+
+def model_flops_per_step(L, E, S, T):
+    """6 N T + 12 L S E T with N = 12 E^2 per layer (blocks only; full attention counted)."""
+    return L * T * (72 * E * E + 12 * S * E)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm=d["hbm_gbs"], bf16=d["bf16_tflops"], bf16_sus=d.get("bf16_tflops_sustained", d["bf16_tflops"]),
+                    src="measured")
+    return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons, power = [], [], set(), []
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        with open(self.f.name) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx.append(float(parts[2]))
+                    power.append(float(parts[3]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        os.unlink(self.f.name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(mx), "power_w_max": max(power),
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- CPU oracle timing
+def oracle_block_sample(E, H, S, seq=1, reps=None, budget_s=15.0):
+    """Time the oracle (as it stands) on one block fwd+bwd+Adam over `seq` sequences of S tokens."""
+    import nnt_inputs
+    from oracle import dense
+    P = {k: v.astype(np.float64) for k, v in nnt_inputs.make_params(E, seed=1234, init="gpt2").items()}
+    x = nnt_inputs.make_x(E, S, 0, seq, seed=1001).astype(np.float64)
+    r = nnt_inputs.make_r(E, S, 0, seq, seed=1001).astype(np.float64)
+
+    def one():
+        y, cache = dense.block_fwd(P, x, H)
+        dense.probe_loss(y, r, seq * S)
+        _, g = dense.block_bwd(P, cache, dense.probe_loss_grad(r, seq * S))
+        for k in P:
+            dense.adam_step(P[k], g[k], np.zeros_like(P[k]), np.zeros_like(P[k]), 1)
+
+    t0 = time.perf_counter()
+    one()
+    t1 = time.perf_counter() - t0
+    n = reps if reps is not None else max(1, min(20, int(budget_s / max(t1, 1e-3))))
+    times = [t1]
+    for _ in range(n - 1):
+        t0 = time.perf_counter()
+        one()
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times)), len(times)
+
+
+def host_cores():
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count()
+    threads = None
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        threads = max((i.get("num_threads", 0) for i in info), default=None)
+    except Exception:
+        pass
+    return n, threads
+
+
+def oracle_sample_shape(E):
+    # bounded CPU sample: one sequence; shorter for the very wide shape
+    return 1024 if E <= 1600 else 256
+
+
+# ---------------------------------------------------------------- arms
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, bounded samples of the workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    L, E, H, S, B = CONFIGS[args.config]
+    Ss = min(S, oracle_sample_shape(E))
+    for _ in range(args.warmup):
+        oracle_block_sample(E, H, Ss, reps=1)
+    times = []
+    for _ in range(args.steps):
+        t, _ = oracle_block_sample(E, H, Ss, reps=1)
+        times.append(t)
+    t = float(np.mean(times))
+    # one sample = one block over Ss tokens; a full-model token needs L blocks
+    value = Ss / (t * L)
+    cores, threads = host_cores()
+    sample = f"one block fwd+bwd+Adam, 1 sequence x {Ss} tokens, E={E}, H={H}, fp64 NumPy; tokens/s scaled by 1/L (L={L})"
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"gpt2-{args.config} block stack fwd+bwd+Adam (oracle sample)", "layers": L,
+                      "d_model": E, "heads": H, "seq_len": S},
+           "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads or cores, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+def run_nnt(args):
+    import torch
+    import torch.distributed as dist
+
+    import nnt_inputs
+    from paper_2504_13236_b200 import model, nnt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist.group.WORLD
+    nnt.nnt_device_check(local)
+    L, E, H, S, B = CONFIGS[args.config]
+    dtype = "f32" if args.config == "tiny" else "bf16"
+    tile = 16 if args.config == "tiny" else 1024
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype)
+    layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+    st = model.BlockStack(sc, layers, process_group=pg, global_tokens=B * S * world)
+    del layers
+    # rank r's batch tiles of the global batch (nnt_partition), two distinct synthetic batches
+    b0, b1 = nnt.nnt_partition(B * world, world, rank)
+    batches = []
+    for i in range(2):
+        x = nnt_inputs.make_x(E, S, b0, b1, seed=1000 + i)
+        r = nnt_inputs.make_r(E, S, b0, b1, seed=1000 + i)
+        batches.append((torch.from_numpy(x).pin_memory(), torch.from_numpy(r).pin_memory()))
+    dev_batches = [(x.cuda(), r.cuda()) for x, r in batches]
+    T = B * S
+    peaks = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        x, r = dev_batches[i % 2]
+        st.train_step(x, r)
+    torch.cuda.synchronize()
+
+    # ---------------- timed region: device-resident inputs
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.2)
+    n0 = nnt.nnt_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.steps):
+        x, r = dev_batches[i % 2]
+        st.train_step(x, r)
+    e1.record()
+    torch.cuda.synchronize()
+    launches = nnt.nnt_launch_count() - n0
+    barrier()
+    clocks = sampler.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    loss = float(st.loss.item())
+
+    # ---------------- per-kernel timing (CUDA events around every libnnt launch), same steps again
+    nnt.nnt_timing_enable(True)
+    for i in range(args.steps):
+        x, r = dev_batches[i % 2]
+        st.train_step(x, r)
+    torch.cuda.synchronize()
+    kt = nnt.nnt_timing_read()
+    nnt.nnt_timing_enable(False)
+
+    # ---------------- end to end: pinned host inputs copied every step, loss read back every step
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for i in range(args.steps):
+        x, r = batches[i % 2]
+        lv = st.train_step(x, r).item()
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(max(f0.elapsed_time(f1), 1000 * (time.perf_counter() - t0)) / args.steps)
+    h2d = batches[0][0].numel() * 4 * 2
+    d2h = 4
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    tokens = T * world
+    value = tokens / (ms / 1e3)
+    mflops = model_flops_per_step(L, E, S, T) * world
+    model_tflops = mflops / (ms / 1e3) / 1e12
+    # roofline of the dominant kernel class
+    steps = args.steps
+    kernels = {}
+    total_k = sum(v["ms"] for v in kt.values())
+    for k, v in kt.items():
+        if v["launches"] == 0:
+            continue
+        tensor = k == "gemm_tc"
+        ach = (v["flops"] / (v["ms"] / 1e3) / 1e12) if tensor else (v["bytes"] / (v["ms"] / 1e3) / 1e9)
+        peak = peaks["bf16_sus"] if tensor else peaks["hbm"]
+        kernels[k] = {"ms_per_step": v["ms"] / steps, "share": v["ms"] / total_k, "launches_per_step": v["launches"] / steps,
+                      "bound": "tensor" if tensor else "hbm", "achieved": ach,
+                      "unit": "TFLOP/s" if tensor else "GB/s", "frac": ach / peak}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_per_step"])
+    d = kernels[dom]
+    roof = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
+            "peak": peaks["bf16_sus"] if d["bound"] == "tensor" else peaks["hbm"], "unit": d["unit"],
+            "frac": d["frac"], "traffic": None, "peak_source": peaks["src"] +
+            (" bf16_tflops_sustained (kernel timed inside a long step)" if d["bound"] == "tensor" else " hbm_gbs"),
+            "timing": "CUDA events around every launch on its stream, K steps after the timed region",
+            "share_of_step": d["share"]}
+    out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded N(0,1) activations, GPT-2 init weights)",
+           "config": {"workload": f"gpt2-{args.config}: {L} pre-LN GPT-2 blocks fwd+bwd+Adam (block stack; "
+                                  f"embeddings/LM head are NEXT f1)",
+                      "model": f"gpt2-{args.config}-blocks", "layers": L, "d_model": E, "heads": H,
+                      "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}",
+                      "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
+           "model_tflops": model_tflops, "model_tflops_frac_of_bf16": model_tflops / peaks["bf16"],
+           "loss": loss, "gpu_launches": int(launches),
+           "clocks": clocks, "roofline": roof, "kernels": kernels,
+           "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}}
+    if world == 1 and not args.no_cpu_baseline:
+        Ss = min(S, oracle_sample_shape(E))
+        t, n = oracle_block_sample(E, H, Ss)
+        cores, threads = host_cores()
+        out["cpu_baseline"] = {"value": Ss / (t * L), "unit": "tokens/s", "cores": threads or cores,
+                               "kind": "oracle",
+                               "sample": f"{n} x one block fwd+bwd+Adam over 1 sequence x {Ss} tokens (E={E}, H={H}, "
+                                         f"fp64 NumPy), median {t:.2f} s; tokens/s scaled by 1/L (L={L})"}
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="nnt", choices=["nnt", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_nnt(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,380 @@
+/*
+ * nnt.h — C ABI of libnnt.so, the B200 (sm_100a) hot path of NNTile's
+ * data-parallel GPT-2 block (arXiv 2504.13236).
+ *
+ * Citations: "P:n" = /root/reference/PAPER.md line n; "S:n" = SPEC.md line n
+ * (interfaces/test ideas only); "Rk" = reading k in DESIGN.md §Readings.
+ *
+ * General conventions (apply to every entry point unless stated otherwise)
+ * -----------------------------------------------------------------------
+ *  - C linkage, no exceptions cross the ABI.  Every call returns nnt_status.
+ *    On failure the thread-local nnt_last_error() holds a one-line message.
+ *  - Validation happens before any launch: a call that returns an error has
+ *    enqueued NOTHING.  Fail fast, first error wins.
+ *  - Ownership: the caller owns all memory.  Pointers marked "device" must be
+ *    device memory of the current CUDA device; pointers marked "host" are host
+ *    memory.  The library never allocates or frees device memory on the hot
+ *    path; scratch/saved workspaces are caller-provided and sized by the
+ *    *_bytes / *_size functions.
+ *  - Asynchrony: every device-touching call is asynchronous on the given
+ *    stream (a cudaStream_t; NULL = legacy default stream) and does not
+ *    synchronise the host.
+ *  - Layout: row-major; leading dimensions ("ld") and strides in ELEMENTS.
+ *    Tensors that feed the tensor-core path need 16-byte aligned base
+ *    pointers and leading dimensions / batch strides whose byte size is a
+ *    multiple of 16 (TMA requirement) — else NNT_ERR_ALIGN.
+ *  - dtypes: NNT_F32 (fp32 path: SIMT FFMA, true fp32) and NNT_BF16 (bf16
+ *    operands on tcgen05 tensor cores, fp32 accumulation) (R15).
+ *  - Tiles: tensors are split into tiles with a tile shape; a
+ *    tile larger than its dimension is clamped; tile <= 0 is
+ *    NNT_ERR_TILE.  Logical tiles define the tile-task grid (nnt_block_dag_*);
+ *    one kernel launch executes every independent tile task of a level, so
+ *    results do not depend on the tile shape beyond floating-point rounding
+ *    order (tile invariance, tests/test_gpu_*).
+ */
+#ifndef NNT_H_
+#define NNT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NNT_ABI_VERSION 1
+
+/* Causal write/read alignment of attention-probability rows (see nnt_softmax). */
+#define NNT_CAUSAL_ALIGN 128
+
+typedef struct CUstream_st* nnt_stream_t; /* == cudaStream_t */
+typedef struct CUevent_st* nnt_event_t;   /* == cudaEvent_t  */
+
+typedef enum {
+  NNT_OK = 0,
+  NNT_ERR_NULL = 1,        /* required pointer is NULL                        */
+  NNT_ERR_SHAPE = 2,       /* non-positive or inconsistent dimension          */
+  NNT_ERR_TILE = 3,        /* non-positive tile size                          */
+  NNT_ERR_DTYPE = 4,       /* unsupported dtype / dtype combination           */
+  NNT_ERR_ALIGN = 5,       /* pointer / leading-dimension alignment violated  */
+  NNT_ERR_UNSUPPORTED = 6, /* valid request outside what the library implements */
+  NNT_ERR_WORKSPACE = 7,   /* caller workspace too small                      */
+  NNT_ERR_CUDA = 8,        /* a CUDA runtime/driver call failed               */
+  NNT_ERR_ARG = 9          /* other invalid argument (enum out of range, ...) */
+} nnt_status;
+
+typedef enum { NNT_F32 = 0, NNT_BF16 = 1 } nnt_dtype;
+typedef enum { NNT_NOTRANS = 0, NNT_TRANS = 1 } nnt_trans;
+
+/* ------------------------------------------------------------------------- */
+/* Library / device                                                           */
+/* ------------------------------------------------------------------------- */
+int nnt_abi_version(void);
+const char* nnt_last_error(void);
+/* NNT_OK iff `device` is compute capability 10.0 (sm_100a SASS in this library). */
+nnt_status nnt_device_check(int device);
+
+/* ------------------------------------------------------------------------- */
+/* Tile bookkeeping (host only, integer, bit-exact) — P:72-75          */
+/* ------------------------------------------------------------------------- */
+/* grid[d] = ceil(shape[d] / min(tile[d], shape[d])).  host arrays of length ndim. */
+nnt_status nnt_tile_grid(int ndim, const int64_t* shape, const int64_t* tile, int64_t* grid);
+/* offset / extent of tile `idx` along one axis: extent = min(t, dim - idx*t), t = min(tile, dim). */
+nnt_status nnt_tile_extent(int64_t dim, int64_t tile, int64_t idx, int64_t* offset, int64_t* extent);
+/* Batch tiles owned by rank r of R: [floor(r n / R), floor((r+1) n / R)). */
+nnt_status nnt_partition(int64_t n_units, int n_ranks, int rank, int64_t* begin, int64_t* end);
+
+/* ------------------------------------------------------------------------- */
+/* Tiled GEMM — linear layer Y = W X +. b, attention products     */
+/* (P:181).                                                                   */
+/* ------------------------------------------------------------------------- */
+typedef enum {
+  NNT_CAUSAL_NONE = 0,
+  /* Only C[i][j] with j <= i is required; C entries with j > i may be left
+   * untouched or hold arbitrary finite values (attention scores, dP).       */
+  NNT_CAUSAL_OUT_LOWER = 1,
+  /* op(A) is lower triangular (op(A)[i][k] == 0 for k > i): the kernel may
+   * skip the zero K-blocks.  Result = the full product (P·V, dA·K).         */
+  NNT_CAUSAL_A_LOWER = 2,
+  /* op(A) is upper triangular (op(A)[i][k] == 0 for k < i): zero K-blocks
+   * may be skipped (P^T·dO, dA^T·Q).                                         */
+  NNT_CAUSAL_A_UPPER = 3
+} nnt_causal;
+
+typedef enum {
+  NNT_ACT_NONE = 0,
+  NNT_ACT_GELU = 1,     /* aux <- pre ; C <- gelu(pre)           (R11) */
+  NNT_ACT_GELU_BWD = 2  /* C <- pre * gelu'(aux)                  (R18)          */
+} nnt_act;
+
+typedef struct {
+  const float* bias;      /* device fp32 [N] added to every row, or NULL          */
+  const float* residual;  /* device fp32 [M][ld_residual] added, or NULL (may alias C
+                             only when C is fp32 with ldc == ld_residual)          */
+  int64_t ld_residual;
+  int act;                /* nnt_act                                               */
+  void* aux;              /* device, same dtype as C, [M][ld_aux]: GELU pre-activation
+                             (written by NNT_ACT_GELU, read by NNT_ACT_GELU_BWD)    */
+  int64_t ld_aux;
+  int causal;             /* nnt_causal (applies per batch item)                   */
+} nnt_epilogue;
+
+/*
+ * C = epilogue( alpha * op(A) · op(B) ),  for each of batch[0]*batch[1] items.
+ *   pre = alpha * sum_k op(A)[i][k] op(B)[k][j]  (+ bias[j]) (+ beta * C_old[i][j])
+ *         (+ residual[i][j]);  C = act(pre).
+ * op(A) is M x K: A is stored [M][lda] if trans_a == NNT_NOTRANS, [K][lda] if NNT_TRANS.
+ * op(B) is K x N: B is stored [K][ldb] if trans_b == NNT_NOTRANS, [N][ldb] if NNT_TRANS.
+ * Batch item (p, q) uses A + p*stride_a[0] + q*stride_a[1] (elements), likewise B, C
+ * (strides may be 0; batch/strides may be NULL for a single item).  This is how
+ * attention's (N_b, N_h) views of the fused [N_b, N_s, 3, N_h, h] QKV buffer are
+ * addressed without copies.
+ * dtypes: (A,B) both NNT_F32 (SIMT fp32 path) or both NNT_BF16 (tcgen05 path);
+ * C NNT_F32 or NNT_BF16.  Accumulation is fp32 over K in ascending order, i.e. the
+ * K-tile Reduce of the tiled GEMM in a fixed, deterministic order.
+ * tile: host int64[3] logical tile (tile_m, tile_n, tile_k); NULL = untiled.
+ */
+nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
+                         const int64_t* batch,
+                         float alpha,
+                         const void* A, int a_dtype, int64_t lda, const int64_t* stride_a,
+                         const void* B, int b_dtype, int64_t ldb, const int64_t* stride_b,
+                         float beta,
+                         void* C, int c_dtype, int64_t ldc, const int64_t* stride_c,
+                         const int64_t* tile, const nnt_epilogue* epi, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* SoftMax as two subroutines                                     */
+/* ------------------------------------------------------------------------- */
+/*
+ * Subroutine 1: for every slice (row) r of x (device fp32 [rows][ldx])
+ * over columns [0, cols): per key tile of tile_k columns the partial
+ * (m_j = max, s_j = sum e^{x - m_j}), merged in ascending tile order with
+ * (m,s)(+)(m',s') = (M, s e^{m-M} + s' e^{m'-M}); (-inf, 0) is the identity (R10).
+ * causal != 0: row r is query q = r % seq_q and columns k > q are excluded (R2).
+ * stats: device fp32 [rows][2] = (max, sumexp).  accumulate != 0 merges the
+ * result into the existing stats instead of overwriting (one call per key tile).
+ */
+nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx,
+                         int64_t tile_k, int causal, int64_t seq_q,
+                         float* stats, int accumulate, nnt_stream_t stream);
+
+/*
+ * Subroutine 2: y[r][k] = e^{x[r][k] - M_r} / S_r with (M_r, S_r) = stats[r].
+ * y is device fp32 or bf16 [rows][ldy].  causal != 0: entries with k > q are written
+ * as 0 for k < min(cols, roundup(q+1, NNT_CAUSAL_ALIGN)) and not written beyond;
+ * x entries with k > q are never read.
+ */
+nnt_status nnt_softmax(const float* x, int64_t rows, int64_t cols, int64_t ldx, int64_t tile_k,
+                       int causal, int64_t seq_q, const float* stats,
+                       void* y, int y_dtype, int64_t ldy, nnt_stream_t stream);
+
+/*
+ * Softmax backward (R18): da = scale * P ⊙ (dP − D), D[r] = sum_k P[r][k] dP[r][k].
+ * p: device fp32/bf16 [rows][ldp]; dp: device fp32 [rows][lddp]; da: device
+ * fp32/bf16 [rows][ldda].  causal: same read/write extents as nnt_softmax
+ * (masked entries written as exact 0; dP above the diagonal is never read).
+ */
+nnt_status nnt_softmax_bwd(const void* p, int p_dtype, int64_t ldp,
+                           const float* dp, int64_t lddp,
+                           int64_t rows, int64_t cols, int causal, int64_t seq_q, float scale,
+                           void* da, int da_dtype, int64_t ldda, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* LayerNorm in three steps                                       */
+/* ------------------------------------------------------------------------- */
+/*
+ * For every token row t of x (device fp32 [T][ldx]) over E columns:
+ *   step 1, per E-tile of tile_e columns: shifted sums S1 = sum (x - c), S2 = sum (x - c)^2
+ *           with c = x[t][0]; merged over tiles in ascending order (R9);
+ *           mean = c + S1/E, var = max(S2/E - (S1/E)^2, 0), rstd = 1/sqrt(var + eps);
+ *   step 2: xhat = (x - mean) * rstd;   step 3: y = gamma * xhat + beta.
+ * y: device fp32/bf16 [T][ldy]; mean, rstd: device fp32 [T] (saved for backward).
+ */
+nnt_status nnt_layernorm_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, int64_t tile_e,
+                             const float* gamma, const float* beta, float eps,
+                             void* y, int y_dtype, int64_t ldy,
+                             float* mean, float* rstd, nnt_stream_t stream);
+
+/* Scratch bytes nnt_layernorm_bwd needs for its ordered dgamma/dbeta partials. */
+size_t nnt_layernorm_bwd_scratch_bytes(int64_t T, int64_t E);
+
+/*
+ * LayerNorm backward (R18):
+ *   dxhat = dy * gamma;  dx = dres + rstd * (dxhat - mean_e dxhat - xhat * mean_e(dxhat xhat))
+ *   dgamma (+)= sum_t dy * xhat;  dbeta (+)= sum_t dy   (column partials over row
+ *   chunks, merged in ascending chunk order: deterministic).
+ * dy: device fp32 [T][lddy]; x, mean, rstd, gamma as in the forward; dres: device
+ * fp32 [T][lddx] or NULL (residual-stream gradient added to dx; may alias dx);
+ * dx: device fp32 [T][lddx]; dx_bf16: device bf16 [T][lddx] copy of dx or NULL;
+ * dgamma, dbeta: device fp32 [E]; accumulate_params != 0 adds into them.
+ */
+nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int64_t ldx,
+                             const float* mean, const float* rstd, const float* gamma,
+                             int64_t T, int64_t E,
+                             const float* dres, float* dx, int64_t lddx, void* dx_bf16,
+                             float* dgamma, float* dbeta, int accumulate_params,
+                             void* scratch, size_t scratch_bytes, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Elementwise GELU (R11 tanh form)                                */
+/* ------------------------------------------------------------------------- */
+/* y[i] = gelu(x[i]); x, y device arrays of n elements of `dtype`. */
+nnt_status nnt_gelu_fwd(const void* x, void* y, int dtype, int64_t n, nnt_stream_t stream);
+/* dx[i] = dy[i] * gelu'(x[i]). */
+nnt_status nnt_gelu_bwd(const void* x, const void* dy, void* dx, int dtype, int64_t n,
+                        nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Bias gradient: column sums db[j] (+)= sum_t dy[t][j] (R18)                 */
+/* ------------------------------------------------------------------------- */
+size_t nnt_bias_grad_scratch_bytes(int64_t T, int64_t N);
+/* dy: device fp32/bf16 [T][lddy]; db device fp32 [N]; dy_bf16_out: optional device
+ * bf16 [T][lddy] copy of dy (cast fused into the same pass; fp32 dy only). */
+nnt_status nnt_bias_grad(const void* dy, int dy_dtype, int64_t T, int64_t N, int64_t lddy,
+                         float* db, int accumulate, void* dy_bf16_out,
+                         void* scratch, size_t scratch_bytes, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Adam / AdamW per tile (R12)                                     */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  float lr, beta1, beta2, eps;
+  float weight_decay; /* 0 = Adam; > 0 = AdamW decoupled decay w -= lr*wd*w_old */
+  float bias_corr1;   /* 1 - beta1^t, computed by the caller in fp64, t >= 1    */
+  float bias_corr2;   /* 1 - beta2^t                                            */
+  float grad_scale;   /* g is multiplied by this first (1 = none)               */
+} nnt_adam_hparams;
+
+/* m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; w -= lr (m/bc1) / (sqrt(v/bc2) + eps).
+ * w, g, m, v: device fp32 [n] (one flat tile range); w_bf16: optional device bf16 [n]
+ * shadow written as round-to-nearest-even(w_new); hp: host struct. */
+nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v, void* w_bf16,
+                         const nnt_adam_hparams* hp, nnt_stream_t stream);
+
+/* fp32 -> bf16 (round to nearest even) or bf16 -> fp32 conversion of n elements. */
+nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,
+                       nnt_stream_t stream);
+
+/* y[i] = alpha * x[i] (fp32, n elements; y may alias x).  Used for dy = r / T_global (R13). */
+nnt_status nnt_scale(const float* x, float alpha, float* y, int64_t n, nnt_stream_t stream);
+
+/* Block-only loss (R13): out[0] = scale * sum_i y[i] r[i] (deterministic order). */
+size_t nnt_dot_scratch_bytes(int64_t n);
+nnt_status nnt_dot(const float* y, const float* r, int64_t n, float scale, float* out,
+                   void* scratch, size_t scratch_bytes, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* GPT-2 block (pre-LN, R1) forward / backward on one GPU's batch tiles        */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t E;       /* N_e embedding size                     */
+  int64_t H;       /* N_h heads, h = E / H                   */
+  int64_t S;       /* N_s sequence length                    */
+  int64_t B;       /* N_b sequences on this GPU              */
+  int64_t tile_e;  /* logical tile along embedding axes      */
+  int64_t tile_f;  /* logical tile along the MLP hidden axis */
+  int64_t tile_s;  /* logical tile along the sequence axis   */
+  int64_t tile_t;  /* logical tile along tokens (rows)       */
+  int dtype;       /* NNT_F32 or NNT_BF16 compute path       */
+  float ln_eps;    /* LayerNorm epsilon (R9: 1e-5)           */
+  int causal;      /* 1 = GPT-2 causal mask (R2)             */
+} nnt_block_cfg;
+
+/* Parameters of one block.  LayerNorm and bias vectors are fp32 masters; the four
+ * weight matrices are in cfg.dtype (bf16 shadows on the bf16 path).
+ * Shapes: w_qkv [3E][E] (q, k, v row blocks), w_o [E][E], w_fc [4E][E], w_pr [E][4E]. */
+typedef struct {
+  const float *ln1_g, *ln1_b, *b_qkv, *b_o, *ln2_g, *ln2_b, *b_fc, *b_pr;
+  const void *w_qkv, *w_o, *w_fc, *w_pr;
+} nnt_block_params;
+
+/* fp32 gradients, same shapes as the parameters. */
+typedef struct {
+  float *ln1_g, *ln1_b, *w_qkv, *b_qkv, *w_o, *b_o, *ln2_g, *ln2_b, *w_fc, *b_fc, *w_pr, *b_pr;
+} nnt_block_grads;
+
+/* Bytes of the per-block `saved` activation workspace (kept from fwd to bwd, one per
+ * layer) and of the shared `scratch` workspace (reusable across layers). */
+nnt_status nnt_block_workspace_size(const nnt_block_cfg* cfg, size_t* saved_bytes,
+                                    size_t* scratch_bytes);
+
+/* y = block(x).  x, y: device fp32 [B][S][E]; saved/scratch: device workspaces.
+ * Executes the block's lowered tile-task DAG (nnt_block_dag_describe) in order. */
+nnt_status nnt_block_fwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
+                         float* y, void* saved, void* scratch, nnt_stream_t stream);
+
+/* Backward of nnt_block_fwd.  x: the same input; dy: device fp32 [B][S][E]; dx: device
+ * fp32 [B][S][E] (may alias dy); g: fp32 gradients (accumulate_grads != 0 adds into
+ * them).  grad_ready: NULL or 4 events recorded on `stream` when the gradients of
+ * {mlp.proj, mlp.fc+ln2, attn.out, attn.qkv+ln1} are final (for overlapped DP
+ * all-reduce). */
+nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
+                         const void* saved, void* scratch, const float* dy, float* dx,
+                         const nnt_block_grads* g, int accumulate_grads,
+                         nnt_event_t* grad_ready, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
+/* Tile-task DAG (STF rules S:46)                               */
+/* ------------------------------------------------------------------------- */
+typedef struct {
+  int32_t op;        /* nnt_block_op                                        */
+  int32_t level;     /* topological level (longest dependency chain)        */
+  int64_t tile[3];   /* tile coordinates of the task within the op's grid   */
+  int32_t n_deps;    /* number of predecessor tasks                          */
+  int32_t group;     /* index of the launch group executing this task       */
+} nnt_task;
+
+typedef struct {
+  int32_t op;
+  int32_t level;
+  int64_t n_tasks;
+} nnt_launch_group;
+
+/* Ops of the block DAG, in submission (program) order. */
+typedef enum {
+  NNT_OP_LN1 = 0, NNT_OP_QKV, NNT_OP_SCORES, NNT_OP_MAXSUMEXP, NNT_OP_SOFTMAX, NNT_OP_PV,
+  NNT_OP_OUT, NNT_OP_LN2, NNT_OP_FC, NNT_OP_PROJ,
+  /* backward */
+  NNT_OP_PROJ_DB, NNT_OP_PROJ_DW, NNT_OP_PROJ_DX, NNT_OP_FC_DB, NNT_OP_FC_DW, NNT_OP_FC_DX,
+  NNT_OP_LN2_BWD, NNT_OP_OUT_DB, NNT_OP_OUT_DW, NNT_OP_OUT_DX, NNT_OP_ATT_DP, NNT_OP_ATT_DV,
+  NNT_OP_SOFTMAX_BWD, NNT_OP_ATT_DQ, NNT_OP_ATT_DK, NNT_OP_QKV_DB, NNT_OP_QKV_DW,
+  NNT_OP_QKV_DX, NNT_OP_LN1_BWD,
+  NNT_OP_COUNT
+} nnt_block_op;
+
+const char* nnt_op_name(int op);
+
+/* Builds (or returns the cached) tile-task DAG of one block pass (pass 0 = forward,
+ * 1 = backward) from STF submission of per-tile tasks with R/W/RW/Reduce accesses,
+ * and its lowering into launch groups: one group per op, launched at the highest
+ * level its tasks reach (every dependency edge crosses launch levels; ops that
+ * share a launch level are independent).  Writes up to
+ * task_cap tasks / group_cap groups (host arrays, may be NULL with cap 0) and the
+ * full counts. */
+nnt_status nnt_block_dag_describe(const nnt_block_cfg* cfg, int pass,
+                                  nnt_task* tasks, int64_t task_cap, int64_t* n_tasks,
+                                  nnt_launch_group* groups, int64_t group_cap, int64_t* n_groups);
+
+/* ------------------------------------------------------------------------- */
+/* Kernel timing (bench.py roofline): CUDA events around every launch.         */
+/* ------------------------------------------------------------------------- */
+typedef enum {
+  NNT_K_GEMM_TC = 0, NNT_K_GEMM_TC_ATTN, NNT_K_GEMM_SIMT, NNT_K_MAXSUMEXP, NNT_K_SOFTMAX, NNT_K_SOFTMAX_BWD,
+  NNT_K_LN_FWD, NNT_K_LN_BWD, NNT_K_GELU, NNT_K_BIAS_GRAD, NNT_K_ADAM, NNT_K_MISC,
+  NNT_K_COUNT
+} nnt_kernel_class;
+
+/* enable != 0 starts recording (clears previous records). */
+nnt_status nnt_timing_enable(int enable);
+/* Synchronises the recorded events and returns, per kernel class, the summed
+ * device time in ms, the launch count and the summed algorithmic bytes and flops
+ * (host arrays of length NNT_K_COUNT; any may be NULL). */
+nnt_status nnt_timing_read(double* ms, int64_t* launches, double* bytes, double* flops);
+/* Number of kernels this library launched since load (all classes). */
+int64_t nnt_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NNT_H_ */

@@ -1,0 +1,352 @@
+// nnt_block_fwd / nnt_block_bwd: execute the lowered tile-task DAG of one
+// pre-LN GPT-2 block (reading R1) on one stream.  Every launch group of the
+// plan (dag.cpp) maps to one kernel launch that executes all of that group's
+// tile tasks.  Workspace layout ("saved" per layer, "scratch" shared) is
+// computed here; the caller owns the memory.
+#include <cmath>
+
+#include "dag.h"
+#include "nnt_internal.h"
+
+namespace nnt {
+namespace {
+
+struct Layout {
+  // saved (per layer)
+  size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
+  // scratch
+  size_t scores, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, scratch_bytes;
+  size_t colsum_bytes, lnscr_bytes;
+};
+
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+Layout make_layout(const nnt_block_cfg& c) {
+  const size_t T = c.B * c.S, E = c.E, F = 4 * c.E, H = c.H, S = c.S, B = c.B;
+  const size_t dt = c.dtype == NNT_BF16 ? 2 : 4;
+  Layout L{};
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t at = o;
+    o = align256(o + bytes);
+    return at;
+  };
+  L.mean1 = take(4 * T);
+  L.rstd1 = take(4 * T);
+  L.h1 = take(dt * T * E);
+  L.qkv = take(dt * T * 3 * E);
+  L.P = take(dt * B * H * S * S);
+  L.stats = take(4 * 2 * B * H * S);
+  L.O = take(dt * T * E);
+  L.x1 = take(4 * T * E);
+  L.mean2 = take(4 * T);
+  L.rstd2 = take(4 * T);
+  L.h2 = take(dt * T * E);
+  L.u = take(dt * T * F);
+  L.g = take(dt * T * F);
+  L.saved_bytes = o;
+  o = 0;
+  L.scores = take(4 * B * H * S * S);
+  L.dy16 = take(dt * T * E);
+  L.du = take(dt * T * F);
+  L.dh = take(4 * T * E);
+  L.dx1 = take(4 * T * E);
+  L.dx116 = take(dt * T * E);
+  L.dO = take(dt * T * E);
+  L.dA = take(dt * B * H * S * S);
+  L.dqkv = take(dt * T * 3 * E);
+  size_t cs = nnt_bias_grad_scratch_bytes(T, F);
+  size_t cs2 = nnt_bias_grad_scratch_bytes(T, 3 * E);
+  L.colsum_bytes = cs > cs2 ? cs : cs2;
+  L.colsum = take(L.colsum_bytes);
+  L.lnscr_bytes = nnt_layernorm_bwd_scratch_bytes(T, E);
+  L.lnscr = take(L.lnscr_bytes);
+  L.scratch_bytes = o;
+  return L;
+}
+
+nnt_status check_cfg(const nnt_block_cfg* c) {
+  NNT_REQUIRE(c, NNT_ERR_NULL, "block: NULL cfg");
+  NNT_REQUIRE(c->E > 0 && c->H > 0 && c->S > 0 && c->B > 0 && c->E % c->H == 0, NNT_ERR_SHAPE,
+              "block: bad shape E=%lld H=%lld S=%lld B=%lld", (long long)c->E, (long long)c->H, (long long)c->S,
+              (long long)c->B);
+  NNT_REQUIRE(c->tile_e > 0 && c->tile_f > 0 && c->tile_s > 0 && c->tile_t > 0, NNT_ERR_TILE,
+              "block: tiles must be positive");
+  NNT_REQUIRE(valid_dtype(c->dtype), NNT_ERR_DTYPE, "block: dtype %d", c->dtype);
+  NNT_REQUIRE(c->E % 8 == 0 && c->S % 8 == 0 && (c->E / c->H) % 8 == 0, NNT_ERR_ALIGN,
+              "block: E, S and head size must be multiples of 8");
+  NNT_REQUIRE(c->S <= 2048, NNT_ERR_UNSUPPORTED, "block: S > 2048 unsupported (materialised softmax rows)");
+  return NNT_OK;
+}
+
+struct Ctx {
+  const nnt_block_cfg& c;
+  int64_t T, E, F, H, S, B, Dh;
+  int dt;
+  float inv_sqrt_dh;
+  int64_t tile_lin[3];
+  uint8_t* sv;
+  uint8_t* sc;
+  Layout L;
+  cudaStream_t st;
+  template <typename P>
+  P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
+  template <typename P>
+  P* k(size_t off) const { return reinterpret_cast<P*>(sc + off); }
+};
+
+nnt_status gemm(const Ctx& x, int ta, int tb, int64_t M, int64_t N, int64_t K, const int64_t* batch, float alpha,
+                const void* A, int64_t lda, const int64_t* sa, const void* B, int64_t ldb, const int64_t* sb,
+                float beta, void* C, int cdt, int64_t ldc, const int64_t* sc, const nnt_epilogue* epi) {
+  return nnt_tile_gemm(ta, tb, M, N, K, batch, alpha, A, x.dt, lda, sa, B, x.dt, ldb, sb, beta, C, cdt, ldc, sc,
+                       x.tile_lin, epi, x.st);
+}
+
+nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const float* xin, float* y) {
+  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh;
+  const int dt = x.dt;
+  const int64_t batch[2] = {B, H};
+  nnt_epilogue e{};
+  switch (op) {
+    case NNT_OP_LN1:
+      return nnt_layernorm_fwd(xin, T, E, E, x.c.tile_e, p->ln1_g, p->ln1_b, x.c.ln_eps, x.s<void>(x.L.h1), dt, E,
+                               x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), x.st);
+    case NNT_OP_QKV:
+      e.bias = p->b_qkv;
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, 3 * E, E, nullptr, 1.f, x.s<void>(x.L.h1), E, nullptr, p->w_qkv, E,
+                  nullptr, 0.f, x.s<void>(x.L.qkv), dt, 3 * E, nullptr, &e);
+    case NNT_OP_SCORES: {
+      const size_t es = dt == NNT_BF16 ? 2 : 4;
+      const int64_t sq[2] = {S * 3 * E, Dh}, ssc[2] = {H * S * S, S * S};
+      e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
+      uint8_t* q = x.s<uint8_t>(x.L.qkv);
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + es * E, 3 * E, sq, 0.f,
+                  x.k<float>(x.L.scores), NNT_F32, S, ssc, &e);
+    }
+    case NNT_OP_MAXSUMEXP:
+      return nnt_maxsumexp(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S,
+                           x.s<float>(x.L.stats), 0, x.st);
+    case NNT_OP_SOFTMAX:
+      return nnt_softmax(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S, x.s<float>(x.L.stats),
+                         x.s<void>(x.L.P), dt, S, x.st);
+    case NNT_OP_PV: {
+      const size_t es = dt == NNT_BF16 ? 2 : 4;
+      const int64_t sp[2] = {H * S * S, S * S}, sv[2] = {S * 3 * E, Dh}, so[2] = {S * E, Dh};
+      e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp,
+                  x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.s<void>(x.L.O), dt, E, so, &e);
+    }
+    case NNT_OP_OUT:
+      e.bias = p->b_o;
+      e.residual = xin;
+      e.ld_residual = E;
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, E, nullptr, 1.f, x.s<void>(x.L.O), E, nullptr, p->w_o, E, nullptr,
+                  0.f, x.s<float>(x.L.x1), NNT_F32, E, nullptr, &e);
+    case NNT_OP_LN2:
+      return nnt_layernorm_fwd(x.s<float>(x.L.x1), T, E, E, x.c.tile_e, p->ln2_g, p->ln2_b, x.c.ln_eps,
+                               x.s<void>(x.L.h2), dt, E, x.s<float>(x.L.mean2), x.s<float>(x.L.rstd2), x.st);
+    case NNT_OP_FC:
+      e.bias = p->b_fc;
+      e.act = NNT_ACT_GELU;
+      e.aux = x.s<void>(x.L.u);
+      e.ld_aux = F;
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, F, E, nullptr, 1.f, x.s<void>(x.L.h2), E, nullptr, p->w_fc, E,
+                  nullptr, 0.f, x.s<void>(x.L.g), dt, F, nullptr, &e);
+    case NNT_OP_PROJ:
+      e.bias = p->b_pr;
+      e.residual = x.s<float>(x.L.x1);
+      e.ld_residual = E;
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, F, nullptr, 1.f, x.s<void>(x.L.g), F, nullptr, p->w_pr, F,
+                  nullptr, 0.f, y, NNT_F32, E, nullptr, &e);
+  }
+  return fail(NNT_ERR_ARG, "block fwd: unexpected op in plan");
+}
+
+nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const float* xin, const float* dy, float* dx,
+                      const nnt_block_grads* g, int acc) {
+  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh;
+  const int dt = x.dt;
+  const bool bf = dt == NNT_BF16;
+  const size_t es = bf ? 2 : 4;
+  const int64_t batch[2] = {B, H};
+  const float beta = acc ? 1.f : 0.f;
+  // GEMM operand views of dy and dx1 (bf16 copies on the bf16 path)
+  const void* dyA = bf ? x.k<void>(x.L.dy16) : (const void*)dy;
+  const void* dx1A = bf ? x.k<void>(x.L.dx116) : x.k<void>(x.L.dx1);
+  nnt_epilogue e{};
+  switch (op) {
+    case NNT_OP_PROJ_DB:
+      return nnt_bias_grad(dy, NNT_F32, T, E, E, g->b_pr, acc, bf ? x.k<void>(x.L.dy16) : nullptr,
+                           x.k<void>(x.L.colsum), x.L.colsum_bytes, x.st);
+    case NNT_OP_PROJ_DW:
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, E, F, T, nullptr, 1.f, dyA, E, nullptr, x.s<void>(x.L.g), F, nullptr,
+                  beta, g->w_pr, NNT_F32, F, nullptr, nullptr);
+    case NNT_OP_PROJ_DX:
+      e.act = NNT_ACT_GELU_BWD;
+      e.aux = x.s<void>(x.L.u);
+      e.ld_aux = F;
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, F, E, nullptr, 1.f, dyA, E, nullptr, p->w_pr, F, nullptr, 0.f,
+                  x.k<void>(x.L.du), dt, F, nullptr, &e);
+    case NNT_OP_FC_DB:
+      return nnt_bias_grad(x.k<void>(x.L.du), dt, T, F, F, g->b_fc, acc, nullptr, x.k<void>(x.L.colsum),
+                           x.L.colsum_bytes, x.st);
+    case NNT_OP_FC_DW:
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, F, E, T, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr,
+                  x.s<void>(x.L.h2), E, nullptr, beta, g->w_fc, NNT_F32, E, nullptr, nullptr);
+    case NNT_OP_FC_DX:
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
+                  nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
+    case NNT_OP_LN2_BWD:
+      return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, x.s<float>(x.L.x1), E, x.s<float>(x.L.mean2),
+                               x.s<float>(x.L.rstd2), p->ln2_g, T, E, dy, x.k<float>(x.L.dx1), E,
+                               bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, acc, x.k<void>(x.L.lnscr),
+                               x.L.lnscr_bytes, x.st);
+    case NNT_OP_OUT_DB:
+      return nnt_bias_grad(x.k<float>(x.L.dx1), NNT_F32, T, E, E, g->b_o, acc, nullptr, x.k<void>(x.L.colsum),
+                           x.L.colsum_bytes, x.st);
+    case NNT_OP_OUT_DW:
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, E, E, T, nullptr, 1.f, dx1A, E, nullptr, x.s<void>(x.L.O), E, nullptr,
+                  beta, g->w_o, NNT_F32, E, nullptr, nullptr);
+    case NNT_OP_OUT_DX:
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, E, nullptr, 1.f, dx1A, E, nullptr, p->w_o, E, nullptr, 0.f,
+                  x.k<void>(x.L.dO), dt, E, nullptr, nullptr);
+    case NNT_OP_ATT_DP: {
+      const int64_t so[2] = {S * E, Dh}, sv[2] = {S * 3 * E, Dh}, sp[2] = {H * S * S, S * S};
+      e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), E, so,
+                  x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.k<float>(x.L.scores), NNT_F32, S, sp, &e);
+    }
+    case NNT_OP_ATT_DV: {
+      const int64_t sp[2] = {H * S * S, S * S}, so[2] = {S * E, Dh}, sq[2] = {S * 3 * E, Dh};
+      e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp, x.k<void>(x.L.dO), E, so,
+                  0.f, x.k<uint8_t>(x.L.dqkv) + es * 2 * E, dt, 3 * E, sq, &e);
+    }
+    case NNT_OP_SOFTMAX_BWD:
+      return nnt_softmax_bwd(x.s<void>(x.L.P), dt, S, x.k<float>(x.L.scores), S, B * H * S, S, x.c.causal, S,
+                             x.inv_sqrt_dh, x.k<void>(x.L.dA), dt, S, x.st);
+    case NNT_OP_ATT_DQ: {
+      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * E, Dh};
+      e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
+                  x.s<uint8_t>(x.L.qkv) + es * E, 3 * E, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * E, sq, &e);
+    }
+    case NNT_OP_ATT_DK: {
+      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * E, Dh};
+      e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp, x.s<void>(x.L.qkv),
+                  3 * E, sq, 0.f, x.k<uint8_t>(x.L.dqkv) + es * E, dt, 3 * E, sq, &e);
+    }
+    case NNT_OP_QKV_DB:
+      return nnt_bias_grad(x.k<void>(x.L.dqkv), dt, T, 3 * E, 3 * E, g->b_qkv, acc, nullptr, x.k<void>(x.L.colsum),
+                           x.L.colsum_bytes, x.st);
+    case NNT_OP_QKV_DW:
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * E, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
+                  x.s<void>(x.L.h1), E, nullptr, beta, g->w_qkv, NNT_F32, E, nullptr, nullptr);
+    case NNT_OP_QKV_DX:
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, 3 * E, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
+                  p->w_qkv, E, nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
+    case NNT_OP_LN1_BWD:
+      return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, xin, E, x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), p->ln1_g,
+                               T, E, x.k<float>(x.L.dx1), dx, E, nullptr, g->ln1_g, g->ln1_b, acc,
+                               x.k<void>(x.L.lnscr), x.L.lnscr_bytes, x.st);
+  }
+  return fail(NNT_ERR_ARG, "block bwd: unexpected op in plan");
+}
+
+Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st) {
+  Ctx x{c};
+  x.T = c.B * c.S;
+  x.E = c.E;
+  x.F = 4 * c.E;
+  x.H = c.H;
+  x.S = c.S;
+  x.B = c.B;
+  x.Dh = c.E / c.H;
+  x.dt = c.dtype;
+  x.inv_sqrt_dh = (float)(1.0 / std::sqrt((double)x.Dh));
+  x.tile_lin[0] = c.tile_t;
+  x.tile_lin[1] = c.tile_e;
+  x.tile_lin[2] = c.tile_e;
+  x.sv = (uint8_t*)saved;
+  x.sc = (uint8_t*)scratch;
+  x.L = make_layout(c);
+  x.st = st;
+  return x;
+}
+
+// Each op must form exactly one launch group (all its tile tasks independent).
+nnt_status check_plan(const BlockPlan* plan) {
+  int seen[NNT_OP_COUNT] = {0};
+  for (auto& gr : plan->groups) {
+    NNT_REQUIRE(++seen[gr.op] == 1, NNT_ERR_UNSUPPORTED, "block plan: op %s spans several levels",
+                nnt_op_name(gr.op));
+  }
+  return NNT_OK;
+}
+
+}  // namespace
+}  // namespace nnt
+
+using namespace nnt;
+
+extern "C" {
+
+nnt_status nnt_block_workspace_size(const nnt_block_cfg* cfg, size_t* saved_bytes, size_t* scratch_bytes) {
+  NNT_TRY(check_cfg(cfg));
+  NNT_REQUIRE(saved_bytes && scratch_bytes, NNT_ERR_NULL, "nnt_block_workspace_size: NULL output");
+  Layout L = make_layout(*cfg);
+  *saved_bytes = L.saved_bytes;
+  *scratch_bytes = L.scratch_bytes;
+  return NNT_OK;
+}
+
+nnt_status nnt_block_fwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x, float* y, void* saved,
+                         void* scratch, nnt_stream_t stream) {
+  NNT_TRY(check_cfg(cfg));
+  NNT_REQUIRE(p && x && y && saved && scratch, NNT_ERR_NULL, "nnt_block_fwd: NULL argument");
+  NNT_REQUIRE(p->ln1_g && p->ln1_b && p->ln2_g && p->ln2_b && p->w_qkv && p->w_o && p->w_fc && p->w_pr && p->b_qkv &&
+                  p->b_o && p->b_fc && p->b_pr,
+              NNT_ERR_NULL, "nnt_block_fwd: NULL parameter");
+  const BlockPlan* plan = block_plan(*cfg, 0);
+  NNT_REQUIRE(plan != nullptr, NNT_ERR_SHAPE, "nnt_block_fwd: %s", nnt_last_error());
+  NNT_TRY(check_plan(plan));
+  Ctx c = make_ctx(*cfg, saved, scratch, stream);
+  for (const auto& gr : plan->groups) NNT_TRY(run_fwd_op(c, gr.op, p, x, y));
+  return NNT_OK;
+}
+
+nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x, const void* saved,
+                         void* scratch, const float* dy, float* dx, const nnt_block_grads* g, int accumulate_grads,
+                         nnt_event_t* grad_ready, nnt_stream_t stream) {
+  NNT_TRY(check_cfg(cfg));
+  NNT_REQUIRE(p && x && saved && scratch && dy && dx && g, NNT_ERR_NULL, "nnt_block_bwd: NULL argument");
+  NNT_REQUIRE(g->ln1_g && g->ln1_b && g->ln2_g && g->ln2_b && g->w_qkv && g->w_o && g->w_fc && g->w_pr && g->b_qkv &&
+                  g->b_o && g->b_fc && g->b_pr,
+              NNT_ERR_NULL, "nnt_block_bwd: NULL gradient");
+  const BlockPlan* plan = block_plan(*cfg, 1);
+  NNT_REQUIRE(plan != nullptr, NNT_ERR_SHAPE, "nnt_block_bwd: %s", nnt_last_error());
+  NNT_TRY(check_plan(plan));
+  Ctx c = make_ctx(*cfg, const_cast<void*>(saved), scratch, stream);
+  // Gradient sets for the DP events: each fires once every op that writes the set's
+  // gradients OR reads the set's weights has been enqueued, so an optimizer step
+  // on another stream after the event cannot race with this backward pass.
+  static const int sets[4][4] = {{NNT_OP_PROJ_DB, NNT_OP_PROJ_DW, NNT_OP_PROJ_DX, -1},
+                                 {NNT_OP_FC_DB, NNT_OP_FC_DW, NNT_OP_FC_DX, NNT_OP_LN2_BWD},
+                                 {NNT_OP_OUT_DB, NNT_OP_OUT_DW, NNT_OP_OUT_DX, -1},
+                                 {NNT_OP_QKV_DB, NNT_OP_QKV_DW, NNT_OP_QKV_DX, NNT_OP_LN1_BWD}};
+  int remaining[4];
+  for (int k = 0; k < 4; ++k) remaining[k] = sets[k][3] < 0 ? 3 : 4;
+  for (const auto& gr : plan->groups) {
+    NNT_TRY(run_bwd_op(c, gr.op, p, x, dy, dx, g, accumulate_grads));
+    if (grad_ready) {
+      for (int k = 0; k < 4; ++k)
+        for (int j = 0; j < 4; ++j)
+          if (sets[k][j] == gr.op && --remaining[k] == 0 && grad_ready[k])
+            NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
+    }
+  }
+  return NNT_OK;
+}
+
+}  // extern "C"

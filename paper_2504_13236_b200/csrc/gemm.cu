@@ -1,0 +1,86 @@
+// nnt_tile_gemm: argument validation and dispatch (P:150-153 linear layer,
+// P:181 attention products).  fp32 operands -> SIMT fp32 path; bf16 operands
+// -> tcgen05 tensor-core path.  There is no other route and no fallback.
+#include "gemm_common.cuh"
+
+using namespace nnt;
+
+extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const int64_t* batch,
+                                    float alpha, const void* A, int a_dtype, int64_t lda, const int64_t* stride_a,
+                                    const void* B, int b_dtype, int64_t ldb, const int64_t* stride_b, float beta,
+                                    void* C, int c_dtype, int64_t ldc, const int64_t* stride_c, const int64_t* tile,
+                                    const nnt_epilogue* epi, nnt_stream_t stream) {
+  NNT_REQUIRE(A && B && C, NNT_ERR_NULL, "nnt_tile_gemm: NULL operand");
+  NNT_REQUIRE(trans_a == NNT_NOTRANS || trans_a == NNT_TRANS, NNT_ERR_ARG, "nnt_tile_gemm: trans_a=%d", trans_a);
+  NNT_REQUIRE(trans_b == NNT_NOTRANS || trans_b == NNT_TRANS, NNT_ERR_ARG, "nnt_tile_gemm: trans_b=%d", trans_b);
+  NNT_REQUIRE(M > 0 && N > 0 && K > 0, NNT_ERR_SHAPE, "nnt_tile_gemm: M=%lld N=%lld K=%lld", (long long)M,
+              (long long)N, (long long)K);
+  NNT_REQUIRE(valid_dtype(a_dtype) && a_dtype == b_dtype && valid_dtype(c_dtype), NNT_ERR_DTYPE,
+              "nnt_tile_gemm: dtypes A=%d B=%d C=%d (A and B must match)", a_dtype, b_dtype, c_dtype);
+  int64_t b0 = batch ? batch[0] : 1, b1 = batch ? batch[1] : 1;
+  NNT_REQUIRE(b0 > 0 && b1 > 0, NNT_ERR_SHAPE, "nnt_tile_gemm: batch {%lld,%lld}", (long long)b0, (long long)b1);
+  NNT_REQUIRE(lda >= (trans_a == NNT_NOTRANS ? K : M), NNT_ERR_SHAPE, "nnt_tile_gemm: lda=%lld too small",
+              (long long)lda);
+  NNT_REQUIRE(ldb >= (trans_b == NNT_NOTRANS ? N : K), NNT_ERR_SHAPE, "nnt_tile_gemm: ldb=%lld too small",
+              (long long)ldb);
+  NNT_REQUIRE(ldc >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ldc=%lld < N", (long long)ldc);
+  if (tile) {
+    NNT_REQUIRE(tile[0] > 0 && tile[1] > 0 && tile[2] > 0, NNT_ERR_TILE, "nnt_tile_gemm: tile must be positive");
+  }
+  GemmArgs g{};
+  g.ta = trans_a;
+  g.tb = trans_b;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.batch0 = b0;
+  g.batch1 = b1;
+  g.alpha = alpha;
+  g.beta = beta;
+  g.A = A;
+  g.lda = lda;
+  g.sa0 = stride_a ? stride_a[0] : 0;
+  g.sa1 = stride_a ? stride_a[1] : 0;
+  g.B = B;
+  g.ldb = ldb;
+  g.sb0 = stride_b ? stride_b[0] : 0;
+  g.sb1 = stride_b ? stride_b[1] : 0;
+  g.C = C;
+  g.ldc = ldc;
+  g.sc0 = stride_c ? stride_c[0] : 0;
+  g.sc1 = stride_c ? stride_c[1] : 0;
+  g.c_dtype = c_dtype;
+  g.in_dtype = a_dtype;
+  g.causal = NNT_CAUSAL_NONE;
+  if (epi) {
+    NNT_REQUIRE(epi->act >= NNT_ACT_NONE && epi->act <= NNT_ACT_GELU_BWD, NNT_ERR_ARG, "nnt_tile_gemm: act=%d",
+                epi->act);
+    NNT_REQUIRE(epi->causal >= NNT_CAUSAL_NONE && epi->causal <= NNT_CAUSAL_A_UPPER, NNT_ERR_ARG,
+                "nnt_tile_gemm: causal=%d", epi->causal);
+    NNT_REQUIRE(epi->act == NNT_ACT_NONE || epi->aux, NNT_ERR_NULL, "nnt_tile_gemm: GELU epilogue needs aux");
+    NNT_REQUIRE(!epi->residual || epi->ld_residual >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_residual");
+    NNT_REQUIRE(!epi->aux || epi->ld_aux >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_aux");
+    NNT_REQUIRE((!epi->residual && !epi->aux) || (b0 == 1 && b1 == 1), NNT_ERR_UNSUPPORTED,
+                "nnt_tile_gemm: residual/aux epilogues are for unbatched GEMMs");
+    g.bias = epi->bias;
+    g.residual = epi->residual;
+    g.ld_res = epi->ld_residual;
+    g.act = epi->act;
+    g.aux = epi->aux;
+    g.ld_aux = epi->ld_aux;
+    g.causal = epi->causal;
+  }
+  const double frac = g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5;
+  const double flops = 2.0 * (double)M * N * K * b0 * b1 * frac;
+  const double es = (double)dtype_size(a_dtype);
+  const double bytes = ((double)M * K * es + (double)K * N * es) * b0 * b1 * (g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5) +
+                       (double)M * N * dtype_size(c_dtype) * b0 * b1 *
+                           (g.causal == NNT_CAUSAL_OUT_LOWER ? 0.5 : 1.0) * (beta != 0.f ? 2.0 : 1.0) +
+                       (g.residual ? 4.0 * M * N : 0.0) + (g.aux ? (double)M * N * dtype_size(c_dtype) : 0.0);
+  if (a_dtype == NNT_F32) {
+    LaunchScope sc(NNT_K_GEMM_SIMT, stream, bytes, flops);
+    return gemm_simt_launch(g, stream);
+  }
+  LaunchScope sc(b0 * b1 > 1 ? NNT_K_GEMM_TC_ATTN : NNT_K_GEMM_TC, stream, bytes, flops);
+  return gemm_tc_launch(g, stream);
+}

@@ -1,0 +1,51 @@
+// Shared GEMM argument block and epilogue (SIMT fp32 path and tcgen05 bf16 path).
+#pragma once
+#include "nnt_internal.h"
+
+namespace nnt {
+
+struct GemmArgs {
+  int ta, tb;
+  int64_t M, N, K;
+  int64_t batch0, batch1;
+  float alpha, beta;
+  const void* A;
+  int64_t lda, sa0, sa1;
+  const void* B;
+  int64_t ldb, sb0, sb1;
+  void* C;
+  int64_t ldc, sc0, sc1;
+  int c_dtype;
+  int in_dtype;
+  // epilogue
+  const float* bias;
+  const float* residual;
+  int64_t ld_res;
+  int act;
+  void* aux;
+  int64_t ld_aux;
+  int causal;
+};
+
+nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);
+nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s);
+
+// Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.
+template <typename TC>
+__device__ __forceinline__ void epilogue_store(const GemmArgs& g, TC* __restrict__ Cb, TC* __restrict__ auxb,
+                                               int64_t i, int64_t j, float acc) {
+  float pre = g.alpha * acc;
+  if (g.bias) pre += __ldg(g.bias + j);
+  if (g.beta != 0.f) pre += g.beta * to_f32(Cb[i * g.ldc + j]);
+  if (g.residual) pre += g.residual[i * g.ld_res + j];
+  float out = pre;
+  if (g.act == NNT_ACT_GELU) {
+    auxb[i * g.ld_aux + j] = from_f32<TC>(pre);
+    out = gelu_f(pre);
+  } else if (g.act == NNT_ACT_GELU_BWD) {
+    out = pre * gelu_grad_f(to_f32(auxb[i * g.ld_aux + j]));
+  }
+  Cb[i * g.ldc + j] = from_f32<TC>(out);
+}
+
+}  // namespace nnt

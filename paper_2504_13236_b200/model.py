@@ -1,0 +1,240 @@
+"""GPT-2 block stack driver: device memory, streams and process groups (torch)
+around libnnt's C-ABI calls.  Every arithmetic step runs in libnnt kernels.
+
+Memory layout (HBM, per GPU):
+  * one flat fp32 master-parameter buffer, one flat fp32 gradient buffer, fp32
+    Adam m and v, and a flat bf16 shadow of the parameters (GEMM operands on the
+    bf16 path).  Layers are stored last-to-first and, inside a layer, in the
+    order backward completes them ({proj}, {fc, ln2}, {out}, {qkv, ln1}), so the
+    DP buckets (one per set) are contiguous slices in backward-completion order;
+  * per layer: the input activation x_l (fp32 [B,S,E]) and the `saved`
+    workspace of nnt_block_fwd; one `scratch` workspace shared by all layers.
+
+Data parallelism (reading R14): batch tiles are partitioned
+across ranks (nnt_partition), each rank runs the full stack on its tiles, and
+gradient buckets are SUM-all-reduced with NCCL on a communication stream as
+soon as nnt_block_bwd records the bucket's event, followed by Adam on that
+bucket, overlapping the rest of the backward pass.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import nnt
+
+# (parameter, set) in flat-buffer order inside one layer
+SETS = (("w_pr", "b_pr"), ("w_fc", "b_fc", "ln2_g", "ln2_b"), ("w_o", "b_o"), ("w_qkv", "b_qkv", "ln1_g", "ln1_b"))
+ALIGN = 64  # elements; keeps every parameter view 256-byte aligned in fp32 and 128-byte in bf16
+
+
+def param_shapes(E):
+    F = 4 * E
+    return {"ln1_g": (E,), "ln1_b": (E,), "w_qkv": (3 * E, E), "b_qkv": (3 * E,), "w_o": (E, E), "b_o": (E,),
+            "ln2_g": (E,), "ln2_b": (E,), "w_fc": (F, E), "b_fc": (F,), "w_pr": (E, F), "b_pr": (E,)}
+
+
+@dataclass
+class StackConfig:
+    L: int
+    E: int
+    H: int
+    S: int
+    B: int                  # sequences on this GPU
+    tile_e: int = 1024
+    tile_f: int = 1024
+    tile_s: int = 1024
+    tile_t: int = 1024
+    dtype: str = "bf16"     # "bf16" (tcgen05 path) or "f32" (SIMT fp32 path)
+    ln_eps: float = 1e-5
+    causal: bool = True
+    lr: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    weight_decay: float = 0.0
+
+    def block_cfg(self):
+        return nnt.nnt_block_cfg(self.E, self.H, self.S, self.B, self.tile_e, self.tile_f, self.tile_s, self.tile_t,
+                                 nnt.NNT_BF16 if self.dtype == "bf16" else nnt.NNT_F32, self.ln_eps,
+                                 1 if self.causal else 0)
+
+    @property
+    def T(self):
+        return self.B * self.S
+
+
+class BlockStack:
+    def __init__(self, cfg: StackConfig, layer_params, device="cuda", process_group=None, global_tokens=None):
+        """layer_params: list (len L) of dicts name -> host array/tensor (fp32)."""
+        assert len(layer_params) == cfg.L
+        self.cfg = cfg
+        self.dev = torch.device(device)
+        self.pg = process_group
+        self.world = torch.distributed.get_world_size(process_group) if process_group is not None else 1
+        self.T_global = global_tokens if global_tokens is not None else cfg.T * self.world
+        self.bcfg = cfg.block_cfg()
+        E = cfg.E
+        shapes = param_shapes(E)
+        # ---- flat layout
+        self.offsets = []       # per layer: name -> (offset, numel)
+        self.buckets = []       # (layer, set index, begin, end) in backward-completion order
+        off = 0
+        per_layer = [None] * cfg.L
+        for l in range(cfg.L - 1, -1, -1):
+            d = {}
+            for si, names in enumerate(SETS):
+                b0 = off
+                for n in names:
+                    numel = math.prod(shapes[n])
+                    d[n] = (off, numel)
+                    off += -(-numel // ALIGN) * ALIGN
+                self.buckets.append((l, si, b0, off))
+            per_layer[l] = d
+        self.offsets = per_layer
+        self.numel = off
+        f32 = dict(device=self.dev, dtype=torch.float32)
+        self.w = torch.zeros(off, **f32)
+        self.g = torch.zeros(off, **f32)
+        self.m = torch.zeros(off, **f32)
+        self.v = torch.zeros(off, **f32)
+        self.bf16 = cfg.dtype == "bf16"
+        self.w16 = torch.zeros(off, device=self.dev, dtype=torch.bfloat16) if self.bf16 else None
+        for l, P in enumerate(layer_params):
+            for n, (o, k) in self.offsets[l].items():
+                src = torch.as_tensor(P[n], dtype=torch.float32).reshape(-1)
+                self.w[o:o + k].copy_(src.to(self.dev))
+        if self.bf16:
+            nnt.nnt_convert(self.w, nnt.NNT_F32, self.w16, nnt.NNT_BF16, off)
+        self.step_count = 0
+        # ---- views / ABI structs
+        self._params = []
+        self._grads = []
+        for l in range(cfg.L):
+            self._params.append(self._make_params(l))
+            self._grads.append(self._make_grads(l))
+        saved_b, scratch_b = nnt.nnt_block_workspace_size(self.bcfg)
+        self.saved = [torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for _ in range(cfg.L)]
+        self.scratch = torch.empty(scratch_b, device=self.dev, dtype=torch.uint8)
+        act = dict(device=self.dev, dtype=torch.float32)
+        self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
+        self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
+        self.loss = torch.zeros(1, **act)
+        self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
+        self.comm = torch.cuda.Stream(device=self.dev) if self.world > 1 else None
+        self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.world > 1 else None
+
+    # ------------------------------------------------------------ views
+    def view(self, buf, l, name):
+        o, k = self.offsets[l][name]
+        return buf[o:o + k]
+
+    def _make_params(self, l):
+        wsrc = self.w16 if self.bf16 else self.w
+        p = nnt.nnt_block_params()
+        for n in ("ln1_g", "ln1_b", "b_qkv", "b_o", "ln2_g", "ln2_b", "b_fc", "b_pr"):
+            setattr(p, n, self.view(self.w, l, n).data_ptr())
+        for n in ("w_qkv", "w_o", "w_fc", "w_pr"):
+            setattr(p, n, self.view(wsrc, l, n).data_ptr())
+        return p
+
+    def _make_grads(self, l):
+        gr = nnt.nnt_block_grads()
+        for n in param_shapes(self.cfg.E):
+            setattr(gr, n, self.view(self.g, l, n).data_ptr())
+        return gr
+
+    def params_of(self, l, buf=None):
+        shapes = param_shapes(self.cfg.E)
+        buf = self.w if buf is None else buf
+        return {n: self.view(buf, l, n).reshape(shapes[n]) for n in shapes}
+
+    def grads_of(self, l):
+        return self.params_of(l, self.g)
+
+    # ------------------------------------------------------------ passes
+    def forward(self, x=None):
+        if x is not None:
+            self.xs[0].copy_(x)
+        for l in range(self.cfg.L):
+            nnt.nnt_block_fwd(self.bcfg, self._params[l], self.xs[l], self.xs[l + 1], self.saved[l], self.scratch)
+        return self.xs[-1]
+
+    def probe_loss(self, r):
+        """L = (1/T_global) sum <y, r> on device; dy = r / T_global (reading R13)."""
+        n = self.cfg.T * self.cfg.E
+        inv = 1.0 / self.T_global
+        nnt.nnt_dot(self.xs[-1], r, n, inv, self.loss, self.dot_scratch, self.dot_scratch.numel())
+        nnt.nnt_scale(r, inv, self.dy[0], n)
+        return self.loss
+
+    def backward(self, overlap_optimizer=True):
+        """Backward through the stack; with DP, bucket all-reduce (+ Adam) overlapped on the comm stream."""
+        cur = 0
+        compute = torch.cuda.current_stream()
+        dp = self.world > 1
+        for l in range(self.cfg.L - 1, -1, -1):
+            ev = self.events[l] if dp else None
+            nnt.nnt_block_bwd(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch, self.dy[cur],
+                              self.dy[1 - cur], self._grads[l], 0, ev)
+            if dp:
+                for si in range(4):
+                    self._reduce_bucket(l, si, ev[si], overlap_optimizer)
+            cur = 1 - cur
+        if dp:
+            compute.wait_stream(self.comm)
+        return self.dy[cur]
+
+    def _bucket_range(self, l, si):
+        for (bl, bs, b0, b1) in self.buckets:
+            if bl == l and bs == si:
+                return b0, b1
+        raise KeyError((l, si))
+
+    def _reduce_bucket(self, l, si, event, with_adam):
+        b0, b1 = self._bucket_range(l, si)
+        with torch.cuda.stream(self.comm):
+            self.comm.wait_event(event)
+            torch.distributed.all_reduce(self.g[b0:b1], group=self.pg)
+            if with_adam:
+                self._adam_range(b0, b1, self.step_count + 1, stream=self.comm)
+
+    def _hparams(self, t):
+        c = self.cfg
+        return nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0 - c.beta1 ** t,
+                                    1.0 - c.beta2 ** t, 1.0)
+
+    def _adam_range(self, b0, b1, t, stream=None):
+        hp = self._hparams(t)
+        nnt.nnt_adam_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1], self.v[b0:b1],
+                          self.w16[b0:b1] if self.bf16 else None, hp, stream=stream)
+
+    def adam(self):
+        """Adam over every parameter (one launch over the flat buffer); bias corrections in fp64 on host."""
+        self.step_count += 1
+        self._adam_range(0, self.numel, self.step_count)
+
+    def train_step(self, x=None, r=None):
+        """forward -> probe loss -> backward (+ DP all-reduce) -> Adam.  Returns the device loss tensor.
+
+        x, r: [B,S,E] fp32, on this device or on the host (pinned host tensors are
+        copied asynchronously into the device input buffers first)."""
+        if x is not None and x.device.type == "cpu":
+            self.xs[0].copy_(x, non_blocking=True)
+            x = None
+        if r is not None and r.device.type == "cpu":
+            if not hasattr(self, "r_buf"):
+                self.r_buf = torch.empty_like(self.xs[0])
+            self.r_buf.copy_(r, non_blocking=True)
+            r = self.r_buf
+        self.forward(x)
+        self.probe_loss(r)
+        if self.world > 1:
+            self.backward(overlap_optimizer=True)
+            self.step_count += 1
+        else:
+            self.backward()
+            self.adam()
+        return self.loss

@@ -1,0 +1,329 @@
+"""Thin ctypes binding of libnnt.so (include/nnt.h) — argument marshalling only.
+
+Every function has the C name and argument order of the ABI.  Tensor arguments
+may be torch tensors (their data_ptr() is passed), plain integers (raw
+pointers) or None (NULL).  ``stream`` defaults to torch's current CUDA stream.
+Non-OK statuses raise NNTError carrying nnt_last_error().  There is no
+fallback: if libnnt.so is missing this module fails to import.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libnnt.so")
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2504_13236_b200.build` "
+                      "(there is no CPU fallback)")
+lib = C.CDLL(LIB_PATH)
+
+# ---------------------------------------------------------------- constants
+NNT_OK = 0
+NNT_ERR_NULL, NNT_ERR_SHAPE, NNT_ERR_TILE, NNT_ERR_DTYPE, NNT_ERR_ALIGN = 1, 2, 3, 4, 5
+NNT_ERR_UNSUPPORTED, NNT_ERR_WORKSPACE, NNT_ERR_CUDA, NNT_ERR_ARG = 6, 7, 8, 9
+STATUS_NAMES = {0: "NNT_OK", 1: "NNT_ERR_NULL", 2: "NNT_ERR_SHAPE", 3: "NNT_ERR_TILE", 4: "NNT_ERR_DTYPE",
+                5: "NNT_ERR_ALIGN", 6: "NNT_ERR_UNSUPPORTED", 7: "NNT_ERR_WORKSPACE", 8: "NNT_ERR_CUDA",
+                9: "NNT_ERR_ARG"}
+NNT_F32, NNT_BF16 = 0, 1
+NNT_NOTRANS, NNT_TRANS = 0, 1
+NNT_CAUSAL_NONE, NNT_CAUSAL_OUT_LOWER, NNT_CAUSAL_A_LOWER, NNT_CAUSAL_A_UPPER = 0, 1, 2, 3
+NNT_ACT_NONE, NNT_ACT_GELU, NNT_ACT_GELU_BWD = 0, 1, 2
+NNT_CAUSAL_ALIGN = 128
+KERNEL_CLASSES = ("gemm_tc", "gemm_tc_attn", "gemm_simt", "maxsumexp", "softmax", "softmax_bwd", "ln_fwd", "ln_bwd", "gelu",
+                  "bias_grad", "adam", "misc")
+OP_NAMES = ("ln1", "qkv", "scores", "maxsumexp", "softmax", "pv", "out", "ln2", "fc", "proj",
+            "proj_db", "proj_dw", "proj_dx", "fc_db", "fc_dw", "fc_dx", "ln2_bwd", "out_db", "out_dw", "out_dx",
+            "att_dp", "att_dv", "softmax_bwd", "att_dq", "att_dk", "qkv_db", "qkv_dw", "qkv_dx", "ln1_bwd")
+
+# The exported symbols include/nnt.h declares (checked by tests/test_abi.py).
+EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_grid", "nnt_tile_extent",
+           "nnt_partition", "nnt_tile_gemm", "nnt_maxsumexp", "nnt_softmax", "nnt_softmax_bwd",
+           "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
+           "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_convert",
+           "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
+           "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_launch_count")
+
+
+class NNTError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+# ---------------------------------------------------------------- structs
+class nnt_epilogue(C.Structure):
+    _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
+                ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int)]
+
+
+class nnt_adam_hparams(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay", "bias_corr1",
+                                          "bias_corr2", "grad_scale")]
+
+
+class nnt_block_cfg(C.Structure):
+    _fields_ = [("E", C.c_int64), ("H", C.c_int64), ("S", C.c_int64), ("B", C.c_int64), ("tile_e", C.c_int64),
+                ("tile_f", C.c_int64), ("tile_s", C.c_int64), ("tile_t", C.c_int64), ("dtype", C.c_int),
+                ("ln_eps", C.c_float), ("causal", C.c_int)]
+
+
+class nnt_block_params(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("ln1_g", "ln1_b", "b_qkv", "b_o", "ln2_g", "ln2_b", "b_fc", "b_pr",
+                                           "w_qkv", "w_o", "w_fc", "w_pr")]
+
+
+class nnt_block_grads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("ln1_g", "ln1_b", "w_qkv", "b_qkv", "w_o", "b_o", "ln2_g", "ln2_b",
+                                           "w_fc", "b_fc", "w_pr", "b_pr")]
+
+
+class nnt_task(C.Structure):
+    _fields_ = [("op", C.c_int32), ("level", C.c_int32), ("tile", C.c_int64 * 3), ("n_deps", C.c_int32),
+                ("group", C.c_int32)]
+
+
+class nnt_launch_group(C.Structure):
+    _fields_ = [("op", C.c_int32), ("level", C.c_int32), ("n_tasks", C.c_int64)]
+
+
+# ---------------------------------------------------------------- signatures
+_i64, _i32, _vp, _f32, _sz = C.c_int64, C.c_int, C.c_void_p, C.c_float, C.c_size_t
+_P64 = C.POINTER(C.c_int64)
+_sig = {
+    "nnt_abi_version": (C.c_int, []),
+    "nnt_last_error": (C.c_char_p, []),
+    "nnt_device_check": (_i32, [_i32]),
+    "nnt_tile_grid": (_i32, [_i32, _P64, _P64, _P64]),
+    "nnt_tile_extent": (_i32, [_i64, _i64, _i64, _P64, _P64]),
+    "nnt_partition": (_i32, [_i64, _i32, _i32, _P64, _P64]),
+    "nnt_tile_gemm": (_i32, [_i32, _i32, _i64, _i64, _i64, _P64, _f32, _vp, _i32, _i64, _P64, _vp, _i32, _i64, _P64,
+                             _f32, _vp, _i32, _i64, _P64, _P64, C.POINTER(nnt_epilogue), _vp]),
+    "nnt_maxsumexp": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _i32, _vp]),
+    "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
+    "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
+    "nnt_layernorm_fwd": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _i32, _i64, _vp, _vp, _vp]),
+    "nnt_layernorm_bwd_scratch_bytes": (_sz, [_i64, _i64]),
+    "nnt_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp,
+                                 _i32, _vp, _sz, _vp]),
+    "nnt_gelu_fwd": (_i32, [_vp, _vp, _i32, _i64, _vp]),
+    "nnt_gelu_bwd": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp]),
+    "nnt_bias_grad_scratch_bytes": (_sz, [_i64, _i64]),
+    "nnt_bias_grad": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _sz, _vp]),
+    "nnt_adam_step": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, C.POINTER(nnt_adam_hparams), _vp]),
+    "nnt_convert": (_i32, [_vp, _i32, _vp, _i32, _i64, _vp]),
+    "nnt_scale": (_i32, [_vp, _f32, _vp, _i64, _vp]),
+    "nnt_dot_scratch_bytes": (_sz, [_i64]),
+    "nnt_dot": (_i32, [_vp, _vp, _i64, _f32, _vp, _vp, _sz, _vp]),
+    "nnt_block_workspace_size": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(_sz), C.POINTER(_sz)]),
+    "nnt_block_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp]),
+    "nnt_block_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp,
+                             C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp]),
+    "nnt_op_name": (C.c_char_p, [_i32]),
+    "nnt_block_dag_describe": (_i32, [C.POINTER(nnt_block_cfg), _i32, C.POINTER(nnt_task), _i64, _P64,
+                                      C.POINTER(nnt_launch_group), _i64, _P64]),
+    "nnt_timing_enable": (_i32, [_i32]),
+    "nnt_timing_read": (_i32, [C.POINTER(C.c_double), _P64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "nnt_launch_count": (_i64, []),
+}
+for _name, (_res, _args) in _sig.items():
+    _fn = getattr(lib, _name)
+    _fn.restype = _res
+    _fn.argtypes = _args
+
+
+# ---------------------------------------------------------------- marshalling helpers
+def ptr(x):
+    """torch tensor / int / None -> void* value."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _arr64(vals):
+    if vals is None:
+        return None
+    return (C.c_int64 * len(vals))(*[int(v) for v in vals])
+
+
+def check(status):
+    if status != NNT_OK:
+        raise NNTError(status, lib.nnt_last_error().decode())
+    return status
+
+
+def dtype_code(t):
+    import torch
+    return {torch.float32: NNT_F32, torch.bfloat16: NNT_BF16}[t.dtype]
+
+
+# ---------------------------------------------------------------- ABI functions (same names)
+def nnt_abi_version():
+    return lib.nnt_abi_version()
+
+
+def nnt_last_error():
+    return lib.nnt_last_error().decode()
+
+
+def nnt_device_check(device=0):
+    return check(lib.nnt_device_check(device))
+
+
+def nnt_tile_grid(shape, tile):
+    g = (C.c_int64 * len(shape))()
+    check(lib.nnt_tile_grid(len(shape), _arr64(shape), _arr64(tile), g))
+    return list(g)
+
+
+def nnt_tile_extent(dim, tile, idx):
+    o, e = C.c_int64(), C.c_int64()
+    check(lib.nnt_tile_extent(dim, tile, idx, C.byref(o), C.byref(e)))
+    return o.value, e.value
+
+
+def nnt_partition(n_units, n_ranks, rank):
+    b, e = C.c_int64(), C.c_int64()
+    check(lib.nnt_partition(n_units, n_ranks, rank, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
+                  causal=NNT_CAUSAL_NONE):
+    return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal)
+
+
+def nnt_tile_gemm(trans_a, trans_b, M, N, K, batch, alpha, A, a_dtype, lda, stride_a, B, b_dtype, ldb, stride_b,
+                  beta, Cm, c_dtype, ldc, stride_c, tile=None, epi=None, stream=None):
+    return check(lib.nnt_tile_gemm(trans_a, trans_b, M, N, K, _arr64(batch), alpha, ptr(A), a_dtype, lda,
+                                   _arr64(stride_a), ptr(B), b_dtype, ldb, _arr64(stride_b), beta, ptr(Cm),
+                                   c_dtype, ldc, _arr64(stride_c), _arr64(tile),
+                                   C.byref(epi) if epi is not None else None, _stream(stream)))
+
+
+def nnt_maxsumexp(x, rows, cols, ldx, tile_k, causal, seq_q, stats, accumulate=0, stream=None):
+    return check(lib.nnt_maxsumexp(ptr(x), rows, cols, ldx, tile_k, causal, seq_q, ptr(stats), accumulate,
+                                   _stream(stream)))
+
+
+def nnt_softmax(x, rows, cols, ldx, tile_k, causal, seq_q, stats, y, y_dtype, ldy, stream=None):
+    return check(lib.nnt_softmax(ptr(x), rows, cols, ldx, tile_k, causal, seq_q, ptr(stats), ptr(y), y_dtype, ldy,
+                                 _stream(stream)))
+
+
+def nnt_softmax_bwd(p, p_dtype, ldp, dp, lddp, rows, cols, causal, seq_q, scale, da, da_dtype, ldda, stream=None):
+    return check(lib.nnt_softmax_bwd(ptr(p), p_dtype, ldp, ptr(dp), lddp, rows, cols, causal, seq_q, scale, ptr(da),
+                                     da_dtype, ldda, _stream(stream)))
+
+
+def nnt_layernorm_fwd(x, T, E, ldx, tile_e, gamma, beta, eps, y, y_dtype, ldy, mean, rstd, stream=None):
+    return check(lib.nnt_layernorm_fwd(ptr(x), T, E, ldx, tile_e, ptr(gamma), ptr(beta), eps, ptr(y), y_dtype, ldy,
+                                       ptr(mean), ptr(rstd), _stream(stream)))
+
+
+def nnt_layernorm_bwd_scratch_bytes(T, E):
+    return lib.nnt_layernorm_bwd_scratch_bytes(T, E)
+
+
+def nnt_layernorm_bwd(dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, dx_bf16, dgamma, dbeta,
+                      accumulate_params, scratch, scratch_bytes, stream=None):
+    return check(lib.nnt_layernorm_bwd(ptr(dy), lddy, ptr(x), ldx, ptr(mean), ptr(rstd), ptr(gamma), T, E,
+                                       ptr(dres), ptr(dx), lddx, ptr(dx_bf16), ptr(dgamma), ptr(dbeta),
+                                       accumulate_params, ptr(scratch), scratch_bytes, _stream(stream)))
+
+
+def nnt_gelu_fwd(x, y, dtype, n, stream=None):
+    return check(lib.nnt_gelu_fwd(ptr(x), ptr(y), dtype, n, _stream(stream)))
+
+
+def nnt_gelu_bwd(x, dy, dx, dtype, n, stream=None):
+    return check(lib.nnt_gelu_bwd(ptr(x), ptr(dy), ptr(dx), dtype, n, _stream(stream)))
+
+
+def nnt_bias_grad_scratch_bytes(T, N):
+    return lib.nnt_bias_grad_scratch_bytes(T, N)
+
+
+def nnt_bias_grad(dy, dy_dtype, T, N, lddy, db, accumulate, dy_bf16_out, scratch, scratch_bytes, stream=None):
+    return check(lib.nnt_bias_grad(ptr(dy), dy_dtype, T, N, lddy, ptr(db), accumulate, ptr(dy_bf16_out),
+                                   ptr(scratch), scratch_bytes, _stream(stream)))
+
+
+def nnt_adam_step(n, w, g, m, v, w_bf16, hp, stream=None):
+    return check(lib.nnt_adam_step(n, ptr(w), ptr(g), ptr(m), ptr(v), ptr(w_bf16), C.byref(hp), _stream(stream)))
+
+
+def nnt_convert(x, x_dtype, y, y_dtype, n, stream=None):
+    return check(lib.nnt_convert(ptr(x), x_dtype, ptr(y), y_dtype, n, _stream(stream)))
+
+
+def nnt_scale(x, alpha, y, n, stream=None):
+    return check(lib.nnt_scale(ptr(x), alpha, ptr(y), n, _stream(stream)))
+
+
+def nnt_dot_scratch_bytes(n):
+    return lib.nnt_dot_scratch_bytes(n)
+
+
+def nnt_dot(y, r, n, scale, out, scratch, scratch_bytes, stream=None):
+    return check(lib.nnt_dot(ptr(y), ptr(r), n, scale, ptr(out), ptr(scratch), scratch_bytes, _stream(stream)))
+
+
+def nnt_block_workspace_size(cfg):
+    a, b = C.c_size_t(), C.c_size_t()
+    check(lib.nnt_block_workspace_size(C.byref(cfg), C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def nnt_block_fwd(cfg, params, x, y, saved, scratch, stream=None):
+    return check(lib.nnt_block_fwd(C.byref(cfg), C.byref(params), ptr(x), ptr(y), ptr(saved), ptr(scratch),
+                                   _stream(stream)))
+
+
+def nnt_block_bwd(cfg, params, x, saved, scratch, dy, dx, grads, accumulate_grads, grad_ready=None, stream=None):
+    ev = None
+    if grad_ready is not None:
+        ev = (C.c_void_p * 4)(*[e.cuda_event if hasattr(e, "cuda_event") else e for e in grad_ready])
+    return check(lib.nnt_block_bwd(C.byref(cfg), C.byref(params), ptr(x), ptr(saved), ptr(scratch), ptr(dy), ptr(dx),
+                                   C.byref(grads), accumulate_grads, ev, _stream(stream)))
+
+
+def nnt_op_name(op):
+    return lib.nnt_op_name(op).decode()
+
+
+def nnt_block_dag_describe(cfg, pass_):
+    nt, ng = C.c_int64(), C.c_int64()
+    check(lib.nnt_block_dag_describe(C.byref(cfg), pass_, None, 0, C.byref(nt), None, 0, C.byref(ng)))
+    tasks = (nnt_task * nt.value)()
+    groups = (nnt_launch_group * ng.value)()
+    check(lib.nnt_block_dag_describe(C.byref(cfg), pass_, tasks, nt.value, C.byref(nt), groups, ng.value,
+                                     C.byref(ng)))
+    return list(tasks), list(groups)
+
+
+def nnt_timing_enable(enable=True):
+    return check(lib.nnt_timing_enable(1 if enable else 0))
+
+
+def nnt_timing_read():
+    n = len(KERNEL_CLASSES)
+    ms, cnt, by, fl = (C.c_double * n)(), (C.c_int64 * n)(), (C.c_double * n)(), (C.c_double * n)()
+    check(lib.nnt_timing_read(ms, cnt, by, fl))
+    return {KERNEL_CLASSES[i]: dict(ms=ms[i], launches=cnt[i], bytes=by[i], flops=fl[i]) for i in range(n)}
+
+
+def nnt_launch_count():
+    return lib.nnt_launch_count()

@@ -1,0 +1,157 @@
+"""nnt_tile_gemm (SIMT fp32 path and tcgen05 bf16 path) vs the oracle.
+
+Integer-valued inputs in [-4, 4] make every product and fp32 sum exact, so the
+tensor-core path must match the oracle BIT-EXACTLY: this pins operand majors
+(K-major / MN-major SW128 layouts), transposes, batch strides, ragged M/N/K
+tails (TMA zero fill) and causal block skipping.  Real-valued epilogue tests
+use the path tolerances.
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import nnt_inputs
+from oracle import dense, tiled
+from gpu_util import bf16_round, dev, host, rel
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2504_13236_b200 import nnt
+
+DT = {"f32": (torch.float32, 0), "bf16": (torch.bfloat16, 1)}
+
+
+def _op(a, trans):
+    return a.T if trans else a
+
+
+def _run(dtype, ta, tb, M, N, K, a, b, c_dtype="f32", beta=0.0, c0=None, epi=None, alpha=1.0):
+    tdt, code = DT[dtype]
+    A = dev(a, tdt)
+    B = dev(b, tdt)
+    ctdt, ccode = DT[c_dtype]
+    Cm = dev(c0, ctdt) if c0 is not None else torch.zeros(M, N, device="cuda", dtype=ctdt)
+    lda, ldb = a.shape[1], b.shape[1]
+    nnt.nnt_tile_gemm(ta, tb, M, N, K, None, alpha, A, code, lda, None, B, code, ldb, None, beta, Cm, ccode, N, None,
+                      (1024, 1024, 1024), epi)
+    torch.cuda.synchronize()
+    return Cm
+
+
+SHAPES = [(128, 256, 64), (200, 136, 72), (256, 64, 192), (8, 24, 16), (384, 512, 320)]
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("ta", [0, 1])
+@pytest.mark.parametrize("tb", [0, 1])
+@pytest.mark.parametrize("shape", SHAPES)
+def test_gemm_integer_bit_exact(dtype, ta, tb, shape):
+    M, N, K = shape
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + 7 * N + K, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=3 * M + N + K, kind="int")
+    want = tiled.gemm_tiled(_op(a, ta), _op(b, tb), 64, 64, 64)
+    got = host(_run(dtype, ta, tb, M, N, K, a, b))
+    assert np.array_equal(got, want), f"max |diff| {np.abs(got - want).max()}"
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0)])
+def test_gemm_bf16_output_rounding_exact(ta, tb):
+    M, N, K = 256, 128, 128
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=11, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=12, kind="int")
+    want = bf16_round(tiled.gemm_tiled(_op(a, ta), _op(b, tb), 64, 64, 64))
+    got = host(_run("bf16", ta, tb, M, N, K, a, b, c_dtype="bf16"))
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gemm_epilogues(dtype):
+    M, N, K = 192, 320, 256
+    rng = np.random.default_rng(5)
+    a = rng.standard_normal((M, K)).astype(np.float32) / 8
+    b = rng.standard_normal((N, K)).astype(np.float32) / 8
+    bias = rng.standard_normal(N).astype(np.float32)
+    res = rng.standard_normal((M, N)).astype(np.float32)
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    if dtype == "bf16":
+        a, b = bf16_round(a), bf16_round(b)
+    base = np.asarray(a, np.float64) @ np.asarray(b, np.float64).T
+    tol = 1e-5
+    # alpha, bias, beta*C, residual
+    epi = nnt.make_epilogue(bias=dev(bias), residual=dev(res), ld_residual=N)
+    got = _run(dtype, 0, 1, M, N, K, a, b, beta=0.5, c0=c0, epi=epi, alpha=0.75)
+    assert rel(host(got), 0.75 * base + bias + 0.5 * c0 + res) < tol
+    # GELU forward: aux <- pre, C <- gelu(pre)
+    aux = torch.zeros(M, N, device="cuda", dtype=DT[dtype][0])
+    epi = nnt.make_epilogue(bias=dev(bias), act=nnt.NNT_ACT_GELU, aux=aux, ld_aux=N)
+    got = _run(dtype, 0, 1, M, N, K, a, b, c_dtype=dtype, epi=epi)
+    pre = base + bias
+    t2 = 1e-6 if dtype == "f32" else 1e-2
+    assert rel(host(aux), pre) < t2
+    assert rel(host(got), dense.gelu(pre)) < t2
+    # GELU backward: C <- pre * gelu'(aux)
+    u = rng.standard_normal((M, N)).astype(np.float32)
+    if dtype == "bf16":
+        u = bf16_round(u)
+    auxu = dev(u, DT[dtype][0])
+    epi = nnt.make_epilogue(act=nnt.NNT_ACT_GELU_BWD, aux=auxu, ld_aux=N)
+    got = _run(dtype, 0, 1, M, N, K, a, b, c_dtype=dtype, epi=epi)
+    assert rel(host(got), base * dense.gelu_grad(u)) < t2
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+@pytest.mark.parametrize("causal", [0, 1, 2, 3])
+def test_gemm_attention_views_and_causal(dtype, causal):
+    """Batched (N_b, N_h) views into a fused [B, S, 3E] qkv buffer, integer data."""
+    B, S, H, Dh = 2, 384, 3, 64
+    E = H * Dh
+    tdt, code = DT[dtype]
+    qkv = nnt_inputs.make_matrix((B, S, 3 * E), seed=40 + causal, kind="int")
+    q = qkv[:, :, :E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    k = qkv[:, :, E:2 * E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    Q = dev(qkv, tdt)
+    es = Q.element_size()
+    sq = (S * 3 * E, Dh)
+    batch = (B, H)
+    if causal in (0, 1):
+        # scores = Q K^T, C [B][H][S][S]
+        Cm = torch.zeros(B, H, S, S, device="cuda", dtype=torch.float32)
+        epi = nnt.make_epilogue(causal=causal)
+        nnt.nnt_tile_gemm(0, 1, S, S, Dh, batch, 1.0, Q, code, 3 * E, sq, Q.data_ptr() + es * E, code, 3 * E, sq, 0.0,
+                          Cm, 0, S, (H * S * S, S * S), None, epi)
+        torch.cuda.synchronize()
+        want = q @ k.transpose(0, 1, 3, 2)
+        got = host(Cm)
+        if causal:
+            mask = np.tril(np.ones((S, S), bool))
+            assert np.array_equal(got[..., mask], want[..., mask])
+        else:
+            assert np.array_equal(got, want)
+    else:
+        # causal=2: O = P V with P lower triangular; causal=3: dV = P^T dO with P^T upper
+        P = nnt_inputs.make_matrix((B, H, S, S), seed=50, kind="int")
+        P = P * np.tril(np.ones((S, S), np.float32))
+        Pd = dev(P, tdt)
+        v = qkv[:, :, 2 * E:].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+        O = torch.zeros(B, S, E, device="cuda", dtype=torch.float32)
+        epi = nnt.make_epilogue(causal=causal)
+        ta = 0 if causal == 2 else 1
+        nnt.nnt_tile_gemm(ta, 0, S, Dh, S, batch, 1.0, Pd, code, S, (H * S * S, S * S), Q.data_ptr() + es * 2 * E,
+                          code, 3 * E, sq, 0.0, O, 0, E, (S * E, Dh), None, epi)
+        torch.cuda.synchronize()
+        Pop = P if causal == 2 else P.transpose(0, 1, 3, 2)
+        want = (Pop @ v).transpose(0, 2, 1, 3).reshape(B, S, E)
+        assert np.array_equal(host(O), want)
+
+
+def test_gemm_rejects_bad_arguments():
+    A = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(nnt.NNTError) as e:  # misaligned leading dimension for TMA
+        nnt.nnt_tile_gemm(0, 1, 64, 64, 60, None, 1.0, A, 1, 60, None, A, 1, 60, None, 0.0, A, 1, 64, None)
+    assert e.value.status == nnt.NNT_ERR_ALIGN
+    with pytest.raises(nnt.NNTError) as e:  # mixed operand dtypes
+        nnt.nnt_tile_gemm(0, 1, 64, 64, 64, None, 1.0, A, 1, 64, None, A, 0, 64, None, 0.0, A, 1, 64, None)
+    assert e.value.status == nnt.NNT_ERR_DTYPE
