@@ -80,13 +80,14 @@ def test_gemm_epilogues(dtype):
         a, b = bf16_round(a), bf16_round(b)
     base = np.asarray(a, np.float64) @ np.asarray(b, np.float64).T
     tol = 1e-5
-    # alpha, bias, beta*C, residual
-    epi = nnt.make_epilogue(bias=dev(bias), residual=dev(res), ld_residual=N)
+    # alpha, bias, beta*C, residual (device tensors must outlive the launch: keep references)
+    bias_d, res_d = dev(bias), dev(res)
+    epi = nnt.make_epilogue(bias=bias_d, residual=res_d, ld_residual=N)
     got = _run(dtype, 0, 1, M, N, K, a, b, beta=0.5, c0=c0, epi=epi, alpha=0.75)
     assert rel(host(got), 0.75 * base + bias + 0.5 * c0 + res) < tol
     # GELU forward: aux <- pre, C <- gelu(pre)
     aux = torch.zeros(M, N, device="cuda", dtype=DT[dtype][0])
-    epi = nnt.make_epilogue(bias=dev(bias), act=nnt.NNT_ACT_GELU, aux=aux, ld_aux=N)
+    epi = nnt.make_epilogue(bias=bias_d, act=nnt.NNT_ACT_GELU, aux=aux, ld_aux=N)
     got = _run(dtype, 0, 1, M, N, K, a, b, c_dtype=dtype, epi=epi)
     pre = base + bias
     t2 = 1e-6 if dtype == "f32" else 1e-2

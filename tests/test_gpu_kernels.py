@@ -242,7 +242,9 @@ def test_adam_matches_oracle_and_step1_closed_form():
         nnt.nnt_adam_step(n, W, dev(g), M, V, W16, hp)
         wr, mr, vr = dense.adam_step(wr, g, mr, vr, t)
         torch.cuda.synchronize()
-        assert rel(host(W) - w, wr - w) < 1e-5  # compare the update, not w
+        # compare the update, not w; fp32 storage of w ~ N(0,1) bounds the update's rel error
+        # near 2^-24 / lr ~ 6e-5 (worst element), hence the fp32-path tolerance
+        assert rel(host(W) - w, wr - w) < 1e-4
         assert rel(host(M), mr) < 1e-6 and rel(host(V), vr) < 1e-5
         assert np.array_equal(host(W16), bf16_round(host(W)))
 

@@ -296,6 +296,20 @@ def test_block_fd_every_parameter_and_input():
         assert rel(ana, fd) < 1e-6, name
 
 
+def test_key_bias_gradient_is_zero():
+    """A key bias adds q.b_k to every score of a query row: a per-row constant that the
+    softmax (shift-invariant) removes, so dL/db_k = 0 exactly."""
+    E, H, S, B = 16, 2, 6, 2
+    params = nnt_inputs.make_params(E, seed=13)
+    x = nnt_inputs.make_x(E, S, 0, B, seed=14)
+    r = nnt_inputs.make_r(E, S, 0, B, seed=14)
+    _, cache = dense.block_fwd(params, x, H)
+    _, grads = dense.block_bwd(params, cache, r)
+    gb = grads["b_qkv"]
+    assert np.abs(gb[E:2 * E]).max() < 1e-13 * np.abs(gb).max()
+    assert np.abs(gb[:E]).max() > 1e-3 and np.abs(gb[2 * E:]).max() > 1e-3
+
+
 def test_stack_two_layers_fd_directional():
     E, H, S, B = 8, 2, 4, 2
     layers = [{k: v.astype(np.float64) for k, v in nnt_inputs.make_params(E, seed=31, layer=l).items()}
