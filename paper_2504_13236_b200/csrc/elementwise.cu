@@ -2,7 +2,7 @@
 // bias-gradient column sums, dtype conversion and the probe-loss dot product.
 // All are HBM-bound: 128-bit vector access, grid-stride loops sized in
 // multiples of the SM count, deterministic (ordered) reductions, no atomics.
-#include "nnt_internal.h"
+#include "reduce.cuh"
 
 namespace nnt {
 namespace {
@@ -138,7 +138,15 @@ inline ColsumPlan colsum_plan(int64_t T, int64_t N) {
   return {chunks, rows_per};
 }
 
-template <typename T>
+__device__ __forceinline__ float4 load4f(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 load4f(const __nv_bfloat16* p) {
+  uint2 u = *reinterpret_cast<const uint2*>(p);
+  float2 a = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.x));
+  float2 b = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u.y));
+  return make_float4(a.x, a.y, b.x, b.y);
+}
+
+template <typename T, bool VEC>
 __global__ void __launch_bounds__(kThreads) colsum_partial_kernel(const T* __restrict__ dy, int64_t T_, int64_t N,
                                                                   int64_t ld, int64_t rows_per,
                                                                   float* __restrict__ partial,
@@ -150,15 +158,32 @@ __global__ void __launch_bounds__(kThreads) colsum_partial_kernel(const T* __res
   int64_t r1 = r0 + rows_per;
   if (r1 > T_) r1 = T_;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int64_t r = r0 + warp; r < r1; r += 8) {
-    const T* row = dy + r * ld;
+  if (VEC) {
+    if (col0 < N) {
+#pragma unroll 4
+      for (int64_t r = r0 + warp; r < r1; r += 8) {
+        float4 v = load4f(dy + r * ld + col0);
+        acc[0] += v.x; acc[1] += v.y; acc[2] += v.z; acc[3] += v.w;
+        if (copy16) {
+          __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+          uint2 pk;
+          pk.x = *reinterpret_cast<uint32_t*>(&lo);
+          pk.y = *reinterpret_cast<uint32_t*>(&hi);
+          *reinterpret_cast<uint2*>(copy16 + r * ld + col0) = pk;
+        }
+      }
+    }
+  } else {
+    for (int64_t r = r0 + warp; r < r1; r += 8) {
+      const T* row = dy + r * ld;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      int64_t c = col0 + j;
-      if (c < N) {
-        float v = to_f32(row[c]);
-        acc[j] += v;
-        if (copy16) copy16[r * ld + c] = __float2bfloat16_rn(v);
+      for (int j = 0; j < 4; ++j) {
+        int64_t c = col0 + j;
+        if (c < N) {
+          float v = to_f32(row[c]);
+          acc[j] += v;
+          if (copy16) copy16[r * ld + c] = __float2bfloat16_rn(v);
+        }
       }
     }
   }
@@ -172,15 +197,6 @@ __global__ void __launch_bounds__(kThreads) colsum_partial_kernel(const T* __res
     int64_t c = (int64_t)blockIdx.x * 128 + threadIdx.x;
     if (c < N) partial[(int64_t)blockIdx.y * N + c] = s;
   }
-}
-
-__global__ void __launch_bounds__(kThreads) colsum_merge_kernel(const float* __restrict__ partial, int64_t chunks,
-                                                                int64_t N, float* __restrict__ out, int accumulate) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= N) return;
-  float s = 0.f;
-  for (int64_t k = 0; k < chunks; ++k) s += partial[k * N + c];
-  out[c] = accumulate ? out[c] + s : s;
 }
 
 // ------------------------------------------------------------------ dot
@@ -313,15 +329,27 @@ nnt_status nnt_bias_grad(const void* dy, int dy_dtype, int64_t T, int64_t N, int
   double bytes = (double)T * N * dtype_size(dy_dtype) + (dy_bf16_out ? 2.0 * T * N : 0.0) + 4.0 * N;
   LaunchScope sc(NNT_K_BIAS_GRAD, stream, bytes, 0, 2);
   dim3 grid((unsigned)((N + 127) / 128), (unsigned)p.chunks);
-  if (dy_dtype == NNT_F32)
-    colsum_partial_kernel<float><<<grid, kThreads, 0, stream>>>((const float*)dy, T, N, lddy, p.rows_per,
-                                                                (float*)scratch, (__nv_bfloat16*)dy_bf16_out);
-  else
-    colsum_partial_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>(
-        (const __nv_bfloat16*)dy, T, N, lddy, p.rows_per, (float*)scratch, nullptr);
+  const size_t es = dtype_size(dy_dtype);
+  const bool vec = N % 4 == 0 && lddy % 4 == 0 && (reinterpret_cast<uintptr_t>(dy) % (4 * es)) == 0 &&
+                   (!dy_bf16_out || (reinterpret_cast<uintptr_t>(dy_bf16_out) & 7u) == 0);
+  __nv_bfloat16* c16 = (__nv_bfloat16*)dy_bf16_out;
+  if (dy_dtype == NNT_F32) {
+    if (vec)
+      colsum_partial_kernel<float, true><<<grid, kThreads, 0, stream>>>((const float*)dy, T, N, lddy, p.rows_per,
+                                                                        (float*)scratch, c16);
+    else
+      colsum_partial_kernel<float, false><<<grid, kThreads, 0, stream>>>((const float*)dy, T, N, lddy, p.rows_per,
+                                                                         (float*)scratch, c16);
+  } else {
+    if (vec)
+      colsum_partial_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, stream>>>(
+          (const __nv_bfloat16*)dy, T, N, lddy, p.rows_per, (float*)scratch, nullptr);
+    else
+      colsum_partial_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, stream>>>(
+          (const __nv_bfloat16*)dy, T, N, lddy, p.rows_per, (float*)scratch, nullptr);
+  }
   NNT_TRY(check_launch("bias_grad partial"));
-  colsum_merge_kernel<<<(unsigned)((N + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
-      (const float*)scratch, p.chunks, N, db, accumulate);
+  launch_column_merge((const float*)scratch, p.chunks, N, db, accumulate, stream);
   return check_launch("bias_grad merge");
 }
 

@@ -1,28 +1,19 @@
-// LayerNorm forward / backward.  HBM-bound row kernels: one
-// 128-thread CTA per token row, the row held in registers (128-bit loads),
-// block reductions by warp shuffle + a 4-entry shared array.  The backward's
-// dgamma/dbeta are per-row-chunk column partials merged in ascending chunk
-// order (deterministic, no atomics).
-#include "nnt_internal.h"
+// LayerNorm forward / backward.  HBM-bound row kernels.
+//   E <= 1024: one WARP per token row (row in registers as float4, reductions by
+//              warp shuffle only), 8 rows per 256-thread CTA;
+//   E  > 1024: one 128-thread CTA per row (shuffle + 4-entry shared array).
+// The backward's dgamma/dbeta are per-CTA column partials (rows of a CTA are
+// accumulated in a fixed order) merged by the deterministic column merge
+// (reduce.cuh): bitwise reproducible, no atomics.
+#include "reduce.cuh"
 
 namespace nnt {
 namespace {
 
-constexpr int kT = 128;          // threads per CTA
-constexpr int kMaxNV = 16;       // float4 per thread -> E <= 8192
-constexpr int kBwdRowsPer = 16;  // rows per dgamma/dbeta partial chunk
-
-__device__ __forceinline__ float block_sum(float v, float* sh) {
-  v = warp_sum(v);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) sh[w] = v;
-  __syncthreads();
-  float t = 0.f;
-#pragma unroll
-  for (int i = 0; i < kT / 32; ++i) t += sh[i];  // fixed order
-  return t;
-}
+constexpr int kWarpRowsPerCta = 8;   // warp kernels: 8 warps
+constexpr int kWarpBwdRows = 32;     // warp bwd kernel: rows per CTA (= per partial)
+constexpr int kT = 128;              // CTA-per-row kernels: threads
+constexpr int kCtaBwdRows = 16;      // CTA-per-row bwd kernel: rows per partial
 
 template <typename T>
 __device__ __forceinline__ void store4(T* p, float4 v);
@@ -37,15 +28,75 @@ __device__ __forceinline__ void store4<__nv_bfloat16>(__nv_bfloat16* p, float4 v
   *reinterpret_cast<uint2*>(p) = pk;
 }
 
-// Forward: steps 1-3 of P:162 for one row.  Column index of (thread, j) is
-// 4*(tid + j*kT); shifted sums with c = x[row][0] (R9); tile_e partials are
-// merged in ascending tile order by summation, which is what the block
-// reduction computes (fixed order).
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < kT / 32; ++i) t += sh[i];  // fixed order
+  return t;
+}
+
+// Normalise + affine of one float4 (steps 2 and 3 of P:162).
+__device__ __forceinline__ float4 affine(float4 v, float4 g, float4 b, float mu, float rs) {
+  return make_float4(g.x * ((v.x - mu) * rs) + b.x, g.y * ((v.y - mu) * rs) + b.y, g.z * ((v.z - mu) * rs) + b.z,
+                     g.w * ((v.w - mu) * rs) + b.w);
+}
+
+// ------------------------------------------------------------------ forward, warp per row
+// Step 1 with shifted sums (c = x[row][0], R9); E-tile partials are merged by
+// summation, which is what the (fixed-order) shuffle reduction computes.
 template <typename TO, int NV>
-__global__ void __launch_bounds__(kT) ln_fwd_kernel(const float* __restrict__ x, int64_t E, int64_t ldx,
-                                                    const float* __restrict__ gamma, const float* __restrict__ beta,
-                                                    float eps, TO* __restrict__ y, int64_t ldy,
-                                                    float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+__global__ void __launch_bounds__(32 * kWarpRowsPerCta)
+    ln_fwd_warp(const float* __restrict__ x, int64_t T, int E, int64_t ldx, const float* __restrict__ gamma,
+                const float* __restrict__ beta, float eps, TO* __restrict__ y, int64_t ldy,
+                float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
+  if (row >= T) return;
+  const float* xr = x + row * ldx;
+  const float c = __ldg(xr);
+  float4 v[NV];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int col = 4 * (lane + 32 * j);
+    if (col < E) {
+      v[j] = ldg4(xr + col);
+      float d0 = v[j].x - c, d1 = v[j].y - c, d2 = v[j].z - c, d3 = v[j].w - c;
+      s1 += (d0 + d1) + (d2 + d3);
+      s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    }
+  }
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
+  const float inv_e = 1.0f / (float)E;
+  const float ms = s1 * inv_e;
+  const float var = fmaxf(s2 * inv_e - ms * ms, 0.f);
+  const float mu = c + ms, rs = rsqrtf(var + eps);
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+  TO* yr = y + row * ldy;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int col = 4 * (lane + 32 * j);
+    if (col < E) store4<TO>(yr + col, affine(v[j], ldg4(gamma + col), ldg4(beta + col), mu, rs));
+  }
+}
+
+// ------------------------------------------------------------------ forward, CTA per row
+template <typename TO, int NV>
+__global__ void __launch_bounds__(kT) ln_fwd_cta(const float* __restrict__ x, int64_t E, int64_t ldx,
+                                                 const float* __restrict__ gamma, const float* __restrict__ beta,
+                                                 float eps, TO* __restrict__ y, int64_t ldy,
+                                                 float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   __shared__ float sh[kT / 32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * ldx;
@@ -56,7 +107,7 @@ __global__ void __launch_bounds__(kT) ln_fwd_kernel(const float* __restrict__ x,
   for (int j = 0; j < NV; ++j) {
     int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
     if (col < E) {
-      v[j] = __ldg(reinterpret_cast<const float4*>(xr + col));
+      v[j] = ldg4(xr + col);
       float d0 = v[j].x - c, d1 = v[j].y - c, d2 = v[j].z - c, d3 = v[j].w - c;
       s1 += (d0 + d1) + (d2 + d3);
       s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
@@ -67,8 +118,7 @@ __global__ void __launch_bounds__(kT) ln_fwd_kernel(const float* __restrict__ x,
   const float inv_e = 1.0f / (float)E;
   const float ms = s1 * inv_e;
   const float var = fmaxf(s2 * inv_e - ms * ms, 0.f);
-  const float mu = c + ms;
-  const float rs = rsqrtf(var + eps);
+  const float mu = c + ms, rs = rsqrtf(var + eps);
   if (threadIdx.x == 0) {
     mean_out[row] = mu;
     rstd_out[row] = rs;
@@ -77,28 +127,106 @@ __global__ void __launch_bounds__(kT) ln_fwd_kernel(const float* __restrict__ x,
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
     int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-    if (col < E) {
-      float4 g = __ldg(reinterpret_cast<const float4*>(gamma + col));
-      float4 b = __ldg(reinterpret_cast<const float4*>(beta + col));
-      float4 o;
-      o.x = g.x * ((v[j].x - mu) * rs) + b.x;
-      o.y = g.y * ((v[j].y - mu) * rs) + b.y;
-      o.z = g.z * ((v[j].z - mu) * rs) + b.z;
-      o.w = g.w * ((v[j].w - mu) * rs) + b.w;
-      store4<TO>(yr + col, o);
-    }
+    if (col < E) store4<TO>(yr + col, affine(v[j], ldg4(gamma + col), ldg4(beta + col), mu, rs));
   }
 }
 
-// Backward for a chunk of kBwdRowsPer rows; dgamma/dbeta partial of the chunk.
+// ------------------------------------------------------------------ backward helpers
+struct RowGrad {
+  float4 xh, dxh;
+};
+
+// dx of one float4 given the row means sa = mean(dxhat), sb = mean(dxhat*xhat)
+__device__ __forceinline__ float4 dx_of(const RowGrad& r, float rs, float sa, float sb) {
+  return make_float4(rs * (r.dxh.x - sa - r.xh.x * sb), rs * (r.dxh.y - sa - r.xh.y * sb),
+                     rs * (r.dxh.z - sa - r.xh.z * sb), rs * (r.dxh.w - sa - r.xh.w * sb));
+}
+
+// ------------------------------------------------------------------ backward, warp per row
 template <int NV>
-__global__ void __launch_bounds__(kT) ln_bwd_kernel(const float* __restrict__ dy, int64_t lddy,
-                                                    const float* __restrict__ x, int64_t ldx,
-                                                    const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                    const float* __restrict__ gamma, int64_t T, int64_t E,
-                                                    const float* dres, float* dx, int64_t lddx,
-                                                    __nv_bfloat16* __restrict__ dx16,
-                                                    float* __restrict__ pg, float* __restrict__ pb) {
+__global__ void __launch_bounds__(32 * kWarpRowsPerCta)
+    ln_bwd_warp(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
+                const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
+                int64_t T, int E, const float* dres, float* dx, int64_t lddx, __nv_bfloat16* __restrict__ dx16,
+                float* __restrict__ pg, float* __restrict__ pb) {
+  __shared__ float red[kWarpRowsPerCta][1024];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  float4 accg[NV], accb[NV], g4[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    accg[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    accb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int col = 4 * (lane + 32 * j);
+    g4[j] = col < E ? ldg4(gamma + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int64_t r0 = (int64_t)blockIdx.x * kWarpBwdRows;
+  const int64_t r1 = min(r0 + kWarpBwdRows, T);
+  const float inv_e = 1.0f / (float)E;
+  for (int64_t row = r0 + w; row < r1; row += kWarpRowsPerCta) {
+    const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
+    RowGrad rg[NV];
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int col = 4 * (lane + 32 * j);
+      if (col < E) {
+        float4 xv = ldg4(x + row * ldx + col);
+        float4 d = ldg4(dy + row * lddy + col);
+        rg[j].xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        rg[j].dxh = make_float4(d.x * g4[j].x, d.y * g4[j].y, d.z * g4[j].z, d.w * g4[j].w);
+        sa += (rg[j].dxh.x + rg[j].dxh.y) + (rg[j].dxh.z + rg[j].dxh.w);
+        sb += (rg[j].dxh.x * rg[j].xh.x + rg[j].dxh.y * rg[j].xh.y) +
+              (rg[j].dxh.z * rg[j].xh.z + rg[j].dxh.w * rg[j].xh.w);
+        accg[j].x += d.x * rg[j].xh.x; accg[j].y += d.y * rg[j].xh.y;
+        accg[j].z += d.z * rg[j].xh.z; accg[j].w += d.w * rg[j].xh.w;
+        accb[j].x += d.x; accb[j].y += d.y; accb[j].z += d.z; accb[j].w += d.w;
+      }
+    }
+    sa = warp_sum(sa) * inv_e;
+    sb = warp_sum(sb) * inv_e;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int col = 4 * (lane + 32 * j);
+      if (col < E) {
+        float4 o = dx_of(rg[j], rs, sa, sb);
+        if (dres) {
+          float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + col);
+          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+        }
+        *reinterpret_cast<float4*>(dx + row * lddx + col) = o;
+        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + col, o);
+      }
+    }
+  }
+  // per-CTA partial: warps combined in fixed order through shared memory (gamma, then beta)
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int col = 4 * (lane + 32 * j);
+      if (col < E) *reinterpret_cast<float4*>(&red[w][col]) = pass == 0 ? accg[j] : accb[j];
+    }
+    __syncthreads();
+    float* out = pass == 0 ? pg : pb;
+    for (int col = threadIdx.x; col < E; col += 32 * kWarpRowsPerCta) {
+      float s = 0.f;
+#pragma unroll
+      for (int i = 0; i < kWarpRowsPerCta; ++i) s += red[i][col];
+      out[(int64_t)blockIdx.x * E + col] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ backward, CTA per row
+template <int NV>
+__global__ void __launch_bounds__(kT) ln_bwd_cta(const float* __restrict__ dy, int64_t lddy,
+                                                 const float* __restrict__ x, int64_t ldx,
+                                                 const float* __restrict__ mean, const float* __restrict__ rstd,
+                                                 const float* __restrict__ gamma, int64_t T, int64_t E,
+                                                 const float* dres, float* dx, int64_t lddx,
+                                                 __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg,
+                                                 float* __restrict__ pb) {
   __shared__ float sh[kT / 32];
   float4 accg[NV], accb[NV], g4[NV];
 #pragma unroll
@@ -106,27 +234,28 @@ __global__ void __launch_bounds__(kT) ln_bwd_kernel(const float* __restrict__ dy
     accg[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     accb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
     int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-    if (col < E) g4[j] = __ldg(reinterpret_cast<const float4*>(gamma + col));
+    if (col < E) g4[j] = ldg4(gamma + col);
   }
-  const int64_t r0 = (int64_t)blockIdx.x * kBwdRowsPer;
-  const int64_t r1 = min(r0 + kBwdRowsPer, T);
+  const int64_t r0 = (int64_t)blockIdx.x * kCtaBwdRows;
+  const int64_t r1 = min(r0 + kCtaBwdRows, T);
   const float inv_e = 1.0f / (float)E;
   for (int64_t row = r0; row < r1; ++row) {
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    float4 xh[NV], dxh[NV];
+    RowGrad rg[NV];
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
       if (col < E) {
-        float4 xv = __ldg(reinterpret_cast<const float4*>(x + row * ldx + col));
-        float4 d = __ldg(reinterpret_cast<const float4*>(dy + row * lddy + col));
-        xh[j] = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        dxh[j] = make_float4(d.x * g4[j].x, d.y * g4[j].y, d.z * g4[j].z, d.w * g4[j].w);
-        sa += (dxh[j].x + dxh[j].y) + (dxh[j].z + dxh[j].w);
-        sb += (dxh[j].x * xh[j].x + dxh[j].y * xh[j].y) + (dxh[j].z * xh[j].z + dxh[j].w * xh[j].w);
-        accg[j].x += d.x * xh[j].x; accg[j].y += d.y * xh[j].y;
-        accg[j].z += d.z * xh[j].z; accg[j].w += d.w * xh[j].w;
+        float4 xv = ldg4(x + row * ldx + col);
+        float4 d = ldg4(dy + row * lddy + col);
+        rg[j].xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        rg[j].dxh = make_float4(d.x * g4[j].x, d.y * g4[j].y, d.z * g4[j].z, d.w * g4[j].w);
+        sa += (rg[j].dxh.x + rg[j].dxh.y) + (rg[j].dxh.z + rg[j].dxh.w);
+        sb += (rg[j].dxh.x * rg[j].xh.x + rg[j].dxh.y * rg[j].xh.y) +
+              (rg[j].dxh.z * rg[j].xh.z + rg[j].dxh.w * rg[j].xh.w);
+        accg[j].x += d.x * rg[j].xh.x; accg[j].y += d.y * rg[j].xh.y;
+        accg[j].z += d.z * rg[j].xh.z; accg[j].w += d.w * rg[j].xh.w;
         accb[j].x += d.x; accb[j].y += d.y; accb[j].z += d.z; accb[j].w += d.w;
       }
     }
@@ -136,11 +265,7 @@ __global__ void __launch_bounds__(kT) ln_bwd_kernel(const float* __restrict__ dy
     for (int j = 0; j < NV; ++j) {
       int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
       if (col < E) {
-        float4 o;
-        o.x = rs * (dxh[j].x - sa - xh[j].x * sb);
-        o.y = rs * (dxh[j].y - sa - xh[j].y * sb);
-        o.z = rs * (dxh[j].z - sa - xh[j].z * sb);
-        o.w = rs * (dxh[j].w - sa - xh[j].w * sb);
+        float4 o = dx_of(rg[j], rs, sa, sb);
         if (dres) {
           float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + col);
           o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
@@ -160,38 +285,43 @@ __global__ void __launch_bounds__(kT) ln_bwd_kernel(const float* __restrict__ dy
   }
 }
 
-__global__ void ln_param_merge_kernel(const float* __restrict__ pg, const float* __restrict__ pb, int64_t chunks,
-                                      int64_t E, float* dgamma, float* dbeta, int accumulate) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= E) return;
-  float sg = 0.f, sb = 0.f;
-  for (int64_t k = 0; k < chunks; ++k) {
-    sg += pg[k * E + c];
-    sb += pb[k * E + c];
-  }
-  dgamma[c] = accumulate ? dgamma[c] + sg : sg;
-  dbeta[c] = accumulate ? dbeta[c] + sb : sb;
+int pick_nv_cta(int64_t E) {
+  int64_t need = (E / 4 + kT - 1) / kT;
+  const int opts[] = {1, 2, 3, 4, 6, 8, 12, 16};
+  for (int o : opts)
+    if (o >= need) return o;
+  return -1;
+}
+int pick_nv_warp(int64_t E) {
+  if (E > 1024) return -1;
+  int64_t need = (E / 4 + 31) / 32;
+  const int opts[] = {1, 2, 4, 6, 8};
+  for (int o : opts)
+    if (o >= need) return o;
+  return -1;
 }
 
 template <typename TO>
-nnt_status launch_fwd(int nv, const float* x, int64_t T, int64_t E, int64_t ldx, const float* g, const float* b,
-                      float eps, TO* y, int64_t ldy, float* mean, float* rstd, cudaStream_t s) {
-#define NNT_LNF(NVV) \
-  case NVV: ln_fwd_kernel<TO, NVV><<<(unsigned)T, kT, 0, s>>>(x, E, ldx, g, b, eps, y, ldy, mean, rstd); break;
+nnt_status launch_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, const float* g, const float* b, float eps,
+                      TO* y, int64_t ldy, float* mean, float* rstd, cudaStream_t s) {
+  int nvw = pick_nv_warp(E);
+  if (nvw > 0) {
+    unsigned grid = (unsigned)((T + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+#define NNT_LNFW(N) \
+  case N: ln_fwd_warp<TO, N><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(x, T, (int)E, ldx, g, b, eps, y, ldy, mean, rstd); break;
+    switch (nvw) { NNT_LNFW(1) NNT_LNFW(2) NNT_LNFW(4) NNT_LNFW(6) NNT_LNFW(8) }
+#undef NNT_LNFW
+    return check_launch("layernorm_fwd");
+  }
+  int nv = pick_nv_cta(E);
+#define NNT_LNF(N) \
+  case N: ln_fwd_cta<TO, N><<<(unsigned)T, kT, 0, s>>>(x, E, ldx, g, b, eps, y, ldy, mean, rstd); break;
   switch (nv) {
     NNT_LNF(1) NNT_LNF(2) NNT_LNF(3) NNT_LNF(4) NNT_LNF(6) NNT_LNF(8) NNT_LNF(12) NNT_LNF(16)
     default: return fail(NNT_ERR_UNSUPPORTED, "layernorm: unsupported E");
   }
 #undef NNT_LNF
   return check_launch("layernorm_fwd");
-}
-
-int pick_nv(int64_t E) {
-  int64_t need = (E / 4 + kT - 1) / kT;
-  const int opts[] = {1, 2, 3, 4, 6, 8, 12, 16};
-  for (int o : opts)
-    if (o >= need) return o;
-  return -1;
 }
 
 }  // namespace
@@ -212,16 +342,15 @@ nnt_status nnt_layernorm_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, 
   NNT_REQUIRE(E % 4 == 0 && ldx % 4 == 0 && ldy % 4 == 0 && aligned16(x) && aligned16(gamma) &&
                   aligned16(beta) && aligned16(y),
               NNT_ERR_ALIGN, "nnt_layernorm_fwd: E, ld must be multiples of 4 and pointers 16B aligned");
-  int nv = pick_nv(E);
-  NNT_REQUIRE(nv > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_fwd: E=%lld > 8192", (long long)E);
+  NNT_REQUIRE(pick_nv_cta(E) > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_fwd: E=%lld > 8192", (long long)E);
   LaunchScope sc(NNT_K_LN_FWD, stream, (double)T * E * (4 + dtype_size(y_dtype)) + 8.0 * T, 0);
-  if (y_dtype == NNT_F32) return launch_fwd<float>(nv, x, T, E, ldx, gamma, beta, eps, (float*)y, ldy, mean, rstd, stream);
-  return launch_fwd<__nv_bfloat16>(nv, x, T, E, ldx, gamma, beta, eps, (__nv_bfloat16*)y, ldy, mean, rstd, stream);
+  if (y_dtype == NNT_F32) return launch_fwd<float>(x, T, E, ldx, gamma, beta, eps, (float*)y, ldy, mean, rstd, stream);
+  return launch_fwd<__nv_bfloat16>(x, T, E, ldx, gamma, beta, eps, (__nv_bfloat16*)y, ldy, mean, rstd, stream);
 }
 
 size_t nnt_layernorm_bwd_scratch_bytes(int64_t T, int64_t E) {
   if (T <= 0 || E <= 0) return 0;
-  int64_t chunks = (T + kBwdRowsPer - 1) / kBwdRowsPer;
+  int64_t chunks = (T + kCtaBwdRows - 1) / kCtaBwdRows;  // >= the warp kernel's chunk count
   return (size_t)(2 * chunks * E) * sizeof(float);
 }
 
@@ -239,26 +368,34 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
               NNT_ERR_ALIGN, "nnt_layernorm_bwd: alignment");
   NNT_REQUIRE(scratch_bytes >= nnt_layernorm_bwd_scratch_bytes(T, E), NNT_ERR_WORKSPACE,
               "nnt_layernorm_bwd: scratch %zu < %zu", scratch_bytes, nnt_layernorm_bwd_scratch_bytes(T, E));
-  int nv = pick_nv(E);
-  NNT_REQUIRE(nv > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: E=%lld > 8192", (long long)E);
-  int64_t chunks = (T + kBwdRowsPer - 1) / kBwdRowsPer;
+  NNT_REQUIRE(pick_nv_cta(E) > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: E=%lld > 8192", (long long)E);
+  const int nvw = pick_nv_warp(E);
+  const int64_t chunks = nvw > 0 ? (T + kWarpBwdRows - 1) / kWarpBwdRows : (T + kCtaBwdRows - 1) / kCtaBwdRows;
   float* pg = (float*)scratch;
   float* pb = pg + chunks * E;
   double bytes = (double)T * E * (4 + 4 + 4 + (dres ? 4 : 0) + (dx_bf16 ? 2 : 0)) + 8.0 * T;
-  LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 2);
-#define NNT_LNB(NVV)                                                                                        \
-  case NVV:                                                                                                 \
-    ln_bwd_kernel<NVV><<<(unsigned)chunks, kT, 0, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, \
-                                                            dx, lddx, (__nv_bfloat16*)dx_bf16, pg, pb);      \
+  LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 3);
+  __nv_bfloat16* d16 = (__nv_bfloat16*)dx_bf16;
+  if (nvw > 0) {
+#define NNT_LNBW(N)                                                                                         \
+  case N:                                                                                                   \
+    ln_bwd_warp<N><<<(unsigned)chunks, 32 * kWarpRowsPerCta, 0, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, \
+                                                                          T, (int)E, dres, dx, lddx, d16, pg, pb); \
     break;
-  switch (nv) {
-    NNT_LNB(1) NNT_LNB(2) NNT_LNB(3) NNT_LNB(4) NNT_LNB(6) NNT_LNB(8) NNT_LNB(12) NNT_LNB(16)
-    default: return fail(NNT_ERR_UNSUPPORTED, "layernorm_bwd: unsupported E");
-  }
+    switch (nvw) { NNT_LNBW(1) NNT_LNBW(2) NNT_LNBW(4) NNT_LNBW(6) NNT_LNBW(8) }
+#undef NNT_LNBW
+  } else {
+#define NNT_LNB(N)                                                                                               \
+  case N:                                                                                                        \
+    ln_bwd_cta<N><<<(unsigned)chunks, kT, 0, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, \
+                                                       d16, pg, pb);                                             \
+    break;
+    switch (pick_nv_cta(E)) { NNT_LNB(1) NNT_LNB(2) NNT_LNB(3) NNT_LNB(4) NNT_LNB(6) NNT_LNB(8) NNT_LNB(12) NNT_LNB(16) }
 #undef NNT_LNB
+  }
   NNT_TRY(check_launch("layernorm_bwd"));
-  ln_param_merge_kernel<<<(unsigned)((E + 255) / 256), 256, 0, stream>>>(pg, pb, chunks, E, dgamma, dbeta,
-                                                                          accumulate_params);
+  launch_column_merge(pg, chunks, E, dgamma, accumulate_params, stream);
+  launch_column_merge(pb, chunks, E, dbeta, accumulate_params, stream);
   return check_launch("layernorm_bwd merge");
 }
 

@@ -1,0 +1,47 @@
+// Deterministic column merge of row-chunk partials: out[c] (+)= sum_k part[k][c],
+// k ascending within each of 8 contiguous k-ranges, then the 8 range sums in
+// ascending order.  A fixed association (no atomics), so results are bitwise
+// reproducible; 32 columns per CTA (coalesced 128 B rows), 8 warps split k.
+#pragma once
+#include "nnt_internal.h"
+
+namespace nnt {
+
+constexpr int kMergeWarps = 8;
+
+static __global__ void __launch_bounds__(32 * kMergeWarps)
+    column_merge_kernel(const float* __restrict__ part, int64_t chunks, int64_t N, float* __restrict__ out,
+                        int accumulate) {
+  __shared__ float red[kMergeWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * 32 + lane;
+  const int64_t per = (chunks + kMergeWarps - 1) / kMergeWarps;
+  const int64_t k0 = w * per, k1 = min(chunks, k0 + per);
+  float s = 0.f;
+  if (c < N) {
+    int64_t k = k0;
+    for (; k + 4 <= k1; k += 4) {
+      float a = part[k * N + c], b = part[(k + 1) * N + c], d = part[(k + 2) * N + c], e = part[(k + 3) * N + c];
+      s += a;
+      s += b;
+      s += d;
+      s += e;
+    }
+    for (; k < k1; ++k) s += part[k * N + c];
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < N) {
+    float t = 0.f;
+#pragma unroll
+    for (int i = 0; i < kMergeWarps; ++i) t += red[i][lane];
+    out[c] = accumulate ? out[c] + t : t;
+  }
+}
+
+static inline void launch_column_merge(const float* part, int64_t chunks, int64_t N, float* out, int accumulate,
+                                cudaStream_t s) {
+  column_merge_kernel<<<(unsigned)((N + 31) / 32), 32 * kMergeWarps, 0, s>>>(part, chunks, N, out, accumulate);
+}
+
+}  // namespace nnt

@@ -92,8 +92,24 @@ __global__ void __launch_bounds__(kThreads) maxsumexp_kernel(const float* __rest
     }
   }
   float M = -CUDART_INF_F, S = 0.f;
+  if (tile_k >= nvalid) {
+    // one key tile covers the slice: (m, s) straight from registers (masked entries are -inf -> 0)
+    float mj = -CUDART_INF_F;
+#pragma unroll
+    for (int c = 0; c < NC; ++c) mj = fmaxf(fmaxf(mj, fmaxf(v[c].x, v[c].y)), fmaxf(v[c].z, v[c].w));
+    mj = warp_max(mj);
+    float sj = 0.f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+      if (c * 128 < nvalid)  // warp-uniform: skip chunks entirely past the causal prefix
+        sj += (ex2((v[c].x - mj) * kLog2e) + ex2((v[c].y - mj) * kLog2e)) +
+              (ex2((v[c].z - mj) * kLog2e) + ex2((v[c].w - mj) * kLog2e));
+    sj = warp_sum(sj);
+    M = mj;
+    S = sj;
+  }
   // per key tile [t0, t0 + tile_k): partial (m_j, s_j), merged in ascending order
-  for (int64_t t0 = 0; t0 < nvalid; t0 += tile_k) {
+  for (int64_t t0 = 0; tile_k < nvalid && t0 < nvalid; t0 += tile_k) {
     const int64_t t1 = min(t0 + tile_k, nvalid);
     float mj = -CUDART_INF_F;
 #pragma unroll

@@ -1,0 +1,44 @@
+"""One steady-state training step of a config inside cudaProfilerStart/Stop, for
+`ncu --profile-from-start off` (launch lists, --set full captures).
+
+    python tools/profile_step.py [--config small] [--warmup 2]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import nnt_inputs  # noqa: E402
+from paper_2504_13236_b200 import model  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="small")
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--layers", type=int, default=None)
+    a = ap.parse_args()
+    L, E, H, S, B = bench.CONFIGS[a.config]
+    L = a.layers or L
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    st = model.BlockStack(sc, [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L)
+                               for l in range(L)])
+    x = torch.from_numpy(nnt_inputs.make_x(E, S, 0, B)).cuda()
+    r = torch.from_numpy(nnt_inputs.make_r(E, S, 0, B)).cuda()
+    for _ in range(a.warmup):
+        st.train_step(x, r)
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStart()
+    st.train_step(x, r)
+    torch.cuda.synchronize()
+    torch.cuda.cudart().cudaProfilerStop()
+    print("profiled one step; loss", st.loss.item())
+
+
+if __name__ == "__main__":
+    main()
