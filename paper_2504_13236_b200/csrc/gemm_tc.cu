@@ -3,13 +3,22 @@
 // warp-specialised persistent CTAs:
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bias / residual /
-//               GELU / GELU' -> global, double-buffered accumulators so the
-//               epilogue of tile i overlaps the MMAs of tile i+1.
-// Both operand majors are supported natively (instruction-descriptor major
-// bits + the canonical K-major / MN-major SW128 shared-memory layouts), so
-// dX = dY W, dW = dY^T X and all six attention products run without transposes.
-// Batch items (b, head) are the two outer dimensions of 4-D TMA tensor maps.
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bias / beta*C /
+//               residual / GELU / GELU' -> swizzled smem staging -> TMA bulk
+//               tensor store (coalesced, asynchronous); double-buffered TMEM
+//               accumulators so the epilogue of tile i overlaps tile i+1's MMAs.
+// Both operand majors are native (instruction-descriptor major bits + the
+// canonical K-major / MN-major SW128 shared-memory layouts), so dX = dY W,
+// dW = dY^T X and the six attention products run without transposes.  Batch
+// items (b, head) are the two outer dimensions of 4-D TMA tensor maps.
+//
+// Split-K (small output grids with long K, i.e. the dW GEMMs): the K range of a
+// tile is cut into `splits` contiguous pieces computed by different CTAs; their
+// fp32 partial tiles are accumulated into C in ascending split order through a
+// per-tile semaphore (split s waits until split s-1 has stored), so the sum
+// has one fixed association and results are bitwise reproducible.  Split-K
+// GEMMs on one device must not run concurrently (they share the semaphores);
+// the block executor issues them on one stream.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -18,11 +27,17 @@
 #include "gemm_common.cuh"
 
 namespace nnt {
+
+__device__ unsigned int g_tile_sem[65536];  // split-K semaphores (zero at load, reset by the last split)
+
 namespace {
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one SW128 row
 constexpr int kThreads = 192;
+constexpr int kEpiWarps = 4;
+constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for one TMA store box
+constexpr int kMaxSemTiles = 65536;
 
 template <int BN>
 struct Cfg {
@@ -31,14 +46,18 @@ struct Cfg {
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
   static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr int EPI_BYTES = kEpiWarps * 2 * kStageBytesPerWarp;  // C + aux staging per warp
+  static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
 struct TcParams {
   GemmArgs g;
-  int64_t mt, nt, tiles_per_batch, num_tiles;
+  int64_t mt, nt, tiles_per_batch, num_tiles, num_tasks;
+  int64_t splits, kb_per_split;
   uint32_t idesc;
   int a_kmajor, b_kmajor;
+  int tma_store;  // epilogue stores through TMA (C and aux maps valid)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -74,6 +93,17 @@ __device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -91,7 +121,8 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -102,6 +133,8 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
 // SW128 shared-memory matrix descriptor (sm_100 "version 1" format).
@@ -115,117 +148,138 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// Which tiles exist and which K range each covers (nnt_causal semantics).
+// Which tiles exist and which K-blocks each task covers (nnt_causal semantics + split-K).
 struct TileInfo {
-  int64_t bz, m0, n0, kb_begin, kb_end;
+  int64_t tile, bz, m0, n0, kb_begin, kb_end, split;
   bool skip;
 };
-__device__ __forceinline__ TileInfo decode_tile(const TcParams& P, int64_t t, int bn) {
+__device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, int bn) {
   TileInfo ti;
-  ti.bz = t / P.tiles_per_batch;
-  int64_t r = t % P.tiles_per_batch;
+  ti.split = t % P.splits;
+  ti.tile = t / P.splits;
+  ti.bz = ti.tile / P.tiles_per_batch;
+  int64_t r = ti.tile % P.tiles_per_batch;
   int64_t nb = r / P.mt, mb = r % P.mt;
   ti.m0 = mb * BM;
   ti.n0 = nb * bn;
   int64_t k_begin = 0, k_end = P.g.K;
   if (P.g.causal == NNT_CAUSAL_A_LOWER) k_end = min(P.g.K, ti.m0 + BM);
   if (P.g.causal == NNT_CAUSAL_A_UPPER) k_begin = min(P.g.K, ti.m0);
-  ti.kb_begin = k_begin / BK;
-  ti.kb_end = (k_end + BK - 1) / BK;
+  int64_t kb0 = k_begin / BK, kb1 = (k_end + BK - 1) / BK;
+  ti.kb_begin = min(kb1, kb0 + ti.split * P.kb_per_split);
+  ti.kb_end = min(kb1, ti.kb_begin + P.kb_per_split);
   ti.skip = (P.g.causal == NNT_CAUSAL_OUT_LOWER) && (ti.n0 > ti.m0 + BM - 1);
   return ti;
 }
 
-// ------------------------------------------------------------------ epilogue
-template <typename TC>
-__device__ __forceinline__ void store32(TC* dst, const float (&v)[32]);
-template <>
-__device__ __forceinline__ void store32<float>(float* dst, const float (&v)[32]) {
-#pragma unroll
-  for (int j = 0; j < 32; j += 4) *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-}
-template <>
-__device__ __forceinline__ void store32<__nv_bfloat16>(__nv_bfloat16* dst, const float (&v)[32]) {
-#pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    uint4 u;
-    __nv_bfloat162 t0 = __floats2bfloat162_rn(v[j], v[j + 1]), t1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
-    __nv_bfloat162 t2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]), t3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
-    u.x = *reinterpret_cast<uint32_t*>(&t0);
-    u.y = *reinterpret_cast<uint32_t*>(&t1);
-    u.z = *reinterpret_cast<uint32_t*>(&t2);
-    u.w = *reinterpret_cast<uint32_t*>(&t3);
-    *reinterpret_cast<uint4*>(dst + j) = u;
+// ------------------------------------------------------------------ epilogue math
+template <bool kFast>
+__device__ __forceinline__ float tanh_f(float x) {
+  if (kFast) {  // bf16 outputs: tanh.approx (rel err ~2^-11) is below bf16 rounding
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
   }
+  return tanhf(x);  // fp32 outputs: accurate tanh (R15)
 }
-template <typename TC>
-__device__ __forceinline__ void load32(const TC* src, float (&v)[32]);
-template <>
-__device__ __forceinline__ void load32<float>(const float* src, float (&v)[32]) {
+template <bool kFast>
+__device__ __forceinline__ float gelu_e(float u) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  return 0.5f * u * (1.0f + tanh_f<kFast>(c * (u + a * u * u * u)));
+}
+template <bool kFast>
+__device__ __forceinline__ float gelu_grad_e(float u) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  float t = tanh_f<kFast>(c * (u + a * u * u * u));
+  return 0.5f * (1.0f + t) + 0.5f * u * (1.0f - t * t) * c * (1.0f + 3.0f * a * u * u);
+}
+
+template <typename T>
+__device__ __forceinline__ float ld_elem(const T* p) { return to_f32(*p); }
+// C is re-read after other CTAs (split-K) or TMA stores wrote it: bypass L1.
+__device__ __forceinline__ float ld_c(const float* p) { return __ldcg(p); }
+__device__ __forceinline__ float ld_c(const __nv_bfloat16* p) {
+  unsigned short u = __ldcg(reinterpret_cast<const unsigned short*>(p));
+  return __bfloat162float(__ushort_as_bfloat16(u));
+}
+
+// Computes the W outputs of one row chunk in registers.  pre-activation kept in `pre`.
+template <typename TC, int W>
+__device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const TC* auxb, int64_t row, int64_t col0,
+                                         float beta, bool first, float (&v)[W], float (&pre)[W]) {
+  constexpr bool kFast = sizeof(TC) == 2;
+  const bool full = (row < g.M) && (col0 + W <= g.N);
 #pragma unroll
-  for (int j = 0; j < 32; j += 4) {
-    float4 t = *reinterpret_cast<const float4*>(src + j);
-    v[j] = t.x; v[j + 1] = t.y; v[j + 2] = t.z; v[j + 3] = t.w;
+  for (int j = 0; j < W; ++j) v[j] *= g.alpha;
+  if (row < g.M) {
+    if (first && g.bias) {
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (full || col0 + j < g.N) v[j] += __ldg(g.bias + col0 + j);
+    }
+    if (beta != 0.f) {
+      const TC* cr = Cb + row * g.ldc + col0;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (full || col0 + j < g.N) v[j] += beta * ld_c(cr + j);
+    }
+    if (first && g.residual) {
+      const float* rr = g.residual + row * g.ld_res + col0;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (full || col0 + j < g.N) v[j] += rr[j];
+    }
+    if (g.act == NNT_ACT_GELU_BWD) {
+      const TC* ar = auxb + row * g.ld_aux + col0;
+#pragma unroll
+      for (int j = 0; j < W; ++j)
+        if (full || col0 + j < g.N) v[j] *= gelu_grad_e<kFast>(ld_elem(ar + j));
+    }
   }
-}
-template <>
-__device__ __forceinline__ void load32<__nv_bfloat16>(const __nv_bfloat16* src, float (&v)[32]) {
+  if (g.act == NNT_ACT_GELU) {
 #pragma unroll
-  for (int j = 0; j < 32; j += 8) {
-    uint4 u = *reinterpret_cast<const uint4*>(src + j);
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      float2 f = __bfloat1622float2(h[t]);
-      v[j + 2 * t] = f.x;
-      v[j + 2 * t + 1] = f.y;
+    for (int j = 0; j < W; ++j) {
+      pre[j] = v[j];
+      v[j] = gelu_e<kFast>(v[j]);
     }
   }
 }
 
-template <typename TC>
-__device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, TC* Cb, TC* auxb, int64_t row, int64_t col0,
-                                               const uint32_t (&r)[32], bool vec_ok) {
+// Writes a 128-byte row chunk to SW128-swizzled staging (row = lane, 8 x 16 B pieces).
+template <typename TC, int W>
+__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float (&v)[W]) {
+  uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint4 u;
+    if (sizeof(TC) == 4) {
+      u.x = __float_as_uint(v[4 * j]);
+      u.y = __float_as_uint(v[4 * j + 1]);
+      u.z = __float_as_uint(v[4 * j + 2]);
+      u.w = __float_as_uint(v[4 * j + 3]);
+    } else {
+      __nv_bfloat162 t0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+      __nv_bfloat162 t1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+      __nv_bfloat162 t3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+      u.x = *reinterpret_cast<uint32_t*>(&t0);
+      u.y = *reinterpret_cast<uint32_t*>(&t1);
+      u.z = *reinterpret_cast<uint32_t*>(&t2);
+      u.w = *reinterpret_cast<uint32_t*>(&t3);
+    }
+    *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
+  }
+}
+
+template <typename TC, int W>
+__device__ __forceinline__ void direct_store(const GemmArgs& g, TC* Cb, TC* auxb, int64_t row, int64_t col0,
+                                             const float (&v)[W], const float (&pre)[W]) {
   if (row >= g.M) return;
-  if (vec_ok && col0 + 32 <= g.N) {
-    float v[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = g.alpha * __uint_as_float(r[j]);
-    if (g.bias) {
-#pragma unroll
-      for (int j = 0; j < 32; j += 4) {
-        float4 b = __ldg(reinterpret_cast<const float4*>(g.bias + col0 + j));
-        v[j] += b.x; v[j + 1] += b.y; v[j + 2] += b.z; v[j + 3] += b.w;
-      }
-    }
-    if (g.beta != 0.f) {
-      float o[32];
-      load32<TC>(Cb + row * g.ldc + col0, o);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += g.beta * o[j];
-    }
-    if (g.residual) {
-      float o[32];
-      load32<float>(g.residual + row * g.ld_res + col0, o);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] += o[j];
-    }
-    if (g.act == NNT_ACT_GELU) {
-      store32<TC>(auxb + row * g.ld_aux + col0, v);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
-    } else if (g.act == NNT_ACT_GELU_BWD) {
-      float u[32];
-      load32<TC>(auxb + row * g.ld_aux + col0, u);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(u[j]);
-    }
-    store32<TC>(Cb + row * g.ldc + col0, v);
-  } else {
-#pragma unroll 1
-    for (int j = 0; j < 32; ++j) {
-      int64_t col = col0 + j;
-      if (col < g.N) epilogue_store<TC>(g, Cb, auxb, row, col, __uint_as_float(r[j]));
+  for (int j = 0; j < W; ++j) {
+    if (col0 + j < g.N) {
+      Cb[row * g.ldc + col0 + j] = from_f32<TC>(v[j]);
+      if (g.act == NNT_ACT_GELU) auxb[row * g.ld_aux + col0 + j] = from_f32<TC>(pre[j]);
     }
   }
 }
@@ -234,11 +288,13 @@ __device__ __forceinline__ void epilogue_chunk(const GemmArgs& g, TC* Cb, TC* au
 template <int BN, typename TC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
-                   const __grid_constant__ CUtensorMap tmB) {
+                   const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
+                   const __grid_constant__ CUtensorMap tmAux) {
   using C = Cfg<BN>;
+  constexpr int W = 128 / (int)sizeof(TC);  // columns per 128-byte staging row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::EPI_OFF + C::EPI_BYTES);
   uint64_t* full = bars;
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
@@ -255,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&tfull[s]), 1);
-      mbar_init(smem_u32(&tempty[s]), 4);
+      mbar_init(smem_u32(&tempty[s]), kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -277,8 +333,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-        TileInfo ti = decode_tile(P, t, BN);
+      for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
+        TileInfo ti = decode_task(P, t, BN);
         if (ti.skip) continue;
         const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
@@ -319,8 +375,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // apart; +2 KB per UMMA_K=16.
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
-      for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-        TileInfo ti = decode_tile(P, t, BN);
+      for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
+        TileInfo ti = decode_task(P, t, BN);
         if (ti.skip) continue;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
@@ -352,34 +408,64 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ===================== epilogue (warps 2..5 -> TMEM lane quadrants 2,3,0,1)
     const int quad = warp & 3;
+    uint8_t* stage_c = smem + C::EPI_OFF + quad * 2 * kStageBytesPerWarp;
+    uint8_t* stage_a = stage_c + kStageBytesPerWarp;
+    const uint32_t stage_c_u32 = smem_u32(stage_c), stage_a_u32 = smem_u32(stage_a);
     int acc = 0;
     uint32_t acc_phase = 0;
-    const size_t cs = sizeof(TC);
-    const bool vec_ok = ((g.ldc * cs) % 16 == 0) && ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) &&
-                        (!g.residual || (g.ld_res % 4 == 0 && (reinterpret_cast<uintptr_t>(g.residual) & 15) == 0)) &&
-                        (!g.aux || ((g.ld_aux * cs) % 16 == 0 && (reinterpret_cast<uintptr_t>(g.aux) & 15) == 0)) &&
-                        (!g.bias || (reinterpret_cast<uintptr_t>(g.bias) & 15) == 0) &&
-                        ((g.sc0 * cs) % 16 == 0) && ((g.sc1 * cs) % 16 == 0);
-    for (int64_t t = blockIdx.x; t < P.num_tiles; t += gridDim.x) {
-      TileInfo ti = decode_tile(P, t, BN);
+    for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
+      TileInfo ti = decode_task(P, t, BN);
       if (ti.skip) continue;
       const int64_t p = ti.bz / g.batch1, q = ti.bz % g.batch1;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
+      const bool first = ti.split == 0;
+      const float beta = first ? g.beta : 1.0f;  // later splits accumulate onto the stored partial sum
+      if (P.splits > 1 && !first) {
+        // ordered split-K: wait until split (s-1) of this tile has stored its partial sum
+        if (warp == 2 && lane == 0) {
+          const unsigned int want = (unsigned int)ti.split;
+          unsigned int cur;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&g_tile_sem[ti.tile]) : "memory");
+          } while (cur != want);
+        }
+        epi_bar();
+      }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
       const int64_t row = ti.m0 + quad * 32 + lane;
       const bool has_k = ti.kb_end > ti.kb_begin;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        if (has_k) {
-          tmem_ld32(tmem_base + (uint32_t)(acc * BN + c) + ((uint32_t)(quad * 32) << 16), r);
-        } else {
+      for (int c = 0; c < BN; c += W) {
+        if (ti.n0 + c >= g.N) break;  // warp-uniform
+        float v[W], pre[W];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) r[j] = 0u;
+        for (int h = 0; h < W / 32; ++h) {
+          if (has_k) {
+            tmem_ld32(tmem_base + (uint32_t)(acc * BN + c + 32 * h) + ((uint32_t)(quad * 32) << 16), v + 32 * h);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 * h + j] = 0.f;
+          }
         }
-        if (ti.n0 + c < g.N) epilogue_chunk<TC>(g, Cb, auxb, row, ti.n0 + c, r, vec_ok);
+        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, beta, first, v, pre);
+        if (P.tma_store) {
+          if (lane == 0) bulk_wait_read0();  // staging buffers free again
+          __syncwarp();
+          stage_row<TC, W>(stage_c, lane, v);
+          if (g.act == NNT_ACT_GELU) stage_row<TC, W>(stage_a, lane, pre);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
+            tma_store_4d(&tmC, stage_c_u32, cx, cy, (int)q, (int)p);
+            if (g.act == NNT_ACT_GELU) tma_store_4d(&tmAux, stage_a_u32, cx, cy, (int)q, (int)p);
+            bulk_commit();
+          }
+        } else {
+          direct_store<TC, W>(g, Cb, auxb, row, ti.n0 + c, v, pre);
+        }
       }
       tc_fence_before();
       __syncwarp();
@@ -388,7 +474,19 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if (P.splits > 1) {
+        // publish: this split's sum is in C (stores complete and visible), then signal split s+1
+        if (lane == 0 && P.tma_store) bulk_wait0();
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        epi_bar();
+        if (warp == 2 && lane == 0) {
+          const unsigned int next = (ti.split + 1 == P.splits) ? 0u : (unsigned int)(ti.split + 1);
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&g_tile_sem[ti.tile]), "r"(next) : "memory");
+        }
+      }
     }
+    if (lane == 0 && P.tma_store) bulk_wait0();
   }
 
   tc_fence_before();
@@ -417,23 +515,36 @@ nnt_status get_encoder() {
   return NNT_OK;
 }
 
-// 4-D bf16 tensor map: dims {inner, outer, batch1, batch0}.
-nnt_status make_map(CUtensorMap* map, const void* base, int64_t inner, int64_t outer, int64_t ld, int64_t b1,
-                    int64_t s1, int64_t b0, int64_t s0, int box_inner, int box_outer) {
+// 4-D tensor map: dims {inner, outer, batch1, batch0}; es = element bytes.
+nnt_status make_map(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t inner, int64_t outer,
+                    int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_inner, int box_outer) {
   cuuint64_t dims[4] = {(cuuint64_t)inner, (cuuint64_t)outer, (cuuint64_t)b1, (cuuint64_t)b0};
   // size-1 batch dims get a harmless valid stride
   int64_t st1 = b1 > 1 ? s1 : ld * outer;
   int64_t st0 = b0 > 1 ? s0 : st1 * b1;
-  cuuint64_t strides[3] = {(cuuint64_t)(ld * 2), (cuuint64_t)(st1 * 2), (cuuint64_t)(st0 * 2)};
+  cuuint64_t strides[3] = {(cuuint64_t)(ld * es), (cuuint64_t)(st1 * es), (cuuint64_t)(st0 * es)};
   cuuint32_t box[4] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, estr,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = g_encode(map, dt, 4, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   NNT_REQUIRE(r == CUDA_SUCCESS, NNT_ERR_CUDA,
               "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld s1=%lld s0=%lld", (int)r,
               (long long)inner, (long long)outer, (long long)ld, (long long)s1, (long long)s0);
   return NNT_OK;
+}
+
+// Split-K factor: only for fp32 C without activation (the dW GEMMs) whose output grid
+// leaves most SMs idle and whose K is long enough to cut.
+int64_t choose_splits(const GemmArgs& a, int64_t tiles, int64_t nkb) {
+  if (a.c_dtype != NNT_F32 || a.act != NNT_ACT_NONE || a.causal != NNT_CAUSAL_NONE || a.batch0 * a.batch1 != 1)
+    return 1;
+  const int64_t sms = num_sms();
+  if (tiles * 2 > sms || tiles > kMaxSemTiles) return 1;
+  int64_t s = sms / tiles;
+  if (s > nkb / 8) s = nkb / 8;  // keep >= 8 K-blocks per split
+  if (s > 16) s = 16;
+  return s < 1 ? 1 : s;
 }
 
 template <int BN, typename TC>
@@ -455,20 +566,42 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s) {
   P.nt = (a.N + BN - 1) / BN;
   P.tiles_per_batch = P.mt * P.nt;
   P.num_tiles = P.tiles_per_batch * a.batch0 * a.batch1;
+  const int64_t nkb = (a.K + BK - 1) / BK;
+  P.splits = choose_splits(a, P.num_tiles, nkb);
+  P.kb_per_split = (nkb + P.splits - 1) / P.splits;
+  P.splits = (nkb + P.kb_per_split - 1) / P.kb_per_split;  // no empty splits
+  P.num_tasks = P.num_tiles * P.splits;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((P.b_kmajor ? 0u : 1u) << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC, tmAux;
+  const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (P.a_kmajor)
-    NNT_TRY(make_map(&tmA, a.A, a.K, a.M, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, BK, BM));
+    NNT_TRY(make_map(&tmA, bf, 2, a.A, a.K, a.M, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, BK, BM));
   else
-    NNT_TRY(make_map(&tmA, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, 64, BK));
+    NNT_TRY(make_map(&tmA, bf, 2, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, 64, BK));
   if (P.b_kmajor)
-    NNT_TRY(make_map(&tmB, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN));
+    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN));
   else
-    NNT_TRY(make_map(&tmB, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
-  int64_t grid = P.num_tiles < num_sms() ? P.num_tiles : num_sms();
+    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
+  // epilogue through TMA stores when C (and aux) satisfy the tensor-map rules
+  const size_t es = sizeof(TC);
+  const CUtensorMapDataType cdt = sizeof(TC) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : bf;
+  const int W = (int)(128 / es);
+  auto ok16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  bool tma_ok = ok16(a.C) && (a.ldc * es) % 16 == 0 && (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
+                (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
+                (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
+  P.tma_store = tma_ok ? 1 : 0;
+  memset(&tmC, 0, sizeof(tmC));
+  memset(&tmAux, 0, sizeof(tmAux));
+  if (tma_ok) {
+    NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+    if (a.act == NNT_ACT_GELU)
+      NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+  }
+  int64_t grid = P.num_tasks < num_sms() ? P.num_tasks : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, TC><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB);
+  gemm_tc_kernel<BN, TC><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
   return check_launch("gemm_tc");
 }
 

@@ -11,7 +11,7 @@ namespace nnt {
 namespace {
 
 constexpr int kWarpRowsPerCta = 8;   // warp kernels: 8 warps
-constexpr int kWarpBwdRows = 32;     // warp bwd kernel: rows per CTA (= per partial)
+constexpr int kWarpBwdRows = 16;     // warp bwd kernel: rows per CTA (= per partial)
 constexpr int kT = 128;              // CTA-per-row kernels: threads
 constexpr int kCtaBwdRows = 16;      // CTA-per-row bwd kernel: rows per partial
 
@@ -143,78 +143,81 @@ __device__ __forceinline__ float4 dx_of(const RowGrad& r, float rs, float sa, fl
 }
 
 // ------------------------------------------------------------------ backward, warp per row
+// Per row two passes over x and dy (the second hits L1): pass 1 forms the two row
+// means and accumulates dgamma/dbeta into this warp's shared-memory slice (each lane
+// owns fixed columns, so no atomics); pass 2 writes dx.  Registers stay low enough
+// for 3+ CTAs (24+ warps) per SM.
 template <int NV>
 __global__ void __launch_bounds__(32 * kWarpRowsPerCta)
     ln_bwd_warp(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 int64_t T, int E, const float* dres, float* dx, int64_t lddx, __nv_bfloat16* __restrict__ dx16,
                 float* __restrict__ pg, float* __restrict__ pb) {
-  __shared__ float red[kWarpRowsPerCta][1024];
+  extern __shared__ float4 sacc4[];  // [warps][2][E/4]
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  float4 accg[NV], accb[NV], g4[NV];
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    accg[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    accb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int col = 4 * (lane + 32 * j);
-    g4[j] = col < E ? ldg4(gamma + col) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const int E4 = E / 4;
+  float4* accg = sacc4 + (size_t)w * 2 * E4;
+  float4* accb = accg + E4;
+  for (int i = lane; i < E4; i += 32) {
+    accg[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    accb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   const int64_t r0 = (int64_t)blockIdx.x * kWarpBwdRows;
   const int64_t r1 = min(r0 + kWarpBwdRows, T);
   const float inv_e = 1.0f / (float)E;
   for (int64_t row = r0 + w; row < r1; row += kWarpRowsPerCta) {
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    RowGrad rg[NV];
+    const float* xr = x + row * ldx;
+    const float* dr = dy + row * lddy;
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int col = 4 * (lane + 32 * j);
-      if (col < E) {
-        float4 xv = ldg4(x + row * ldx + col);
-        float4 d = ldg4(dy + row * lddy + col);
-        rg[j].xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        rg[j].dxh = make_float4(d.x * g4[j].x, d.y * g4[j].y, d.z * g4[j].z, d.w * g4[j].w);
-        sa += (rg[j].dxh.x + rg[j].dxh.y) + (rg[j].dxh.z + rg[j].dxh.w);
-        sb += (rg[j].dxh.x * rg[j].xh.x + rg[j].dxh.y * rg[j].xh.y) +
-              (rg[j].dxh.z * rg[j].xh.z + rg[j].dxh.w * rg[j].xh.w);
-        accg[j].x += d.x * rg[j].xh.x; accg[j].y += d.y * rg[j].xh.y;
-        accg[j].z += d.z * rg[j].xh.z; accg[j].w += d.w * rg[j].xh.w;
-        accb[j].x += d.x; accb[j].y += d.y; accb[j].z += d.z; accb[j].w += d.w;
+      const int i4 = lane + 32 * j;
+      if (4 * i4 < E) {
+        float4 xv = ldg4(xr + 4 * i4), d = ldg4(dr + 4 * i4), g = ldg4(gamma + 4 * i4);
+        float4 xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        float4 dxh = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
+        sa += (dxh.x + dxh.y) + (dxh.z + dxh.w);
+        sb += (dxh.x * xh.x + dxh.y * xh.y) + (dxh.z * xh.z + dxh.w * xh.w);
+        float4 ag = accg[i4], ab = accb[i4];
+        ag.x += d.x * xh.x; ag.y += d.y * xh.y; ag.z += d.z * xh.z; ag.w += d.w * xh.w;
+        ab.x += d.x; ab.y += d.y; ab.z += d.z; ab.w += d.w;
+        accg[i4] = ag;
+        accb[i4] = ab;
       }
     }
     sa = warp_sum(sa) * inv_e;
     sb = warp_sum(sb) * inv_e;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      const int col = 4 * (lane + 32 * j);
-      if (col < E) {
-        float4 o = dx_of(rg[j], rs, sa, sb);
+      const int i4 = lane + 32 * j;
+      if (4 * i4 < E) {
+        float4 xv = ldg4(xr + 4 * i4), d = ldg4(dr + 4 * i4), g = ldg4(gamma + 4 * i4);
+        RowGrad rg;
+        rg.xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
+        rg.dxh = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
+        float4 o = dx_of(rg, rs, sa, sb);
         if (dres) {
-          float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + col);
+          float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + 4 * i4);
           o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
         }
-        *reinterpret_cast<float4*>(dx + row * lddx + col) = o;
-        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + col, o);
+        *reinterpret_cast<float4*>(dx + row * lddx + 4 * i4) = o;
+        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + 4 * i4, o);
       }
     }
   }
-  // per-CTA partial: warps combined in fixed order through shared memory (gamma, then beta)
+  __syncthreads();
+  // per-CTA partial: the warps' slices combined in fixed warp order
+  for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kWarpRowsPerCta) {
+    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), sb4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int col = 4 * (lane + 32 * j);
-      if (col < E) *reinterpret_cast<float4*>(&red[w][col]) = pass == 0 ? accg[j] : accb[j];
+    for (int k = 0; k < kWarpRowsPerCta; ++k) {
+      float4 a = sacc4[(size_t)k * 2 * E4 + i4], b = sacc4[(size_t)k * 2 * E4 + E4 + i4];
+      sg.x += a.x; sg.y += a.y; sg.z += a.z; sg.w += a.w;
+      sb4.x += b.x; sb4.y += b.y; sb4.z += b.z; sb4.w += b.w;
     }
-    __syncthreads();
-    float* out = pass == 0 ? pg : pb;
-    for (int col = threadIdx.x; col < E; col += 32 * kWarpRowsPerCta) {
-      float s = 0.f;
-#pragma unroll
-      for (int i = 0; i < kWarpRowsPerCta; ++i) s += red[i][col];
-      out[(int64_t)blockIdx.x * E + col] = s;
-    }
-    __syncthreads();
+    reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E)[i4] = sg;
+    reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = sb4;
   }
 }
 
@@ -377,11 +380,22 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
   LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 3);
   __nv_bfloat16* d16 = (__nv_bfloat16*)dx_bf16;
   if (nvw > 0) {
-#define NNT_LNBW(N)                                                                                         \
-  case N:                                                                                                   \
-    ln_bwd_warp<N><<<(unsigned)chunks, 32 * kWarpRowsPerCta, 0, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, \
-                                                                          T, (int)E, dres, dx, lddx, d16, pg, pb); \
+#define NNT_LNBW(N)                                                                                              \
+  case N:                                                                                                        \
+    ln_bwd_warp<N><<<(unsigned)chunks, 32 * kWarpRowsPerCta, smem_acc, stream>>>(dy, lddy, x, ldx, mean, rstd,   \
+                                                                                 gamma, T, (int)E, dres, dx,     \
+                                                                                 lddx, d16, pg, pb);             \
     break;
+    const size_t smem_acc = (size_t)kWarpRowsPerCta * 2 * E * sizeof(float);  // <= 64 KB (E <= 1024)
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(ln_bwd_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(ln_bwd_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(ln_bwd_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(ln_bwd_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      cudaFuncSetAttribute(ln_bwd_warp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+      attr_set = true;
+    }
     switch (nvw) { NNT_LNBW(1) NNT_LNBW(2) NNT_LNBW(4) NNT_LNBW(6) NNT_LNBW(8) }
 #undef NNT_LNBW
   } else {

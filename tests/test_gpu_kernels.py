@@ -245,7 +245,8 @@ def test_adam_matches_oracle_and_step1_closed_form():
         # compare the update, not w; fp32 storage of w ~ N(0,1) bounds the update's rel error
         # near 2^-24 / lr ~ 6e-5 (worst element), hence the fp32-path tolerance
         assert rel(host(W) - w, wr - w) < 1e-4
-        assert rel(host(M), mr) < 1e-6 and rel(host(V), vr) < 1e-5
+        # fp32 beta2 = 0.999f makes (1 - beta2) off by 1.3e-5 relative: v inherits it
+        assert rel(host(M), mr) < 1e-6 and rel(host(V), vr) < 3e-5
         assert np.array_equal(host(W16), bf16_round(host(W)))
 
 
