@@ -117,7 +117,17 @@ typedef struct {
                              (written by NNT_ACT_GELU, read by NNT_ACT_GELU_BWD)    */
   int64_t ld_aux;
   int causal;             /* nnt_causal (applies per batch item)                   */
+  void* workspace;        /* device scratch for split-K partials, or NULL (no split);
+                             see nnt_tile_gemm_workspace_bytes                     */
+  size_t workspace_bytes;
 } nnt_epilogue;
+
+/* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would
+ * not split).  Splitting applies to fp32 C without activation or causal mode (the dW GEMMs):
+ * split s writes alpha * (its K-range partial) to workspace slice s and an ordered reduce
+ * forms C = beta*C + sum_s partial_s (+bias, +residual), splits added in ascending order. */
+size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int c_dtype, int act, int causal,
+                                     int64_t batch_items);
 
 /*
  * C = epilogue( alpha * op(A) · op(B) ),  for each of batch[0]*batch[1] items.

@@ -15,8 +15,8 @@ struct Layout {
   // saved (per layer)
   size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
   // scratch
-  size_t scores, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, scratch_bytes;
-  size_t colsum_bytes, lnscr_bytes;
+  size_t scores, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
+  size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -61,6 +61,17 @@ Layout make_layout(const nnt_block_cfg& c) {
   L.colsum = take(L.colsum_bytes);
   L.lnscr_bytes = nnt_layernorm_bwd_scratch_bytes(T, E);
   L.lnscr = take(L.lnscr_bytes);
+  // split-K partials of the four dW GEMMs ([3E x E], [E x E], [4E x E], [E x 4E], K = T)
+  L.gemm_ws_bytes = 0;
+  if (c.dtype == NNT_BF16) {
+    const size_t shapes[4][2] = {{3 * E, E}, {E, E}, {F, E}, {E, F}};
+    for (auto& sh : shapes) {
+      size_t b = nnt_tile_gemm_workspace_bytes((int64_t)sh[0], (int64_t)sh[1], (int64_t)T, NNT_F32, NNT_ACT_NONE,
+                                               NNT_CAUSAL_NONE, 1);
+      if (b > L.gemm_ws_bytes) L.gemm_ws_bytes = b;
+    }
+  }
+  L.gemm_ws = take(L.gemm_ws_bytes);
   L.scratch_bytes = o;
   return L;
 }
@@ -174,13 +185,16 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
   const void* dyA = bf ? x.k<void>(x.L.dy16) : (const void*)dy;
   const void* dx1A = bf ? x.k<void>(x.L.dx116) : x.k<void>(x.L.dx1);
   nnt_epilogue e{};
+  nnt_epilogue ws{};  // dW GEMMs: split-K partials in the shared scratch
+  ws.workspace = x.L.gemm_ws_bytes ? x.k<void>(x.L.gemm_ws) : nullptr;
+  ws.workspace_bytes = x.L.gemm_ws_bytes;
   switch (op) {
     case NNT_OP_PROJ_DB:
       return nnt_bias_grad(dy, NNT_F32, T, E, E, g->b_pr, acc, bf ? x.k<void>(x.L.dy16) : nullptr,
                            x.k<void>(x.L.colsum), x.L.colsum_bytes, x.st);
     case NNT_OP_PROJ_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, E, F, T, nullptr, 1.f, dyA, E, nullptr, x.s<void>(x.L.g), F, nullptr,
-                  beta, g->w_pr, NNT_F32, F, nullptr, nullptr);
+                  beta, g->w_pr, NNT_F32, F, nullptr, &ws);
     case NNT_OP_PROJ_DX:
       e.act = NNT_ACT_GELU_BWD;
       e.aux = x.s<void>(x.L.u);
@@ -192,7 +206,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                            x.L.colsum_bytes, x.st);
     case NNT_OP_FC_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, F, E, T, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr,
-                  x.s<void>(x.L.h2), E, nullptr, beta, g->w_fc, NNT_F32, E, nullptr, nullptr);
+                  x.s<void>(x.L.h2), E, nullptr, beta, g->w_fc, NNT_F32, E, nullptr, &ws);
     case NNT_OP_FC_DX:
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
                   nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
@@ -206,7 +220,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                            x.L.colsum_bytes, x.st);
     case NNT_OP_OUT_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, E, E, T, nullptr, 1.f, dx1A, E, nullptr, x.s<void>(x.L.O), E, nullptr,
-                  beta, g->w_o, NNT_F32, E, nullptr, nullptr);
+                  beta, g->w_o, NNT_F32, E, nullptr, &ws);
     case NNT_OP_OUT_DX:
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, E, nullptr, 1.f, dx1A, E, nullptr, p->w_o, E, nullptr, 0.f,
                   x.k<void>(x.L.dO), dt, E, nullptr, nullptr);
@@ -242,7 +256,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                            x.L.colsum_bytes, x.st);
     case NNT_OP_QKV_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * E, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
-                  x.s<void>(x.L.h1), E, nullptr, beta, g->w_qkv, NNT_F32, E, nullptr, nullptr);
+                  x.s<void>(x.L.h1), E, nullptr, beta, g->w_qkv, NNT_F32, E, nullptr, &ws);
     case NNT_OP_QKV_DX:
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, 3 * E, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
                   p->w_qkv, E, nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);

@@ -5,6 +5,22 @@
 
 using namespace nnt;
 
+extern "C" size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int c_dtype, int act, int causal,
+                                                int64_t batch_items) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.c_dtype = c_dtype;
+  g.act = act;
+  g.causal = causal;
+  g.batch0 = batch_items > 0 ? batch_items : 1;
+  g.batch1 = 1;
+  const int64_t s = gemm_tc_splits(g);
+  return s > 1 ? (size_t)s * (size_t)M * (size_t)N * sizeof(float) : 0;
+}
+
 extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const int64_t* batch,
                                     float alpha, const void* A, int a_dtype, int64_t lda, const int64_t* stride_a,
                                     const void* B, int b_dtype, int64_t ldb, const int64_t* stride_b, float beta,
@@ -69,6 +85,8 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.aux = epi->aux;
     g.ld_aux = epi->ld_aux;
     g.causal = epi->causal;
+    g.workspace = epi->workspace;
+    g.workspace_bytes = epi->workspace_bytes;
   }
   const double frac = g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5;
   const double flops = 2.0 * (double)M * N * K * b0 * b1 * frac;

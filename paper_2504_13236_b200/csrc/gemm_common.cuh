@@ -25,10 +25,13 @@ struct GemmArgs {
   void* aux;
   int64_t ld_aux;
   int causal;
+  void* workspace;  // split-K partials (optional)
+  size_t workspace_bytes;
 };
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);
 nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s);
+int64_t gemm_tc_splits(const GemmArgs& a);  // split-K factor the tcgen05 path would use
 
 // Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.
 template <typename TC>

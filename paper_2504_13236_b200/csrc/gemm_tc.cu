@@ -3,22 +3,26 @@
 // warp-specialised persistent CTAs:
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> bias / beta*C /
+//   warps 2..9  epilogue: tcgen05.ld TMEM -> registers -> bias / beta*C /
 //               residual / GELU / GELU' -> swizzled smem staging -> TMA bulk
-//               tensor store (coalesced, asynchronous); double-buffered TMEM
-//               accumulators so the epilogue of tile i overlaps tile i+1's MMAs.
+//               tensor store; two warps per TMEM lane quadrant take alternating
+//               128-byte column chunks; TMEM accumulators are double-buffered so
+//               the epilogue of tile i overlaps the MMAs of tile i+1.
 // Both operand majors are native (instruction-descriptor major bits + the
 // canonical K-major / MN-major SW128 shared-memory layouts), so dX = dY W,
 // dW = dY^T X and the six attention products run without transposes.  Batch
 // items (b, head) are the two outer dimensions of 4-D TMA tensor maps.
 //
-// Split-K (small output grids with long K, i.e. the dW GEMMs): the K range of a
-// tile is cut into `splits` contiguous pieces computed by different CTAs; their
-// fp32 partial tiles are accumulated into C in ascending split order through a
-// per-tile semaphore (split s waits until split s-1 has stored), so the sum
-// has one fixed association and results are bitwise reproducible.  Split-K
-// GEMMs on one device must not run concurrently (they share the semaphores);
-// the block executor issues them on one stream.
+// Tile width BN in {64, 128, 192, 256} is chosen per GEMM from a wave model
+// (tiles per 148 SMs).  Causal GEMMs enumerate only the lower-triangular output
+// tiles (OUT_LOWER) or order tiles heaviest-K-range first (A_LOWER / A_UPPER)
+// so the static persistent schedule stays balanced.
+//
+// Split-K (small output grids with long K: the dW GEMMs), when the caller passes a
+// workspace: split s writes alpha * (its K-range partial) to workspace slice s;
+// a reduce kernel then forms C = beta*C + sum_s partial_s (+bias +residual) with
+// the splits added in ascending order — one fixed association, bitwise
+// reproducible.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -27,29 +31,30 @@
 #include "gemm_common.cuh"
 
 namespace nnt {
-
-__device__ unsigned int g_tile_sem[65536];  // split-K semaphores (zero at load, reset by the last split)
-
 namespace {
 
 constexpr int BM = 128;
-constexpr int BK = 64;  // 64 bf16 = 128 B = one SW128 row
-constexpr int kThreads = 192;
-constexpr int kEpiWarps = 4;
+constexpr int BK = 64;        // 64 bf16 = 128 B = one SW128 row
+constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for one TMA store box
-constexpr int kMaxSemTiles = 65536;
+constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int EPI_BYTES = kEpiWarps * kStageBytesPerWarp;
+  static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * 2 * kStageBytesPerWarp;  // C + aux staging per warp
   static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(SMEM_BYTES <= kMaxSmem, "shared memory budget");
 };
+
+enum TileOrder { ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3 };
 
 struct TcParams {
   GemmArgs g;
@@ -57,7 +62,9 @@ struct TcParams {
   int64_t splits, kb_per_split;
   uint32_t idesc;
   int a_kmajor, b_kmajor;
-  int tma_store;  // epilogue stores through TMA (C and aux maps valid)
+  int tma_store;  // epilogue stores through TMA (C / aux / workspace maps valid)
+  int order;      // TileOrder
+  int ws_mode;    // split partials go to the workspace map; bias/beta/residual applied by the reduce
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -103,7 +110,6 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kEpiWarps) : "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -148,27 +154,44 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
-// Which tiles exist and which K-blocks each task covers (nnt_causal semantics + split-K).
+// Which tile a task computes and which K-blocks it covers (nnt_causal semantics + split-K).
 struct TileInfo {
   int64_t tile, bz, m0, n0, kb_begin, kb_end, split;
-  bool skip;
 };
 __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, int bn) {
   TileInfo ti;
   ti.split = t % P.splits;
   ti.tile = t / P.splits;
-  ti.bz = ti.tile / P.tiles_per_batch;
-  int64_t r = ti.tile % P.tiles_per_batch;
-  int64_t nb = r / P.mt, mb = r % P.mt;
+  int64_t mb, nb;
+  if (P.order == ORDER_TRI) {
+    // compact lower-triangular enumeration (BN == BM, square grid): row mb holds mb+1 tiles
+    ti.bz = ti.tile / P.tiles_per_batch;
+    const int64_t r = ti.tile % P.tiles_per_batch;
+    mb = (int64_t)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+    while ((mb + 1) * (mb + 2) / 2 <= r) ++mb;
+    while (mb * (mb + 1) / 2 > r) --mb;
+    nb = r - mb * (mb + 1) / 2;
+  } else if (P.order == ORDER_N_OUTER) {
+    ti.bz = ti.tile / P.tiles_per_batch;
+    const int64_t r = ti.tile % P.tiles_per_batch;
+    nb = r / P.mt;
+    mb = r % P.mt;
+  } else {
+    // heaviest K-range first: the m-block level is outermost, (batch, n) inner
+    const int64_t per_level = P.num_tiles / P.mt;
+    const int64_t level = ti.tile / per_level, r = ti.tile % per_level;
+    mb = P.order == ORDER_HEAVY_HIGH_M ? P.mt - 1 - level : level;
+    ti.bz = r / P.nt;
+    nb = r % P.nt;
+  }
   ti.m0 = mb * BM;
   ti.n0 = nb * bn;
   int64_t k_begin = 0, k_end = P.g.K;
   if (P.g.causal == NNT_CAUSAL_A_LOWER) k_end = min(P.g.K, ti.m0 + BM);
   if (P.g.causal == NNT_CAUSAL_A_UPPER) k_begin = min(P.g.K, ti.m0);
-  int64_t kb0 = k_begin / BK, kb1 = (k_end + BK - 1) / BK;
+  const int64_t kb0 = k_begin / BK, kb1 = (k_end + BK - 1) / BK;
   ti.kb_begin = min(kb1, kb0 + ti.split * P.kb_per_split);
   ti.kb_end = min(kb1, ti.kb_begin + P.kb_per_split);
-  ti.skip = (P.g.causal == NNT_CAUSAL_OUT_LOWER) && (ti.n0 > ti.m0 + BM - 1);
   return ti;
 }
 
@@ -196,34 +219,87 @@ __device__ __forceinline__ float gelu_grad_e(float u) {
 
 template <typename T>
 __device__ __forceinline__ float ld_elem(const T* p) { return to_f32(*p); }
-// C is re-read after other CTAs (split-K) or TMA stores wrote it: bypass L1.
+// C may have been written by TMA stores of this kernel's earlier launches: bypass L1.
 __device__ __forceinline__ float ld_c(const float* p) { return __ldcg(p); }
 __device__ __forceinline__ float ld_c(const __nv_bfloat16* p) {
   unsigned short u = __ldcg(reinterpret_cast<const unsigned short*>(p));
   return __bfloat162float(__ushort_as_bfloat16(u));
 }
 
-// Computes the W outputs of one row chunk in registers.  pre-activation kept in `pre`.
+// 8 consecutive values as floats (one 16-byte load for bf16, two for fp32)
+__device__ __forceinline__ void ld8(const float* p, float* o, bool cg) {
+  float4 a = cg ? __ldcg(reinterpret_cast<const float4*>(p)) : *reinterpret_cast<const float4*>(p);
+  float4 b = cg ? __ldcg(reinterpret_cast<const float4*>(p) + 1) : *(reinterpret_cast<const float4*>(p) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+}
+__device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o, bool cg) {
+  uint4 u = cg ? __ldcg(reinterpret_cast<const uint4*>(p)) : *reinterpret_cast<const uint4*>(p);
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    float2 f = __bfloat1622float2(h[t]);
+    o[2 * t] = f.x;
+    o[2 * t + 1] = f.y;
+  }
+}
+
+// The W pre-activation outputs of one row chunk (GELU is applied by the caller after
+// staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
 template <typename TC, int W>
 __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const TC* auxb, int64_t row, int64_t col0,
-                                         float beta, bool first, float (&v)[W], float (&pre)[W]) {
+                                         bool extras, bool vec, float (&v)[W]) {
   constexpr bool kFast = sizeof(TC) == 2;
-  const bool full = (row < g.M) && (col0 + W <= g.N);
 #pragma unroll
   for (int j = 0; j < W; ++j) v[j] *= g.alpha;
-  if (row < g.M) {
-    if (first && g.bias) {
+  if (!extras) return;  // split-K partial: bias/beta/residual belong to the reduce
+  if (vec && row < g.M && col0 + W <= g.N) {
+    float t[8];
+    if (g.bias) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        ld8(g.bias + col0 + j, t, false);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += t[i];
+      }
+    }
+    if (g.beta != 0.f) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        ld8(Cb + row * g.ldc + col0 + j, t, true);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += g.beta * t[i];
+      }
+    }
+    if (g.residual) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        ld8(g.residual + row * g.ld_res + col0 + j, t, false);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] += t[i];
+      }
+    }
+    if (g.act == NNT_ACT_GELU_BWD) {
+#pragma unroll
+      for (int j = 0; j < W; j += 8) {
+        ld8(auxb + row * g.ld_aux + col0 + j, t, false);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_e<kFast>(t[i]);
+      }
+    }
+  } else if (row < g.M) {
+    const bool full = col0 + W <= g.N;
+    if (g.bias) {
 #pragma unroll
       for (int j = 0; j < W; ++j)
         if (full || col0 + j < g.N) v[j] += __ldg(g.bias + col0 + j);
     }
-    if (beta != 0.f) {
+    if (g.beta != 0.f) {
       const TC* cr = Cb + row * g.ldc + col0;
 #pragma unroll
       for (int j = 0; j < W; ++j)
-        if (full || col0 + j < g.N) v[j] += beta * ld_c(cr + j);
+        if (full || col0 + j < g.N) v[j] += g.beta * ld_c(cr + j);
     }
-    if (first && g.residual) {
+    if (g.residual) {
       const float* rr = g.residual + row * g.ld_res + col0;
 #pragma unroll
       for (int j = 0; j < W; ++j)
@@ -236,23 +312,16 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
         if (full || col0 + j < g.N) v[j] *= gelu_grad_e<kFast>(ld_elem(ar + j));
     }
   }
-  if (g.act == NNT_ACT_GELU) {
-#pragma unroll
-    for (int j = 0; j < W; ++j) {
-      pre[j] = v[j];
-      v[j] = gelu_e<kFast>(v[j]);
-    }
-  }
 }
 
 // Writes a 128-byte row chunk to SW128-swizzled staging (row = lane, 8 x 16 B pieces).
-template <typename TC, int W>
+template <typename TS, int W>
 __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float (&v)[W]) {
   uint8_t* rowp = buf + lane * 128;
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     uint4 u;
-    if (sizeof(TC) == 4) {
+    if (sizeof(TS) == 4) {
       u.x = __float_as_uint(v[4 * j]);
       u.y = __float_as_uint(v[4 * j + 1]);
       u.z = __float_as_uint(v[4 * j + 2]);
@@ -272,16 +341,12 @@ __device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float (&
 }
 
 template <typename TC, int W>
-__device__ __forceinline__ void direct_store(const GemmArgs& g, TC* Cb, TC* auxb, int64_t row, int64_t col0,
-                                             const float (&v)[W], const float (&pre)[W]) {
-  if (row >= g.M) return;
+__device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, TC* base, int64_t row, int64_t col0,
+                                             const float (&v)[W]) {
+  if (row >= M) return;
 #pragma unroll
-  for (int j = 0; j < W; ++j) {
-    if (col0 + j < g.N) {
-      Cb[row * g.ldc + col0 + j] = from_f32<TC>(v[j]);
-      if (g.act == NNT_ACT_GELU) auxb[row * g.ld_aux + col0 + j] = from_f32<TC>(pre[j]);
-    }
-  }
+  for (int j = 0; j < W; ++j)
+    if (col0 + j < N) base[row * ld + col0 + j] = from_f32<TC>(v[j]);
 }
 
 // ------------------------------------------------------------------ kernel
@@ -335,7 +400,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
         TileInfo ti = decode_task(P, t, BN);
-        if (ti.skip) continue;
         const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -377,7 +441,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
       for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
         TileInfo ti = decode_task(P, t, BN);
-        if (ti.skip) continue;
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -406,40 +469,32 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    // ===================== epilogue (warps 2..5 -> TMEM lane quadrants 2,3,0,1)
+    // ===================== epilogue: warps 2..9; TMEM lane quadrant = warp % 4 (tcgen05.ld rule),
+    // the two warps of a quadrant take alternating 128-byte column chunks
     const int quad = warp & 3;
-    uint8_t* stage_c = smem + C::EPI_OFF + quad * 2 * kStageBytesPerWarp;
-    uint8_t* stage_a = stage_c + kStageBytesPerWarp;
-    const uint32_t stage_c_u32 = smem_u32(stage_c), stage_a_u32 = smem_u32(stage_a);
+    const int half = (warp - 2) >> 2;
+    uint8_t* stage_buf = smem + C::EPI_OFF + (warp - 2) * kStageBytesPerWarp;
+    const size_t cs = sizeof(TC);
+    auto a16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
+    const bool vec = a16(g.C) && (g.ldc * cs) % 16 == 0 && (!g.bias || a16(g.bias)) &&
+                     (!g.residual || (a16(g.residual) && g.ld_res % 4 == 0)) &&
+                     (!g.aux || (a16(g.aux) && (g.ld_aux * cs) % 16 == 0)) && (g.sc0 * cs) % 16 == 0 &&
+                     (g.sc1 * cs) % 16 == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
       TileInfo ti = decode_task(P, t, BN);
-      if (ti.skip) continue;
       const int64_t p = ti.bz / g.batch1, q = ti.bz % g.batch1;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
-      const bool first = ti.split == 0;
-      const float beta = first ? g.beta : 1.0f;  // later splits accumulate onto the stored partial sum
-      if (P.splits > 1 && !first) {
-        // ordered split-K: wait until split (s-1) of this tile has stored its partial sum
-        if (warp == 2 && lane == 0) {
-          const unsigned int want = (unsigned int)ti.split;
-          unsigned int cur;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&g_tile_sem[ti.tile]) : "memory");
-          } while (cur != want);
-        }
-        epi_bar();
-      }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
       const int64_t row = ti.m0 + quad * 32 + lane;
       const bool has_k = ti.kb_end > ti.kb_begin;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += W) {
+      for (int c = half * W; c < BN; c += 2 * W) {
         if (ti.n0 + c >= g.N) break;  // warp-uniform
-        float v[W], pre[W];
+        float v[W];
 #pragma unroll
         for (int h = 0; h < W / 32; ++h) {
           if (has_k) {
@@ -449,23 +504,45 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) v[32 * h + j] = 0.f;
           }
         }
-        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, beta, first, v, pre);
-        if (P.tma_store) {
-          if (lane == 0) bulk_wait_read0();  // staging buffers free again
+        const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
+        if (P.ws_mode) {
+          // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce kernel
+          epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, v);
+          if (lane == 0) bulk_wait_read0();
           __syncwarp();
-          stage_row<TC, W>(stage_c, lane, v);
-          if (g.act == NNT_ACT_GELU) stage_row<TC, W>(stage_a, lane, pre);
+          stage_row<float, W>(stage_buf, lane, v);
           fence_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
-            tma_store_4d(&tmC, stage_c_u32, cx, cy, (int)q, (int)p);
-            if (g.act == NNT_ACT_GELU) tma_store_4d(&tmAux, stage_a_u32, cx, cy, (int)q, (int)p);
+            tma_store_4d(&tmAux, smem_u32(stage_buf), cx, cy, (int)ti.split, 0);
             bulk_commit();
           }
-        } else {
-          direct_store<TC, W>(g, Cb, auxb, row, ti.n0 + c, v, pre);
+          continue;
         }
+        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, v);
+        auto stage_store = [&](const CUtensorMap* map) {
+          if (lane == 0) bulk_wait_read0();  // the previous bulk store finished reading the buffer
+          __syncwarp();
+          stage_row<TC, W>(stage_buf, lane, v);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(map, smem_u32(stage_buf), cx, cy, (int)q, (int)p);
+            bulk_commit();
+          }
+        };
+        if (g.act == NNT_ACT_GELU) {  // pre-activation -> aux, then gelu in place -> C
+          if (P.tma_store)
+            stage_store(&tmAux);
+          else
+            direct_store<TC, W>(g.M, g.N, g.ld_aux, auxb, row, ti.n0 + c, v);
+#pragma unroll
+          for (int j = 0; j < W; ++j) v[j] = gelu_e<sizeof(TC) == 2>(v[j]);
+        }
+        if (P.tma_store)
+          stage_store(&tmC);
+        else
+          direct_store<TC, W>(g.M, g.N, g.ldc, Cb, row, ti.n0 + c, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -474,19 +551,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1;
       }
-      if (P.splits > 1) {
-        // publish: this split's sum is in C (stores complete and visible), then signal split s+1
-        if (lane == 0 && P.tma_store) bulk_wait0();
-        __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        epi_bar();
-        if (warp == 2 && lane == 0) {
-          const unsigned int next = (ti.split + 1 == P.splits) ? 0u : (unsigned int)(ti.split + 1);
-          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&g_tile_sem[ti.tile]), "r"(next) : "memory");
-        }
-      }
     }
-    if (lane == 0 && P.tma_store) bulk_wait0();
+    if (lane == 0) bulk_wait0();
   }
 
   tc_fence_before();
@@ -496,6 +562,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                  "r"((uint32_t)C::TMEM_COLS)
                  : "memory");
+  }
+}
+
+// C = beta*C + sum_s ws[s] (+bias) (+residual), splits added in ascending order (fp32 C).
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int64_t splits, int64_t M,
+                                                            int64_t N, float* C, int64_t ldc, float beta,
+                                                            const float* __restrict__ bias,
+                                                            const float* __restrict__ residual, int64_t ld_res) {
+  const int64_t nq = N / 4;  // N % 4 == 0 (checked on the host)
+  const int64_t total = M * nq;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / nq, c = (i % nq) * 4;
+    float4 s = __ldcg(reinterpret_cast<const float4*>(ws + r * N + c));
+    for (int64_t k = 1; k < splits; ++k) {
+      float4 t = __ldcg(reinterpret_cast<const float4*>(ws + (k * M + r) * N + c));
+      s.x += t.x; s.y += t.y; s.z += t.z; s.w += t.w;
+    }
+    if (bias) {
+      float4 b = *reinterpret_cast<const float4*>(bias + c);
+      s.x += b.x; s.y += b.y; s.z += b.z; s.w += b.w;
+    }
+    float4* cp = reinterpret_cast<float4*>(C + r * ldc + c);
+    if (beta != 0.f) {
+      float4 o = *cp;
+      s.x += beta * o.x; s.y += beta * o.y; s.z += beta * o.z; s.w += beta * o.w;
+    }
+    if (residual) {
+      float4 o = *reinterpret_cast<const float4*>(residual + r * ld_res + c);
+      s.x += o.x; s.y += o.y; s.z += o.z; s.w += o.w;
+    }
+    *cp = s;
   }
 }
 
@@ -534,21 +631,30 @@ nnt_status make_map(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const v
   return NNT_OK;
 }
 
-// Split-K factor: only for fp32 C without activation (the dW GEMMs) whose output grid
-// leaves most SMs idle and whose K is long enough to cut.
-int64_t choose_splits(const GemmArgs& a, int64_t tiles, int64_t nkb) {
-  if (a.c_dtype != NNT_F32 || a.act != NNT_ACT_NONE || a.causal != NNT_CAUSAL_NONE || a.batch0 * a.batch1 != 1)
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace
+
+// Split-K factor for a GEMM: fp32 C, no activation, unbatched, non-causal, an output grid
+// that leaves SMs idle and a K long enough to cut (>= 8 K-blocks per split).
+int64_t gemm_tc_splits(const GemmArgs& a) {
+  if (a.c_dtype != NNT_F32 || a.act != NNT_ACT_NONE || a.causal != NNT_CAUSAL_NONE || a.batch0 * a.batch1 != 1 ||
+      a.N % 4 != 0)
     return 1;
+  const int64_t tiles = cdiv(a.M, BM) * cdiv(a.N, 256);
+  const int64_t nkb = cdiv(a.K, BK);
   const int64_t sms = num_sms();
-  if (tiles * 2 > sms || tiles > kMaxSemTiles) return 1;
+  if (tiles * 2 > sms) return 1;
   int64_t s = sms / tiles;
-  if (s > nkb / 8) s = nkb / 8;  // keep >= 8 K-blocks per split
-  if (s > 16) s = 16;
+  if (s > nkb / 8) s = nkb / 8;
+  if (s > 8) s = 8;
   return s < 1 ? 1 : s;
 }
 
+namespace {
+
 template <int BN, typename TC>
-nnt_status launch_bn(const GemmArgs& a, cudaStream_t s) {
+nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   using C = Cfg<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
@@ -562,15 +668,22 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s) {
   P.g = a;
   P.a_kmajor = a.ta == NNT_NOTRANS;
   P.b_kmajor = a.tb == NNT_TRANS;
-  P.mt = (a.M + BM - 1) / BM;
-  P.nt = (a.N + BN - 1) / BN;
-  P.tiles_per_batch = P.mt * P.nt;
+  P.mt = cdiv(a.M, BM);
+  P.nt = cdiv(a.N, BN);
+  if (a.causal == NNT_CAUSAL_OUT_LOWER && BN == BM && P.mt == P.nt) {
+    P.order = ORDER_TRI;
+    P.tiles_per_batch = P.mt * (P.mt + 1) / 2;
+  } else {
+    P.order = a.causal == NNT_CAUSAL_A_LOWER ? ORDER_HEAVY_HIGH_M
+                                             : (a.causal == NNT_CAUSAL_A_UPPER ? ORDER_HEAVY_LOW_M : ORDER_N_OUTER);
+    P.tiles_per_batch = P.mt * P.nt;
+  }
   P.num_tiles = P.tiles_per_batch * a.batch0 * a.batch1;
-  const int64_t nkb = (a.K + BK - 1) / BK;
-  P.splits = choose_splits(a, P.num_tiles, nkb);
-  P.kb_per_split = (nkb + P.splits - 1) / P.splits;
-  P.splits = (nkb + P.kb_per_split - 1) / P.kb_per_split;  // no empty splits
+  const int64_t nkb = cdiv(a.K, BK);
+  P.splits = splits;
+  P.kb_per_split = cdiv(nkb, P.splits);
   P.num_tasks = P.num_tiles * P.splits;
+  P.ws_mode = splits > 1 ? 1 : 0;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((P.b_kmajor ? 0u : 1u) << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   CUtensorMap tmA, tmB, tmC, tmAux;
@@ -583,33 +696,72 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s) {
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN));
   else
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
-  // epilogue through TMA stores when C (and aux) satisfy the tensor-map rules
   const size_t es = sizeof(TC);
   const CUtensorMapDataType cdt = sizeof(TC) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : bf;
   const int W = (int)(128 / es);
   auto ok16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  bool tma_ok = ok16(a.C) && (a.ldc * es) % 16 == 0 && (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
-                (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
-                (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
-  P.tma_store = tma_ok ? 1 : 0;
   memset(&tmC, 0, sizeof(tmC));
   memset(&tmAux, 0, sizeof(tmAux));
-  if (tma_ok) {
-    NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
-    if (a.act == NNT_ACT_GELU)
-      NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+  if (P.ws_mode) {
+    // workspace [splits][M][N] fp32; the aux map slot carries it
+    P.tma_store = 1;
+    NNT_TRY(make_map(&tmAux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.workspace, a.N, a.M, a.N, splits, a.M * a.N, 1, 0,
+                     32, 32));
+  } else {
+    const bool tma_ok = ok16(a.C) && (a.ldc * es) % 16 == 0 &&
+                        (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
+                        (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
+                        (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
+    P.tma_store = tma_ok ? 1 : 0;
+    if (tma_ok) {
+      NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+      if (a.act == NNT_ACT_GELU)
+        NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+    }
   }
   int64_t grid = P.num_tasks < num_sms() ? P.num_tasks : num_sms();
   if (grid < 1) grid = 1;
   gemm_tc_kernel<BN, TC><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
-  return check_launch("gemm_tc");
+  NNT_TRY(check_launch("gemm_tc"));
+  if (P.ws_mode) {
+    const int64_t total = a.M * (a.N / 4);
+    int64_t blocks = cdiv(total, 256);
+    if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
+    splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>((const float*)a.workspace, splits, a.M, a.N, (float*)a.C,
+                                                          a.ldc, a.beta, a.bias, a.residual, a.ld_res);
+    NNT_TRY(check_launch("gemm_tc splitk reduce"));
+  }
+  return NNT_OK;
+}
+
+// Tile width from a wave model: time ~ ceil(tiles / SMs) * BN (per-tile time ~ BN at fixed
+// BM, K); ties go to the wider tile (more operand reuse per byte of L2 traffic).
+int choose_bn(const GemmArgs& a) {
+  if (a.N <= 64) return 64;
+  if (a.causal == NNT_CAUSAL_OUT_LOWER) return 128;
+  const int64_t sms = num_sms(), mt = cdiv(a.M, BM), nb = a.batch0 * a.batch1;
+  const int cands[3] = {256, 192, 128};
+  int best = 256;
+  double best_cost = 1e300;
+  for (int bn : cands) {
+    const int64_t tiles = mt * cdiv(a.N, bn) * nb;
+    const double cost = (double)cdiv(tiles, sms) * bn * (1.0 + 0.02 * (256 - bn) / 64.0);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
 }
 
 template <typename TC>
-nnt_status launch_tc(const GemmArgs& a, cudaStream_t s) {
-  if (a.N <= 64) return launch_bn<64, TC>(a, s);
-  if (a.N <= 128 || a.causal == NNT_CAUSAL_OUT_LOWER) return launch_bn<128, TC>(a, s);
-  return launch_bn<256, TC>(a, s);
+nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
+  switch (splits > 1 ? 256 : choose_bn(a)) {
+    case 64: return launch_bn<64, TC>(a, s, splits);
+    case 128: return launch_bn<128, TC>(a, s, splits);
+    case 192: return launch_bn<192, TC>(a, s, splits);
+    default: return launch_bn<256, TC>(a, s, splits);
+  }
 }
 
 }  // namespace
@@ -623,8 +775,15 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s) {
               NNT_ERR_ALIGN, "gemm(bf16): batch strides must be positive multiples of 8");
   NNT_REQUIRE(a.M < (1ll << 31) && a.N < (1ll << 31) && a.K < (1ll << 31), NNT_ERR_UNSUPPORTED,
               "gemm(bf16): dims must fit int32 TMA coordinates");
-  if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s);
-  return launch_tc<__nv_bfloat16>(a, s);
+  int64_t splits = gemm_tc_splits(a);
+  const bool ws_ok = a.workspace && (reinterpret_cast<uintptr_t>(a.workspace) & 15u) == 0 &&
+                     a.workspace_bytes >= (size_t)splits * a.M * a.N * sizeof(float) &&
+                     (reinterpret_cast<uintptr_t>(a.C) & 15u) == 0 && a.ldc % 4 == 0 &&
+                     (!a.residual || ((reinterpret_cast<uintptr_t>(a.residual) & 15u) == 0 && a.ld_res % 4 == 0)) &&
+                     (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);
+  if (!ws_ok) splits = 1;
+  if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits);
+  return launch_tc<__nv_bfloat16>(a, s, splits);
 }
 
 }  // namespace nnt

@@ -39,7 +39,7 @@ OP_NAMES = ("ln1", "qkv", "scores", "maxsumexp", "softmax", "pv", "out", "ln2", 
 
 # The exported symbols include/nnt.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_grid", "nnt_tile_extent",
-           "nnt_partition", "nnt_tile_gemm", "nnt_maxsumexp", "nnt_softmax", "nnt_softmax_bwd",
+           "nnt_partition", "nnt_tile_gemm", "nnt_tile_gemm_workspace_bytes", "nnt_maxsumexp", "nnt_softmax", "nnt_softmax_bwd",
            "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
@@ -55,7 +55,8 @@ class NNTError(RuntimeError):
 # ---------------------------------------------------------------- structs
 class nnt_epilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
-                ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int)]
+                ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int), ("workspace", C.c_void_p),
+                ("workspace_bytes", C.c_size_t)]
 
 
 class nnt_adam_hparams(C.Structure):
@@ -100,6 +101,7 @@ _sig = {
     "nnt_partition": (_i32, [_i64, _i32, _i32, _P64, _P64]),
     "nnt_tile_gemm": (_i32, [_i32, _i32, _i64, _i64, _i64, _P64, _f32, _vp, _i32, _i64, _P64, _vp, _i32, _i64, _P64,
                              _f32, _vp, _i32, _i64, _P64, _P64, C.POINTER(nnt_epilogue), _vp]),
+    "nnt_tile_gemm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i32, _i32, _i32, _i64]),
     "nnt_maxsumexp": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _i32, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
     "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
@@ -201,8 +203,16 @@ def nnt_partition(n_units, n_ranks, rank):
 
 
 def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
-                  causal=NNT_CAUSAL_NONE):
-    return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal)
+                  causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0):
+    """The caller keeps every tensor passed here alive until the launch has run."""
+    if workspace is not None and not workspace_bytes and hasattr(workspace, "numel"):
+        workspace_bytes = workspace.numel() * workspace.element_size()
+    return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal, ptr(workspace),
+                        workspace_bytes)
+
+
+def nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act=NNT_ACT_NONE, causal=NNT_CAUSAL_NONE, batch_items=1):
+    return lib.nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act, causal, batch_items)
 
 
 def nnt_tile_gemm(trans_a, trans_b, M, N, K, batch, alpha, A, a_dtype, lda, stride_a, B, b_dtype, ldb, stride_b,

@@ -148,6 +148,40 @@ def test_gemm_attention_views_and_causal(dtype, causal):
         assert np.array_equal(host(O), want)
 
 
+@pytest.mark.parametrize("M,N", [(768, 768), (2304, 768), (768, 3072)])
+def test_gemm_split_k_workspace_bit_exact(M, N):
+    """dW-shaped GEMMs (K = T = 8192) split K into a workspace and reduce in split order:
+    integer data keeps every partial exact, so the result is bit-exact and run-to-run identical."""
+    K = 8192
+    a = nnt_inputs.make_matrix((K, M), seed=M + N, kind="int")     # dY  [T][N_out] -> op(A) = dY^T
+    b = nnt_inputs.make_matrix((K, N), seed=M * 3 + N, kind="int")  # X   [T][N_in]
+    c0 = nnt_inputs.make_matrix((M, N), seed=5, kind="int")
+    nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
+    assert nb > 0  # the library splits these shapes
+    ws = torch.empty(nb, device="cuda", dtype=torch.uint8)
+    epi = nnt.make_epilogue(workspace=ws)
+    A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
+    want = tiled.gemm_tiled(a.T, b, 256, 256, 1024) + c0
+    outs = []
+    for _ in range(2):
+        Cm = dev(c0)
+        nnt.nnt_tile_gemm(1, 0, M, N, K, None, 1.0, A, 1, M, None, B, 1, N, None, 1.0, Cm, 0, N, None, None, epi)
+        torch.cuda.synchronize()
+        outs.append(host(Cm))
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("N", [768, 3072])
+def test_gemm_wave_model_tile_widths_bit_exact(N):
+    """M = 8192 rows with N = 768 / 3072 select BN = 192 tiles (wave model)."""
+    M, K = 8192, 256
+    a = nnt_inputs.make_matrix((M, K), seed=N, kind="int")
+    b = nnt_inputs.make_matrix((N, K), seed=N + 1, kind="int")
+    got = host(_run("bf16", 0, 1, M, N, K, a, b))
+    assert np.array_equal(got, a.astype(np.float64) @ b.T.astype(np.float64))
+
+
 def test_gemm_rejects_bad_arguments():
     A = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(nnt.NNTError) as e:  # misaligned leading dimension for TMA
