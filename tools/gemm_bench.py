@@ -40,6 +40,7 @@ def main():
     res = torch.zeros(T, E, **f32)
     bh = (B, H)
     es = 2
+    big = torch.randn(8192, 8192, **bf) * 0.05
     cases = [
         # name, ta, tb, M, N, K, batch, A, lda, sa, B, ldb, sb, C, cdt, ldc, sc, epi, causal-frac
         ("qkv", 0, 1, T, 3 * E, E, None, h, E, None, w, E, None, outb, 1, 3 * E, None,
@@ -71,13 +72,21 @@ def main():
          (S * 3 * E, Dh), nnt.make_epilogue(causal=3), 0.5),
         ("qkv_dw", 1, 0, 3 * E, E, T, None, h, 3 * E, None, h, E, None, outf, 0, E, None, None, 1.0),
         ("qkv_dx", 0, 0, T, E, 3 * E, None, h, 3 * E, None, w, E, None, outf, 0, E, None, None, 1.0),
+        ("square8192", 0, 1, 8192, 8192, 8192, None, big, 8192, None, big, 8192, None, outb, 1, 8192, None,
+         None, 1.0),
     ]
+    ws = torch.empty(64 << 20, device="cuda", dtype=torch.uint8)  # split-K workspace for the dW GEMMs
     total = 0.0
     print(f"{'gemm':14s} {'M':>6s} {'N':>6s} {'K':>6s} {'batch':>8s} {'us':>8s} {'TFLOP/s':>8s}")
     for (name, ta, tb, M, N, K, batch, A, lda, sa, Bm, ldb, sb, Cm, cdt, ldc, sc, epi, frac) in cases:
         if a.only and name not in a.only.split(","):
             continue
         beta = 1.0 if name.endswith("_dw") else 0.0
+        if name.endswith("_dw"):
+            epi = nnt.make_epilogue(workspace=ws)
+        if name == "square8192" and T * F < 8192 * 8192:
+            outb = torch.empty(8192 * 8192, **bf)
+            Cm = outb
 
         def run():
             nnt.nnt_tile_gemm(ta, tb, M, N, K, batch, 1.0, A, 1, lda, sa, Bm, 1, ldb, sb, beta, Cm, cdt, ldc, sc,
