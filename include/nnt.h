@@ -120,6 +120,14 @@ typedef struct {
   void* workspace;        /* device scratch for split-K partials, or NULL (no split);
                              see nnt_tile_gemm_workspace_bytes                     */
   size_t workspace_bytes;
+  /* SoftMax subroutine 1 fused into the epilogue, bf16 path with fp32 C:
+   * for every output row and every 32-column key tile g the partial
+   * (m_g, s_g) = (max, sum e^{x - m_g}) of x = alpha*acc over the tile's valid columns
+   * (col <= row when causal == NNT_CAUSAL_OUT_LOWER; (-inf, 0) if none) is written to
+   * row_stats[((p*batch1 + q)*M + row)*ld_row_stats + g] as two floats.  Merged by
+   * nnt_maxsumexp_merge.  NULL = off. */
+  float* row_stats;
+  int64_t ld_row_stats;   /* in (max, sumexp) pairs, >= ceil(N / 32) */
 } nnt_epilogue;
 
 /* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would
@@ -168,6 +176,17 @@ nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t
 nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx,
                          int64_t tile_k, int causal, int64_t seq_q,
                          float* stats, int accumulate, nnt_stream_t stream);
+
+/*
+ * Aggregation of subroutine 1 ("aggregates them"): merges per-key-tile partials
+ * part[r][g] = (m_g, s_g) (device fp32 pairs, row pitch ld_parts pairs, tile width
+ * part_cols) in ascending g into stats[r] = (M, S); with causal != 0 only the tiles holding
+ * a valid column (g*part_cols <= q, q = r % seq_q) are read.  Same merge rule as
+ * nnt_maxsumexp.
+ */
+nnt_status nnt_maxsumexp_merge(const float* part, int64_t rows, int64_t nparts, int64_t ld_parts,
+                               int64_t part_cols, int causal, int64_t seq_q, float* stats,
+                               nnt_stream_t stream);
 
 /*
  * Subroutine 2: y[r][k] = e^{x[r][k] - M_r} / S_r with (M_r, S_r) = stats[r].

@@ -87,6 +87,13 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.causal = epi->causal;
     g.workspace = epi->workspace;
     g.workspace_bytes = epi->workspace_bytes;
+    g.row_stats = epi->row_stats;
+    g.ld_stats = epi->ld_row_stats;
+    NNT_REQUIRE(!epi->row_stats || (a_dtype == NNT_BF16 && c_dtype == NNT_F32 && epi->act == NNT_ACT_NONE &&
+                                    epi->ld_row_stats >= (N + 31) / 32 &&
+                                    (epi->causal == NNT_CAUSAL_NONE || epi->causal == NNT_CAUSAL_OUT_LOWER)),
+                NNT_ERR_UNSUPPORTED,
+                "nnt_tile_gemm: row_stats needs bf16 operands, fp32 C, no activation, ld >= ceil(N/32)");
   }
   const double frac = g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5;
   const double flops = 2.0 * (double)M * N * K * b0 * b1 * frac;

@@ -27,6 +27,8 @@ struct GemmArgs {
   int causal;
   void* workspace;  // split-K partials (optional)
   size_t workspace_bytes;
+  float* row_stats;  // fused softmax subroutine 1: per (row, 32-column tile) (max, sumexp)
+  int64_t ld_stats;  // pairs per row
 };
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);

@@ -520,6 +520,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           continue;
         }
         epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, v);
+        if (g.row_stats != nullptr && row < g.M) {
+          // fused softmax subroutine 1: (max, sumexp) of this row over the chunk's
+          // valid columns (W = 32 for fp32 C: one 32-column key tile)
+          const int64_t col0 = ti.n0 + c;
+          int64_t lim = g.N - col0;
+          if (g.causal == NNT_CAUSAL_OUT_LOWER && row - col0 + 1 < lim) lim = row - col0 + 1;
+          float m = -INFINITY, s = 0.f;
+#pragma unroll
+          for (int j = 0; j < W; ++j)
+            if (j < lim) m = fmaxf(m, v[j]);
+          if (m != -INFINITY) {
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+              if (j < lim) s += exp2f((v[j] - m) * 1.4426950408889634f);
+          }
+          *reinterpret_cast<float2*>(g.row_stats + 2 * ((ti.bz * g.M + row) * g.ld_stats + col0 / 32)) =
+              make_float2(m, s);
+        }
         auto stage_store = [&](const CUtensorMap* map) {
           if (lane == 0) bulk_wait_read0();  // the previous bulk store finished reading the buffer
           __syncwarp();

@@ -1,13 +1,13 @@
 // Deterministic column merge of row-chunk partials: out[c] (+)= sum_k part[k][c],
-// k ascending within each of 8 contiguous k-ranges, then the 8 range sums in
-// ascending order.  A fixed association (no atomics), so results are bitwise
-// reproducible; 32 columns per CTA (coalesced 128 B rows), 8 warps split k.
+// k ascending within each of kMergeWarps contiguous k-ranges, then the range sums
+// in ascending order.  A fixed association (no atomics), so results are bitwise
+// reproducible; 32 columns per CTA (coalesced 128 B rows), the warps split k.
 #pragma once
 #include "nnt_internal.h"
 
 namespace nnt {
 
-constexpr int kMergeWarps = 8;
+constexpr int kMergeWarps = 32;
 
 static __global__ void __launch_bounds__(32 * kMergeWarps)
     column_merge_kernel(const float* __restrict__ part, int64_t chunks, int64_t N, float* __restrict__ out,

@@ -144,6 +144,25 @@ __global__ void __launch_bounds__(kThreads) maxsumexp_kernel(const float* __rest
   }
 }
 
+// ------------------------------------------------------------------ aggregation of subroutine 1
+// One thread per slice: merges its key-tile partials in ascending tile order (R10).
+__global__ void __launch_bounds__(kThreads) maxsumexp_merge_kernel(const float2* __restrict__ part, int64_t rows,
+                                                                   int64_t nparts, int64_t ld, int64_t part_cols,
+                                                                   int causal, int64_t seq_q,
+                                                                   float2* __restrict__ stats) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  int64_t n = nparts;
+  if (causal) n = min(n, (row % seq_q) / part_cols + 1);
+  const float2* pr = part + row * ld;
+  float M = -CUDART_INF_F, S = 0.f;
+  for (int64_t gi = 0; gi < n; ++gi) {
+    const float2 p = pr[gi];
+    mse_merge(M, S, p.x, p.y);
+  }
+  stats[row] = make_float2(M, S);
+}
+
 // ------------------------------------------------------------------ subroutine 2
 template <typename TO>
 __global__ void __launch_bounds__(kThreads) softmax_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
@@ -260,6 +279,22 @@ nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx
   switch (nc) { NNT_MSE(1) NNT_MSE(2) NNT_MSE(4) NNT_MSE(8) NNT_MSE(16) }
 #undef NNT_MSE
   return check_launch("maxsumexp");
+}
+
+nnt_status nnt_maxsumexp_merge(const float* part, int64_t rows, int64_t nparts, int64_t ld_parts, int64_t part_cols,
+                               int causal, int64_t seq_q, float* stats, nnt_stream_t stream) {
+  NNT_REQUIRE(part && stats, NNT_ERR_NULL, "nnt_maxsumexp_merge: NULL pointer");
+  NNT_REQUIRE(rows > 0 && nparts > 0 && ld_parts >= nparts, NNT_ERR_SHAPE,
+              "nnt_maxsumexp_merge: rows=%lld nparts=%lld ld=%lld", (long long)rows, (long long)nparts,
+              (long long)ld_parts);
+  NNT_REQUIRE(part_cols > 0, NNT_ERR_TILE, "nnt_maxsumexp_merge: part_cols=%lld", (long long)part_cols);
+  NNT_REQUIRE(!causal || seq_q > 0, NNT_ERR_SHAPE, "nnt_maxsumexp_merge: causal needs seq_q > 0");
+  NNT_REQUIRE((reinterpret_cast<uintptr_t>(part) & 7u) == 0 && (reinterpret_cast<uintptr_t>(stats) & 7u) == 0,
+              NNT_ERR_ALIGN, "nnt_maxsumexp_merge: pointers must be 8-byte aligned");
+  LaunchScope sc(NNT_K_MAXSUMEXP, stream, 8.0 * rows * (causal ? 0.5 : 1.0) * nparts + 8.0 * rows, 0);
+  maxsumexp_merge_kernel<<<(unsigned)((rows + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+      (const float2*)part, rows, nparts, ld_parts, part_cols, causal, seq_q, (float2*)stats);
+  return check_launch("maxsumexp_merge");
 }
 
 nnt_status nnt_softmax(const float* x, int64_t rows, int64_t cols, int64_t ldx, int64_t tile_k, int causal,

@@ -39,7 +39,8 @@ OP_NAMES = ("ln1", "qkv", "scores", "maxsumexp", "softmax", "pv", "out", "ln2", 
 
 # The exported symbols include/nnt.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_grid", "nnt_tile_extent",
-           "nnt_partition", "nnt_tile_gemm", "nnt_tile_gemm_workspace_bytes", "nnt_maxsumexp", "nnt_softmax", "nnt_softmax_bwd",
+           "nnt_partition", "nnt_tile_gemm", "nnt_tile_gemm_workspace_bytes", "nnt_maxsumexp",
+           "nnt_maxsumexp_merge", "nnt_softmax", "nnt_softmax_bwd",
            "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
@@ -56,7 +57,7 @@ class NNTError(RuntimeError):
 class nnt_epilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
                 ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t)]
+                ("workspace_bytes", C.c_size_t), ("row_stats", C.c_void_p), ("ld_row_stats", C.c_int64)]
 
 
 class nnt_adam_hparams(C.Structure):
@@ -103,6 +104,7 @@ _sig = {
                              _f32, _vp, _i32, _i64, _P64, _P64, C.POINTER(nnt_epilogue), _vp]),
     "nnt_tile_gemm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i32, _i32, _i32, _i64]),
     "nnt_maxsumexp": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _i32, _vp]),
+    "nnt_maxsumexp_merge": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
     "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
     "nnt_layernorm_fwd": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _i32, _i64, _vp, _vp, _vp]),
@@ -203,12 +205,12 @@ def nnt_partition(n_units, n_ranks, rank):
 
 
 def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
-                  causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0):
+                  causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0, row_stats=None, ld_row_stats=0):
     """The caller keeps every tensor passed here alive until the launch has run."""
     if workspace is not None and not workspace_bytes and hasattr(workspace, "numel"):
         workspace_bytes = workspace.numel() * workspace.element_size()
     return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal, ptr(workspace),
-                        workspace_bytes)
+                        workspace_bytes, ptr(row_stats), ld_row_stats)
 
 
 def nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act=NNT_ACT_NONE, causal=NNT_CAUSAL_NONE, batch_items=1):
@@ -226,6 +228,11 @@ def nnt_tile_gemm(trans_a, trans_b, M, N, K, batch, alpha, A, a_dtype, lda, stri
 def nnt_maxsumexp(x, rows, cols, ldx, tile_k, causal, seq_q, stats, accumulate=0, stream=None):
     return check(lib.nnt_maxsumexp(ptr(x), rows, cols, ldx, tile_k, causal, seq_q, ptr(stats), accumulate,
                                    _stream(stream)))
+
+
+def nnt_maxsumexp_merge(part, rows, nparts, ld_parts, part_cols, causal, seq_q, stats, stream=None):
+    return check(lib.nnt_maxsumexp_merge(ptr(part), rows, nparts, ld_parts, part_cols, causal, seq_q, ptr(stats),
+                                         _stream(stream)))
 
 
 def nnt_softmax(x, rows, cols, ldx, tile_k, causal, seq_q, stats, y, y_dtype, ldy, stream=None):

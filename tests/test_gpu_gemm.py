@@ -182,6 +182,36 @@ def test_gemm_wave_model_tile_widths_bit_exact(N):
     assert np.array_equal(got, a.astype(np.float64) @ b.T.astype(np.float64))
 
 
+@pytest.mark.parametrize("causal", [0, 1])
+def test_scores_gemm_fused_maxsumexp_partials(causal):
+    """Softmax subroutine 1 per 32-key tile in the score-GEMM epilogue + nnt_maxsumexp_merge
+    equals the oracle's (max, sumexp) of the same scores."""
+    B, S, H, Dh = 2, 384, 3, 64
+    E = H * Dh
+    rng = np.random.default_rng(61 + causal)
+    qkv = bf16_round(rng.standard_normal((B, S, 3 * E)))
+    Q = dev(qkv, torch.bfloat16)
+    sq = (S * 3 * E, Dh)
+    alpha = 1.0 / math.sqrt(Dh)
+    scores = torch.zeros(B, H, S, S, device="cuda")
+    nparts = S // 32
+    part = torch.zeros(B * H * S, nparts, 2, device="cuda")
+    epi = nnt.make_epilogue(causal=causal, row_stats=part, ld_row_stats=nparts)
+    nnt.nnt_tile_gemm(0, 1, S, S, Dh, (B, H), alpha, Q, 1, 3 * E, sq, Q.data_ptr() + 2 * E, 1, 3 * E, sq, 0.0, scores,
+                      0, S, (H * S * S, S * S), None, epi)
+    stats = torch.zeros(B * H * S, 2, device="cuda")
+    nnt.nnt_maxsumexp_merge(part, B * H * S, nparts, nparts, 32, causal, S, stats)
+    torch.cuda.synchronize()
+    q = qkv[:, :, :E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    k = qkv[:, :, E:2 * E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    a = alpha * (q @ k.transpose(0, 1, 3, 2))
+    mask = np.tril(np.ones((S, S), bool)) if causal else None
+    m_ref, s_ref = dense.maxsumexp(a, mask)
+    got = host(stats).reshape(B, H, S, 2)
+    np.testing.assert_allclose(got[..., 0], m_ref, rtol=1e-5, atol=1e-5)
+    assert rel(got[..., 1], s_ref) < 1e-5
+
+
 def test_gemm_rejects_bad_arguments():
     A = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(nnt.NNTError) as e:  # misaligned leading dimension for TMA
