@@ -104,7 +104,11 @@ typedef enum {
 typedef enum {
   NNT_ACT_NONE = 0,
   NNT_ACT_GELU = 1,     /* aux <- pre ; C <- gelu(pre)           (R11) */
-  NNT_ACT_GELU_BWD = 2  /* C <- pre * gelu'(aux)                  (R18)          */
+  NNT_ACT_GELU_BWD = 2, /* C <- pre * gelu'(aux)                  (R18)          */
+  /* Softmax backward fused into the dP = dO V^T GEMM (R18 with D from the dO.O identity):
+   * C <- rowscale * aux * (pre - rowvec[item*M + i]); aux = P (same dtype, batch strides and
+   * ld as C), rowvec = D (fp32), rowscale = 1/sqrt(h).  bf16 path only. */
+  NNT_ACT_SOFTMAX_BWD = 3
 } nnt_act;
 
 typedef struct {
@@ -128,6 +132,8 @@ typedef struct {
    * nnt_maxsumexp_merge.  NULL = off. */
   float* row_stats;
   int64_t ld_row_stats;   /* in (max, sumexp) pairs, >= ceil(N / 32) */
+  const float* rowvec;    /* NNT_ACT_SOFTMAX_BWD: per-row D, indexed (p*batch1 + q)*M + i */
+  float rowscale;         /* NNT_ACT_SOFTMAX_BWD: output scale                            */
 } nnt_epilogue;
 
 /* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would
@@ -208,6 +214,15 @@ nnt_status nnt_softmax_bwd(const void* p, int p_dtype, int64_t ldp,
                            const float* dp, int64_t lddp,
                            int64_t rows, int64_t cols, int causal, int64_t seq_q, float scale,
                            void* da, int da_dtype, int64_t ldda, nnt_stream_t stream);
+
+/*
+ * D for the softmax backward through the identity sum_k P[q][k] dP[q][k] = sum_i dO[q][i] O[q][i]
+ * (dP = dO V^T and O = P V; pinned in tests/test_oracle_pins.py):
+ *   D[(b*H + n)*S + s] = sum_{i<h} dO[b][s][n*h + i] * O[b][s][n*h + i]
+ * dO, O: device bf16 or fp32 [B][S][H*h] (`dtype`); D: device fp32 [B*H*S].
+ */
+nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, int64_t S, int64_t H,
+                           int64_t h, float* D, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
 /* LayerNorm in three steps                                       */

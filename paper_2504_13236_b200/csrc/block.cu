@@ -15,7 +15,7 @@ struct Layout {
   // saved (per layer)
   size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
   // scratch
-  size_t scores, spart, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
+  size_t scores, spart, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
   size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes;
 };
 
@@ -49,6 +49,7 @@ Layout make_layout(const nnt_block_cfg& c) {
   L.scores = take(4 * B * H * S * S);
   // bf16 path: per (slice, 32-key tile) (max, sumexp) partials from the score GEMM epilogue
   L.spart = take(c.dtype == NNT_BF16 ? 8 * B * H * S * ((S + 31) / 32) : 0);
+  L.dvec = take(c.dtype == NNT_BF16 ? 4 * B * H * S : 0);  // D = rowdot(dO, O) (bf16 path)
   L.dy16 = take(dt * T * E);
   L.du = take(dt * T * F);
   L.dh = take(4 * T * E);
@@ -236,6 +237,15 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
     case NNT_OP_ATT_DP: {
       const int64_t so[2] = {S * E, Dh}, sv[2] = {S * 3 * E, Dh}, sp[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
+      if (bf) {  // softmax backward in the epilogue: dA = P * (dO V^T - D) / sqrt(h), straight to bf16
+        e.act = NNT_ACT_SOFTMAX_BWD;
+        e.aux = x.s<void>(x.L.P);
+        e.ld_aux = S;
+        e.rowvec = x.k<float>(x.L.dvec);
+        e.rowscale = x.inv_sqrt_dh;
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), E, so,
+                    x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.k<void>(x.L.dA), dt, S, sp, &e);
+      }
       return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), E, so,
                   x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.k<float>(x.L.scores), NNT_F32, S, sp, &e);
     }
@@ -246,6 +256,8 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                   0.f, x.k<uint8_t>(x.L.dqkv) + es * 2 * E, dt, 3 * E, sq, &e);
     }
     case NNT_OP_SOFTMAX_BWD:
+      if (bf)  // the reduction D = sum_k P dP via the dO.O identity; dA is formed in the dP GEMM
+        return nnt_attn_rowdot(x.k<void>(x.L.dO), x.s<void>(x.L.O), dt, B, S, H, Dh, x.k<float>(x.L.dvec), x.st);
       return nnt_softmax_bwd(x.s<void>(x.L.P), dt, S, x.k<float>(x.L.scores), S, B * H * S, S, x.c.causal, S,
                              x.inv_sqrt_dh, x.k<void>(x.L.dA), dt, S, x.st);
     case NNT_OP_ATT_DQ: {

@@ -194,6 +194,7 @@ struct BlockTensors {
   T2 dy, dyA, du, dh, dx1, dx1A, dO, dqkv, dx;
   T2 gln1, gln2, gwqkv, gbqkv, gwo, gbo, gwfc, gbfc, gwpr, gbpr;
   TAtt dP, dA;
+  TStats Dv;  // bf16 path: D = rowdot(dO, O) per query tile
 };
 
 using Acc = std::vector<std::pair<int64_t, int>>;
@@ -251,6 +252,7 @@ void make_bwd_tensors(StfGraph& g, const Shapes& s, BlockTensors& t) {
   t.gbpr.make(g, 1, E, 1, s.te);
   t.dP.make(g, s);
   t.dA.make(g, s);
+  t.Dv.make(g, s);
 }
 
 // LayerNorm: one task per token tile (steps 1-3 of P:162 over every E-tile of the row block).
@@ -432,14 +434,39 @@ void build_bwd(StfGraph& g, const Shapes& s) {
           for (int64_t kj = 0; kj < ag.nq; ++kj)
             if (ag.needed(qi, kj)) fn(b, h, qi, kj);
   };
-  each_pair([&](int64_t b, int64_t h, int64_t qi, int64_t kj) {  // dP = dO V^T
-    Acc a;
-    t.dO.region(g, ag.row0(b, qi), ag.row1(b, qi), h * s.Dh, (h + 1) * s.Dh, ACC_R, a);
-    t.qkv.region(g, ag.row0(b, kj), ag.row1(b, kj), ag.col0(2, h), ag.col1(2, h), ACC_R, a);
-    a.emplace_back(t.dP.h(g, b, h, qi, kj), ACC_W);
-    int64_t tl[3] = {b * s.H + h, qi, kj};
-    g.submit(NNT_OP_ATT_DP, tl, a);
-  });
+  if (s.bf16) {
+    // bf16 path: D = rowdot(dO, O) per query tile first (softmax-bwd reduction through the
+    // dO.O identity), then dA = scale * P * (dO V^T - D) straight from the dP GEMM epilogue.
+    for (int64_t b = 0; b < s.B; ++b)
+      for (int64_t h = 0; h < s.H; ++h)
+        for (int64_t qi = 0; qi < ag.nq; ++qi) {
+          Acc a;
+          t.dO.region(g, ag.row0(b, qi), ag.row1(b, qi), h * s.Dh, (h + 1) * s.Dh, ACC_R, a);
+          t.O.region(g, ag.row0(b, qi), ag.row1(b, qi), h * s.Dh, (h + 1) * s.Dh, ACC_R, a);
+          a.emplace_back(t.Dv.h(g, b, h, qi), ACC_W);
+          int64_t tl[3] = {b * s.H + h, qi, 0};
+          g.submit(NNT_OP_SOFTMAX_BWD, tl, a);
+        }
+    each_pair([&](int64_t b, int64_t h, int64_t qi, int64_t kj) {  // dA tile = f(dO V^T, P, D)
+      Acc a;
+      t.dO.region(g, ag.row0(b, qi), ag.row1(b, qi), h * s.Dh, (h + 1) * s.Dh, ACC_R, a);
+      t.qkv.region(g, ag.row0(b, kj), ag.row1(b, kj), ag.col0(2, h), ag.col1(2, h), ACC_R, a);
+      a.emplace_back(t.P.h(g, b, h, qi, kj), ACC_R);
+      a.emplace_back(t.Dv.h(g, b, h, qi), ACC_R);
+      a.emplace_back(t.dA.h(g, b, h, qi, kj), ACC_W);
+      int64_t tl[3] = {b * s.H + h, qi, kj};
+      g.submit(NNT_OP_ATT_DP, tl, a);
+    });
+  } else {
+    each_pair([&](int64_t b, int64_t h, int64_t qi, int64_t kj) {  // dP = dO V^T
+      Acc a;
+      t.dO.region(g, ag.row0(b, qi), ag.row1(b, qi), h * s.Dh, (h + 1) * s.Dh, ACC_R, a);
+      t.qkv.region(g, ag.row0(b, kj), ag.row1(b, kj), ag.col0(2, h), ag.col1(2, h), ACC_R, a);
+      a.emplace_back(t.dP.h(g, b, h, qi, kj), ACC_W);
+      int64_t tl[3] = {b * s.H + h, qi, kj};
+      g.submit(NNT_OP_ATT_DP, tl, a);
+    });
+  }
   each_pair([&](int64_t b, int64_t h, int64_t qi, int64_t kj) {  // dV = P^T dO
     Acc a;
     a.emplace_back(t.P.h(g, b, h, qi, kj), ACC_R);
@@ -448,19 +475,20 @@ void build_bwd(StfGraph& g, const Shapes& s) {
     int64_t tl[3] = {b * s.H + h, kj, qi};
     g.submit(NNT_OP_ATT_DV, tl, a);
   });
-  for (int64_t b = 0; b < s.B; ++b)
-    for (int64_t h = 0; h < s.H; ++h)
-      for (int64_t qi = 0; qi < ag.nq; ++qi) {  // softmax bwd needs the whole slice for D
-        Acc a;
-        for (int64_t kj = 0; kj < ag.nq; ++kj) {
-          if (!ag.needed(qi, kj)) continue;
-          a.emplace_back(t.P.h(g, b, h, qi, kj), ACC_R);
-          a.emplace_back(t.dP.h(g, b, h, qi, kj), ACC_R);
-          a.emplace_back(t.dA.h(g, b, h, qi, kj), ACC_W);
+  if (!s.bf16)
+    for (int64_t b = 0; b < s.B; ++b)
+      for (int64_t h = 0; h < s.H; ++h)
+        for (int64_t qi = 0; qi < ag.nq; ++qi) {  // softmax bwd needs the whole slice for D
+          Acc a;
+          for (int64_t kj = 0; kj < ag.nq; ++kj) {
+            if (!ag.needed(qi, kj)) continue;
+            a.emplace_back(t.P.h(g, b, h, qi, kj), ACC_R);
+            a.emplace_back(t.dP.h(g, b, h, qi, kj), ACC_R);
+            a.emplace_back(t.dA.h(g, b, h, qi, kj), ACC_W);
+          }
+          int64_t tl[3] = {b * s.H + h, qi, 0};
+          g.submit(NNT_OP_SOFTMAX_BWD, tl, a);
         }
-        int64_t tl[3] = {b * s.H + h, qi, 0};
-        g.submit(NNT_OP_SOFTMAX_BWD, tl, a);
-      }
   each_pair([&](int64_t b, int64_t h, int64_t qi, int64_t kj) {  // dQ = dA K
     Acc a;
     a.emplace_back(t.dA.h(g, b, h, qi, kj), ACC_R);

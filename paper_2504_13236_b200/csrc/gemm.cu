@@ -69,15 +69,17 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
   g.in_dtype = a_dtype;
   g.causal = NNT_CAUSAL_NONE;
   if (epi) {
-    NNT_REQUIRE(epi->act >= NNT_ACT_NONE && epi->act <= NNT_ACT_GELU_BWD, NNT_ERR_ARG, "nnt_tile_gemm: act=%d",
+    NNT_REQUIRE(epi->act >= NNT_ACT_NONE && epi->act <= NNT_ACT_SOFTMAX_BWD, NNT_ERR_ARG, "nnt_tile_gemm: act=%d",
                 epi->act);
+    NNT_REQUIRE(epi->act != NNT_ACT_SOFTMAX_BWD || (a_dtype == NNT_BF16 && epi->rowvec && epi->aux),
+                NNT_ERR_UNSUPPORTED, "nnt_tile_gemm: SOFTMAX_BWD epilogue needs bf16 operands, aux (P) and rowvec (D)");
     NNT_REQUIRE(epi->causal >= NNT_CAUSAL_NONE && epi->causal <= NNT_CAUSAL_A_UPPER, NNT_ERR_ARG,
                 "nnt_tile_gemm: causal=%d", epi->causal);
     NNT_REQUIRE(epi->act == NNT_ACT_NONE || epi->aux, NNT_ERR_NULL, "nnt_tile_gemm: GELU epilogue needs aux");
     NNT_REQUIRE(!epi->residual || epi->ld_residual >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_residual");
     NNT_REQUIRE(!epi->aux || epi->ld_aux >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_aux");
-    NNT_REQUIRE((!epi->residual && !epi->aux) || (b0 == 1 && b1 == 1), NNT_ERR_UNSUPPORTED,
-                "nnt_tile_gemm: residual/aux epilogues are for unbatched GEMMs");
+    NNT_REQUIRE((!epi->residual && (!epi->aux || epi->act == NNT_ACT_SOFTMAX_BWD)) || (b0 == 1 && b1 == 1),
+                NNT_ERR_UNSUPPORTED, "nnt_tile_gemm: residual/GELU-aux epilogues are for unbatched GEMMs");
     g.bias = epi->bias;
     g.residual = epi->residual;
     g.ld_res = epi->ld_residual;
@@ -89,6 +91,8 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.workspace_bytes = epi->workspace_bytes;
     g.row_stats = epi->row_stats;
     g.ld_stats = epi->ld_row_stats;
+    g.rowvec = epi->rowvec;
+    g.rowscale = epi->rowscale;
     NNT_REQUIRE(!epi->row_stats || (a_dtype == NNT_BF16 && c_dtype == NNT_F32 && epi->act == NNT_ACT_NONE &&
                                     epi->ld_row_stats >= (N + 31) / 32 &&
                                     (epi->causal == NNT_CAUSAL_NONE || epi->causal == NNT_CAUSAL_OUT_LOWER)),

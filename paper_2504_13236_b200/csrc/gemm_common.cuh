@@ -29,6 +29,8 @@ struct GemmArgs {
   size_t workspace_bytes;
   float* row_stats;  // fused softmax subroutine 1: per (row, 32-column tile) (max, sumexp)
   int64_t ld_stats;  // pairs per row
+  const float* rowvec;  // NNT_ACT_SOFTMAX_BWD: D per row
+  float rowscale;
 };
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);

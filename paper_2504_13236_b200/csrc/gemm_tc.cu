@@ -38,6 +38,7 @@ constexpr int BK = 64;        // 64 bf16 = 128 B = one SW128 row
 constexpr int kEpiWarps = 8;  // two per TMEM lane quadrant
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for one TMA store box
+constexpr int kStageBufs = 2;             // staging ring per epilogue warp (one store in flight while refilling)
 constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory per CTA
 
 template <int BN>
@@ -45,7 +46,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * kStageBytesPerWarp;
+  static constexpr int EPI_BYTES = kEpiWarps * kStageBufs * kStageBytesPerWarp;
   static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -247,11 +248,30 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o, bool cg) {
 // staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
 template <typename TC, int W>
 __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const TC* auxb, int64_t row, int64_t col0,
-                                         bool extras, bool vec, float (&v)[W]) {
+                                         bool extras, bool vec, float dval, float (&v)[W]) {
   constexpr bool kFast = sizeof(TC) == 2;
 #pragma unroll
   for (int j = 0; j < W; ++j) v[j] *= g.alpha;
   if (!extras) return;  // split-K partial: bias/beta/residual belong to the reduce
+  if (g.act == NNT_ACT_SOFTMAX_BWD) {
+    // dA = scale * P * (dP - D): aux holds P with C's layout, dval = D of this row
+    if (row < g.M) {
+      const TC* ar = auxb + row * g.ld_aux + col0;
+      if (vec && col0 + W <= g.N) {
+        float t[8];
+#pragma unroll
+        for (int j = 0; j < W; j += 8) {
+          ld8(ar + j, t, false);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[j + i] = g.rowscale * t[i] * (v[j + i] - dval);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < W; ++j) v[j] = col0 + j < g.N ? g.rowscale * ld_elem(ar + j) * (v[j] - dval) : 0.f;
+      }
+    }
+    return;
+  }
   if (vec && row < g.M && col0 + W <= g.N) {
     float t[8];
     if (g.bias) {
@@ -473,7 +493,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the two warps of a quadrant take alternating 128-byte column chunks
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    uint8_t* stage_buf = smem + C::EPI_OFF + (warp - 2) * kStageBytesPerWarp;
+    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * kStageBufs * kStageBytesPerWarp;
+    int ring = 0;
+    // Stage one 32-row x 128-byte chunk and issue its TMA store; before refilling a buffer,
+    // at most kStageBufs-1 earlier stores (those reading the other buffers) may be in flight.
+    auto stage_and_store = [&](const CUtensorMap* map, const auto& vals, bool as_f32, int c0, int c1, int c2,
+                               int c3) {
+      uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
+      __syncwarp();
+      if (as_f32)
+        stage_row<float, W>(buf, lane, vals);
+      else
+        stage_row<TC, W>(buf, lane, vals);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(map, smem_u32(buf), c0, c1, c2, c3);
+        bulk_commit();
+      }
+      ring = ring + 1 == kStageBufs ? 0 : ring + 1;
+    };
     const size_t cs = sizeof(TC);
     auto a16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
     const bool vec = a16(g.C) && (g.ldc * cs) % 16 == 0 && (!g.bias || a16(g.bias)) &&
@@ -491,6 +531,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const int64_t row = ti.m0 + quad * 32 + lane;
       const bool has_k = ti.kb_end > ti.kb_begin;
+      const float dval =
+          (g.act == NNT_ACT_SOFTMAX_BWD && row < g.M) ? __ldg(g.rowvec + ti.bz * g.M + row) : 0.f;
 #pragma unroll 1
       for (int c = half * W; c < BN; c += 2 * W) {
         if (ti.n0 + c >= g.N) break;  // warp-uniform
@@ -507,19 +549,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
         if (P.ws_mode) {
           // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce kernel
-          epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, v);
-          if (lane == 0) bulk_wait_read0();
-          __syncwarp();
-          stage_row<float, W>(stage_buf, lane, v);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(&tmAux, smem_u32(stage_buf), cx, cy, (int)ti.split, 0);
-            bulk_commit();
-          }
+          epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, 0.f, v);
+          stage_and_store(&tmAux, v, true, cx, cy, (int)ti.split, 0);
           continue;
         }
-        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, v);
+        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, v);
         if (g.row_stats != nullptr && row < g.M) {
           // fused softmax subroutine 1: (max, sumexp) of this row over the chunk's
           // valid columns (W = 32 for fp32 C: one 32-column key tile)
@@ -538,17 +572,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           *reinterpret_cast<float2*>(g.row_stats + 2 * ((ti.bz * g.M + row) * g.ld_stats + col0 / 32)) =
               make_float2(m, s);
         }
-        auto stage_store = [&](const CUtensorMap* map) {
-          if (lane == 0) bulk_wait_read0();  // the previous bulk store finished reading the buffer
-          __syncwarp();
-          stage_row<TC, W>(stage_buf, lane, v);
-          fence_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            tma_store_4d(map, smem_u32(stage_buf), cx, cy, (int)q, (int)p);
-            bulk_commit();
-          }
-        };
+        auto stage_store = [&](const CUtensorMap* map) { stage_and_store(map, v, false, cx, cy, (int)q, (int)p); };
         if (g.act == NNT_ACT_GELU) {  // pre-activation -> aux, then gelu in place -> C
           if (P.tma_store)
             stage_store(&tmAux);

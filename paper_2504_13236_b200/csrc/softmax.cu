@@ -163,6 +163,34 @@ __global__ void __launch_bounds__(kThreads) maxsumexp_merge_kernel(const float2*
   stats[row] = make_float2(M, S);
 }
 
+// ------------------------------------------------------------------ D = rowdot(dO, O) per (b, head, s)
+// One thread per (b, s, head): h contiguous elements of dO and O (16-byte loads when
+// h*sizeof(T) % 16 == 0); output index (b*H + n)*S + s.
+template <typename T>
+__global__ void __launch_bounds__(kThreads) attn_rowdot_kernel(const T* __restrict__ dO, const T* __restrict__ O,
+                                                               int64_t B, int64_t S, int64_t H, int64_t h,
+                                                               float* __restrict__ D) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // ((b*S + s)*H + n)
+  if (idx >= B * S * H) return;
+  const int64_t n = idx % H, bs = idx / H, b = bs / S, s = bs % S;
+  const T* a = dO + bs * H * h + n * h;
+  const T* o = O + bs * H * h + n * h;
+  float acc = 0.f;
+  constexpr int V = 16 / sizeof(T);
+  if ((h * sizeof(T)) % 16 == 0) {
+    for (int64_t i = 0; i < h; i += V) {
+      uint4 ua = *reinterpret_cast<const uint4*>(a + i), uo = *reinterpret_cast<const uint4*>(o + i);
+      const T* ea = reinterpret_cast<const T*>(&ua);
+      const T* eo = reinterpret_cast<const T*>(&uo);
+#pragma unroll
+      for (int j = 0; j < V; ++j) acc = fmaf(to_f32(ea[j]), to_f32(eo[j]), acc);
+    }
+  } else {
+    for (int64_t i = 0; i < h; ++i) acc = fmaf(to_f32(a[i]), to_f32(o[i]), acc);
+  }
+  D[(b * H + n) * S + s] = acc;
+}
+
 // ------------------------------------------------------------------ subroutine 2
 template <typename TO>
 __global__ void __launch_bounds__(kThreads) softmax_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
@@ -279,6 +307,23 @@ nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx
   switch (nc) { NNT_MSE(1) NNT_MSE(2) NNT_MSE(4) NNT_MSE(8) NNT_MSE(16) }
 #undef NNT_MSE
   return check_launch("maxsumexp");
+}
+
+nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, int64_t S, int64_t H, int64_t h,
+                           float* D, nnt_stream_t stream) {
+  NNT_REQUIRE(dO && O && D, NNT_ERR_NULL, "nnt_attn_rowdot: NULL pointer");
+  NNT_REQUIRE(B > 0 && S > 0 && H > 0 && h > 0, NNT_ERR_SHAPE, "nnt_attn_rowdot: bad shape");
+  NNT_REQUIRE(valid_dtype(dtype), NNT_ERR_DTYPE, "nnt_attn_rowdot: dtype %d", dtype);
+  NNT_REQUIRE(aligned16(dO) && aligned16(O), NNT_ERR_ALIGN, "nnt_attn_rowdot: pointers must be 16-byte aligned");
+  const int64_t n = B * S * H;
+  LaunchScope sc(NNT_K_MISC, stream, 2.0 * dtype_size(dtype) * n * h + 4.0 * n, 2.0 * n * h);
+  const unsigned grid = (unsigned)((n + kThreads - 1) / kThreads);
+  if (dtype == NNT_BF16)
+    attn_rowdot_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>((const __nv_bfloat16*)dO,
+                                                                     (const __nv_bfloat16*)O, B, S, H, h, D);
+  else
+    attn_rowdot_kernel<float><<<grid, kThreads, 0, stream>>>((const float*)dO, (const float*)O, B, S, H, h, D);
+  return check_launch("attn_rowdot");
 }
 
 nnt_status nnt_maxsumexp_merge(const float* part, int64_t rows, int64_t nparts, int64_t ld_parts, int64_t part_cols,

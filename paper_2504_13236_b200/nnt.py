@@ -29,7 +29,7 @@ STATUS_NAMES = {0: "NNT_OK", 1: "NNT_ERR_NULL", 2: "NNT_ERR_SHAPE", 3: "NNT_ERR_
 NNT_F32, NNT_BF16 = 0, 1
 NNT_NOTRANS, NNT_TRANS = 0, 1
 NNT_CAUSAL_NONE, NNT_CAUSAL_OUT_LOWER, NNT_CAUSAL_A_LOWER, NNT_CAUSAL_A_UPPER = 0, 1, 2, 3
-NNT_ACT_NONE, NNT_ACT_GELU, NNT_ACT_GELU_BWD = 0, 1, 2
+NNT_ACT_NONE, NNT_ACT_GELU, NNT_ACT_GELU_BWD, NNT_ACT_SOFTMAX_BWD = 0, 1, 2, 3
 NNT_CAUSAL_ALIGN = 128
 KERNEL_CLASSES = ("gemm_tc", "gemm_tc_attn", "gemm_simt", "maxsumexp", "softmax", "softmax_bwd", "ln_fwd", "ln_bwd", "gelu",
                   "bias_grad", "adam", "misc")
@@ -40,7 +40,7 @@ OP_NAMES = ("ln1", "qkv", "scores", "maxsumexp", "softmax", "pv", "out", "ln2", 
 # The exported symbols include/nnt.h declares (checked by tests/test_abi.py).
 EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_grid", "nnt_tile_extent",
            "nnt_partition", "nnt_tile_gemm", "nnt_tile_gemm_workspace_bytes", "nnt_maxsumexp",
-           "nnt_maxsumexp_merge", "nnt_softmax", "nnt_softmax_bwd",
+           "nnt_maxsumexp_merge", "nnt_attn_rowdot", "nnt_softmax", "nnt_softmax_bwd",
            "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
@@ -57,7 +57,8 @@ class NNTError(RuntimeError):
 class nnt_epilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
                 ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int), ("workspace", C.c_void_p),
-                ("workspace_bytes", C.c_size_t), ("row_stats", C.c_void_p), ("ld_row_stats", C.c_int64)]
+                ("workspace_bytes", C.c_size_t), ("row_stats", C.c_void_p), ("ld_row_stats", C.c_int64),
+                ("rowvec", C.c_void_p), ("rowscale", C.c_float)]
 
 
 class nnt_adam_hparams(C.Structure):
@@ -105,6 +106,7 @@ _sig = {
     "nnt_tile_gemm_workspace_bytes": (_sz, [_i64, _i64, _i64, _i32, _i32, _i32, _i64]),
     "nnt_maxsumexp": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _i32, _vp]),
     "nnt_maxsumexp_merge": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp]),
+    "nnt_attn_rowdot": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
     "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
     "nnt_layernorm_fwd": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _i32, _i64, _vp, _vp, _vp]),
@@ -205,12 +207,13 @@ def nnt_partition(n_units, n_ranks, rank):
 
 
 def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
-                  causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0, row_stats=None, ld_row_stats=0):
+                  causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0, row_stats=None, ld_row_stats=0,
+                  rowvec=None, rowscale=1.0):
     """The caller keeps every tensor passed here alive until the launch has run."""
     if workspace is not None and not workspace_bytes and hasattr(workspace, "numel"):
         workspace_bytes = workspace.numel() * workspace.element_size()
     return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal, ptr(workspace),
-                        workspace_bytes, ptr(row_stats), ld_row_stats)
+                        workspace_bytes, ptr(row_stats), ld_row_stats, ptr(rowvec), rowscale)
 
 
 def nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act=NNT_ACT_NONE, causal=NNT_CAUSAL_NONE, batch_items=1):
@@ -233,6 +236,10 @@ def nnt_maxsumexp(x, rows, cols, ldx, tile_k, causal, seq_q, stats, accumulate=0
 def nnt_maxsumexp_merge(part, rows, nparts, ld_parts, part_cols, causal, seq_q, stats, stream=None):
     return check(lib.nnt_maxsumexp_merge(ptr(part), rows, nparts, ld_parts, part_cols, causal, seq_q, ptr(stats),
                                          _stream(stream)))
+
+
+def nnt_attn_rowdot(dO, O, dtype, B, S, H, h, D, stream=None):
+    return check(lib.nnt_attn_rowdot(ptr(dO), ptr(O), dtype, B, S, H, h, ptr(D), _stream(stream)))
 
 
 def nnt_softmax(x, rows, cols, ldx, tile_k, causal, seq_q, stats, y, y_dtype, ldy, stream=None):

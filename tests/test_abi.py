@@ -144,7 +144,7 @@ def _expected_counts(c, tile):
            "out": nt * ne * ne, "ln2": nt, "fc": nt * nf * ne, "proj": nt * ne * nf}
     bwd = {"proj_db": nt * ne, "proj_dw": ne * nf * nt, "proj_dx": nt * nf * ne, "fc_db": nt * nf,
            "fc_dw": nf * ne * nt, "fc_dx": nt * ne * nf, "ln2_bwd": nt, "out_db": nt * ne, "out_dw": ne * ne * nt,
-           "out_dx": nt * ne * ne, "att_dp": pairs, "att_dv": pairs, "softmax_bwd": c.B * c.H * nq, "att_dq": pairs,
+           "out_dx": nt * ne * ne, "softmax_bwd": c.B * c.H * nq, "att_dp": pairs, "att_dv": pairs, "att_dq": pairs,
            "att_dk": pairs, "qkv_db": nt * n3, "qkv_dw": n3 * ne * nt, "qkv_dx": nt * ne * n3, "ln1_bwd": nt}
     return fwd, bwd
 
@@ -168,9 +168,14 @@ def test_dag_task_counts_and_levels(nnt, name, tile):
     assert lv["proj_dw"] == lv["proj_dx"] == lv["proj_db"] + (1 if bf else 0)
     assert lv["fc_db"] == lv["fc_dw"] == lv["fc_dx"] == lv["proj_dx"] + 1
     assert lv["ln2_bwd"] == lv["fc_dx"] + 1
-    assert lv["att_dp"] == lv["att_dv"] == lv["out_dx"] + 1
-    assert lv["softmax_bwd"] == lv["att_dp"] + 1
-    assert lv["att_dq"] == lv["att_dk"] == lv["softmax_bwd"] + 1
+    if bf:  # D = rowdot(dO, O) first, then the dP GEMM emits dA directly
+        assert lv["softmax_bwd"] == lv["att_dv"] == lv["out_dx"] + 1
+        assert lv["att_dp"] == lv["softmax_bwd"] + 1
+        assert lv["att_dq"] == lv["att_dk"] == lv["att_dp"] + 1
+    else:
+        assert lv["att_dp"] == lv["att_dv"] == lv["out_dx"] + 1
+        assert lv["softmax_bwd"] == lv["att_dp"] + 1
+        assert lv["att_dq"] == lv["att_dk"] == lv["softmax_bwd"] + 1
     assert lv["qkv_dx"] == lv["att_dq"] + 1
     assert lv["ln1_bwd"] == lv["qkv_dx"] + 1
     assert [g.level for g in groups] == sorted(g.level for g in groups)

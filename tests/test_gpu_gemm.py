@@ -212,6 +212,38 @@ def test_scores_gemm_fused_maxsumexp_partials(causal):
     assert rel(got[..., 1], s_ref) < 1e-5
 
 
+def test_fused_softmax_bwd_gemm_and_rowdot():
+    """dA = P * (dO V^T - D) / sqrt(h) from the dP GEMM epilogue, with D = rowdot(dO, O)
+    (identity sum_k P dP = sum_i dO O), vs the oracle's softmax backward (R18)."""
+    B, S, H, Dh = 2, 384, 3, 64
+    E = H * Dh
+    rng = np.random.default_rng(71)
+    qkv = bf16_round(rng.standard_normal((B, S, 3 * E)))
+    do = bf16_round(rng.standard_normal((B, S, E)))
+    o_ref, p_ref = dense.attention_core_fwd(qkv, H, True)
+    P16 = bf16_round(p_ref)
+    O16 = bf16_round(o_ref)
+    Qd, dOd = dev(qkv, torch.bfloat16), dev(do, torch.bfloat16)
+    Pd, Od = dev(P16, torch.bfloat16), dev(O16, torch.bfloat16)
+    D = torch.zeros(B * H * S, device="cuda")
+    nnt.nnt_attn_rowdot(dOd, Od, 1, B, S, H, Dh, D)
+    dA = torch.full((B, H, S, S), float("nan"), device="cuda", dtype=torch.bfloat16)
+    scale = 1.0 / math.sqrt(Dh)
+    epi = nnt.make_epilogue(act=nnt.NNT_ACT_SOFTMAX_BWD, aux=Pd, ld_aux=S, causal=1, rowvec=D, rowscale=scale)
+    nnt.nnt_tile_gemm(0, 1, S, S, Dh, (B, H), 1.0, dOd, 1, E, (S * E, Dh), Qd.data_ptr() + 2 * 2 * E, 1, 3 * E,
+                      (S * 3 * E, Dh), 0.0, dA, 1, S, (H * S * S, S * S), None, epi)
+    torch.cuda.synchronize()
+    dob = do.reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    ob = O16.reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    assert rel(host(D).reshape(B, H, S), (dob * ob).sum(-1)) < 1e-5
+    v = qkv[:, :, 2 * E:].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    want = scale * dense.softmax_bwd(P16, dob @ v.transpose(0, 1, 3, 2))
+    got = host(dA)
+    mask = np.tril(np.ones((S, S), bool))
+    assert np.all(got[..., ~mask & (np.arange(S)[None, :] < ((np.arange(S)[:, None] // 128 + 1) * 128))] == 0.0)
+    assert rel(np.where(mask, got, 0.0), want) < 2e-2
+
+
 def test_gemm_rejects_bad_arguments():
     A = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(nnt.NNTError) as e:  # misaligned leading dimension for TMA
