@@ -369,8 +369,45 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
     if (col0 + j < N) base[row * ld + col0 + j] = from_f32<TC>(v[j]);
 }
 
+// 32 consecutive elements of TC (128 B fp32 / 64 B bf16) through the read-only path (the two
+// 16-byte halves of a 32-byte sector share one L1 fill), unpacked 8 at a time.
+struct Raw8 {
+  uint4 u[8];
+};
+template <typename TC>
+__device__ __forceinline__ void raw_load(Raw8& r, const void* p) {
+  const uint4* src = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 32 * (int)sizeof(TC) / 16; ++i) r.u[i] = __ldg(src + i);
+}
+template <typename TC>
+__device__ __forceinline__ void unpack8(const Raw8& r, int j, float* t) {
+  if (sizeof(TC) == 4) {
+    const uint4 a = r.u[j / 4], b = r.u[j / 4 + 1];
+    t[0] = __uint_as_float(a.x); t[1] = __uint_as_float(a.y); t[2] = __uint_as_float(a.z); t[3] = __uint_as_float(a.w);
+    t[4] = __uint_as_float(b.x); t[5] = __uint_as_float(b.y); t[6] = __uint_as_float(b.z); t[7] = __uint_as_float(b.w);
+  } else {
+    const uint4 a = r.u[j / 8];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      t[2 * i] = f.x;
+      t[2 * i + 1] = f.y;
+    }
+  }
+}
+
 // ------------------------------------------------------------------ kernel
-template <int BN, typename TC>
+// Epilogue specialisations (separate instantiations keep each one small and branch-light):
+//   EPI_GENERIC  bias / beta*C / residual / GELU / GELU' / split-K partials
+//   EPI_SCORES   fp32 C = alpha*acc (attention scores) + optional fused per-32-key-tile
+//                (max, sumexp) (softmax subroutine 1)
+//   EPI_DA       bf16 C = rowscale * P * (acc - D[row]) (softmax backward), P prefetched a
+//                chunk ahead
+enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2 };
+
+template <int BN, typename TC, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
@@ -488,6 +525,146 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+  } else if constexpr (EPI == EPI_SCORES || EPI == EPI_DA) {
+    // ===================== specialised epilogues (attention score-type GEMMs)
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * kStageBufs * kStageBytesPerWarp;
+    int ring = 0;
+    const float L2E = 1.4426950408889634f;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
+      TileInfo ti = decode_task(P, t, BN);
+      const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
+      const int row_in = (int)ti.m0 + quad * 32 + lane;  // row of this lane within the batch item
+      const bool row_ok = row_in < g.M;
+      const int cy = (int)ti.m0 + quad * 32;
+      const int c_first = half * W;
+      // EPI_DA: P row pointer of this lane and the prefetch of its first chunk
+      const TC* prow = nullptr;
+      Raw8 raw_cur, raw_nxt;
+      float dval = 0.f;
+      if constexpr (EPI == EPI_DA) {
+        prow = (const TC*)g.aux + p * g.sc0 + q * g.sc1 + (int64_t)row_in * g.ld_aux + ti.n0;
+        if (row_ok && ti.n0 + c_first + W <= g.N) raw_load<TC>(raw_cur, prow + c_first);
+        if constexpr (W == 64) {
+          if (row_ok && ti.n0 + c_first + W <= g.N) raw_load<TC>(raw_nxt, prow + c_first + 32);
+        }
+        dval = row_ok ? __ldg(g.rowvec + ti.bz * g.M + row_in) : 0.f;
+      }
+      mbar_wait(smem_u32(&tfull[acc]), acc_phase);
+      tc_fence_after();
+      const bool has_k = ti.kb_end > ti.kb_begin;
+#pragma unroll 1
+      for (int c = c_first; c < BN; c += 2 * W) {
+        if (ti.n0 + c >= g.N) break;  // warp-uniform
+        const int col0 = (int)ti.n0 + c;
+        float v[W];
+#pragma unroll
+        for (int h = 0; h < W / 32; ++h) {
+          if (has_k)
+            tmem_ld32(tmem_base + (uint32_t)(acc * BN + c + 32 * h) + ((uint32_t)(quad * 32) << 16), v + 32 * h);
+          else
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 * h + j] = 0.f;
+        }
+        if constexpr (EPI == EPI_SCORES) {
+#pragma unroll
+          for (int j = 0; j < W; ++j) v[j] *= g.alpha;
+          if (g.row_stats != nullptr && row_ok) {
+            // softmax subroutine 1 on this 32-key tile; warp-uniform fast path when every lane's
+            // row sees all 32 columns (causal: col0 + 31 <= smallest row of the warp)
+            const bool all_valid = (col0 + 32 <= g.N) && (g.causal != NNT_CAUSAL_OUT_LOWER || col0 + 31 <= cy);
+            float m, s = 0.f;
+            if (all_valid) {
+              float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]);
+#pragma unroll
+              for (int j = 4; j < 32; j += 4) {
+                m0 = fmaxf(m0, fmaxf(v[j], v[j + 1]));
+                m1 = fmaxf(m1, fmaxf(v[j + 2], v[j + 3]));
+              }
+              m = fmaxf(m0, m1);
+              const float ml = m * L2E;
+              float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                s0 += exp2f(fmaf(v[j], L2E, -ml));
+                s1 += exp2f(fmaf(v[j + 1], L2E, -ml));
+                s2 += exp2f(fmaf(v[j + 2], L2E, -ml));
+                s3 += exp2f(fmaf(v[j + 3], L2E, -ml));
+              }
+              s = (s0 + s1) + (s2 + s3);
+            } else {
+              int lim = g.N - col0;
+              if (g.causal == NNT_CAUSAL_OUT_LOWER && row_in - col0 + 1 < lim) lim = row_in - col0 + 1;
+              m = -INFINITY;
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < lim) m = fmaxf(m, v[j]);
+              if (m != -INFINITY) {
+                const float ml = m * L2E;
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (j < lim) s += exp2f(fmaf(v[j], L2E, -ml));
+              }
+            }
+            reinterpret_cast<float2*>(g.row_stats)[(ti.bz * g.M + row_in) * g.ld_stats + col0 / 32] =
+                make_float2(m, s);
+          }
+        } else {
+          // dA = rowscale * P * (dP - D); P of this chunk was prefetched (raw_cur[, raw_nxt])
+          const bool full = row_ok && col0 + W <= g.N;
+          if (full) {
+            float t[8];
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              unpack8<TC>(raw_cur, j, t);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) v[j + i] = g.rowscale * t[i] * (v[j + i] - dval);
+            }
+            if constexpr (W == 64) {
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                unpack8<TC>(raw_nxt, j, t);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[32 + j + i] = g.rowscale * t[i] * (v[32 + j + i] - dval);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < W; ++j)
+              v[j] = (row_ok && col0 + j < g.N) ? g.rowscale * ld_elem(prow + c + j) * (v[j] - dval) : 0.f;
+          }
+          // prefetch the next chunk's P; it lands while this chunk is staged and stored
+          const int cn = c + 2 * W;
+          if (cn < BN && row_ok && ti.n0 + cn + W <= g.N) {
+            raw_load<TC>(raw_cur, prow + cn);
+            if constexpr (W == 64) raw_load<TC>(raw_nxt, prow + cn + 32);
+          }
+        }
+        // stage + TMA store (2-buffer ring per warp)
+        uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
+        __syncwarp();
+        stage_row<TC, W>(buf, lane, v);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&tmC, smem_u32(buf), col0, cy, q, p);
+          bulk_commit();
+        }
+        ring ^= 1;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+    if (lane == 0) bulk_wait0();
   } else {
     // ===================== epilogue: warps 2..9; TMEM lane quadrant = warp % 4 (tcgen05.ld rule),
     // the two warps of a quadrant take alternating 128-byte column chunks
@@ -695,13 +872,21 @@ int64_t gemm_tc_splits(const GemmArgs& a) {
 
 namespace {
 
-template <int BN, typename TC>
+// C (and the GELU aux) can be written by TMA tensor stores
+bool c_tma_ok(const GemmArgs& a, size_t es) {
+  auto ok16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
+  return ok16(a.C) && (a.ldc * es) % 16 == 0 && (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
+         (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
+         (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
+}
+
+template <int BN, typename TC, int EPI>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   using C = Cfg<BN>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES);
   });
   NNT_REQUIRE(attr_err == cudaSuccess, NNT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -750,10 +935,9 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     NNT_TRY(make_map(&tmAux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.workspace, a.N, a.M, a.N, splits, a.M * a.N, 1, 0,
                      32, 32));
   } else {
-    const bool tma_ok = ok16(a.C) && (a.ldc * es) % 16 == 0 &&
-                        (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
-                        (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
-                        (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
+    const bool tma_ok = c_tma_ok(a, es);
+    NNT_REQUIRE(EPI == EPI_GENERIC || tma_ok, NNT_ERR_ALIGN, "gemm(bf16): specialised epilogue needs TMA-able C");
+    (void)ok16;
     P.tma_store = tma_ok ? 1 : 0;
     if (tma_ok) {
       NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
@@ -763,7 +947,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   }
   int64_t grid = P.num_tasks < num_sms() ? P.num_tasks : num_sms();
   if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, TC><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
+  gemm_tc_kernel<BN, TC, EPI><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
   NNT_TRY(check_launch("gemm_tc"));
   if (P.ws_mode) {
     const int64_t total = a.M * (a.N / 4);
@@ -798,11 +982,19 @@ int choose_bn(const GemmArgs& a) {
 
 template <typename TC>
 nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
+  const bool tma_ok = splits == 1 && c_tma_ok(a, sizeof(TC));
+  if constexpr (sizeof(TC) == 2) {
+    if (tma_ok && a.act == NNT_ACT_SOFTMAX_BWD) return launch_bn<128, TC, EPI_DA>(a, s, 1);
+  } else {
+    if (tma_ok && a.act == NNT_ACT_NONE && !a.bias && !a.residual && a.beta == 0.f &&
+        (a.row_stats || a.causal == NNT_CAUSAL_OUT_LOWER))
+      return launch_bn<128, TC, EPI_SCORES>(a, s, 1);
+  }
   switch (splits > 1 ? 256 : choose_bn(a)) {
-    case 64: return launch_bn<64, TC>(a, s, splits);
-    case 128: return launch_bn<128, TC>(a, s, splits);
-    case 192: return launch_bn<192, TC>(a, s, splits);
-    default: return launch_bn<256, TC>(a, s, splits);
+    case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
+    case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
+    case 192: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);
+    default: return launch_bn<256, TC, EPI_GENERIC>(a, s, splits);
   }
 }
 

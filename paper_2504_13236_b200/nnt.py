@@ -12,7 +12,8 @@ import ctypes as C
 import os
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libnnt.so")
+# NNT_LIB: an alternative build of the same ABI (A/B timing of kernel variants in one run)
+LIB_PATH = os.environ.get("NNT_LIB") or os.path.join(_PKG, "libnnt.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is not built; run `python -m paper_2504_13236_b200.build` "

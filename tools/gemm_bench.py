@@ -41,12 +41,20 @@ def main():
     bh = (B, H)
     es = 2
     big = torch.randn(8192, 8192, **bf) * 0.05
+    spart = torch.empty(B * H * S * (S // 32) * 2, **f32)
+    dvec = torch.zeros(B * H * S, **f32)
     cases = [
         # name, ta, tb, M, N, K, batch, A, lda, sa, B, ldb, sb, C, cdt, ldc, sc, epi, causal-frac
         ("qkv", 0, 1, T, 3 * E, E, None, h, E, None, w, E, None, outb, 1, 3 * E, None,
          nnt.make_epilogue(bias=bias), 1.0),
         ("scores", 0, 1, S, S, Dh, bh, h, 3 * E, (S * 3 * E, Dh), h.data_ptr() + es * E, 3 * E, (S * 3 * E, Dh),
          outf, 0, S, (H * S * S, S * S), nnt.make_epilogue(causal=1), 0.5),
+        ("scores+stats", 0, 1, S, S, Dh, bh, h, 3 * E, (S * 3 * E, Dh), h.data_ptr() + es * E, 3 * E,
+         (S * 3 * E, Dh), outf, 0, S, (H * S * S, S * S),
+         nnt.make_epilogue(causal=1, row_stats=spart, ld_row_stats=S // 32), 0.5),
+        ("dp_dA", 0, 1, S, S, Dh, bh, h, E, (S * E, Dh), h.data_ptr() + es * 2 * E, 3 * E, (S * 3 * E, Dh),
+         outb, 1, S, (H * S * S, S * S),
+         nnt.make_epilogue(causal=1, act=3, aux=P, ld_aux=S, rowvec=dvec, rowscale=0.125), 0.5),
         ("pv", 0, 0, S, Dh, S, bh, P, S, (H * S * S, S * S), h, 3 * E, (S * 3 * E, Dh), outb, 1, E, (S * E, Dh),
          nnt.make_epilogue(causal=2), 0.5),
         ("out", 0, 1, T, E, E, None, h, E, None, w, E, None, outf, 0, E, None,
