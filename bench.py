@@ -230,6 +230,12 @@ def run_nnt(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    use_graph = world == 1 and not args.no_graph
+    graph_launches = 0
+    if use_graph:  # the whole step as one CUDA graph (captured launches counted once)
+        n_cap = nnt.nnt_launch_count()
+        st.enable_graph()
+        graph_launches = nnt.nnt_launch_count() - n_cap
     for i in range(args.warmup):
         x, r = dev_batches[i % 2]
         st.train_step(x, r)
@@ -249,13 +255,15 @@ def run_nnt(args):
         st.train_step(x, r)
     e1.record()
     torch.cuda.synchronize()
-    launches = nnt.nnt_launch_count() - n0
+    launches = nnt.nnt_launch_count() - n0 + graph_launches * args.steps
     barrier()
     clocks = sampler.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     loss = float(st.loss.item())
 
-    # ---------------- per-kernel timing (CUDA events around every libnnt launch), same steps again
+    # ---------------- per-kernel timing (CUDA events around every libnnt launch), same kernels
+    # launched eagerly (events cannot be inserted into the replayed graph)
+    graph, st.graph = getattr(st, "graph", None), None
     nnt.nnt_timing_enable(True)
     for i in range(args.steps):
         x, r = dev_batches[i % 2]
@@ -263,6 +271,9 @@ def run_nnt(args):
     torch.cuda.synchronize()
     kt = nnt.nnt_timing_read()
     nnt.nnt_timing_enable(False)
+    st.graph = graph
+    if graph is not None:
+        st.t_dev.fill_(st.step_count)  # keep the device step counter in line with the eager steps
 
     # ---------------- end to end: pinned host inputs copied every step, loss read back every step
     barrier()
@@ -316,6 +327,7 @@ def run_nnt(args):
                                   f"embeddings/LM head are NEXT f1)",
                       "model": f"gpt2-{args.config}-blocks", "layers": L, "d_model": E, "heads": H,
                       "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}",
+                      "launch": "one CUDA graph per step" if use_graph else "eager launches",
                       "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
            "model_tflops": model_tflops, "model_tflops_frac_of_bf16": model_tflops / peaks["bf16"],
            "loss": loss, "gpu_launches": int(launches),
@@ -344,6 +356,7 @@ def main():
     ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="nnt", choices=["nnt", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -288,6 +288,9 @@ typedef struct {
   float bias_corr1;   /* 1 - beta1^t, computed by the caller in fp64, t >= 1    */
   float bias_corr2;   /* 1 - beta2^t                                            */
   float grad_scale;   /* g is multiplied by this first (1 = none)               */
+  /* device fp32 [2] = {bias_corr1, bias_corr2}, read by the kernel instead of the two
+   * scalars above when non-NULL (lets a captured CUDA graph advance the step count) */
+  const float* bias_corr_dev;
 } nnt_adam_hparams;
 
 /* m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; w -= lr (m/bc1) / (sqrt(v/bc2) + eps).
@@ -295,6 +298,12 @@ typedef struct {
  * shadow written as round-to-nearest-even(w_new); hp: host struct. */
 nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v, void* w_bf16,
                          const nnt_adam_hparams* hp, nnt_stream_t stream);
+
+/* Advances a device step counter and writes the Adam bias corrections for it:
+ * t_dev[0] += 1;  bias_corr_dev = {1 - beta1^t, 1 - beta2^t} computed in fp64 (R12).
+ * t_dev: device int64 [1]; bias_corr_dev: device fp32 [2] (pass it as
+ * nnt_adam_hparams.bias_corr_dev).  One thread; usable inside a captured CUDA graph. */
+nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias_corr_dev, nnt_stream_t stream);
 
 /* fp32 -> bf16 (round to nearest even) or bf16 -> fp32 conversion of n elements. */
 nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,

@@ -55,7 +55,9 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
                                                         float* __restrict__ v, __nv_bfloat16* __restrict__ w16,
                                                         nnt_adam_hparams hp, bool vec_ok) {
   const float b1 = hp.beta1, b2 = hp.beta2, c1 = 1.f - hp.beta1, c2 = 1.f - hp.beta2;
-  const float inv_bc1 = 1.f / hp.bias_corr1, inv_bc2 = 1.f / hp.bias_corr2;
+  const float bc1 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev) : hp.bias_corr1;
+  const float bc2 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev + 1) : hp.bias_corr2;
+  const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   auto upd = [&](float& wi, float gi, float& mi, float& vi) {
@@ -97,6 +99,15 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
     m[i] = mi;
     v[i] = vi;
     if (w16) w16[i] = __float2bfloat16_rn(wi);
+  }
+}
+
+__global__ void adam_tick_kernel(double beta1, double beta2, int64_t* t, float* bc) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int64_t s = t[0] + 1;
+    t[0] = s;
+    bc[0] = (float)(1.0 - pow(beta1, (double)s));
+    bc[1] = (float)(1.0 - pow(beta2, (double)s));
   }
 }
 
@@ -270,7 +281,7 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
                          const nnt_adam_hparams* hp, nnt_stream_t stream) {
   NNT_REQUIRE(w && g && m && v && hp, NNT_ERR_NULL, "nnt_adam_step: NULL pointer");
   NNT_REQUIRE(n >= 0, NNT_ERR_SHAPE, "nnt_adam_step: n=%lld", (long long)n);
-  NNT_REQUIRE(hp->bias_corr1 > 0.f && hp->bias_corr2 > 0.f, NNT_ERR_ARG,
+  NNT_REQUIRE(hp->bias_corr_dev || (hp->bias_corr1 > 0.f && hp->bias_corr2 > 0.f), NNT_ERR_ARG,
               "nnt_adam_step: bias corrections must be > 0 (t >= 1)");
   if (n == 0) return NNT_OK;
   bool vec = aligned16(w) && aligned16(g) && aligned16(m) && aligned16(v) &&
@@ -278,6 +289,14 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
   LaunchScope sc(NNT_K_ADAM, stream, (28.0 + (w_bf16 ? 2.0 : 0.0)) * n, 0);
   adam_kernel<<<grid_for(n / 4 + 1), kThreads, 0, stream>>>(n, w, g, m, v, (__nv_bfloat16*)w_bf16, *hp, vec);
   return check_launch("adam");
+}
+
+nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias_corr_dev, nnt_stream_t stream) {
+  NNT_REQUIRE(t_dev && bias_corr_dev, NNT_ERR_NULL, "nnt_adam_tick: NULL pointer");
+  NNT_REQUIRE(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0, NNT_ERR_ARG, "nnt_adam_tick: beta");
+  LaunchScope sc(NNT_K_ADAM, stream, 16.0, 0);
+  adam_tick_kernel<<<1, 32, 0, stream>>>(beta1, beta2, t_dev, bias_corr_dev);
+  return check_launch("adam_tick");
 }
 
 nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n, nnt_stream_t stream) {

@@ -66,6 +66,7 @@ struct TcParams {
   int tma_store;  // epilogue stores through TMA (C / aux / workspace maps valid)
   int order;      // TileOrder
   int ws_mode;    // split partials go to the workspace map; bias/beta/residual applied by the reduce
+  int in_kind;    // InKind: the epilogue input prefetched a chunk ahead (generic epilogue)
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -244,11 +245,44 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o, bool cg) {
   }
 }
 
+// One 128-byte row chunk of an epilogue input (W elements of TI) loaded through the
+// read-only path (the two 16-byte halves of a 32-byte sector share one L1 fill) one chunk
+// ahead of its use, unpacked 8 values at a time.
+struct Raw8 {
+  uint4 u[8];
+};
+__device__ __forceinline__ void raw_load(Raw8& r, const void* p) {
+  const uint4* src = reinterpret_cast<const uint4*>(p);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) r.u[i] = __ldg(src + i);
+}
+template <typename TI>
+__device__ __forceinline__ void unpack8(const Raw8& r, int j, float* t) {
+  if (sizeof(TI) == 4) {
+    const uint4 a = r.u[j / 4], b = r.u[j / 4 + 1];
+    t[0] = __uint_as_float(a.x); t[1] = __uint_as_float(a.y); t[2] = __uint_as_float(a.z); t[3] = __uint_as_float(a.w);
+    t[4] = __uint_as_float(b.x); t[5] = __uint_as_float(b.y); t[6] = __uint_as_float(b.z); t[7] = __uint_as_float(b.w);
+  } else {
+    const uint4 a = r.u[j / 8];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      float2 f = __bfloat1622float2(h[i]);
+      t[2 * i] = f.x;
+      t[2 * i + 1] = f.y;
+    }
+  }
+}
+// The streamed (prefetched) epilogue input of a GEMM: at most one, element type = C's.
+enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3 };
+
 // The W pre-activation outputs of one row chunk (GELU is applied by the caller after
 // staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
+// raw: the prefetched chunk of input `in_kind` (valid when vec and the chunk is full).
 template <typename TC, int W>
 __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const TC* auxb, int64_t row, int64_t col0,
-                                         bool extras, bool vec, float dval, float (&v)[W]) {
+                                         bool extras, bool vec, float dval, int in_kind, const Raw8& raw,
+                                         float (&v)[W]) {
   constexpr bool kFast = sizeof(TC) == 2;
 #pragma unroll
   for (int j = 0; j < W; ++j) v[j] *= g.alpha;
@@ -285,7 +319,10 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
     if (g.beta != 0.f) {
 #pragma unroll
       for (int j = 0; j < W; j += 8) {
-        ld8(Cb + row * g.ldc + col0 + j, t, true);
+        if (in_kind == IN_COLD)
+          unpack8<TC>(raw, j, t);
+        else
+          ld8(Cb + row * g.ldc + col0 + j, t, true);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[j + i] += g.beta * t[i];
       }
@@ -293,7 +330,10 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
     if (g.residual) {
 #pragma unroll
       for (int j = 0; j < W; j += 8) {
-        ld8(g.residual + row * g.ld_res + col0 + j, t, false);
+        if (in_kind == IN_RESIDUAL)
+          unpack8<float>(raw, j, t);
+        else
+          ld8(g.residual + row * g.ld_res + col0 + j, t, false);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[j + i] += t[i];
       }
@@ -301,7 +341,10 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
     if (g.act == NNT_ACT_GELU_BWD) {
 #pragma unroll
       for (int j = 0; j < W; j += 8) {
-        ld8(auxb + row * g.ld_aux + col0 + j, t, false);
+        if (in_kind == IN_AUX)
+          unpack8<TC>(raw, j, t);
+        else
+          ld8(auxb + row * g.ld_aux + col0 + j, t, false);
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_e<kFast>(t[i]);
       }
@@ -367,35 +410,6 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
 #pragma unroll
   for (int j = 0; j < W; ++j)
     if (col0 + j < N) base[row * ld + col0 + j] = from_f32<TC>(v[j]);
-}
-
-// 32 consecutive elements of TC (128 B fp32 / 64 B bf16) through the read-only path (the two
-// 16-byte halves of a 32-byte sector share one L1 fill), unpacked 8 at a time.
-struct Raw8 {
-  uint4 u[8];
-};
-template <typename TC>
-__device__ __forceinline__ void raw_load(Raw8& r, const void* p) {
-  const uint4* src = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-  for (int i = 0; i < 32 * (int)sizeof(TC) / 16; ++i) r.u[i] = __ldg(src + i);
-}
-template <typename TC>
-__device__ __forceinline__ void unpack8(const Raw8& r, int j, float* t) {
-  if (sizeof(TC) == 4) {
-    const uint4 a = r.u[j / 4], b = r.u[j / 4 + 1];
-    t[0] = __uint_as_float(a.x); t[1] = __uint_as_float(a.y); t[2] = __uint_as_float(a.z); t[3] = __uint_as_float(a.w);
-    t[4] = __uint_as_float(b.x); t[5] = __uint_as_float(b.y); t[6] = __uint_as_float(b.z); t[7] = __uint_as_float(b.w);
-  } else {
-    const uint4 a = r.u[j / 8];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 f = __bfloat1622float2(h[i]);
-      t[2 * i] = f.x;
-      t[2 * i + 1] = f.y;
-    }
-  }
 }
 
 // ------------------------------------------------------------------ kernel
@@ -543,14 +557,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int c_first = half * W;
       // EPI_DA: P row pointer of this lane and the prefetch of its first chunk
       const TC* prow = nullptr;
-      Raw8 raw_cur, raw_nxt;
+      Raw8 raw;  // P of the next chunk (128 bytes of this lane's row)
       float dval = 0.f;
       if constexpr (EPI == EPI_DA) {
         prow = (const TC*)g.aux + p * g.sc0 + q * g.sc1 + (int64_t)row_in * g.ld_aux + ti.n0;
-        if (row_ok && ti.n0 + c_first + W <= g.N) raw_load<TC>(raw_cur, prow + c_first);
-        if constexpr (W == 64) {
-          if (row_ok && ti.n0 + c_first + W <= g.N) raw_load<TC>(raw_nxt, prow + c_first + 32);
-        }
+        if (row_ok && ti.n0 + c_first + W <= g.N) raw_load(raw, prow + c_first);
         dval = row_ok ? __ldg(g.rowvec + ti.bz * g.M + row_in) : 0.f;
       }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
@@ -613,23 +624,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                 make_float2(m, s);
           }
         } else {
-          // dA = rowscale * P * (dP - D); P of this chunk was prefetched (raw_cur[, raw_nxt])
+          // dA = rowscale * P * (dP - D); P of this chunk was prefetched into raw
           const bool full = row_ok && col0 + W <= g.N;
           if (full) {
             float t[8];
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              unpack8<TC>(raw_cur, j, t);
+            for (int j = 0; j < W; j += 8) {
+              unpack8<TC>(raw, j, t);
 #pragma unroll
               for (int i = 0; i < 8; ++i) v[j + i] = g.rowscale * t[i] * (v[j + i] - dval);
-            }
-            if constexpr (W == 64) {
-#pragma unroll
-              for (int j = 0; j < 32; j += 8) {
-                unpack8<TC>(raw_nxt, j, t);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) v[32 + j + i] = g.rowscale * t[i] * (v[32 + j + i] - dval);
-              }
             }
           } else {
 #pragma unroll
@@ -638,10 +641,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           // prefetch the next chunk's P; it lands while this chunk is staged and stored
           const int cn = c + 2 * W;
-          if (cn < BN && row_ok && ti.n0 + cn + W <= g.N) {
-            raw_load<TC>(raw_cur, prow + cn);
-            if constexpr (W == 64) raw_load<TC>(raw_nxt, prow + cn + 32);
-          }
+          if (cn < BN && row_ok && ti.n0 + cn + W <= g.N) raw_load(raw, prow + cn);
         }
         // stage + TMA store (2-buffer ring per warp)
         uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
@@ -704,9 +704,22 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int64_t p = ti.bz / g.batch1, q = ti.bz % g.batch1;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
+      const int64_t row = ti.m0 + quad * 32 + lane;
+      // the streamed input (residual / GELU' aux / beta*C) of a chunk, prefetched one chunk ahead
+      auto in_ptr = [&](int c) -> const void* {
+        const int64_t col0 = ti.n0 + c;
+        if (P.in_kind == IN_AUX) return auxb + row * g.ld_aux + col0;
+        if (P.in_kind == IN_RESIDUAL) return g.residual + row * g.ld_res + col0;
+        return Cb + row * g.ldc + col0;
+      };
+      // (fp32 C only: a bf16 chunk already holds 64 live values, a prefetch buffer would spill)
+      auto can_stream = [&](int c) {
+        return sizeof(TC) == 4 && P.in_kind != IN_NONE && vec && row < g.M && c < BN && ti.n0 + c + W <= g.N;
+      };
+      Raw8 raw;
+      if (can_stream(half * W)) raw_load(raw, in_ptr(half * W));  // overlaps the wait for the MMAs
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
-      const int64_t row = ti.m0 + quad * 32 + lane;
       const bool has_k = ti.kb_end > ti.kb_begin;
       const float dval =
           (g.act == NNT_ACT_SOFTMAX_BWD && row < g.M) ? __ldg(g.rowvec + ti.bz * g.M + row) : 0.f;
@@ -726,11 +739,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
         if (P.ws_mode) {
           // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce kernel
-          epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, 0.f, v);
+          epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, 0.f, IN_NONE, raw, v);
           stage_and_store(&tmAux, v, true, cx, cy, (int)ti.split, 0);
           continue;
         }
-        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, v);
+        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, can_stream(c) ? P.in_kind : IN_NONE, raw, v);
+        if (can_stream(c + 2 * W)) raw_load(raw, in_ptr(c + 2 * W));  // next chunk's input, in flight meanwhile
         if (g.row_stats != nullptr && row < g.M) {
           // fused softmax subroutine 1: (max, sumexp) of this row over the chunk's
           // valid columns (W = 32 for fp32 C: one 32-column key tile)
@@ -911,6 +925,17 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.kb_per_split = cdiv(nkb, P.splits);
   P.num_tasks = P.num_tiles * P.splits;
   P.ws_mode = splits > 1 ? 1 : 0;
+  // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
+  if (P.ws_mode || EPI != EPI_GENERIC)
+    P.in_kind = IN_NONE;
+  else if (a.act == NNT_ACT_GELU_BWD)
+    P.in_kind = IN_AUX;
+  else if (a.residual && sizeof(TC) == 4)
+    P.in_kind = IN_RESIDUAL;
+  else if (a.beta != 0.f)
+    P.in_kind = IN_COLD;
+  else
+    P.in_kind = IN_NONE;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((P.b_kmajor ? 0u : 1u) << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
   CUtensorMap tmA, tmB, tmC, tmAux;

@@ -220,7 +220,10 @@ class BlockStack:
         """forward -> probe loss -> backward (+ DP all-reduce) -> Adam.  Returns the device loss tensor.
 
         x, r: [B,S,E] fp32, on this device or on the host (pinned host tensors are
-        copied asynchronously into the device input buffers first)."""
+        copied asynchronously into the device input buffers first).  After
+        enable_graph() the whole step is one CUDA-graph replay."""
+        if getattr(self, "graph", None) is not None:
+            return self._graph_step(x, r)
         if x is not None and x.device.type == "cpu":
             self.xs[0].copy_(x, non_blocking=True)
             x = None
@@ -237,4 +240,40 @@ class BlockStack:
         else:
             self.backward()
             self.adam()
+        return self.loss
+
+    # ------------------------------------------------------------ CUDA graph (single GPU)
+    def enable_graph(self):
+        """Capture one whole training step (Adam step counter advanced on the device, fp64
+        bias corrections, then forward, probe loss, backward, Adam) as a CUDA graph; later
+        train_step calls copy the batch into the static input buffers and replay it.  This
+        removes the host cost of ~500 launches (ctypes + TMA-descriptor encoding) per step."""
+        assert self.world == 1, "graph capture is single-GPU (the DP path stays eager)"
+        dev = self.dev
+        if not hasattr(self, "r_buf"):
+            self.r_buf = torch.empty_like(self.xs[0])
+        self.t_dev = torch.tensor([self.step_count], device=dev, dtype=torch.int64)
+        self.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
+        c = self.cfg
+        hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
+        hp.bias_corr_dev = self.bc_dev.data_ptr()
+        self._graph_hp = hp
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            nnt.nnt_adam_tick(c.beta1, c.beta2, self.t_dev, self.bc_dev)
+            self.forward()
+            self.probe_loss(self.r_buf)
+            self.backward()
+            nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16 if self.bf16 else None, hp)
+        self.graph = g
+        return g
+
+    def _graph_step(self, x, r):
+        if x is not None:
+            self.xs[0].copy_(x, non_blocking=True)
+        if r is not None:
+            self.r_buf.copy_(r, non_blocking=True)
+        self.graph.replay()
+        self.step_count += 1
         return self.loss

@@ -144,6 +144,29 @@ def test_bf16_first_query_pin():
     assert torch.equal(O[:, 0, :], qkv[:, 0, 2 * E:])
 
 
+def test_cuda_graph_step_equals_eager_bitwise():
+    """enable_graph(): a replayed step (device step counter + fp64 bias corrections) is bitwise
+    identical to the eager step, over 3 steps with changing inputs."""
+    E, H, S, B, L = 768, 12, 256, 2, 2
+    outs = []
+    for use_graph in (False, True):
+        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+        layers = [nnt_inputs.make_params(E, seed=9, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+        st = model.BlockStack(sc, layers)
+        if use_graph:
+            st.enable_graph()
+        losses = []
+        for t in range(3):
+            x = dev(nnt_inputs.make_x(E, S, 0, B, seed=50 + t))
+            r = dev(nnt_inputs.make_r(E, S, 0, B, seed=50 + t))
+            losses.append(st.train_step(x, r).item())
+        torch.cuda.synchronize()
+        outs.append((losses, st.w.clone(), st.m.clone(), st.v.clone()))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1:], outs[1][1:]):
+        assert torch.equal(a, b)
+
+
 def test_block_determinism_bitwise():
     sc, layers, st = _stack("tiny")
     c = nnt_inputs.CONFIGS["tiny"]
