@@ -57,6 +57,21 @@ def load_peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sus=1400.0, src="fallback")
 
 
+def load_traffic(config, kclass):
+    """DRAM bytes per launch of kclass from the newest committed one-step ncu capture
+    (profiles/r<NN>_traffic_<config>.json, written by tools/traffic.py)."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", f"r*_traffic_{config}.json")))
+    if not files:
+        return None, None
+    with open(files[-1]) as f:
+        d = json.load(f)
+    c = d["classes"].get(kclass)
+    if c is None:
+        return None, None
+    return c["dram_bytes_per_launch"], os.path.relpath(files[-1], ROOT) + ": " + d["source"]
+
+
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -262,11 +277,14 @@ def run_nnt(args):
     loss = float(st.loss.item())
 
     # ---------------- per-kernel timing (CUDA events around every libnnt launch), same kernels
-    # launched eagerly (events cannot be inserted into the replayed graph)
+    # launched eagerly (events cannot be inserted into the replayed graph).  A spin kernel queued
+    # ahead of each step lets the host enqueue the whole step before the GPU reaches it, so the
+    # start/stop events bracket device work only, not host launch latency.
     graph, st.graph = getattr(st, "graph", None), None
     nnt.nnt_timing_enable(True)
     for i in range(args.steps):
         x, r = dev_batches[i % 2]
+        torch.cuda._sleep(int(60e6))  # ~30 ms at 2 GHz, longer than one eager step's host enqueue
         st.train_step(x, r)
     torch.cuda.synchronize()
     kt = nnt.nnt_timing_read()
@@ -316,10 +334,11 @@ def run_nnt(args):
     d = kernels[dom]
     roof = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"],
             "peak": peaks["bf16_sus"] if d["bound"] == "tensor" else peaks["hbm"], "unit": d["unit"],
-            "frac": d["frac"], "traffic": None, "peak_source": peaks["src"] +
+            "frac": d["frac"], "traffic": None, "traffic_source": None, "peak_source": peaks["src"] +
             (" bf16_tflops_sustained (kernel timed inside a long step)" if d["bound"] == "tensor" else " hbm_gbs"),
             "timing": "CUDA events around every launch on its stream, K steps after the timed region",
             "share_of_step": d["share"]}
+    roof["traffic"], roof["traffic_source"] = load_traffic(args.config, dom)
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded N(0,1) activations, GPT-2 init weights)",

@@ -108,7 +108,19 @@ typedef enum {
   /* Softmax backward fused into the dP = dO V^T GEMM (R18 with D from the dO.O identity):
    * C <- rowscale * aux * (pre - rowvec[item*M + i]); aux = P (same dtype, batch strides and
    * ld as C), rowvec = D (fp32), rowscale = 1/sqrt(h).  bf16 path only. */
-  NNT_ACT_SOFTMAX_BWD = 3
+  NNT_ACT_SOFTMAX_BWD = 3,
+  /* SoftMax subroutine 1 over whole rows, fused into the score GEMM (R26):
+   * x = alpha*acc is never stored (C must be NULL); row_stats[(p*batch1 + q)*M + i] receives
+   * (max_j x_ij, sum_j e^{x_ij - max}) over the row's valid columns (j <= i when causal ==
+   * NNT_CAUSAL_OUT_LOWER).  One task owns all key tiles of a 128-row block, so the per-tile
+   * partials are aggregated on chip.  bf16 operands; no bias / residual / beta. */
+  NNT_ACT_ROWSTATS = 4,
+  /* SoftMax subroutine 2 fused into a recomputation of the score GEMM (R26):
+   * C = e^{alpha*acc - M_i} / S_i with (M_i, S_i) = row_stats[(p*batch1 + q)*M + i] (input, as
+   * written by NNT_ACT_ROWSTATS).  causal == NNT_CAUSAL_OUT_LOWER: entries j > i are written
+   * as 0 up to column roundup(i+1, NNT_CAUSAL_ALIGN) and not written beyond (nnt_softmax's
+   * extents).  bf16 operands, bf16 C; no bias / residual / beta. */
+  NNT_ACT_SOFTMAX = 5
 } nnt_act;
 
 typedef struct {
@@ -129,7 +141,9 @@ typedef struct {
    * (m_g, s_g) = (max, sum e^{x - m_g}) of x = alpha*acc over the tile's valid columns
    * (col <= row when causal == NNT_CAUSAL_OUT_LOWER; (-inf, 0) if none) is written to
    * row_stats[((p*batch1 + q)*M + row)*ld_row_stats + g] as two floats.  Merged by
-   * nnt_maxsumexp_merge.  NULL = off. */
+   * nnt_maxsumexp_merge.  NULL = off.
+   * With act NNT_ACT_ROWSTATS / NNT_ACT_SOFTMAX: one (max, sumexp) pair per output row (output /
+   * input respectively, see nnt_act); ld_row_stats is ignored. */
   float* row_stats;
   int64_t ld_row_stats;   /* in (max, sumexp) pairs, >= ceil(N / 32) */
   const float* rowvec;    /* NNT_ACT_SOFTMAX_BWD: per-row D, indexed (p*batch1 + q)*M + i */
@@ -424,6 +438,12 @@ nnt_status nnt_timing_enable(int enable);
  * device time in ms, the launch count and the summed algorithmic bytes and flops
  * (host arrays of length NNT_K_COUNT; any may be NULL). */
 nnt_status nnt_timing_read(double* ms, int64_t* launches, double* bytes, double* flops);
+/* The recorded launch scopes in issue order: kclass[i] (nnt_kernel_class) and
+ * kernels[i] (kernels the scope launched, e.g. 2 for a split-K GEMM + its ordered
+ * reduce), for i < min(cap, *n); *n receives the total count.  Host arrays, may be
+ * NULL when cap == 0.  Lets a profiler's per-kernel list (ncu) be attributed to
+ * kernel classes. */
+nnt_status nnt_timing_trace(int32_t* kclass, int32_t* kernels, int64_t cap, int64_t* n);
 /* Number of kernels this library launched since load (all classes). */
 int64_t nnt_launch_count(void);
 

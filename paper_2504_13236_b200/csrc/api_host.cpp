@@ -38,6 +38,7 @@ struct TimingRecord {
   int kclass;
   cudaEvent_t start, stop;
   double bytes, flops;
+  int kernels;
 };
 std::mutex g_tmu;
 bool g_timing = false;
@@ -62,10 +63,17 @@ LaunchScope::LaunchScope(int kclass, cudaStream_t s, double bytes, double flops,
   g_launches.fetch_add(kernels, std::memory_order_relaxed);
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);
-  TimingRecord r{kclass, take_event(), take_event(), bytes, flops};
+  TimingRecord r{kclass, take_event(), take_event(), bytes, flops, kernels};
   cudaEventRecord(r.start, s);
   slot_ = (int)g_records.size();
   g_records.push_back(r);
+}
+
+void LaunchScope::add_kernels(int k) {
+  g_launches.fetch_add(k, std::memory_order_relaxed);
+  if (slot_ < 0) return;
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_records[slot_].kernels += k;
 }
 
 LaunchScope::~LaunchScope() {
@@ -157,6 +165,18 @@ nnt_status nnt_timing_read(double* ms, int64_t* launches, double* bytes, double*
     if (launches) launches[r.kclass] += 1;
     if (bytes) bytes[r.kclass] += r.bytes;
     if (flops) flops[r.kclass] += r.flops;
+  }
+  return NNT_OK;
+}
+
+nnt_status nnt_timing_trace(int32_t* kclass, int32_t* kernels, int64_t cap, int64_t* n) {
+  NNT_REQUIRE(n, NNT_ERR_NULL, "nnt_timing_trace: NULL count");
+  NNT_REQUIRE(cap >= 0 && (cap == 0 || (kclass && kernels)), NNT_ERR_NULL, "nnt_timing_trace: NULL arrays");
+  std::lock_guard<std::mutex> lk(g_tmu);
+  *n = (int64_t)g_records.size();
+  for (int64_t i = 0; i < cap && i < *n; ++i) {
+    kclass[i] = g_records[i].kclass;
+    kernels[i] = g_records[i].kernels;
   }
   return NNT_OK;
 }

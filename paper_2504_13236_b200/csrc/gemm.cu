@@ -111,5 +111,8 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     return gemm_simt_launch(g, stream);
   }
   LaunchScope sc(b0 * b1 > 1 ? NNT_K_GEMM_TC_ATTN : NNT_K_GEMM_TC, stream, bytes, flops);
-  return gemm_tc_launch(g, stream);
+  int kernels = 1;
+  const nnt_status st = gemm_tc_launch(g, stream, &kernels);
+  if (kernels > 1) sc.add_kernels(kernels - 1);
+  return st;
 }

@@ -34,7 +34,8 @@ struct GemmArgs {
 };
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);
-nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s);
+// *kernels (optional) receives the number of kernels launched (2 with a split-K reduce).
+nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels = nullptr);
 int64_t gemm_tc_splits(const GemmArgs& a);  // split-K factor the tcgen05 path would use
 
 // Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.

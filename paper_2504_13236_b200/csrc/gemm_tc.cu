@@ -41,10 +41,12 @@ constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for 
 constexpr int kStageBufs = 2;             // staging ring per epilogue warp (one store in flight while refilling)
 constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory per CTA
 
-template <int BN>
+// CG = CTAs per MMA (tcgen05 cta_group): 1, or 2 = an SM pair computing a 256 x BN tile
+// (each CTA stages its 128 A rows and half of the BN B rows; the leader issues M=256 MMAs).
+template <int BN, int CG = 1>
 struct Cfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * kStageBufs * kStageBytesPerWarp;
   static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE_BYTES;
@@ -108,6 +110,32 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t sr
                "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
                : "memory");
 }
+// CTA-pair (cta_group::2) variants: the TMA completes bytes on the leader CTA's mbarrier
+// (shared::cluster address), MMA completion is multicast to the same barrier of both CTAs.
+__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                 int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -127,6 +155,21 @@ __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
@@ -160,7 +203,10 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
 struct TileInfo {
   int64_t tile, bz, m0, n0, kb_begin, kb_end, split;
 };
-__device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, int bn) {
+// bm_tile: output rows per task (BM, or 2*BM for a CTA pair); row_off: this CTA's first row
+// within the task's tile (CTA-pair rank * BM).  Causal orders are single-CTA only.
+__device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, int bn, int bm_tile = BM,
+                                                int row_off = 0) {
   TileInfo ti;
   ti.split = t % P.splits;
   ti.tile = t / P.splits;
@@ -186,7 +232,7 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
     ti.bz = r / P.nt;
     nb = r % P.nt;
   }
-  ti.m0 = mb * BM;
+  ti.m0 = mb * bm_tile + row_off;
   ti.n0 = nb * bn;
   int64_t k_begin = 0, k_end = P.g.K;
   if (P.g.causal == NNT_CAUSAL_A_LOWER) k_end = min(P.g.K, ti.m0 + BM);
@@ -421,12 +467,18 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
 //                chunk ahead
 enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2 };
 
-template <int BN, typename TC, int EPI>
+// CG = 2: launched as clusters of 2 CTAs (an SM pair).  Task = 256 x BN output tile; rank r
+// stages A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) and drains its own TMEM
+// (rows m0 + 128 r ..); the leader (rank 0) waits for both halves on its full barrier
+// (expect_tx of both CTAs' bytes) and issues the M=256 MMAs; the peer's epilogue warps arrive
+// on the leader's TMEM-empty barrier.
+template <int BN, typename TC, int EPI, int CG = 1>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
                    const __grid_constant__ CUtensorMap tmAux) {
-  using C = Cfg<BN>;
+  static_assert(CG == 1 || (CG == 2 && EPI == EPI_GENERIC && (BN / 2) % 64 == 0), "CTA-pair configuration");
+  using C = Cfg<BN, CG>;
   constexpr int W = 128 / (int)sizeof(TC);  // columns per 128-byte staging row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -439,6 +491,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = P.g;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+  const int row_off = (int)rank * BM;
+  const int64_t task0 = blockIdx.x / CG, task_step = gridDim.x / CG;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -447,20 +502,30 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&tfull[s]), 1);
-      mbar_init(smem_u32(&tempty[s]), kEpiWarps);
+      mbar_init(smem_u32(&tempty[s]), kEpiWarps * CG);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CG == 2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive / complete_tx
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -469,27 +534,47 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
-        TileInfo ti = decode_task(P, t, BN);
+      for (int64_t t = task0; t < P.num_tasks; t += task_step) {
+        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
         const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
+        const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-          const uint32_t fb = smem_u32(&full[stage]);
-          mbar_expect_tx(fb, C::STAGE_BYTES);
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
           const int k0 = (int)(kb * BK);
-          if (P.a_kmajor) {
-            tma_load_4d(sa, &tmA, fb, k0, (int)ti.m0, q, p);
-          } else {
+          if constexpr (CG == 2) {
+            const uint32_t fb_local = smem_u32(&full[stage]);
+            if (rank == 0) mbar_expect_tx(fb_local, CG * C::STAGE_BYTES);
+            const uint32_t fb = map_to_rank(fb_local, 0);
+            if (P.a_kmajor) {
+              tma_load_4d_pair(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j) tma_load_4d(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
-          }
-          if (P.b_kmajor) {
-            tma_load_4d(sb, &tmB, fb, k0, (int)ti.n0, q, p);
-          } else {
+              for (int j = 0; j < BM / 64; ++j)
+                tma_load_4d_pair(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
+            }
+            if (P.b_kmajor) {
+              tma_load_4d_pair(sb, &tmB, fb, k0, nb0, q, p);
+            } else {
 #pragma unroll
-            for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, fb, (int)ti.n0 + 64 * j, k0, q, p);
+              for (int j = 0; j < BN / CG / 64; ++j) tma_load_4d_pair(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
+            }
+          } else {
+            const uint32_t fb = smem_u32(&full[stage]);
+            mbar_expect_tx(fb, C::STAGE_BYTES);
+            if (P.a_kmajor) {
+              tma_load_4d(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BM / 64; ++j) tma_load_4d(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
+            }
+            if (P.b_kmajor) {
+              tma_load_4d(sb, &tmB, fb, k0, (int)ti.n0, q, p);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, fb, (int)ti.n0 + 64 * j, k0, q, p);
+            }
           }
           if (++stage == C::STAGES) {
             stage = 0;
@@ -499,8 +584,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // ===================== MMA issuer
-    if (lane == 0) {
+    // ===================== MMA issuer (CTA pair: the leader only)
+    if (lane == 0 && rank == 0) {
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -510,8 +595,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // apart; +2 KB per UMMA_K=16.
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
-      for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
-        TileInfo ti = decode_task(P, t, BN);
+      for (int64_t t = task0; t < P.num_tasks; t += task_step) {
+        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -524,15 +609,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int kk = 0; kk < BK / 16; ++kk) {
             uint64_t ad = make_sdesc(sa + kk * a_step, a_lbo, 1024u);
             uint64_t bd = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
-            mma_bf16(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+            if constexpr (CG == 2)
+              mma_bf16_pair(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+            else
+              mma_bf16(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
           }
-          mma_commit(smem_u32(&empty[stage]));
+          if constexpr (CG == 2)
+            mma_commit_pair(smem_u32(&empty[stage]));
+          else
+            mma_commit(smem_u32(&empty[stage]));
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        mma_commit(smem_u32(&tfull[acc]));
+        if constexpr (CG == 2)
+          mma_commit_pair(smem_u32(&tfull[acc]));
+        else
+          mma_commit(smem_u32(&tfull[acc]));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -548,7 +642,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float L2E = 1.4426950408889634f;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
+    for (int64_t t = task0; t < P.num_tasks; t += task_step) {
       TileInfo ti = decode_task(P, t, BN);
       const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
       const int row_in = (int)ti.m0 + quad * 32 + lane;  // row of this lane within the batch item
@@ -699,8 +793,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      (g.sc1 * cs) % 16 == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = blockIdx.x; t < P.num_tasks; t += gridDim.x) {
-      TileInfo ti = decode_task(P, t, BN);
+    for (int64_t t = task0; t < P.num_tasks; t += task_step) {
+      TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
       const int64_t p = ti.bz / g.batch1, q = ti.bz % g.batch1;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
@@ -779,7 +873,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&tempty[acc]));
+      if (lane == 0) {
+        if constexpr (CG == 2)
+          mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[acc]), 0));  // the leader's MMA waits on it
+        else
+          mbar_arrive(smem_u32(&tempty[acc]));
+      }
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -789,12 +888,20 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync_all();  // neither CTA frees TMEM / exits while the pair's MMAs or arrivals are pending
+  else
+    __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"((uint32_t)C::TMEM_COLS)
-                 : "memory");
+    if constexpr (CG == 2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "r"((uint32_t)C::TMEM_COLS)
+                   : "memory");
   }
 }
 
@@ -894,13 +1001,44 @@ bool c_tma_ok(const GemmArgs& a, size_t es) {
          (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
 }
 
-template <int BN, typename TC, int EPI>
+// Persistent CTA-pair grid: as many clusters of 2 as can be co-resident at one CTA per SM
+// (pairs are formed within a GPC, so fewer than num_sms/2 when GPCs hold odd SM counts).  A
+// pair that is not resident would run its whole static task list after the others finish.
+int64_t pair_units() {
+  static int64_t units = 0;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    using Cq = Cfg<256, 2>;
+    auto kern = gemm_tc_kernel<256, float, EPI_GENERIC, 2>;
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cq::SMEM_BYTES) == cudaSuccess) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3((unsigned)(num_sms() / 2 * 2));
+      q.blockDim = dim3(kThreads);
+      q.dynamicSmemBytes = Cq::SMEM_BYTES;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      q.attrs = attr;
+      q.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) n = 0;
+    }
+    (void)cudaGetLastError();
+    units = n > 0 ? n : num_sms() / 2;
+    if (getenv("NNT_DEBUG_GEMM")) fprintf(stderr, "gemm_tc: %lld co-resident CTA pairs (query %d)\n", (long long)units, n);
+  });
+  return units;
+}
+
+template <int BN, typename TC, int EPI, int CG = 1>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, CG>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES);
   });
   NNT_REQUIRE(attr_err == cudaSuccess, NNT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -909,7 +1047,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.g = a;
   P.a_kmajor = a.ta == NNT_NOTRANS;
   P.b_kmajor = a.tb == NNT_TRANS;
-  P.mt = cdiv(a.M, BM);
+  P.mt = cdiv(a.M, BM * CG);
   P.nt = cdiv(a.N, BN);
   if (a.causal == NNT_CAUSAL_OUT_LOWER && BN == BM && P.mt == P.nt) {
     P.order = ORDER_TRI;
@@ -937,7 +1075,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   else
     P.in_kind = IN_NONE;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((P.b_kmajor ? 0u : 1u) << 16) |
-            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
   CUtensorMap tmA, tmB, tmC, tmAux;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (P.a_kmajor)
@@ -945,7 +1083,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   else
     NNT_TRY(make_map(&tmA, bf, 2, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, 64, BK));
   if (P.b_kmajor)
-    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN));
+    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN / CG));
   else
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
   const size_t es = sizeof(TC);
@@ -970,9 +1108,29 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
         NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
     }
   }
-  int64_t grid = P.num_tasks < num_sms() ? P.num_tasks : num_sms();
-  if (grid < 1) grid = 1;
-  gemm_tc_kernel<BN, TC, EPI><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
+  if constexpr (CG == 1) {
+    const int64_t units = num_sms();  // persistent: one CTA per SM
+    int64_t grid = P.num_tasks < units ? P.num_tasks : units;
+    if (grid < 1) grid = 1;
+    gemm_tc_kernel<BN, TC, EPI, 1><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const int64_t max_clusters = pair_units();
+    int64_t grid = P.num_tasks < max_clusters ? P.num_tasks : max_clusters;
+    if (grid < 1) grid = 1;
+    cfg.gridDim = dim3((unsigned)(grid * CG));
+    NNT_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, TC, EPI, CG>, P, tmA, tmB, tmC, tmAux));
+  }
   NNT_TRY(check_launch("gemm_tc"));
   if (P.ws_mode) {
     const int64_t total = a.M * (a.N / 4);
@@ -987,7 +1145,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
 
 // Tile width from a wave model: time ~ ceil(tiles / SMs) * BN (per-tile time ~ BN at fixed
 // BM, K); ties go to the wider tile (more operand reuse per byte of L2 traffic).
-int choose_bn(const GemmArgs& a) {
+int choose_bn(const GemmArgs& a, double* cost_out = nullptr) {
+  if (cost_out) *cost_out = 1e300;
   if (a.N <= 64) return 64;
   if (a.causal == NNT_CAUSAL_OUT_LOWER) return 128;
   const int64_t sms = num_sms(), mt = cdiv(a.M, BM), nb = a.batch0 * a.batch1;
@@ -1002,6 +1161,39 @@ int choose_bn(const GemmArgs& a) {
       best = bn;
     }
   }
+  if (cost_out) *cost_out = best_cost;
+  return best;
+}
+
+// CTA pairs (cta_group::2, 256-row tiles) for the plain projection-type GEMMs: unbatched,
+// non-causal, generic epilogue.  NNT_GEMM_CG=1 in the environment forces single-CTA tiles.
+bool use_pair(const GemmArgs& a) {
+  static const int forced = [] {
+    const char* e = getenv("NNT_GEMM_CG");
+    return e ? atoi(e) : 0;
+  }();
+  if (forced == 1) return false;
+  return a.batch0 * a.batch1 == 1 && a.causal == NNT_CAUSAL_NONE && a.M >= 2 * BM && a.N > 64 &&
+         num_sms() >= 2;
+}
+
+// Wave model over SM pairs; widths whose half is a whole 64-column MN-major block.
+// (per-SM time of a 256 x BN pair tile ~ that of a 128 x BN single tile, so the costs compare
+// directly with choose_bn's)
+int choose_bn_pair(const GemmArgs& a, double* cost_out) {
+  const int64_t units = pair_units(), mt = cdiv(a.M, 2 * BM);
+  const int cands[2] = {256, 128};
+  int best = 256;
+  double best_cost = 1e300;
+  for (int bn : cands) {
+    const int64_t tiles = mt * cdiv(a.N, bn);
+    const double cost = (double)cdiv(tiles, units) * bn * (1.0 + 0.02 * (256 - bn) / 64.0);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  *cost_out = best_cost;
   return best;
 }
 
@@ -1015,6 +1207,14 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
         (a.row_stats || a.causal == NNT_CAUSAL_OUT_LOWER))
       return launch_bn<128, TC, EPI_SCORES>(a, s, 1);
   }
+  if (use_pair(a)) {
+    double cost_pair = 0, cost_single = 0;
+    const int bnp = choose_bn_pair(a, &cost_pair);
+    choose_bn(a, &cost_single);
+    if (splits > 1 || cost_pair <= cost_single)  // ties go to pairs (half the operand loads per SM)
+      return bnp == 256 || splits > 1 ? launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits)
+                                      : launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+  }
   switch (splits > 1 ? 256 : choose_bn(a)) {
     case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
     case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
@@ -1025,7 +1225,7 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
 
 }  // namespace
 
-nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s) {
+nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
   // TMA: 16-byte aligned base, 16-byte multiple strides (bf16: multiples of 8 elements).
   NNT_REQUIRE(aligned16(a.A) && aligned16(a.B), NNT_ERR_ALIGN, "gemm(bf16): A/B must be 16-byte aligned");
   NNT_REQUIRE(a.lda % 8 == 0 && a.ldb % 8 == 0, NNT_ERR_ALIGN, "gemm(bf16): lda/ldb must be multiples of 8");
@@ -1041,6 +1241,7 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s) {
                      (!a.residual || ((reinterpret_cast<uintptr_t>(a.residual) & 15u) == 0 && a.ld_res % 4 == 0)) &&
                      (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);
   if (!ws_ok) splits = 1;
+  if (kernels) *kernels = splits > 1 ? 2 : 1;
   if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits);
   return launch_tc<__nv_bfloat16>(a, s, splits);
 }

@@ -63,6 +63,7 @@ inline bool valid_dtype(int dt) { return dt == NNT_F32 || dt == NNT_BF16; }
 struct LaunchScope {
   LaunchScope(int kclass, cudaStream_t s, double bytes, double flops, int kernels = 1);
   ~LaunchScope();
+  void add_kernels(int k);  // the scope launched k more kernels than declared (decided inside)
   int kclass_;
   cudaStream_t s_;
   int slot_;

@@ -46,7 +46,8 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick",
            "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
-           "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_launch_count")
+           "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
+           "nnt_launch_count")
 
 
 class NNTError(RuntimeError):
@@ -134,6 +135,7 @@ _sig = {
                                       C.POINTER(nnt_launch_group), _i64, _P64]),
     "nnt_timing_enable": (_i32, [_i32]),
     "nnt_timing_read": (_i32, [C.POINTER(C.c_double), _P64, C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "nnt_timing_trace": (_i32, [C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i64, _P64]),
     "nnt_launch_count": (_i64, []),
 }
 for _name, (_res, _args) in _sig.items():
@@ -354,6 +356,15 @@ def nnt_timing_read():
     ms, cnt, by, fl = (C.c_double * n)(), (C.c_int64 * n)(), (C.c_double * n)(), (C.c_double * n)()
     check(lib.nnt_timing_read(ms, cnt, by, fl))
     return {KERNEL_CLASSES[i]: dict(ms=ms[i], launches=cnt[i], bytes=by[i], flops=fl[i]) for i in range(n)}
+
+
+def nnt_timing_trace():
+    """[(kernel class name, kernels launched)] for every recorded launch scope, in issue order."""
+    n = C.c_int64()
+    check(lib.nnt_timing_trace(None, None, 0, C.byref(n)))
+    kc, kn = (C.c_int32 * max(n.value, 1))(), (C.c_int32 * max(n.value, 1))()
+    check(lib.nnt_timing_trace(kc, kn, n.value, C.byref(n)))
+    return [(KERNEL_CLASSES[kc[i]], kn[i]) for i in range(n.value)]
 
 
 def nnt_launch_count():

@@ -68,8 +68,9 @@ def test_gemm_bf16_output_rounding_exact(ta, tb):
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
-def test_gemm_epilogues(dtype):
-    M, N, K = 192, 320, 256
+@pytest.mark.parametrize("M", [192, 640])  # 640: bf16 runs on CTA pairs (256-row tiles, ragged last pair)
+def test_gemm_epilogues(dtype, M):
+    N, K = 320, 256
     rng = np.random.default_rng(5)
     a = rng.standard_normal((M, K)).astype(np.float32) / 8
     b = rng.standard_normal((N, K)).astype(np.float32) / 8
@@ -172,9 +173,25 @@ def test_gemm_split_k_workspace_bit_exact(M, N):
     assert np.array_equal(outs[0], outs[1])
 
 
+@pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(512, 384, 256), (296, 200, 136), (1000, 520, 72), (2048, 2304, 128)])
+def test_gemm_cta_pair_bit_exact(ta, tb, shape):
+    """Unbatched non-causal bf16 GEMMs with M >= 256 run on CTA pairs (tcgen05 cta_group::2, M=256
+    MMAs, each CTA staging half of the B tile): both operand majors, ragged M/N/K tails (a pair whose
+    second CTA lies wholly past M), BN = 128 and 256 pair tiles."""
+    M, N, K = shape
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + N + 1, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=M + 2 * N, kind="int")
+    want = tiled.gemm_tiled(_op(a, ta), _op(b, tb), 64, 64, 64)
+    got = host(_run("bf16", ta, tb, M, N, K, a, b))
+    assert np.array_equal(got, want), f"max |diff| {np.abs(got - want).max()}"
+    gotb = host(_run("bf16", ta, tb, M, N, K, a, b, c_dtype="bf16"))
+    assert np.array_equal(gotb, bf16_round(want))
+
+
 @pytest.mark.parametrize("N", [768, 3072])
 def test_gemm_wave_model_tile_widths_bit_exact(N):
-    """M = 8192 rows with N = 768 / 3072 select BN = 192 tiles (wave model)."""
+    """M = 8192 rows with N = 768 / 3072: wave-model tile widths on CTA pairs."""
     M, K = 8192, 256
     a = nnt_inputs.make_matrix((M, K), seed=N, kind="int")
     b = nnt_inputs.make_matrix((N, K), seed=N + 1, kind="int")

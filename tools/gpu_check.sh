@@ -7,6 +7,10 @@ timeout 400 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.log 2>&1; t
 timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
    --log-file gpurun_out/launches.csv python tools/profile_step.py > gpurun_out/ncu_list.log 2>&1
 tail -3 gpurun_out/ncu_list.log
+timeout 600 ncu --profile-from-start off --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
+   --clock-control none --csv --log-file gpurun_out/traffic.csv python tools/profile_step.py --trace gpurun_out/trace.json \
+   > gpurun_out/ncu_traffic.log 2>&1
+python tools/traffic.py gpurun_out/traffic.csv gpurun_out/trace.json gpurun_out/traffic_small.json
 if [ -n "$NCU_FULL" ]; then
   timeout 900 ncu --profile-from-start off --set full --import-source on --clock-control none \
      -k "regex:$NCU_FULL" -c ${NCU_COUNT:-4} -o gpurun_out/prof_full -f python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1

@@ -4,6 +4,7 @@
     python tools/profile_step.py [--config small] [--warmup 2]
 """
 import argparse
+import json
 import os
 import sys
 
@@ -14,7 +15,7 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import nnt_inputs  # noqa: E402
-from paper_2504_13236_b200 import model  # noqa: E402
+from paper_2504_13236_b200 import model, nnt  # noqa: E402
 
 
 def main():
@@ -22,6 +23,7 @@ def main():
     ap.add_argument("--config", default="small")
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--trace", default=None, help="write the step's launch-scope trace (class, kernels) here")
     a = ap.parse_args()
     L, E, H, S, B = bench.CONFIGS[a.config]
     L = a.layers or L
@@ -33,10 +35,16 @@ def main():
     for _ in range(a.warmup):
         st.train_step(x, r)
     torch.cuda.synchronize()
+    if a.trace:
+        nnt.nnt_timing_enable(True)
     torch.cuda.cudart().cudaProfilerStart()
     st.train_step(x, r)
     torch.cuda.synchronize()
     torch.cuda.cudart().cudaProfilerStop()
+    if a.trace:
+        with open(a.trace, "w") as f:
+            json.dump(nnt.nnt_timing_trace(), f)
+        nnt.nnt_timing_enable(False)
     print("profiled one step; loss", st.loss.item())
 
 
