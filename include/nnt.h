@@ -113,7 +113,7 @@ typedef enum {
    * x = alpha*acc is never stored (C must be NULL); row_stats[(p*batch1 + q)*M + i] receives
    * (max_j x_ij, sum_j e^{x_ij - max}) over the row's valid columns (j <= i when causal ==
    * NNT_CAUSAL_OUT_LOWER).  One task owns all key tiles of a 128-row block, so the per-tile
-   * partials are aggregated on chip.  bf16 operands; no bias / residual / beta. */
+   * partials are aggregated on chip.  bf16 operands, alpha > 0; no bias / residual / beta. */
   NNT_ACT_ROWSTATS = 4,
   /* SoftMax subroutine 2 fused into a recomputation of the score GEMM (R26):
    * C = e^{alpha*acc - M_i} / S_i with (M_i, S_i) = row_stats[(p*batch1 + q)*M + i] (input, as

@@ -15,7 +15,7 @@ struct Layout {
   // saved (per layer)
   size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
   // scratch
-  size_t scores, spart, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
+  size_t scores, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
   size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes;
 };
 
@@ -46,9 +46,8 @@ Layout make_layout(const nnt_block_cfg& c) {
   L.g = take(dt * T * F);
   L.saved_bytes = o;
   o = 0;
-  L.scores = take(4 * B * H * S * S);
-  // bf16 path: per (slice, 32-key tile) (max, sumexp) partials from the score GEMM epilogue
-  L.spart = take(c.dtype == NNT_BF16 ? 8 * B * H * S * ((S + 31) / 32) : 0);
+  // fp32 path: the materialised scores; the bf16 path keeps score tiles on chip (R26)
+  L.scores = take(c.dtype == NNT_BF16 ? 0 : 4 * B * H * S * S);
   L.dvec = take(c.dtype == NNT_BF16 ? 4 * B * H * S : 0);  // D = rowdot(dO, O) (bf16 path)
   L.dy16 = take(dt * T * E);
   L.du = take(dt * T * F);
@@ -133,21 +132,32 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       const size_t es = dt == NNT_BF16 ? 2 : 4;
       const int64_t sq[2] = {S * 3 * E, Dh}, ssc[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
-      if (dt == NNT_BF16) {  // softmax subroutine 1 per 32-key tile fused into the epilogue
-        e.row_stats = x.k<float>(x.L.spart);
-        e.ld_row_stats = (S + 31) / 32;
-      }
       uint8_t* q = x.s<uint8_t>(x.L.qkv);
+      if (dt == NNT_BF16) {
+        // R26: the score tiles stay on chip; subroutine 1 and its aggregation over all key tiles
+        // of a row run in the GEMM epilogue, producing the slice stats directly
+        e.act = NNT_ACT_ROWSTATS;
+        e.row_stats = x.s<float>(x.L.stats);
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + es * E, 3 * E, sq,
+                    0.f, nullptr, NNT_F32, S, ssc, &e);
+      }
       return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + es * E, 3 * E, sq, 0.f,
                   x.k<float>(x.L.scores), NNT_F32, S, ssc, &e);
     }
-    case NNT_OP_MAXSUMEXP:
-      if (dt == NNT_BF16)  // aggregate the per-tile partials the score GEMM produced
-        return nnt_maxsumexp_merge(x.k<float>(x.L.spart), B * H * S, (S + 31) / 32, (S + 31) / 32, 32, x.c.causal,
-                                   S, x.s<float>(x.L.stats), x.st);
+    case NNT_OP_MAXSUMEXP:  // fp32 path only (the bf16 path fuses it into NNT_OP_SCORES)
       return nnt_maxsumexp(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S,
                            x.s<float>(x.L.stats), 0, x.st);
     case NNT_OP_SOFTMAX:
+      if (dt == NNT_BF16) {
+        // R26: subroutine 2 on recomputed score tiles (same MMA order as the stats pass), P in bf16
+        const int64_t sq[2] = {S * 3 * E, Dh}, sp[2] = {H * S * S, S * S};
+        e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
+        e.act = NNT_ACT_SOFTMAX;
+        e.row_stats = x.s<float>(x.L.stats);
+        uint8_t* q = x.s<uint8_t>(x.L.qkv);
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + 2 * E, 3 * E, sq,
+                    0.f, x.s<void>(x.L.P), dt, S, sp, &e);
+      }
       return nnt_softmax(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S, x.s<float>(x.L.stats),
                          x.s<void>(x.L.P), dt, S, x.st);
     case NNT_OP_PV: {

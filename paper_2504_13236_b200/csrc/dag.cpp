@@ -353,30 +353,41 @@ void build_fwd(StfGraph& g, const Shapes& s) {
           Acc a;
           t.qkv.region(g, ag.row0(b, qi), ag.row1(b, qi), ag.col0(0, h), ag.col1(0, h), ACC_R, a);
           t.qkv.region(g, ag.row0(b, kj), ag.row1(b, kj), ag.col0(1, h), ag.col1(1, h), ACC_R, a);
-          a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_W);
+          if (s.bf16)  // R26: score tile kept on chip, its subroutine-1 partial Reduced into the stats
+            a.emplace_back(t.stats.h(g, b, h, qi), ACC_REDUCE);
+          else
+            a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_W);
           int64_t tl[3] = {b * s.H + h, qi, kj};
           g.submit(NNT_OP_SCORES, tl, a);
         }
   // softmax subroutine 1: per key tile partial, Reduce into the slice stats
+  // (bf16 path: fused into NNT_OP_SCORES above)
+  if (!s.bf16)
+    for (int64_t b = 0; b < s.B; ++b)
+      for (int64_t h = 0; h < s.H; ++h)
+        for (int64_t qi = 0; qi < ag.nq; ++qi)
+          for (int64_t kj = 0; kj < ag.nq; ++kj) {
+            if (!ag.needed(qi, kj)) continue;
+            Acc a;
+            a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_R);
+            a.emplace_back(t.stats.h(g, b, h, qi), ACC_REDUCE);
+            int64_t tl[3] = {b * s.H + h, qi, kj};
+            g.submit(NNT_OP_MAXSUMEXP, tl, a);
+          }
+  // subroutine 2: normalise every tile with the aggregated stats (bf16 path: on the recomputed
+  // score tile, from q and k)
   for (int64_t b = 0; b < s.B; ++b)
     for (int64_t h = 0; h < s.H; ++h)
       for (int64_t qi = 0; qi < ag.nq; ++qi)
         for (int64_t kj = 0; kj < ag.nq; ++kj) {
           if (!ag.needed(qi, kj)) continue;
           Acc a;
-          a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_R);
-          a.emplace_back(t.stats.h(g, b, h, qi), ACC_REDUCE);
-          int64_t tl[3] = {b * s.H + h, qi, kj};
-          g.submit(NNT_OP_MAXSUMEXP, tl, a);
-        }
-  // subroutine 2: normalise every tile with the aggregated stats
-  for (int64_t b = 0; b < s.B; ++b)
-    for (int64_t h = 0; h < s.H; ++h)
-      for (int64_t qi = 0; qi < ag.nq; ++qi)
-        for (int64_t kj = 0; kj < ag.nq; ++kj) {
-          if (!ag.needed(qi, kj)) continue;
-          Acc a;
-          a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_R);
+          if (s.bf16) {
+            t.qkv.region(g, ag.row0(b, qi), ag.row1(b, qi), ag.col0(0, h), ag.col1(0, h), ACC_R, a);
+            t.qkv.region(g, ag.row0(b, kj), ag.row1(b, kj), ag.col0(1, h), ag.col1(1, h), ACC_R, a);
+          } else {
+            a.emplace_back(t.scores.h(g, b, h, qi, kj), ACC_R);
+          }
           a.emplace_back(t.stats.h(g, b, h, qi), ACC_R);
           a.emplace_back(t.P.h(g, b, h, qi, kj), ACC_W);
           int64_t tl[3] = {b * s.H + h, qi, kj};

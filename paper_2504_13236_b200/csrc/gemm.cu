@@ -26,7 +26,9 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
                                     const void* B, int b_dtype, int64_t ldb, const int64_t* stride_b, float beta,
                                     void* C, int c_dtype, int64_t ldc, const int64_t* stride_c, const int64_t* tile,
                                     const nnt_epilogue* epi, nnt_stream_t stream) {
-  NNT_REQUIRE(A && B && C, NNT_ERR_NULL, "nnt_tile_gemm: NULL operand");
+  const bool stats_only = epi && epi->act == NNT_ACT_ROWSTATS;  // C is not written
+  NNT_REQUIRE(A && B && (C || stats_only), NNT_ERR_NULL, "nnt_tile_gemm: NULL operand");
+  NNT_REQUIRE(!stats_only || !C, NNT_ERR_ARG, "nnt_tile_gemm: ROWSTATS writes no C (pass NULL)");
   NNT_REQUIRE(trans_a == NNT_NOTRANS || trans_a == NNT_TRANS, NNT_ERR_ARG, "nnt_tile_gemm: trans_a=%d", trans_a);
   NNT_REQUIRE(trans_b == NNT_NOTRANS || trans_b == NNT_TRANS, NNT_ERR_ARG, "nnt_tile_gemm: trans_b=%d", trans_b);
   NNT_REQUIRE(M > 0 && N > 0 && K > 0, NNT_ERR_SHAPE, "nnt_tile_gemm: M=%lld N=%lld K=%lld", (long long)M,
@@ -39,7 +41,7 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
               (long long)lda);
   NNT_REQUIRE(ldb >= (trans_b == NNT_NOTRANS ? N : K), NNT_ERR_SHAPE, "nnt_tile_gemm: ldb=%lld too small",
               (long long)ldb);
-  NNT_REQUIRE(ldc >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ldc=%lld < N", (long long)ldc);
+  NNT_REQUIRE(stats_only || ldc >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ldc=%lld < N", (long long)ldc);
   if (tile) {
     NNT_REQUIRE(tile[0] > 0 && tile[1] > 0 && tile[2] > 0, NNT_ERR_TILE, "nnt_tile_gemm: tile must be positive");
   }
@@ -69,13 +71,21 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
   g.in_dtype = a_dtype;
   g.causal = NNT_CAUSAL_NONE;
   if (epi) {
-    NNT_REQUIRE(epi->act >= NNT_ACT_NONE && epi->act <= NNT_ACT_SOFTMAX_BWD, NNT_ERR_ARG, "nnt_tile_gemm: act=%d",
+    NNT_REQUIRE(epi->act >= NNT_ACT_NONE && epi->act <= NNT_ACT_SOFTMAX, NNT_ERR_ARG, "nnt_tile_gemm: act=%d",
                 epi->act);
+    const bool sm = epi->act == NNT_ACT_ROWSTATS || epi->act == NNT_ACT_SOFTMAX;
+    NNT_REQUIRE(!sm || (a_dtype == NNT_BF16 && epi->row_stats && !epi->bias && !epi->residual && beta == 0.f &&
+                        alpha > 0.f &&
+                        (epi->act == NNT_ACT_ROWSTATS || c_dtype == NNT_BF16) &&
+                        (epi->causal == NNT_CAUSAL_NONE || epi->causal == NNT_CAUSAL_OUT_LOWER)),
+                NNT_ERR_UNSUPPORTED,
+                "nnt_tile_gemm: ROWSTATS/SOFTMAX epilogues need bf16 operands, row_stats, alpha > 0, no bias/residual/beta, "
+                "bf16 C (SOFTMAX), causal NONE or OUT_LOWER");
     NNT_REQUIRE(epi->act != NNT_ACT_SOFTMAX_BWD || (a_dtype == NNT_BF16 && epi->rowvec && epi->aux),
                 NNT_ERR_UNSUPPORTED, "nnt_tile_gemm: SOFTMAX_BWD epilogue needs bf16 operands, aux (P) and rowvec (D)");
     NNT_REQUIRE(epi->causal >= NNT_CAUSAL_NONE && epi->causal <= NNT_CAUSAL_A_UPPER, NNT_ERR_ARG,
                 "nnt_tile_gemm: causal=%d", epi->causal);
-    NNT_REQUIRE(epi->act == NNT_ACT_NONE || epi->aux, NNT_ERR_NULL, "nnt_tile_gemm: GELU epilogue needs aux");
+    NNT_REQUIRE(epi->act == NNT_ACT_NONE || sm || epi->aux, NNT_ERR_NULL, "nnt_tile_gemm: GELU epilogue needs aux");
     NNT_REQUIRE(!epi->residual || epi->ld_residual >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_residual");
     NNT_REQUIRE(!epi->aux || epi->ld_aux >= N, NNT_ERR_SHAPE, "nnt_tile_gemm: ld_aux");
     NNT_REQUIRE((!epi->residual && (!epi->aux || epi->act == NNT_ACT_SOFTMAX_BWD)) || (b0 == 1 && b1 == 1),
@@ -93,7 +103,7 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.ld_stats = epi->ld_row_stats;
     g.rowvec = epi->rowvec;
     g.rowscale = epi->rowscale;
-    NNT_REQUIRE(!epi->row_stats || (a_dtype == NNT_BF16 && c_dtype == NNT_F32 && epi->act == NNT_ACT_NONE &&
+    NNT_REQUIRE(!epi->row_stats || sm || (a_dtype == NNT_BF16 && c_dtype == NNT_F32 && epi->act == NNT_ACT_NONE &&
                                     epi->ld_row_stats >= (N + 31) / 32 &&
                                     (epi->causal == NNT_CAUSAL_NONE || epi->causal == NNT_CAUSAL_OUT_LOWER)),
                 NNT_ERR_UNSUPPORTED,
@@ -102,10 +112,13 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
   const double frac = g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5;
   const double flops = 2.0 * (double)M * N * K * b0 * b1 * frac;
   const double es = (double)dtype_size(a_dtype);
+  const double c_bytes = stats_only ? 0.0
+                                    : (double)M * N * dtype_size(c_dtype) * b0 * b1 *
+                                          (g.causal == NNT_CAUSAL_OUT_LOWER ? 0.5 : 1.0) * (beta != 0.f ? 2.0 : 1.0);
+  const bool sm_act = g.act == NNT_ACT_ROWSTATS || g.act == NNT_ACT_SOFTMAX;
   const double bytes = ((double)M * K * es + (double)K * N * es) * b0 * b1 * (g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5) +
-                       (double)M * N * dtype_size(c_dtype) * b0 * b1 *
-                           (g.causal == NNT_CAUSAL_OUT_LOWER ? 0.5 : 1.0) * (beta != 0.f ? 2.0 : 1.0) +
-                       (g.residual ? 4.0 * M * N : 0.0) + (g.aux ? (double)M * N * dtype_size(c_dtype) : 0.0);
+                       c_bytes + (g.residual ? 4.0 * M * N : 0.0) +
+                       (g.aux ? (double)M * N * dtype_size(c_dtype) : 0.0) + (sm_act ? 8.0 * M * b0 * b1 : 0.0);
   if (a_dtype == NNT_F32) {
     LaunchScope sc(NNT_K_GEMM_SIMT, stream, bytes, flops);
     return gemm_simt_launch(g, stream);

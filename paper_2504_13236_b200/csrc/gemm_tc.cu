@@ -57,12 +57,29 @@ struct Cfg {
   static_assert(SMEM_BYTES <= kMaxSmem, "shared memory budget");
 };
 
-enum TileOrder { ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3 };
+enum TileOrder { ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3, ORDER_ROWS = 4 };
+
+// n / d and n % d for a runtime divisor d >= 1 and n < 2^31 with a multiply-high and a shift
+// (round-up multiplier method).  The single-thread TMA producer and MMA issuer decode a tile per
+// task; with 64-bit division subroutines that decode cost ~2k cycles, more than the MMAs of a
+// K = 64 attention tile.
+struct FastDiv {
+  uint32_t d, mul, shr;
+  void init(int64_t div) {
+    d = (uint32_t)(div < 1 ? 1 : div);
+    shr = 0;
+    while (shr < 32 && (1ull << shr) < d) ++shr;
+    mul = (uint32_t)(((1ull << 32) * ((1ull << shr) - d)) / d + 1);
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const { return (__umulhi(n, mul) + n) >> shr; }
+  __device__ __forceinline__ uint32_t mod(uint32_t n, uint32_t q) const { return n - q * d; }
+};
 
 struct TcParams {
   GemmArgs g;
   int64_t mt, nt, tiles_per_batch, num_tiles, num_tasks;
   int64_t splits, kb_per_split;
+  FastDiv f_splits, f_tpb, f_mt, f_nt, f_nbat, f_level, f_b1;  // divisors of the task decode
   uint32_t idesc;
   int a_kmajor, b_kmajor;
   int tma_store;  // epilogue stores through TMA (C / aux / workspace maps valid)
@@ -172,6 +189,29 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// 32 consecutive fp32 columns of this warp's TMEM lane quadrant, no wait
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// n x 32 columns (n loads in flight, one wait)
+template <int n>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
+  uint32_t r[32 * n];
+#pragma unroll
+  for (int h = 0; h < n; ++h) tmem_ld32_nowait(taddr + 32 * h, r + 32 * h);
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32 * n; ++j) v[j] = __uint_as_float(r[j]);
+}
+
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   uint32_t r[32];
   asm volatile(
@@ -199,41 +239,62 @@ __device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uin
   return d;
 }
 
+// Output tiles per task: 1, or (ORDER_ROWS) the key tiles of the task's row block.
+__device__ __forceinline__ int64_t task_subtiles(const TcParams& P, int64_t t, int bn) {
+  if (P.order != ORDER_ROWS) return 1;
+  const int64_t mb = P.mt - 1 - (int64_t)P.f_nbat.div((uint32_t)t);  // splits == 1
+  if (P.g.causal == NNT_CAUSAL_OUT_LOWER) return min(P.nt, ((mb + 1) * BM + bn - 1) / bn);
+  return P.nt;
+}
+
 // Which tile a task computes and which K-blocks it covers (nnt_causal semantics + split-K).
 struct TileInfo {
   int64_t tile, bz, m0, n0, kb_begin, kb_end, split;
+  int p, q;  // batch item (bz = p * batch1 + q)
 };
 // bm_tile: output rows per task (BM, or 2*BM for a CTA pair); row_off: this CTA's first row
 // within the task's tile (CTA-pair rank * BM).  Causal orders are single-CTA only.
+// ORDER_ROWS: a task is one (batch item, row block) and owns all its key tiles; j = key tile.
+// 32-bit index math with precomputed divisors (host guarantees num_tasks < 2^31).
 __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, int bn, int bm_tile = BM,
-                                                int row_off = 0) {
+                                                int row_off = 0, int64_t j = 0) {
   TileInfo ti;
-  ti.split = t % P.splits;
-  ti.tile = t / P.splits;
-  int64_t mb, nb;
-  if (P.order == ORDER_TRI) {
+  const uint32_t tt = (uint32_t)t;
+  const uint32_t tile = P.f_splits.div(tt);
+  ti.split = P.f_splits.mod(tt, tile);
+  ti.tile = tile;
+  uint32_t mb, nb, bz;
+  if (P.order == ORDER_ROWS) {
+    // heaviest row blocks first (causal: row block mb holds mb+1 key tiles)
+    const uint32_t level = P.f_nbat.div(tile);
+    bz = P.f_nbat.mod(tile, level);
+    mb = (uint32_t)P.mt - 1 - level;
+    nb = (uint32_t)j;
+  } else if (P.order == ORDER_TRI) {
     // compact lower-triangular enumeration (BN == BM, square grid): row mb holds mb+1 tiles
-    ti.bz = ti.tile / P.tiles_per_batch;
-    const int64_t r = ti.tile % P.tiles_per_batch;
-    mb = (int64_t)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
+    bz = P.f_tpb.div(tile);
+    const uint32_t r = P.f_tpb.mod(tile, bz);
+    mb = (uint32_t)((sqrtf(8.0f * (float)r + 1.0f) - 1.0f) * 0.5f);
     while ((mb + 1) * (mb + 2) / 2 <= r) ++mb;
     while (mb * (mb + 1) / 2 > r) --mb;
     nb = r - mb * (mb + 1) / 2;
   } else if (P.order == ORDER_N_OUTER) {
-    ti.bz = ti.tile / P.tiles_per_batch;
-    const int64_t r = ti.tile % P.tiles_per_batch;
-    nb = r / P.mt;
-    mb = r % P.mt;
+    bz = P.f_tpb.div(tile);
+    const uint32_t r = P.f_tpb.mod(tile, bz);
+    nb = P.f_mt.div(r);
+    mb = P.f_mt.mod(r, nb);
   } else {
     // heaviest K-range first: the m-block level is outermost, (batch, n) inner
-    const int64_t per_level = P.num_tiles / P.mt;
-    const int64_t level = ti.tile / per_level, r = ti.tile % per_level;
-    mb = P.order == ORDER_HEAVY_HIGH_M ? P.mt - 1 - level : level;
-    ti.bz = r / P.nt;
-    nb = r % P.nt;
+    const uint32_t level = P.f_level.div(tile), r = P.f_level.mod(tile, level);
+    mb = P.order == ORDER_HEAVY_HIGH_M ? (uint32_t)P.mt - 1 - level : level;
+    bz = P.f_nt.div(r);
+    nb = P.f_nt.mod(r, bz);
   }
-  ti.m0 = mb * bm_tile + row_off;
-  ti.n0 = nb * bn;
+  ti.bz = bz;
+  ti.p = (int)P.f_b1.div(bz);
+  ti.q = (int)P.f_b1.mod(bz, (uint32_t)ti.p);
+  ti.m0 = (int64_t)mb * bm_tile + row_off;
+  ti.n0 = (int64_t)nb * bn;
   int64_t k_begin = 0, k_end = P.g.K;
   if (P.g.causal == NNT_CAUSAL_A_LOWER) k_end = min(P.g.K, ti.m0 + BM);
   if (P.g.causal == NNT_CAUSAL_A_UPPER) k_begin = min(P.g.K, ti.m0);
@@ -244,6 +305,14 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
 }
 
 // ------------------------------------------------------------------ epilogue math
+// 2^x as one MUFU.EX2 (results below 2^-126 flush to 0: immaterial for softmax weights <= 1;
+// exp2f's IEEE path adds a denormal-range rescale around every MUFU op)
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 template <bool kFast>
 __device__ __forceinline__ float tanh_f(float x) {
   if (kFast) {  // bf16 outputs: tanh.approx (rel err ~2^-11) is below bf16 rounding
@@ -465,7 +534,10 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
 //                (max, sumexp) (softmax subroutine 1)
 //   EPI_DA       bf16 C = rowscale * P * (acc - D[row]) (softmax backward), P prefetched a
 //                chunk ahead
-enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2 };
+//   EPI_ROWSTATS per-row (max, sumexp) over all key tiles of a row block (ORDER_ROWS tasks),
+//                no C (softmax subroutine 1 with on-chip aggregation, R26)
+//   EPI_SOFTMAX  bf16 C = e^{alpha*acc - M} / S from the row's stats (subroutine 2, R26)
+enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4 };
 
 // CG = 2: launched as clusters of 2 CTAs (an SM pair).  Task = 256 x BN output tile; rank r
 // stages A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) and drains its own TMEM
@@ -534,9 +606,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = task0; t < P.num_tasks; t += task_step) {
-        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
-        const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
+      for (int64_t t = task0, sub = 0; t < P.num_tasks;
+           sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
+        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off, sub);
+        const int p = ti.p, q = ti.q;
         const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
@@ -595,8 +668,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // apart; +2 KB per UMMA_K=16.
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
-      for (int64_t t = task0; t < P.num_tasks; t += task_step) {
-        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
+      for (int64_t t = task0, sub = 0; t < P.num_tasks;
+           sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
+        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off, sub);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -633,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else if constexpr (EPI == EPI_SCORES || EPI == EPI_DA) {
+  } else if constexpr (EPI != EPI_GENERIC) {
     // ===================== specialised epilogues (attention score-type GEMMs)
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -642,13 +716,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float L2E = 1.4426950408889634f;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int64_t t = task0; t < P.num_tasks; t += task_step) {
-      TileInfo ti = decode_task(P, t, BN);
-      const int p = (int)(ti.bz / g.batch1), q = (int)(ti.bz % g.batch1);
+    // EPI_ROWSTATS: running (max, sumexp) of this lane's row over this half's columns of the
+    // task's key tiles (online merge rule of R10); the quadrant's two halves combine at task end
+    float m_run = -INFINITY, l_run = 0.f;
+    int xbuf = 0;
+    const float sc_c = g.alpha * L2E;  // EPI_ROWSTATS / EPI_SOFTMAX: e^{alpha*a} = 2^{a*sc_c}
+    // columns per chunk: a 128-byte staging row of C, or (ROWSTATS, no C) 64 columns so one
+    // wait covers two TMEM loads and the exp chain has twice the independent work
+    constexpr int WE = EPI == EPI_ROWSTATS ? 64 : W;
+    for (int64_t t = task0, sub = 0; t < P.num_tasks;
+         sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
+      TileInfo ti = decode_task(P, t, BN, BM, 0, sub);
+      const int p = ti.p, q = ti.q;
       const int row_in = (int)ti.m0 + quad * 32 + lane;  // row of this lane within the batch item
       const bool row_ok = row_in < g.M;
       const int cy = (int)ti.m0 + quad * 32;
-      const int c_first = half * W;
+      const int c_first = half * WE;
       // EPI_DA: P row pointer of this lane and the prefetch of its first chunk
       const TC* prow = nullptr;
       Raw8 raw;  // P of the next chunk (128 bytes of this lane's row)
@@ -658,21 +741,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (row_ok && ti.n0 + c_first + W <= g.N) raw_load(raw, prow + c_first);
         dval = row_ok ? __ldg(g.rowvec + ti.bz * g.M + row_in) : 0.f;
       }
+      // EPI_SOFTMAX: the row's (M, S) from the statistics pass
+      float sm_ml = 0.f, sm_inv = 0.f;
+      if constexpr (EPI == EPI_SOFTMAX) {
+        if (row_ok) {
+          const float2 rs = __ldg(reinterpret_cast<const float2*>(g.row_stats) + ti.bz * g.M + row_in);
+          sm_ml = rs.x * L2E;
+          sm_inv = 1.f / rs.y;
+        }
+      }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
       const bool has_k = ti.kb_end > ti.kb_begin;
 #pragma unroll 1
-      for (int c = c_first; c < BN; c += 2 * W) {
+      for (int c = c_first; c < BN; c += 2 * WE) {
         if (ti.n0 + c >= g.N) break;  // warp-uniform
         const int col0 = (int)ti.n0 + c;
-        float v[W];
+        float v[WE];
+        if (has_k) {
+          tmem_ld_cols<WE / 32>(tmem_base + (uint32_t)(acc * BN + c) + ((uint32_t)(quad * 32) << 16), v);
+        } else {
 #pragma unroll
-        for (int h = 0; h < W / 32; ++h) {
-          if (has_k)
-            tmem_ld32(tmem_base + (uint32_t)(acc * BN + c + 32 * h) + ((uint32_t)(quad * 32) << 16), v + 32 * h);
-          else
-#pragma unroll
-            for (int j = 0; j < 32; ++j) v[32 * h + j] = 0.f;
+          for (int j = 0; j < WE; ++j) v[j] = 0.f;
         }
         if constexpr (EPI == EPI_SCORES) {
 #pragma unroll
@@ -717,6 +807,52 @@ __global__ void __launch_bounds__(kThreads, 1)
             reinterpret_cast<float2*>(g.row_stats)[(ti.bz * g.M + row_in) * g.ld_stats + col0 / 32] =
                 make_float2(m, s);
           }
+        } else if constexpr (EPI == EPI_ROWSTATS) {
+          // subroutine 1 on this 32-key chunk, merged into the running (m, l): no C store.
+          // (per-lane branch only: the next chunk's tcgen05.ld is warp-collective)
+          // m_run is kept in accumulator units (alpha > 0: max(alpha*acc) = alpha*max(acc)
+          // exactly); e^{alpha*acc - alpha*m} = 2^{acc*c - m*c} with c = alpha*log2(e)
+          int lim = row_ok ? g.N - col0 : 0;
+          if (g.causal == NNT_CAUSAL_OUT_LOWER && row_in - col0 + 1 < lim) lim = row_in - col0 + 1;
+          if (lim > 0) {
+            if (lim < WE) {
+#pragma unroll
+              for (int j = 0; j < WE; ++j)
+                if (j >= lim) v[j] = -INFINITY;
+            }
+            float mx[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) mx[i] = fmaxf(v[i], v[i + 4]);
+#pragma unroll
+            for (int j = 8; j < WE; j += 8)
+#pragma unroll
+              for (int i = 0; i < 4; ++i) mx[i] = fmaxf(mx[i], fmaxf(v[j + i], v[j + 4 + i]));
+            const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));  // finite
+            const float mc = m_new * sc_c;
+            float s[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) s[i] = 0.f;
+#pragma unroll
+            for (int j = 0; j < WE; j += 8)  // 2^{-inf} = 0 for the masked columns
+#pragma unroll
+              for (int i = 0; i < 8; ++i) s[i] += ex2_approx(fmaf(v[j + i], sc_c, -mc));
+            const float st = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+            l_run = fmaf(l_run, ex2_approx((m_run - m_new) * sc_c), st);
+            m_run = m_new;
+          }
+          continue;
+        } else if constexpr (EPI == EPI_SOFTMAX) {
+          // subroutine 2: P = e^{x - M} / S on the recomputed scores; masked entries 0
+          int lim = g.N - col0;
+          if (g.causal == NNT_CAUSAL_OUT_LOWER && row_in - col0 + 1 < lim) lim = row_in - col0 + 1;
+          if (!row_ok) lim = 0;
+          if (lim >= W) {
+#pragma unroll
+            for (int j = 0; j < W; ++j) v[j] = ex2_approx(fmaf(v[j], sc_c, -sm_ml)) * sm_inv;
+          } else {
+#pragma unroll
+            for (int j = 0; j < W; ++j) v[j] = j < lim ? ex2_approx(fmaf(v[j], sc_c, -sm_ml)) * sm_inv : 0.f;
+          }
         } else {
           // dA = rowscale * P * (dP - D); P of this chunk was prefetched into raw
           const bool full = row_ok && col0 + W <= g.N;
@@ -757,6 +893,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if constexpr (EPI == EPI_ROWSTATS) {
+        if (sub + 1 == task_subtiles(P, t, BN)) {
+          // task end: half 1 publishes its (m, l); half 0 merges both and writes the row's stats
+          // (double-buffered exchange slot: the next task's write waits behind this barrier)
+          float2* xch = reinterpret_cast<float2*>(smem + C::EPI_OFF) + xbuf * BM + quad * 32 + lane;
+          if (half == 1) *xch = make_float2(m_run, l_run);
+          asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+          if (half == 0 && row_ok) {
+            const float2 o = *xch;
+            const float M = fmaxf(m_run, o.x);  // accumulator units
+            float S = 0.f;
+            if (M != -INFINITY) S = l_run * ex2_approx((m_run - M) * sc_c) + o.y * ex2_approx((o.x - M) * sc_c);
+            reinterpret_cast<float2*>(g.row_stats)[ti.bz * g.M + row_in] = make_float2(M * g.alpha, S);
+          }
+          xbuf ^= 1;
+          m_run = -INFINITY;
+          l_run = 0.f;
+        }
+      }
     }
     if (lane == 0) bulk_wait0();
   } else {
@@ -795,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc_phase = 0;
     for (int64_t t = task0; t < P.num_tasks; t += task_step) {
       TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
-      const int64_t p = ti.bz / g.batch1, q = ti.bz % g.batch1;
+      const int64_t p = ti.p, q = ti.q;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
       const int64_t row = ti.m0 + quad * 32 + lane;
@@ -1049,7 +1204,10 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.b_kmajor = a.tb == NNT_TRANS;
   P.mt = cdiv(a.M, BM * CG);
   P.nt = cdiv(a.N, BN);
-  if (a.causal == NNT_CAUSAL_OUT_LOWER && BN == BM && P.mt == P.nt) {
+  if (EPI == EPI_ROWSTATS) {
+    P.order = ORDER_ROWS;  // task = (batch item, row block) with all its key tiles
+    P.tiles_per_batch = P.mt;
+  } else if (a.causal == NNT_CAUSAL_OUT_LOWER && BN == BM && P.mt == P.nt) {
     P.order = ORDER_TRI;
     P.tiles_per_batch = P.mt * (P.mt + 1) / 2;
   } else {
@@ -1062,6 +1220,15 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.splits = splits;
   P.kb_per_split = cdiv(nkb, P.splits);
   P.num_tasks = P.num_tiles * P.splits;
+  NNT_REQUIRE(P.num_tasks < (1ll << 31), NNT_ERR_UNSUPPORTED, "gemm(bf16): %lld tile tasks (> 2^31)",
+              (long long)P.num_tasks);
+  P.f_splits.init(P.splits);
+  P.f_tpb.init(P.tiles_per_batch);
+  P.f_mt.init(P.mt);
+  P.f_nt.init(P.nt);
+  P.f_nbat.init(a.batch0 * a.batch1);
+  P.f_level.init(P.num_tiles / P.mt);
+  P.f_b1.init(a.batch1);
   P.ws_mode = splits > 1 ? 1 : 0;
   // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
   if (P.ws_mode || EPI != EPI_GENERIC)
@@ -1097,6 +1264,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.tma_store = 1;
     NNT_TRY(make_map(&tmAux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.workspace, a.N, a.M, a.N, splits, a.M * a.N, 1, 0,
                      32, 32));
+  } else if (EPI == EPI_ROWSTATS) {
+    P.tma_store = 0;  // no C
   } else {
     const bool tma_ok = c_tma_ok(a, es);
     NNT_REQUIRE(EPI == EPI_GENERIC || tma_ok, NNT_ERR_ALIGN, "gemm(bf16): specialised epilogue needs TMA-able C");
@@ -1202,6 +1371,7 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   const bool tma_ok = splits == 1 && c_tma_ok(a, sizeof(TC));
   if constexpr (sizeof(TC) == 2) {
     if (tma_ok && a.act == NNT_ACT_SOFTMAX_BWD) return launch_bn<128, TC, EPI_DA>(a, s, 1);
+    if (a.act == NNT_ACT_SOFTMAX) return launch_bn<128, TC, EPI_SOFTMAX>(a, s, 1);
   } else {
     if (tma_ok && a.act == NNT_ACT_NONE && !a.bias && !a.residual && a.beta == 0.f &&
         (a.row_stats || a.causal == NNT_CAUSAL_OUT_LOWER))
@@ -1242,6 +1412,7 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
                      (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);
   if (!ws_ok) splits = 1;
   if (kernels) *kernels = splits > 1 ? 2 : 1;
+  if (a.act == NNT_ACT_ROWSTATS) return launch_bn<128, float, EPI_ROWSTATS>(a, s, 1);
   if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits);
   return launch_tc<__nv_bfloat16>(a, s, splits);
 }

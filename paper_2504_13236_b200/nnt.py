@@ -30,7 +30,7 @@ STATUS_NAMES = {0: "NNT_OK", 1: "NNT_ERR_NULL", 2: "NNT_ERR_SHAPE", 3: "NNT_ERR_
 NNT_F32, NNT_BF16 = 0, 1
 NNT_NOTRANS, NNT_TRANS = 0, 1
 NNT_CAUSAL_NONE, NNT_CAUSAL_OUT_LOWER, NNT_CAUSAL_A_LOWER, NNT_CAUSAL_A_UPPER = 0, 1, 2, 3
-NNT_ACT_NONE, NNT_ACT_GELU, NNT_ACT_GELU_BWD, NNT_ACT_SOFTMAX_BWD = 0, 1, 2, 3
+NNT_ACT_NONE, NNT_ACT_GELU, NNT_ACT_GELU_BWD, NNT_ACT_SOFTMAX_BWD, NNT_ACT_ROWSTATS, NNT_ACT_SOFTMAX = 0, 1, 2, 3, 4, 5
 NNT_CAUSAL_ALIGN = 128
 KERNEL_CLASSES = ("gemm_tc", "gemm_tc_attn", "gemm_simt", "maxsumexp", "softmax", "softmax_bwd", "ln_fwd", "ln_bwd", "gelu",
                   "bias_grad", "adam", "misc")

@@ -132,7 +132,8 @@ def test_block_workspace_sizes(nnt, name):
     att = c.B * c.H * c.S * c.S
     need_saved = dt * (T * E * 3 + T * 3 * E + 2 * T * F + att) + 4 * (T * E + 4 * T + 2 * c.B * c.H * c.S)
     assert need_saved <= saved <= need_saved + 256 * 16
-    assert scratch >= 4 * att + dt * att
+    # fp32 path: materialised scores + dA; bf16 path: dA only (score tiles stay on chip, R26)
+    assert scratch >= (dt * att if c.dtype == "bf16" else 4 * att + dt * att)
 
 
 def _expected_counts(c, tile):
@@ -142,6 +143,8 @@ def _expected_counts(c, tile):
     pairs = c.B * c.H * nq * (nq + 1) // 2
     fwd = {"ln1": nt, "qkv": nt * n3 * ne, "scores": pairs, "maxsumexp": pairs, "softmax": pairs, "pv": pairs,
            "out": nt * ne * ne, "ln2": nt, "fc": nt * nf * ne, "proj": nt * ne * nf}
+    if c.dtype == "bf16":  # R26: subroutine 1 fused into the score tasks (no scores tensor, no maxsumexp)
+        del fwd["maxsumexp"]
     bwd = {"proj_db": nt * ne, "proj_dw": ne * nf * nt, "proj_dx": nt * nf * ne, "fc_db": nt * nf,
            "fc_dw": nf * ne * nt, "fc_dx": nt * ne * nf, "ln2_bwd": nt, "out_db": nt * ne, "out_dw": ne * ne * nt,
            "out_dx": nt * ne * ne, "softmax_bwd": c.B * c.H * nq, "att_dp": pairs, "att_dv": pairs, "att_dq": pairs,
@@ -156,7 +159,7 @@ def test_dag_task_counts_and_levels(nnt, name, tile):
     tasks, groups = nnt.nnt_block_dag_describe(cfg, 0)
     names = [nnt.OP_NAMES[g.op] for g in groups]
     assert names == list(fwd_n)                              # program order == level order
-    assert [g.level for g in groups] == list(range(10))      # a chain: LN1 -> ... -> PROJ
+    assert [g.level for g in groups] == list(range(len(fwd_n)))  # a chain: LN1 -> ... -> PROJ
     assert {nnt.OP_NAMES[g.op]: g.n_tasks for g in groups} == fwd_n
     assert len(tasks) == sum(fwd_n.values())
     assert all(t.n_deps == 0 for t in tasks if t.op == 0)    # LN1 tasks are sources

@@ -229,6 +229,47 @@ def test_scores_gemm_fused_maxsumexp_partials(causal):
     assert rel(got[..., 1], s_ref) < 1e-5
 
 
+@pytest.mark.parametrize("causal", [0, 1])
+@pytest.mark.parametrize("S", [384, 200])
+def test_rowstats_then_softmax_gemms(causal, S):
+    """R26: the statistics pass (NNT_ACT_ROWSTATS: subroutine 1 aggregated over all key tiles of
+    a row on chip, no scores stored) and the P pass (NNT_ACT_SOFTMAX: subroutine 2 on the
+    recomputed score tile) vs the oracle's maxsumexp / softmax of the same scores."""
+    B, H, Dh = 2, 3, 64
+    E = H * Dh
+    rng = np.random.default_rng(81 + causal + S)
+    qkv = bf16_round(2.0 * rng.standard_normal((B, S, 3 * E)))
+    Q = dev(qkv, torch.bfloat16)
+    sq = (S * 3 * E, Dh)
+    alpha = 1.0 / math.sqrt(Dh)
+    stats = torch.full((B * H * S, 2), float("nan"), device="cuda")
+    epi = nnt.make_epilogue(act=nnt.NNT_ACT_ROWSTATS, causal=causal, row_stats=stats)
+    nnt.nnt_tile_gemm(0, 1, S, S, Dh, (B, H), alpha, Q, 1, 3 * E, sq, Q.data_ptr() + 2 * E, 1, 3 * E, sq, 0.0, None,
+                      0, S, (H * S * S, S * S), None, epi)
+    P = torch.full((B, H, S, S), float("nan"), device="cuda", dtype=torch.bfloat16)
+    epi2 = nnt.make_epilogue(act=nnt.NNT_ACT_SOFTMAX, causal=causal, row_stats=stats)
+    nnt.nnt_tile_gemm(0, 1, S, S, Dh, (B, H), alpha, Q, 1, 3 * E, sq, Q.data_ptr() + 2 * E, 1, 3 * E, sq, 0.0, P,
+                      1, S, (H * S * S, S * S), None, epi2)
+    torch.cuda.synchronize()
+    q = qkv[:, :, :E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    k = qkv[:, :, E:2 * E].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
+    a = alpha * (q @ k.transpose(0, 1, 3, 2))
+    mask = np.tril(np.ones((S, S), bool)) if causal else None
+    m_ref, s_ref = dense.maxsumexp(a, mask)
+    got = host(stats).reshape(B, H, S, 2)
+    np.testing.assert_allclose(got[..., 0], m_ref, rtol=1e-5, atol=1e-5)
+    assert rel(got[..., 1], s_ref) < 1e-5
+    p = host(P)
+    p_ref = dense.softmax(a, mask)
+    r, c = np.arange(S)[:, None], np.arange(S)[None, :]
+    written = c < np.minimum(S, (r // 128 + 1) * 128) if causal else np.ones((S, S), bool)
+    assert not np.isnan(p[..., written]).any() and np.isnan(p[..., ~written]).all()
+    if causal:
+        assert np.all(p[..., written & (c > r)] == 0.0)
+    assert rel(np.where(written, p, 0.0), p_ref) < 4e-3  # bf16 rounding of P
+    np.testing.assert_allclose(np.where(written, p, 0.0).sum(-1), 1.0, atol=2e-2)
+
+
 def test_fused_softmax_bwd_gemm_and_rowdot():
     """dA = P * (dO V^T - D) / sqrt(h) from the dP GEMM epilogue, with D = rowdot(dO, O)
     (identity sum_k P dP = sum_i dO O), vs the oracle's softmax backward (R18)."""

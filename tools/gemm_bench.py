@@ -43,6 +43,7 @@ def main():
     big = torch.randn(8192, 8192, **bf) * 0.05
     spart = torch.empty(B * H * S * (S // 32) * 2, **f32)
     dvec = torch.zeros(B * H * S, **f32)
+    rstats = torch.zeros(B * H * S * 2, **f32)
     cases = [
         # name, ta, tb, M, N, K, batch, A, lda, sa, B, ldb, sb, C, cdt, ldc, sc, epi, causal-frac
         ("qkv", 0, 1, T, 3 * E, E, None, h, E, None, w, E, None, outb, 1, 3 * E, None,
@@ -52,6 +53,10 @@ def main():
         ("scores+stats", 0, 1, S, S, Dh, bh, h, 3 * E, (S * 3 * E, Dh), h.data_ptr() + es * E, 3 * E,
          (S * 3 * E, Dh), outf, 0, S, (H * S * S, S * S),
          nnt.make_epilogue(causal=1, row_stats=spart, ld_row_stats=S // 32), 0.5),
+        ("rowstats", 0, 1, S, S, Dh, bh, h, 3 * E, (S * 3 * E, Dh), h.data_ptr() + es * E, 3 * E, (S * 3 * E, Dh),
+         None, 0, S, (H * S * S, S * S), nnt.make_epilogue(causal=1, act=4, row_stats=rstats), 0.5),
+        ("softmaxP", 0, 1, S, S, Dh, bh, h, 3 * E, (S * 3 * E, Dh), h.data_ptr() + es * E, 3 * E, (S * 3 * E, Dh),
+         outb, 1, S, (H * S * S, S * S), nnt.make_epilogue(causal=1, act=5, row_stats=rstats), 0.5),
         ("dp_dA", 0, 1, S, S, Dh, bh, h, E, (S * E, Dh), h.data_ptr() + es * 2 * E, 3 * E, (S * 3 * E, Dh),
          outb, 1, S, (H * S * S, S * S),
          nnt.make_epilogue(causal=1, act=3, aux=P, ld_aux=S, rowvec=dvec, rowscale=0.125), 0.5),
@@ -117,7 +122,8 @@ def main():
         us = ts[len(ts) // 2]
         nb = (batch[0] * batch[1]) if batch else 1
         fl = 2.0 * M * N * K * nb * frac
-        total += us
+        if name != "square8192":
+            total += us
         print(f"{name:14s} {M:6d} {N:6d} {K:6d} {str(nb):>8s} {us:8.1f} {fl / us / 1e6:8.1f}")
     print(f"total per layer {total:.1f} us  -> x{L} layers = {total * L / 1e3:.2f} ms")
 
