@@ -873,18 +873,20 @@ __global__ void __launch_bounds__(kThreads, 1)
           const int cn = c + 2 * W;
           if (cn < BN && row_ok && ti.n0 + cn + W <= g.N) raw_load(raw, prow + cn);
         }
-        // stage + TMA store (2-buffer ring per warp)
-        uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
-        __syncwarp();
-        stage_row<TC, W>(buf, lane, v);
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          tma_store_4d(&tmC, smem_u32(buf), col0, cy, q, p);
-          bulk_commit();
+        if constexpr (EPI != EPI_ROWSTATS) {  // (ROWSTATS has no C)
+          // stage + TMA store (2-buffer ring per warp)
+          uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
+          __syncwarp();
+          stage_row<TC, W>(buf, lane, v);
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_4d(&tmC, smem_u32(buf), col0, cy, q, p);
+            bulk_commit();
+          }
+          ring ^= 1;
         }
-        ring ^= 1;
       }
       tc_fence_before();
       __syncwarp();
