@@ -40,6 +40,9 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for one TMA store box
 constexpr int kStageBufs = 2;             // staging ring per epilogue warp (one store in flight while refilling)
 constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory per CTA
+// mbarriers: full/empty per stage (<= 8 each), TMEM full/empty (2 each), per epilogue warp
+// and staging buffer an epilogue-input TMA barrier (kEpiWarps * kStageBufs), the TMEM slot
+constexpr int kBarBytes = 512;
 
 // CG = CTAs per MMA (tcgen05 cta_group): 1, or 2 = an SM pair computing a 256 x BN tile
 // (each CTA stages its 128 A rows and half of the BN B rows; the leader issues M=256 MMAs).
@@ -49,11 +52,11 @@ struct Cfg {
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int EPI_BYTES = kEpiWarps * kStageBufs * kStageBytesPerWarp;
-  static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - 256) / STAGE_BYTES;
+  static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - kBarBytes) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
-  static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + kBarBytes;
   static_assert(SMEM_BYTES <= kMaxSmem, "shared memory budget");
 };
 
@@ -334,6 +337,29 @@ __device__ __forceinline__ float gelu_grad_e(float u) {
   return 0.5f * (1.0f + t) + 0.5f * u * (1.0f - t * t) * c * (1.0f + 3.0f * a * u * u);
 }
 
+// Packed fp32x2 forms (sm_100 FFMA2/FMUL2/FADD2: two lanes of fp32 math per instruction) of
+// the epilogue activations, for bf16 outputs (tanh.approx): same formulas as gelu_e / gelu_grad_e
+// up to fp32 rounding order.
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ float2 tanh2_approx(float2 z) { return make_float2(tanh_f<true>(z.x), tanh_f<true>(z.y)); }
+__device__ __forceinline__ float2 gelu2(float2 u) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float2 u2 = __fmul2_rn(u, u);
+  const float2 z = __fmul2_rn(__fmul2_rn(u, f2(c)), __ffma2_rn(u2, f2(a), f2(1.f)));  // c u (1 + a u^2)
+  const float2 hu = __fmul2_rn(u, f2(0.5f));
+  return __ffma2_rn(hu, tanh2_approx(z), hu);  // u/2 (1 + t)
+}
+__device__ __forceinline__ float2 gelu_grad2(float2 u) {
+  const float c = 0.7978845608028654f, a = 0.044715f;
+  const float2 u2 = __fmul2_rn(u, u);
+  const float2 z = __fmul2_rn(__fmul2_rn(u, f2(c)), __ffma2_rn(u2, f2(a), f2(1.f)));
+  const float2 t = tanh2_approx(z);
+  const float2 ne = __fmul2_rn(u, __ffma2_rn(u2, f2(-3.f * a * c), f2(-c)));  // -u c (1 + 3 a u^2)
+  const float2 m = __ffma2_rn(t, t, f2(-1.f));                                // t^2 - 1
+  const float2 h = __ffma2_rn(ne, m, t);                                      // t + u c (1+3au^2)(1-t^2)
+  return __ffma2_rn(h, f2(0.5f), f2(0.5f));
+}
+
 template <typename T>
 __device__ __forceinline__ float ld_elem(const T* p) { return to_f32(*p); }
 // C may have been written by TMA stores of this kernel's earlier launches: bypass L1.
@@ -389,7 +415,17 @@ __device__ __forceinline__ void unpack8(const Raw8& r, int j, float* t) {
   }
 }
 // The streamed (prefetched) epilogue input of a GEMM: at most one, element type = C's.
-enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3 };
+// IN_AUX_SMEM: the aux chunk is TMA-loaded into the chunk's staging buffer at tile start
+// (before the accumulator wait) and read from shared memory; the output overwrites it in place.
+enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3, IN_AUX_SMEM = 4 };
+
+// Reads back one 128-byte row chunk from SW128 staging (the layout stage_row writes and a
+// 32-row TMA box of the same map loads).
+__device__ __forceinline__ void unstage_row(Raw8& r, const uint8_t* buf, int lane) {
+  const uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r.u[j] = *reinterpret_cast<const uint4*>(rowp + ((j ^ (lane & 7)) << 4));
+}
 
 // The W pre-activation outputs of one row chunk (GELU is applied by the caller after
 // staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
@@ -399,8 +435,14 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
                                          bool extras, bool vec, float dval, int in_kind, const Raw8& raw,
                                          float (&v)[W]) {
   constexpr bool kFast = sizeof(TC) == 2;
+  if (g.alpha != 1.f) {
 #pragma unroll
-  for (int j = 0; j < W; ++j) v[j] *= g.alpha;
+    for (int j = 0; j < W; j += 2) {
+      const float2 x = __fmul2_rn(make_float2(v[j], v[j + 1]), f2(g.alpha));
+      v[j] = x.x;
+      v[j + 1] = x.y;
+    }
+  }
   if (!extras) return;  // split-K partial: bias/beta/residual belong to the reduce
   if (g.act == NNT_ACT_SOFTMAX_BWD) {
     // dA = scale * P * (dP - D): aux holds P with C's layout, dval = D of this row
@@ -423,12 +465,19 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
   }
   if (vec && row < g.M && col0 + W <= g.N) {
     float t[8];
+    auto add8 = [&](int j) {  // v[j..j+8) += t, two lanes per FADD2
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) {
+        const float2 x = __fadd2_rn(make_float2(v[j + i], v[j + i + 1]), make_float2(t[i], t[i + 1]));
+        v[j + i] = x.x;
+        v[j + i + 1] = x.y;
+      }
+    };
     if (g.bias) {
 #pragma unroll
       for (int j = 0; j < W; j += 8) {
         ld8(g.bias + col0 + j, t, false);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[j + i] += t[i];
+        add8(j);
       }
     }
     if (g.beta != 0.f) {
@@ -449,8 +498,7 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
           unpack8<float>(raw, j, t);
         else
           ld8(g.residual + row * g.ld_res + col0 + j, t, false);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[j + i] += t[i];
+        add8(j);
       }
     }
     if (g.act == NNT_ACT_GELU_BWD) {
@@ -460,8 +508,17 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
           unpack8<TC>(raw, j, t);
         else
           ld8(auxb + row * g.ld_aux + col0 + j, t, false);
+        if constexpr (kFast) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_e<kFast>(t[i]);
+          for (int i = 0; i < 8; i += 2) {
+            const float2 x = __fmul2_rn(make_float2(v[j + i], v[j + i + 1]), gelu_grad2(make_float2(t[i], t[i + 1])));
+            v[j + i] = x.x;
+            v[j + i + 1] = x.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) v[j + i] *= gelu_grad_e<kFast>(t[i]);
+        }
       }
     }
   } else if (row < g.M) {
@@ -559,7 +616,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = bars + C::STAGES;
   uint64_t* tfull = bars + 2 * C::STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* inbar = tempty + 2;  // [kEpiWarps][kStageBufs]: epilogue-input TMA loads (IN_AUX_SMEM)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + kEpiWarps * kStageBufs);
+  static_assert((2 * 8 + 4 + kEpiWarps * kStageBufs) * 8 + 4 <= kBarBytes, "barrier area");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = P.g;
@@ -576,6 +635,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(smem_u32(&tfull[s]), 1);
       mbar_init(smem_u32(&tempty[s]), kEpiWarps * CG);
     }
+    for (int s = 0; s < kEpiWarps * kStageBufs; ++s) mbar_init(smem_u32(&inbar[s]), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -829,14 +889,17 @@ __global__ void __launch_bounds__(kThreads, 1)
               for (int i = 0; i < 4; ++i) mx[i] = fmaxf(mx[i], fmaxf(v[j + i], v[j + 4 + i]));
             const float m_new = fmaxf(m_run, fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])));  // finite
             const float mc = m_new * sc_c;
-            float s[8];
+            float2 s[4];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) s[i] = 0.f;
+            for (int i = 0; i < 4; ++i) s[i] = f2(0.f);
 #pragma unroll
             for (int j = 0; j < WE; j += 8)  // 2^{-inf} = 0 for the masked columns
 #pragma unroll
-              for (int i = 0; i < 8; ++i) s[i] += ex2_approx(fmaf(v[j + i], sc_c, -mc));
-            const float st = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+              for (int i = 0; i < 4; ++i) {
+                const float2 x = __ffma2_rn(make_float2(v[j + 2 * i], v[j + 2 * i + 1]), f2(sc_c), f2(-mc));
+                s[i] = __fadd2_rn(s[i], make_float2(ex2_approx(x.x), ex2_approx(x.y)));
+              }
+            const float st = ((s[0].x + s[0].y) + (s[1].x + s[1].y)) + ((s[2].x + s[2].y) + (s[3].x + s[3].y));
             l_run = fmaf(l_run, ex2_approx((m_run - m_new) * sc_c), st);
             m_run = m_new;
           }
@@ -848,7 +911,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (!row_ok) lim = 0;
           if (lim >= W) {
 #pragma unroll
-            for (int j = 0; j < W; ++j) v[j] = ex2_approx(fmaf(v[j], sc_c, -sm_ml)) * sm_inv;
+            for (int j = 0; j < W; j += 2) {
+              const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), f2(sc_c), f2(-sm_ml));
+              const float2 y = __fmul2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), f2(sm_inv));
+              v[j] = y.x;
+              v[j + 1] = y.y;
+            }
           } else {
 #pragma unroll
             for (int j = 0; j < W; ++j) v[j] = j < lim ? ex2_approx(fmaf(v[j], sc_c, -sm_ml)) * sm_inv : 0.f;
@@ -862,7 +930,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < W; j += 8) {
               unpack8<TC>(raw, j, t);
 #pragma unroll
-              for (int i = 0; i < 8; ++i) v[j + i] = g.rowscale * t[i] * (v[j + i] - dval);
+              for (int i = 0; i < 8; i += 2) {  // (rowscale * P) * (dP - D), same rounding order
+                const float2 d = __fadd2_rn(make_float2(v[j + i], v[j + i + 1]), f2(-dval));
+                const float2 y = __fmul2_rn(__fmul2_rn(make_float2(t[i], t[i + 1]), f2(g.rowscale)), d);
+                v[j + i] = y.x;
+                v[j + i + 1] = y.y;
+              }
             }
           } else {
 #pragma unroll
@@ -950,6 +1023,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                      (g.sc1 * cs) % 16 == 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    uint32_t in_phase = 0;  // IN_AUX_SMEM: bit i = phase of this warp's input barrier i
     for (int64_t t = task0; t < P.num_tasks; t += task_step) {
       TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
       const int64_t p = ti.p, q = ti.q;
@@ -969,13 +1043,30 @@ __global__ void __launch_bounds__(kThreads, 1)
       };
       Raw8 raw;
       if (can_stream(half * W)) raw_load(raw, in_ptr(half * W));  // overlaps the wait for the MMAs
+      if (P.in_kind == IN_AUX_SMEM) {
+        // TMA-load this warp's aux chunks of the tile into its staging buffers (chunk i ->
+        // buffer i) before the accumulator wait, so the loads overlap the MMAs
+        if (lane == 0) {
+          bulk_wait_read0();  // earlier TMA stores have finished reading the buffers
+          int i = 0;
+          for (int c = half * W; c < BN && ti.n0 + c < g.N; c += 2 * W, ++i) {
+            const uint32_t bar = smem_u32(&inbar[(warp - 2) * kStageBufs + i]);
+            mbar_expect_tx(bar, kStageBytesPerWarp);
+            tma_load_4d(smem_u32(stage_base + i * kStageBytesPerWarp), &tmAux, bar, (int)(ti.n0 + c),
+                        (int)(ti.m0 + quad * 32), (int)q, (int)p);
+          }
+        }
+        __syncwarp();
+        ring = 0;
+      }
       mbar_wait(smem_u32(&tfull[acc]), acc_phase);
       tc_fence_after();
       const bool has_k = ti.kb_end > ti.kb_begin;
       const float dval =
           (g.act == NNT_ACT_SOFTMAX_BWD && row < g.M) ? __ldg(g.rowvec + ti.bz * g.M + row) : 0.f;
+      int ci = 0;  // chunk index within the tile (IN_AUX_SMEM: its staging buffer)
 #pragma unroll 1
-      for (int c = half * W; c < BN; c += 2 * W) {
+      for (int c = half * W; c < BN; c += 2 * W, ++ci) {
         if (ti.n0 + c >= g.N) break;  // warp-uniform
         float v[W];
 #pragma unroll
@@ -994,7 +1085,14 @@ __global__ void __launch_bounds__(kThreads, 1)
           stage_and_store(&tmAux, v, true, cx, cy, (int)ti.split, 0);
           continue;
         }
-        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, can_stream(c) ? P.in_kind : IN_NONE, raw, v);
+        int kind = can_stream(c) ? P.in_kind : IN_NONE;
+        if (P.in_kind == IN_AUX_SMEM) {  // the aux chunk landed in staging buffer ci (== ring)
+          mbar_wait(smem_u32(&inbar[(warp - 2) * kStageBufs + ci]), (in_phase >> ci) & 1u);
+          in_phase ^= 1u << ci;
+          unstage_row(raw, stage_base + ci * kStageBytesPerWarp, lane);
+          kind = IN_AUX;
+        }
+        epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, kind, raw, v);
         if (can_stream(c + 2 * W)) raw_load(raw, in_ptr(c + 2 * W));  // next chunk's input, in flight meanwhile
         if (g.row_stats != nullptr && row < g.M) {
           // fused softmax subroutine 1: (max, sumexp) of this row over the chunk's
@@ -1020,8 +1118,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_store(&tmAux);
           else
             direct_store<TC, W>(g.M, g.N, g.ld_aux, auxb, row, ti.n0 + c, v);
+          if constexpr (sizeof(TC) == 2) {
 #pragma unroll
-          for (int j = 0; j < W; ++j) v[j] = gelu_e<sizeof(TC) == 2>(v[j]);
+            for (int j = 0; j < W; j += 2) {
+              const float2 x = gelu2(make_float2(v[j], v[j + 1]));
+              v[j] = x.x;
+              v[j + 1] = x.y;
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < W; ++j) v[j] = gelu_e<false>(v[j]);
+          }
         }
         if (P.tma_store)
           stage_store(&tmC);
@@ -1236,7 +1343,10 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   if (P.ws_mode || EPI != EPI_GENERIC)
     P.in_kind = IN_NONE;
   else if (a.act == NNT_ACT_GELU_BWD)
-    P.in_kind = IN_AUX;
+    P.in_kind = sizeof(TC) == 2 && c_tma_ok(a, sizeof(TC)) && aligned16(a.aux) &&
+                        (a.ld_aux * (int64_t)sizeof(TC)) % 16 == 0
+                    ? IN_AUX_SMEM  // bf16: the register prefetch would spill; stage it through smem
+                    : IN_AUX;
   else if (a.residual && sizeof(TC) == 4)
     P.in_kind = IN_RESIDUAL;
   else if (a.beta != 0.f)
@@ -1275,7 +1385,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.tma_store = tma_ok ? 1 : 0;
     if (tma_ok) {
       NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
-      if (a.act == NNT_ACT_GELU)
+      if (a.act == NNT_ACT_GELU || P.in_kind == IN_AUX_SMEM)  // GELU pre-activation out / GELU' aux in
         NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
     }
   }
