@@ -784,6 +784,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     // columns per chunk: a 128-byte staging row of C, or (ROWSTATS, no C) 64 columns so one
     // wait covers two TMEM loads and the exp chain has twice the independent work
     constexpr int WE = EPI == EPI_ROWSTATS ? 64 : W;
+    static_assert(EPI != EPI_DA || BN == 2 * W, "EPI_DA: one P chunk per epilogue warp and task");
+    // EPI_DA: P chunk loads (TMA, aux map) into this warp's staging buffer b
+    int da_buf = 0;
+    uint32_t da_phase = 0;
+    auto da_load = [&](const TileInfo& tt, int b) {
+      const uint32_t bar = smem_u32(&inbar[(warp - 2) * kStageBufs + b]);
+      mbar_expect_tx(bar, kStageBytesPerWarp);
+      tma_load_4d(smem_u32(stage_base + b * kStageBytesPerWarp), &tmAux, bar, (int)tt.n0 + half * W,
+                  (int)tt.m0 + quad * 32, tt.q, tt.p);
+    };
+    if constexpr (EPI == EPI_DA) {
+      if (lane == 0 && task0 < P.num_tasks) da_load(decode_task(P, task0, BN), 0);
+    }
     for (int64_t t = task0, sub = 0; t < P.num_tasks;
          sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
       TileInfo ti = decode_task(P, t, BN, BM, 0, sub);
@@ -792,13 +805,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool row_ok = row_in < g.M;
       const int cy = (int)ti.m0 + quad * 32;
       const int c_first = half * WE;
-      // EPI_DA: P row pointer of this lane and the prefetch of its first chunk
-      const TC* prow = nullptr;
-      Raw8 raw;  // P of the next chunk (128 bytes of this lane's row)
+      // EPI_DA: this warp's P chunk of the task (BN == 2W: one chunk per warp) arrives by TMA in
+      // staging buffer da_buf, loaded during the previous task; the next task's chunk is
+      // prefetched into the other buffer now, once the store that last used it has read it
+      Raw8 raw;
       float dval = 0.f;
       if constexpr (EPI == EPI_DA) {
-        prow = (const TC*)g.aux + p * g.sc0 + q * g.sc1 + (int64_t)row_in * g.ld_aux + ti.n0;
-        if (row_ok && ti.n0 + c_first + W <= g.N) raw_load(raw, prow + c_first);
+        if (lane == 0) {
+          bulk_wait_read0();
+          const int64_t tn = t + task_step;
+          if (tn < P.num_tasks) da_load(decode_task(P, tn, BN), da_buf ^ 1);
+        }
+        __syncwarp();
         dval = row_ok ? __ldg(g.rowvec + ti.bz * g.M + row_in) : 0.f;
       }
       // EPI_SOFTMAX: the row's (M, S) from the statistics pass
@@ -922,29 +940,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < W; ++j) v[j] = j < lim ? ex2_approx(fmaf(v[j], sc_c, -sm_ml)) * sm_inv : 0.f;
           }
         } else {
-          // dA = rowscale * P * (dP - D); P of this chunk was prefetched into raw
-          const bool full = row_ok && col0 + W <= g.N;
-          if (full) {
-            float t[8];
+          // dA = rowscale * P * (dP - D) with P from staging buffer da_buf (zero-filled past M / N;
+          // those outputs are clipped by the TMA store)
+          mbar_wait(smem_u32(&inbar[(warp - 2) * kStageBufs + da_buf]), (da_phase >> da_buf) & 1u);
+          da_phase ^= 1u << da_buf;
+          unstage_row(raw, stage_base + da_buf * kStageBytesPerWarp, lane);
+          float t[8];
 #pragma unroll
-            for (int j = 0; j < W; j += 8) {
-              unpack8<TC>(raw, j, t);
+          for (int j = 0; j < W; j += 8) {
+            unpack8<TC>(raw, j, t);
 #pragma unroll
-              for (int i = 0; i < 8; i += 2) {  // (rowscale * P) * (dP - D), same rounding order
-                const float2 d = __fadd2_rn(make_float2(v[j + i], v[j + i + 1]), f2(-dval));
-                const float2 y = __fmul2_rn(__fmul2_rn(make_float2(t[i], t[i + 1]), f2(g.rowscale)), d);
-                v[j + i] = y.x;
-                v[j + i + 1] = y.y;
-              }
+            for (int i = 0; i < 8; i += 2) {  // (rowscale * P) * (dP - D), same rounding order
+              const float2 d = __fadd2_rn(make_float2(v[j + i], v[j + i + 1]), f2(-dval));
+              const float2 y = __fmul2_rn(__fmul2_rn(make_float2(t[i], t[i + 1]), f2(g.rowscale)), d);
+              v[j + i] = y.x;
+              v[j + i + 1] = y.y;
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < W; ++j)
-              v[j] = (row_ok && col0 + j < g.N) ? g.rowscale * ld_elem(prow + c + j) * (v[j] - dval) : 0.f;
           }
-          // prefetch the next chunk's P; it lands while this chunk is staged and stored
-          const int cn = c + 2 * W;
-          if (cn < BN && row_ok && ti.n0 + cn + W <= g.N) raw_load(raw, prow + cn);
+          ring = da_buf;  // the output overwrites P in place
         }
         if constexpr (EPI != EPI_ROWSTATS) {  // (ROWSTATS has no C)
           // stage + TMA store (2-buffer ring per warp)
@@ -968,6 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc = 0;
         acc_phase ^= 1;
       }
+      if constexpr (EPI == EPI_DA) da_buf ^= 1;
       if constexpr (EPI == EPI_ROWSTATS) {
         if (sub + 1 == task_subtiles(P, t, BN)) {
           // task end: half 1 publishes its (m, l); half 0 merges both and writes the row's stats
@@ -1385,7 +1399,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.tma_store = tma_ok ? 1 : 0;
     if (tma_ok) {
       NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
-      if (a.act == NNT_ACT_GELU || P.in_kind == IN_AUX_SMEM)  // GELU pre-activation out / GELU' aux in
+      if (a.act == NNT_ACT_GELU || P.in_kind == IN_AUX_SMEM || EPI == EPI_DA)  // GELU out / GELU', P in
         NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
     }
   }
@@ -1482,7 +1496,8 @@ template <typename TC>
 nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   const bool tma_ok = splits == 1 && c_tma_ok(a, sizeof(TC));
   if constexpr (sizeof(TC) == 2) {
-    if (tma_ok && a.act == NNT_ACT_SOFTMAX_BWD) return launch_bn<128, TC, EPI_DA>(a, s, 1);
+    if (tma_ok && a.act == NNT_ACT_SOFTMAX_BWD && aligned16(a.aux) && (a.ld_aux * 2) % 16 == 0)
+      return launch_bn<128, TC, EPI_DA>(a, s, 1);  // P staged by TMA a task ahead
     if (a.act == NNT_ACT_SOFTMAX) return launch_bn<128, TC, EPI_SOFTMAX>(a, s, 1);
   } else {
     if (tma_ok && a.act == NNT_ACT_NONE && !a.bias && !a.residual && a.beta == 0.f &&
