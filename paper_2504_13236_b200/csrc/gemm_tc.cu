@@ -44,20 +44,39 @@ constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory
 // and staging buffer an epilogue-input TMA barrier (kEpiWarps * kStageBufs), the TMEM slot
 constexpr int kBarBytes = 512;
 
+// Epilogue specialisations (separate instantiations keep each one small and branch-light):
+//   EPI_GENERIC  bias / beta*C / residual / GELU / GELU' / split-K partials
+//   EPI_SCORES   fp32 C = alpha*acc (attention scores) + optional fused per-32-key-tile
+//                (max, sumexp) (softmax subroutine 1, P:172-173)
+//   EPI_DA       bf16 C = rowscale * P * (acc - D[row]) (softmax backward), P staged by TMA a
+//                task ahead
+//   EPI_ROWSTATS per-row (max, sumexp) over all key tiles of a row block (ORDER_ROWS tasks),
+//                no C (softmax subroutine 1 with on-chip aggregation, R26)
+//   EPI_SOFTMAX  bf16 C = e^{alpha*acc - M} / S from the row's stats (subroutine 2, R26)
+enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4 };
+
 // CG = CTAs per MMA (tcgen05 cta_group): 1, or 2 = an SM pair computing a 256 x BN tile
 // (each CTA stages its 128 A rows and half of the BN B rows; the leader issues M=256 MMAs).
-template <int BN, int CG = 1>
+// CTAS = CTAs resident per SM: the softmax passes (K = 64: one K block per tile, MUFU/latency-
+// bound epilogues) run two CTAs per SM for twice the epilogue warps, in <= 113 KB each with
+// fewer stages and one staging buffer per warp.
+template <int BN, int CG = 1, int EPI = EPI_GENERIC>
 struct Cfg {
+  static constexpr int CTAS = (EPI == EPI_ROWSTATS || EPI == EPI_SOFTMAX) ? 2 : 1;
+  static constexpr int BUFS = CTAS == 2 ? 1 : kStageBufs;  // staging buffers per epilogue warp
+  static constexpr int SMEM_LIMIT = CTAS == 2 ? 113 * 1024 : kMaxSmem;
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = (BN / CG) * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int EPI_BYTES = kEpiWarps * kStageBufs * kStageBytesPerWarp;
-  static constexpr int STAGES_FIT = (kMaxSmem - EPI_BYTES - 1024 - kBarBytes) / STAGE_BYTES;
+  // ROWSTATS: no C staging, only the half-merge exchange slots (2 x BM float2)
+  static constexpr int EPI_BYTES = EPI == EPI_ROWSTATS ? 2 * BM * 8 : kEpiWarps * BUFS * kStageBytesPerWarp;
+  static constexpr int STAGES_FIT = (SMEM_LIMIT - EPI_BYTES - 1024 - kBarBytes) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
   static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + kBarBytes;
-  static_assert(SMEM_BYTES <= kMaxSmem, "shared memory budget");
+  static_assert(STAGES >= 2 && SMEM_BYTES <= SMEM_LIMIT, "shared memory budget");
+  static_assert(CTAS * TMEM_COLS <= 512, "TMEM columns per SM");
 };
 
 enum TileOrder { ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3, ORDER_ROWS = 4 };
@@ -249,6 +268,26 @@ __device__ __forceinline__ int64_t task_subtiles(const TcParams& P, int64_t t, i
   if (P.g.causal == NNT_CAUSAL_OUT_LOWER) return min(P.nt, ((mb + 1) * BM + bn - 1) / bn);
   return P.nt;
 }
+
+// The static persistent schedule, walked identically by the producer, MMA and epilogue roles:
+// CTA (pair) c of G takes task k*G + c in even rounds k and k*G + G-1-c in odd rounds
+// (boustrophedon), which balances the heaviest-first causal orders; ORDER_ROWS tasks are
+// walked tile by tile (sub).
+struct TaskIter {
+  int64_t c, G, k, t, sub;
+  __device__ __forceinline__ TaskIter(int64_t c_, int64_t G_) : c(c_), G(G_), k(0), t(c_), sub(0) {}
+  __device__ __forceinline__ static int64_t at(int64_t c, int64_t G, int64_t k) {
+    return k * G + ((k & 1) ? (G - 1 - c) : c);
+  }
+  __device__ __forceinline__ int64_t next_task() const { return at(c, G, k + 1); }
+  __device__ __forceinline__ void next(const TcParams& P, int bn) {
+    if (++sub >= task_subtiles(P, t, bn)) {
+      sub = 0;
+      ++k;
+      t = at(c, G, k);
+    }
+  }
+};
 
 // Which tile a task computes and which K-blocks it covers (nnt_causal semantics + split-K).
 struct TileInfo {
@@ -585,16 +624,6 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
 }
 
 // ------------------------------------------------------------------ kernel
-// Epilogue specialisations (separate instantiations keep each one small and branch-light):
-//   EPI_GENERIC  bias / beta*C / residual / GELU / GELU' / split-K partials
-//   EPI_SCORES   fp32 C = alpha*acc (attention scores) + optional fused per-32-key-tile
-//                (max, sumexp) (softmax subroutine 1, P:172-173)
-//   EPI_DA       bf16 C = rowscale * P * (acc - D[row]) (softmax backward), P prefetched a
-//                chunk ahead
-//   EPI_ROWSTATS per-row (max, sumexp) over all key tiles of a row block (ORDER_ROWS tasks),
-//                no C (softmax subroutine 1 with on-chip aggregation, R26)
-//   EPI_SOFTMAX  bf16 C = e^{alpha*acc - M} / S from the row's stats (subroutine 2, R26)
-enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4 };
 
 // CG = 2: launched as clusters of 2 CTAs (an SM pair).  Task = 256 x BN output tile; rank r
 // stages A rows [m0 + 128 r, +128) and B rows [n0 + r BN/2, +BN/2) and drains its own TMEM
@@ -602,12 +631,13 @@ enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EP
 // (expect_tx of both CTAs' bytes) and issues the M=256 MMAs; the peer's epilogue warps arrive
 // on the leader's TMEM-empty barrier.
 template <int BN, typename TC, int EPI, int CG = 1>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
                    const __grid_constant__ CUtensorMap tmAux) {
   static_assert(CG == 1 || (CG == 2 && EPI == EPI_GENERIC && (BN / 2) % 64 == 0), "CTA-pair configuration");
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
+  static_assert(EPI != EPI_DA || C::BUFS == 2, "EPI_DA double-buffers P");
   constexpr int W = 128 / (int)sizeof(TC);  // columns per 128-byte staging row
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -666,9 +696,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int64_t t = task0, sub = 0; t < P.num_tasks;
-           sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
-        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off, sub);
+      for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
+        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
         const int p = ti.p, q = ti.q;
         const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
@@ -728,9 +757,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       // apart; +2 KB per UMMA_K=16.
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
-      for (int64_t t = task0, sub = 0; t < P.num_tasks;
-           sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
-        TileInfo ti = decode_task(P, t, BN, BM * CG, row_off, sub);
+      for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
+        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -771,7 +799,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================== specialised epilogues (attention score-type GEMMs)
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * kStageBufs * kStageBytesPerWarp;
+    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * C::BUFS * kStageBytesPerWarp;
     int ring = 0;
     const float L2E = 1.4426950408889634f;
     int acc = 0;
@@ -797,8 +825,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (EPI == EPI_DA) {
       if (lane == 0 && task0 < P.num_tasks) da_load(decode_task(P, task0, BN), 0);
     }
-    for (int64_t t = task0, sub = 0; t < P.num_tasks;
-         sub = sub + 1 < task_subtiles(P, t, BN) ? sub + 1 : 0, t += sub == 0 ? task_step : 0) {
+    for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
+      const int64_t t = it.t, sub = it.sub;
       TileInfo ti = decode_task(P, t, BN, BM, 0, sub);
       const int p = ti.p, q = ti.q;
       const int row_in = (int)ti.m0 + quad * 32 + lane;  // row of this lane within the batch item
@@ -813,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if constexpr (EPI == EPI_DA) {
         if (lane == 0) {
           bulk_wait_read0();
-          const int64_t tn = t + task_step;
+          const int64_t tn = it.next_task();  // (EPI_DA tasks are single tiles)
           if (tn < P.num_tasks) da_load(decode_task(P, tn, BN), da_buf ^ 1);
         }
         __syncwarp();
@@ -962,7 +990,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (EPI != EPI_ROWSTATS) {  // (ROWSTATS has no C)
           // stage + TMA store (2-buffer ring per warp)
           uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::BUFS - 1) : "memory");
           __syncwarp();
           stage_row<TC, W>(buf, lane, v);
           fence_async_smem();
@@ -971,7 +999,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_4d(&tmC, smem_u32(buf), col0, cy, q, p);
             bulk_commit();
           }
-          ring ^= 1;
+          ring = ring + 1 == C::BUFS ? 0 : ring + 1;
         }
       }
       tc_fence_before();
@@ -1008,14 +1036,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // the two warps of a quadrant take alternating 128-byte column chunks
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
-    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * kStageBufs * kStageBytesPerWarp;
+    uint8_t* const stage_base = smem + C::EPI_OFF + (warp - 2) * C::BUFS * kStageBytesPerWarp;
     int ring = 0;
     // Stage one 32-row x 128-byte chunk and issue its TMA store; before refilling a buffer,
     // at most kStageBufs-1 earlier stores (those reading the other buffers) may be in flight.
     auto stage_and_store = [&](const CUtensorMap* map, const auto& vals, bool as_f32, int c0, int c1, int c2,
                                int c3) {
       uint8_t* buf = stage_base + ring * kStageBytesPerWarp;
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kStageBufs - 1) : "memory");
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(C::BUFS - 1) : "memory");
       __syncwarp();
       if (as_f32)
         stage_row<float, W>(buf, lane, vals);
@@ -1027,7 +1055,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_store_4d(map, smem_u32(buf), c0, c1, c2, c3);
         bulk_commit();
       }
-      ring = ring + 1 == kStageBufs ? 0 : ring + 1;
+      ring = ring + 1 == C::BUFS ? 0 : ring + 1;
     };
     const size_t cs = sizeof(TC);
     auto a16 = [](const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 15u) == 0; };
@@ -1038,8 +1066,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t in_phase = 0;  // IN_AUX_SMEM: bit i = phase of this warp's input barrier i
-    for (int64_t t = task0; t < P.num_tasks; t += task_step) {
-      TileInfo ti = decode_task(P, t, BN, BM * CG, row_off);
+    for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
+      TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off);
       const int64_t p = ti.p, q = ti.q;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
@@ -1312,7 +1340,7 @@ int64_t pair_units() {
 
 template <int BN, typename TC, int EPI, int CG = 1>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
-  using C = Cfg<BN, CG>;
+  using C = Cfg<BN, CG, EPI>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
@@ -1404,7 +1432,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     }
   }
   if constexpr (CG == 1) {
-    const int64_t units = num_sms();  // persistent: one CTA per SM
+    const int64_t units = num_sms() * C::CTAS;  // persistent: C::CTAS CTAs per SM
     int64_t grid = P.num_tasks < units ? P.num_tasks : units;
     if (grid < 1) grid = 1;
     gemm_tc_kernel<BN, TC, EPI, 1><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
