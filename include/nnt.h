@@ -148,6 +148,13 @@ typedef struct {
   int64_t ld_row_stats;   /* in (max, sumexp) pairs, >= ceil(N / 32) */
   const float* rowvec;    /* NNT_ACT_SOFTMAX_BWD: per-row D, indexed (p*batch1 + q)*M + i */
   float rowscale;         /* NNT_ACT_SOFTMAX_BWD: output scale                            */
+  /* Row sums of op(A), fused into the GEMM (R27): a_rowsum[i] = beta * a_rowsum[i] +
+   * alpha * sum_k op(A)[i][k], device fp32 [M], or NULL = off.  With A = dY^T (the dW = dY^T X
+   * GEMM of a linear layer) this is the bias gradient db = sum over tokens of dY,
+   * computed by the tensor cores against a ones vector from the bf16 operand the GEMM already
+   * stages.  bf16 operands, unbatched, non-causal, no activation; it uses the GEMM's split-K
+   * workspace when the GEMM splits K (nnt_tile_gemm_workspace_bytes includes its slices). */
+  float* a_rowsum;
 } nnt_epilogue;
 
 /* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would

@@ -18,7 +18,8 @@ extern "C" size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K,
   g.batch0 = batch_items > 0 ? batch_items : 1;
   g.batch1 = 1;
   const int64_t s = gemm_tc_splits(g);
-  return s > 1 ? (size_t)s * (size_t)M * (size_t)N * sizeof(float) : 0;
+  // split partials of C, then of the a_rowsum row sums (R27)
+  return s > 1 ? (size_t)s * ((size_t)M * (size_t)N + (size_t)M) * sizeof(float) : 0;
 }
 
 extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const int64_t* batch,
@@ -103,6 +104,11 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.ld_stats = epi->ld_row_stats;
     g.rowvec = epi->rowvec;
     g.rowscale = epi->rowscale;
+    g.a_rowsum = epi->a_rowsum;
+    NNT_REQUIRE(!epi->a_rowsum || (a_dtype == NNT_BF16 && b0 == 1 && b1 == 1 && epi->causal == NNT_CAUSAL_NONE &&
+                                   epi->act == NNT_ACT_NONE && !epi->row_stats),
+                NNT_ERR_UNSUPPORTED,
+                "nnt_tile_gemm: a_rowsum needs bf16 operands, an unbatched non-causal GEMM, no activation");
     NNT_REQUIRE(!epi->row_stats || sm || (a_dtype == NNT_BF16 && c_dtype == NNT_F32 && epi->act == NNT_ACT_NONE &&
                                     epi->ld_row_stats >= (N + 31) / 32 &&
                                     (epi->causal == NNT_CAUSAL_NONE || epi->causal == NNT_CAUSAL_OUT_LOWER)),
@@ -118,7 +124,8 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
   const bool sm_act = g.act == NNT_ACT_ROWSTATS || g.act == NNT_ACT_SOFTMAX;
   const double bytes = ((double)M * K * es + (double)K * N * es) * b0 * b1 * (g.causal == NNT_CAUSAL_NONE ? 1.0 : 0.5) +
                        c_bytes + (g.residual ? 4.0 * M * N : 0.0) +
-                       (g.aux ? (double)M * N * dtype_size(c_dtype) : 0.0) + (sm_act ? 8.0 * M * b0 * b1 : 0.0);
+                       (g.aux ? (double)M * N * dtype_size(c_dtype) : 0.0) + (sm_act ? 8.0 * M * b0 * b1 : 0.0) +
+                       (g.a_rowsum ? 4.0 * M * (beta != 0.f ? 2.0 : 1.0) : 0.0);
   if (a_dtype == NNT_F32) {
     LaunchScope sc(NNT_K_GEMM_SIMT, stream, bytes, flops);
     return gemm_simt_launch(g, stream);

@@ -31,6 +31,7 @@ struct GemmArgs {
   int64_t ld_stats;  // pairs per row
   const float* rowvec;  // NNT_ACT_SOFTMAX_BWD: D per row
   float rowscale;
+  float* a_rowsum;  // R27: beta * a_rowsum + alpha * sum_k op(A)[i][k] (bias gradient of dW GEMMs)
 };
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);

@@ -41,8 +41,12 @@ constexpr int kStageBytesPerWarp = 4096;  // 32 rows x 128 B, SW128 staging for 
 constexpr int kStageBufs = 2;             // staging ring per epilogue warp (one store in flight while refilling)
 constexpr int kMaxSmem = 232448;          // 227 KB opt-in dynamic shared memory per CTA
 // mbarriers: full/empty per stage (<= 8 each), TMEM full/empty (2 each), per epilogue warp
-// and staging buffer an epilogue-input TMA barrier (kEpiWarps * kStageBufs), the TMEM slot
-constexpr int kBarBytes = 512;
+// and staging buffer an epilogue-input TMA barrier (kEpiWarps * kStageBufs), the TMEM slot;
+// then (at kOnesOff) the all-ones B tile of the a_rowsum MMA (R27): 16 x 16 bf16, K-major,
+// no swizzle (4 core matrices of 8 rows x 16 B).
+constexpr int kOnesOff = 512;
+constexpr int kOnesBytes = 512;
+constexpr int kBarBytes = kOnesOff + kOnesBytes;
 
 // Epilogue specialisations (separate instantiations keep each one small and branch-light):
 //   EPI_GENERIC  bias / beta*C / residual / GELU / GELU' / split-K partials
@@ -72,7 +76,11 @@ struct Cfg {
   static constexpr int EPI_BYTES = EPI == EPI_ROWSTATS ? 2 * BM * 8 : kEpiWarps * BUFS * kStageBytesPerWarp;
   static constexpr int STAGES_FIT = (SMEM_LIMIT - EPI_BYTES - 1024 - kBarBytes) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-  static constexpr int TMEM_COLS = 2 * BN <= 32 ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  // generic epilogue with BN <= 192: 32 more columns hold the a_rowsum accumulators (R27), 16 per
+  // TMEM accumulator buffer
+  static constexpr bool ROWSUM = EPI == EPI_GENERIC && 2 * BN + 32 <= 512;
+  static constexpr int TCOLS = 2 * BN + (ROWSUM ? 32 : 0);
+  static constexpr int TMEM_COLS = TCOLS <= 32 ? 32 : (TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512)));
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
   static constexpr int SMEM_BYTES = EPI_OFF + EPI_BYTES + 1024 /*align*/ + kBarBytes;
   static_assert(STAGES >= 2 && SMEM_BYTES <= SMEM_LIMIT, "shared memory budget");
@@ -103,6 +111,8 @@ struct TcParams {
   int64_t splits, kb_per_split;
   FastDiv f_splits, f_tpb, f_mt, f_nt, f_nbat, f_level, f_b1;  // divisors of the task decode
   uint32_t idesc;
+  uint32_t idesc_ones;  // a_rowsum MMA: N = 16, B (ones) K-major
+  int rowsum;           // a_rowsum requested (R27)
   int a_kmajor, b_kmajor;
   int tma_store;  // epilogue stores through TMA (C / aux / workspace maps valid)
   int order;      // TileOrder
@@ -248,6 +258,23 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// No-swizzle K-major descriptor (core matrices of 8 rows x 16 B; lbo / sbo between core matrices
+// along K / along M-N).  Only the all-ones a_rowsum tile uses it, whose bytes are all equal.
+__device__ __forceinline__ uint64_t make_sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell); layout type 0 = SWIZZLE_NONE
+  return d;
+}
+__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
+  uint32_t r;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return __uint_as_float(r);
 }
 
 // SW128 shared-memory matrix descriptor (sm_100 "version 1" format).
@@ -648,13 +675,21 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
   uint64_t* tempty = tfull + 2;
   uint64_t* inbar = tempty + 2;  // [kEpiWarps][kStageBufs]: epilogue-input TMA loads (IN_AUX_SMEM)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inbar + kEpiWarps * kStageBufs);
-  static_assert((2 * 8 + 4 + kEpiWarps * kStageBufs) * 8 + 4 <= kBarBytes, "barrier area");
+  static_assert((2 * 8 + 4 + kEpiWarps * kStageBufs) * 8 + 4 <= kOnesOff, "barrier area");
+  uint8_t* const ones = reinterpret_cast<uint8_t*>(bars) + kOnesOff;  // a_rowsum B operand (R27)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = P.g;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
   const int row_off = (int)rank * BM;
   const int64_t task0 = blockIdx.x / CG, task_step = gridDim.x / CG;
+
+  if constexpr (C::ROWSUM) {
+    if (P.rowsum && warp == 2) {  // bf16 ones (0x3F80), visible to the tensor cores (async proxy)
+      reinterpret_cast<uint4*>(ones)[lane] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+      fence_async_smem();
+    }
+  }
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
@@ -775,6 +810,18 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
               mma_bf16_pair(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
             else
               mma_bf16(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+            if constexpr (C::ROWSUM) {
+              // R27: sum_k op(A)[i][k] = op(A) x ones, into 16 columns past the two accumulators
+              // (the first N tile of each row block only)
+              if (P.rowsum && ti.n0 == 0) {
+                const uint64_t od = make_sdesc_noswz(smem_u32(ones), 128u, 256u);
+                const uint32_t tr = tmem_base + (uint32_t)(2 * BN + acc * 16);
+                if constexpr (CG == 2)
+                  mma_bf16_pair(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+                else
+                  mma_bf16(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+              }
+            }
           }
           if constexpr (CG == 2)
             mma_commit_pair(smem_u32(&empty[stage]));
@@ -1177,6 +1224,19 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         else
           direct_store<TC, W>(g.M, g.N, g.ldc, Cb, row, ti.n0 + c, v);
       }
+      if constexpr (C::ROWSUM) {
+        // R27: this row's sum of op(A) over the task's K range (one warp per lane quadrant)
+        if (P.rowsum && ti.n0 == 0 && half == 0) {
+          float rv = has_k ? tmem_ld1(tmem_base + (uint32_t)(2 * BN + acc * 16) + ((uint32_t)(quad * 32) << 16)) : 0.f;
+          if (row < g.M) {
+            rv *= g.alpha;
+            if (P.ws_mode)  // split partial, after the C partials; the reduce adds them in split order
+              ((float*)g.workspace)[P.splits * g.M * g.N + ti.split * g.M + row] = rv;
+            else
+              g.a_rowsum[row] = g.beta != 0.f ? fmaf(g.beta, g.a_rowsum[row], rv) : rv;
+          }
+        }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -1215,9 +1275,18 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restrict__ ws, int64_t splits, int64_t M,
                                                             int64_t N, float* C, int64_t ldc, float beta,
                                                             const float* __restrict__ bias,
-                                                            const float* __restrict__ residual, int64_t ld_res) {
+                                                            const float* __restrict__ residual, int64_t ld_res,
+                                                            float* __restrict__ rowsum) {
   const int64_t nq = N / 4;  // N % 4 == 0 (checked on the host)
   const int64_t total = M * nq;
+  if (rowsum) {  // R27: a_rowsum = beta * a_rowsum + sum_s partial_s (slices after the C partials)
+    const float* wsr = ws + splits * M * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (int64_t)gridDim.x * blockDim.x) {
+      float s = __ldcg(wsr + i);
+      for (int64_t k = 1; k < splits; ++k) s += __ldcg(wsr + k * M + i);
+      rowsum[i] = beta != 0.f ? fmaf(beta, rowsum[i], s) : s;
+    }
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / nq, c = (i % nq) * 4;
     float4 s = __ldcg(reinterpret_cast<const float4*>(ws + r * N + c));
@@ -1397,6 +1466,10 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.in_kind = IN_NONE;
   P.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((P.b_kmajor ? 0u : 1u) << 16) |
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
+  P.idesc_ones = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((uint32_t)(16 >> 3) << 17) |
+                 ((uint32_t)((BM * CG) >> 4) << 24);
+  P.rowsum = a.a_rowsum != nullptr ? 1 : 0;
+  NNT_REQUIRE(!P.rowsum || C::ROWSUM, NNT_ERR_UNSUPPORTED, "gemm(bf16): a_rowsum needs a tile width <= 192");
   CUtensorMap tmA, tmB, tmC, tmAux;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   if (P.a_kmajor)
@@ -1460,7 +1533,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     int64_t blocks = cdiv(total, 256);
     if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
     splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>((const float*)a.workspace, splits, a.M, a.N, (float*)a.C,
-                                                          a.ldc, a.beta, a.bias, a.residual, a.ld_res);
+                                                          a.ldc, a.beta, a.bias, a.residual, a.ld_res,
+                                                          P.rowsum ? a.a_rowsum : nullptr);
     NNT_TRY(check_launch("gemm_tc splitk reduce"));
   }
   return NNT_OK;
@@ -1532,6 +1606,14 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
         (a.row_stats || a.causal == NNT_CAUSAL_OUT_LOWER))
       return launch_bn<128, TC, EPI_SCORES>(a, s, 1);
   }
+  if (a.a_rowsum) {  // R27: tiles <= 192 wide leave TMEM columns for the row-sum accumulators
+    if (use_pair(a)) return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+    switch (choose_bn(a)) {
+      case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
+      case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
+      default: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);
+    }
+  }
   if (use_pair(a)) {
     double cost_pair = 0, cost_single = 0;
     const int bnp = choose_bn_pair(a, &cost_pair);
@@ -1559,9 +1641,17 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
               NNT_ERR_ALIGN, "gemm(bf16): batch strides must be positive multiples of 8");
   NNT_REQUIRE(a.M < (1ll << 31) && a.N < (1ll << 31) && a.K < (1ll << 31), NNT_ERR_UNSUPPORTED,
               "gemm(bf16): dims must fit int32 TMA coordinates");
-  int64_t splits = gemm_tc_splits(a);
+  int64_t splits = gemm_tc_splits(a);  // the workspace is sized for this split count
+  if (a.a_rowsum && splits > 1) {
+    // row-sum GEMMs run 128-wide tiles (pairs when M >= 256): refit the split to that grid
+    const bool pair = use_pair(a);
+    const int64_t units = pair ? pair_units() : num_sms();
+    const int64_t tiles = cdiv(a.M, BM * (pair ? 2 : 1)) * cdiv(a.N, 128);
+    int64_t s2 = units / tiles;
+    splits = s2 < 1 ? 1 : (s2 < splits ? s2 : splits);
+  }
   const bool ws_ok = a.workspace && (reinterpret_cast<uintptr_t>(a.workspace) & 15u) == 0 &&
-                     a.workspace_bytes >= (size_t)splits * a.M * a.N * sizeof(float) &&
+                     a.workspace_bytes >= (size_t)splits * (a.M * a.N + (a.a_rowsum ? a.M : 0)) * sizeof(float) &&
                      (reinterpret_cast<uintptr_t>(a.C) & 15u) == 0 && a.ldc % 4 == 0 &&
                      (!a.residual || ((reinterpret_cast<uintptr_t>(a.residual) & 15u) == 0 && a.ld_res % 4 == 0)) &&
                      (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);

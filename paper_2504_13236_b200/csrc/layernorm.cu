@@ -1,6 +1,7 @@
 // LayerNorm forward / backward.  HBM-bound row kernels.
 //   E <= 1024: one WARP per token row (row in registers as float4, reductions by
-//              warp shuffle only), 8 rows per 256-thread CTA;
+//              warp shuffle only); forward warps stride over rows with the next row
+//              prefetched, backward CTAs own a block of rows (single pass);
 //   E  > 1024: one 128-thread CTA per row (shuffle + 4-entry shared array).
 // The backward's dgamma/dbeta are per-CTA column partials (rows of a CTA are
 // accumulated in a fixed order) merged by the deterministic column merge
@@ -11,7 +12,6 @@ namespace nnt {
 namespace {
 
 constexpr int kWarpRowsPerCta = 8;   // warp kernels: 8 warps
-constexpr int kWarpBwdRows = 16;     // warp bwd kernel: rows per CTA (= per partial)
 constexpr int kT = 128;              // CTA-per-row kernels: threads
 constexpr int kCtaBwdRows = 16;      // CTA-per-row bwd kernel: rows per partial
 
@@ -51,43 +51,58 @@ __device__ __forceinline__ float4 affine(float4 v, float4 g, float4 b, float mu,
 // ------------------------------------------------------------------ forward, warp per row
 // Step 1 with shifted sums (c = x[row][0], R9); E-tile partials are merged by
 // summation, which is what the (fixed-order) shuffle reduction computes.
+// Warps stride over rows (row = warp id + k * total warps) with the next row's loads issued
+// before the current row's reduction, so reads and writes of neighbouring rows overlap.
 template <typename TO, int NV>
 __global__ void __launch_bounds__(32 * kWarpRowsPerCta)
     ln_fwd_warp(const float* __restrict__ x, int64_t T, int E, int64_t ldx, const float* __restrict__ gamma,
                 const float* __restrict__ beta, float eps, TO* __restrict__ y, int64_t ldy,
                 float* __restrict__ mean_out, float* __restrict__ rstd_out) {
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
+  const int64_t stride = (int64_t)gridDim.x * kWarpRowsPerCta;
+  int64_t row = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
   if (row >= T) return;
-  const float* xr = x + row * ldx;
-  const float c = __ldg(xr);
-  float4 v[NV];
-  float s1 = 0.f, s2 = 0.f;
-#pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int col = 4 * (lane + 32 * j);
-    if (col < E) {
-      v[j] = ldg4(xr + col);
-      float d0 = v[j].x - c, d1 = v[j].y - c, d2 = v[j].z - c, d3 = v[j].w - c;
-      s1 += (d0 + d1) + (d2 + d3);
-      s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
-    }
-  }
-  s1 = warp_sum(s1);
-  s2 = warp_sum(s2);
   const float inv_e = 1.0f / (float)E;
-  const float ms = s1 * inv_e;
-  const float var = fmaxf(s2 * inv_e - ms * ms, 0.f);
-  const float mu = c + ms, rs = rsqrtf(var + eps);
-  if (lane == 0) {
-    mean_out[row] = mu;
-    rstd_out[row] = rs;
-  }
-  TO* yr = y + row * ldy;
+  float4 v[NV], nx[NV];
+  float c = __ldg(x + row * ldx), cn = 0.f;
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const int col = 4 * (lane + 32 * j);
-    if (col < E) store4<TO>(yr + col, affine(v[j], ldg4(gamma + col), ldg4(beta + col), mu, rs));
+  for (int j = 0; j < NV; ++j)
+    if (4 * (lane + 32 * j) < E) v[j] = ldg4(x + row * ldx + 4 * (lane + 32 * j));
+  for (; row < T; row += stride) {
+    const int64_t nrow = row + stride;
+    if (nrow < T) {  // next row in flight while this one is reduced and stored
+      cn = __ldg(x + nrow * ldx);
+#pragma unroll
+      for (int j = 0; j < NV; ++j)
+        if (4 * (lane + 32 * j) < E) nx[j] = ldg4(x + nrow * ldx + 4 * (lane + 32 * j));
+    }
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      if (4 * (lane + 32 * j) < E) {
+        float d0 = v[j].x - c, d1 = v[j].y - c, d2 = v[j].z - c, d3 = v[j].w - c;
+        s1 += (d0 + d1) + (d2 + d3);
+        s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    const float ms = s1 * inv_e;
+    const float var = fmaxf(s2 * inv_e - ms * ms, 0.f);
+    const float mu = c + ms, rs = rsqrtf(var + eps);
+    if (lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+    TO* yr = y + row * ldy;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int col = 4 * (lane + 32 * j);
+      if (col < E) store4<TO>(yr + col, affine(v[j], ldg4(gamma + col), ldg4(beta + col), mu, rs));
+    }
+    c = cn;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = nx[j];
   }
 }
 
@@ -142,48 +157,56 @@ __device__ __forceinline__ float4 dx_of(const RowGrad& r, float rs, float sa, fl
                      rs * (r.dxh.z - sa - r.xh.z * sb), rs * (r.dxh.w - sa - r.xh.w * sb));
 }
 
-// ------------------------------------------------------------------ backward, warp per row
-// Per row two passes over x and dy (the second hits L1): pass 1 forms the two row
-// means and accumulates dgamma/dbeta into this warp's shared-memory slice (each lane
-// owns fixed columns, so no atomics); pass 2 writes dx.  Registers stay low enough
-// for 3+ CTAs (24+ warps) per SM.
+// ------------------------------------------------------------------ backward, warp per row, single pass
+// One warp per row in a CTA of kRowsWarps warps that owns `rows_per_cta` consecutive rows: x,
+// dy and the residual gradient of a row are loaded once (all loads of a row in flight
+// together), xhat and dxhat stay in registers for the dx pass, and the lane's dgamma/dbeta
+// columns accumulate in registers over the CTA's rows.  The CTA's warps are combined in fixed
+// order at the end into one partial row (deterministic, no atomics).  Two 192-thread CTAs per
+// SM leave 168 registers per thread: no spills at E = 768.
+constexpr int kRowsWarps = 6;
+
 template <int NV>
-__global__ void __launch_bounds__(32 * kWarpRowsPerCta)
-    ln_bwd_warp(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(32 * kRowsWarps, 2)
+    ln_bwd_rows(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
-                int64_t T, int E, const float* dres, float* dx, int64_t lddx, __nv_bfloat16* __restrict__ dx16,
-                float* __restrict__ pg, float* __restrict__ pb) {
-  extern __shared__ float4 sacc4[];  // [warps][2][E/4]
+                int64_t T, int E, int64_t rows_per_cta, const float* __restrict__ dres, float* __restrict__ dx,
+                int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb) {
+  extern __shared__ float4 red[];  // [kRowsWarps][2][E/4], used once at the end
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int E4 = E / 4;
-  float4* accg = sacc4 + (size_t)w * 2 * E4;
-  float4* accb = accg + E4;
-  for (int i = lane; i < E4; i += 32) {
-    accg[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    accb[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  const int64_t r0 = (int64_t)blockIdx.x * kWarpBwdRows;
-  const int64_t r1 = min(r0 + kWarpBwdRows, T);
   const float inv_e = 1.0f / (float)E;
-  for (int64_t row = r0 + w; row < r1; row += kWarpRowsPerCta) {
+  float4 ag[NV], ab[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) ag[j] = ab[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(r0 + rows_per_cta, T);
+  for (int64_t row = r0 + w; row < r1; row += kRowsWarps) {
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    const float* xr = x + row * ldx;
-    const float* dr = dy + row * lddy;
+    float4 xh[NV], dh[NV], rr[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * j;
+      if (i4 < E4) {
+        xh[j] = ldg4(x + row * ldx + 4 * i4);
+        dh[j] = ldg4(dy + row * lddy + 4 * i4);
+        rr[j] = dres ? ldg4(dres + row * lddx + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int i4 = lane + 32 * j;
-      if (4 * i4 < E) {
-        float4 xv = ldg4(xr + 4 * i4), d = ldg4(dr + 4 * i4), g = ldg4(gamma + 4 * i4);
-        float4 xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        float4 dxh = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
-        sa += (dxh.x + dxh.y) + (dxh.z + dxh.w);
-        sb += (dxh.x * xh.x + dxh.y * xh.y) + (dxh.z * xh.z + dxh.w * xh.w);
-        float4 ag = accg[i4], ab = accb[i4];
-        ag.x += d.x * xh.x; ag.y += d.y * xh.y; ag.z += d.z * xh.z; ag.w += d.w * xh.w;
-        ab.x += d.x; ab.y += d.y; ab.z += d.z; ab.w += d.w;
-        accg[i4] = ag;
-        accb[i4] = ab;
+      if (i4 < E4) {
+        const float4 g = ldg4(gamma + 4 * i4), d = dh[j];
+        float4& h = xh[j];
+        h = make_float4((h.x - mu) * rs, (h.y - mu) * rs, (h.z - mu) * rs, (h.w - mu) * rs);
+        ag[j].x += d.x * h.x; ag[j].y += d.y * h.y; ag[j].z += d.z * h.z; ag[j].w += d.w * h.w;
+        ab[j].x += d.x; ab[j].y += d.y; ab[j].z += d.z; ab[j].w += d.w;
+        const float4 e = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);  // dxhat
+        dh[j] = e;
+        sa += (e.x + e.y) + (e.z + e.w);
+        sb += (e.x * h.x + e.y * h.y) + (e.z * h.z + e.w * h.w);
       }
     }
     sa = warp_sum(sa) * inv_e;
@@ -191,33 +214,34 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta)
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
       const int i4 = lane + 32 * j;
-      if (4 * i4 < E) {
-        float4 xv = ldg4(xr + 4 * i4), d = ldg4(dr + 4 * i4), g = ldg4(gamma + 4 * i4);
-        RowGrad rg;
-        rg.xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        rg.dxh = make_float4(d.x * g.x, d.y * g.y, d.z * g.z, d.w * g.w);
+      if (i4 < E4) {
+        RowGrad rg{xh[j], dh[j]};
         float4 o = dx_of(rg, rs, sa, sb);
-        if (dres) {
-          float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + 4 * i4);
-          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
-        }
+        o.x += rr[j].x; o.y += rr[j].y; o.z += rr[j].z; o.w += rr[j].w;
         *reinterpret_cast<float4*>(dx + row * lddx + 4 * i4) = o;
         if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + 4 * i4, o);
       }
     }
   }
-  __syncthreads();
-  // per-CTA partial: the warps' slices combined in fixed warp order
-  for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kWarpRowsPerCta) {
-    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), sb4 = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int k = 0; k < kWarpRowsPerCta; ++k) {
-      float4 a = sacc4[(size_t)k * 2 * E4 + i4], b = sacc4[(size_t)k * 2 * E4 + E4 + i4];
+  for (int j = 0; j < NV; ++j) {
+    const int i4 = lane + 32 * j;
+    if (i4 < E4) {
+      red[(size_t)(2 * w) * E4 + i4] = ag[j];
+      red[(size_t)(2 * w + 1) * E4 + i4] = ab[j];
+    }
+  }
+  __syncthreads();
+  for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kRowsWarps) {
+    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < kRowsWarps; ++k) {  // fixed warp order
+      const float4 a = red[(size_t)(2 * k) * E4 + i4], b = red[(size_t)(2 * k + 1) * E4 + i4];
       sg.x += a.x; sg.y += a.y; sg.z += a.z; sg.w += a.w;
-      sb4.x += b.x; sb4.y += b.y; sb4.z += b.z; sb4.w += b.w;
+      s4.x += b.x; s4.y += b.y; s4.z += b.z; s4.w += b.w;
     }
     reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E)[i4] = sg;
-    reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = sb4;
+    reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = s4;
   }
 }
 
@@ -309,7 +333,9 @@ nnt_status launch_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, const f
                       TO* y, int64_t ldy, float* mean, float* rstd, cudaStream_t s) {
   int nvw = pick_nv_warp(E);
   if (nvw > 0) {
-    unsigned grid = (unsigned)((T + kWarpRowsPerCta - 1) / kWarpRowsPerCta);
+    int64_t g64 = (T + kWarpRowsPerCta - 1) / kWarpRowsPerCta;  // warps stride over rows: 2 CTAs per SM
+    if (g64 > 2 * num_sms()) g64 = 2 * num_sms();
+    unsigned grid = (unsigned)g64;
 #define NNT_LNFW(N) \
   case N: ln_fwd_warp<TO, N><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(x, T, (int)E, ldx, g, b, eps, y, ldy, mean, rstd); break;
     switch (nvw) { NNT_LNFW(1) NNT_LNFW(2) NNT_LNFW(4) NNT_LNFW(6) NNT_LNFW(8) }
@@ -373,31 +399,26 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
               "nnt_layernorm_bwd: scratch %zu < %zu", scratch_bytes, nnt_layernorm_bwd_scratch_bytes(T, E));
   NNT_REQUIRE(pick_nv_cta(E) > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: E=%lld > 8192", (long long)E);
   const int nvw = pick_nv_warp(E);
-  const int64_t chunks = nvw > 0 ? (T + kWarpBwdRows - 1) / kWarpBwdRows : (T + kCtaBwdRows - 1) / kCtaBwdRows;
+  // single-pass row kernel: rows per CTA so that two CTAs per SM cover T in one wave (>= 16
+  // rows, so the partial count stays within nnt_layernorm_bwd_scratch_bytes)
+  int64_t rows_per_cta = (T + 2 * num_sms() - 1) / (2 * num_sms());
+  if (rows_per_cta < kCtaBwdRows) rows_per_cta = kCtaBwdRows;
+  const int64_t chunks = nvw > 0 ? (T + rows_per_cta - 1) / rows_per_cta : (T + kCtaBwdRows - 1) / kCtaBwdRows;
   float* pg = (float*)scratch;
   float* pb = pg + chunks * E;
   double bytes = (double)T * E * (4 + 4 + 4 + (dres ? 4 : 0) + (dx_bf16 ? 2 : 0)) + 8.0 * T;
-  LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 3);
+  LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 2);
   __nv_bfloat16* d16 = (__nv_bfloat16*)dx_bf16;
   if (nvw > 0) {
-#define NNT_LNBW(N)                                                                                              \
-  case N:                                                                                                        \
-    ln_bwd_warp<N><<<(unsigned)chunks, 32 * kWarpRowsPerCta, smem_acc, stream>>>(dy, lddy, x, ldx, mean, rstd,   \
-                                                                                 gamma, T, (int)E, dres, dx,     \
-                                                                                 lddx, d16, pg, pb);             \
+    const size_t smem_red = (size_t)kRowsWarps * 2 * E * sizeof(float);  // <= 48 KB (E <= 1024)
+#define NNT_LNBR(N)                                                                                                \
+  case N:                                                                                                          \
+    ln_bwd_rows<N><<<(unsigned)chunks, 32 * kRowsWarps, smem_red, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, T, \
+                                                                            (int)E, rows_per_cta, dres, dx, lddx,  \
+                                                                            d16, pg, pb);                          \
     break;
-    const size_t smem_acc = (size_t)kWarpRowsPerCta * 2 * E * sizeof(float);  // <= 64 KB (E <= 1024)
-    static bool attr_set = false;
-    if (!attr_set) {
-      cudaFuncSetAttribute(ln_bwd_warp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      cudaFuncSetAttribute(ln_bwd_warp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      cudaFuncSetAttribute(ln_bwd_warp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      cudaFuncSetAttribute(ln_bwd_warp<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      cudaFuncSetAttribute(ln_bwd_warp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-      attr_set = true;
-    }
-    switch (nvw) { NNT_LNBW(1) NNT_LNBW(2) NNT_LNBW(4) NNT_LNBW(6) NNT_LNBW(8) }
-#undef NNT_LNBW
+    switch (nvw) { NNT_LNBR(1) NNT_LNBR(2) NNT_LNBR(4) NNT_LNBR(6) NNT_LNBR(8) }
+#undef NNT_LNBR
   } else {
 #define NNT_LNB(N)                                                                                               \
   case N:                                                                                                        \
@@ -408,8 +429,7 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
 #undef NNT_LNB
   }
   NNT_TRY(check_launch("layernorm_bwd"));
-  launch_column_merge(pg, chunks, E, dgamma, accumulate_params, stream);
-  launch_column_merge(pb, chunks, E, dbeta, accumulate_params, stream);
+  launch_column_merge2(pg, chunks * E, chunks, E, dgamma, dbeta, accumulate_params, stream);
   return check_launch("layernorm_bwd merge");
 }
 

@@ -9,11 +9,15 @@ namespace nnt {
 
 constexpr int kMergeWarps = 32;
 
+// blockIdx.y selects one of up to two independent merges (part + y * group_stride -> out[y]),
+// so paired reductions (LayerNorm dgamma / dbeta) take one launch.
 static __global__ void __launch_bounds__(32 * kMergeWarps)
-    column_merge_kernel(const float* __restrict__ part, int64_t chunks, int64_t N, float* __restrict__ out,
-                        int accumulate) {
+    column_merge_kernel(const float* __restrict__ part_base, int64_t chunks, int64_t N, float* __restrict__ out0,
+                        int accumulate, int64_t group_stride, float* __restrict__ out1) {
   __shared__ float red[kMergeWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const float* __restrict__ part = part_base + blockIdx.y * group_stride;
+  float* __restrict__ out = blockIdx.y ? out1 : out0;
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const int64_t per = (chunks + kMergeWarps - 1) / kMergeWarps;
   const int64_t k0 = w * per, k1 = min(chunks, k0 + per);
@@ -41,7 +45,14 @@ static __global__ void __launch_bounds__(32 * kMergeWarps)
 
 static inline void launch_column_merge(const float* part, int64_t chunks, int64_t N, float* out, int accumulate,
                                 cudaStream_t s) {
-  column_merge_kernel<<<(unsigned)((N + 31) / 32), 32 * kMergeWarps, 0, s>>>(part, chunks, N, out, accumulate);
+  column_merge_kernel<<<dim3((unsigned)((N + 31) / 32), 1), 32 * kMergeWarps, 0, s>>>(part, chunks, N, out, accumulate,
+                                                                                    0, out);
+}
+// two merges in one launch: part0 -> out0 and part0 + group_stride -> out1
+static inline void launch_column_merge2(const float* part0, int64_t group_stride, int64_t chunks, int64_t N,
+                                        float* out0, float* out1, int accumulate, cudaStream_t s) {
+  column_merge_kernel<<<dim3((unsigned)((N + 31) / 32), 2), 32 * kMergeWarps, 0, s>>>(part0, chunks, N, out0,
+                                                                                    accumulate, group_stride, out1);
 }
 
 }  // namespace nnt

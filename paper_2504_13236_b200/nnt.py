@@ -61,7 +61,7 @@ class nnt_epilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
                 ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("row_stats", C.c_void_p), ("ld_row_stats", C.c_int64),
-                ("rowvec", C.c_void_p), ("rowscale", C.c_float)]
+                ("rowvec", C.c_void_p), ("rowscale", C.c_float), ("a_rowsum", C.c_void_p)]
 
 
 class nnt_adam_hparams(C.Structure):
@@ -213,12 +213,12 @@ def nnt_partition(n_units, n_ranks, rank):
 
 def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
                   causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0, row_stats=None, ld_row_stats=0,
-                  rowvec=None, rowscale=1.0):
+                  rowvec=None, rowscale=1.0, a_rowsum=None):
     """The caller keeps every tensor passed here alive until the launch has run."""
     if workspace is not None and not workspace_bytes and hasattr(workspace, "numel"):
         workspace_bytes = workspace.numel() * workspace.element_size()
     return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal, ptr(workspace),
-                        workspace_bytes, ptr(row_stats), ld_row_stats, ptr(rowvec), rowscale)
+                        workspace_bytes, ptr(row_stats), ld_row_stats, ptr(rowvec), rowscale, ptr(a_rowsum))
 
 
 def nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act=NNT_ACT_NONE, causal=NNT_CAUSAL_NONE, batch_items=1):

@@ -189,6 +189,29 @@ def test_gemm_cta_pair_bit_exact(ta, tb, shape):
     assert np.array_equal(gotb, bf16_round(want))
 
 
+@pytest.mark.parametrize("M,N,K,ta", [(768, 768, 8192, 1), (3072, 768, 8192, 1), (768, 3072, 8192, 1),
+                                       (296, 200, 136, 1), (200, 136, 72, 1), (512, 384, 256, 0)])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_gemm_a_rowsum_bias_grad_bit_exact(M, N, K, ta, beta):
+    """R27: a_rowsum = beta * a_rowsum + sum_k op(A)[i][k] fused into the GEMM (tensor cores against
+    a ones vector) -- the bias gradient of a dW = dY^T X GEMM.  Integer data: C and the row sums
+    are exact; covers single-CTA and CTA-pair tiles, split-K (workspace) and unsplit GEMMs."""
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + K, kind="int")
+    b = nnt_inputs.make_matrix((K, N), seed=N + K, kind="int")
+    c0 = nnt_inputs.make_matrix((M, N), seed=7, kind="int")
+    r0 = nnt_inputs.make_matrix((M,), seed=8, kind="int")
+    nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
+    ws = torch.empty(max(nb, 16), device="cuda", dtype=torch.uint8)
+    rs = dev(r0)
+    epi = nnt.make_epilogue(workspace=ws if nb else None, a_rowsum=rs)
+    A, B, Cm = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(c0)
+    nnt.nnt_tile_gemm(ta, 0, M, N, K, None, 1.0, A, 1, a.shape[1], None, B, 1, N, None, beta, Cm, 0, N, None, None, epi)
+    torch.cuda.synchronize()
+    opa = (a.T if ta else a).astype(np.float64)
+    assert np.array_equal(host(Cm), opa @ b.astype(np.float64) + beta * c0)
+    assert np.array_equal(host(rs), opa.sum(axis=1) + beta * r0)
+
+
 @pytest.mark.parametrize("N", [768, 3072])
 def test_gemm_wave_model_tile_widths_bit_exact(N):
     """M = 8192 rows with N = 768 / 3072: wave-model tile widths on CTA pairs."""

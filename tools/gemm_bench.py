@@ -44,6 +44,7 @@ def main():
     spart = torch.empty(B * H * S * (S // 32) * 2, **f32)
     dvec = torch.zeros(B * H * S, **f32)
     rstats = torch.zeros(B * H * S * 2, **f32)
+    rowsum = torch.zeros(F, **f32)
     cases = [
         # name, ta, tb, M, N, K, batch, A, lda, sa, B, ldb, sb, C, cdt, ldc, sc, epi, causal-frac
         ("qkv", 0, 1, T, 3 * E, E, None, h, E, None, w, E, None, outb, 1, 3 * E, None,
@@ -85,6 +86,8 @@ def main():
          (S * 3 * E, Dh), nnt.make_epilogue(causal=2), 0.5),
         ("att_dk", 1, 0, S, Dh, S, bh, P, S, (H * S * S, S * S), h, 3 * E, (S * 3 * E, Dh), outb, 1, 3 * E,
          (S * 3 * E, Dh), nnt.make_epilogue(causal=3), 0.5),
+        ("proj_dw+db", 1, 0, E, F, T, None, h, E, None, g, F, None, outf, 0, F, None, None, 1.0),
+        ("fc_dw+db", 1, 0, F, E, T, None, g, F, None, h, E, None, outf, 0, E, None, None, 1.0),
         ("qkv_dw", 1, 0, 3 * E, E, T, None, h, 3 * E, None, h, E, None, outf, 0, E, None, None, 1.0),
         ("qkv_dx", 0, 0, T, E, 3 * E, None, h, 3 * E, None, w, E, None, outf, 0, E, None, None, 1.0),
         ("square8192", 0, 1, 8192, 8192, 8192, None, big, 8192, None, big, 8192, None, outb, 1, 8192, None,
@@ -99,6 +102,9 @@ def main():
         beta = 1.0 if name.endswith("_dw") else 0.0
         if name.endswith("_dw"):
             epi = nnt.make_epilogue(workspace=ws)
+        if name.endswith("_dw+db"):
+            beta = 1.0
+            epi = nnt.make_epilogue(workspace=ws, a_rowsum=rowsum)
         if name == "square8192" and T * F < 8192 * 8192:
             outb = torch.empty(8192 * 8192, **bf)
             Cm = outb
