@@ -245,12 +245,18 @@ def run_nnt(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    use_graph = world == 1 and not args.no_graph
+    use_graph = not args.no_graph
     graph_launches = 0
-    if use_graph:  # the whole step as one CUDA graph (captured launches counted once)
+    if use_graph:  # the whole step as one CUDA graph (captured launches counted once); with DP the
+        # bucket all-reduces + Adam are captured on the comm stream (model.BlockStack.enable_graph)
         n_cap = nnt.nnt_launch_count()
-        st.enable_graph()
-        graph_launches = nnt.nnt_launch_count() - n_cap
+        try:
+            st.enable_graph()
+        except Exception as exc:  # NCCL capture unsupported here: the DP step stays eager
+            print(f"# graph capture failed ({exc!r}); eager launches", file=sys.stderr)
+            st.graph, use_graph = None, False
+            torch.cuda.synchronize()
+        graph_launches = nnt.nnt_launch_count() - n_cap if use_graph else 0
     for i in range(args.warmup):
         x, r = dev_batches[i % 2]
         st.train_step(x, r)

@@ -36,6 +36,30 @@ def param_shapes(E):
             "ln2_g": (E,), "ln2_b": (E,), "w_fc": (F, E), "b_fc": (F,), "w_pr": (E, F), "b_pr": (E,)}
 
 
+def flat_layout(L, E):
+    """Host bookkeeping of the flat parameter / gradient buffers (integer, bit-exact across ranks).
+
+    Returns (offsets, buckets, numel): offsets[l][name] = (element offset, numel); buckets =
+    [(layer, set index, begin, end)] in backward-completion order (layer L-1 first; inside a
+    layer the SETS order), each bucket a contiguous slice; every tensor starts on an ALIGN
+    boundary.  These buckets are the units of the DP all-reduce."""
+    shapes = param_shapes(E)
+    offsets = [None] * L
+    buckets = []
+    off = 0
+    for l in range(L - 1, -1, -1):
+        d = {}
+        for si, names in enumerate(SETS):
+            b0 = off
+            for n in names:
+                numel = math.prod(shapes[n])
+                d[n] = (off, numel)
+                off += -(-numel // ALIGN) * ALIGN
+            buckets.append((l, si, b0, off))
+        offsets[l] = d
+    return offsets, buckets, off
+
+
 @dataclass
 class StackConfig:
     L: int
@@ -74,26 +98,14 @@ class BlockStack:
         self.dev = torch.device(device)
         self.pg = process_group
         self.world = torch.distributed.get_world_size(process_group) if process_group is not None else 1
+        # the DP path (bucketed all-reduce on a comm stream) runs whenever a process group is given,
+        # also at world size 1 (so the GPU tests can exercise it on one device)
+        self.dp = process_group is not None
         self.T_global = global_tokens if global_tokens is not None else cfg.T * self.world
         self.bcfg = cfg.block_cfg()
         E = cfg.E
         shapes = param_shapes(E)
-        # ---- flat layout
-        self.offsets = []       # per layer: name -> (offset, numel)
-        self.buckets = []       # (layer, set index, begin, end) in backward-completion order
-        off = 0
-        per_layer = [None] * cfg.L
-        for l in range(cfg.L - 1, -1, -1):
-            d = {}
-            for si, names in enumerate(SETS):
-                b0 = off
-                for n in names:
-                    numel = math.prod(shapes[n])
-                    d[n] = (off, numel)
-                    off += -(-numel // ALIGN) * ALIGN
-                self.buckets.append((l, si, b0, off))
-            per_layer[l] = d
-        self.offsets = per_layer
+        self.offsets, self.buckets, off = flat_layout(cfg.L, E)
         self.numel = off
         f32 = dict(device=self.dev, dtype=torch.float32)
         self.w = torch.zeros(off, **f32)
@@ -123,8 +135,14 @@ class BlockStack:
         self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
         self.loss = torch.zeros(1, **act)
         self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
-        self.comm = torch.cuda.Stream(device=self.dev) if self.world > 1 else None
-        self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.world > 1 else None
+        self.comm = torch.cuda.Stream(device=self.dev) if self.dp else None
+        self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.dp else None
+        if self.dp:  # torch creates the CUDA event handles lazily, at the first record()
+            for evs in self.events:
+                for e in evs:
+                    e.record()
+            torch.cuda.synchronize(self.dev)
+        self._graph_hp = None  # during enable_graph()'s capture: Adam reads its bias corrections from the device
 
     # ------------------------------------------------------------ views
     def view(self, buf, l, name):
@@ -174,7 +192,7 @@ class BlockStack:
         """Backward through the stack; with DP, bucket all-reduce (+ Adam) overlapped on the comm stream."""
         cur = 0
         compute = torch.cuda.current_stream()
-        dp = self.world > 1
+        dp = self.dp
         for l in range(self.cfg.L - 1, -1, -1):
             ev = self.events[l] if dp else None
             nnt.nnt_block_bwd(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch, self.dy[cur],
@@ -207,7 +225,7 @@ class BlockStack:
                                     1.0 - c.beta2 ** t, 1.0)
 
     def _adam_range(self, b0, b1, t, stream=None):
-        hp = self._hparams(t)
+        hp = self._graph_hp if self._graph_hp is not None else self._hparams(t)
         nnt.nnt_adam_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1], self.v[b0:b1],
                           self.w16[b0:b1] if self.bf16 else None, hp, stream=stream)
 
@@ -234,7 +252,7 @@ class BlockStack:
             r = self.r_buf
         self.forward(x)
         self.probe_loss(r)
-        if self.world > 1:
+        if self.dp:
             self.backward(overlap_optimizer=True)
             self.step_count += 1
         else:
@@ -242,13 +260,16 @@ class BlockStack:
             self.adam()
         return self.loss
 
-    # ------------------------------------------------------------ CUDA graph (single GPU)
+    # ------------------------------------------------------------ CUDA graph
     def enable_graph(self):
         """Capture one whole training step (Adam step counter advanced on the device, fp64
         bias corrections, then forward, probe loss, backward, Adam) as a CUDA graph; later
         train_step calls copy the batch into the static input buffers and replay it.  This
-        removes the host cost of ~500 launches (ctypes + TMA-descriptor encoding) per step."""
-        assert self.world == 1, "graph capture is single-GPU (the DP path stays eager)"
+        removes the host cost of ~500 launches (ctypes + TMA-descriptor encoding) per step.
+
+        With a process group (DP) the capture forks the communication stream off the compute
+        stream at every bucket event: each bucket's NCCL all-reduce and Adam are graph nodes
+        that overlap the rest of the backward pass, joined before the step ends."""
         dev = self.dev
         if not hasattr(self, "r_buf"):
             self.r_buf = torch.empty_like(self.xs[0])
@@ -257,15 +278,25 @@ class BlockStack:
         c = self.cfg
         hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
         hp.bias_corr_dev = self.bc_dev.data_ptr()
-        self._graph_hp = hp
+        if self.dp:  # the communicator must exist before capture: one eager collective on the comm stream
+            with torch.cuda.stream(self.comm):
+                torch.distributed.all_reduce(torch.zeros(1, device=dev), group=self.pg)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            nnt.nnt_adam_tick(c.beta1, c.beta2, self.t_dev, self.bc_dev)
-            self.forward()
-            self.probe_loss(self.r_buf)
-            self.backward()
-            nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16 if self.bf16 else None, hp)
+        self._graph_hp = hp
+        try:
+            with torch.cuda.graph(g):
+                nnt.nnt_adam_tick(c.beta1, c.beta2, self.t_dev, self.bc_dev)
+                self.forward()
+                self.probe_loss(self.r_buf)
+                if self.dp:
+                    self.backward(overlap_optimizer=True)
+                else:
+                    self.backward()
+                    nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v,
+                                      self.w16 if self.bf16 else None, hp)
+        finally:
+            self._graph_hp = None  # eager steps keep host-side bias corrections
         self.graph = g
         return g
 

@@ -328,7 +328,12 @@ def nnt_block_fwd(cfg, params, x, y, saved, scratch, stream=None):
 def nnt_block_bwd(cfg, params, x, saved, scratch, dy, dx, grads, accumulate_grads, grad_ready=None, stream=None):
     ev = None
     if grad_ready is not None:
-        ev = (C.c_void_p * 4)(*[e.cuda_event if hasattr(e, "cuda_event") else e for e in grad_ready])
+        handles = [e.cuda_event if hasattr(e, "cuda_event") else e for e in grad_ready]
+        # torch creates an Event's CUDA handle lazily at its first record(): a 0 handle here would
+        # silently disable the event (the library skips NULL events) and race the comm stream
+        if not all(handles):
+            raise ValueError("nnt_block_bwd: grad_ready events must be created (record() once) before use")
+        ev = (C.c_void_p * 4)(*handles)
     return check(lib.nnt_block_bwd(C.byref(cfg), C.byref(params), ptr(x), ptr(saved), ptr(scratch), ptr(dy), ptr(dx),
                                    C.byref(grads), accumulate_grads, ev, _stream(stream)))
 

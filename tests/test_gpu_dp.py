@@ -1,0 +1,62 @@
+"""The DP code path on one GPU: a world-size-1 NCCL process group makes BlockStack run the
+data-parallel backward (bucket events from nnt_block_bwd, NCCL SUM all-reduce of each bucket
+on the communication stream, Adam per bucket overlapping the rest of the backward pass),
+eagerly and captured in a CUDA graph.  A one-rank SUM is the identity and Adam is elementwise,
+so parameters, moments and losses must equal the single-GPU path bitwise (reading R17)."""
+import os
+import socket
+
+import pytest
+import torch
+
+import nnt_inputs
+from gpu_util import dev
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2504_13236_b200 import model
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    yield dist.group.WORLD
+    dist.destroy_process_group()
+
+
+def _run(pg, graph, steps=3):
+    E, H, S, B, L = 768, 12, 256, 2, 2
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    layers = [nnt_inputs.make_params(E, seed=9, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+    st = model.BlockStack(sc, layers, process_group=pg)
+    if graph:
+        st.enable_graph()
+    losses = []
+    for t in range(steps):
+        x = dev(nnt_inputs.make_x(E, S, 0, B, seed=70 + t))
+        r = dev(nnt_inputs.make_r(E, S, 0, B, seed=70 + t))
+        losses.append(st.train_step(x, r).item())
+    torch.cuda.synchronize()
+    return losses, st.w.clone(), st.m.clone(), st.v.clone(), st.w16.clone()
+
+
+@pytest.mark.timeout(300)
+def test_dp_path_world1_equals_single_gpu_bitwise(pg):
+    ref = _run(None, graph=False)
+    for graph in (False, True):
+        got = _run(pg, graph=graph)
+        assert got[0] == ref[0], graph
+        for a, b in zip(got[1:], ref[1:]):
+            assert torch.equal(a, b), graph

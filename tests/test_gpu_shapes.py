@@ -1,0 +1,73 @@
+"""bf16 tensor-core path at the other BASELINE.json shapes, and the bench configuration itself.
+
+* One block of the GPT-2 large (E=1280, H=20), XL (E=1600, H=25: boundary tiles 1024+576,
+  4800 = 4x1024+704, 6400 = 6x1024+256) and wide (E=8192, H=128) shapes vs the fp64 oracle,
+  every tensor rel <= 2e-2 (north_star's bf16 tolerance).
+* The exact configuration bench.py times (GPT-2 small, 12 layers, B=8, S=1024, GPT-2 init,
+  one CUDA-graph training step): y and dx of sampled sequences vs the oracle run on those
+  sequences alone (every block is independent across sequences: LayerNorm is per token,
+  attention per (sequence, head), the probe-loss gradient dy = r / T per token).
+"""
+import numpy as np
+import pytest
+import torch
+
+import nnt_inputs
+from oracle import dense
+from gpu_util import bf16_round, dev, host, rel
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2504_13236_b200 import model
+
+
+def _used(p):
+    """The parameters the GPU computes with: bf16-rounded weight matrices, fp32 vectors."""
+    return {k: (bf16_round(v) if k.startswith("w_") else v.astype(np.float64)) for k, v in p.items()}
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("E,H,S,B", [(1280, 20, 1024, 1), (1600, 25, 1024, 1), (8192, 128, 128, 1)],
+                         ids=["large", "xl", "wide"])
+def test_bf16_block_baseline_shapes(E, H, S, B):
+    sc = model.StackConfig(L=1, E=E, H=H, S=S, B=B, dtype="bf16")
+    layers = [nnt_inputs.make_params(E, seed=4321, init="parity")]
+    st = model.BlockStack(sc, layers)
+    x = nnt_inputs.make_x(E, S, 0, B, seed=21)
+    r = nnt_inputs.make_r(E, S, 0, B, seed=21)
+    st.forward(dev(x))
+    st.probe_loss(dev(r))
+    dx_dev = st.backward()
+    torch.cuda.synchronize()
+    used = _used(layers[0])
+    del layers
+    y_ref, cache = dense.block_fwd(used, x, H)
+    dx_ref, g_ref = dense.block_bwd(used, cache, dense.probe_loss_grad(r, B * S))
+    assert rel(host(st.xs[-1]), y_ref) < 2e-2
+    assert rel(host(dx_dev), dx_ref) < 2e-2
+    for n, gv in st.grads_of(0).items():
+        assert rel(host(gv), g_ref[n]) < 2e-2, n
+
+
+@pytest.mark.timeout(900)
+def test_bench_config_sampled_sequences():
+    import bench
+    L, E, H, S, B = bench.CONFIGS["small"]
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+    st = model.BlockStack(sc, layers)
+    st.enable_graph()
+    x = nnt_inputs.make_x(E, S, 0, B, seed=1000)
+    r = nnt_inputs.make_r(E, S, 0, B, seed=1000)
+    st.train_step(dev(x), dev(r))
+    torch.cuda.synchronize()
+    y = st.xs[-1]
+    dx = st.dy[L % 2]  # backward ping-pongs between the two dy buffers, one flip per layer
+    used = [_used(p) for p in layers]
+    for j in (0, B - 1):
+        xj, rj = x[j:j + 1], r[j:j + 1]
+        yr, caches = dense.stack_fwd(used, xj, H)
+        dxr, _ = dense.stack_bwd(used, caches, dense.probe_loss_grad(rj, B * S))
+        assert rel(host(y[j]), yr[0]) < 2e-2, j
+        assert rel(host(dx[j]), dxr[0]) < 2e-2, j
