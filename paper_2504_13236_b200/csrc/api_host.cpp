@@ -1,5 +1,6 @@
 // Library plumbing: errors, version/device checks, tile bookkeeping (P:72-75,
 // P:231) and the per-launch CUDA-event timer used by bench.py's roofline.
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 #include <atomic>
@@ -30,6 +31,14 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("NNT_PDL");  // off by default: measured slower on the GPT-2 step
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 // ---------------------------------------------------------------- timing

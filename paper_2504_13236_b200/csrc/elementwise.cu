@@ -22,6 +22,7 @@ inline int grid_for(int64_t work_items, int per_sm = 8) {
 template <typename T, bool kBwd>
 __global__ void __launch_bounds__(kThreads) gelu_kernel(const T* __restrict__ x, const T* __restrict__ dy,
                                                         T* __restrict__ y, int64_t n, bool vec_ok) {
+  NNT_PDL_ENTRY();
   constexpr int V = 16 / sizeof(T);
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -54,6 +55,7 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
                                                         const float* __restrict__ g, float* __restrict__ m,
                                                         float* __restrict__ v, __nv_bfloat16* __restrict__ w16,
                                                         nnt_adam_hparams hp, bool vec_ok) {
+  NNT_PDL_ENTRY();
   const float b1 = hp.beta1, b2 = hp.beta2, c1 = 1.f - hp.beta1, c2 = 1.f - hp.beta2;
   const float bc1 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev) : hp.bias_corr1;
   const float bc2 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev + 1) : hp.bias_corr2;
@@ -103,6 +105,7 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
 }
 
 __global__ void adam_tick_kernel(double beta1, double beta2, int64_t* t, float* bc) {
+  NNT_PDL_ENTRY();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const int64_t s = t[0] + 1;
     t[0] = s;
@@ -114,12 +117,14 @@ __global__ void adam_tick_kernel(double beta1, double beta2, int64_t* t, float* 
 // ------------------------------------------------------------------ convert
 template <typename TI, typename TO>
 __global__ void __launch_bounds__(kThreads) convert_kernel(const TI* __restrict__ x, TO* __restrict__ y, int64_t n) {
+  NNT_PDL_ENTRY();
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = tid; i < n; i += stride) y[i] = from_f32<TO>(to_f32(x[i]));
 }
 
 __global__ void __launch_bounds__(kThreads) scale_kernel(const float* x, float alpha, float* y, int64_t n, bool vec_ok) {
+  NNT_PDL_ENTRY();
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t nv = vec_ok ? n / 4 : 0;
@@ -162,6 +167,7 @@ __global__ void __launch_bounds__(kThreads) colsum_partial_kernel(const T* __res
                                                                   int64_t ld, int64_t rows_per,
                                                                   float* __restrict__ partial,
                                                                   __nv_bfloat16* __restrict__ copy16) {
+  NNT_PDL_ENTRY();
   __shared__ float red[8][128];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t col0 = (int64_t)blockIdx.x * 128 + lane * 4;
@@ -214,6 +220,7 @@ __global__ void __launch_bounds__(kThreads) colsum_partial_kernel(const T* __res
 constexpr int kDotBlocks = 2 * kPartitionSMs;
 __global__ void __launch_bounds__(kThreads) dot_partial_kernel(const float* __restrict__ a, const float* __restrict__ b,
                                                                int64_t n, double* __restrict__ partial) {
+  NNT_PDL_ENTRY();
   __shared__ double red[kThreads / 32];
   double s = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -230,6 +237,7 @@ __global__ void __launch_bounds__(kThreads) dot_partial_kernel(const float* __re
 }
 
 __global__ void dot_merge_kernel(const double* __restrict__ partial, int n, float scale, float* out) {
+  NNT_PDL_ENTRY();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < n; ++i) t += partial[i];
@@ -253,9 +261,9 @@ nnt_status nnt_gelu_fwd(const void* x, void* y, int dtype, int64_t n, nnt_stream
   size_t es = dtype_size(dtype);
   LaunchScope sc(NNT_K_GELU, stream, 2.0 * es * n, 0);
   if (dtype == NNT_F32)
-    gelu_kernel<float, false><<<grid_for(n / 4 + 1), kThreads, 0, stream>>>((const float*)x, nullptr, (float*)y, n, vec);
+    ::nnt::launch(gelu_kernel<float, false>, grid_for(n / 4 + 1), kThreads, 0, stream, (const float*)x, nullptr, (float*)y, n, vec);
   else
-    gelu_kernel<__nv_bfloat16, false><<<grid_for(n / 8 + 1), kThreads, 0, stream>>>(
+    ::nnt::launch(gelu_kernel<__nv_bfloat16, false>, grid_for(n / 8 + 1), kThreads, 0, stream, 
         (const __nv_bfloat16*)x, nullptr, (__nv_bfloat16*)y, n, vec);
   return check_launch("gelu_fwd");
 }
@@ -269,10 +277,10 @@ nnt_status nnt_gelu_bwd(const void* x, const void* dy, void* dx, int dtype, int6
   size_t es = dtype_size(dtype);
   LaunchScope sc(NNT_K_GELU, stream, 3.0 * es * n, 0);
   if (dtype == NNT_F32)
-    gelu_kernel<float, true><<<grid_for(n / 4 + 1), kThreads, 0, stream>>>((const float*)x, (const float*)dy,
+    ::nnt::launch(gelu_kernel<float, true>, grid_for(n / 4 + 1), kThreads, 0, stream, (const float*)x, (const float*)dy,
                                                                           (float*)dx, n, vec);
   else
-    gelu_kernel<__nv_bfloat16, true><<<grid_for(n / 8 + 1), kThreads, 0, stream>>>(
+    ::nnt::launch(gelu_kernel<__nv_bfloat16, true>, grid_for(n / 8 + 1), kThreads, 0, stream, 
         (const __nv_bfloat16*)x, (const __nv_bfloat16*)dy, (__nv_bfloat16*)dx, n, vec);
   return check_launch("gelu_bwd");
 }
@@ -287,7 +295,7 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
   bool vec = aligned16(w) && aligned16(g) && aligned16(m) && aligned16(v) &&
              (w_bf16 == nullptr || (reinterpret_cast<uintptr_t>(w_bf16) & 7u) == 0);
   LaunchScope sc(NNT_K_ADAM, stream, (28.0 + (w_bf16 ? 2.0 : 0.0)) * n, 0);
-  adam_kernel<<<grid_for(n / 4 + 1), kThreads, 0, stream>>>(n, w, g, m, v, (__nv_bfloat16*)w_bf16, *hp, vec);
+  ::nnt::launch(adam_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, n, w, g, m, v, (__nv_bfloat16*)w_bf16, *hp, vec);
   return check_launch("adam");
 }
 
@@ -295,7 +303,7 @@ nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias
   NNT_REQUIRE(t_dev && bias_corr_dev, NNT_ERR_NULL, "nnt_adam_tick: NULL pointer");
   NNT_REQUIRE(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0, NNT_ERR_ARG, "nnt_adam_tick: beta");
   LaunchScope sc(NNT_K_ADAM, stream, 16.0, 0);
-  adam_tick_kernel<<<1, 32, 0, stream>>>(beta1, beta2, t_dev, bias_corr_dev);
+  ::nnt::launch(adam_tick_kernel, 1, 32, 0, stream, beta1, beta2, t_dev, bias_corr_dev);
   return check_launch("adam_tick");
 }
 
@@ -307,13 +315,13 @@ nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t
   LaunchScope sc(NNT_K_MISC, stream, (double)(dtype_size(x_dtype) + dtype_size(y_dtype)) * n, 0);
   int grid = grid_for(n);
   if (x_dtype == NNT_F32 && y_dtype == NNT_BF16)
-    convert_kernel<float, __nv_bfloat16><<<grid, kThreads, 0, stream>>>((const float*)x, (__nv_bfloat16*)y, n);
+    ::nnt::launch(convert_kernel<float, __nv_bfloat16>, grid, kThreads, 0, stream, (const float*)x, (__nv_bfloat16*)y, n);
   else if (x_dtype == NNT_BF16 && y_dtype == NNT_F32)
-    convert_kernel<__nv_bfloat16, float><<<grid, kThreads, 0, stream>>>((const __nv_bfloat16*)x, (float*)y, n);
+    ::nnt::launch(convert_kernel<__nv_bfloat16, float>, grid, kThreads, 0, stream, (const __nv_bfloat16*)x, (float*)y, n);
   else if (x_dtype == NNT_F32)
-    convert_kernel<float, float><<<grid, kThreads, 0, stream>>>((const float*)x, (float*)y, n);
+    ::nnt::launch(convert_kernel<float, float>, grid, kThreads, 0, stream, (const float*)x, (float*)y, n);
   else
-    convert_kernel<__nv_bfloat16, __nv_bfloat16><<<grid, kThreads, 0, stream>>>((const __nv_bfloat16*)x,
+    ::nnt::launch(convert_kernel<__nv_bfloat16, __nv_bfloat16>, grid, kThreads, 0, stream, (const __nv_bfloat16*)x,
                                                                                   (__nv_bfloat16*)y, n);
   return check_launch("convert");
 }
@@ -323,7 +331,7 @@ nnt_status nnt_scale(const float* x, float alpha, float* y, int64_t n, nnt_strea
   NNT_REQUIRE(n >= 0, NNT_ERR_SHAPE, "nnt_scale: n=%lld", (long long)n);
   if (n == 0) return NNT_OK;
   LaunchScope sc(NNT_K_MISC, stream, 8.0 * n, (double)n);
-  scale_kernel<<<grid_for(n / 4 + 1), kThreads, 0, stream>>>(x, alpha, y, n, aligned16(x) && aligned16(y));
+  ::nnt::launch(scale_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, x, alpha, y, n, aligned16(x) && aligned16(y));
   return check_launch("scale");
 }
 
@@ -354,17 +362,17 @@ nnt_status nnt_bias_grad(const void* dy, int dy_dtype, int64_t T, int64_t N, int
   __nv_bfloat16* c16 = (__nv_bfloat16*)dy_bf16_out;
   if (dy_dtype == NNT_F32) {
     if (vec)
-      colsum_partial_kernel<float, true><<<grid, kThreads, 0, stream>>>((const float*)dy, T, N, lddy, p.rows_per,
+      ::nnt::launch(colsum_partial_kernel<float, true>, grid, kThreads, 0, stream, (const float*)dy, T, N, lddy, p.rows_per,
                                                                         (float*)scratch, c16);
     else
-      colsum_partial_kernel<float, false><<<grid, kThreads, 0, stream>>>((const float*)dy, T, N, lddy, p.rows_per,
+      ::nnt::launch(colsum_partial_kernel<float, false>, grid, kThreads, 0, stream, (const float*)dy, T, N, lddy, p.rows_per,
                                                                          (float*)scratch, c16);
   } else {
     if (vec)
-      colsum_partial_kernel<__nv_bfloat16, true><<<grid, kThreads, 0, stream>>>(
+      ::nnt::launch(colsum_partial_kernel<__nv_bfloat16, true>, grid, kThreads, 0, stream, 
           (const __nv_bfloat16*)dy, T, N, lddy, p.rows_per, (float*)scratch, nullptr);
     else
-      colsum_partial_kernel<__nv_bfloat16, false><<<grid, kThreads, 0, stream>>>(
+      ::nnt::launch(colsum_partial_kernel<__nv_bfloat16, false>, grid, kThreads, 0, stream, 
           (const __nv_bfloat16*)dy, T, N, lddy, p.rows_per, (float*)scratch, nullptr);
   }
   NNT_TRY(check_launch("bias_grad partial"));
@@ -380,9 +388,9 @@ nnt_status nnt_dot(const float* y, const float* r, int64_t n, float scale, float
   NNT_REQUIRE(n > 0, NNT_ERR_SHAPE, "nnt_dot: n=%lld", (long long)n);
   NNT_REQUIRE(scratch_bytes >= nnt_dot_scratch_bytes(n), NNT_ERR_WORKSPACE, "nnt_dot: scratch too small");
   LaunchScope sc(NNT_K_MISC, stream, 8.0 * n, 2.0 * n, 2);
-  dot_partial_kernel<<<kDotBlocks, kThreads, 0, stream>>>(y, r, n, (double*)scratch);
+  ::nnt::launch(dot_partial_kernel, kDotBlocks, kThreads, 0, stream, y, r, n, (double*)scratch);
   NNT_TRY(check_launch("dot partial"));
-  dot_merge_kernel<<<1, 32, 0, stream>>>((const double*)scratch, kDotBlocks, scale, out);
+  ::nnt::launch(dot_merge_kernel, 1, 32, 0, stream, (const double*)scratch, kDotBlocks, scale, out);
   return check_launch("dot merge");
 }
 

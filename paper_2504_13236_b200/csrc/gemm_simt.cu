@@ -12,6 +12,7 @@ constexpr int BM = 64, BN = 64, BK = 16, NT = 256;
 
 template <typename TC>
 __global__ void __launch_bounds__(NT) gemm_simt_kernel(GemmArgs g) {
+  NNT_PDL_ENTRY();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int64_t bz = blockIdx.z;
@@ -76,9 +77,9 @@ nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s) {
   dim3 grid((unsigned)((a.N + BN - 1) / BN), (unsigned)((a.M + BM - 1) / BM), (unsigned)(a.batch0 * a.batch1));
   NNT_REQUIRE(grid.y <= 65535 && grid.z <= 65535, NNT_ERR_UNSUPPORTED, "gemm_simt: grid too large");
   if (a.c_dtype == NNT_F32)
-    gemm_simt_kernel<float><<<grid, NT, 0, s>>>(a);
+    ::nnt::launch(gemm_simt_kernel<float>, grid, NT, 0, s, a);
   else
-    gemm_simt_kernel<__nv_bfloat16><<<grid, NT, 0, s>>>(a);
+    ::nnt::launch(gemm_simt_kernel<__nv_bfloat16>, grid, NT, 0, s, a);
   return check_launch("gemm_simt");
 }
 

@@ -182,8 +182,12 @@ __device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+// Arrive on a (possibly remote) barrier of the cluster.  Default .release.cta semantics: the
+// only thing the waiter (the leader's MMA issuer) relies on is that this warp's tcgen05.ld of
+// the accumulator completed, which tcgen05.wait::ld + tcgen05.fence::before_thread_sync order
+// before the arrive; a .release.cluster arrive costs a GPU-scope MEMBAR per warp and tile.
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
@@ -725,6 +729,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // PDL: everything above (barrier init, TMEM allocation, tensor-map prefetch) overlapped the
+  // previous kernel's tail; inputs are read only after it has completed
+  NNT_PDL_ENTRY();
 
   if (warp == 0) {
     // ===================== TMA producer
@@ -1277,6 +1284,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
                                                             const float* __restrict__ bias,
                                                             const float* __restrict__ residual, int64_t ld_res,
                                                             float* __restrict__ rowsum) {
+  NNT_PDL_ENTRY();
   const int64_t nq = N / 4;  // N % 4 == 0 (checked on the host)
   const int64_t total = M * nq;
   if (rowsum) {  // R27: a_rowsum = beta * a_rowsum + sum_s partial_s (slices after the C partials)
@@ -1508,19 +1516,21 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     const int64_t units = num_sms() * C::CTAS;  // persistent: C::CTAS CTAs per SM
     int64_t grid = P.num_tasks < units ? P.num_tasks : units;
     if (grid < 1) grid = 1;
-    gemm_tc_kernel<BN, TC, EPI, 1><<<(unsigned)grid, kThreads, C::SMEM_BYTES, s>>>(P, tmA, tmB, tmC, tmAux);
+    ::nnt::launch(gemm_tc_kernel<BN, TC, EPI, 1>, (unsigned)grid, kThreads, C::SMEM_BYTES, s, P, tmA, tmB, tmC, tmAux);
   } else {
     cudaLaunchConfig_t cfg = {};
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = C::SMEM_BYTES;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
     const int64_t max_clusters = pair_units();
     int64_t grid = P.num_tasks < max_clusters ? P.num_tasks : max_clusters;
     if (grid < 1) grid = 1;
@@ -1532,7 +1542,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     const int64_t total = a.M * (a.N / 4);
     int64_t blocks = cdiv(total, 256);
     if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
-    splitk_reduce_kernel<<<(unsigned)blocks, 256, 0, s>>>((const float*)a.workspace, splits, a.M, a.N, (float*)a.C,
+    ::nnt::launch(splitk_reduce_kernel, (unsigned)blocks, 256, 0, s, (const float*)a.workspace, splits, a.M, a.N, (float*)a.C,
                                                           a.ldc, a.beta, a.bias, a.residual, a.ld_res,
                                                           P.rowsum ? a.a_rowsum : nullptr);
     NNT_TRY(check_launch("gemm_tc splitk reduce"));
@@ -1540,20 +1550,49 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   return NNT_OK;
 }
 
-// Tile width from a wave model: time ~ ceil(tiles / SMs) * BN (per-tile time ~ BN at fixed
-// BM, K); ties go to the wider tile (more operand reuse per byte of L2 traffic).
-int choose_bn(const GemmArgs& a, double* cost_out = nullptr) {
+// Tile shape from a two-term roofline per round of the persistent schedule.  Per SM, a tile
+// costs max(MMA cycles, L2 cycles): the tensor core retires 8192 bf16 FLOP per cycle
+// (128 x BN x K tile = BN*K/32 cycles), and the SM's operand + epilogue traffic,
+//   (128 + BN/CG) * K * 2 bytes (a CTA pair stages half of B per SM) + 128 * BN * epilogue bytes,
+// shares the L2 slice throughput (~5200 B per SM cycle chip-wide at 1965 MHz, calibrated on the
+// K = 768 / 3072 projection GEMMs; B300_MICROARCH: LTS cap ~6300 B/cyc at locked clocks) with
+// every SM busy in that round.  Small-K projection GEMMs are L2-bound with 128-row tiles, which
+// is why the 256-row CTA-pair tiles (half the operand bytes per FLOP) usually win.
+double l2_bytes_per_cycle() {
+  static const double v = [] {
+    const char* e = getenv("NNT_GEMM_L2");
+    return e ? atof(e) : 5200.0;
+  }();
+  return v;
+}
+
+double tile_cost(const GemmArgs& a, int bn, int cg, int64_t units, size_t es_c) {
+  const int64_t nb = a.batch0 * a.batch1;
+  const int64_t tiles = cdiv(a.M, (int64_t)BM * cg) * cdiv(a.N, bn) * nb;
+  const double kp = (double)(cdiv(a.K, BK) * BK);
+  const double mma = bn * kp / 32.0;
+  double epi = (double)es_c;                                    // C
+  if (a.act == NNT_ACT_GELU || a.act == NNT_ACT_GELU_BWD) epi += (double)es_c;  // aux out / in
+  if (a.residual) epi += 4.0;
+  if (a.beta != 0.f) epi += (double)es_c;
+  const double bytes_sm = (BM + (double)bn / cg) * kp * 2.0 + (double)BM * bn * epi;
+  const double l2 = l2_bytes_per_cycle();
+  const int64_t full = tiles / units, rem = tiles % units;
+  double cost = (double)full * fmax(mma, (double)units * cg * bytes_sm / l2);
+  if (rem) cost += fmax(mma, (double)rem * cg * bytes_sm / l2);
+  return cost;
+}
+
+int choose_bn(const GemmArgs& a, size_t es_c, double* cost_out = nullptr) {
   if (cost_out) *cost_out = 1e300;
   if (a.N <= 64) return 64;
   if (a.causal == NNT_CAUSAL_OUT_LOWER) return 128;
-  const int64_t sms = num_sms(), mt = cdiv(a.M, BM), nb = a.batch0 * a.batch1;
   const int cands[3] = {256, 192, 128};
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
-    const int64_t tiles = mt * cdiv(a.N, bn) * nb;
-    const double cost = (double)cdiv(tiles, sms) * bn * (1.0 + 0.02 * (256 - bn) / 64.0);
-    if (cost < best_cost) {
+    const double cost = tile_cost(a, bn, 1, num_sms(), es_c);
+    if (cost < best_cost * 0.999) {  // ties go to the wider tile
       best_cost = cost;
       best = bn;
     }
@@ -1563,29 +1602,29 @@ int choose_bn(const GemmArgs& a, double* cost_out = nullptr) {
 }
 
 // CTA pairs (cta_group::2, 256-row tiles) for the plain projection-type GEMMs: unbatched,
-// non-causal, generic epilogue.  NNT_GEMM_CG=1 in the environment forces single-CTA tiles.
-bool use_pair(const GemmArgs& a) {
+// non-causal, generic epilogue.  NNT_GEMM_CG=1 in the environment forces single-CTA tiles,
+// NNT_GEMM_CG=2 forces pairs wherever they are legal.
+int forced_cg() {
   static const int forced = [] {
     const char* e = getenv("NNT_GEMM_CG");
     return e ? atoi(e) : 0;
   }();
-  if (forced == 1) return false;
+  return forced;
+}
+bool use_pair(const GemmArgs& a) {
+  if (forced_cg() == 1) return false;
   return a.batch0 * a.batch1 == 1 && a.causal == NNT_CAUSAL_NONE && a.M >= 2 * BM && a.N > 64 &&
          num_sms() >= 2;
 }
 
-// Wave model over SM pairs; widths whose half is a whole 64-column MN-major block.
-// (per-SM time of a 256 x BN pair tile ~ that of a 128 x BN single tile, so the costs compare
-// directly with choose_bn's)
-int choose_bn_pair(const GemmArgs& a, double* cost_out) {
-  const int64_t units = pair_units(), mt = cdiv(a.M, 2 * BM);
+// Pair widths whose half is a whole 64-column MN-major block.
+int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
   const int cands[2] = {256, 128};
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
-    const int64_t tiles = mt * cdiv(a.N, bn);
-    const double cost = (double)cdiv(tiles, units) * bn * (1.0 + 0.02 * (256 - bn) / 64.0);
-    if (cost < best_cost) {
+    const double cost = tile_cost(a, bn, 2, pair_units(), es_c);
+    if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = bn;
     }
@@ -1608,7 +1647,7 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   }
   if (a.a_rowsum) {  // R27: tiles <= 192 wide leave TMEM columns for the row-sum accumulators
     if (use_pair(a)) return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
-    switch (choose_bn(a)) {
+    switch (choose_bn(a, sizeof(TC))) {
       case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
       case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
       default: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);
@@ -1616,13 +1655,13 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   }
   if (use_pair(a)) {
     double cost_pair = 0, cost_single = 0;
-    const int bnp = choose_bn_pair(a, &cost_pair);
-    choose_bn(a, &cost_single);
-    if (splits > 1 || cost_pair <= cost_single)  // ties go to pairs (half the operand loads per SM)
+    const int bnp = choose_bn_pair(a, sizeof(TC), &cost_pair);
+    choose_bn(a, sizeof(TC), &cost_single);
+    if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single)  // ties go to pairs
       return bnp == 256 || splits > 1 ? launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits)
                                       : launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
   }
-  switch (splits > 1 ? 256 : choose_bn(a)) {
+  switch (splits > 1 ? 256 : choose_bn(a, sizeof(TC))) {
     case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
     case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
     case 192: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);

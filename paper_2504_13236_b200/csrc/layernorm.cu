@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(32 * kWarpRowsPerCta)
     ln_fwd_warp(const float* __restrict__ x, int64_t T, int E, int64_t ldx, const float* __restrict__ gamma,
                 const float* __restrict__ beta, float eps, TO* __restrict__ y, int64_t ldy,
                 float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  NNT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t stride = (int64_t)gridDim.x * kWarpRowsPerCta;
   int64_t row = (int64_t)blockIdx.x * kWarpRowsPerCta + (threadIdx.x >> 5);
@@ -112,6 +113,7 @@ __global__ void __launch_bounds__(kT) ln_fwd_cta(const float* __restrict__ x, in
                                                  const float* __restrict__ gamma, const float* __restrict__ beta,
                                                  float eps, TO* __restrict__ y, int64_t ldy,
                                                  float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  NNT_PDL_ENTRY();
   __shared__ float sh[kT / 32];
   const int64_t row = blockIdx.x;
   const float* xr = x + row * ldx;
@@ -172,6 +174,7 @@ __global__ void __launch_bounds__(32 * kRowsWarps, 2)
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 int64_t T, int E, int64_t rows_per_cta, const float* __restrict__ dres, float* __restrict__ dx,
                 int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb) {
+  NNT_PDL_ENTRY();
   extern __shared__ float4 red[];  // [kRowsWarps][2][E/4], used once at the end
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int E4 = E / 4;
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(kT) ln_bwd_cta(const float* __restrict__ dy, i
                                                  const float* dres, float* dx, int64_t lddx,
                                                  __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg,
                                                  float* __restrict__ pb) {
+  NNT_PDL_ENTRY();
   __shared__ float sh[kT / 32];
   float4 accg[NV], accb[NV], g4[NV];
 #pragma unroll
@@ -337,14 +341,14 @@ nnt_status launch_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, const f
     if (g64 > 2 * num_sms()) g64 = 2 * num_sms();
     unsigned grid = (unsigned)g64;
 #define NNT_LNFW(N) \
-  case N: ln_fwd_warp<TO, N><<<grid, 32 * kWarpRowsPerCta, 0, s>>>(x, T, (int)E, ldx, g, b, eps, y, ldy, mean, rstd); break;
+  case N: ::nnt::launch(ln_fwd_warp<TO, N>, grid, 32 * kWarpRowsPerCta, 0, s, x, T, (int)E, ldx, g, b, eps, y, ldy, mean, rstd); break;
     switch (nvw) { NNT_LNFW(1) NNT_LNFW(2) NNT_LNFW(4) NNT_LNFW(6) NNT_LNFW(8) }
 #undef NNT_LNFW
     return check_launch("layernorm_fwd");
   }
   int nv = pick_nv_cta(E);
 #define NNT_LNF(N) \
-  case N: ln_fwd_cta<TO, N><<<(unsigned)T, kT, 0, s>>>(x, E, ldx, g, b, eps, y, ldy, mean, rstd); break;
+  case N: ::nnt::launch(ln_fwd_cta<TO, N>, (unsigned)T, kT, 0, s, x, E, ldx, g, b, eps, y, ldy, mean, rstd); break;
   switch (nv) {
     NNT_LNF(1) NNT_LNF(2) NNT_LNF(3) NNT_LNF(4) NNT_LNF(6) NNT_LNF(8) NNT_LNF(12) NNT_LNF(16)
     default: return fail(NNT_ERR_UNSUPPORTED, "layernorm: unsupported E");
@@ -413,7 +417,7 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
     const size_t smem_red = (size_t)kRowsWarps * 2 * E * sizeof(float);  // <= 48 KB (E <= 1024)
 #define NNT_LNBR(N)                                                                                                \
   case N:                                                                                                          \
-    ln_bwd_rows<N><<<(unsigned)chunks, 32 * kRowsWarps, smem_red, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, T, \
+    ::nnt::launch(ln_bwd_rows<N>, (unsigned)chunks, 32 * kRowsWarps, smem_red, stream, dy, lddy, x, ldx, mean, rstd, gamma, T, \
                                                                             (int)E, rows_per_cta, dres, dx, lddx,  \
                                                                             d16, pg, pb);                          \
     break;
@@ -422,7 +426,7 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
   } else {
 #define NNT_LNB(N)                                                                                               \
   case N:                                                                                                        \
-    ln_bwd_cta<N><<<(unsigned)chunks, kT, 0, stream>>>(dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, \
+    ::nnt::launch(ln_bwd_cta<N>, (unsigned)chunks, kT, 0, stream, dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, \
                                                        d16, pg, pb);                                             \
     break;
     switch (pick_nv_cta(E)) { NNT_LNB(1) NNT_LNB(2) NNT_LNB(3) NNT_LNB(4) NNT_LNB(6) NNT_LNB(8) NNT_LNB(12) NNT_LNB(16) }

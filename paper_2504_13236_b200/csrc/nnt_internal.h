@@ -8,6 +8,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <string>
+#include <utility>
 
 #include "../../include/nnt.h"
 
@@ -71,7 +72,45 @@ struct LaunchScope {
 
 int num_sms();
 
+// ---------------------------------------------------------------- launches
+// Every libnnt kernel is launched with programmatic dependent launch (PDL) allowed: the next
+// kernel on the stream may be scheduled while this one drains, its CTAs run their prologue
+// (smem carve-up, barrier init, TMEM allocation) and then block in griddepcontrol.wait until
+// the previous grid has completed and its writes are visible (NNT_PDL_ENTRY at the top of
+// every kernel).  Inside a CUDA graph this becomes a programmatic edge, hiding the per-kernel
+// launch gap of the ~450-launch training step.  Enabled by NNT_PDL=1 in the environment.
+bool pdl_enabled();
+
 #if defined(__CUDACC__)
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                          Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+#endif
+
+#if defined(__CUDACC__)
+// ---------------------------------------------------------------- PDL (see launch())
+// Wait until the previous grid on the stream has completed (its memory visible), then allow
+// the next grid to be scheduled.  A no-op when the kernel was launched without PDL.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifndef NNT_PDL_NO_TRIGGER
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+#define NNT_PDL_ENTRY() ::nnt::pdl_entry()
+
 // ---------------------------------------------------------------- device math
 __device__ __forceinline__ float bf16_to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
 __device__ __forceinline__ __nv_bfloat16 f32_to_bf16(float v) { return __float2bfloat16_rn(v); }

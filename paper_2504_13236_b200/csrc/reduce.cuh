@@ -14,6 +14,7 @@ constexpr int kMergeWarps = 32;
 static __global__ void __launch_bounds__(32 * kMergeWarps)
     column_merge_kernel(const float* __restrict__ part_base, int64_t chunks, int64_t N, float* __restrict__ out0,
                         int accumulate, int64_t group_stride, float* __restrict__ out1) {
+  NNT_PDL_ENTRY();
   __shared__ float red[kMergeWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* __restrict__ part = part_base + blockIdx.y * group_stride;
@@ -45,13 +46,13 @@ static __global__ void __launch_bounds__(32 * kMergeWarps)
 
 static inline void launch_column_merge(const float* part, int64_t chunks, int64_t N, float* out, int accumulate,
                                 cudaStream_t s) {
-  column_merge_kernel<<<dim3((unsigned)((N + 31) / 32), 1), 32 * kMergeWarps, 0, s>>>(part, chunks, N, out, accumulate,
+  ::nnt::launch(column_merge_kernel, dim3((unsigned)((N + 31) / 32), 1), 32 * kMergeWarps, 0, s, part, chunks, N, out, accumulate,
                                                                                     0, out);
 }
 // two merges in one launch: part0 -> out0 and part0 + group_stride -> out1
 static inline void launch_column_merge2(const float* part0, int64_t group_stride, int64_t chunks, int64_t N,
                                         float* out0, float* out1, int accumulate, cudaStream_t s) {
-  column_merge_kernel<<<dim3((unsigned)((N + 31) / 32), 2), 32 * kMergeWarps, 0, s>>>(part0, chunks, N, out0,
+  ::nnt::launch(column_merge_kernel, dim3((unsigned)((N + 31) / 32), 2), 32 * kMergeWarps, 0, s, part0, chunks, N, out0,
                                                                                     accumulate, group_stride, out1);
 }
 

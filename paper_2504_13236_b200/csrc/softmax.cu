@@ -73,6 +73,7 @@ template <int NC>
 __global__ void __launch_bounds__(kThreads) maxsumexp_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
                                                              int64_t ldx, int64_t tile_k, int causal, int64_t seq_q,
                                                              float* __restrict__ stats, int accumulate) {
+  NNT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -150,6 +151,7 @@ __global__ void __launch_bounds__(kThreads) maxsumexp_merge_kernel(const float2*
                                                                    int64_t nparts, int64_t ld, int64_t part_cols,
                                                                    int causal, int64_t seq_q,
                                                                    float2* __restrict__ stats) {
+  NNT_PDL_ENTRY();
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (row >= rows) return;
   int64_t n = nparts;
@@ -170,6 +172,7 @@ template <typename T>
 __global__ void __launch_bounds__(kThreads) attn_rowdot_kernel(const T* __restrict__ dO, const T* __restrict__ O,
                                                                int64_t B, int64_t S, int64_t H, int64_t h,
                                                                float* __restrict__ D) {
+  NNT_PDL_ENTRY();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // ((b*S + s)*H + n)
   if (idx >= B * S * H) return;
   const int64_t n = idx % H, bs = idx / H, b = bs / S, s = bs % S;
@@ -197,6 +200,7 @@ __global__ void __launch_bounds__(kThreads) softmax_kernel(const float* __restri
                                                            int64_t ldx, int causal, int64_t seq_q,
                                                            const float* __restrict__ stats, TO* __restrict__ y,
                                                            int64_t ldy) {
+  NNT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -224,6 +228,7 @@ __global__ void __launch_bounds__(kThreads) softmax_bwd_kernel(const TP* __restr
                                                                const float* __restrict__ dp, int64_t lddp,
                                                                int64_t rows, int64_t cols, int causal, int64_t seq_q,
                                                                float scale, TO* __restrict__ da, int64_t ldda) {
+  NNT_PDL_ENTRY();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -301,7 +306,7 @@ nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx
   int nc = chunks_for(cols);
 #define NNT_MSE(N)                                                                                         \
   case N:                                                                                                  \
-    maxsumexp_kernel<N><<<row_blocks(rows), kThreads, 0, stream>>>(x, rows, cols, ldx, tile_k, causal, seq_q, \
+    ::nnt::launch(maxsumexp_kernel<N>, row_blocks(rows), kThreads, 0, stream, x, rows, cols, ldx, tile_k, causal, seq_q, \
                                                                    stats, accumulate);                     \
     break;
   switch (nc) { NNT_MSE(1) NNT_MSE(2) NNT_MSE(4) NNT_MSE(8) NNT_MSE(16) }
@@ -319,10 +324,10 @@ nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, 
   LaunchScope sc(NNT_K_MISC, stream, 2.0 * dtype_size(dtype) * n * h + 4.0 * n, 2.0 * n * h);
   const unsigned grid = (unsigned)((n + kThreads - 1) / kThreads);
   if (dtype == NNT_BF16)
-    attn_rowdot_kernel<__nv_bfloat16><<<grid, kThreads, 0, stream>>>((const __nv_bfloat16*)dO,
+    ::nnt::launch(attn_rowdot_kernel<__nv_bfloat16>, grid, kThreads, 0, stream, (const __nv_bfloat16*)dO,
                                                                      (const __nv_bfloat16*)O, B, S, H, h, D);
   else
-    attn_rowdot_kernel<float><<<grid, kThreads, 0, stream>>>((const float*)dO, (const float*)O, B, S, H, h, D);
+    ::nnt::launch(attn_rowdot_kernel<float>, grid, kThreads, 0, stream, (const float*)dO, (const float*)O, B, S, H, h, D);
   return check_launch("attn_rowdot");
 }
 
@@ -337,7 +342,7 @@ nnt_status nnt_maxsumexp_merge(const float* part, int64_t rows, int64_t nparts, 
   NNT_REQUIRE((reinterpret_cast<uintptr_t>(part) & 7u) == 0 && (reinterpret_cast<uintptr_t>(stats) & 7u) == 0,
               NNT_ERR_ALIGN, "nnt_maxsumexp_merge: pointers must be 8-byte aligned");
   LaunchScope sc(NNT_K_MAXSUMEXP, stream, 8.0 * rows * (causal ? 0.5 : 1.0) * nparts + 8.0 * rows, 0);
-  maxsumexp_merge_kernel<<<(unsigned)((rows + kThreads - 1) / kThreads), kThreads, 0, stream>>>(
+  ::nnt::launch(maxsumexp_merge_kernel, (unsigned)((rows + kThreads - 1) / kThreads), kThreads, 0, stream, 
       (const float2*)part, rows, nparts, ld_parts, part_cols, causal, seq_q, (float2*)stats);
   return check_launch("maxsumexp_merge");
 }
@@ -353,10 +358,10 @@ nnt_status nnt_softmax(const float* x, int64_t rows, int64_t cols, int64_t ldx, 
   double frac = causal ? 0.5 * (1.0 + 1.0 / (double)cols) : 1.0;
   LaunchScope sc(NNT_K_SOFTMAX, stream, (4.0 + dtype_size(y_dtype)) * rows * cols * frac + 8.0 * rows, 0);
   if (y_dtype == NNT_F32)
-    softmax_kernel<float><<<row_blocks(rows), kThreads, 0, stream>>>(x, rows, cols, ldx, causal, seq_q, stats,
+    ::nnt::launch(softmax_kernel<float>, row_blocks(rows), kThreads, 0, stream, x, rows, cols, ldx, causal, seq_q, stats,
                                                                      (float*)y, ldy);
   else
-    softmax_kernel<__nv_bfloat16><<<row_blocks(rows), kThreads, 0, stream>>>(x, rows, cols, ldx, causal, seq_q,
+    ::nnt::launch(softmax_kernel<__nv_bfloat16>, row_blocks(rows), kThreads, 0, stream, x, rows, cols, ldx, causal, seq_q,
                                                                              stats, (__nv_bfloat16*)y, ldy);
   return check_launch("softmax");
 }
@@ -377,7 +382,7 @@ nnt_status nnt_softmax_bwd(const void* p, int p_dtype, int64_t ldp, const float*
   unsigned g = row_blocks(rows);
 #define NNT_SMB(TP, TO, N)                                                                               \
   case N:                                                                                                \
-    softmax_bwd_kernel<TP, TO, N><<<g, kThreads, 0, stream>>>((const TP*)p, ldp, dp, lddp, rows, cols,    \
+    ::nnt::launch(softmax_bwd_kernel<TP, TO, N>, g, kThreads, 0, stream, (const TP*)p, ldp, dp, lddp, rows, cols,    \
                                                               causal, seq_q, scale, (TO*)da, ldda);      \
     break;
 #define NNT_SMB_ALL(TP, TO) \

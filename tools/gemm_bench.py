@@ -68,6 +68,7 @@ def main():
         ("fc+gelu", 0, 1, T, F, E, None, h, E, None, w, E, None, outb, 1, F, None,
          nnt.make_epilogue(bias=bias, act=1, aux=aux, ld_aux=F), 1.0),
         ("fc_plain", 0, 1, T, F, E, None, h, E, None, w, E, None, outb, 1, F, None, None, 1.0),
+        ("proj_plain", 0, 1, T, E, F, None, g, F, None, w, F, None, outb, 1, E, None, None, 1.0),
         ("proj_dx_plain", 0, 0, T, F, E, None, h, E, None, w, F, None, outb, 1, F, None, None, 1.0),
         ("proj", 0, 1, T, E, F, None, g, F, None, w, F, None, outf, 0, E, None,
          nnt.make_epilogue(bias=bias, residual=res, ld_residual=E), 1.0),
