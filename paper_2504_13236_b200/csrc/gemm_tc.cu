@@ -649,9 +649,27 @@ template <typename TC, int W>
 __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, TC* base, int64_t row, int64_t col0,
                                              const float (&v)[W]) {
   if (row >= M) return;
+  TC* dst = base + row * ld + col0;
+  if (col0 + W <= N && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0) {  // 16-byte vector stores
+#pragma unroll
+    for (int j = 0; j < W; j += 16 / (int)sizeof(TC)) {
+      uint4 u;
+      if (sizeof(TC) == 4) {
+        u = make_uint4(__float_as_uint(v[j]), __float_as_uint(v[j + 1]), __float_as_uint(v[j + 2]),
+                       __float_as_uint(v[j + 3]));
+      } else {
+        __nv_bfloat162 t0 = __floats2bfloat162_rn(v[j], v[j + 1]), t1 = __floats2bfloat162_rn(v[j + 2], v[j + 3]);
+        __nv_bfloat162 t2 = __floats2bfloat162_rn(v[j + 4], v[j + 5]), t3 = __floats2bfloat162_rn(v[j + 6], v[j + 7]);
+        u = make_uint4(*reinterpret_cast<uint32_t*>(&t0), *reinterpret_cast<uint32_t*>(&t1),
+                       *reinterpret_cast<uint32_t*>(&t2), *reinterpret_cast<uint32_t*>(&t3));
+      }
+      *reinterpret_cast<uint4*>(dst + j) = u;
+    }
+    return;
+  }
 #pragma unroll
   for (int j = 0; j < W; ++j)
-    if (col0 + j < N) base[row * ld + col0 + j] = from_f32<TC>(v[j]);
+    if (col0 + j < N) dst[j] = from_f32<TC>(v[j]);
 }
 
 // ------------------------------------------------------------------ kernel
@@ -1505,7 +1523,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     const bool tma_ok = c_tma_ok(a, es);
     NNT_REQUIRE(EPI == EPI_GENERIC || tma_ok, NNT_ERR_ALIGN, "gemm(bf16): specialised epilogue needs TMA-able C");
     (void)ok16;
-    P.tma_store = tma_ok ? 1 : 0;
+    P.tma_store = tma_ok ? 1 : 0;  // (direct 16-byte stores measured 1.5x slower than TMA stores)
     if (tma_ok) {
       NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
       if (a.act == NNT_ACT_GELU || P.in_kind == IN_AUX_SMEM || EPI == EPI_DA)  // GELU out / GELU', P in
