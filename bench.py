@@ -282,22 +282,52 @@ def run_nnt(args):
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     loss = float(st.loss.item())
 
-    # ---------------- per-kernel timing (CUDA events around every libnnt launch), same kernels
-    # launched eagerly (events cannot be inserted into the replayed graph).  A spin kernel queued
-    # ahead of each step lets the host enqueue the whole step before the GPU reaches it, so the
-    # start/stop events bracket device work only, not host launch latency.
-    graph, st.graph = getattr(st, "graph", None), None
-    nnt.nnt_timing_enable(True)
-    for i in range(args.steps):
-        x, r = dev_batches[i % 2]
-        torch.cuda._sleep(int(60e6))  # ~30 ms at 2 GHz, longer than one eager step's host enqueue
-        st.train_step(x, r)
-    torch.cuda.synchronize()
-    kt = nnt.nnt_timing_read()
-    nnt.nnt_timing_enable(False)
-    st.graph = graph
-    if graph is not None:
-        st.t_dev.fill_(st.step_count)  # keep the device step counter in line with the eager steps
+    # ---------------- per-kernel timing: CUDA events around every libnnt launch scope.  With graphs,
+    # a second graph of the same step is captured with timing on (the scopes become event-record
+    # nodes) and replayed, so the kernels are timed as they run in the timed region; otherwise the
+    # kernels run eagerly, a spin kernel queued ahead of each step so the events bracket device
+    # work only, not host launch latency.
+    kt = None
+    timing_mode = "eager"
+    if use_graph:
+        try:
+            nnt.nnt_timing_enable(True)
+            tg = st.capture_graph()
+            acc = {}
+            for i in range(args.steps):
+                x, r = dev_batches[i % 2]
+                st.xs[0].copy_(x)
+                st.r_buf.copy_(r)
+                tg.replay()
+                st.step_count += 1
+                torch.cuda.synchronize()
+                for k, v in nnt.nnt_timing_read().items():
+                    a = acc.setdefault(k, dict(ms=0.0, launches=0, bytes=0.0, flops=0.0))
+                    for f in a:
+                        a[f] += v[f]
+            kt = acc
+            timing_mode = "graph"
+            print(f"# graph-timed kernel sum {sum(v['ms'] for v in acc.values()) / args.steps:.3f} ms/step "
+                  f"(timed region {ms:.3f} ms/step)", file=sys.stderr)
+            del tg
+        except Exception as exc:  # event nodes unsupported: fall back to the eager pass
+            print(f"# graph timing failed ({exc!r}); eager timing pass", file=sys.stderr)
+            kt = None
+        finally:
+            nnt.nnt_timing_enable(False)
+    if kt is None:
+        graph, st.graph = getattr(st, "graph", None), None
+        nnt.nnt_timing_enable(True)
+        for i in range(args.steps):
+            x, r = dev_batches[i % 2]
+            torch.cuda._sleep(int(60e6))  # ~30 ms at 2 GHz, longer than one eager step's host enqueue
+            st.train_step(x, r)
+        torch.cuda.synchronize()
+        kt = nnt.nnt_timing_read()
+        nnt.nnt_timing_enable(False)
+        st.graph = graph
+        if graph is not None:
+            st.t_dev.fill_(st.step_count)  # keep the device step counter in line with the eager steps
 
     # ---------------- end to end: pinned host inputs copied every step, loss read back every step
     barrier()
@@ -342,7 +372,9 @@ def run_nnt(args):
             "peak": peaks["bf16_sus"] if d["bound"] == "tensor" else peaks["hbm"], "unit": d["unit"],
             "frac": d["frac"], "traffic": None, "traffic_source": None, "peak_source": peaks["src"] +
             (" bf16_tflops_sustained (kernel timed inside a long step)" if d["bound"] == "tensor" else " hbm_gbs"),
-            "timing": "CUDA events around every launch on its stream, K steps after the timed region",
+            "timing": f"CUDA events around every launch scope on its stream ({timing_mode}: "
+                      + ("event nodes in a replayed copy of the step graph" if timing_mode == "graph" else
+                         "eager launches behind a spin kernel") + "), K steps after the timed region",
             "share_of_step": d["share"]}
     roof["traffic"], roof["traffic_source"] = load_traffic(args.config, dom)
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

@@ -55,6 +55,16 @@ std::vector<TimingRecord> g_records;
 std::vector<cudaEvent_t> g_event_pool;
 std::atomic<int64_t> g_launches{0};
 
+// Inside a stream capture a plain cudaEventRecord only expresses a dependency; an
+// external record makes it an event-record node that timestamps every graph replay.
+void record(cudaEvent_t e, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(e, s);
+}
+
 cudaEvent_t take_event() {
   if (!g_event_pool.empty()) {
     cudaEvent_t e = g_event_pool.back();
@@ -73,7 +83,7 @@ LaunchScope::LaunchScope(int kclass, cudaStream_t s, double bytes, double flops,
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);
   TimingRecord r{kclass, take_event(), take_event(), bytes, flops, kernels};
-  cudaEventRecord(r.start, s);
+  record(r.start, s);
   slot_ = (int)g_records.size();
   g_records.push_back(r);
 }
@@ -88,7 +98,7 @@ void LaunchScope::add_kernels(int k) {
 LaunchScope::~LaunchScope() {
   if (slot_ < 0) return;
   std::lock_guard<std::mutex> lk(g_tmu);
-  cudaEventRecord(g_records[slot_].stop, s_);
+  record(g_records[slot_].stop, s_);
 }
 
 }  // namespace nnt
@@ -167,9 +177,14 @@ nnt_status nnt_timing_read(double* ms, int64_t* launches, double* bytes, double*
     if (flops) flops[k] = 0;
   }
   for (auto& r : g_records) {
-    NNT_CUDA_TRY(cudaEventSynchronize(r.stop));
     float t = 0.f;
-    NNT_CUDA_TRY(cudaEventElapsedTime(&t, r.start, r.stop));
+    cudaError_t e = cudaEventSynchronize(r.stop);
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&t, r.start, r.stop);
+    if (e != cudaSuccess) {
+      (void)cudaGetLastError();  // do not leave it for the next launch check
+      set_error("nnt_timing_read: %s", cudaGetErrorString(e));
+      return NNT_ERR_CUDA;
+    }
     if (ms) ms[r.kclass] += t;
     if (launches) launches[r.kclass] += 1;
     if (bytes) bytes[r.kclass] += r.bytes;

@@ -270,11 +270,20 @@ class BlockStack:
         With a process group (DP) the capture forks the communication stream off the compute
         stream at every bucket event: each bucket's NCCL all-reduce and Adam are graph nodes
         that overlap the rest of the backward pass, joined before the step ends."""
+        self.graph = self.capture_graph()
+        return self.graph
+
+    def capture_graph(self):
+        """One training step as a new CUDA graph (replay = one step; shares the step counter and
+        input buffers with enable_graph's graph).  With nnt_timing_enable(True) around the capture
+        the libnnt launch scopes become event-record nodes, timing every kernel class inside the
+        replayed graph (bench.py's per-kernel roofline)."""
         dev = self.dev
         if not hasattr(self, "r_buf"):
             self.r_buf = torch.empty_like(self.xs[0])
-        self.t_dev = torch.tensor([self.step_count], device=dev, dtype=torch.int64)
-        self.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
+        if not hasattr(self, "t_dev"):
+            self.t_dev = torch.tensor([self.step_count], device=dev, dtype=torch.int64)
+            self.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
         c = self.cfg
         hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
         hp.bias_corr_dev = self.bc_dev.data_ptr()
@@ -297,7 +306,6 @@ class BlockStack:
                                       self.w16 if self.bf16 else None, hp)
         finally:
             self._graph_hp = None  # eager steps keep host-side bias corrections
-        self.graph = g
         return g
 
     def _graph_step(self, x, r):
