@@ -57,7 +57,11 @@ constexpr int kBarBytes = kOnesOff + kOnesBytes;
 //   EPI_ROWSTATS per-row (max, sumexp) over all key tiles of a row block (ORDER_ROWS tasks),
 //                no C (softmax subroutine 1 with on-chip aggregation, R26)
 //   EPI_SOFTMAX  bf16 C = e^{alpha*acc - M} / S from the row's stats (subroutine 2, R26)
-enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4 };
+enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4, EPI_GENERIC_RS = 5 };
+// EPI_GENERIC_RS: the generic epilogue plus the a_rowsum ones-vector MMAs (R27).  A separate
+// instantiation: even predicated off, the extra tcgen05.mma issue sequences in the MMA loop cost
+// ~30% of the single-thread issue rate (measured 422 -> 286 ns per K-block of a lone tile).
+constexpr bool generic_epi(int e) { return e == EPI_GENERIC || e == EPI_GENERIC_RS; }
 
 // CG = CTAs per MMA (tcgen05 cta_group): 1, or 2 = an SM pair computing a 256 x BN tile
 // (each CTA stages its 128 A rows and half of the BN B rows; the leader issues M=256 MMAs).
@@ -78,7 +82,7 @@ struct Cfg {
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   // generic epilogue with BN <= 192: 32 more columns hold the a_rowsum accumulators (R27), 16 per
   // TMEM accumulator buffer
-  static constexpr bool ROWSUM = EPI == EPI_GENERIC && 2 * BN + 32 <= 512;
+  static constexpr bool ROWSUM = EPI == EPI_GENERIC_RS && 2 * BN + 32 <= 512;
   static constexpr int TCOLS = 2 * BN + (ROWSUM ? 32 : 0);
   static constexpr int TMEM_COLS = TCOLS <= 32 ? 32 : (TCOLS <= 64 ? 64 : (TCOLS <= 128 ? 128 : (TCOLS <= 256 ? 256 : 512)));
   static constexpr int EPI_OFF = STAGES * STAGE_BYTES;
@@ -223,6 +227,66 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
       "h"((uint16_t)3)
       : "memory");
+}
+
+
+// ---- warp-wide issue: the producer and MMA loops run on all 32 lanes of their warp (uniform
+// control flow, operands in uniform registers); each issuing instruction is guarded by an
+// elect.sync inside its asm, so exactly one lane issues it.  (A single-lane loop made the
+// compiler wrap every tcgen05.mma in an R2UR/ELECT waterfall: ~140 cycles per MMA issue.)
+#define NNT_ELECT "elect.sync _|e, 0xffffffff;\n\t"
+__device__ __forceinline__ void mbar_expect_tx_w(uint32_t bar, uint32_t bytes) {
+  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_w(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
+                                              int c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" NNT_ELECT
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_pair_w(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
+                                                   int c1, int c2, int c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" NNT_ELECT
+      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6}], [%2];\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" NNT_ELECT
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                                uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t" NNT_ELECT
+      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint32_t bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
+               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_commit_pair_w(uint32_t bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
+               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
+                   bar),
+               "h"((uint16_t)3)
+               : "memory");
 }
 
 // 32 consecutive fp32 columns of this warp's TMEM lane quadrant, no wait
@@ -684,7 +748,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
                    const __grid_constant__ CUtensorMap tmAux) {
-  static_assert(CG == 1 || (CG == 2 && EPI == EPI_GENERIC && (BN / 2) % 64 == 0), "CTA-pair configuration");
+  static_assert(CG == 1 || (CG == 2 && generic_epi(EPI) && (BN / 2) % 64 == 0), "CTA-pair configuration");
   using C = Cfg<BN, CG, EPI>;
   static_assert(EPI != EPI_DA || C::BUFS == 2, "EPI_DA double-buffers P");
   constexpr int W = 128 / (int)sizeof(TC);  // columns per 128-byte staging row
@@ -752,8 +816,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
   NNT_PDL_ENTRY();
 
   if (warp == 0) {
-    // ===================== TMA producer
-    if (lane == 0) {
+    // ===================== TMA producer (warp-wide, elected issue)
+    {
       int stage = 0;
       uint32_t phase = 0;
       for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
@@ -767,35 +831,35 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           const int k0 = (int)(kb * BK);
           if constexpr (CG == 2) {
             const uint32_t fb_local = smem_u32(&full[stage]);
-            if (rank == 0) mbar_expect_tx(fb_local, CG * C::STAGE_BYTES);
+            if (rank == 0) mbar_expect_tx_w(fb_local, CG * C::STAGE_BYTES);
             const uint32_t fb = map_to_rank(fb_local, 0);
             if (P.a_kmajor) {
-              tma_load_4d_pair(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+              tma_load_4d_pair_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
-                tma_load_4d_pair(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
+                tma_load_4d_pair_w(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
             }
             if (P.b_kmajor) {
-              tma_load_4d_pair(sb, &tmB, fb, k0, nb0, q, p);
+              tma_load_4d_pair_w(sb, &tmB, fb, k0, nb0, q, p);
             } else {
 #pragma unroll
-              for (int j = 0; j < BN / CG / 64; ++j) tma_load_4d_pair(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
+              for (int j = 0; j < BN / CG / 64; ++j) tma_load_4d_pair_w(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
             }
           } else {
             const uint32_t fb = smem_u32(&full[stage]);
-            mbar_expect_tx(fb, C::STAGE_BYTES);
+            mbar_expect_tx_w(fb, C::STAGE_BYTES);
             if (P.a_kmajor) {
-              tma_load_4d(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+              tma_load_4d_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
             } else {
 #pragma unroll
-              for (int j = 0; j < BM / 64; ++j) tma_load_4d(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
+              for (int j = 0; j < BM / 64; ++j) tma_load_4d_w(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
             }
             if (P.b_kmajor) {
-              tma_load_4d(sb, &tmB, fb, k0, (int)ti.n0, q, p);
+              tma_load_4d_w(sb, &tmB, fb, k0, (int)ti.n0, q, p);
             } else {
 #pragma unroll
-              for (int j = 0; j < BN / 64; ++j) tma_load_4d(sb + j * 8192, &tmB, fb, (int)ti.n0 + 64 * j, k0, q, p);
+              for (int j = 0; j < BN / 64; ++j) tma_load_4d_w(sb + j * 8192, &tmB, fb, (int)ti.n0 + 64 * j, k0, q, p);
             }
           }
           if (++stage == C::STAGES) {
@@ -807,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (CTA pair: the leader only)
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // warp-wide loop, elected issue
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -832,9 +896,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             uint64_t ad = make_sdesc(sa + kk * a_step, a_lbo, 1024u);
             uint64_t bd = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
             if constexpr (CG == 2)
-              mma_bf16_pair(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+              mma_bf16_pair_w(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
             else
-              mma_bf16(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+              mma_bf16_w(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
             if constexpr (C::ROWSUM) {
               // R27: sum_k op(A)[i][k] = op(A) x ones, into 16 columns past the two accumulators
               // (the first N tile of each row block only)
@@ -842,32 +906,32 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
                 const uint64_t od = make_sdesc_noswz(smem_u32(ones), 128u, 256u);
                 const uint32_t tr = tmem_base + (uint32_t)(2 * BN + acc * 16);
                 if constexpr (CG == 2)
-                  mma_bf16_pair(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+                  mma_bf16_pair_w(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
                 else
-                  mma_bf16(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+                  mma_bf16_w(tr, ad, od, P.idesc_ones, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
               }
             }
           }
           if constexpr (CG == 2)
-            mma_commit_pair(smem_u32(&empty[stage]));
+            mma_commit_pair_w(smem_u32(&empty[stage]));
           else
-            mma_commit(smem_u32(&empty[stage]));
+            mma_commit_w(smem_u32(&empty[stage]));
           if (++stage == C::STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
         if constexpr (CG == 2)
-          mma_commit_pair(smem_u32(&tfull[acc]));
+          mma_commit_pair_w(smem_u32(&tfull[acc]));
         else
-          mma_commit(smem_u32(&tfull[acc]));
+          mma_commit_w(smem_u32(&tfull[acc]));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
         }
       }
     }
-  } else if constexpr (EPI != EPI_GENERIC) {
+  } else if constexpr (!generic_epi(EPI)) {
     // ===================== specialised epilogues (attention score-type GEMMs)
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
@@ -1477,7 +1541,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.f_b1.init(a.batch1);
   P.ws_mode = splits > 1 ? 1 : 0;
   // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
-  if (P.ws_mode || EPI != EPI_GENERIC)
+  if (P.ws_mode || !generic_epi(EPI))
     P.in_kind = IN_NONE;
   else if (a.act == NNT_ACT_GELU_BWD)
     P.in_kind = sizeof(TC) == 2 && c_tma_ok(a, sizeof(TC)) && aligned16(a.aux) &&
@@ -1521,7 +1585,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.tma_store = 0;  // no C
   } else {
     const bool tma_ok = c_tma_ok(a, es);
-    NNT_REQUIRE(EPI == EPI_GENERIC || tma_ok, NNT_ERR_ALIGN, "gemm(bf16): specialised epilogue needs TMA-able C");
+    NNT_REQUIRE(generic_epi(EPI) || tma_ok, NNT_ERR_ALIGN, "gemm(bf16): specialised epilogue needs TMA-able C");
     (void)ok16;
     P.tma_store = tma_ok ? 1 : 0;  // (direct 16-byte stores measured 1.5x slower than TMA stores)
     if (tma_ok) {
@@ -1671,11 +1735,11 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
       return launch_bn<128, TC, EPI_SCORES>(a, s, 1);
   }
   if (a.a_rowsum) {  // R27: tiles <= 192 wide leave TMEM columns for the row-sum accumulators
-    if (use_pair(a)) return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+    if (use_pair(a)) return launch_bn<128, TC, EPI_GENERIC_RS, 2>(a, s, splits);
     switch (choose_bn(a, sizeof(TC))) {
-      case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
-      case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
-      default: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);
+      case 64: return launch_bn<64, TC, EPI_GENERIC_RS>(a, s, splits);
+      case 128: return launch_bn<128, TC, EPI_GENERIC_RS>(a, s, splits);
+      default: return launch_bn<192, TC, EPI_GENERIC_RS>(a, s, splits);
     }
   }
   if (use_pair(a)) {
