@@ -292,7 +292,11 @@ def run_nnt(args):
     if use_graph:
         try:
             nnt.nnt_timing_enable(True)
-            tg = st.capture_graph()
+            side, st.side = st.side, None  # kernels timed one at a time (no side-stream overlap)
+            try:
+                tg = st.capture_graph()
+            finally:
+                st.side = side
             acc = {}
             for i in range(args.steps):
                 x, r = dev_batches[i % 2]

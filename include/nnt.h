@@ -388,6 +388,18 @@ nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, co
                          const nnt_block_grads* g, int accumulate_grads,
                          nnt_event_t* grad_ready, nnt_stream_t stream);
 
+/* nnt_block_bwd with a second stream: the ops that only produce weight / bias gradients
+ * (the four dW GEMMs, the FC / out / QKV bias column sums) run on `side_stream`, forked
+ * from `stream` after the ops they depend on and joined back into `stream` before the call
+ * returns, so they fill the gaps of the dX chain.  Same results bit for bit.  side_stream
+ * NULL = nnt_block_bwd.  grad_ready events (if given) are recorded on `stream` after the
+ * join.  NNT_ERR_ARG if side_stream == stream. */
+nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
+                                 const void* saved, void* scratch, const float* dy, float* dx,
+                                 const nnt_block_grads* g, int accumulate_grads,
+                                 nnt_event_t* grad_ready, nnt_stream_t stream,
+                                 nnt_stream_t side_stream);
+
 /* ------------------------------------------------------------------------- */
 /* Tile-task DAG (STF rules S:46)                               */
 /* ------------------------------------------------------------------------- */

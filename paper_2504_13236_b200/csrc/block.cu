@@ -15,7 +15,7 @@ struct Layout {
   // saved (per layer)
   size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
   // scratch
-  size_t scores, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, lnscr, gemm_ws, scratch_bytes;
+  size_t scores, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, colsum2, lnscr, gemm_ws, scratch_bytes;
   size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes;
 };
 
@@ -61,6 +61,7 @@ Layout make_layout(const nnt_block_cfg& c) {
   size_t cs2 = nnt_bias_grad_scratch_bytes(T, 3 * E);
   L.colsum_bytes = cs > cs2 ? cs : cs2;
   L.colsum = take(L.colsum_bytes);
+  L.colsum2 = take(L.colsum_bytes);  // the side stream's column sums (FC_DB, OUT_DB, QKV_DB)
   L.lnscr_bytes = nnt_layernorm_bwd_scratch_bytes(T, E);
   L.lnscr = take(L.lnscr_bytes);
   // split-K partials of the four dW GEMMs ([3E x E], [E x E], [4E x E], [E x 4E], K = T)
@@ -102,6 +103,7 @@ struct Ctx {
   uint8_t* sc;
   Layout L;
   cudaStream_t st;
+  cudaStream_t side;  // nnt_block_bwd_streams: weight/bias-gradient ops run here (or NULL)
   template <typename P>
   P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
   template <typename P>
@@ -222,7 +224,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, F, E, nullptr, 1.f, dyA, E, nullptr, p->w_pr, F, nullptr, 0.f,
                   x.k<void>(x.L.du), dt, F, nullptr, &e);
     case NNT_OP_FC_DB:
-      return nnt_bias_grad(x.k<void>(x.L.du), dt, T, F, F, g->b_fc, acc, nullptr, x.k<void>(x.L.colsum),
+      return nnt_bias_grad(x.k<void>(x.L.du), dt, T, F, F, g->b_fc, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_FC_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, F, E, T, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr,
@@ -236,7 +238,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                                bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, acc, x.k<void>(x.L.lnscr),
                                x.L.lnscr_bytes, x.st);
     case NNT_OP_OUT_DB:
-      return nnt_bias_grad(x.k<float>(x.L.dx1), NNT_F32, T, E, E, g->b_o, acc, nullptr, x.k<void>(x.L.colsum),
+      return nnt_bias_grad(x.k<float>(x.L.dx1), NNT_F32, T, E, E, g->b_o, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_OUT_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, E, E, T, nullptr, 1.f, dx1A, E, nullptr, x.s<void>(x.L.O), E, nullptr,
@@ -283,7 +285,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                   3 * E, sq, 0.f, x.k<uint8_t>(x.L.dqkv) + es * E, dt, 3 * E, sq, &e);
     }
     case NNT_OP_QKV_DB:
-      return nnt_bias_grad(x.k<void>(x.L.dqkv), dt, T, 3 * E, 3 * E, g->b_qkv, acc, nullptr, x.k<void>(x.L.colsum),
+      return nnt_bias_grad(x.k<void>(x.L.dqkv), dt, T, 3 * E, 3 * E, g->b_qkv, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_QKV_DW:
       return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * E, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
@@ -317,6 +319,7 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.sc = (uint8_t*)scratch;
   x.L = make_layout(c);
   x.st = st;
+  x.side = nullptr;
   return x;
 }
 
@@ -364,15 +367,43 @@ nnt_status nnt_block_fwd(const nnt_block_cfg* cfg, const nnt_block_params* p, co
 nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x, const void* saved,
                          void* scratch, const float* dy, float* dx, const nnt_block_grads* g, int accumulate_grads,
                          nnt_event_t* grad_ready, nnt_stream_t stream) {
+  return nnt_block_bwd_streams(cfg, p, x, saved, scratch, dy, dx, g, accumulate_grads, grad_ready, stream, nullptr);
+}
+
+nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
+                                 const void* saved, void* scratch, const float* dy, float* dx,
+                                 const nnt_block_grads* g, int accumulate_grads, nnt_event_t* grad_ready,
+                                 nnt_stream_t stream, nnt_stream_t side_stream) {
   NNT_TRY(check_cfg(cfg));
   NNT_REQUIRE(p && x && saved && scratch && dy && dx && g, NNT_ERR_NULL, "nnt_block_bwd: NULL argument");
   NNT_REQUIRE(g->ln1_g && g->ln1_b && g->ln2_g && g->ln2_b && g->w_qkv && g->w_o && g->w_fc && g->w_pr && g->b_qkv &&
                   g->b_o && g->b_fc && g->b_pr,
               NNT_ERR_NULL, "nnt_block_bwd: NULL gradient");
+  NNT_REQUIRE(side_stream == nullptr || side_stream != stream, NNT_ERR_ARG,
+              "nnt_block_bwd_streams: side stream must differ from the main stream");
   const BlockPlan* plan = block_plan(*cfg, 1);
   NNT_REQUIRE(plan != nullptr, NNT_ERR_SHAPE, "nnt_block_bwd: %s", nnt_last_error());
   NNT_TRY(check_plan(plan));
   Ctx c = make_ctx(*cfg, const_cast<void*>(saved), scratch, stream);
+  cudaStream_t side = (cudaStream_t)side_stream;
+  // Ops that only produce weight / bias gradients leave the critical dX chain: with a side
+  // stream they run there, each after everything enqueued on the main stream so far (one
+  // fork event per batch of side ops), and the main stream joins the side stream at the end.
+  // They write disjoint gradients and read buffers the main stream does not overwrite within
+  // this call (the side column sums use their own scratch), so results are bitwise unchanged.
+  auto on_side = [&](int op) {
+    return side != nullptr && (op == NNT_OP_PROJ_DW || op == NNT_OP_FC_DB || op == NNT_OP_FC_DW ||
+                               op == NNT_OP_OUT_DB || op == NNT_OP_OUT_DW || op == NNT_OP_QKV_DB ||
+                               op == NNT_OP_QKV_DW);
+  };
+  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (side && !ev_fork) {
+    NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  }
+  Ctx cs = c;
+  cs.st = side;
+  bool main_advanced = true;  // main-stream work not yet visible to the side stream
   // Gradient sets for the DP events: each fires once every op that writes the set's
   // gradients OR reads the set's weights has been enqueued, so an optimizer step
   // on another stream after the event cannot race with this backward pass.
@@ -383,13 +414,30 @@ nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, co
   int remaining[4];
   for (int k = 0; k < 4; ++k) remaining[k] = sets[k][3] < 0 ? 3 : 4;
   for (const auto& gr : plan->groups) {
-    NNT_TRY(run_bwd_op(c, gr.op, p, x, dy, dx, g, accumulate_grads));
-    if (grad_ready) {
+    if (on_side(gr.op)) {
+      if (main_advanced) {
+        NNT_CUDA_TRY(cudaEventRecord(ev_fork, stream));
+        NNT_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+        main_advanced = false;
+      }
+      NNT_TRY(run_bwd_op(cs, gr.op, p, x, dy, dx, g, accumulate_grads));
+    } else {
+      NNT_TRY(run_bwd_op(c, gr.op, p, x, dy, dx, g, accumulate_grads));
+      main_advanced = true;
+    }
+    if (grad_ready && !side) {
       for (int k = 0; k < 4; ++k)
         for (int j = 0; j < 4; ++j)
           if (sets[k][j] == gr.op && --remaining[k] == 0 && grad_ready[k])
             NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
     }
+  }
+  if (side) {  // join: the main stream continues only after the side stream's work
+    NNT_CUDA_TRY(cudaEventRecord(ev_join, side));
+    NNT_CUDA_TRY(cudaStreamWaitEvent(stream, ev_join, 0));
+    if (grad_ready)
+      for (int k = 0; k < 4; ++k)
+        if (grad_ready[k]) NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
   }
   return NNT_OK;
 }

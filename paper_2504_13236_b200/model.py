@@ -79,6 +79,7 @@ class StackConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 0.0
+    side_stream: bool = True  # weight/bias-gradient ops of the backward on a second stream
 
     def block_cfg(self):
         return nnt.nnt_block_cfg(self.E, self.H, self.S, self.B, self.tile_e, self.tile_f, self.tile_s, self.tile_t,
@@ -136,6 +137,7 @@ class BlockStack:
         self.loss = torch.zeros(1, **act)
         self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
         self.comm = torch.cuda.Stream(device=self.dev) if self.dp else None
+        self.side = torch.cuda.Stream(device=self.dev) if cfg.side_stream else None
         self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.dp else None
         if self.dp:  # torch creates the CUDA event handles lazily, at the first record()
             for evs in self.events:
@@ -195,8 +197,9 @@ class BlockStack:
         dp = self.dp
         for l in range(self.cfg.L - 1, -1, -1):
             ev = self.events[l] if dp else None
-            nnt.nnt_block_bwd(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch, self.dy[cur],
-                              self.dy[1 - cur], self._grads[l], 0, ev)
+            nnt.nnt_block_bwd_streams(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch,
+                                      self.dy[cur], self.dy[1 - cur], self._grads[l], 0, ev,
+                                      side_stream=self.side)
             if dp:
                 for si in range(4):
                     self._reduce_bucket(l, si, ev[si], overlap_optimizer)

@@ -45,7 +45,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick",
            "nnt_convert",
-           "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd",
+           "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd", "nnt_block_bwd_streams",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count")
 
@@ -130,6 +130,8 @@ _sig = {
     "nnt_block_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp]),
     "nnt_block_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp,
                              C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp]),
+    "nnt_block_bwd_streams": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp,
+                                     _vp, C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp, _vp]),
     "nnt_op_name": (C.c_char_p, [_i32]),
     "nnt_block_dag_describe": (_i32, [C.POINTER(nnt_block_cfg), _i32, C.POINTER(nnt_task), _i64, _P64,
                                       C.POINTER(nnt_launch_group), _i64, _P64]),
@@ -325,17 +327,28 @@ def nnt_block_fwd(cfg, params, x, y, saved, scratch, stream=None):
                                    _stream(stream)))
 
 
+def nnt_block_bwd_streams(cfg, params, x, saved, scratch, dy, dx, grads, accumulate_grads, grad_ready=None,
+                          stream=None, side_stream=None):
+    ev = _events(grad_ready)
+    return check(lib.nnt_block_bwd_streams(C.byref(cfg), C.byref(params), ptr(x), ptr(saved), ptr(scratch), ptr(dy),
+                                           ptr(dx), C.byref(grads), accumulate_grads, ev, _stream(stream),
+                                           None if side_stream is None else _stream(side_stream)))
+
+
+def _events(grad_ready):
+    if grad_ready is None:
+        return None
+    handles = [e.cuda_event if hasattr(e, "cuda_event") else e for e in grad_ready]
+    # torch creates an Event's CUDA handle lazily at its first record(): a 0 handle here would
+    # silently disable the event (the library skips NULL events) and race the comm stream
+    if not all(handles):
+        raise ValueError("nnt_block_bwd: grad_ready events must be created (record() once) before use")
+    return (C.c_void_p * 4)(*handles)
+
+
 def nnt_block_bwd(cfg, params, x, saved, scratch, dy, dx, grads, accumulate_grads, grad_ready=None, stream=None):
-    ev = None
-    if grad_ready is not None:
-        handles = [e.cuda_event if hasattr(e, "cuda_event") else e for e in grad_ready]
-        # torch creates an Event's CUDA handle lazily at its first record(): a 0 handle here would
-        # silently disable the event (the library skips NULL events) and race the comm stream
-        if not all(handles):
-            raise ValueError("nnt_block_bwd: grad_ready events must be created (record() once) before use")
-        ev = (C.c_void_p * 4)(*handles)
     return check(lib.nnt_block_bwd(C.byref(cfg), C.byref(params), ptr(x), ptr(saved), ptr(scratch), ptr(dy), ptr(dx),
-                                   C.byref(grads), accumulate_grads, ev, _stream(stream)))
+                                   C.byref(grads), accumulate_grads, _events(grad_ready), _stream(stream)))
 
 
 def nnt_op_name(op):

@@ -180,3 +180,27 @@ def test_block_determinism_bitwise():
         torch.cuda.synchronize()
         outs.append((st.xs[-1].clone(), st.g.clone()))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_side_stream_backward_bitwise(graph):
+    """nnt_block_bwd_streams: the weight/bias-gradient ops on a second stream (forked and joined
+    inside each call) give results bitwise equal to the single-stream backward."""
+    E, H, S, B, L = 768, 12, 256, 2, 2
+    outs = []
+    for side in (False, True):
+        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", side_stream=side)
+        layers = [nnt_inputs.make_params(E, seed=11, layer=l, init="parity", n_layers=L) for l in range(L)]
+        st = model.BlockStack(sc, layers)
+        if graph:
+            st.enable_graph()
+        losses = []
+        for t in range(2):
+            x = dev(nnt_inputs.make_x(E, S, 0, B, seed=90 + t))
+            r = dev(nnt_inputs.make_r(E, S, 0, B, seed=90 + t))
+            losses.append(st.train_step(x, r).item())
+        torch.cuda.synchronize()
+        outs.append((losses, st.g.clone(), st.w.clone(), st.dy[L % 2].clone()))
+    assert outs[0][0] == outs[1][0]
+    for a, b in zip(outs[0][1:], outs[1][1:]):
+        assert torch.equal(a, b)

@@ -35,5 +35,7 @@ def launches(path, top=30):
 
 
 if __name__ == "__main__":
+    import signal
+    signal.signal(signal.SIGPIPE, signal.SIG_DFL)
     for p in sys.argv[1:]:
         (bench if p.endswith('.log') or p.endswith('.json') else launches)(p)
