@@ -19,6 +19,7 @@ bucket, overlapping the rest of the backward pass.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -79,7 +80,8 @@ class StackConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 0.0
-    side_stream: bool = True  # weight/bias-gradient ops of the backward on a second stream
+    # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
+    side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
 
     def block_cfg(self):
         return nnt.nnt_block_cfg(self.E, self.H, self.S, self.B, self.tile_e, self.tile_f, self.tile_s, self.tile_t,
