@@ -125,3 +125,30 @@ def make_matrix(shape, seed, kind="normal", lo=-4, hi=4):
     if kind == "int":
         return rng.integers(lo, hi + 1, size=shape).astype(np.float32)
     raise ValueError(kind)
+
+
+# ---------------------------------------------------------------- GPT-2 shell
+def make_shell_params(V, S_max, E, seed=1234, init="parity"):
+    """Token table wte [V, E], position table wpe [S_max, E], final LayerNorm (lnf_g, lnf_b).
+
+    parity: wte, wpe ~ N(0, 1/E), lnf_g ~ 1 + N(0, 0.1^2), lnf_b ~ N(0, 0.1^2);
+    gpt2:   wte ~ N(0, 0.02^2), wpe ~ N(0, 0.01^2), lnf_g = 1, lnf_b = 0."""
+    out = {}
+    for i, (name, shp) in enumerate((("wte", (V, E)), ("wpe", (S_max, E)), ("lnf_g", (E,)), ("lnf_b", (E,)))):
+        rng = _rng(seed, 999, i)
+        if name in ("wte", "wpe"):
+            std = (0.02 if name == "wte" else 0.01) if init == "gpt2" else 1.0 / math.sqrt(E)
+            a = std * rng.standard_normal(shp, dtype=np.float32)
+        elif name == "lnf_g":
+            a = np.ones(shp) if init == "gpt2" else 1.0 + 0.1 * rng.standard_normal(shp)
+        else:
+            a = np.zeros(shp) if init == "gpt2" else 0.1 * rng.standard_normal(shp)
+        out[name] = np.ascontiguousarray(a, dtype=np.float32)
+    return out
+
+
+def make_ids(V, S, batch_begin, batch_end, seed=5678):
+    """Token ids ~ U[0, V) for global sequences [batch_begin, batch_end) (int32 [n, S + 1]):
+    inputs are [:, :S], next-token labels [:, 1:]."""
+    seqs = [_rng(seed, 2, j).integers(0, V, size=S + 1, dtype=np.int64) for j in range(batch_begin, batch_end)]
+    return np.ascontiguousarray(np.stack(seqs).astype(np.int32))

@@ -301,6 +301,84 @@ def probe_loss_grad(r, t_global):
 
 
 # ---------------------------------------------------------------------------
+# GPT-2 shell: embedding layer, tied LM head, cross-entropy
+# ---------------------------------------------------------------------------
+def embed_fwd(ids, wte, wpe):
+    """x[b, s] = wte[ids[b, s]] + wpe[s].
+
+    PAPER.md:133-137 (the embedding layer equips every token with an N_e vector from an
+    N_v x N_e table); the learned position table wpe is GPT-2's (reading R29)."""
+    ids = np.asarray(ids)
+    return _f64(wte)[ids] + _f64(wpe)[None, : ids.shape[1], :]
+
+
+def embed_bwd(ids, dx, n_vocab, n_pos):
+    """dwte[v] = sum_{(b,s): ids[b,s] = v} dx[b, s];  dwpe[s] = sum_b dx[b, s].
+
+    Written as the one-hot contraction dwte = onehot(ids)^T dx (the adjoint of the gather)."""
+    ids = np.asarray(ids).reshape(-1)
+    dx = _f64(dx)
+    onehot = np.zeros((ids.size, n_vocab))
+    onehot[np.arange(ids.size), ids] = 1.0
+    dwte = onehot.T @ dx.reshape(-1, dx.shape[-1])
+    dwpe = np.zeros((n_pos, dx.shape[-1]))
+    dwpe[: dx.shape[1]] = dx.sum(axis=0)
+    return dwte, dwpe
+
+
+def cross_entropy(logits, labels):
+    """Per-sample loss  -log( e^{x_c} / sum_j e^{x_j} )  (sign typo read as the
+    positive NLL, reading R13), computed through the SoftMax subroutines:
+    (M, S) = maxsumexp(x) per row, loss = log S + M - x_c.  Returns (per-row loss, stats)."""
+    x = _f64(logits)
+    m, ssum = maxsumexp(x)                 # per row: (max, sumexp) = softmax subroutine 1
+    rows = np.arange(x.shape[0])
+    loss = np.log(ssum) + m - x[rows, np.asarray(labels)]
+    return loss, (m, ssum)
+
+
+def cross_entropy_grad(logits, labels, scale):
+    """d(scale * sum_rows loss)/dx = scale * (softmax(x) - onehot(c))."""
+    p = softmax(_f64(logits))
+    p[np.arange(p.shape[0]), np.asarray(labels)] -= 1.0
+    return scale * p
+
+
+def gpt2_fwd(model, ids, labels, n_h, causal=True, eps=1e-5):
+    """Full GPT-2: embedding -> L pre-LN blocks -> final LayerNorm -> tied LM head -> mean CE.
+
+    model: dict with 'wte' [V, E], 'wpe' [S_max, E], 'lnf_g', 'lnf_b' [E] and 'blocks' (list of
+    block parameter dicts).  Loss = (1/T) sum_t CE_t (mean over tokens, reading R13).
+    Returns (loss, cache)."""
+    x0 = embed_fwd(ids, model["wte"], model["wpe"])
+    xl, caches = stack_fwd(model["blocks"], x0, n_h, causal, eps)
+    hf, mu, r = layernorm_fwd(xl, model["lnf_g"], model["lnf_b"], eps)
+    b, s, e = hf.shape
+    logits = hf.reshape(-1, e) @ _f64(model["wte"]).T
+    loss_rows, _ = cross_entropy(logits, np.asarray(labels).reshape(-1))
+    t = b * s
+    cache = dict(ids=np.asarray(ids), labels=np.asarray(labels).reshape(-1), caches=caches, xl=xl, hf=hf, mu=mu,
+                 r=r, logits=logits, t=t)
+    return float(loss_rows.sum() / t), cache
+
+
+def gpt2_bwd(model, cache, t_global=None):
+    """Gradients of gpt2_fwd's loss (scaled by 1/t_global; default the batch's T) w.r.t. every
+    parameter: dict with 'wte' (LM head + embedding, tied), 'wpe', 'lnf_g', 'lnf_b', 'blocks'."""
+    t_global = cache["t"] if t_global is None else t_global
+    wte = _f64(model["wte"])
+    dlogits = cross_entropy_grad(cache["logits"], cache["labels"], 1.0 / t_global)
+    hf = cache["hf"]
+    b, s, e = hf.shape
+    dhf = (dlogits @ wte).reshape(b, s, e)
+    dwte = dlogits.T @ hf.reshape(-1, e)
+    dxl, dlnf_g, dlnf_b = layernorm_bwd(dhf, cache["xl"], model["lnf_g"], cache["mu"], cache["r"])
+    dx0, gblocks = stack_bwd(model["blocks"], cache["caches"], dxl)
+    dwte_e, dwpe = embed_bwd(cache["ids"], dx0, wte.shape[0], _f64(model["wpe"]).shape[0])
+    return dict(wte=dwte + dwte_e, wpe=dwpe, lnf_g=dlnf_g, lnf_b=dlnf_b, blocks=gblocks)
+
+
+# ---------------------------------------------------------------------------
 # Adam / AdamW (PAPER.md:189-194; reading R12)
 # ---------------------------------------------------------------------------
 def adam_step(w, g, m, v, t, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
