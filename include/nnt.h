@@ -339,6 +339,40 @@ nnt_status nnt_dot(const float* y, const float* r, int64_t n, float scale, float
                    void* scratch, size_t scratch_bytes, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* GPT-2 shell: embedding layer and cross-entropy loss       */
+/* ------------------------------------------------------------------------- */
+/* Embedding layer (learned positions, reading R29):
+ *   x[t] = wte[ids[t]] + wpe[t mod S]  for t < T (T = B*S tokens, row-major [B][S]).
+ * ids: device int32 [T] in [0, V) (out-of-range ids are clamped); wte: device fp32 [V][E];
+ * wpe: device fp32 [>= S][E]; x: device fp32 [T][E].  E % 4 == 0, 16-byte aligned. */
+nnt_status nnt_embedding_fwd(const int32_t* ids, int64_t T, int64_t S, const float* wte, int64_t V,
+                             const float* wpe, int64_t E, float* x, nnt_stream_t stream);
+
+/* Scratch bytes of nnt_embedding_bwd (a counting sort of the T token positions by id). */
+size_t nnt_embedding_bwd_scratch_bytes(int64_t T, int64_t V);
+
+/* Adjoint of nnt_embedding_fwd: dwte[v] (+)= sum over tokens t with ids[t] == v of dx[t]
+ * (added in ascending t), dwpe[s] (+)= sum_b dx[b*S + s] (ascending b); accumulate != 0 adds
+ * into dwte / dwpe (rows of dwte whose id does not occur are then untouched), 0 overwrites.
+ * Deterministic (integer counting sort, no floating-point atomics).  dx: device fp32 [T][E];
+ * dwte: [V][E]; dwpe: [>= S][E] (rows >= S untouched). */
+nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const float* dx, int64_t E,
+                             float* dwte, int64_t V, float* dwpe, int accumulate, void* scratch,
+                             size_t scratch_bytes, nnt_stream_t stream);
+
+/* Cross-entropy through the two SoftMax subroutines (R13): per row r of
+ * the logits x (device fp32/bf16 [rows][ld], V classes), subroutine 1 gives (M_r, S_r) =
+ * (max_k x, sum_k e^{x - M}) (R10 merge, fixed order) and
+ *   loss_rows[r] = log S_r + M_r - x[r][labels[r]]            (if loss_rows != NULL)
+ *   stats[r]     = (M_r, S_r)                                 (if stats != NULL, fp32 [rows][2])
+ *   dlogits[r][k] = scale * (e^{x[r][k] - M_r} / S_r - [k == labels[r]])   (if dlogits != NULL;
+ *                   same dtype as x, row pitch ld_d, may alias x)
+ * labels: device int32 [rows] (clamped to [0, V)).  Rows 16-byte aligned. */
+nnt_status nnt_cross_entropy(const void* logits, int dtype, int64_t rows, int64_t V, int64_t ld,
+                             const int32_t* labels, float scale, float* loss_rows, float* stats,
+                             void* dlogits, int64_t ld_d, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* GPT-2 block (pre-LN, R1) forward / backward on one GPU's batch tiles        */
 /* ------------------------------------------------------------------------- */
 typedef struct {

@@ -321,3 +321,189 @@ class BlockStack:
         self.graph.replay()
         self.step_count += 1
         return self.loss
+
+
+# ---------------------------------------------------------------------------------------------
+# Full GPT-2: embedding -> BlockStack -> final LayerNorm -> tied LM head ->
+# cross-entropy.  All arithmetic in libnnt kernels (nnt_embedding_*, nnt_layernorm_*,
+# nnt_tile_gemm for the two LM-head products, nnt_cross_entropy, nnt_dot, nnt_adam_step).
+# ---------------------------------------------------------------------------------------------
+SHELL = ("wte", "wpe", "lnf_g", "lnf_b")
+
+
+def shell_layout(V, S_max, E):
+    """Flat layout of the shell parameters (ALIGN-padded): name -> (offset, numel), total."""
+    shapes = {"wte": (V, E), "wpe": (S_max, E), "lnf_g": (E,), "lnf_b": (E,)}
+    off, d = 0, {}
+    for n in SHELL:
+        k = math.prod(shapes[n])
+        d[n] = (off, k)
+        off += -(-k // ALIGN) * ALIGN
+    return d, shapes, off
+
+
+class GPT2Model:
+    """GPT-2 with tied token embedding / LM head on one GPU's batch tiles (DP: a process group;
+    the shell gradients are one more all-reduce bucket, issued after the embedding backward)."""
+
+    def __init__(self, cfg: StackConfig, V, layer_params, shell_params, device="cuda", process_group=None,
+                 global_tokens=None):
+        self.cfg, self.V = cfg, V
+        self.stack = BlockStack(cfg, layer_params, device, process_group, global_tokens)
+        st = self.stack
+        self.dev = st.dev
+        E, T = cfg.E, cfg.T
+        self.bf16 = cfg.dtype == "bf16"
+        self.dt = nnt.NNT_BF16 if self.bf16 else nnt.NNT_F32
+        tdt = torch.bfloat16 if self.bf16 else torch.float32
+        self.S_max = shell_params["wpe"].shape[0]
+        self.offsets, self.shapes, n = shell_layout(V, self.S_max, E)
+        f32 = dict(device=self.dev, dtype=torch.float32)
+        self.w, self.g = torch.zeros(n, **f32), torch.zeros(n, **f32)
+        self.m, self.v = torch.zeros(n, **f32), torch.zeros(n, **f32)
+        for name, (o, k) in self.offsets.items():
+            self.w[o:o + k].copy_(torch.as_tensor(shell_params[name], dtype=torch.float32).reshape(-1).to(self.dev))
+        self.numel = n
+        self.w16 = torch.zeros(n, device=self.dev, dtype=torch.bfloat16) if self.bf16 else None
+        if self.bf16:
+            nnt.nnt_convert(self.w, nnt.NNT_F32, self.w16, nnt.NNT_BF16, n)
+        self.Vp = -(-V // 8) * 8  # logits row pitch: 16-byte rows for TMA / vector access
+        self.ids = torch.zeros(T, device=self.dev, dtype=torch.int32)
+        self.labels = torch.zeros(T, device=self.dev, dtype=torch.int32)
+        self.hf = torch.empty(T, E, device=self.dev, dtype=tdt)
+        self.mean, self.rstd = torch.empty(T, **f32), torch.empty(T, **f32)
+        self.logits = torch.empty(T, self.Vp, device=self.dev, dtype=tdt)
+        self.loss_rows = torch.empty(T, **f32)
+        self.ones = torch.ones(T, **f32)
+        self.dhf = torch.empty(T, E, **f32)
+        self.lnf_scr = torch.empty(nnt.nnt_layernorm_bwd_scratch_bytes(T, E), device=self.dev, dtype=torch.uint8)
+        self.emb_scr = torch.empty(nnt.nnt_embedding_bwd_scratch_bytes(T, V), device=self.dev, dtype=torch.uint8)
+        self.dot_scr = torch.empty(nnt.nnt_dot_scratch_bytes(T), device=self.dev, dtype=torch.uint8)
+        self.loss = torch.zeros(1, **f32)
+        self.step_count = 0
+        self.ev_shell = torch.cuda.Event()
+        if st.dp:
+            self.ev_shell.record()
+        self.graph = None
+
+    def view(self, buf, name):
+        o, k = self.offsets[name]
+        return buf[o:o + k]
+
+    def params(self):
+        return {n: self.view(self.w, n).reshape(self.shapes[n]) for n in SHELL}
+
+    def grads(self):
+        return {n: self.view(self.g, n).reshape(self.shapes[n]) for n in SHELL}
+
+    # ------------------------------------------------------------------ passes
+    def forward(self, ids=None, labels=None):
+        c, st = self.cfg, self.stack
+        T, E, V = c.T, c.E, self.V
+        if ids is not None:
+            self.ids.copy_(ids.reshape(-1), non_blocking=True)
+        if labels is not None:
+            self.labels.copy_(labels.reshape(-1), non_blocking=True)
+        nnt.nnt_embedding_fwd(self.ids, T, c.S, self.view(self.w, "wte"), V, self.view(self.w, "wpe"), E, st.xs[0])
+        st.forward()
+        nnt.nnt_layernorm_fwd(st.xs[-1], T, E, E, c.tile_e, self.view(self.w, "lnf_g"), self.view(self.w, "lnf_b"),
+                              c.ln_eps, self.hf, self.dt, E, self.mean, self.rstd)
+        wsrc = self.w16 if self.bf16 else self.w
+        # logits = h_f wte^T (tied LM head), C in the compute dtype with a 16-byte row pitch
+        nnt.nnt_tile_gemm(nnt.NNT_NOTRANS, nnt.NNT_TRANS, T, V, E, None, 1.0, self.hf, self.dt, E, None,
+                          self.view(wsrc, "wte"), self.dt, E, None, 0.0, self.logits, self.dt, self.Vp, None,
+                          (c.tile_t, c.tile_e, c.tile_e))
+        # cross-entropy: per-token loss and, in place, dlogits = (softmax - onehot) / T_global
+        inv = 1.0 / st.T_global
+        nnt.nnt_cross_entropy(self.logits, self.dt, T, V, self.Vp, self.labels, inv, self.loss_rows, None,
+                              self.logits, self.Vp)
+        nnt.nnt_dot(self.loss_rows, self.ones, T, inv, self.loss, self.dot_scr, self.dot_scr.numel())
+        return self.loss
+
+    def backward(self):
+        c, st = self.cfg, self.stack
+        T, E, V = c.T, c.E, self.V
+        wsrc = self.w16 if self.bf16 else self.w
+        tiles = (c.tile_t, c.tile_e, c.tile_e)
+        # dh_f = dlogits wte ; dwte = dlogits^T h_f (the LM-head half of the tied gradient)
+        nnt.nnt_tile_gemm(nnt.NNT_NOTRANS, nnt.NNT_NOTRANS, T, E, V, None, 1.0, self.logits, self.dt, self.Vp, None,
+                          self.view(wsrc, "wte"), self.dt, E, None, 0.0, self.dhf, nnt.NNT_F32, E, None, tiles)
+        nnt.nnt_tile_gemm(nnt.NNT_TRANS, nnt.NNT_NOTRANS, V, E, T, None, 1.0, self.logits, self.dt, self.Vp, None,
+                          self.hf, self.dt, E, None, 0.0, self.view(self.g, "wte"), nnt.NNT_F32, E, None, tiles)
+        nnt.nnt_layernorm_bwd(self.dhf, E, st.xs[-1], E, self.mean, self.rstd, self.view(self.w, "lnf_g"), T, E,
+                              None, st.dy[0], E, None, self.view(self.g, "lnf_g"), self.view(self.g, "lnf_b"), 0,
+                              self.lnf_scr, self.lnf_scr.numel())
+        dx0 = st.backward()
+        nnt.nnt_embedding_bwd(self.ids, T, c.S, dx0, E, self.view(self.g, "wte"), V, self.view(self.g, "wpe"), 1,
+                              self.emb_scr, self.emb_scr.numel())
+        if st.dp:  # the shell bucket: all-reduce + Adam on the comm stream
+            self.ev_shell.record()
+            with torch.cuda.stream(st.comm):
+                st.comm.wait_event(self.ev_shell)
+                torch.distributed.all_reduce(self.g, group=st.pg)
+                self._adam(st.step_count + 1, stream=st.comm)
+            torch.cuda.current_stream().wait_stream(st.comm)
+        return dx0
+
+    def _adam(self, t, stream=None):
+        hp = self.stack._graph_hp if self.stack._graph_hp is not None else self.stack._hparams(t)
+        nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp, stream=stream)
+
+    def adam(self):
+        self.stack.adam()
+        self.step_count = self.stack.step_count
+        self._adam(self.step_count)
+
+    def train_step(self, ids=None, labels=None):
+        """forward -> cross-entropy -> backward (+ DP all-reduce) -> Adam; returns the device loss."""
+        if self.graph is not None:
+            if ids is not None:
+                self.ids.copy_(ids.reshape(-1), non_blocking=True)
+            if labels is not None:
+                self.labels.copy_(labels.reshape(-1), non_blocking=True)
+            self.graph.replay()
+            self.stack.step_count += 1
+            self.step_count = self.stack.step_count
+            return self.loss
+        self.forward(ids, labels)
+        if self.stack.dp:
+            self.backward()
+            self.stack.step_count += 1
+            self.step_count = self.stack.step_count
+        else:
+            self.backward()
+            self.adam()
+        return self.loss
+
+    def capture_graph(self):
+        """One training step as a CUDA graph (see BlockStack.capture_graph)."""
+        st, c = self.stack, self.cfg
+        dev = self.dev
+        if not hasattr(st, "t_dev"):
+            st.t_dev = torch.tensor([st.step_count], device=dev, dtype=torch.int64)
+            st.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
+        hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
+        hp.bias_corr_dev = st.bc_dev.data_ptr()
+        if st.dp:
+            with torch.cuda.stream(st.comm):
+                torch.distributed.all_reduce(torch.zeros(1, device=dev), group=st.pg)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        st._graph_hp = hp
+        try:
+            with torch.cuda.graph(g):
+                nnt.nnt_adam_tick(c.beta1, c.beta2, st.t_dev, st.bc_dev)
+                self.forward()
+                if st.dp:
+                    self.backward()
+                else:
+                    self.backward()
+                    nnt.nnt_adam_step(st.numel, st.w, st.g, st.m, st.v, st.w16 if st.bf16 else None, hp)
+                    nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp)
+        finally:
+            st._graph_hp = None
+        return g
+
+    def enable_graph(self):
+        self.graph = self.capture_graph()
+        return self.graph

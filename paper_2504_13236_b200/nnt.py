@@ -47,7 +47,8 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd", "nnt_block_bwd_streams",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
-           "nnt_launch_count")
+           "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
+           "nnt_cross_entropy")
 
 
 class NNTError(RuntimeError):
@@ -126,6 +127,10 @@ _sig = {
     "nnt_scale": (_i32, [_vp, _f32, _vp, _i64, _vp]),
     "nnt_dot_scratch_bytes": (_sz, [_i64]),
     "nnt_dot": (_i32, [_vp, _vp, _i64, _f32, _vp, _vp, _sz, _vp]),
+    "nnt_embedding_fwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
+    "nnt_embedding_bwd_scratch_bytes": (_sz, [_i64, _i64]),
+    "nnt_embedding_bwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _vp, _sz, _vp]),
+    "nnt_cross_entropy": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _i64, _vp]),
     "nnt_block_workspace_size": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(_sz), C.POINTER(_sz)]),
     "nnt_block_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp]),
     "nnt_block_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp,
@@ -314,6 +319,24 @@ def nnt_dot_scratch_bytes(n):
 
 def nnt_dot(y, r, n, scale, out, scratch, scratch_bytes, stream=None):
     return check(lib.nnt_dot(ptr(y), ptr(r), n, scale, ptr(out), ptr(scratch), scratch_bytes, _stream(stream)))
+
+
+def nnt_embedding_fwd(ids, T, S, wte, V, wpe, E, x, stream=None):
+    return check(lib.nnt_embedding_fwd(ptr(ids), T, S, ptr(wte), V, ptr(wpe), E, ptr(x), _stream(stream)))
+
+
+def nnt_embedding_bwd_scratch_bytes(T, V):
+    return lib.nnt_embedding_bwd_scratch_bytes(T, V)
+
+
+def nnt_embedding_bwd(ids, T, S, dx, E, dwte, V, dwpe, accumulate, scratch, scratch_bytes, stream=None):
+    return check(lib.nnt_embedding_bwd(ptr(ids), T, S, ptr(dx), E, ptr(dwte), V, ptr(dwpe), accumulate, ptr(scratch),
+                                       scratch_bytes, _stream(stream)))
+
+
+def nnt_cross_entropy(logits, dtype, rows, V, ld, labels, scale, loss_rows, stats, dlogits, ld_d, stream=None):
+    return check(lib.nnt_cross_entropy(ptr(logits), dtype, rows, V, ld, ptr(labels), scale, ptr(loss_rows), ptr(stats),
+                                       ptr(dlogits), ld_d, _stream(stream)))
 
 
 def nnt_block_workspace_size(cfg):
