@@ -1,19 +1,21 @@
 #!/usr/bin/env python
-"""Benchmark: GPT-2 block-stack training step (fwd + bwd + Adam) on 1..8 B200.
+"""Benchmark: GPT-2 training step (fwd + bwd + Adam) on 1..8 B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config small] [--impl nnt|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config small] [--model gpt2|blocks]
+                    [--impl nnt|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: NCCL, one rank per GPU)
 
 Metric (BASELINE.json): GPT-2 train tokens/s (+ model TFLOP/s, % of bf16 peak).
-A step = one pass of the whole hot path over one synthetic batch per GPU: L
-pre-LN GPT-2 blocks forward, the linear-probe loss, L blocks backward, the DP
-gradient all-reduce (N > 1) and Adam on every parameter.  Weak scaling: each
-GPU holds B = 8 sequences of S = 1024 tokens.  The per-step working set
-(activations of 12 layers, several GB) is far larger than the 126 MB L2, so no
-explicit flush is needed between steps.
+A step = one pass of the whole hot path over one synthetic batch per GPU.  --model gpt2
+(default for small / large / xl): token + position embedding, L pre-LN GPT-2 blocks, final
+LayerNorm, tied LM head over the 50257-token vocabulary, mean cross-entropy, the backward of
+all of it, the DP gradient all-reduce (N > 1) and Adam on every parameter.  --model blocks
+(default for wide / tiny): the L blocks with a linear-probe loss.  Weak scaling: each GPU
+holds B = 8 sequences of S = 1024 tokens.  The per-step working set (activations of every
+layer, GBs) is far larger than the 126 MB L2, so no explicit flush is needed between steps.
 
---impl reference times the CPU oracle (oracle/, fp64 NumPy) on the box's host
-cores on a bounded sample of the same workload (one block, one sequence).
+--impl reference times the CPU oracle (oracle/, fp64 NumPy) on the box's host cores on a
+bounded sample of the same workload (one block over one sequence, plus the shell for gpt2).
 """
 from __future__ import annotations
 
@@ -40,11 +42,19 @@ CONFIGS = {  # name -> (L, E, H, S, B per GPU)
     "wide": (1, 8192, 128, 1024, 8),
 }
 METRIC = "GPT-2 train tokens/s & model TFLOP/s at 1/2/4/8 B200; % of bf16 peak"
+VOCAB = 50257  # GPT-2 BPE vocabulary (the full model: --model gpt2)
 
 
-def model_flops_per_step(L, E, S, T):
-    """6 N T + 12 L S E T with N = 12 E^2 per layer (blocks only; full attention counted)."""
-    return L * T * (72 * E * E + 12 * S * E)
+def default_model(config):
+    """Full GPT-2 (embeddings + blocks + final LN + tied LM head + cross-entropy) for the named GPT-2
+    sizes; the block stack for the single-layer 'wide' shape and the fp32 parity config."""
+    return "blocks" if config in ("wide", "tiny") else "gpt2"
+
+
+def model_flops_per_step(L, E, S, T, V=0):
+    """6 N T + 12 L S E T with N = 12 E^2 per layer (full attention counted), plus 6 E V T for the
+    (tied) LM head when the full model runs (PaLM / nanoGPT convention)."""
+    return L * T * (72 * E * E + 12 * S * E) + 6 * E * V * T
 
 
 def load_peaks():
@@ -149,6 +159,26 @@ def oracle_block_sample(E, H, S, seq=1, reps=None, budget_s=15.0):
     return float(np.median(times)), len(times)
 
 
+def oracle_shell_sample(E, V, S, reps=1):
+    """Time the oracle's GPT-2 shell alone (embedding, final LN, tied LM head, cross-entropy fwd+bwd and
+    Adam on the shell parameters) over one sequence of S tokens."""
+    import nnt_inputs
+    from oracle import dense
+    sh = nnt_inputs.make_shell_params(V, S, E, seed=1234, init="gpt2")
+    model = {k: v.astype(np.float64) for k, v in sh.items()}
+    model["blocks"] = []
+    tok = nnt_inputs.make_ids(V, S, 0, 1, seed=1001)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        _, cache = dense.gpt2_fwd(model, tok[:, :S], tok[:, 1:], 1)
+        g = dense.gpt2_bwd(model, cache)
+        for k in ("wte", "wpe", "lnf_g", "lnf_b"):
+            dense.adam_step(model[k], g[k], np.zeros_like(model[k]), np.zeros_like(model[k]), 1)
+        times.append(time.perf_counter() - t0)
+    return float(np.median(times))
+
+
 def host_cores():
     try:
         n = len(os.sched_getaffinity(0))
@@ -169,6 +199,45 @@ def oracle_sample_shape(E):
     return 1024 if E <= 1600 else 256
 
 
+# ---------------------------------------------------------------- model adapters
+class StackRunner:
+    """The block stack with the linear-probe loss: batches are (x, r)."""
+
+    def __init__(self, st):
+        self.st, self.stack = st, st
+
+    def step(self, batch):
+        return self.st.train_step(*batch)
+
+    def set_inputs(self, batch):
+        if not hasattr(self.st, "r_buf"):
+            self.st.r_buf = self.st.xs[0].new_empty(self.st.xs[0].shape)
+        self.st.xs[0].copy_(batch[0])
+        self.st.r_buf.copy_(batch[1])
+
+    @property
+    def model(self):
+        return self.st
+
+
+class GPT2Runner:
+    """The full GPT-2: batches are (ids, labels) int32 [B, S]."""
+
+    def __init__(self, gm):
+        self.gm, self.stack = gm, gm.stack
+
+    def step(self, batch):
+        return self.gm.train_step(*batch)
+
+    def set_inputs(self, batch):
+        self.gm.ids.copy_(batch[0].reshape(-1))
+        self.gm.labels.copy_(batch[1].reshape(-1))
+
+    @property
+    def model(self):
+        return self.gm
+
+
 # ---------------------------------------------------------------- arms
 def run_reference(args):
     """--impl reference: the oracle as it stands, on the host cores, bounded samples of the workload."""
@@ -176,6 +245,7 @@ def run_reference(args):
     if rank != 0:
         return 0
     L, E, H, S, B = CONFIGS[args.config]
+    mdl = args.model or default_model(args.config)
     Ss = min(S, oracle_sample_shape(E))
     for _ in range(args.warmup):
         oracle_block_sample(E, H, Ss, reps=1)
@@ -184,14 +254,17 @@ def run_reference(args):
         t, _ = oracle_block_sample(E, H, Ss, reps=1)
         times.append(t)
     t = float(np.mean(times))
-    # one sample = one block over Ss tokens; a full-model token needs L blocks
-    value = Ss / (t * L)
+    t_shell = oracle_shell_sample(E, VOCAB, Ss) if mdl == "gpt2" else 0.0
+    # one sample = one block over Ss tokens; a full-model token needs L blocks (+ the shell)
+    value = Ss / (t * L + t_shell)
     cores, threads = host_cores()
-    sample = f"one block fwd+bwd+Adam, 1 sequence x {Ss} tokens, E={E}, H={H}, fp64 NumPy; tokens/s scaled by 1/L (L={L})"
+    sample = (f"one block fwd+bwd+Adam, 1 sequence x {Ss} tokens, E={E}, H={H}, fp64 NumPy; tokens/s = "
+              f"tokens / (L x block time" + (" + shell time (embedding, final LN, tied LM head, CE, Adam)" if
+                                               mdl == "gpt2" else "") + f"), L={L}")
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * t, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"gpt2-{args.config} block stack fwd+bwd+Adam (oracle sample)", "layers": L,
+           "config": {"workload": f"gpt2-{args.config} {mdl} fwd+bwd+Adam (oracle sample)", "layers": L,
                       "d_model": E, "heads": H, "seq_len": S},
            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads or cores, "kind": "oracle",
                             "sample": sample},
@@ -217,19 +290,31 @@ def run_nnt(args):
         pg = dist.group.WORLD
     nnt.nnt_device_check(local)
     L, E, H, S, B = CONFIGS[args.config]
+    mdl = args.model or default_model(args.config)
     dtype = "f32" if args.config == "tiny" else "bf16"
     tile = 16 if args.config == "tiny" else 1024
     sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype)
     layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
-    st = model.BlockStack(sc, layers, process_group=pg, global_tokens=B * S * world)
-    del layers
-    # rank r's batch tiles of the global batch (nnt_partition), two distinct synthetic batches
-    b0, b1 = nnt.nnt_partition(B * world, world, rank)
+    b0, b1 = nnt.nnt_partition(B * world, world, rank)  # rank r's batch tiles of the global batch
     batches = []
-    for i in range(2):
-        x = nnt_inputs.make_x(E, S, b0, b1, seed=1000 + i)
-        r = nnt_inputs.make_r(E, S, b0, b1, seed=1000 + i)
-        batches.append((torch.from_numpy(x).pin_memory(), torch.from_numpy(r).pin_memory()))
+    if mdl == "gpt2":
+        shell = nnt_inputs.make_shell_params(VOCAB, S, E, seed=1234, init="gpt2")
+        gm = model.GPT2Model(sc, VOCAB, layers, shell, process_group=pg, global_tokens=B * S * world)
+        runner = GPT2Runner(gm)
+        for i in range(2):  # two distinct synthetic batches: ids ~ U[0, V), labels = next token
+            tok = nnt_inputs.make_ids(VOCAB, S, b0, b1, seed=1000 + i)
+            batches.append((torch.from_numpy(np.ascontiguousarray(tok[:, :S])).pin_memory(),
+                            torch.from_numpy(np.ascontiguousarray(tok[:, 1:])).pin_memory()))
+    else:
+        st = model.BlockStack(sc, layers, process_group=pg, global_tokens=B * S * world)
+        runner = StackRunner(st)
+        for i in range(2):
+            x = nnt_inputs.make_x(E, S, b0, b1, seed=1000 + i)
+            r = nnt_inputs.make_r(E, S, b0, b1, seed=1000 + i)
+            batches.append((torch.from_numpy(x).pin_memory(), torch.from_numpy(r).pin_memory()))
+    del layers
+    st = runner.stack
+    mm = runner.model
     dev_batches = [(x.cuda(), r.cuda()) for x, r in batches]
     T = B * S
     peaks = load_peaks()
@@ -251,15 +336,14 @@ def run_nnt(args):
         # bucket all-reduces + Adam are captured on the comm stream (model.BlockStack.enable_graph)
         n_cap = nnt.nnt_launch_count()
         try:
-            st.enable_graph()
+            mm.enable_graph()
         except Exception as exc:  # NCCL capture unsupported here: the DP step stays eager
             print(f"# graph capture failed ({exc!r}); eager launches", file=sys.stderr)
-            st.graph, use_graph = None, False
+            mm.graph, use_graph = None, False
             torch.cuda.synchronize()
         graph_launches = nnt.nnt_launch_count() - n_cap if use_graph else 0
     for i in range(args.warmup):
-        x, r = dev_batches[i % 2]
-        st.train_step(x, r)
+        runner.step(dev_batches[i % 2])
     torch.cuda.synchronize()
 
     # ---------------- timed region: device-resident inputs
@@ -272,15 +356,14 @@ def run_nnt(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(args.steps):
-        x, r = dev_batches[i % 2]
-        st.train_step(x, r)
+        runner.step(dev_batches[i % 2])
     e1.record()
     torch.cuda.synchronize()
     launches = nnt.nnt_launch_count() - n0 + graph_launches * args.steps
     barrier()
     clocks = sampler.stop()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    loss = float(st.loss.item())
+    loss = float(mm.loss.item())
 
     # ---------------- per-kernel timing: CUDA events around every libnnt launch scope.  With graphs,
     # a second graph of the same step is captured with timing on (the scopes become event-record
@@ -294,14 +377,12 @@ def run_nnt(args):
             nnt.nnt_timing_enable(True)
             side, st.side = st.side, None  # kernels timed one at a time (no side-stream overlap)
             try:
-                tg = st.capture_graph()
+                tg = mm.capture_graph()
             finally:
                 st.side = side
             acc = {}
             for i in range(args.steps):
-                x, r = dev_batches[i % 2]
-                st.xs[0].copy_(x)
-                st.r_buf.copy_(r)
+                runner.set_inputs(dev_batches[i % 2])
                 tg.replay()
                 st.step_count += 1
                 torch.cuda.synchronize()
@@ -320,16 +401,15 @@ def run_nnt(args):
         finally:
             nnt.nnt_timing_enable(False)
     if kt is None:
-        graph, st.graph = getattr(st, "graph", None), None
+        graph, mm.graph = getattr(mm, "graph", None), None
         nnt.nnt_timing_enable(True)
         for i in range(args.steps):
-            x, r = dev_batches[i % 2]
             torch.cuda._sleep(int(60e6))  # ~30 ms at 2 GHz, longer than one eager step's host enqueue
-            st.train_step(x, r)
+            runner.step(dev_batches[i % 2])
         torch.cuda.synchronize()
         kt = nnt.nnt_timing_read()
         nnt.nnt_timing_enable(False)
-        st.graph = graph
+        mm.graph = graph
         if graph is not None:
             st.t_dev.fill_(st.step_count)  # keep the device step counter in line with the eager steps
 
@@ -340,12 +420,11 @@ def run_nnt(args):
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
     for i in range(args.steps):
-        x, r = batches[i % 2]
-        lv = st.train_step(x, r).item()
+        lv = runner.step(batches[i % 2]).item()
     f1.record()
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(max(f0.elapsed_time(f1), 1000 * (time.perf_counter() - t0)) / args.steps)
-    h2d = batches[0][0].numel() * 4 * 2
+    h2d = sum(t.numel() * t.element_size() for t in batches[0])
     d2h = 4
 
     if rank != 0:
@@ -355,7 +434,7 @@ def run_nnt(args):
 
     tokens = T * world
     value = tokens / (ms / 1e3)
-    mflops = model_flops_per_step(L, E, S, T) * world
+    mflops = model_flops_per_step(L, E, S, T, VOCAB if mdl == "gpt2" else 0) * world
     model_tflops = mflops / (ms / 1e3) / 1e12
     # roofline of the dominant kernel class
     steps = args.steps
@@ -383,10 +462,16 @@ def run_nnt(args):
     roof["traffic"], roof["traffic_source"] = load_traffic(args.config, dom)
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-           "vs_baseline": None, "dtype": dtype, "data": "synthetic (seeded N(0,1) activations, GPT-2 init weights)",
-           "config": {"workload": f"gpt2-{args.config}: {L} pre-LN GPT-2 blocks fwd+bwd+Adam (block stack; "
-                                  f"embeddings/LM head are NEXT f1)",
-                      "model": f"gpt2-{args.config}-blocks", "layers": L, "d_model": E, "heads": H,
+           "vs_baseline": None, "dtype": dtype,
+           "data": ("synthetic (seeded token ids ~ U[0, 50257), next-token labels; GPT-2 init weights)"
+                    if mdl == "gpt2" else "synthetic (seeded N(0,1) activations, GPT-2 init weights)"),
+           "config": {"workload": (f"gpt2-{args.config}: token+position embedding, {L} pre-LN GPT-2 blocks, final "
+                                   f"LayerNorm, tied LM head (V={VOCAB}), mean cross-entropy; fwd+bwd+Adam"
+                                   if mdl == "gpt2" else
+                                   f"gpt2-{args.config}: {L} pre-LN GPT-2 blocks fwd+bwd+Adam (block stack, "
+                                   f"linear-probe loss)"),
+                      "model": f"gpt2-{args.config}" + ("" if mdl == "gpt2" else "-blocks"), "layers": L,
+                      "d_model": E, "heads": H, "vocab": VOCAB if mdl == "gpt2" else None,
                       "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}",
                       "launch": "one CUDA graph per step" if use_graph else "eager launches",
                       "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
@@ -397,12 +482,16 @@ def run_nnt(args):
                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms}}
     if world == 1 and not args.no_cpu_baseline:
         Ss = min(S, oracle_sample_shape(E))
-        t, n = oracle_block_sample(E, H, Ss)
+        t, n = oracle_block_sample(E, H, Ss, budget_s=10.0)
+        t_shell = oracle_shell_sample(E, VOCAB, Ss) if mdl == "gpt2" else 0.0
         cores, threads = host_cores()
-        out["cpu_baseline"] = {"value": Ss / (t * L), "unit": "tokens/s", "cores": threads or cores,
+        out["cpu_baseline"] = {"value": Ss / (t * L + t_shell), "unit": "tokens/s", "cores": threads or cores,
                                "kind": "oracle",
                                "sample": f"{n} x one block fwd+bwd+Adam over 1 sequence x {Ss} tokens (E={E}, H={H}, "
-                                         f"fp64 NumPy), median {t:.2f} s; tokens/s scaled by 1/L (L={L})"}
+                                         f"fp64 NumPy), median {t:.2f} s" +
+                                         (f", plus the shell (embedding, final LN, tied LM head, CE, Adam) once, "
+                                          f"{t_shell:.2f} s" if mdl == "gpt2" else "") +
+                                         f"; tokens/s = tokens / (L x block + shell), L={L}"}
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
@@ -416,6 +505,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="small", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="nnt", choices=["nnt", "reference"])
+    ap.add_argument("--model", default=None, choices=["gpt2", "blocks"],
+                    help="gpt2 = full model with embeddings / tied LM head / cross-entropy (default for small, "
+                         "large, xl); blocks = the block stack with a linear-probe loss (default for wide, tiny)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()

@@ -23,15 +23,24 @@ def main():
     ap.add_argument("--config", default="small")
     ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--model", default=None, choices=["gpt2", "blocks"])
     ap.add_argument("--trace", default=None, help="write the step's launch-scope trace (class, kernels) here")
     a = ap.parse_args()
     L, E, H, S, B = bench.CONFIGS[a.config]
     L = a.layers or L
+    mdl = a.model or bench.default_model(a.config)
     sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
-    st = model.BlockStack(sc, [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L)
-                               for l in range(L)])
-    x = torch.from_numpy(nnt_inputs.make_x(E, S, 0, B)).cuda()
-    r = torch.from_numpy(nnt_inputs.make_r(E, S, 0, B)).cuda()
+    layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+    if mdl == "gpt2":
+        V = bench.VOCAB
+        st = model.GPT2Model(sc, V, layers, nnt_inputs.make_shell_params(V, S, E, seed=1234, init="gpt2"))
+        tok = torch.from_numpy(nnt_inputs.make_ids(V, S, 0, B)).cuda()
+        batch = (tok[:, :S].contiguous(), tok[:, 1:].contiguous())
+    else:
+        st = model.BlockStack(sc, layers)
+        batch = (torch.from_numpy(nnt_inputs.make_x(E, S, 0, B)).cuda(),
+                 torch.from_numpy(nnt_inputs.make_r(E, S, 0, B)).cuda())
+    x, r = batch
     for _ in range(a.warmup):
         st.train_step(x, r)
     torch.cuda.synchronize()
