@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(kT) embed_fwd_kernel(const int32_t* __restrict
 }
 
 // ------------------------------------------------------------------ embedding backward
-// scratch layout (ints): hist[V + 1] | offs[V + 1] | rank[T] | order[T]
+// scratch layout (ints): hist[V + 1] | rank[T] | offs[V + 1] | order[T]
 __global__ void __launch_bounds__(kT) embed_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
                                                         int* __restrict__ hist) {
   NNT_PDL_ENTRY();
@@ -58,15 +58,21 @@ __global__ void __launch_bounds__(kT) zero_ints_kernel(int* __restrict__ p, int6
   for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kT) p[i] = 0;
 }
 
-// offs[v] = sum_{u < v} hist[u] for v <= V (one CTA: each thread scans a contiguous chunk)
+// offs[v] = sum_{u < v} hist[u] for v < n (one CTA): the counts are staged in shared memory with
+// coalesced loads, each thread scans a contiguous chunk there, the chunk sums are scanned
+// across the CTA, and the offsets leave through shared memory with coalesced stores.
+constexpr int kScanMax = 54 * 1024;  // ints staged in shared memory (216 KB, + 4 KB static)
 __global__ void __launch_bounds__(1024) embed_scan_kernel(const int* __restrict__ hist, int64_t n,
                                                           int* __restrict__ offs) {
   NNT_PDL_ENTRY();
+  extern __shared__ int buf[];  // [n]
   __shared__ int part[1024];
+  for (int64_t i = threadIdx.x; i < n; i += 1024) buf[i] = hist[i];
+  __syncthreads();
   const int64_t per = (n + 1023) / 1024;
   const int64_t b = threadIdx.x * per, e = b + per < n ? b + per : n;
   int s = 0;
-  for (int64_t i = b; i < e; ++i) s += hist[i];
+  for (int64_t i = b; i < e; ++i) s += buf[i];
   part[threadIdx.x] = s;
   __syncthreads();
   for (int d = 1; d < 1024; d <<= 1) {  // inclusive Hillis-Steele scan of the chunk sums
@@ -77,35 +83,51 @@ __global__ void __launch_bounds__(1024) embed_scan_kernel(const int* __restrict_
   }
   int run = threadIdx.x ? part[threadIdx.x - 1] : 0;
   for (int64_t i = b; i < e; ++i) {
-    offs[i] = run;
-    run += hist[i];
+    const int h = buf[i];
+    buf[i] = run;
+    run += h;
   }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < n; i += 1024) offs[i] = buf[i];
 }
 
-// rank[t] = #{t' < t : ids[t'] == ids[t]} (stable position inside the id's bucket); the
-// earlier ids are streamed through shared memory in tiles of kT
+// rank[t] = #{t' < t : ids[t'] == ids[t]} (stable position inside the id's bucket).  CTA (x, y)
+// compares its kT tokens with the earlier tokens of chunk y (kRankChunk ids staged in shared
+// memory) and adds its counts with integer atomics (order-independent, exact).
+constexpr int kRankChunk = 1024;
 __global__ void __launch_bounds__(kT) embed_rank_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
-                                                        const int* __restrict__ offs, int* __restrict__ order) {
+                                                        int* __restrict__ rank) {
   NNT_PDL_ENTRY();
-  __shared__ int tile[kT];
+  __shared__ int tile[kRankChunk];
   const int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x;
-  int64_t my = t < T ? ids[t] : -1;
-  if (t < T) my = my < 0 ? 0 : (my >= V ? V - 1 : my);
-  int r = 0;
-  const int64_t last = (int64_t)blockIdx.x * kT + kT;  // tokens this CTA can need to look at
-  for (int64_t base = 0; base < last && base < T; base += kT) {
-    __syncthreads();
-    const int64_t j = base + threadIdx.x;
+  const int64_t c0 = (int64_t)blockIdx.y * kRankChunk;
+  if (c0 >= (int64_t)blockIdx.x * kT + kT || c0 >= T) return;  // chunk entirely after this CTA's tokens
+  for (int i = threadIdx.x; i < kRankChunk; i += kT) {
+    const int64_t j = c0 + i;
     int64_t v = j < T ? ids[j] : -2;
     if (j < T) v = v < 0 ? 0 : (v >= V ? V - 1 : v);
-    tile[threadIdx.x] = (int)v;
-    __syncthreads();
-    if (t < T) {
-      const int lim = (int)(t - base < kT ? t - base : kT);
-      for (int k = 0; k < lim; ++k) r += tile[k] == (int)my;
-    }
+    tile[i] = (int)v;
   }
-  if (t < T) order[offs[my] + r] = (int)t;
+  __syncthreads();
+  if (t >= T) return;
+  int64_t my = ids[t];
+  my = my < 0 ? 0 : (my >= V ? V - 1 : my);
+  const int64_t lim64 = t - c0 < kRankChunk ? t - c0 : kRankChunk;
+  const int lim = lim64 > 0 ? (int)lim64 : 0;
+  int r = 0;
+  for (int k = 0; k < lim; ++k) r += tile[k] == (int)my;
+  if (r) atomicAdd(rank + t, r);
+}
+
+__global__ void __launch_bounds__(kT) embed_place_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
+                                                         const int* __restrict__ offs, const int* __restrict__ rank,
+                                                         int* __restrict__ order) {
+  NNT_PDL_ENTRY();
+  for (int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x; t < T; t += (int64_t)gridDim.x * kT) {
+    int64_t my = ids[t];
+    my = my < 0 ? 0 : (my >= V ? V - 1 : my);
+    order[offs[my] + rank[t]] = (int)t;
+  }
 }
 
 // dwte[v] (+)= sum over the bucket of v in token order; one warp per vocabulary row
@@ -300,15 +322,28 @@ nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const flo
   NNT_REQUIRE(scratch_bytes >= nnt_embedding_bwd_scratch_bytes(T, V), NNT_ERR_WORKSPACE,
               "nnt_embedding_bwd: scratch %zu < %zu", scratch_bytes, nnt_embedding_bwd_scratch_bytes(T, V));
   cudaStream_t s = (cudaStream_t)stream;
-  int* hist = (int*)scratch;
-  int* offs = hist + (V + 1);
+  int* hist = (int*)scratch;  // hist[V + 1] then rank[T] (zeroed together)
+  int* rank = hist + (V + 1);
+  int* offs = rank + T;
   int* order = offs + (V + 1);
-  LaunchScope sc(NNT_K_MISC, s, 8.0 * T * E + 8.0 * V * 4 + 4.0 * V * E, 0, 6);
-  NNT_CUDA_TRY(::nnt::launch(zero_ints_kernel, dim3(grid_cap(V + 1, kT)), dim3(kT), 0, s, hist, V + 1));
+  LaunchScope sc(NNT_K_MISC, s, 8.0 * T * E + 8.0 * V * 4 + 4.0 * V * E, 0, 7);
+  static const size_t scan_smem = [] {
+    cudaFuncSetAttribute(embed_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(kScanMax * sizeof(int)));
+    return (size_t)kScanMax * sizeof(int);
+  }();
+  NNT_REQUIRE(V + 1 <= kScanMax, NNT_ERR_UNSUPPORTED, "nnt_embedding_bwd: V=%lld > %d", (long long)V,
+              kScanMax - 1);
+  NNT_CUDA_TRY(::nnt::launch(zero_ints_kernel, dim3(grid_cap(V + 1 + T, kT)), dim3(kT), 0, s, hist, V + 1 + T));
   NNT_CUDA_TRY(::nnt::launch(embed_hist_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V, hist));
-  NNT_CUDA_TRY(::nnt::launch(embed_scan_kernel, dim3(1), dim3(1024), 0, s, (const int*)hist, V + 1, offs));
-  NNT_CUDA_TRY(::nnt::launch(embed_rank_kernel, dim3((unsigned)((T + kT - 1) / kT)), dim3(kT), 0, s, ids, T, V,
-                             (const int*)offs, order));
+  NNT_CUDA_TRY(::nnt::launch(embed_scan_kernel, dim3(1), dim3(1024), (size_t)(V + 1) * sizeof(int), s,
+                             (const int*)hist, V + 1, offs));
+  (void)scan_smem;
+  NNT_CUDA_TRY(::nnt::launch(embed_rank_kernel,
+                             dim3((unsigned)((T + kT - 1) / kT), (unsigned)((T + kRankChunk - 1) / kRankChunk)),
+                             dim3(kT), 0, s, ids, T, V, rank));
+  NNT_CUDA_TRY(::nnt::launch(embed_place_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V,
+                             (const int*)offs, (const int*)rank, order));
   NNT_CUDA_TRY(::nnt::launch(embed_bucket_kernel, dim3((unsigned)((V + kT / 32 - 1) / (kT / 32))), dim3(kT), 0, s,
                              (const int*)offs, (const int*)order, dx, (int)E, V, dwte, accumulate));
   NNT_CUDA_TRY(::nnt::launch(embed_pos_kernel, dim3(grid_cap(S * E / 4, kT)), dim3(kT), 0, s, dx, T / S, S, (int)E,
