@@ -1442,6 +1442,10 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Split-K factor for a GEMM: fp32 C, no activation, unbatched, non-causal, an output grid
 // that leaves SMs idle and a K long enough to cut (>= 8 K-blocks per split).
+namespace {
+int64_t long_k_splits(const GemmArgs& a);
+}
+
 int64_t gemm_tc_splits(const GemmArgs& a) {
   if (a.c_dtype != NNT_F32 || a.act != NNT_ACT_NONE || a.causal != NNT_CAUSAL_NONE || a.batch0 * a.batch1 != 1 ||
       a.N % 4 != 0)
@@ -1449,7 +1453,7 @@ int64_t gemm_tc_splits(const GemmArgs& a) {
   const int64_t tiles = cdiv(a.M, BM) * cdiv(a.N, 256);
   const int64_t nkb = cdiv(a.K, BK);
   const int64_t sms = num_sms();
-  if (tiles * 2 > sms) return 1;
+  if (tiles * 2 > sms) return long_k_splits(a);
   int64_t s = sms / tiles;
   if (s > nkb / 8) s = nkb / 8;
   if (s > 8) s = 8;
@@ -1719,6 +1723,29 @@ int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
     }
   }
   *cost_out = best_cost;
+  return best;
+}
+
+// Very long K with a grid of CTA-pair tiles that fills its last round badly (the LM head's
+// dh = dlogits wte: 96 tiles of K = 50257 on 74 pairs): splitting K evens the rounds.  Chosen by
+// the tile model plus the ordered reduce's traffic (~3300 B per SM cycle of HBM).
+int64_t long_k_splits(const GemmArgs& a) {
+  if (a.K < 16384 || !use_pair(a)) return 1;
+  const int64_t units = pair_units();
+  int64_t best = 1;
+  double best_cost = tile_cost(a, 256, 2, units, 4);
+  for (int64_t sp = 2; sp <= 4; ++sp) {
+    GemmArgs b = a;
+    b.K = cdiv(a.K, sp);
+    b.batch0 = sp;  // sp independent K ranges of the same tile grid
+    b.batch1 = 1;
+    const double reduce = (double)a.M * a.N * 4.0 * (sp + 1) / 3300.0;
+    const double cost = tile_cost(b, 256, 2, units, 4) + reduce;
+    if (cost < best_cost * 0.97) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
   return best;
 }
 

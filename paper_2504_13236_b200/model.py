@@ -376,6 +376,11 @@ class GPT2Model:
         self.loss_rows = torch.empty(T, **f32)
         self.ones = torch.ones(T, **f32)
         self.dhf = torch.empty(T, E, **f32)
+        # split-K workspace of dh_f = dlogits wte (K = V: the library splits K when the tile grid
+        # fills its last round badly); None when the library would not split
+        wsb = nnt.nnt_tile_gemm_workspace_bytes(T, E, V, nnt.NNT_F32) if self.bf16 else 0
+        self.dh_ws = torch.empty(wsb, device=self.dev, dtype=torch.uint8) if wsb else None
+        self.dh_epi = nnt.make_epilogue(workspace=self.dh_ws) if wsb else None
         self.lnf_scr = torch.empty(nnt.nnt_layernorm_bwd_scratch_bytes(T, E), device=self.dev, dtype=torch.uint8)
         self.emb_scr = torch.empty(nnt.nnt_embedding_bwd_scratch_bytes(T, V), device=self.dev, dtype=torch.uint8)
         self.dot_scr = torch.empty(nnt.nnt_dot_scratch_bytes(T), device=self.dev, dtype=torch.uint8)
@@ -427,7 +432,8 @@ class GPT2Model:
         tiles = (c.tile_t, c.tile_e, c.tile_e)
         # dh_f = dlogits wte ; dwte = dlogits^T h_f (the LM-head half of the tied gradient)
         nnt.nnt_tile_gemm(nnt.NNT_NOTRANS, nnt.NNT_NOTRANS, T, E, V, None, 1.0, self.logits, self.dt, self.Vp, None,
-                          self.view(wsrc, "wte"), self.dt, E, None, 0.0, self.dhf, nnt.NNT_F32, E, None, tiles)
+                          self.view(wsrc, "wte"), self.dt, E, None, 0.0, self.dhf, nnt.NNT_F32, E, None, tiles,
+                          self.dh_epi)
         nnt.nnt_tile_gemm(nnt.NNT_TRANS, nnt.NNT_NOTRANS, V, E, T, None, 1.0, self.logits, self.dt, self.Vp, None,
                           self.hf, self.dt, E, None, 0.0, self.view(self.g, "wte"), nnt.NNT_F32, E, None, tiles)
         nnt.nnt_layernorm_bwd(self.dhf, E, st.xs[-1], E, self.mean, self.rstd, self.view(self.w, "lnf_g"), T, E,
