@@ -71,3 +71,30 @@ def test_bench_config_sampled_sequences():
         dxr, _ = dense.stack_bwd(used, caches, dense.probe_loss_grad(rj, B * S))
         assert rel(host(y[j]), yr[0]) < 2e-2, j
         assert rel(host(dx[j]), dxr[0]) < 2e-2, j
+
+
+@pytest.mark.timeout(900)
+def test_bench_config_full_gpt2_sampled_sequences():
+    """The bench's default workload (full GPT-2 small: B=8, S=1024, 12 layers, V=50257, GPT-2 init,
+    one CUDA-graph step): the per-token cross-entropy of sequences 0 and 7 against the oracle run
+    on those sequences alone (the forward is independent across sequences)."""
+    import bench
+    L, E, H, S, B = bench.CONFIGS["small"]
+    V = bench.VOCAB
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
+    shell = nnt_inputs.make_shell_params(V, S, E, seed=1234, init="gpt2")
+    gm = model.GPT2Model(sc, V, layers, shell)
+    gm.enable_graph()
+    tok = nnt_inputs.make_ids(V, S, 0, B, seed=1000)
+    T = torch.as_tensor(tok).cuda()
+    gm.train_step(T[:, :S].contiguous(), T[:, 1:].contiguous())
+    torch.cuda.synchronize()
+    rows = host(gm.loss_rows).reshape(B, S)
+    om = dict(wte=bf16_round(shell["wte"]), wpe=shell["wpe"].astype(np.float64),
+              lnf_g=shell["lnf_g"].astype(np.float64), lnf_b=shell["lnf_b"].astype(np.float64),
+              blocks=[_used(p) for p in layers])
+    for j in (0, B - 1):
+        _, cache = dense.gpt2_fwd(om, tok[j:j + 1, :S], tok[j:j + 1, 1:], H)
+        want, _ = dense.cross_entropy(cache["logits"], tok[j, 1:])
+        assert rel(rows[j], want) < 2e-2, j
