@@ -289,27 +289,6 @@ __device__ __forceinline__ void mma_commit_pair_w(uint32_t bar) {
                : "memory");
 }
 
-// MC = 2 (two CTA pairs per cluster sharing B): a B piece is written to the same offset in this
-// CTA and its counterpart of the other pair (ctaMask); with .cta_group::2 the bytes complete on
-// each destination pair's leader barrier (the barrier address with the pair bit cleared).
-__device__ __forceinline__ void tma_load_4d_pair_mc_w(uint32_t dst, const CUtensorMap* map, uint32_t bar_local,
-                                                      uint16_t mask, int c0, int c1, int c2, int c3) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t" NNT_ELECT
-      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%4, %5, %6, %7}], [%2], %3;\n\t}" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_local & 0xFEFFFFFFu), "h"(mask), "r"(c0), "r"(c1), "r"(c2),
-      "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_pair_mask_w(uint32_t bar, uint16_t mask) {
-  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
-               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-                   bar),
-               "h"(mask)
-               : "memory");
-}
-
 // 32 consecutive fp32 columns of this warp's TMEM lane quadrant, no wait
 __device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
   asm volatile(
@@ -764,7 +743,7 @@ __device__ __forceinline__ void direct_store(int64_t M, int64_t N, int64_t ld, T
 // (rows m0 + 128 r ..); the leader (rank 0) waits for both halves on its full barrier
 // (expect_tx of both CTAs' bytes) and issues the M=256 MMAs; the peer's epilogue warps arrive
 // on the leader's TMEM-empty barrier.
-template <int BN, typename TC, int EPI, int CG = 1, int MC = 1>
+template <int BN, typename TC, int EPI, int CG = 1>
 __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
@@ -787,12 +766,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const GemmArgs& g = P.g;
-  static_assert(MC == 1 || (MC == 2 && CG == 2), "multicast clusters are pairs of CTA pairs");
-  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;  // MC = 2: pair = rank >> 1, CTA in pair = rank & 1
-  const uint32_t prank = rank & 1u;                       // rank within the CTA pair
-  const uint32_t pleader = rank & ~1u;                    // the pair's leader CTA
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
   const int row_off = (int)rank * BM;
-  const int64_t task0 = blockIdx.x / (CG * MC), task_step = gridDim.x / (CG * MC);
+  const int64_t task0 = blockIdx.x / CG, task_step = gridDim.x / CG;
 
   if constexpr (C::ROWSUM) {
     if (P.rowsum && warp == 2) {  // bf16 ones (0x3F80), visible to the tensor cores (async proxy)
@@ -804,7 +780,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), MC);  // MC = 2: both pairs' MMAs release a stage
+      mbar_init(smem_u32(&empty[s]), 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(smem_u32(&tfull[s]), 1);
@@ -845,9 +821,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       int stage = 0;
       uint32_t phase = 0;
       for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-        TileInfo ti = decode_task(P, it.t, BN, BM * CG * MC, row_off, it.sub);
+        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
         const int p = ti.p, q = ti.q;
-        const int nb0 = (int)ti.n0 + (int)prank * (BN / CG);  // this CTA's B rows
+        const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -855,8 +831,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           const int k0 = (int)(kb * BK);
           if constexpr (CG == 2) {
             const uint32_t fb_local = smem_u32(&full[stage]);
-            if (prank == 0) mbar_expect_tx_w(fb_local, CG * C::STAGE_BYTES);
-            const uint32_t fb = map_to_rank(fb_local, pleader);
+            if (rank == 0) mbar_expect_tx_w(fb_local, CG * C::STAGE_BYTES);
+            const uint32_t fb = map_to_rank(fb_local, 0);
             if (P.a_kmajor) {
               tma_load_4d_pair_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
             } else {
@@ -864,16 +840,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
               for (int j = 0; j < BM / 64; ++j)
                 tma_load_4d_pair_w(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
             }
-            if constexpr (MC == 2) {
-              // this CTA's B half is shared with its counterpart in the other pair (rank ^ 2): each
-              // of the two loads its 64-row piece and multicasts it to both
-              const int piece = (int)(rank >> 1);
-              const uint16_t mask = (uint16_t)((1u << rank) | (1u << (rank ^ 2u)));
-              if (P.b_kmajor)
-                tma_load_4d_pair_mc_w(sb + piece * 8192, &tmB, fb_local, mask, k0, nb0 + 64 * piece, q, p);
-              else
-                tma_load_4d_pair_mc_w(sb + piece * 8192, &tmB, fb_local, mask, nb0 + 64 * piece, k0, q, p);
-            } else if (P.b_kmajor) {
+            if (P.b_kmajor) {
               tma_load_4d_pair_w(sb, &tmB, fb, k0, nb0, q, p);
             } else {
 #pragma unroll
@@ -904,7 +871,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (CTA pair: the leader only)
-    if (prank == 0) {  // warp-wide loop, elected issue
+    if (rank == 0) {  // warp-wide loop, elected issue
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -915,7 +882,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
       for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-        TileInfo ti = decode_task(P, it.t, BN, BM * CG * MC, row_off, it.sub);
+        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -945,9 +912,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
               }
             }
           }
-          if constexpr (MC == 2)
-            mma_commit_pair_mask_w(smem_u32(&empty[stage]), (uint16_t)0xF);  // the stage is shared by both pairs
-          else if constexpr (CG == 2)
+          if constexpr (CG == 2)
             mma_commit_pair_w(smem_u32(&empty[stage]));
           else
             mma_commit_w(smem_u32(&empty[stage]));
@@ -956,9 +921,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             phase ^= 1;
           }
         }
-        if constexpr (MC == 2)
-          mma_commit_pair_mask_w(smem_u32(&tfull[acc]), (uint16_t)(3u << pleader));
-        else if constexpr (CG == 2)
+        if constexpr (CG == 2)
           mma_commit_pair_w(smem_u32(&tfull[acc]));
         else
           mma_commit_w(smem_u32(&tfull[acc]));
@@ -1240,7 +1203,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     uint32_t acc_phase = 0;
     uint32_t in_phase = 0;  // IN_AUX_SMEM: bit i = phase of this warp's input barrier i
     for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-      TileInfo ti = decode_task(P, it.t, BN, BM * CG * MC, row_off);
+      TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off);
       const int64_t p = ti.p, q = ti.q;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
@@ -1367,7 +1330,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 2)
-          mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[acc]), pleader));  // the leader's MMA waits on it
+          mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[acc]), 0));  // the leader's MMA waits on it
         else
           mbar_arrive(smem_u32(&tempty[acc]));
       }
@@ -1538,45 +1501,14 @@ int64_t pair_units() {
   return units;
 }
 
-// Co-resident 4-CTA clusters (two CTA pairs sharing B through multicast).
-int64_t quad_units() {
-  static int64_t units = 0;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    using Cq = Cfg<256, 2>;
-    auto kern = gemm_tc_kernel<256, float, EPI_GENERIC, 2, 2>;
-    int n = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cq::SMEM_BYTES) == cudaSuccess) {
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3((unsigned)(num_sms() / 4 * 4));
-      q.blockDim = dim3(kThreads);
-      q.dynamicSmemBytes = Cq::SMEM_BYTES;
-      cudaLaunchAttribute attr[1];
-      attr[0].id = cudaLaunchAttributeClusterDimension;
-      attr[0].val.clusterDim.x = 4;
-      attr[0].val.clusterDim.y = 1;
-      attr[0].val.clusterDim.z = 1;
-      q.attrs = attr;
-      q.numAttrs = 1;
-      if (cudaOccupancyMaxActiveClusters(&n, kern, &q) != cudaSuccess) n = 0;
-    }
-    (void)cudaGetLastError();
-    units = n > 0 ? n : num_sms() / 4;
-    if (getenv("NNT_DEBUG_GEMM")) fprintf(stderr, "gemm_tc: %lld co-resident 4-CTA clusters (query %d)\n", (long long)units, n);
-  });
-  return units;
-}
-
-template <int BN, typename TC, int EPI, int CG = 1, int MC = 1>
+template <int BN, typename TC, int EPI, int CG = 1>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   using C = Cfg<BN, CG, EPI>;
   static std::once_flag once;
   static cudaError_t attr_err = cudaSuccess;
   std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI, CG, MC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     C::SMEM_BYTES);
-    if (attr_err == cudaSuccess && CG * MC > 2)  // 4-CTA clusters are portable (<= 8): nothing more to enable
-      attr_err = cudaSuccess;
   });
   NNT_REQUIRE(attr_err == cudaSuccess, NNT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   NNT_TRY(get_encoder());
@@ -1584,7 +1516,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.g = a;
   P.a_kmajor = a.ta == NNT_NOTRANS;
   P.b_kmajor = a.tb == NNT_TRANS;
-  P.mt = cdiv(a.M, BM * CG * MC);
+  P.mt = cdiv(a.M, BM * CG);
   P.nt = cdiv(a.N, BN);
   if (EPI == EPI_ROWSTATS) {
     P.order = ORDER_ROWS;  // task = (batch item, row block) with all its key tiles
@@ -1639,7 +1571,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   else
     NNT_TRY(make_map(&tmA, bf, 2, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, 64, BK));
   if (P.b_kmajor)
-    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN / CG / MC));
+    NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN / CG));
   else
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
   const size_t es = sizeof(TC);
@@ -1678,18 +1610,18 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG * MC;
+    attr[0].val.clusterDim.x = CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
-    const int64_t max_clusters = MC == 2 ? quad_units() : pair_units();
+    const int64_t max_clusters = pair_units();
     int64_t grid = P.num_tasks < max_clusters ? P.num_tasks : max_clusters;
     if (grid < 1) grid = 1;
-    cfg.gridDim = dim3((unsigned)(grid * CG * MC));
-    NNT_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, TC, EPI, CG, MC>, P, tmA, tmB, tmC, tmAux));
+    cfg.gridDim = dim3((unsigned)(grid * CG));
+    NNT_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, TC, EPI, CG>, P, tmA, tmB, tmC, tmAux));
   }
   NNT_TRY(check_launch("gemm_tc"));
   if (P.ws_mode) {
@@ -1778,15 +1710,6 @@ bool use_pair(const GemmArgs& a) {
          num_sms() >= 2;
 }
 
-// Two CTA pairs per cluster sharing B by TMA multicast (NNT_GEMM_MC=1 enables; measured A/B).
-bool use_multicast(const GemmArgs& a) {
-  static const int mc = [] {
-    const char* e = getenv("NNT_GEMM_MC");
-    return e ? atoi(e) : 0;
-  }();
-  return mc == 1 && a.M >= 4 * BM;
-}
-
 // Pair widths whose half is a whole 64-column MN-major block.
 int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
   const int cands[2] = {256, 128};
@@ -1853,12 +1776,9 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     if (getenv("NNT_DEBUG_GEMM"))
       fprintf(stderr, "gemm_tc %lldx%lldx%lld: pair BN %d cost %.0f, single BN %d cost %.0f\n", (long long)a.M,
               (long long)a.N, (long long)a.K, bnp, cost_pair, bns, cost_single);
-    if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single) {  // ties go to pairs
-      if ((bnp == 256 || splits > 1) && use_multicast(a))
-        return launch_bn<256, TC, EPI_GENERIC, 2, 2>(a, s, splits);
+    if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single)  // ties go to pairs
       return bnp == 256 || splits > 1 ? launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits)
                                       : launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
-    }
   }
   switch (splits > 1 ? 256 : choose_bn(a, sizeof(TC))) {
     case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
