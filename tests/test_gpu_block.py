@@ -204,3 +204,34 @@ def test_side_stream_backward_bitwise(graph):
     assert outs[0][0] == outs[1][0]
     for a, b in zip(outs[0][1:], outs[1][1:]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_gradient_accumulation_over_two_batches(dtype):
+    """accumulate_grads = 1 adds into the gradients (split-K dW reduce with beta = 1, bias-gradient
+    and LayerNorm-parameter accumulation): two micro-batches give the oracle's summed gradients."""
+    if dtype == "f32":
+        c = nnt_inputs.CONFIGS["tiny"]
+        E, H, S, B, tile, tol = c.E, c.H, c.S, c.B, c.tile, 1e-4
+    else:
+        E, H, S, B, tile, tol = 768, 12, 256, 1, 1024, 2e-2
+    sc = model.StackConfig(L=1, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile,
+                           dtype=dtype)
+    layers = [nnt_inputs.make_params(E, seed=31, init="parity")]
+    st = model.BlockStack(sc, layers)
+    used = {k: (bf16_round(v) if (dtype == "bf16" and k.startswith("w_")) else v.astype(np.float64))
+            for k, v in layers[0].items()}
+    want = None
+    for i, seed in enumerate((41, 42)):
+        x = nnt_inputs.make_x(E, S, 0, B, seed=seed)
+        r = nnt_inputs.make_r(E, S, 0, B, seed=seed)
+        st.forward(dev(x))
+        st.probe_loss(dev(r))
+        nnt.nnt_block_bwd(st.bcfg, st._params[0], st.xs[0], st.saved[0], st.scratch, st.dy[0], st.dy[1],
+                          st._grads[0], i)
+        y, cache = dense.block_fwd(used, x, H)
+        _, g = dense.block_bwd(used, cache, dense.probe_loss_grad(r, B * S))
+        want = g if want is None else {k: want[k] + g[k] for k in g}
+    torch.cuda.synchronize()
+    for n, gv in st.grads_of(0).items():
+        assert rel(host(gv), want[n]) < tol, n

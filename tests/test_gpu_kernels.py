@@ -250,6 +250,23 @@ def test_adam_matches_oracle_and_step1_closed_form():
         assert np.array_equal(host(W16), bf16_round(host(W)))
 
 
+def test_adamw_decoupled_decay_matches_oracle():
+    """AdamW (weight_decay > 0, decoupled: w -= lr * wd * w_old, reading R12) vs the oracle, which
+    is itself pinned to torch.optim.AdamW."""
+    n = 4099
+    rng = np.random.default_rng(5)
+    w = rng.standard_normal(n).astype(np.float32)
+    W, M, V = dev(w), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    wr, mr, vr = w.astype(np.float64), np.zeros(n), np.zeros(n)
+    for t in range(1, 4):
+        g = rng.standard_normal(n).astype(np.float32)
+        hp = nnt.nnt_adam_hparams(1e-2, 0.9, 0.999, 1e-8, 0.1, 1 - 0.9 ** t, 1 - 0.999 ** t, 1.0)
+        nnt.nnt_adam_step(n, W, dev(g), M, V, None, hp)
+        wr, mr, vr = dense.adam_step(wr, g, mr, vr, t, lr=1e-2, weight_decay=0.1)
+        torch.cuda.synchronize()
+        assert rel(host(W) - w, wr - w) < 1e-4
+
+
 def test_dot_and_scale():
     n = 123457
     rng = np.random.default_rng(2)
