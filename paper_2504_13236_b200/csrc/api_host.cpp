@@ -54,6 +54,7 @@ bool g_timing = false;
 std::vector<TimingRecord> g_records;
 std::vector<cudaEvent_t> g_event_pool;
 std::atomic<int64_t> g_launches{0};
+std::atomic<uint32_t> g_class_mask{0xFFFFFFFFu};
 
 // Inside a stream capture a plain cudaEventRecord only expresses a dependency; an
 // external record makes it an event-record node that timestamps every graph replay.
@@ -78,7 +79,8 @@ cudaEvent_t take_event() {
 }  // namespace
 
 LaunchScope::LaunchScope(int kclass, cudaStream_t s, double bytes, double flops, int kernels)
-    : kclass_(kclass), s_(s), slot_(-1) {
+    : kclass_(kclass), s_(s), slot_(-1), skip_(((g_class_mask.load(std::memory_order_relaxed) >> kclass) & 1u) == 0) {
+  if (skip_) return;
   g_launches.fetch_add(kernels, std::memory_order_relaxed);
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);
@@ -206,5 +208,7 @@ nnt_status nnt_timing_trace(int32_t* kclass, int32_t* kernels, int64_t cap, int6
 }
 
 int64_t nnt_launch_count(void) { return g_launches.load(); }
+
+uint32_t nnt_timing_class_mask(uint32_t mask) { return g_class_mask.exchange(mask); }
 
 }  // extern "C"
