@@ -395,38 +395,6 @@ def run_nnt(args):
             print(f"# graph-timed kernel sum {sum(v['ms'] for v in acc.values()) / args.steps:.3f} ms/step "
                   f"(timed region {ms:.3f} ms/step)", file=sys.stderr)
             del tg
-            if world == 1:
-                # Per-class device time without timing nodes: for each class, a graph of one step
-                # with every other class masked out (nnt_timing_class_mask) holds exactly that
-                # class's kernels back to back; its replay time / step is the class's time.
-                nnt.nnt_timing_enable(False)
-                side, st.side = st.side, None
-                names = list(nnt.KERNEL_CLASSES)
-                try:
-                    for k, name in enumerate(names):
-                        if kt.get(name, {}).get("launches", 0) == 0:
-                            continue
-                        old = nnt.nnt_timing_class_mask(1 << k)
-                        try:
-                            cg = mm.capture_graph()
-                        finally:
-                            nnt.nnt_timing_class_mask(old)
-                        cg.replay()
-                        torch.cuda.synchronize()
-                        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                        c0.record()
-                        for _ in range(args.steps):
-                            cg.replay()
-                        c1.record()
-                        torch.cuda.synchronize()
-                        kt[name]["ms"] = c0.elapsed_time(c1)  # over args.steps replays, like the event pass
-                        del cg
-                    timing_mode = "class-graphs"
-                    print(f"# class-graph kernel sum {sum(v['ms'] for v in kt.values()) / args.steps:.3f} ms/step",
-                          file=sys.stderr)
-                finally:
-                    st.side = side
-                    nnt.nnt_timing_class_mask(0xFFFFFFFF)
         except Exception as exc:  # event nodes unsupported: fall back to the eager pass
             print(f"# graph timing failed ({exc!r}); eager timing pass", file=sys.stderr)
             kt = None
@@ -487,13 +455,9 @@ def run_nnt(args):
             "peak": peaks["bf16_sus"] if d["bound"] == "tensor" else peaks["hbm"], "unit": d["unit"],
             "frac": d["frac"], "traffic": None, "traffic_source": None, "peak_source": peaks["src"] +
             (" bf16_tflops_sustained (kernel timed inside a long step)" if d["bound"] == "tensor" else " hbm_gbs"),
-            "timing": {"class-graphs": "CUDA events around K replays of a graph of one step holding only this "
-                                       "class's kernels (the other classes masked out with nnt_timing_class_mask), "
-                                       "captured from the real step after the timed region",
-                       "graph": "CUDA events around every launch scope (event nodes in a replayed copy of the step "
-                                "graph), K steps after the timed region",
-                       "eager": "CUDA events around every launch scope, eager launches behind a spin kernel, K steps "
-                                "after the timed region"}[timing_mode],
+            "timing": f"CUDA events around every launch scope on its stream ({timing_mode}: "
+                      + ("event nodes in a replayed copy of the step graph" if timing_mode == "graph" else
+                         "eager launches behind a spin kernel") + "), K steps after the timed region",
             "share_of_step": d["share"]}
     roof["traffic"], roof["traffic_source"] = load_traffic(args.config, dom)
     out = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,

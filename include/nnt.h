@@ -499,11 +499,6 @@ nnt_status nnt_timing_read(double* ms, int64_t* launches, double* bytes, double*
 nnt_status nnt_timing_trace(int32_t* kclass, int32_t* kernels, int64_t cap, int64_t* n);
 /* Number of kernels this library launched since load (all classes). */
 int64_t nnt_launch_count(void);
-/* Bit k set = kernel class k is launched (default: all).  Calls whose kernels belong to a
- * masked-out class validate their arguments and return NNT_OK without launching, so a graph of
- * one class's kernels can be captured from a real step and timed (bench.py).  Returns the
- * previous mask.  Measurement only: results are garbage while a mask is set. */
-uint32_t nnt_timing_class_mask(uint32_t mask);
 
 #ifdef __cplusplus
 }

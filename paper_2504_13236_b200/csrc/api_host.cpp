@@ -54,7 +54,6 @@ bool g_timing = false;
 std::vector<TimingRecord> g_records;
 std::vector<cudaEvent_t> g_event_pool;
 std::atomic<int64_t> g_launches{0};
-std::atomic<uint32_t> g_class_mask{0xFFFFFFFFu};
 
 // Inside a stream capture a plain cudaEventRecord only expresses a dependency; an
 // external record makes it an event-record node that timestamps every graph replay.
@@ -79,8 +78,7 @@ cudaEvent_t take_event() {
 }  // namespace
 
 LaunchScope::LaunchScope(int kclass, cudaStream_t s, double bytes, double flops, int kernels)
-    : kclass_(kclass), s_(s), slot_(-1), skip_(((g_class_mask.load(std::memory_order_relaxed) >> kclass) & 1u) == 0) {
-  if (skip_) return;
+    : kclass_(kclass), s_(s), slot_(-1) {
   g_launches.fetch_add(kernels, std::memory_order_relaxed);
   if (!g_timing) return;
   std::lock_guard<std::mutex> lk(g_tmu);
@@ -208,7 +206,5 @@ nnt_status nnt_timing_trace(int32_t* kclass, int32_t* kernels, int64_t cap, int6
 }
 
 int64_t nnt_launch_count(void) { return g_launches.load(); }
-
-uint32_t nnt_timing_class_mask(uint32_t mask) { return g_class_mask.exchange(mask); }
 
 }  // extern "C"

@@ -260,7 +260,6 @@ nnt_status nnt_gelu_fwd(const void* x, void* y, int dtype, int64_t n, nnt_stream
   bool vec = aligned16(x) && aligned16(y);
   size_t es = dtype_size(dtype);
   LaunchScope sc(NNT_K_GELU, stream, 2.0 * es * n, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   if (dtype == NNT_F32)
     ::nnt::launch(gelu_kernel<float, false>, grid_for(n / 4 + 1), kThreads, 0, stream, (const float*)x, nullptr, (float*)y, n, vec);
   else
@@ -277,7 +276,6 @@ nnt_status nnt_gelu_bwd(const void* x, const void* dy, void* dx, int dtype, int6
   bool vec = aligned16(x) && aligned16(dy) && aligned16(dx);
   size_t es = dtype_size(dtype);
   LaunchScope sc(NNT_K_GELU, stream, 3.0 * es * n, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   if (dtype == NNT_F32)
     ::nnt::launch(gelu_kernel<float, true>, grid_for(n / 4 + 1), kThreads, 0, stream, (const float*)x, (const float*)dy,
                                                                           (float*)dx, n, vec);
@@ -297,7 +295,6 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
   bool vec = aligned16(w) && aligned16(g) && aligned16(m) && aligned16(v) &&
              (w_bf16 == nullptr || (reinterpret_cast<uintptr_t>(w_bf16) & 7u) == 0);
   LaunchScope sc(NNT_K_ADAM, stream, (28.0 + (w_bf16 ? 2.0 : 0.0)) * n, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   ::nnt::launch(adam_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, n, w, g, m, v, (__nv_bfloat16*)w_bf16, *hp, vec);
   return check_launch("adam");
 }
@@ -306,7 +303,6 @@ nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias
   NNT_REQUIRE(t_dev && bias_corr_dev, NNT_ERR_NULL, "nnt_adam_tick: NULL pointer");
   NNT_REQUIRE(beta1 >= 0.0 && beta1 < 1.0 && beta2 >= 0.0 && beta2 < 1.0, NNT_ERR_ARG, "nnt_adam_tick: beta");
   LaunchScope sc(NNT_K_ADAM, stream, 16.0, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   ::nnt::launch(adam_tick_kernel, 1, 32, 0, stream, beta1, beta2, t_dev, bias_corr_dev);
   return check_launch("adam_tick");
 }
@@ -317,7 +313,6 @@ nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t
   NNT_REQUIRE(n >= 0, NNT_ERR_SHAPE, "nnt_convert: n=%lld", (long long)n);
   if (n == 0) return NNT_OK;
   LaunchScope sc(NNT_K_MISC, stream, (double)(dtype_size(x_dtype) + dtype_size(y_dtype)) * n, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   int grid = grid_for(n);
   if (x_dtype == NNT_F32 && y_dtype == NNT_BF16)
     ::nnt::launch(convert_kernel<float, __nv_bfloat16>, grid, kThreads, 0, stream, (const float*)x, (__nv_bfloat16*)y, n);
@@ -336,7 +331,6 @@ nnt_status nnt_scale(const float* x, float alpha, float* y, int64_t n, nnt_strea
   NNT_REQUIRE(n >= 0, NNT_ERR_SHAPE, "nnt_scale: n=%lld", (long long)n);
   if (n == 0) return NNT_OK;
   LaunchScope sc(NNT_K_MISC, stream, 8.0 * n, (double)n);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   ::nnt::launch(scale_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, x, alpha, y, n, aligned16(x) && aligned16(y));
   return check_launch("scale");
 }
@@ -361,7 +355,6 @@ nnt_status nnt_bias_grad(const void* dy, int dy_dtype, int64_t T, int64_t N, int
   ColsumPlan p = colsum_plan(T, N);
   double bytes = (double)T * N * dtype_size(dy_dtype) + (dy_bf16_out ? 2.0 * T * N : 0.0) + 4.0 * N;
   LaunchScope sc(NNT_K_BIAS_GRAD, stream, bytes, 0, 2);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   dim3 grid((unsigned)((N + 127) / 128), (unsigned)p.chunks);
   const size_t es = dtype_size(dy_dtype);
   const bool vec = N % 4 == 0 && lddy % 4 == 0 && (reinterpret_cast<uintptr_t>(dy) % (4 * es)) == 0 &&
@@ -395,7 +388,6 @@ nnt_status nnt_dot(const float* y, const float* r, int64_t n, float scale, float
   NNT_REQUIRE(n > 0, NNT_ERR_SHAPE, "nnt_dot: n=%lld", (long long)n);
   NNT_REQUIRE(scratch_bytes >= nnt_dot_scratch_bytes(n), NNT_ERR_WORKSPACE, "nnt_dot: scratch too small");
   LaunchScope sc(NNT_K_MISC, stream, 8.0 * n, 2.0 * n, 2);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   ::nnt::launch(dot_partial_kernel, kDotBlocks, kThreads, 0, stream, y, r, n, (double*)scratch);
   NNT_TRY(check_launch("dot partial"));
   ::nnt::launch(dot_merge_kernel, 1, 32, 0, stream, (const double*)scratch, kDotBlocks, scale, out);

@@ -128,11 +128,9 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
                        (g.a_rowsum ? 4.0 * M * (beta != 0.f ? 2.0 : 1.0) : 0.0);
   if (a_dtype == NNT_F32) {
     LaunchScope sc(NNT_K_GEMM_SIMT, stream, bytes, flops);
-    if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
     return gemm_simt_launch(g, stream);
   }
   LaunchScope sc(b0 * b1 > 1 ? NNT_K_GEMM_TC_ATTN : NNT_K_GEMM_TC, stream, bytes, flops);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   int kernels = 1;
   const nnt_status st = gemm_tc_launch(g, stream, &kernels);
   if (kernels > 1) sc.add_kernels(kernels - 1);

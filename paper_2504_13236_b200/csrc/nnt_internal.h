@@ -65,13 +65,9 @@ struct LaunchScope {
   LaunchScope(int kclass, cudaStream_t s, double bytes, double flops, int kernels = 1);
   ~LaunchScope();
   void add_kernels(int k);  // the scope launched k more kernels than declared (decided inside)
-  // nnt_timing_class_mask(): launches of masked-out classes are skipped (the API call returns
-  // NNT_OK without launching) so a graph of one class's kernels can be captured and timed
-  bool skip() const { return skip_; }
   int kclass_;
   cudaStream_t s_;
   int slot_;
-  bool skip_;
 };
 
 int num_sms();

@@ -301,7 +301,6 @@ nnt_status nnt_embedding_fwd(const int32_t* ids, int64_t T, int64_t S, const flo
   NNT_REQUIRE(E % 4 == 0 && aligned16(wte) && aligned16(wpe) && aligned16(x), NNT_ERR_ALIGN,
               "nnt_embedding_fwd: E %% 4 and 16-byte alignment required");
   LaunchScope sc(NNT_K_MISC, stream, 12.0 * T * E + 4.0 * T, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   NNT_CUDA_TRY(::nnt::launch(embed_fwd_kernel, dim3(grid_cap(T, kT / 32)), dim3(kT), 0, (cudaStream_t)stream, ids, T,
                              S, wte, V, wpe, (int)E, x));
   return NNT_OK;
@@ -328,7 +327,6 @@ nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const flo
   int* offs = rank + T;
   int* order = offs + (V + 1);
   LaunchScope sc(NNT_K_MISC, s, 8.0 * T * E + 8.0 * V * 4 + 4.0 * V * E, 0, 7);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   static const size_t scan_smem = [] {
     cudaFuncSetAttribute(embed_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)(kScanMax * sizeof(int)));
@@ -364,7 +362,6 @@ nnt_status nnt_cross_entropy(const void* logits, int dtype, int64_t rows, int64_
   NNT_REQUIRE(aligned16(logits) && (ld * es) % 16 == 0 && (!dlogits || (aligned16(dlogits) && (ld_d * es) % 16 == 0)),
               NNT_ERR_ALIGN, "nnt_cross_entropy: 16-byte aligned rows required");
   LaunchScope sc(NNT_K_SOFTMAX, stream, (double)rows * V * es * (dlogits ? 3.0 : 1.0) + 16.0 * rows, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   cudaStream_t s = (cudaStream_t)stream;
   if (dtype == NNT_BF16)
     NNT_CUDA_TRY(::nnt::launch(cross_entropy_kernel<__nv_bfloat16>, dim3((unsigned)rows), dim3(kT), 0, s,

@@ -303,7 +303,6 @@ nnt_status nnt_maxsumexp(const float* x, int64_t rows, int64_t cols, int64_t ldx
   NNT_REQUIRE(aligned16(x), NNT_ERR_ALIGN, "nnt_maxsumexp: x not 16B aligned");
   double frac = causal ? 0.5 * (1.0 + 1.0 / (double)cols) : 1.0;
   LaunchScope sc(NNT_K_MAXSUMEXP, stream, 4.0 * rows * cols * frac + 8.0 * rows, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   int nc = chunks_for(cols);
 #define NNT_MSE(N)                                                                                         \
   case N:                                                                                                  \
@@ -323,7 +322,6 @@ nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, 
   NNT_REQUIRE(aligned16(dO) && aligned16(O), NNT_ERR_ALIGN, "nnt_attn_rowdot: pointers must be 16-byte aligned");
   const int64_t n = B * S * H;
   LaunchScope sc(NNT_K_MISC, stream, 2.0 * dtype_size(dtype) * n * h + 4.0 * n, 2.0 * n * h);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   const unsigned grid = (unsigned)((n + kThreads - 1) / kThreads);
   if (dtype == NNT_BF16)
     ::nnt::launch(attn_rowdot_kernel<__nv_bfloat16>, grid, kThreads, 0, stream, (const __nv_bfloat16*)dO,
@@ -344,7 +342,6 @@ nnt_status nnt_maxsumexp_merge(const float* part, int64_t rows, int64_t nparts, 
   NNT_REQUIRE((reinterpret_cast<uintptr_t>(part) & 7u) == 0 && (reinterpret_cast<uintptr_t>(stats) & 7u) == 0,
               NNT_ERR_ALIGN, "nnt_maxsumexp_merge: pointers must be 8-byte aligned");
   LaunchScope sc(NNT_K_MAXSUMEXP, stream, 8.0 * rows * (causal ? 0.5 : 1.0) * nparts + 8.0 * rows, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   ::nnt::launch(maxsumexp_merge_kernel, (unsigned)((rows + kThreads - 1) / kThreads), kThreads, 0, stream, 
       (const float2*)part, rows, nparts, ld_parts, part_cols, causal, seq_q, (float2*)stats);
   return check_launch("maxsumexp_merge");
@@ -360,7 +357,6 @@ nnt_status nnt_softmax(const float* x, int64_t rows, int64_t cols, int64_t ldx, 
   NNT_REQUIRE(aligned16(x) && aligned16(y), NNT_ERR_ALIGN, "nnt_softmax: pointers not 16B aligned");
   double frac = causal ? 0.5 * (1.0 + 1.0 / (double)cols) : 1.0;
   LaunchScope sc(NNT_K_SOFTMAX, stream, (4.0 + dtype_size(y_dtype)) * rows * cols * frac + 8.0 * rows, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   if (y_dtype == NNT_F32)
     ::nnt::launch(softmax_kernel<float>, row_blocks(rows), kThreads, 0, stream, x, rows, cols, ldx, causal, seq_q, stats,
                                                                      (float*)y, ldy);
@@ -382,7 +378,6 @@ nnt_status nnt_softmax_bwd(const void* p, int p_dtype, int64_t ldp, const float*
   double frac = causal ? 0.5 * (1.0 + 1.0 / (double)cols) : 1.0;
   LaunchScope sc(NNT_K_SOFTMAX_BWD, stream,
                  (dtype_size(p_dtype) + 4.0 + dtype_size(da_dtype)) * rows * cols * frac, 0);
-  if (sc.skip()) return NNT_OK;  // class masked out (bench per-class timing)
   int nc = chunks_for(cols);
   unsigned g = row_blocks(rows);
 #define NNT_SMB(TP, TO, N)                                                                               \

@@ -46,7 +46,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick",
            "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd", "nnt_block_bwd_streams",
-           "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace", "nnt_timing_class_mask",
+           "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
            "nnt_cross_entropy")
 
@@ -131,7 +131,6 @@ _sig = {
     "nnt_embedding_bwd_scratch_bytes": (_sz, [_i64, _i64]),
     "nnt_embedding_bwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _vp, _sz, _vp]),
     "nnt_cross_entropy": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _i64, _vp]),
-    "nnt_timing_class_mask": (C.c_uint32, [C.c_uint32]),
     "nnt_block_workspace_size": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(_sz), C.POINTER(_sz)]),
     "nnt_block_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp]),
     "nnt_block_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp,
@@ -407,10 +406,6 @@ def nnt_timing_trace():
     kc, kn = (C.c_int32 * max(n.value, 1))(), (C.c_int32 * max(n.value, 1))()
     check(lib.nnt_timing_trace(kc, kn, n.value, C.byref(n)))
     return [(KERNEL_CLASSES[kc[i]], kn[i]) for i in range(n.value)]
-
-
-def nnt_timing_class_mask(mask):
-    return lib.nnt_timing_class_mask(mask)
 
 
 def nnt_launch_count():

@@ -27,7 +27,7 @@ def _header_functions():
     with open(os.path.join(ROOT, "include", "nnt.h")) as f:
         src = f.read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"^\s*(?:nnt_status|int|const char\s*\*|size_t|int64_t|uint32_t)\s+(nnt_\w+)\s*\(", src,
+    return sorted(set(re.findall(r"^\s*(?:nnt_status|int|const char\s*\*|size_t|int64_t)\s+(nnt_\w+)\s*\(", src,
                                  flags=re.M)))
 
 
