@@ -272,13 +272,15 @@ size_t nnt_layernorm_bwd_scratch_bytes(int64_t T, int64_t E);
  * dy: device fp32 [T][lddy]; x, mean, rstd, gamma as in the forward; dres: device
  * fp32 [T][lddx] or NULL (residual-stream gradient added to dx; may alias dx);
  * dx: device fp32 [T][lddx]; dx_bf16: device bf16 [T][lddx] copy of dx or NULL;
- * dgamma, dbeta: device fp32 [E]; accumulate_params != 0 adds into them.
+ * dgamma, dbeta: device fp32 [E]; dx_colsum: NULL or device fp32 [E] (+)= sum_t dx, the
+ * bias gradient of the linear layer that produced this LayerNorm's input (E <= 1024 only,
+ * else NNT_ERR_UNSUPPORTED); accumulate_params != 0 adds into dgamma / dbeta / dx_colsum.
  */
 nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int64_t ldx,
                              const float* mean, const float* rstd, const float* gamma,
                              int64_t T, int64_t E,
                              const float* dres, float* dx, int64_t lddx, void* dx_bf16,
-                             float* dgamma, float* dbeta, int accumulate_params,
+                             float* dgamma, float* dbeta, float* dx_colsum, int accumulate_params,
                              void* scratch, size_t scratch_bytes, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
@@ -427,12 +429,21 @@ nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, co
  * from `stream` after the ops they depend on and joined back into `stream` before the call
  * returns, so they fill the gaps of the dX chain.  Same results bit for bit.  side_stream
  * NULL = nnt_block_bwd.  grad_ready events (if given) are recorded on `stream` after the
- * join.  NNT_ERR_ARG if side_stream == stream. */
+ * join.  NNT_ERR_ARG if side_stream == stream.  links (nullable): the projection-bias column
+ * sum and the bf16 copy of dy / dx are made by the LayerNorm backward of the layer above /
+ * this layer instead of a separate pass over dy (consecutive blocks of a stack chain them). */
+typedef struct {
+  const void* dy_bf16;  /* bf16 copy of dy made by the caller (the layer above's dx_bf16), or NULL */
+  int dy_colsum_done;   /* != 0: g->b_pr already holds (+)= sum_t dy (the layer above's dx_colsum) */
+  float* dx_colsum;     /* NULL or [E]: (+)= sum_t dx, the output-projection bias gradient of the
+                           layer below (follows accumulate_grads; E <= 1024) */
+  void* dx_bf16;        /* NULL or bf16 [T][E]: copy of dx for the layer below (bf16 path) */
+} nnt_block_bwd_links;
 nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
                                  const void* saved, void* scratch, const float* dy, float* dx,
                                  const nnt_block_grads* g, int accumulate_grads,
                                  nnt_event_t* grad_ready, nnt_stream_t stream,
-                                 nnt_stream_t side_stream);
+                                 nnt_stream_t side_stream, const nnt_block_bwd_links* links);
 
 /* ------------------------------------------------------------------------- */
 /* Tile-task DAG (STF rules S:46)                               */

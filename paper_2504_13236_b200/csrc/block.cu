@@ -104,6 +104,8 @@ struct Ctx {
   Layout L;
   cudaStream_t st;
   cudaStream_t side;  // nnt_block_bwd_streams: weight/bias-gradient ops run here (or NULL)
+  const nnt_block_bwd_links* links;  // nnt_block_bwd_streams: fused cross-layer bias sums (or NULL)
+  bool ln_rows;                      // E <= 1024: the LayerNorm row kernel (column sums of dx fusable)
   template <typename P>
   P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
   template <typename P>
@@ -204,7 +206,9 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
   const int64_t batch[2] = {B, H};
   const float beta = acc ? 1.f : 0.f;
   // GEMM operand views of dy and dx1 (bf16 copies on the bf16 path)
-  const void* dyA = bf ? x.k<void>(x.L.dy16) : (const void*)dy;
+  // the layer above's LayerNorm already made sum_t dy (into g->b_pr) and the bf16 copy of dy
+  const bool dy_done = x.links && x.links->dy_colsum_done && (!bf || x.links->dy_bf16);
+  const void* dyA = bf ? (dy_done ? x.links->dy_bf16 : x.k<void>(x.L.dy16)) : (const void*)dy;
   const void* dx1A = bf ? x.k<void>(x.L.dx116) : x.k<void>(x.L.dx1);
   nnt_epilogue e{};
   nnt_epilogue ws{};  // dW GEMMs: split-K partials in the shared scratch
@@ -212,6 +216,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
   ws.workspace_bytes = x.L.gemm_ws_bytes;
   switch (op) {
     case NNT_OP_PROJ_DB:
+      if (dy_done) return NNT_OK;  // fused into the layer above's LayerNorm backward
       return nnt_bias_grad(dy, NNT_F32, T, E, E, g->b_pr, acc, bf ? x.k<void>(x.L.dy16) : nullptr,
                            x.k<void>(x.L.colsum), x.L.colsum_bytes, x.st);
     case NNT_OP_PROJ_DW:
@@ -233,11 +238,13 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
                   nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
     case NNT_OP_LN2_BWD:
+      // b_o's gradient sum_t dx1 is the column sum of this LayerNorm's output: fused (E <= 1024)
       return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, x.s<float>(x.L.x1), E, x.s<float>(x.L.mean2),
                                x.s<float>(x.L.rstd2), p->ln2_g, T, E, dy, x.k<float>(x.L.dx1), E,
-                               bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, acc, x.k<void>(x.L.lnscr),
-                               x.L.lnscr_bytes, x.st);
+                               bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, x.ln_rows ? g->b_o : nullptr,
+                               acc, x.k<void>(x.L.lnscr), x.L.lnscr_bytes, x.st);
     case NNT_OP_OUT_DB:
+      if (x.ln_rows) return NNT_OK;  // fused into NNT_OP_LN2_BWD
       return nnt_bias_grad(x.k<float>(x.L.dx1), NNT_F32, T, E, E, g->b_o, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_OUT_DW:
@@ -295,7 +302,8 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                   p->w_qkv, E, nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
     case NNT_OP_LN1_BWD:
       return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, xin, E, x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), p->ln1_g,
-                               T, E, x.k<float>(x.L.dx1), dx, E, nullptr, g->ln1_g, g->ln1_b, acc,
+                               T, E, x.k<float>(x.L.dx1), dx, E, x.links ? x.links->dx_bf16 : nullptr, g->ln1_g,
+                               g->ln1_b, x.links && x.ln_rows ? x.links->dx_colsum : nullptr, acc,
                                x.k<void>(x.L.lnscr), x.L.lnscr_bytes, x.st);
   }
   return fail(NNT_ERR_ARG, "block bwd: unexpected op in plan");
@@ -320,6 +328,8 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.L = make_layout(c);
   x.st = st;
   x.side = nullptr;
+  x.links = nullptr;
+  x.ln_rows = c.E <= 1024;
   return x;
 }
 
@@ -367,13 +377,14 @@ nnt_status nnt_block_fwd(const nnt_block_cfg* cfg, const nnt_block_params* p, co
 nnt_status nnt_block_bwd(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x, const void* saved,
                          void* scratch, const float* dy, float* dx, const nnt_block_grads* g, int accumulate_grads,
                          nnt_event_t* grad_ready, nnt_stream_t stream) {
-  return nnt_block_bwd_streams(cfg, p, x, saved, scratch, dy, dx, g, accumulate_grads, grad_ready, stream, nullptr);
+  return nnt_block_bwd_streams(cfg, p, x, saved, scratch, dy, dx, g, accumulate_grads, grad_ready, stream, nullptr,
+                               nullptr);
 }
 
 nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
                                  const void* saved, void* scratch, const float* dy, float* dx,
                                  const nnt_block_grads* g, int accumulate_grads, nnt_event_t* grad_ready,
-                                 nnt_stream_t stream, nnt_stream_t side_stream) {
+                                 nnt_stream_t stream, nnt_stream_t side_stream, const nnt_block_bwd_links* links) {
   NNT_TRY(check_cfg(cfg));
   NNT_REQUIRE(p && x && saved && scratch && dy && dx && g, NNT_ERR_NULL, "nnt_block_bwd: NULL argument");
   NNT_REQUIRE(g->ln1_g && g->ln1_b && g->ln2_g && g->ln2_b && g->w_qkv && g->w_o && g->w_fc && g->w_pr && g->b_qkv &&
@@ -385,6 +396,11 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
   NNT_REQUIRE(plan != nullptr, NNT_ERR_SHAPE, "nnt_block_bwd: %s", nnt_last_error());
   NNT_TRY(check_plan(plan));
   Ctx c = make_ctx(*cfg, const_cast<void*>(saved), scratch, stream);
+  NNT_REQUIRE(!links || !links->dx_colsum || c.ln_rows, NNT_ERR_UNSUPPORTED,
+              "nnt_block_bwd_streams: links.dx_colsum needs E <= 1024");
+  NNT_REQUIRE(!links || !links->dx_bf16 || cfg->dtype == NNT_BF16, NNT_ERR_DTYPE,
+              "nnt_block_bwd_streams: links.dx_bf16 is for the bf16 path");
+  c.links = links;
   cudaStream_t side = (cudaStream_t)side_stream;
   // Ops that only produce weight / bias gradients leave the critical dX chain: with a side
   // stream they run there, each after everything enqueued on the main stream so far (one

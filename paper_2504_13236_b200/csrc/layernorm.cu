@@ -168,20 +168,27 @@ __device__ __forceinline__ float4 dx_of(const RowGrad& r, float rs, float sa, fl
 // SM leave 168 registers per thread: no spills at E = 768.
 constexpr int kRowsWarps = 6;
 
-template <int NV>
+// SUM: also the column sums of the output dx (a third partial row: the bias gradient of the
+// linear layer whose output this LayerNorm's input is, e.g. the previous block's projection).
+template <int NV, bool SUM>
 __global__ void __launch_bounds__(32 * kRowsWarps, 2)
     ln_bwd_rows(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
                 const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
                 int64_t T, int E, int64_t rows_per_cta, const float* __restrict__ dres, float* __restrict__ dx,
-                int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb) {
+                int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb,
+                float* __restrict__ ps) {
   NNT_PDL_ENTRY();
-  extern __shared__ float4 red[];  // [kRowsWarps][2][E/4], used once at the end
+  extern __shared__ float4 red[];  // [kRowsWarps][2 + SUM][E/4], used once at the end
+  constexpr int NP = SUM ? 3 : 2;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int E4 = E / 4;
   const float inv_e = 1.0f / (float)E;
-  float4 ag[NV], ab[NV];
+  float4 ag[NV], ab[NV], as[SUM ? NV : 1];
 #pragma unroll
   for (int j = 0; j < NV; ++j) ag[j] = ab[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (SUM)
+#pragma unroll
+    for (int j = 0; j < (SUM ? NV : 1); ++j) as[j] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
   const int64_t r1 = min(r0 + rows_per_cta, T);
   for (int64_t row = r0 + w; row < r1; row += kRowsWarps) {
@@ -223,6 +230,9 @@ __global__ void __launch_bounds__(32 * kRowsWarps, 2)
         o.x += rr[j].x; o.y += rr[j].y; o.z += rr[j].z; o.w += rr[j].w;
         *reinterpret_cast<float4*>(dx + row * lddx + 4 * i4) = o;
         if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + 4 * i4, o);
+        if constexpr (SUM) {
+          as[j].x += o.x; as[j].y += o.y; as[j].z += o.z; as[j].w += o.w;
+        }
       }
     }
   }
@@ -230,21 +240,28 @@ __global__ void __launch_bounds__(32 * kRowsWarps, 2)
   for (int j = 0; j < NV; ++j) {
     const int i4 = lane + 32 * j;
     if (i4 < E4) {
-      red[(size_t)(2 * w) * E4 + i4] = ag[j];
-      red[(size_t)(2 * w + 1) * E4 + i4] = ab[j];
+      red[(size_t)(NP * w) * E4 + i4] = ag[j];
+      red[(size_t)(NP * w + 1) * E4 + i4] = ab[j];
+      if constexpr (SUM) red[(size_t)(NP * w + 2) * E4 + i4] = as[j];
     }
   }
   __syncthreads();
   for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kRowsWarps) {
-    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f),
+           ss = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < kRowsWarps; ++k) {  // fixed warp order
-      const float4 a = red[(size_t)(2 * k) * E4 + i4], b = red[(size_t)(2 * k + 1) * E4 + i4];
+      const float4 a = red[(size_t)(NP * k) * E4 + i4], b = red[(size_t)(NP * k + 1) * E4 + i4];
       sg.x += a.x; sg.y += a.y; sg.z += a.z; sg.w += a.w;
       s4.x += b.x; s4.y += b.y; s4.z += b.z; s4.w += b.w;
+      if constexpr (SUM) {
+        const float4 c = red[(size_t)(NP * k + 2) * E4 + i4];
+        ss.x += c.x; ss.y += c.y; ss.z += c.z; ss.w += c.w;
+      }
     }
     reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E)[i4] = sg;
     reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = s4;
+    if constexpr (SUM) reinterpret_cast<float4*>(ps + (int64_t)blockIdx.x * E)[i4] = ss;
   }
 }
 
@@ -384,13 +401,14 @@ nnt_status nnt_layernorm_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, 
 size_t nnt_layernorm_bwd_scratch_bytes(int64_t T, int64_t E) {
   if (T <= 0 || E <= 0) return 0;
   int64_t chunks = (T + kCtaBwdRows - 1) / kCtaBwdRows;  // >= the warp kernel's chunk count
-  return (size_t)(2 * chunks * E) * sizeof(float);
+  return (size_t)(3 * chunks * E) * sizeof(float);  // dgamma, dbeta and (optional) sum_t dx partials
 }
 
 nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int64_t ldx, const float* mean,
                              const float* rstd, const float* gamma, int64_t T, int64_t E, const float* dres,
                              float* dx, int64_t lddx, void* dx_bf16, float* dgamma, float* dbeta,
-                             int accumulate_params, void* scratch, size_t scratch_bytes, nnt_stream_t stream) {
+                             float* dx_colsum, int accumulate_params, void* scratch, size_t scratch_bytes,
+                             nnt_stream_t stream) {
   NNT_REQUIRE(dy && x && mean && rstd && gamma && dx && dgamma && dbeta && scratch, NNT_ERR_NULL,
               "nnt_layernorm_bwd: NULL pointer");
   NNT_REQUIRE(T > 0 && E > 0 && lddy >= E && ldx >= E && lddx >= E, NNT_ERR_SHAPE,
@@ -403,6 +421,8 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
               "nnt_layernorm_bwd: scratch %zu < %zu", scratch_bytes, nnt_layernorm_bwd_scratch_bytes(T, E));
   NNT_REQUIRE(pick_nv_cta(E) > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: E=%lld > 8192", (long long)E);
   const int nvw = pick_nv_warp(E);
+  NNT_REQUIRE(dx_colsum == nullptr || nvw > 0, NNT_ERR_UNSUPPORTED,
+              "nnt_layernorm_bwd: dx_colsum needs E <= 1024 (the row kernel), E=%lld", (long long)E);
   // single-pass row kernel: rows per CTA so that two CTAs per SM cover T in one wave (>= 16
   // rows, so the partial count stays within nnt_layernorm_bwd_scratch_bytes)
   int64_t rows_per_cta = (T + 2 * num_sms() - 1) / (2 * num_sms());
@@ -410,17 +430,22 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
   const int64_t chunks = nvw > 0 ? (T + rows_per_cta - 1) / rows_per_cta : (T + kCtaBwdRows - 1) / kCtaBwdRows;
   float* pg = (float*)scratch;
   float* pb = pg + chunks * E;
+  float* ps = pb + chunks * E;
   double bytes = (double)T * E * (4 + 4 + 4 + (dres ? 4 : 0) + (dx_bf16 ? 2 : 0)) + 8.0 * T;
+  const bool sum = dx_colsum != nullptr;
   LaunchScope sc(NNT_K_LN_BWD, stream, bytes, 0, 2);
   __nv_bfloat16* d16 = (__nv_bfloat16*)dx_bf16;
   if (nvw > 0) {
-    const size_t smem_red = (size_t)kRowsWarps * 2 * E * sizeof(float);  // <= 48 KB (E <= 1024)
-#define NNT_LNBR(N)                                                                                                \
-  case N:                                                                                                          \
-    ::nnt::launch(ln_bwd_rows<N>, (unsigned)chunks, 32 * kRowsWarps, smem_red, stream, dy, lddy, x, ldx, mean, rstd, gamma, T, \
-                                                                            (int)E, rows_per_cta, dres, dx, lddx,  \
-                                                                            d16, pg, pb);                          \
-    break;
+    const size_t smem_red = (size_t)kRowsWarps * (sum ? 3 : 2) * E * sizeof(float);  // <= 72 KB (E <= 1024)
+    auto run = [&](auto kern) -> nnt_status {
+      if (smem_red > 48 * 1024)
+        NNT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_red));
+      NNT_CUDA_TRY(::nnt::launch(kern, dim3((unsigned)chunks), dim3(32 * kRowsWarps), smem_red, stream, dy, lddy, x,
+                                 ldx, mean, rstd, gamma, T, (int)E, rows_per_cta, dres, dx, lddx, d16, pg, pb, ps));
+      return NNT_OK;
+    };
+#define NNT_LNBR(N) \
+  case N: NNT_TRY(sum ? run(ln_bwd_rows<N, true>) : run(ln_bwd_rows<N, false>)); break;
     switch (nvw) { NNT_LNBR(1) NNT_LNBR(2) NNT_LNBR(4) NNT_LNBR(6) NNT_LNBR(8) }
 #undef NNT_LNBR
   } else {
@@ -433,7 +458,10 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
 #undef NNT_LNB
   }
   NNT_TRY(check_launch("layernorm_bwd"));
-  launch_column_merge2(pg, chunks * E, chunks, E, dgamma, dbeta, accumulate_params, stream);
+  if (sum)
+    launch_column_merge3(pg, chunks * E, chunks, E, dgamma, dbeta, dx_colsum, accumulate_params, stream);
+  else
+    launch_column_merge2(pg, chunks * E, chunks, E, dgamma, dbeta, accumulate_params, stream);
   return check_launch("layernorm_bwd merge");
 }
 

@@ -9,16 +9,16 @@ namespace nnt {
 
 constexpr int kMergeWarps = 32;
 
-// blockIdx.y selects one of up to two independent merges (part + y * group_stride -> out[y]),
-// so paired reductions (LayerNorm dgamma / dbeta) take one launch.
+// blockIdx.y selects one of up to three independent merges (part + y * group_stride -> out[y]),
+// so the LayerNorm reductions (dgamma, dbeta and optionally sum_t dx) take one launch.
 static __global__ void __launch_bounds__(32 * kMergeWarps)
     column_merge_kernel(const float* __restrict__ part_base, int64_t chunks, int64_t N, float* __restrict__ out0,
-                        int accumulate, int64_t group_stride, float* __restrict__ out1) {
+                        int accumulate, int64_t group_stride, float* __restrict__ out1, float* __restrict__ out2) {
   NNT_PDL_ENTRY();
   __shared__ float red[kMergeWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float* __restrict__ part = part_base + blockIdx.y * group_stride;
-  float* __restrict__ out = blockIdx.y ? out1 : out0;
+  float* __restrict__ out = blockIdx.y == 0 ? out0 : (blockIdx.y == 1 ? out1 : out2);
   const int64_t c = (int64_t)blockIdx.x * 32 + lane;
   const int64_t per = (chunks + kMergeWarps - 1) / kMergeWarps;
   const int64_t k0 = w * per, k1 = min(chunks, k0 + per);
@@ -47,13 +47,20 @@ static __global__ void __launch_bounds__(32 * kMergeWarps)
 static inline void launch_column_merge(const float* part, int64_t chunks, int64_t N, float* out, int accumulate,
                                 cudaStream_t s) {
   ::nnt::launch(column_merge_kernel, dim3((unsigned)((N + 31) / 32), 1), 32 * kMergeWarps, 0, s, part, chunks, N, out, accumulate,
-                                                                                    0, out);
+                                                                                    0, out, out);
 }
 // two merges in one launch: part0 -> out0 and part0 + group_stride -> out1
 static inline void launch_column_merge2(const float* part0, int64_t group_stride, int64_t chunks, int64_t N,
                                         float* out0, float* out1, int accumulate, cudaStream_t s) {
   ::nnt::launch(column_merge_kernel, dim3((unsigned)((N + 31) / 32), 2), 32 * kMergeWarps, 0, s, part0, chunks, N, out0,
-                                                                                    accumulate, group_stride, out1);
+                                                                                    accumulate, group_stride, out1, out1);
+}
+
+// three merges in one launch: part0 + y * group_stride -> out_y, y = 0, 1, 2
+static inline void launch_column_merge3(const float* part0, int64_t group_stride, int64_t chunks, int64_t N,
+                                        float* out0, float* out1, float* out2, int accumulate, cudaStream_t s) {
+  ::nnt::launch(column_merge_kernel, dim3((unsigned)((N + 31) / 32), 3), 32 * kMergeWarps, 0, s, part0, chunks, N,
+                out0, accumulate, group_stride, out1, out2);
 }
 
 }  // namespace nnt

@@ -136,6 +136,12 @@ class BlockStack:
         act = dict(device=self.dev, dtype=torch.float32)
         self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
         self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
+        # links between consecutive blocks' backward passes (E <= 1024, the LayerNorm row kernel):
+        # layer l's LayerNorm-1 backward also makes sum_t dx (layer l-1's projection-bias gradient)
+        # and, on the bf16 path, the bf16 copy of dx that layer l-1's projection GEMMs read
+        self.chain = E <= 1024
+        self.dy16 = ([torch.empty(cfg.B, cfg.S, E, device=self.dev, dtype=torch.bfloat16) for _ in range(2)]
+                     if self.chain and cfg.dtype == "bf16" else None)
         self.loss = torch.zeros(1, **act)
         self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
         self.comm = torch.cuda.Stream(device=self.dev) if self.dp else None
@@ -192,16 +198,28 @@ class BlockStack:
         nnt.nnt_scale(r, inv, self.dy[0], n)
         return self.loss
 
-    def backward(self, overlap_optimizer=True):
-        """Backward through the stack; with DP, bucket all-reduce (+ Adam) overlapped on the comm stream."""
+    def backward(self, overlap_optimizer=True, top_done=False):
+        """Backward through the stack; with DP, bucket all-reduce (+ Adam) overlapped on the comm stream.
+
+        top_done: the caller already wrote sum_t dy into the top layer's b_pr gradient and (bf16)
+        the bf16 copy of dy into self.dy16[0] (GPT2Model's final-LayerNorm backward does)."""
         cur = 0
         compute = torch.cuda.current_stream()
         dp = self.dp
         for l in range(self.cfg.L - 1, -1, -1):
             ev = self.events[l] if dp else None
+            links = None
+            if self.chain:
+                links = nnt.nnt_block_bwd_links()
+                done = l < self.cfg.L - 1 or top_done
+                links.dy_colsum_done = 1 if done else 0
+                links.dy_bf16 = self.dy16[cur].data_ptr() if (done and self.dy16 is not None) else None
+                if l > 0:
+                    links.dx_colsum = self.view(self.g, l - 1, "b_pr").data_ptr()
+                    links.dx_bf16 = self.dy16[1 - cur].data_ptr() if self.dy16 is not None else None
             nnt.nnt_block_bwd_streams(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch,
                                       self.dy[cur], self.dy[1 - cur], self._grads[l], 0, ev,
-                                      side_stream=self.side)
+                                      side_stream=self.side, links=links)
             if dp:
                 for si in range(4):
                     self._reduce_bucket(l, si, ev[si], overlap_optimizer)
@@ -436,10 +454,13 @@ class GPT2Model:
                           self.dh_epi)
         nnt.nnt_tile_gemm(nnt.NNT_TRANS, nnt.NNT_NOTRANS, V, E, T, None, 1.0, self.logits, self.dt, self.Vp, None,
                           self.hf, self.dt, E, None, 0.0, self.view(self.g, "wte"), nnt.NNT_F32, E, None, tiles)
+        top = st.chain  # the final LayerNorm's backward also makes the top block's b_pr sum and dy copy
         nnt.nnt_layernorm_bwd(self.dhf, E, st.xs[-1], E, self.mean, self.rstd, self.view(self.w, "lnf_g"), T, E,
-                              None, st.dy[0], E, None, self.view(self.g, "lnf_g"), self.view(self.g, "lnf_b"), 0,
+                              None, st.dy[0], E, st.dy16[0] if (top and st.dy16 is not None) else None,
+                              self.view(self.g, "lnf_g"), self.view(self.g, "lnf_b"),
+                              st.view(st.g, c.L - 1, "b_pr") if top else None, 0,
                               self.lnf_scr, self.lnf_scr.numel())
-        dx0 = st.backward()
+        dx0 = st.backward(top_done=top)
         nnt.nnt_embedding_bwd(self.ids, T, c.S, dx0, E, self.view(self.g, "wte"), V, self.view(self.g, "wpe"), 1,
                               self.emb_scr, self.emb_scr.numel())
         if st.dp:  # the shell bucket: all-reduce + Adam on the comm stream

@@ -86,6 +86,11 @@ class nnt_block_grads(C.Structure):
                                            "w_fc", "b_fc", "w_pr", "b_pr")]
 
 
+class nnt_block_bwd_links(C.Structure):
+    _fields_ = [("dy_bf16", C.c_void_p), ("dy_colsum_done", C.c_int), ("dx_colsum", C.c_void_p),
+                ("dx_bf16", C.c_void_p)]
+
+
 class nnt_task(C.Structure):
     _fields_ = [("op", C.c_int32), ("level", C.c_int32), ("tile", C.c_int64 * 3), ("n_deps", C.c_int32),
                 ("group", C.c_int32)]
@@ -116,7 +121,7 @@ _sig = {
     "nnt_layernorm_fwd": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _i32, _i64, _vp, _vp, _vp]),
     "nnt_layernorm_bwd_scratch_bytes": (_sz, [_i64, _i64]),
     "nnt_layernorm_bwd": (_i32, [_vp, _i64, _vp, _i64, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _i64, _vp, _vp, _vp,
-                                 _i32, _vp, _sz, _vp]),
+                                 _vp, _i32, _vp, _sz, _vp]),
     "nnt_gelu_fwd": (_i32, [_vp, _vp, _i32, _i64, _vp]),
     "nnt_gelu_bwd": (_i32, [_vp, _vp, _vp, _i32, _i64, _vp]),
     "nnt_bias_grad_scratch_bytes": (_sz, [_i64, _i64]),
@@ -136,7 +141,8 @@ _sig = {
     "nnt_block_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp,
                              C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp]),
     "nnt_block_bwd_streams": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp,
-                                     _vp, C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp, _vp]),
+                                     _vp, C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp, _vp,
+                                     C.POINTER(nnt_block_bwd_links)]),
     "nnt_op_name": (C.c_char_p, [_i32]),
     "nnt_block_dag_describe": (_i32, [C.POINTER(nnt_block_cfg), _i32, C.POINTER(nnt_task), _i64, _P64,
                                       C.POINTER(nnt_launch_group), _i64, _P64]),
@@ -274,10 +280,11 @@ def nnt_layernorm_bwd_scratch_bytes(T, E):
 
 
 def nnt_layernorm_bwd(dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, dx_bf16, dgamma, dbeta,
-                      accumulate_params, scratch, scratch_bytes, stream=None):
+                      dx_colsum, accumulate_params, scratch, scratch_bytes, stream=None):
     return check(lib.nnt_layernorm_bwd(ptr(dy), lddy, ptr(x), ldx, ptr(mean), ptr(rstd), ptr(gamma), T, E,
                                        ptr(dres), ptr(dx), lddx, ptr(dx_bf16), ptr(dgamma), ptr(dbeta),
-                                       accumulate_params, ptr(scratch), scratch_bytes, _stream(stream)))
+                                       ptr(dx_colsum), accumulate_params, ptr(scratch), scratch_bytes,
+                                       _stream(stream)))
 
 
 def nnt_gelu_fwd(x, y, dtype, n, stream=None):
@@ -351,11 +358,12 @@ def nnt_block_fwd(cfg, params, x, y, saved, scratch, stream=None):
 
 
 def nnt_block_bwd_streams(cfg, params, x, saved, scratch, dy, dx, grads, accumulate_grads, grad_ready=None,
-                          stream=None, side_stream=None):
+                          stream=None, side_stream=None, links=None):
     ev = _events(grad_ready)
     return check(lib.nnt_block_bwd_streams(C.byref(cfg), C.byref(params), ptr(x), ptr(saved), ptr(scratch), ptr(dy),
                                            ptr(dx), C.byref(grads), accumulate_grads, ev, _stream(stream),
-                                           None if side_stream is None else _stream(side_stream)))
+                                           None if side_stream is None else _stream(side_stream),
+                                           C.byref(links) if links is not None else None))
 
 
 def _events(grad_ready):

@@ -108,8 +108,8 @@ def test_kernel_validation_without_gpu(nnt):
     assert L.nnt_layernorm_fwd(FAKE, 4, 0, 8, 8, FAKE, FAKE, 1e-5, FAKE, 0, 8, FAKE, FAKE, None) == nnt.NNT_ERR_SHAPE
     assert L.nnt_layernorm_fwd(FAKE, 4, 8, 8, 0, FAKE, FAKE, 1e-5, FAKE, 0, 8, FAKE, FAKE, None) == nnt.NNT_ERR_TILE
     assert L.nnt_layernorm_fwd(FAKE, 4, 8, 8, 8, FAKE, FAKE, 1e-5, FAKE, 7, 8, FAKE, FAKE, None) == nnt.NNT_ERR_DTYPE
-    assert L.nnt_layernorm_bwd(FAKE, 8, FAKE, 8, FAKE, FAKE, FAKE, 4, 8, None, FAKE, 8, None, FAKE, FAKE, 0, FAKE,
-                               1, None) == nnt.NNT_ERR_WORKSPACE
+    assert L.nnt_layernorm_bwd(FAKE, 8, FAKE, 8, FAKE, FAKE, FAKE, 4, 8, None, FAKE, 8, None, FAKE, FAKE, None, 0,
+                               FAKE, 1, None) == nnt.NNT_ERR_WORKSPACE
     hp = nnt.nnt_adam_hparams(1e-3, 0.9, 0.999, 1e-8, 0.0, 0.0, 0.001, 1.0)
     assert L.nnt_adam_step(16, FAKE, FAKE, FAKE, FAKE, None, C.byref(hp), None) == nnt.NNT_ERR_ARG
     assert L.nnt_gelu_fwd(FAKE, FAKE, 3, 16, None) == nnt.NNT_ERR_DTYPE

@@ -178,13 +178,22 @@ def test_layernorm_bwd(E):
     DB = dev(np.ones(E, np.float32))
     nb = nnt.nnt_layernorm_bwd_scratch_bytes(T, E)
     scr = torch.empty(nb, device="cuda", dtype=torch.uint8)
+    # the fused column sum of the output dx (the row kernel, E <= 1024)
+    DS = dev(np.full(E, 2.0, np.float32)) if E <= 1024 else None
     nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)), dev(r_ref.astype(np.float32)),
-                          dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, 1, scr, nb)
+                          dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, DS, 1, scr, nb)
     torch.cuda.synchronize()
     assert rel(host(DX), dx_ref + dres) < 1e-5
     assert rel(host(DX16), dx_ref + dres) < 4e-3
     assert rel(host(DG), dg_ref + 1.0) < 1e-5
     assert rel(host(DB), db_ref + 1.0) < 1e-5
+    if DS is not None:
+        assert rel(host(DS), (dx_ref + dres).sum(axis=0) + 2.0) < 1e-5
+    else:  # E > 1024: the CTA-per-row kernel has no fused column sum
+        with pytest.raises(nnt.NNTError):
+            nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)),
+                                  dev(r_ref.astype(np.float32)), dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, DG, 1,
+                                  scr, nb)
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])

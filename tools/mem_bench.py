@@ -76,7 +76,7 @@ def main():
     cases = {
         "ln_fwd": (lambda: nnt.nnt_layernorm_fwd(x, T, E, E, 1024, g, b, 1e-5, h, nnt.NNT_BF16, E, mean, rstd),
                    T * E * (4 + 2) + 8 * T),
-        "ln_bwd": (lambda: nnt.nnt_layernorm_bwd(dy, E, x, E, mean, rstd, g, T, E, dres, dx, E, dx16, dg, dg, 0,
+        "ln_bwd": (lambda: nnt.nnt_layernorm_bwd(dy, E, x, E, mean, rstd, g, T, E, dres, dx, E, dx16, dg, dg, None, 0,
                                                  lscr, lscr.numel()), T * E * (4 * 4 + 2) + 8 * T),
         "colsum_f32+copy": (lambda: nnt.nnt_bias_grad(dy, nnt.NNT_F32, T, E, E, db, 0, dx16, cscr, cscr.numel()),
                             T * E * 6),
