@@ -400,6 +400,17 @@ def adam_step(w, g, m, v, t, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8,
     return w_new, m, v
 
 
+def sgd_step(w, g, buf, lr=1e-2, momentum=0.9, weight_decay=0.0):
+    """SGD with momentum ("a weighted sum of the input vector, gradient, and
+    momentum term"), the usual heavy-ball form: buf <- momentum * buf + (g + wd * w);
+    w <- w - lr * buf.  buf starts at 0 (so the first step's buf is the gradient).
+    Returns new (w, buf)."""
+    w, g, buf = _f64(w), _f64(g), _f64(buf)
+    d = g + weight_decay * w if weight_decay else g
+    buf = momentum * buf + d
+    return w - lr * buf, buf
+
+
 # ---------------------------------------------------------------------------
 # Work counts used for reporting (SURVEY.md §8(d))
 # ---------------------------------------------------------------------------

@@ -387,3 +387,26 @@ def test_param_count_formula():
     for E in (64, 768, 1600):
         shapes = nnt_inputs.param_shapes(E)
         assert sum(int(np.prod(s)) for s in shapes.values()) == dense.block_param_count(E)
+
+
+@pytest.mark.parametrize("wd", [0.0, 0.05])
+def test_sgd_momentum_vs_torch_optim(wd):
+    """SGD with momentum against torch.optim.SGD in fp64 over 4 steps."""
+    rng = np.random.default_rng(8)
+    w0 = rng.standard_normal(37)
+    p = torch.tensor(w0, dtype=torch.float64, requires_grad=True)
+    opt = torch.optim.SGD([p], lr=1e-2, momentum=0.9, weight_decay=wd)
+    w, buf = w0.copy(), np.zeros_like(w0)
+    for _ in range(4):
+        g = rng.standard_normal(37)
+        opt.zero_grad()
+        p.grad = torch.tensor(g, dtype=torch.float64)
+        opt.step()
+        w, buf = dense.sgd_step(w, g, buf, lr=1e-2, momentum=0.9, weight_decay=wd)
+        assert np.abs(w - p.detach().numpy()).max() < 1e-15
+
+
+def test_sgd_zero_momentum_is_plain_gradient_step():
+    w, g = np.array([1.0, -2.0]), np.array([0.5, 0.25])
+    w1, buf = dense.sgd_step(w, g, np.zeros(2), lr=0.1, momentum=0.0)
+    assert np.array_equal(w1, w - 0.1 * g) and np.array_equal(buf, g)
