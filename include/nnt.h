@@ -328,6 +328,12 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
  * nnt_adam_hparams.bias_corr_dev).  One thread; usable inside a captured CUDA graph. */
 nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias_corr_dev, nnt_stream_t stream);
 
+/* SGD with momentum ("a weighted sum of the input vector, gradient, and momentum
+ * term"): buf = momentum * buf + (g + weight_decay * w); w -= lr * buf (buf starts at 0).
+ * w, g, buf: device fp32 [n]; w_bf16: nullable bf16 shadow of w, refreshed in the same pass. */
+nnt_status nnt_sgd_step(int64_t n, float* w, const float* g, float* buf, void* w_bf16, float lr, float momentum,
+                        float weight_decay, nnt_stream_t stream);
+
 /* fp32 -> bf16 (round to nearest even) or bf16 -> fp32 conversion of n elements. */
 nnt_status nnt_convert(const void* x, int x_dtype, void* y, int y_dtype, int64_t n,
                        nnt_stream_t stream);

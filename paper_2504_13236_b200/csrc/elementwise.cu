@@ -104,6 +104,44 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
   }
 }
 
+__global__ void __launch_bounds__(kThreads) sgd_kernel(int64_t n, float* __restrict__ w,
+                                                       const float* __restrict__ g, float* __restrict__ buf,
+                                                       __nv_bfloat16* __restrict__ w16, float lr, float mom, float wd,
+                                                       bool vec_ok) {
+  NNT_PDL_ENTRY();
+  auto upd = [&](float& wi, float gi, float& bi) {
+    const float d = wd != 0.f ? fmaf(wd, wi, gi) : gi;
+    bi = fmaf(mom, bi, d);
+    wi = fmaf(-lr, bi, wi);
+  };
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nv = vec_ok ? n / 4 : 0;
+  for (int64_t i = tid; i < nv; i += stride) {
+    float4 wv = reinterpret_cast<float4*>(w)[i], bv = reinterpret_cast<float4*>(buf)[i];
+    const float4 gv = reinterpret_cast<const float4*>(g)[i];
+    upd(wv.x, gv.x, bv.x);
+    upd(wv.y, gv.y, bv.y);
+    upd(wv.z, gv.z, bv.z);
+    upd(wv.w, gv.w, bv.w);
+    reinterpret_cast<float4*>(w)[i] = wv;
+    reinterpret_cast<float4*>(buf)[i] = bv;
+    if (w16) {
+      __nv_bfloat162 lo = __floats2bfloat162_rn(wv.x, wv.y), hi = __floats2bfloat162_rn(wv.z, wv.w);
+      uint2 pk;
+      pk.x = *reinterpret_cast<uint32_t*>(&lo);
+      pk.y = *reinterpret_cast<uint32_t*>(&hi);
+      reinterpret_cast<uint2*>(w16)[i] = pk;
+    }
+  }
+  for (int64_t i = nv * 4 + tid; i < n; i += stride) {
+    float wi = w[i], bi = buf[i];
+    upd(wi, g[i], bi);
+    w[i] = wi;
+    buf[i] = bi;
+    if (w16) w16[i] = __float2bfloat16_rn(wi);
+  }
+}
+
 __global__ void adam_tick_kernel(double beta1, double beta2, int64_t* t, float* bc) {
   NNT_PDL_ENTRY();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -297,6 +335,19 @@ nnt_status nnt_adam_step(int64_t n, float* w, const float* g, float* m, float* v
   LaunchScope sc(NNT_K_ADAM, stream, (28.0 + (w_bf16 ? 2.0 : 0.0)) * n, 0);
   ::nnt::launch(adam_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, n, w, g, m, v, (__nv_bfloat16*)w_bf16, *hp, vec);
   return check_launch("adam");
+}
+
+nnt_status nnt_sgd_step(int64_t n, float* w, const float* g, float* buf, void* w_bf16, float lr, float momentum,
+                        float weight_decay, nnt_stream_t stream) {
+  NNT_REQUIRE(w && g && buf, NNT_ERR_NULL, "nnt_sgd_step: NULL pointer");
+  NNT_REQUIRE(n >= 0, NNT_ERR_SHAPE, "nnt_sgd_step: n=%lld", (long long)n);
+  if (n == 0) return NNT_OK;
+  const bool vec = aligned16(w) && aligned16(g) && aligned16(buf) &&
+                   (w_bf16 == nullptr || (reinterpret_cast<uintptr_t>(w_bf16) & 7u) == 0);
+  LaunchScope sc(NNT_K_ADAM, stream, (20.0 + (w_bf16 ? 2.0 : 0.0)) * n, 0);
+  ::nnt::launch(sgd_kernel, grid_for(n / 4 + 1), kThreads, 0, stream, n, w, g, buf, (__nv_bfloat16*)w_bf16, lr,
+                momentum, weight_decay, vec);
+  return check_launch("sgd");
 }
 
 nnt_status nnt_adam_tick(double beta1, double beta2, int64_t* t_dev, float* bias_corr_dev, nnt_stream_t stream) {

@@ -80,6 +80,8 @@ class StackConfig:
     beta2: float = 0.999
     eps: float = 1e-8
     weight_decay: float = 0.0
+    optimizer: str = "adam"   # "adam" (Adam / AdamW with weight_decay) or "sgd" (SGD with momentum)
+    momentum: float = 0.9     # SGD momentum
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
 
@@ -248,6 +250,11 @@ class BlockStack:
                                     1.0 - c.beta2 ** t, 1.0)
 
     def _adam_range(self, b0, b1, t, stream=None):
+        c = self.cfg
+        if c.optimizer == "sgd":  # the momentum buffer lives in m
+            nnt.nnt_sgd_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1],
+                             self.w16[b0:b1] if self.bf16 else None, c.lr, c.momentum, c.weight_decay, stream=stream)
+            return
         hp = self._graph_hp if self._graph_hp is not None else self._hparams(t)
         nnt.nnt_adam_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1], self.v[b0:b1],
                           self.w16[b0:b1] if self.bf16 else None, hp, stream=stream)
@@ -325,8 +332,7 @@ class BlockStack:
                     self.backward(overlap_optimizer=True)
                 else:
                     self.backward()
-                    nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v,
-                                      self.w16 if self.bf16 else None, hp)
+                    self._adam_range(0, self.numel, 0)
         finally:
             self._graph_hp = None  # eager steps keep host-side bias corrections
         return g
@@ -473,6 +479,11 @@ class GPT2Model:
         return dx0
 
     def _adam(self, t, stream=None):
+        c = self.cfg
+        if c.optimizer == "sgd":
+            nnt.nnt_sgd_step(self.numel, self.w, self.g, self.m, self.w16, c.lr, c.momentum, c.weight_decay,
+                             stream=stream)
+            return
         hp = self.stack._graph_hp if self.stack._graph_hp is not None else self.stack._hparams(t)
         nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp, stream=stream)
 
@@ -525,8 +536,8 @@ class GPT2Model:
                     self.backward()
                 else:
                     self.backward()
-                    nnt.nnt_adam_step(st.numel, st.w, st.g, st.m, st.v, st.w16 if st.bf16 else None, hp)
-                    nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp)
+                    st._adam_range(0, st.numel, 0)
+                    self._adam(0)
         finally:
             st._graph_hp = None
         return g

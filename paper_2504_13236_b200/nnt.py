@@ -43,7 +43,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_partition", "nnt_tile_gemm", "nnt_tile_gemm_workspace_bytes", "nnt_maxsumexp",
            "nnt_maxsumexp_merge", "nnt_attn_rowdot", "nnt_softmax", "nnt_softmax_bwd",
            "nnt_layernorm_fwd", "nnt_layernorm_bwd_scratch_bytes", "nnt_layernorm_bwd", "nnt_gelu_fwd",
-           "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick",
+           "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick", "nnt_sgd_step",
            "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd", "nnt_block_bwd_streams",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
@@ -128,6 +128,7 @@ _sig = {
     "nnt_bias_grad": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _sz, _vp]),
     "nnt_adam_step": (_i32, [_i64, _vp, _vp, _vp, _vp, _vp, C.POINTER(nnt_adam_hparams), _vp]),
     "nnt_convert": (_i32, [_vp, _i32, _vp, _i32, _i64, _vp]),
+    "nnt_sgd_step": (_i32, [_i64, _vp, _vp, _vp, _vp, _f32, _f32, _f32, _vp]),
     "nnt_adam_tick": (_i32, [C.c_double, C.c_double, _vp, _vp, _vp]),
     "nnt_scale": (_i32, [_vp, _f32, _vp, _i64, _vp]),
     "nnt_dot_scratch_bytes": (_sz, [_i64]),
@@ -306,6 +307,11 @@ def nnt_bias_grad(dy, dy_dtype, T, N, lddy, db, accumulate, dy_bf16_out, scratch
 
 def nnt_adam_step(n, w, g, m, v, w_bf16, hp, stream=None):
     return check(lib.nnt_adam_step(n, ptr(w), ptr(g), ptr(m), ptr(v), ptr(w_bf16), C.byref(hp), _stream(stream)))
+
+
+def nnt_sgd_step(n, w, g, buf, w_bf16, lr, momentum, weight_decay, stream=None):
+    return check(lib.nnt_sgd_step(n, ptr(w), ptr(g), ptr(buf), ptr(w_bf16), lr, momentum, weight_decay,
+                                  _stream(stream)))
 
 
 def nnt_adam_tick(beta1, beta2, t_dev, bias_corr_dev, stream=None):

@@ -235,3 +235,25 @@ def test_gradient_accumulation_over_two_batches(dtype):
     torch.cuda.synchronize()
     for n, gv in st.grads_of(0).items():
         assert rel(host(gv), want[n]) < tol, n
+
+
+def test_tiny_fp32_sgd_training_steps():
+    """StackConfig(optimizer="sgd"): 3 eager steps of forward, backward, SGD-momentum update vs the
+    oracle (the momentum buffer lives in the flat m buffer)."""
+    c = nnt_inputs.CONFIGS["tiny"]
+    sc = model.StackConfig(L=1, E=c.E, H=c.H, S=c.S, B=c.B, tile_e=c.tile, tile_f=c.tile, tile_s=c.tile,
+                           tile_t=c.tile, dtype="f32", optimizer="sgd", lr=1e-2, momentum=0.9)
+    layers = [nnt_inputs.make_params(c.E, seed=1234)]
+    st = model.BlockStack(sc, layers)
+    P = {k: v.astype(np.float64) for k, v in layers[0].items()}
+    buf = {k: np.zeros_like(v) for k, v in P.items()}
+    for t in range(1, 4):
+        x = nnt_inputs.make_x(c.E, c.S, 0, c.B, seed=1000 + t)
+        r = nnt_inputs.make_r(c.E, c.S, 0, c.B, seed=1000 + t)
+        st.train_step(dev(x), dev(r))
+        _, _, _, g = _oracle_step([P], x, r, c.H, c.T)
+        for k in P:
+            P[k], buf[k] = dense.sgd_step(P[k], g[0][k], buf[k], lr=1e-2, momentum=0.9)
+    torch.cuda.synchronize()
+    for n, wv in st.params_of(0).items():
+        assert rel(host(wv) - layers[0][n], P[n] - layers[0][n]) < 1e-4, n

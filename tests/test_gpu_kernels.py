@@ -276,6 +276,22 @@ def test_adamw_decoupled_decay_matches_oracle():
         assert rel(host(W) - w, wr - w) < 1e-4
 
 
+def test_sgd_momentum_matches_oracle():
+    n = 5003
+    rng = np.random.default_rng(6)
+    w = rng.standard_normal(n).astype(np.float32)
+    W, BUF = dev(w), torch.zeros(n, device="cuda")
+    W16 = torch.zeros(n, device="cuda", dtype=torch.bfloat16)
+    wr, br = w.astype(np.float64), np.zeros(n)
+    for t in range(3):
+        g = rng.standard_normal(n).astype(np.float32)
+        nnt.nnt_sgd_step(n, W, dev(g), BUF, W16, 1e-2, 0.9, 0.01)
+        wr, br = dense.sgd_step(wr, g, br, lr=1e-2, momentum=0.9, weight_decay=0.01)
+        torch.cuda.synchronize()
+        assert rel(host(W) - w, wr - w) < 1e-5 and rel(host(BUF), br) < 1e-6
+        assert np.array_equal(host(W16), bf16_round(host(W)))
+
+
 def test_dot_and_scale():
     n = 123457
     rng = np.random.default_rng(2)
