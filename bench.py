@@ -293,7 +293,8 @@ def run_nnt(args):
     mdl = args.model or default_model(args.config)
     dtype = "f32" if args.config == "tiny" else "bf16"
     tile = 16 if args.config == "tiny" else 1024
-    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype)
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype,
+                           optimizer=args.optimizer, zero=args.zero)
     layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
     b0, b1 = nnt.nnt_partition(B * world, world, rank)  # rank r's batch tiles of the global batch
     batches = []
@@ -472,7 +473,8 @@ def run_nnt(args):
                                    f"linear-probe loss)"),
                       "model": f"gpt2-{args.config}" + ("" if mdl == "gpt2" else "-blocks"), "layers": L,
                       "d_model": E, "heads": H, "vocab": VOCAB if mdl == "gpt2" else None,
-                      "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}",
+                      "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}" + ("-zero1" if args.zero and world > 1 else ""),
+                      "optimizer": args.optimizer,
                       "launch": "one CUDA graph per step" if use_graph else "eager launches",
                       "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
            "model_tflops": model_tflops, "model_tflops_frac_of_bf16": model_tflops / peaks["bf16"],
@@ -509,6 +511,9 @@ def main():
                     help="gpt2 = full model with embeddings / tied LM head / cross-entropy (default for small, "
                          "large, xl); blocks = the block stack with a linear-probe loss (default for wide, tiny)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"], help="adam (P:194) or sgd (momentum)")
+    ap.add_argument("--zero", action="store_true", help="N>1: ZeRO-1 optimizer-state sharding (reduce-scatter, "
+                    "owned-slice update, all-gather) instead of all-reduce + replicated update")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3:

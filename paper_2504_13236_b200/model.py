@@ -37,13 +37,15 @@ def param_shapes(E):
             "ln2_g": (E,), "ln2_b": (E,), "w_fc": (F, E), "b_fc": (F,), "w_pr": (E, F), "b_pr": (E,)}
 
 
-def flat_layout(L, E):
+def flat_layout(L, E, shards=1):
     """Host bookkeeping of the flat parameter / gradient buffers (integer, bit-exact across ranks).
 
     Returns (offsets, buckets, numel): offsets[l][name] = (element offset, numel); buckets =
     [(layer, set index, begin, end)] in backward-completion order (layer L-1 first; inside a
     layer the SETS order), each bucket a contiguous slice; every tensor starts on an ALIGN
-    boundary.  These buckets are the units of the DP all-reduce."""
+    boundary.  These buckets are the units of the DP all-reduce.
+    shards > 1 (ZeRO-1): every bucket is padded to a multiple of
+    shards * ALIGN elements, so it splits into `shards` equal ALIGN-aligned owner slices."""
     shapes = param_shapes(E)
     offsets = [None] * L
     buckets = []
@@ -56,9 +58,38 @@ def flat_layout(L, E):
                 numel = math.prod(shapes[n])
                 d[n] = (off, numel)
                 off += -(-numel // ALIGN) * ALIGN
+            q = ALIGN * shards
+            off = b0 + -(-(off - b0) // q) * q
             buckets.append((l, si, b0, off))
         offsets[l] = d
     return offsets, buckets, off
+
+
+def zero_shards(buckets, world, rank):
+    """ZeRO-1 ownership (P:189-194 the update is per tile, so any partition of
+    the flat range is legal): bucket [b0, b1) splits into `world` equal slices, rank r owns
+    [b0 + r n, b0 + (r+1) n), n = (b1 - b0) / world.  Returns {b0: (s0, s1, c)}: the owned slice
+    and its offset c in the rank's compact optimizer-state buffers (owned slices back to back).
+    Integer bookkeeping, identical on every rank."""
+    out, c = {}, 0
+    for b in buckets:
+        b0, b1 = b[-2], b[-1]
+        assert (b1 - b0) % world == 0, (b0, b1, world)
+        n = (b1 - b0) // world
+        out[b0] = (b0 + rank * n, b0 + (rank + 1) * n, c)
+        c += n
+    return out, c
+
+
+def zero1_bucket(g, w, b0, b1, s0, s1, group, update):
+    """One bucket of the ZeRO-1 step: reduce-scatter the gradient slice so
+    this rank holds the SUM over ranks of its owned part (in place: the owned part of g is the
+    NCCL in-place receive position), update the owned parameters (update(s0, s1): Adam / SGD on
+    the owned slice with the rank's compact state), all-gather the updated slices of w back
+    into every rank's replica (in place again).  The caller's current stream orders it."""
+    torch.distributed.reduce_scatter_tensor(g[s0:s1], g[b0:b1], group=group)
+    update(s0, s1)
+    torch.distributed.all_gather_into_tensor(w[b0:b1], w[s0:s1], group=group)
 
 
 @dataclass
@@ -82,6 +113,9 @@ class StackConfig:
     weight_decay: float = 0.0
     optimizer: str = "adam"   # "adam" (Adam / AdamW with weight_decay) or "sgd" (SGD with momentum)
     momentum: float = 0.9     # SGD momentum
+    # DP only: ZeRO-1 -- gradients reduce-scattered by bucket slice, optimizer
+    # state for the owned slices only (1/world of m, v), updated parameters all-gathered
+    zero: bool = False
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
 
@@ -110,13 +144,17 @@ class BlockStack:
         self.bcfg = cfg.block_cfg()
         E = cfg.E
         shapes = param_shapes(E)
-        self.offsets, self.buckets, off = flat_layout(cfg.L, E)
+        self.zero = cfg.zero and self.dp
+        self.offsets, self.buckets, off = flat_layout(cfg.L, E, self.world if self.zero else 1)
         self.numel = off
         f32 = dict(device=self.dev, dtype=torch.float32)
         self.w = torch.zeros(off, **f32)
         self.g = torch.zeros(off, **f32)
-        self.m = torch.zeros(off, **f32)
-        self.v = torch.zeros(off, **f32)
+        nstate = off
+        if self.zero:
+            self.shards, nstate = zero_shards(self.buckets, self.world, torch.distributed.get_rank(process_group))
+        self.m = torch.zeros(nstate, **f32)
+        self.v = torch.zeros(nstate, **f32)
         self.bf16 = cfg.dtype == "bf16"
         self.w16 = torch.zeros(off, device=self.dev, dtype=torch.bfloat16) if self.bf16 else None
         for l, P in enumerate(layer_params):
@@ -240,9 +278,20 @@ class BlockStack:
         b0, b1 = self._bucket_range(l, si)
         with torch.cuda.stream(self.comm):
             self.comm.wait_event(event)
+            if self.zero:
+                assert with_adam, "ZeRO-1 updates inside the bucket step"
+                self._zero_bucket(b0, b1, self.step_count + 1)
+                return
             torch.distributed.all_reduce(self.g[b0:b1], group=self.pg)
             if with_adam:
                 self._adam_range(b0, b1, self.step_count + 1, stream=self.comm)
+
+    def _zero_bucket(self, b0, b1, t):
+        s0, s1, c = self.shards[b0]
+        zero1_bucket(self.g, self.w, b0, b1, s0, s1, self.pg,
+                     lambda a, b: self._update(a, b, c, t, self.comm, shadow=False))
+        if self.bf16:  # the replicas' bf16 shadows, from the gathered fp32 parameters
+            nnt.nnt_convert(self.w[b0:b1], nnt.NNT_F32, self.w16[b0:b1], nnt.NNT_BF16, b1 - b0, stream=self.comm)
 
     def _hparams(self, t):
         c = self.cfg
@@ -250,14 +299,19 @@ class BlockStack:
                                     1.0 - c.beta2 ** t, 1.0)
 
     def _adam_range(self, b0, b1, t, stream=None):
-        c = self.cfg
+        self._update(b0, b1, b0, t, stream, shadow=True)
+
+    def _update(self, b0, b1, c0, t, stream, shadow):
+        """Optimizer step on parameters [b0, b1) with state at [c0, c0 + b1 - b0) of m / v."""
+        c, n = self.cfg, b1 - b0
+        w16 = self.w16[b0:b1] if (self.bf16 and shadow) else None
         if c.optimizer == "sgd":  # the momentum buffer lives in m
-            nnt.nnt_sgd_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1],
-                             self.w16[b0:b1] if self.bf16 else None, c.lr, c.momentum, c.weight_decay, stream=stream)
+            nnt.nnt_sgd_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], w16, c.lr, c.momentum,
+                             c.weight_decay, stream=stream)
             return
         hp = self._graph_hp if self._graph_hp is not None else self._hparams(t)
-        nnt.nnt_adam_step(b1 - b0, self.w[b0:b1], self.g[b0:b1], self.m[b0:b1], self.v[b0:b1],
-                          self.w16[b0:b1] if self.bf16 else None, hp, stream=stream)
+        nnt.nnt_adam_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], self.v[c0:c0 + n], w16, hp,
+                          stream=stream)
 
     def adam(self):
         """Adam over every parameter (one launch over the flat buffer); bias corrections in fp64 on host."""
@@ -355,15 +409,17 @@ class BlockStack:
 SHELL = ("wte", "wpe", "lnf_g", "lnf_b")
 
 
-def shell_layout(V, S_max, E):
-    """Flat layout of the shell parameters (ALIGN-padded): name -> (offset, numel), total."""
+def shell_layout(V, S_max, E, shards=1):
+    """Flat layout of the shell parameters (ALIGN-padded; the total a multiple of shards * ALIGN
+    for ZeRO-1): name -> (offset, numel), total."""
     shapes = {"wte": (V, E), "wpe": (S_max, E), "lnf_g": (E,), "lnf_b": (E,)}
     off, d = 0, {}
     for n in SHELL:
         k = math.prod(shapes[n])
         d[n] = (off, k)
         off += -(-k // ALIGN) * ALIGN
-    return d, shapes, off
+    q = ALIGN * shards
+    return d, shapes, -(-off // q) * q
 
 
 class GPT2Model:
@@ -381,10 +437,14 @@ class GPT2Model:
         self.dt = nnt.NNT_BF16 if self.bf16 else nnt.NNT_F32
         tdt = torch.bfloat16 if self.bf16 else torch.float32
         self.S_max = shell_params["wpe"].shape[0]
-        self.offsets, self.shapes, n = shell_layout(V, self.S_max, E)
+        self.offsets, self.shapes, n = shell_layout(V, self.S_max, E, st.world if st.zero else 1)
         f32 = dict(device=self.dev, dtype=torch.float32)
         self.w, self.g = torch.zeros(n, **f32), torch.zeros(n, **f32)
-        self.m, self.v = torch.zeros(n, **f32), torch.zeros(n, **f32)
+        nstate = n
+        if st.zero:  # the shell is one more bucket
+            self.shard, nstate = zero_shards([(0, n)], st.world, torch.distributed.get_rank(st.pg))
+            self.shard = self.shard[0]
+        self.m, self.v = torch.zeros(nstate, **f32), torch.zeros(nstate, **f32)
         for name, (o, k) in self.offsets.items():
             self.w[o:o + k].copy_(torch.as_tensor(shell_params[name], dtype=torch.float32).reshape(-1).to(self.dev))
         self.numel = n
@@ -473,19 +533,31 @@ class GPT2Model:
             self.ev_shell.record()
             with torch.cuda.stream(st.comm):
                 st.comm.wait_event(self.ev_shell)
-                torch.distributed.all_reduce(self.g, group=st.pg)
-                self._adam(st.step_count + 1, stream=st.comm)
+                if st.zero:
+                    s0, s1, _ = self.shard
+                    zero1_bucket(self.g, self.w, 0, self.numel, s0, s1, st.pg,
+                                 lambda a, b: self._update(a, b, 0, st.step_count + 1, st.comm, shadow=False))
+                    if self.bf16:
+                        nnt.nnt_convert(self.w, nnt.NNT_F32, self.w16, nnt.NNT_BF16, self.numel, stream=st.comm)
+                else:
+                    torch.distributed.all_reduce(self.g, group=st.pg)
+                    self._adam(st.step_count + 1, stream=st.comm)
             torch.cuda.current_stream().wait_stream(st.comm)
         return dx0
 
     def _adam(self, t, stream=None):
-        c = self.cfg
+        self._update(0, self.numel, 0, t, stream, shadow=True)
+
+    def _update(self, b0, b1, c0, t, stream, shadow):
+        c, n = self.cfg, b1 - b0
+        w16 = self.w16[b0:b1] if (self.bf16 and shadow) else None
         if c.optimizer == "sgd":
-            nnt.nnt_sgd_step(self.numel, self.w, self.g, self.m, self.w16, c.lr, c.momentum, c.weight_decay,
-                             stream=stream)
+            nnt.nnt_sgd_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], w16, c.lr, c.momentum,
+                             c.weight_decay, stream=stream)
             return
         hp = self.stack._graph_hp if self.stack._graph_hp is not None else self.stack._hparams(t)
-        nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp, stream=stream)
+        nnt.nnt_adam_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], self.v[c0:c0 + n], w16, hp,
+                          stream=stream)
 
     def adam(self):
         self.stack.adam()

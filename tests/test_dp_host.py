@@ -116,3 +116,95 @@ def test_gloo_world2_bucketed_allreduce_equals_full_batch():
     layers = [nnt_inputs.make_params(E, seed=5, layer=l, n_layers=L) for l in range(L)]
     ref = _flat(_grads(0, NB, layers), offsets, numel)
     assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)
+
+
+def test_zero_shards_partition():
+    """ZeRO-1 ownership: per bucket, the world's owned slices tile the (padded) bucket exactly,
+    ALIGN-aligned, and the compact state offsets pack each rank's slices back to back."""
+    from paper_2504_13236_b200 import model
+    for (LL, EE, R) in ((2, 16, 2), (12, 768, 8), (48, 1600, 4), (1, 8192, 3)):
+        offsets, buckets, numel = model.flat_layout(LL, EE, shards=R)
+        _, _, numel1 = model.flat_layout(LL, EE)
+        assert numel >= numel1 and numel % (R * model.ALIGN) == 0
+        for l in range(LL):  # the tensors still sit inside their buckets
+            for si, names in enumerate(model.SETS):
+                b0, b1 = [(x[2], x[3]) for x in buckets if x[0] == l and x[1] == si][0]
+                for n in names:
+                    o, k = offsets[l][n]
+                    assert b0 <= o and o + k <= b1
+        owned = [model.zero_shards(buckets, R, r) for r in range(R)]
+        for r, (sh, nst) in enumerate(owned):
+            assert nst * R == numel
+            c = 0
+            for (_, _, b0, b1) in buckets:
+                s0, s1, cc = sh[b0]
+                assert cc == c and s0 % model.ALIGN == 0 and s1 - s0 == (b1 - b0) // R
+                assert s0 == b0 + r * (s1 - s0)
+                c += s1 - s0
+        for (_, _, b0, b1) in buckets:
+            cover = sorted((owned[r][0][b0][0], owned[r][0][b0][1]) for r in range(R))
+            assert cover[0][0] == b0 and cover[-1][1] == b1
+            assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+
+
+def _zero_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2504_13236_b200 import model, nnt
+    offsets, buckets, numel = model.flat_layout(L, E, shards=world)
+    sh, nst = model.zero_shards(buckets, world, rank)
+    b0, b1 = nnt.nnt_partition(NB, world, rank)
+    layers = [nnt_inputs.make_params(E, seed=5, layer=l, n_layers=L) for l in range(L)]
+    w = torch.tensor(_flat(layers, offsets, numel))
+    m, v = torch.zeros(nst, dtype=torch.float64), torch.zeros(nst, dtype=torch.float64)
+    for t in (1, 2):  # two optimizer steps, the second on the first's updated replica
+        P = [{n: w[o:o + k].numpy().reshape(layers[0][n].shape).copy() for n, (o, k) in offsets[l].items()}
+             for l in range(L)]
+        g = torch.tensor(_flat(_grads(b0, b1, P), offsets, numel))
+
+        def update(s0, s1, c, t=t, g=g):
+            n = s1 - s0
+            w1, m1, v1 = dense.adam_step(w[s0:s1].numpy(), g[s0:s1].numpy(), m[c:c + n].numpy(),
+                                         v[c:c + n].numpy(), t, weight_decay=0.01)
+            w[s0:s1], m[c:c + n], v[c:c + n] = torch.tensor(w1), torch.tensor(m1), torch.tensor(v1)
+
+        for (_, _, c0, c1) in buckets:
+            s0, s1, c = sh[c0]
+            model.zero1_bucket(g, w, c0, c1, s0, s1, None, lambda a, b, c=c: update(a, b, c))
+    out.put((rank, w.numpy() if rank == 0 else None, nst))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_gloo_world2_zero1_equals_replicated_adam():
+    """The ZeRO-1 bucket step (model.zero1_bucket, the same host code BlockStack runs on NCCL):
+    reduce-scatter by owned slice, AdamW on the owned slice with half-size state, all-gather of
+    the updated parameters -- two steps on two ranks equal two replicated full-batch AdamW
+    steps of the oracle (fp64)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_zero_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=240) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    from paper_2504_13236_b200 import model
+    offsets, buckets, numel = model.flat_layout(L, E, shards=2)
+    assert all(r[2] * 2 == numel for r in res)
+    got = [r[1] for r in res if r[1] is not None][0]
+    layers = [nnt_inputs.make_params(E, seed=5, layer=l, n_layers=L) for l in range(L)]
+    P = [{n: layers[l][n].astype(np.float64) for n in layers[l]} for l in range(L)]
+    st = [{n: (np.zeros_like(p), np.zeros_like(p)) for n, p in d.items()} for d in P]
+    for t in (1, 2):
+        g = _grads(0, NB, P)
+        for l in range(L):
+            for n in P[l]:
+                P[l][n], m1, v1 = dense.adam_step(P[l][n], g[l][n], *st[l][n], t, weight_decay=0.01)
+                st[l][n] = (m1, v1)
+    ref = _flat(P, offsets, numel)
+    assert np.linalg.norm(got - ref) <= 1e-12 * np.linalg.norm(ref)

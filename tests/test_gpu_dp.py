@@ -36,9 +36,9 @@ def pg():
     dist.destroy_process_group()
 
 
-def _run(pg, graph, steps=3):
+def _run(pg, graph, steps=3, zero=False):
     E, H, S, B, L = 768, 12, 256, 2, 2
-    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", zero=zero)
     layers = [nnt_inputs.make_params(E, seed=9, layer=l, init="gpt2", n_layers=L) for l in range(L)]
     st = model.BlockStack(sc, layers, process_group=pg)
     if graph:
@@ -62,9 +62,9 @@ def test_dp_path_world1_equals_single_gpu_bitwise(pg):
             assert torch.equal(a, b), graph
 
 
-def _run_gpt2(pg, graph, steps=3):
+def _run_gpt2(pg, graph, steps=3, zero=False):
     E, H, S, B, L, V = 768, 12, 128, 2, 2, 1000
-    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16")
+    sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", zero=zero)
     layers = [nnt_inputs.make_params(E, seed=9, layer=l, init="gpt2", n_layers=L) for l in range(L)]
     shell = nnt_inputs.make_shell_params(V, S, E, seed=10, init="gpt2")
     gm = model.GPT2Model(sc, V, layers, shell, process_group=pg)
@@ -85,6 +85,27 @@ def test_dp_gpt2_world1_equals_single_gpu_bitwise(pg):
     ref = _run_gpt2(None, graph=False)
     for graph in (False, True):
         got = _run_gpt2(pg, graph=graph)
+        assert got[0] == ref[0], graph
+        for a, b in zip(got[1:], ref[1:]):
+            assert torch.equal(a, b), graph
+
+
+@pytest.mark.timeout(300)
+def test_zero1_world1_equals_single_gpu_bitwise(pg):
+    """ZeRO-1 (StackConfig.zero) through NCCL: per bucket an in-place
+    reduce-scatter, Adam on the owned slice with compact state, an in-place all-gather of the
+    fp32 parameters and the bf16 shadow conversion -- block stack and full model, eager and
+    graph-captured.  At world size 1 every collective is the identity, so the step must equal
+    the single-GPU path bitwise (the ranks>1 bookkeeping is tests/test_dp_host.py's gloo test)."""
+    ref = _run(None, graph=False)
+    for graph in (False, True):
+        got = _run(pg, graph=graph, zero=True)
+        assert got[0] == ref[0], graph
+        for a, b in zip(got[1:], ref[1:]):
+            assert torch.equal(a, b), graph
+    ref = _run_gpt2(None, graph=False)
+    for graph in (False, True):
+        got = _run_gpt2(pg, graph=graph, zero=True)
         assert got[0] == ref[0], graph
         for a, b in zip(got[1:], ref[1:]):
             assert torch.equal(a, b), graph
