@@ -452,6 +452,50 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
                                  nnt_stream_t side_stream, const nnt_block_bwd_links* links);
 
 /* ------------------------------------------------------------------------- */
+/* Tensor-parallel block shards ("split entire data  */
+/* into tiles across embedding dimension", reading R31)                          */
+/* ------------------------------------------------------------------------- */
+/* One shard of a block split over a group of R GPUs along its inner dimensions: the shard
+ * owns `heads` attention heads (the q/k/v rows of w_qkv / b_qkv for those heads, in the
+ * order q-rows, k-rows, v-rows: w_qkv [3*heads*h][E]; the matching columns of w_o:
+ * [E][heads*h]) and `ffn` hidden units (rows of w_fc / b_fc: [ffn][E]; columns of w_pr:
+ * [E][ffn]).  LayerNorm parameters, b_o and b_pr are replicated.  Activations along E
+ * (x, x1, y, dy, dx) are replicated; the shard's contributions to x1, y, dL/dh2 and dL/dh1
+ * are partial sums that the caller reduces over the group (SUM) between stages.  With
+ * heads = H, ffn = 4E, add_bias = 1 a single shard is the whole block. */
+typedef struct {
+  int64_t heads;  /* attention heads of this shard (1..H); heads * h a multiple of 8 */
+  int64_t ffn;    /* MLP hidden units of this shard (1..4E), a multiple of 8           */
+  int add_bias;   /* 1 on exactly one shard of the group: it adds b_o, b_pr and the residuals */
+} nnt_block_tp;
+
+/* Workspace bytes of one shard (as nnt_block_workspace_size). */
+nnt_status nnt_block_tp_workspace_size(const nnt_block_cfg* cfg, const nnt_block_tp* tp,
+                                       size_t* saved_bytes, size_t* scratch_bytes);
+
+/* Forward stages of a shard (p: the shard's parameter pointers, shapes above).
+ *   stage 0: LN1(x) -> QKV -> attention over the shard's heads -> out-projection:
+ *            x1 := this shard's partial of x + attn(x) (the bias and x only if add_bias).
+ *   stage 1: (x1 now the group SUM) LN2(x1) -> FC + GELU -> projection:
+ *            y := this shard's partial of x1 + mlp(x1).
+ * x, x1, y: device fp32 [B][S][E]; x1 must stay untouched until the backward. */
+nnt_status nnt_block_tp_fwd(const nnt_block_cfg* cfg, const nnt_block_tp* tp, const nnt_block_params* p,
+                            int stage, const float* x, float* x1, float* y, void* saved, void* scratch,
+                            nnt_stream_t stream);
+
+/* Backward stages of a shard (dy replicated; g: the shard's gradients; replicated
+ * parameters' gradients come out identical on every shard).
+ *   stage 0: dy -> projection / FC gradients of the shard -> dh := partial dL/dh2.
+ *   stage 1: (dh now the group SUM) LN2 backward (+ dy) -> dx1 (kept in scratch) ->
+ *            out-projection / attention / QKV gradients -> dh := partial dL/dh1.
+ *   stage 2: (dh now the group SUM) LN1 backward (+ dx1) -> dx.
+ * dh: device fp32 [B][S][E], caller-owned; scratch must not be reused between stages. */
+nnt_status nnt_block_tp_bwd(const nnt_block_cfg* cfg, const nnt_block_tp* tp, const nnt_block_params* p,
+                            int stage, const float* x, const float* x1, const void* saved, void* scratch,
+                            const float* dy, float* dh, float* dx, const nnt_block_grads* g,
+                            int accumulate_grads, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* Tile-task DAG (STF rules S:46)                               */
 /* ------------------------------------------------------------------------- */
 typedef struct {

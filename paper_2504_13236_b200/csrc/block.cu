@@ -21,8 +21,10 @@ struct Layout {
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
-Layout make_layout(const nnt_block_cfg& c) {
-  const size_t T = c.B * c.S, E = c.E, F = 4 * c.E, H = c.H, S = c.S, B = c.B;
+// H, F: the heads and FFN width this block instance computes (all of them, or one tensor-parallel
+// shard's, nnt_block_tp); Ea = H * Dh is its attention width.
+Layout make_layout(const nnt_block_cfg& c, int64_t H_l, int64_t F_l) {
+  const size_t T = c.B * c.S, E = c.E, F = F_l, H = H_l, S = c.S, B = c.B, Ea = H * (c.E / c.H);
   const size_t dt = c.dtype == NNT_BF16 ? 2 : 4;
   Layout L{};
   size_t o = 0;
@@ -34,10 +36,10 @@ Layout make_layout(const nnt_block_cfg& c) {
   L.mean1 = take(4 * T);
   L.rstd1 = take(4 * T);
   L.h1 = take(dt * T * E);
-  L.qkv = take(dt * T * 3 * E);
+  L.qkv = take(dt * T * 3 * Ea);
   L.P = take(dt * B * H * S * S);
   L.stats = take(4 * 2 * B * H * S);
-  L.O = take(dt * T * E);
+  L.O = take(dt * T * Ea);
   L.x1 = take(4 * T * E);
   L.mean2 = take(4 * T);
   L.rstd2 = take(4 * T);
@@ -54,12 +56,14 @@ Layout make_layout(const nnt_block_cfg& c) {
   L.dh = take(4 * T * E);
   L.dx1 = take(4 * T * E);
   L.dx116 = take(dt * T * E);
-  L.dO = take(dt * T * E);
+  L.dO = take(dt * T * Ea);
   L.dA = take(dt * B * H * S * S);
-  L.dqkv = take(dt * T * 3 * E);
-  size_t cs = nnt_bias_grad_scratch_bytes(T, F);
-  size_t cs2 = nnt_bias_grad_scratch_bytes(T, 3 * E);
-  L.colsum_bytes = cs > cs2 ? cs : cs2;
+  L.dqkv = take(dt * T * 3 * Ea);
+  L.colsum_bytes = 0;
+  for (size_t n : {E, F, 3 * Ea}) {
+    size_t cs = nnt_bias_grad_scratch_bytes(T, n);
+    if (cs > L.colsum_bytes) L.colsum_bytes = cs;
+  }
   L.colsum = take(L.colsum_bytes);
   L.colsum2 = take(L.colsum_bytes);  // the side stream's column sums (FC_DB, OUT_DB, QKV_DB)
   L.lnscr_bytes = nnt_layernorm_bwd_scratch_bytes(T, E);
@@ -67,7 +71,7 @@ Layout make_layout(const nnt_block_cfg& c) {
   // split-K partials of the four dW GEMMs ([3E x E], [E x E], [4E x E], [E x 4E], K = T)
   L.gemm_ws_bytes = 0;
   if (c.dtype == NNT_BF16) {
-    const size_t shapes[4][2] = {{3 * E, E}, {E, E}, {F, E}, {E, F}};
+    const size_t shapes[4][2] = {{3 * Ea, E}, {E, Ea}, {F, E}, {E, F}};
     for (auto& sh : shapes) {
       size_t b = nnt_tile_gemm_workspace_bytes((int64_t)sh[0], (int64_t)sh[1], (int64_t)T, NNT_F32, NNT_ACT_NONE,
                                                NNT_CAUSAL_NONE, 1);
@@ -96,6 +100,10 @@ nnt_status check_cfg(const nnt_block_cfg* c) {
 struct Ctx {
   const nnt_block_cfg& c;
   int64_t T, E, F, H, S, B, Dh;
+  int64_t Ea;     // attention width H * Dh (= E unless a tensor-parallel shard)
+  bool add_bias;  // OUT / PROJ add the replicated bias and the residual (false on all but one TP shard)
+  float* x1;      // the attention sub-block's output x1 (in `saved`, or the caller's for nnt_block_tp)
+  float* dh;      // dL/dh2, then dL/dh1 (in `scratch`, or the caller's for nnt_block_tp)
   int dt;
   float inv_sqrt_dh;
   int64_t tile_lin[3];
@@ -120,7 +128,7 @@ nnt_status gemm(const Ctx& x, int ta, int tb, int64_t M, int64_t N, int64_t K, c
 }
 
 nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const float* xin, float* y) {
-  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh;
+  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh, Ea = x.Ea;
   const int dt = x.dt;
   const int64_t batch[2] = {B, H};
   nnt_epilogue e{};
@@ -130,11 +138,11 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                                x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), x.st);
     case NNT_OP_QKV:
       e.bias = p->b_qkv;
-      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, 3 * E, E, nullptr, 1.f, x.s<void>(x.L.h1), E, nullptr, p->w_qkv, E,
-                  nullptr, 0.f, x.s<void>(x.L.qkv), dt, 3 * E, nullptr, &e);
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, 3 * Ea, E, nullptr, 1.f, x.s<void>(x.L.h1), E, nullptr, p->w_qkv, E,
+                  nullptr, 0.f, x.s<void>(x.L.qkv), dt, 3 * Ea, nullptr, &e);
     case NNT_OP_SCORES: {
       const size_t es = dt == NNT_BF16 ? 2 : 4;
-      const int64_t sq[2] = {S * 3 * E, Dh}, ssc[2] = {H * S * S, S * S};
+      const int64_t sq[2] = {S * 3 * Ea, Dh}, ssc[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
       uint8_t* q = x.s<uint8_t>(x.L.qkv);
       if (dt == NNT_BF16) {
@@ -142,11 +150,11 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
         // of a row run in the GEMM epilogue, producing the slice stats directly
         e.act = NNT_ACT_ROWSTATS;
         e.row_stats = x.s<float>(x.L.stats);
-        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + es * E, 3 * E, sq,
-                    0.f, nullptr, NNT_F32, S, ssc, &e);
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * Ea, sq, q + es * Ea, 3 * Ea,
+                    sq, 0.f, nullptr, NNT_F32, S, ssc, &e);
       }
-      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + es * E, 3 * E, sq, 0.f,
-                  x.k<float>(x.L.scores), NNT_F32, S, ssc, &e);
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * Ea, sq, q + es * Ea, 3 * Ea, sq,
+                  0.f, x.k<float>(x.L.scores), NNT_F32, S, ssc, &e);
     }
     case NNT_OP_MAXSUMEXP:  // fp32 path only (the bf16 path fuses it into NNT_OP_SCORES)
       return nnt_maxsumexp(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S,
@@ -154,31 +162,33 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
     case NNT_OP_SOFTMAX:
       if (dt == NNT_BF16) {
         // R26: subroutine 2 on recomputed score tiles (same MMA order as the stats pass), P in bf16
-        const int64_t sq[2] = {S * 3 * E, Dh}, sp[2] = {H * S * S, S * S};
+        const int64_t sq[2] = {S * 3 * Ea, Dh}, sp[2] = {H * S * S, S * S};
         e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
         e.act = NNT_ACT_SOFTMAX;
         e.row_stats = x.s<float>(x.L.stats);
         uint8_t* q = x.s<uint8_t>(x.L.qkv);
-        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * E, sq, q + 2 * E, 3 * E, sq,
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, x.inv_sqrt_dh, q, 3 * Ea, sq, q + 2 * Ea, 3 * Ea, sq,
                     0.f, x.s<void>(x.L.P), dt, S, sp, &e);
       }
       return nnt_softmax(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S, x.s<float>(x.L.stats),
                          x.s<void>(x.L.P), dt, S, x.st);
     case NNT_OP_PV: {
       const size_t es = dt == NNT_BF16 ? 2 : 4;
-      const int64_t sp[2] = {H * S * S, S * S}, sv[2] = {S * 3 * E, Dh}, so[2] = {S * E, Dh};
+      const int64_t sp[2] = {H * S * S, S * S}, sv[2] = {S * 3 * Ea, Dh}, so[2] = {S * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp,
-                  x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.s<void>(x.L.O), dt, E, so, &e);
+                  x.s<uint8_t>(x.L.qkv) + es * 2 * Ea, 3 * Ea, sv, 0.f, x.s<void>(x.L.O), dt, Ea, so, &e);
     }
     case NNT_OP_OUT:
-      e.bias = p->b_o;
-      e.residual = xin;
-      e.ld_residual = E;
-      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, E, nullptr, 1.f, x.s<void>(x.L.O), E, nullptr, p->w_o, E, nullptr,
-                  0.f, x.s<float>(x.L.x1), NNT_F32, E, nullptr, &e);
+      if (x.add_bias) {
+        e.bias = p->b_o;
+        e.residual = xin;
+        e.ld_residual = E;
+      }
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, Ea, nullptr, 1.f, x.s<void>(x.L.O), Ea, nullptr, p->w_o, Ea,
+                  nullptr, 0.f, x.x1, NNT_F32, E, nullptr, &e);
     case NNT_OP_LN2:
-      return nnt_layernorm_fwd(x.s<float>(x.L.x1), T, E, E, x.c.tile_e, p->ln2_g, p->ln2_b, x.c.ln_eps,
+      return nnt_layernorm_fwd(x.x1, T, E, E, x.c.tile_e, p->ln2_g, p->ln2_b, x.c.ln_eps,
                                x.s<void>(x.L.h2), dt, E, x.s<float>(x.L.mean2), x.s<float>(x.L.rstd2), x.st);
     case NNT_OP_FC:
       e.bias = p->b_fc;
@@ -188,9 +198,11 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_NOTRANS, NNT_TRANS, T, F, E, nullptr, 1.f, x.s<void>(x.L.h2), E, nullptr, p->w_fc, E,
                   nullptr, 0.f, x.s<void>(x.L.g), dt, F, nullptr, &e);
     case NNT_OP_PROJ:
-      e.bias = p->b_pr;
-      e.residual = x.s<float>(x.L.x1);
-      e.ld_residual = E;
+      if (x.add_bias) {
+        e.bias = p->b_pr;
+        e.residual = x.x1;
+        e.ld_residual = E;
+      }
       return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, F, nullptr, 1.f, x.s<void>(x.L.g), F, nullptr, p->w_pr, F,
                   nullptr, 0.f, y, NNT_F32, E, nullptr, &e);
   }
@@ -199,7 +211,7 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
 
 nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const float* xin, const float* dy, float* dx,
                       const nnt_block_grads* g, int acc) {
-  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh;
+  const int64_t T = x.T, E = x.E, F = x.F, S = x.S, H = x.H, B = x.B, Dh = x.Dh, Ea = x.Ea;
   const int dt = x.dt;
   const bool bf = dt == NNT_BF16;
   const size_t es = bf ? 2 : 4;
@@ -236,10 +248,10 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                   x.s<void>(x.L.h2), E, nullptr, beta, g->w_fc, NNT_F32, E, nullptr, &ws);
     case NNT_OP_FC_DX:
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
-                  nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
+                  nullptr, 0.f, x.dh, NNT_F32, E, nullptr, nullptr);
     case NNT_OP_LN2_BWD:
       // b_o's gradient sum_t dx1 is the column sum of this LayerNorm's output: fused (E <= 1024)
-      return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, x.s<float>(x.L.x1), E, x.s<float>(x.L.mean2),
+      return nnt_layernorm_bwd(x.dh, E, x.x1, E, x.s<float>(x.L.mean2),
                                x.s<float>(x.L.rstd2), p->ln2_g, T, E, dy, x.k<float>(x.L.dx1), E,
                                bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, x.ln_rows ? g->b_o : nullptr,
                                acc, x.k<void>(x.L.lnscr), x.L.lnscr_bytes, x.st);
@@ -248,13 +260,13 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return nnt_bias_grad(x.k<float>(x.L.dx1), NNT_F32, T, E, E, g->b_o, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_OUT_DW:
-      return gemm(x, NNT_TRANS, NNT_NOTRANS, E, E, T, nullptr, 1.f, dx1A, E, nullptr, x.s<void>(x.L.O), E, nullptr,
-                  beta, g->w_o, NNT_F32, E, nullptr, &ws);
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, E, Ea, T, nullptr, 1.f, dx1A, E, nullptr, x.s<void>(x.L.O), Ea, nullptr,
+                  beta, g->w_o, NNT_F32, Ea, nullptr, &ws);
     case NNT_OP_OUT_DX:
-      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, E, nullptr, 1.f, dx1A, E, nullptr, p->w_o, E, nullptr, 0.f,
-                  x.k<void>(x.L.dO), dt, E, nullptr, nullptr);
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, Ea, E, nullptr, 1.f, dx1A, E, nullptr, p->w_o, Ea, nullptr, 0.f,
+                  x.k<void>(x.L.dO), dt, Ea, nullptr, nullptr);
     case NNT_OP_ATT_DP: {
-      const int64_t so[2] = {S * E, Dh}, sv[2] = {S * 3 * E, Dh}, sp[2] = {H * S * S, S * S};
+      const int64_t so[2] = {S * Ea, Dh}, sv[2] = {S * 3 * Ea, Dh}, sp[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
       if (bf) {  // softmax backward in the epilogue: dA = P * (dO V^T - D) / sqrt(h), straight to bf16
         e.act = NNT_ACT_SOFTMAX_BWD;
@@ -262,17 +274,17 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
         e.ld_aux = S;
         e.rowvec = x.k<float>(x.L.dvec);
         e.rowscale = x.inv_sqrt_dh;
-        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), E, so,
-                    x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.k<void>(x.L.dA), dt, S, sp, &e);
+        return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), Ea, so,
+                    x.s<uint8_t>(x.L.qkv) + es * 2 * Ea, 3 * Ea, sv, 0.f, x.k<void>(x.L.dA), dt, S, sp, &e);
       }
-      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), E, so,
-                  x.s<uint8_t>(x.L.qkv) + es * 2 * E, 3 * E, sv, 0.f, x.k<float>(x.L.scores), NNT_F32, S, sp, &e);
+      return gemm(x, NNT_NOTRANS, NNT_TRANS, S, S, Dh, batch, 1.f, x.k<void>(x.L.dO), Ea, so,
+                  x.s<uint8_t>(x.L.qkv) + es * 2 * Ea, 3 * Ea, sv, 0.f, x.k<float>(x.L.scores), NNT_F32, S, sp, &e);
     }
     case NNT_OP_ATT_DV: {
-      const int64_t sp[2] = {H * S * S, S * S}, so[2] = {S * E, Dh}, sq[2] = {S * 3 * E, Dh};
+      const int64_t sp[2] = {H * S * S, S * S}, so[2] = {S * Ea, Dh}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
-      return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp, x.k<void>(x.L.dO), E, so,
-                  0.f, x.k<uint8_t>(x.L.dqkv) + es * 2 * E, dt, 3 * E, sq, &e);
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp, x.k<void>(x.L.dO), Ea, so,
+                  0.f, x.k<uint8_t>(x.L.dqkv) + es * 2 * Ea, dt, 3 * Ea, sq, &e);
     }
     case NNT_OP_SOFTMAX_BWD:
       if (bf)  // the reduction D = sum_k P dP via the dO.O identity; dA is formed in the dP GEMM
@@ -280,28 +292,28 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return nnt_softmax_bwd(x.s<void>(x.L.P), dt, S, x.k<float>(x.L.scores), S, B * H * S, S, x.c.causal, S,
                              x.inv_sqrt_dh, x.k<void>(x.L.dA), dt, S, x.st);
     case NNT_OP_ATT_DQ: {
-      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * E, Dh};
+      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
-                  x.s<uint8_t>(x.L.qkv) + es * E, 3 * E, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * E, sq, &e);
+                  x.s<uint8_t>(x.L.qkv) + es * Ea, 3 * Ea, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * Ea, sq, &e);
     }
     case NNT_OP_ATT_DK: {
-      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * E, Dh};
+      const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
       return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp, x.s<void>(x.L.qkv),
-                  3 * E, sq, 0.f, x.k<uint8_t>(x.L.dqkv) + es * E, dt, 3 * E, sq, &e);
+                  3 * Ea, sq, 0.f, x.k<uint8_t>(x.L.dqkv) + es * Ea, dt, 3 * Ea, sq, &e);
     }
     case NNT_OP_QKV_DB:
-      return nnt_bias_grad(x.k<void>(x.L.dqkv), dt, T, 3 * E, 3 * E, g->b_qkv, acc, nullptr, x.k<void>(x.L.colsum2),
+      return nnt_bias_grad(x.k<void>(x.L.dqkv), dt, T, 3 * Ea, 3 * Ea, g->b_qkv, acc, nullptr, x.k<void>(x.L.colsum2),
                            x.L.colsum_bytes, x.st);
     case NNT_OP_QKV_DW:
-      return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * E, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
+      return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * Ea, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * Ea, nullptr,
                   x.s<void>(x.L.h1), E, nullptr, beta, g->w_qkv, NNT_F32, E, nullptr, &ws);
     case NNT_OP_QKV_DX:
-      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, 3 * E, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * E, nullptr,
-                  p->w_qkv, E, nullptr, 0.f, x.k<float>(x.L.dh), NNT_F32, E, nullptr, nullptr);
+      return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, 3 * Ea, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * Ea, nullptr,
+                  p->w_qkv, E, nullptr, 0.f, x.dh, NNT_F32, E, nullptr, nullptr);
     case NNT_OP_LN1_BWD:
-      return nnt_layernorm_bwd(x.k<float>(x.L.dh), E, xin, E, x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), p->ln1_g,
+      return nnt_layernorm_bwd(x.dh, E, xin, E, x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), p->ln1_g,
                                T, E, x.k<float>(x.L.dx1), dx, E, x.links ? x.links->dx_bf16 : nullptr, g->ln1_g,
                                g->ln1_b, x.links && x.ln_rows ? x.links->dx_colsum : nullptr, acc,
                                x.k<void>(x.L.lnscr), x.L.lnscr_bytes, x.st);
@@ -309,12 +321,12 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
   return fail(NNT_ERR_ARG, "block bwd: unexpected op in plan");
 }
 
-Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st) {
+Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st, const nnt_block_tp* tp = nullptr) {
   Ctx x{c};
   x.T = c.B * c.S;
   x.E = c.E;
-  x.F = 4 * c.E;
-  x.H = c.H;
+  x.F = tp ? tp->ffn : 4 * c.E;
+  x.H = tp ? tp->heads : c.H;
   x.S = c.S;
   x.B = c.B;
   x.Dh = c.E / c.H;
@@ -325,7 +337,11 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.tile_lin[2] = c.tile_e;
   x.sv = (uint8_t*)saved;
   x.sc = (uint8_t*)scratch;
-  x.L = make_layout(c);
+  x.Ea = x.H * x.Dh;
+  x.add_bias = tp ? tp->add_bias != 0 : true;
+  x.L = make_layout(c, x.H, x.F);
+  x.x1 = reinterpret_cast<float*>(x.sv + x.L.x1);
+  x.dh = reinterpret_cast<float*>(x.sc + x.L.dh);
   x.st = st;
   x.side = nullptr;
   x.links = nullptr;
@@ -343,6 +359,29 @@ nnt_status check_plan(const BlockPlan* plan) {
   return NNT_OK;
 }
 
+nnt_status check_tp(const nnt_block_cfg* c, const nnt_block_tp* tp) {
+  NNT_TRY(check_cfg(c));
+  NNT_REQUIRE(tp, NNT_ERR_NULL, "nnt_block_tp: NULL shard descriptor");
+  NNT_REQUIRE(tp->heads > 0 && tp->heads <= c->H && tp->ffn > 0 && tp->ffn <= 4 * c->E, NNT_ERR_SHAPE,
+              "nnt_block_tp: shard heads=%lld (H=%lld) ffn=%lld (4E=%lld)", (long long)tp->heads, (long long)c->H,
+              (long long)tp->ffn, (long long)(4 * c->E));
+  NNT_REQUIRE(tp->ffn % 8 == 0, NNT_ERR_ALIGN, "nnt_block_tp: shard ffn width must be a multiple of 8");
+  NNT_REQUIRE(tp->add_bias == 0 || tp->add_bias == 1, NNT_ERR_ARG, "nnt_block_tp: add_bias must be 0 or 1");
+  return NNT_OK;
+}
+
+// The tensor-parallel stages (nnt.h, nnt_block_tp_*): the ops between two reductions over the
+// shard group, in an order that respects every dependency of the block DAG.
+const int kTpFwd[2][8] = {{NNT_OP_LN1, NNT_OP_QKV, NNT_OP_SCORES, NNT_OP_MAXSUMEXP, NNT_OP_SOFTMAX, NNT_OP_PV,
+                           NNT_OP_OUT, -1},
+                          {NNT_OP_LN2, NNT_OP_FC, NNT_OP_PROJ, -1}};
+const int kTpBwd[3][14] = {{NNT_OP_PROJ_DB, NNT_OP_PROJ_DW, NNT_OP_PROJ_DX, NNT_OP_FC_DB, NNT_OP_FC_DW, NNT_OP_FC_DX,
+                            -1},
+                           {NNT_OP_LN2_BWD, NNT_OP_OUT_DB, NNT_OP_OUT_DW, NNT_OP_OUT_DX, NNT_OP_SOFTMAX_BWD,
+                            NNT_OP_ATT_DP, NNT_OP_SOFTMAX_BWD, NNT_OP_ATT_DV, NNT_OP_ATT_DQ, NNT_OP_ATT_DK,
+                            NNT_OP_QKV_DB, NNT_OP_QKV_DW, NNT_OP_QKV_DX, -1},
+                           {NNT_OP_LN1_BWD, -1}};
+
 }  // namespace
 }  // namespace nnt
 
@@ -353,9 +392,56 @@ extern "C" {
 nnt_status nnt_block_workspace_size(const nnt_block_cfg* cfg, size_t* saved_bytes, size_t* scratch_bytes) {
   NNT_TRY(check_cfg(cfg));
   NNT_REQUIRE(saved_bytes && scratch_bytes, NNT_ERR_NULL, "nnt_block_workspace_size: NULL output");
-  Layout L = make_layout(*cfg);
+  Layout L = make_layout(*cfg, cfg->H, 4 * cfg->E);
   *saved_bytes = L.saved_bytes;
   *scratch_bytes = L.scratch_bytes;
+  return NNT_OK;
+}
+
+nnt_status nnt_block_tp_workspace_size(const nnt_block_cfg* cfg, const nnt_block_tp* tp, size_t* saved_bytes,
+                                      size_t* scratch_bytes) {
+  NNT_TRY(check_tp(cfg, tp));
+  NNT_REQUIRE(saved_bytes && scratch_bytes, NNT_ERR_NULL, "nnt_block_tp_workspace_size: NULL output");
+  Layout L = make_layout(*cfg, tp->heads, tp->ffn);
+  *saved_bytes = L.saved_bytes;
+  *scratch_bytes = L.scratch_bytes;
+  return NNT_OK;
+}
+
+nnt_status nnt_block_tp_fwd(const nnt_block_cfg* cfg, const nnt_block_tp* tp, const nnt_block_params* p, int stage,
+                            const float* x, float* x1, float* y, void* saved, void* scratch, nnt_stream_t stream) {
+  NNT_TRY(check_tp(cfg, tp));
+  NNT_REQUIRE(stage == 0 || stage == 1, NNT_ERR_ARG, "nnt_block_tp_fwd: stage %d", stage);
+  NNT_REQUIRE(p && x && x1 && saved && scratch && (stage == 0 || y), NNT_ERR_NULL, "nnt_block_tp_fwd: NULL argument");
+  Ctx c = make_ctx(*cfg, saved, scratch, stream, tp);
+  c.x1 = x1;
+  const bool bf = cfg->dtype == NNT_BF16;
+  for (const int* op = kTpFwd[stage]; *op >= 0; ++op) {
+    if (*op == NNT_OP_MAXSUMEXP && bf) continue;  // fused into the score GEMM on the bf16 path (R26)
+    NNT_TRY(run_fwd_op(c, *op, p, x, y));
+  }
+  return NNT_OK;
+}
+
+nnt_status nnt_block_tp_bwd(const nnt_block_cfg* cfg, const nnt_block_tp* tp, const nnt_block_params* p, int stage,
+                            const float* x, const float* x1, const void* saved, void* scratch, const float* dy,
+                            float* dh, float* dx, const nnt_block_grads* g, int accumulate_grads,
+                            nnt_stream_t stream) {
+  NNT_TRY(check_tp(cfg, tp));
+  NNT_REQUIRE(stage >= 0 && stage <= 2, NNT_ERR_ARG, "nnt_block_tp_bwd: stage %d", stage);
+  NNT_REQUIRE(p && x && x1 && saved && scratch && dy && dh && g && (stage < 2 || dx), NNT_ERR_NULL,
+              "nnt_block_tp_bwd: NULL argument");
+  Ctx c = make_ctx(*cfg, const_cast<void*>(saved), scratch, stream, tp);
+  c.x1 = const_cast<float*>(x1);
+  c.dh = dh;
+  const bool bf = cfg->dtype == NNT_BF16;
+  bool seen_dp = false;
+  for (const int* op = kTpBwd[stage]; *op >= 0; ++op) {
+    if (*op == NNT_OP_ATT_DP) seen_dp = true;
+    // softmax backward: before the dP GEMM on the bf16 path (D feeds its epilogue), after it on fp32
+    if (*op == NNT_OP_SOFTMAX_BWD && seen_dp == bf) continue;
+    NNT_TRY(run_bwd_op(c, *op, p, x, dy, dx, g, accumulate_grads));
+  }
   return NNT_OK;
 }
 

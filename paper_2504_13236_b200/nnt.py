@@ -46,6 +46,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_gelu_bwd", "nnt_bias_grad_scratch_bytes", "nnt_bias_grad", "nnt_adam_step", "nnt_adam_tick", "nnt_sgd_step",
            "nnt_convert",
            "nnt_scale", "nnt_dot_scratch_bytes", "nnt_dot", "nnt_block_workspace_size", "nnt_block_fwd", "nnt_block_bwd", "nnt_block_bwd_streams",
+           "nnt_block_tp_workspace_size", "nnt_block_tp_fwd", "nnt_block_tp_bwd",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
            "nnt_cross_entropy")
@@ -89,6 +90,10 @@ class nnt_block_grads(C.Structure):
 class nnt_block_bwd_links(C.Structure):
     _fields_ = [("dy_bf16", C.c_void_p), ("dy_colsum_done", C.c_int), ("dx_colsum", C.c_void_p),
                 ("dx_bf16", C.c_void_p)]
+
+
+class nnt_block_tp(C.Structure):
+    _fields_ = [("heads", C.c_int64), ("ffn", C.c_int64), ("add_bias", C.c_int)]
 
 
 class nnt_task(C.Structure):
@@ -144,6 +149,12 @@ _sig = {
     "nnt_block_bwd_streams": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp,
                                      _vp, C.POINTER(nnt_block_grads), _i32, C.POINTER(_vp), _vp, _vp,
                                      C.POINTER(nnt_block_bwd_links)]),
+    "nnt_block_tp_workspace_size": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_tp), C.POINTER(_sz),
+                                           C.POINTER(_sz)]),
+    "nnt_block_tp_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_tp), C.POINTER(nnt_block_params), _i32,
+                                _vp, _vp, _vp, _vp, _vp, _vp]),
+    "nnt_block_tp_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_tp), C.POINTER(nnt_block_params), _i32,
+                                _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(nnt_block_grads), _i32, _vp]),
     "nnt_op_name": (C.c_char_p, [_i32]),
     "nnt_block_dag_describe": (_i32, [C.POINTER(nnt_block_cfg), _i32, C.POINTER(nnt_task), _i64, _P64,
                                       C.POINTER(nnt_launch_group), _i64, _P64]),
@@ -356,6 +367,24 @@ def nnt_block_workspace_size(cfg):
     a, b = C.c_size_t(), C.c_size_t()
     check(lib.nnt_block_workspace_size(C.byref(cfg), C.byref(a), C.byref(b)))
     return a.value, b.value
+
+
+def nnt_block_tp_workspace_size(cfg, tp):
+    a, b = C.c_size_t(), C.c_size_t()
+    check(lib.nnt_block_tp_workspace_size(C.byref(cfg), C.byref(tp), C.byref(a), C.byref(b)))
+    return a.value, b.value
+
+
+def nnt_block_tp_fwd(cfg, tp, params, stage, x, x1, y, saved, scratch, stream=None):
+    return check(lib.nnt_block_tp_fwd(C.byref(cfg), C.byref(tp), C.byref(params), stage, ptr(x), ptr(x1), ptr(y),
+                                      ptr(saved), ptr(scratch), _stream(stream)))
+
+
+def nnt_block_tp_bwd(cfg, tp, params, stage, x, x1, saved, scratch, dy, dh, dx, grads, accumulate_grads,
+                     stream=None):
+    return check(lib.nnt_block_tp_bwd(C.byref(cfg), C.byref(tp), C.byref(params), stage, ptr(x), ptr(x1), ptr(saved),
+                                      ptr(scratch), ptr(dy), ptr(dh), ptr(dx), C.byref(grads), accumulate_grads,
+                                      _stream(stream)))
 
 
 def nnt_block_fwd(cfg, params, x, y, saved, scratch, stream=None):
