@@ -294,7 +294,7 @@ def run_nnt(args):
     dtype = "f32" if args.config == "tiny" else "bf16"
     tile = 16 if args.config == "tiny" else 1024
     sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype,
-                           optimizer=args.optimizer, zero=args.zero)
+                           optimizer=args.optimizer, zero=args.zero, offload=args.offload)
     layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
     b0, b1 = nnt.nnt_partition(B * world, world, rank)  # rank r's batch tiles of the global batch
     batches = []
@@ -474,7 +474,8 @@ def run_nnt(args):
                       "model": f"gpt2-{args.config}" + ("" if mdl == "gpt2" else "-blocks"), "layers": L,
                       "d_model": E, "heads": H, "vocab": VOCAB if mdl == "gpt2" else None,
                       "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}" + ("-zero1" if args.zero and world > 1 else ""),
-                      "optimizer": args.optimizer,
+                      "optimizer": args.optimizer + (" (state offloaded to pinned host memory)" if args.offload
+                                                     else ""),
                       "launch": "one CUDA graph per step" if use_graph else "eager launches",
                       "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
            "model_tflops": model_tflops, "model_tflops_frac_of_bf16": model_tflops / peaks["bf16"],
@@ -514,6 +515,8 @@ def main():
     ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"], help="adam (P:194) or sgd (momentum)")
     ap.add_argument("--zero", action="store_true", help="N>1: ZeRO-1 optimizer-state sharding (reduce-scatter, "
                     "owned-slice update, all-gather) instead of all-reduce + replicated update")
+    ap.add_argument("--offload", action="store_true", help="optimizer state in pinned host memory, streamed "
+                    "through device staging slots around each update (SURVEY f4)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3:

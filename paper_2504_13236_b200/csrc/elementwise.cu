@@ -62,15 +62,18 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
   const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;
   int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const float lr_wd = -hp.lr * hp.weight_decay;
+  // explicit roundings / FMAs: the vector and scalar loops (and any alignment of a range)
+  // give bitwise the same update
   auto upd = [&](float& wi, float gi, float& mi, float& vi) {
-    gi *= hp.grad_scale;
-    mi = b1 * mi + c1 * gi;
-    vi = b2 * vi + c2 * gi * gi;
-    float mhat = mi * inv_bc1;
-    float vhat = vi * inv_bc2;
-    float wold = wi;
-    wi = wi - hp.lr * mhat / (sqrtf(vhat) + hp.eps);
-    if (hp.weight_decay != 0.f) wi -= hp.lr * hp.weight_decay * wold;
+    gi = __fmul_rn(gi, hp.grad_scale);
+    mi = fmaf(b1, mi, __fmul_rn(c1, gi));
+    vi = fmaf(b2, vi, __fmul_rn(__fmul_rn(c2, gi), gi));
+    const float mhat = __fmul_rn(mi, inv_bc1);
+    const float vhat = __fmul_rn(vi, inv_bc2);
+    const float wold = wi;
+    wi = __fsub_rn(wi, __fdiv_rn(__fmul_rn(hp.lr, mhat), __fadd_rn(sqrtf(vhat), hp.eps)));
+    if (hp.weight_decay != 0.f) wi = fmaf(lr_wd, wold, wi);
   };
   int64_t nv = vec_ok ? n / 4 : 0;
   for (int64_t i = tid; i < nv; i += stride) {

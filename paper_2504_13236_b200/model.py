@@ -24,7 +24,7 @@ from dataclasses import dataclass
 
 import torch
 
-from . import nnt
+from . import nnt, offload
 
 # (parameter, set) in flat-buffer order inside one layer
 SETS = (("w_pr", "b_pr"), ("w_fc", "b_fc", "ln2_g", "ln2_b"), ("w_o", "b_o"), ("w_qkv", "b_qkv", "ln1_g", "ln1_b"))
@@ -92,6 +92,17 @@ def zero1_bucket(g, w, b0, b1, s0, s1, group, update):
     torch.distributed.all_gather_into_tensor(w[b0:b1], w[s0:s1], group=group)
 
 
+def _update_kernel(o, b0, b1, m, v, t, stream, shadow):
+    """The optimizer kernel on parameters [b0, b1) of owner o (BlockStack / GPT2Model) with the
+    state views m, v (device memory: resident, or an offload staging slot)."""
+    c, n = o.cfg, b1 - b0
+    w16 = o.w16[b0:b1] if (o.bf16 and shadow) else None
+    if c.optimizer == "sgd":  # the momentum buffer lives in m
+        nnt.nnt_sgd_step(n, o.w[b0:b1], o.g[b0:b1], m, w16, c.lr, c.momentum, c.weight_decay, stream=stream)
+        return
+    nnt.nnt_adam_step(n, o.w[b0:b1], o.g[b0:b1], m, v, w16, o._hp(t), stream=stream)
+
+
 @dataclass
 class StackConfig:
     L: int
@@ -116,6 +127,9 @@ class StackConfig:
     # DP only: ZeRO-1 -- gradients reduce-scattered by bucket slice, optimizer
     # state for the owned slices only (1/world of m, v), updated parameters all-gathered
     zero: bool = False
+    # optimizer state (Adam m, v / SGD momentum) in pinned host memory, streamed through device
+    # staging slots by the copy engines around each update (offload.py)
+    offload: bool = False
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
 
@@ -153,8 +167,13 @@ class BlockStack:
         nstate = off
         if self.zero:
             self.shards, nstate = zero_shards(self.buckets, self.world, torch.distributed.get_rank(process_group))
-        self.m = torch.zeros(nstate, **f32)
-        self.v = torch.zeros(nstate, **f32)
+        self.host_state = None
+        if cfg.offload:
+            self.host_state = offload.HostOptimizerState(nstate, self.dev, two_moments=cfg.optimizer != "sgd")
+            self.m, self.v = self.host_state.m, self.host_state.v
+        else:
+            self.m = torch.zeros(nstate, **f32)
+            self.v = torch.zeros(nstate, **f32)
         self.bf16 = cfg.dtype == "bf16"
         self.w16 = torch.zeros(off, device=self.dev, dtype=torch.bfloat16) if self.bf16 else None
         for l, P in enumerate(layer_params):
@@ -303,15 +322,15 @@ class BlockStack:
 
     def _update(self, b0, b1, c0, t, stream, shadow):
         """Optimizer step on parameters [b0, b1) with state at [c0, c0 + b1 - b0) of m / v."""
-        c, n = self.cfg, b1 - b0
-        w16 = self.w16[b0:b1] if (self.bf16 and shadow) else None
-        if c.optimizer == "sgd":  # the momentum buffer lives in m
-            nnt.nnt_sgd_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], w16, c.lr, c.momentum,
-                             c.weight_decay, stream=stream)
+        if self.host_state is not None:
+            self.host_state.apply([(c0, c0 + b1 - b0)],
+                                  lambda a, b, m, v: _update_kernel(self, b0 + a - c0, b0 + b - c0, m, v, t, stream,
+                                                                    shadow), stream)
             return
-        hp = self._graph_hp if self._graph_hp is not None else self._hparams(t)
-        nnt.nnt_adam_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], self.v[c0:c0 + n], w16, hp,
-                          stream=stream)
+        _update_kernel(self, b0, b1, self.m[c0:c0 + b1 - b0], self.v[c0:c0 + b1 - b0], t, stream, shadow)
+
+    def _hp(self, t):
+        return self._graph_hp if self._graph_hp is not None else self._hparams(t)
 
     def adam(self):
         """Adam over every parameter (one launch over the flat buffer); bias corrections in fp64 on host."""
@@ -444,7 +463,12 @@ class GPT2Model:
         if st.zero:  # the shell is one more bucket
             self.shard, nstate = zero_shards([(0, n)], st.world, torch.distributed.get_rank(st.pg))
             self.shard = self.shard[0]
-        self.m, self.v = torch.zeros(nstate, **f32), torch.zeros(nstate, **f32)
+        self.host_state = None
+        if cfg.offload:
+            self.host_state = offload.HostOptimizerState(nstate, self.dev, two_moments=cfg.optimizer != "sgd")
+            self.m, self.v = self.host_state.m, self.host_state.v
+        else:
+            self.m, self.v = torch.zeros(nstate, **f32), torch.zeros(nstate, **f32)
         for name, (o, k) in self.offsets.items():
             self.w[o:o + k].copy_(torch.as_tensor(shell_params[name], dtype=torch.float32).reshape(-1).to(self.dev))
         self.numel = n
@@ -548,16 +572,10 @@ class GPT2Model:
     def _adam(self, t, stream=None):
         self._update(0, self.numel, 0, t, stream, shadow=True)
 
-    def _update(self, b0, b1, c0, t, stream, shadow):
-        c, n = self.cfg, b1 - b0
-        w16 = self.w16[b0:b1] if (self.bf16 and shadow) else None
-        if c.optimizer == "sgd":
-            nnt.nnt_sgd_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], w16, c.lr, c.momentum,
-                             c.weight_decay, stream=stream)
-            return
-        hp = self.stack._graph_hp if self.stack._graph_hp is not None else self.stack._hparams(t)
-        nnt.nnt_adam_step(n, self.w[b0:b1], self.g[b0:b1], self.m[c0:c0 + n], self.v[c0:c0 + n], w16, hp,
-                          stream=stream)
+    def _hp(self, t):
+        return self.stack._hp(t)
+
+    _update = BlockStack._update
 
     def adam(self):
         self.stack.adam()
