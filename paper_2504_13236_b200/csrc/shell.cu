@@ -9,10 +9,15 @@
 //                      positions by id (integer histogram, one-CTA exclusive scan, stable rank
 //                      = number of earlier tokens with the same id), then one warp per
 //                      vocabulary row sums its bucket in token order
-//   nnt_cross_entropy  per row: subroutine 1 (per-thread running (max, sumexp) over its
-//                      16-byte vocabulary tiles, merged in fixed order, R10) then loss =
+//   nnt_cross_entropy  per row: subroutine 1 (the row's (max, sumexp), R10) then loss =
 //                      log S + M - x[label] and, fused with subroutine 2, the gradient
-//                      scale * (e^{x - M} / S - onehot(label)) written over the logits
+//                      scale * (e^{x - M} / S - onehot(label)) written over the logits.
+//                      bf16 rows up to 104 KB: persistent CTAs, rows double-buffered in shared
+//                      memory by cp.async.bulk (logits read from HBM once, written once);
+//                      rows up to 200 KB: one CTA per row staged in shared memory; longer rows:
+//                      the re-reading kernel (per-thread running (max, sumexp), fixed-order merge)
+#include <cstdlib>
+
 #include "nnt_internal.h"
 
 namespace nnt {
@@ -279,6 +284,236 @@ __global__ void __launch_bounds__(kT) cross_entropy_kernel(const T* logits, int6
     d[k] = from_f32<T>(__expf(to_f32(x[k]) - M) * inv - (k == c ? scale : 0.f));
 }
 
+// Row-staged variant (the product path for bf16 logits): one CTA per row copies the row's full
+// 16-byte vectors into shared memory once while taking the row maximum, so the logits are read
+// from HBM exactly once and written once (the re-reading kernel above touches them twice).
+//   pass A  global -> smem, per-thread max, block max M (fixed xor-tree order)
+//   pass B  S = sum_k e^{x_k - M} from smem (per-thread in vector order, then the fixed tree)
+//   pass C  smem -> global: scale * (e^{x - M} / S - onehot(label))
+// Subroutine 1's (max, sumexp) is thus taken as max first, then the sum relative to it — the
+// same pair the running merge of R10 produces, with one exponential per element per pass.
+constexpr int kCeT = 512;
+constexpr size_t kCeSmemMax = 200 * 1024;
+constexpr float kLog2e = 1.4426950408889634f;
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <bool kMax, int NT = kCeT>
+__device__ __forceinline__ float ce_block_reduce(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, w) : v + w;
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  v = lane < NT / 32 ? red[lane] : (kMax ? -INFINITY : 0.f);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = kMax ? fmaxf(v, w) : v + w;
+  }
+  __syncthreads();  // red[] is reused by the next reduction
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCeT, 2)
+    cross_entropy_staged_kernel(const T* logits, int64_t rows, int64_t V, int64_t ld,
+                                const int32_t* __restrict__ labels, float scale, float* __restrict__ loss_rows,
+                                float* __restrict__ stats, T* dlogits, int64_t ld_d) {
+  NNT_PDL_ENTRY();
+  extern __shared__ __align__(16) unsigned char ce_smem[];
+  T* row = reinterpret_cast<T*>(ce_smem);
+  __shared__ float red[kCeT / 32];
+  __shared__ float tail[8];
+  __shared__ float xlabel;
+  const int64_t r = blockIdx.x;
+  const T* x = logits + r * ld;
+  const int nv = (int)(V / 8), ntail = (int)(V - 8 * (int64_t)nv);
+  int64_t c = labels[r];
+  c = c < 0 ? 0 : (c >= V ? V - 1 : c);
+  // pass A: stage the row, running max (4 vectors in flight per thread)
+  float m = -INFINITY;
+  int i = threadIdx.x;
+  for (; i + 3 * kCeT < nv; i += 4 * kCeT) {
+    float f[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) load8<T>(x + 8 * (int64_t)(i + u * kCeT), f[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      store8<T>(row + 8 * (i + u * kCeT), f[u]);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m = fmaxf(m, f[u][k]);
+    }
+  }
+  for (; i < nv; i += kCeT) {
+    float f[8];
+    load8<T>(x + 8 * (int64_t)i, f);
+    store8<T>(row + 8 * i, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m = fmaxf(m, f[k]);
+  }
+  if (threadIdx.x < ntail) {
+    const float t = to_f32(x[8 * (int64_t)nv + threadIdx.x]);
+    tail[threadIdx.x] = t;
+    m = fmaxf(m, t);
+  }
+  if (threadIdx.x == 0) xlabel = to_f32(x[c]);
+  const float M = ce_block_reduce<true>(m, red);  // its barriers also publish row[], tail[], xlabel
+  const float ML = M * kLog2e;
+  // pass B: S = sum e^{x - M}
+  float s = 0.f;
+  for (int j = threadIdx.x; j < nv; j += kCeT) {
+    float f[8];
+    load8<T>(row + 8 * j, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += ex2f(fmaf(f[k], kLog2e, -ML));
+  }
+  if (threadIdx.x < ntail) s += ex2f(fmaf(tail[threadIdx.x], kLog2e, -ML));
+  const float S = ce_block_reduce<false>(s, red);
+  if (threadIdx.x == 0) {
+    if (loss_rows) loss_rows[r] = logf(S) + M - xlabel;
+    if (stats) {
+      stats[2 * r] = M;
+      stats[2 * r + 1] = S;
+    }
+  }
+  if (dlogits == nullptr) return;
+  // pass C: subroutine 2 fused with the gradient, written over the logits when they alias
+  const float inv = scale / S;
+  T* d = dlogits + r * ld_d;
+  for (int j = threadIdx.x; j < nv; j += kCeT) {
+    float f[8];
+    load8<T>(row + 8 * j, f);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) f[k] = ex2f(fmaf(f[k], kLog2e, -ML)) * inv - (8 * j + k == c ? scale : 0.f);
+    store8<T>(d + 8 * (int64_t)j, f);
+  }
+  if (threadIdx.x < ntail) {
+    const int64_t k = 8 * (int64_t)nv + threadIdx.x;
+    d[k] = from_f32<T>(ex2f(fmaf(tail[threadIdx.x], kLog2e, -ML)) * inv - (k == c ? scale : 0.f));
+  }
+}
+
+// Persistent, double-buffered variant (bf16 GPT-2 vocabulary: 2 x 100.5 KB rows per SM): one
+// CTA per SM walks rows r = blockIdx.x + k * gridDim.x; while it runs the three passes over row
+// k from shared memory, a bulk async copy (cp.async.bulk, completion on an mbarrier) brings row
+// k + 1 into the other buffer, so the HBM read stream never waits for the exponentials.
+// Same arithmetic as cross_entropy_staged_kernel, pass A reading the staged row.
+constexpr int kCePT = 1024;
+constexpr uint32_t kCeChunk = 32768;
+
+__device__ __forceinline__ uint32_t ce_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void ce_mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// one thread: expect `bytes` on `bar`, then copy them global -> shared in kCeChunk pieces
+__device__ __forceinline__ void ce_fetch_row(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of dst first
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  for (uint32_t o = 0; o < bytes; o += kCeChunk) {
+    const uint32_t n = bytes - o < kCeChunk ? bytes - o : kCeChunk;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(dst + o), "l"(reinterpret_cast<const char*>(src) + o), "r"(n), "r"(bar)
+                 : "memory");
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kCePT, 1)
+    cross_entropy_pipe_kernel(const T* logits, int64_t rows, int64_t V, int64_t ld,
+                              const int32_t* __restrict__ labels, float scale, float* __restrict__ loss_rows,
+                              float* __restrict__ stats, T* dlogits, int64_t ld_d) {
+  NNT_PDL_ENTRY();
+  extern __shared__ __align__(128) unsigned char ce_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  __shared__ float red[kCePT / 32];
+  const int nv = (int)(V / 8), ntail = (int)(V - 8 * (int64_t)nv);
+  const uint32_t row_bytes = (uint32_t)nv * 8u * (uint32_t)sizeof(T);
+  const uint32_t buf0 = ce_smem_u32(ce_smem);
+  const uint32_t bar0 = ce_smem_u32(&bar[0]), bar1 = ce_smem_u32(&bar[1]);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar0) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (row_bytes && (int64_t)blockIdx.x < rows)
+      ce_fetch_row(buf0, logits + (int64_t)blockIdx.x * ld, row_bytes, bar0);
+  }
+  __syncthreads();
+  int k = 0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x, ++k) {
+    const int b = k & 1;
+    // every thread is past row k-1's pass C (its last read of buf[b^1]): refill that buffer
+    if (threadIdx.x == 0 && row_bytes && r + gridDim.x < rows)
+      ce_fetch_row(buf0 + (uint32_t)(b ^ 1) * row_bytes, logits + (r + gridDim.x) * ld, row_bytes, b ? bar0 : bar1);
+    const T* x = logits + r * ld;
+    int64_t c = labels[r];
+    c = c < 0 ? 0 : (c >= V ? V - 1 : c);
+    const float xc = to_f32(x[c]);  // read before this row's pass C may overwrite it
+    const float xt = threadIdx.x < ntail ? to_f32(x[8 * (int64_t)nv + threadIdx.x]) : -INFINITY;
+    if (row_bytes) ce_mbar_wait(b ? bar1 : bar0, (uint32_t)(k >> 1) & 1u);
+    const T* row = reinterpret_cast<const T*>(ce_smem + (size_t)b * row_bytes);
+    // pass A: max
+    float m = xt;
+    for (int j = threadIdx.x; j < nv; j += kCePT) {
+      float f[8];
+      load8<T>(row + 8 * j, f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) m = fmaxf(m, f[q]);
+    }
+    const float M = ce_block_reduce<true, kCePT>(m, red);
+    const float ML = M * kLog2e;
+    // pass B: S = sum e^{x - M}
+    float sum = threadIdx.x < ntail ? ex2f(fmaf(xt, kLog2e, -ML)) : 0.f;
+    for (int j = threadIdx.x; j < nv; j += kCePT) {
+      float f[8];
+      load8<T>(row + 8 * j, f);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) sum += ex2f(fmaf(f[q], kLog2e, -ML));
+    }
+    const float S = ce_block_reduce<false, kCePT>(sum, red);
+    if (threadIdx.x == 0) {
+      if (loss_rows) loss_rows[r] = logf(S) + M - xc;
+      if (stats) {
+        stats[2 * r] = M;
+        stats[2 * r + 1] = S;
+      }
+    }
+    if (dlogits != nullptr) {
+      // pass C: subroutine 2 fused with the gradient
+      const float inv = scale / S;
+      T* d = dlogits + r * ld_d;
+      for (int j = threadIdx.x; j < nv; j += kCePT) {
+        float f[8];
+        load8<T>(row + 8 * j, f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) f[q] = ex2f(fmaf(f[q], kLog2e, -ML)) * inv - (8 * j + q == c ? scale : 0.f);
+        store8<T>(d + 8 * (int64_t)j, f);
+      }
+      if (threadIdx.x < ntail) {
+        const int64_t q = 8 * (int64_t)nv + threadIdx.x;
+        d[q] = from_f32<T>(ex2f(fmaf(xt, kLog2e, -ML)) * inv - (q == c ? scale : 0.f));
+      }
+    }
+    __syncthreads();  // buf[b] is refilled at the top of iteration k + 1
+  }
+}
+
 inline int grid_cap(int64_t items, int per_cta) {
   int64_t g = (items + per_cta - 1) / per_cta;
   const int64_t cap = 8LL * num_sms();
@@ -361,8 +596,51 @@ nnt_status nnt_cross_entropy(const void* logits, int dtype, int64_t rows, int64_
   const size_t es = dtype_size(dtype);
   NNT_REQUIRE(aligned16(logits) && (ld * es) % 16 == 0 && (!dlogits || (aligned16(dlogits) && (ld_d * es) % 16 == 0)),
               NNT_ERR_ALIGN, "nnt_cross_entropy: 16-byte aligned rows required");
-  LaunchScope sc(NNT_K_SOFTMAX, stream, (double)rows * V * es * (dlogits ? 3.0 : 1.0) + 16.0 * rows, 0);
+  // algorithmic bytes: the logits read once, the gradient written once (whatever the kernel re-reads)
+  LaunchScope sc(NNT_K_SOFTMAX, stream, (double)rows * V * es * (dlogits ? 2.0 : 1.0) + 16.0 * rows, 0);
   cudaStream_t s = (cudaStream_t)stream;
+  const size_t row_bytes = (size_t)(V / 8) * 8 * es;
+  static const bool restream = [] {  // NNT_CE_RESTREAM=1: the two-read kernel (A/B runs)
+    const char* e = getenv("NNT_CE_RESTREAM");
+    return e && e[0] == '1';
+  }();
+  if (2 * row_bytes <= kCeSmemMax + 8192 && dtype == NNT_BF16 && !restream) {
+    static const bool attr = [] {
+      cudaFuncSetAttribute(cross_entropy_pipe_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(kCeSmemMax + 8192));
+      return true;
+    }();
+    (void)attr;
+    const int64_t grid = rows < num_sms() ? rows : num_sms();
+    NNT_CUDA_TRY(::nnt::launch(cross_entropy_pipe_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kCePT),
+                               2 * row_bytes, s, (const __nv_bfloat16*)logits, rows, V, ld, labels, scale, loss_rows,
+                               stats, (__nv_bfloat16*)dlogits, ld_d));
+    return NNT_OK;
+  }
+  if (row_bytes <= kCeSmemMax && !restream) {
+    if (dtype == NNT_BF16) {
+      static const bool attr = [] {
+        cudaFuncSetAttribute(cross_entropy_staged_kernel<__nv_bfloat16>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCeSmemMax);
+        return true;
+      }();
+      (void)attr;
+      NNT_CUDA_TRY(::nnt::launch(cross_entropy_staged_kernel<__nv_bfloat16>, dim3((unsigned)rows), dim3(kCeT),
+                                 row_bytes, s, (const __nv_bfloat16*)logits, rows, V, ld, labels, scale, loss_rows,
+                                 stats, (__nv_bfloat16*)dlogits, ld_d));
+    } else {
+      static const bool attr = [] {
+        cudaFuncSetAttribute(cross_entropy_staged_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)kCeSmemMax);
+        return true;
+      }();
+      (void)attr;
+      NNT_CUDA_TRY(::nnt::launch(cross_entropy_staged_kernel<float>, dim3((unsigned)rows), dim3(kCeT), row_bytes, s,
+                                 (const float*)logits, rows, V, ld, labels, scale, loss_rows, stats, (float*)dlogits,
+                                 ld_d));
+    }
+    return NNT_OK;
+  }
   if (dtype == NNT_BF16)
     NNT_CUDA_TRY(::nnt::launch(cross_entropy_kernel<__nv_bfloat16>, dim3((unsigned)rows), dim3(kT), 0, s,
                                (const __nv_bfloat16*)logits, rows, V, ld, labels, scale, loss_rows, stats,

@@ -45,7 +45,7 @@ def test_embedding_fwd_bit_exact_and_bwd():
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
-@pytest.mark.parametrize("rows,V", [(37, 1000), (8, 50257)])
+@pytest.mark.parametrize("rows,V", [(37, 1000), (8, 50257), (333, 50257), (301, 4103), (5, 7)])
 def test_cross_entropy_kernel(dt, rows, V):
     rng = np.random.default_rng(2)
     Vp = -(-V // 8) * 8
