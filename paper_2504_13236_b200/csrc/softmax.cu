@@ -194,6 +194,35 @@ __global__ void __launch_bounds__(kThreads) attn_rowdot_kernel(const T* __restri
   D[(b * H + n) * S + s] = acc;
 }
 
+// Lane-cooperative form: L lanes per (token, head) row, one 16-byte vector each (h = L x 16 B),
+// so every warp load instruction reads 32 / L whole rows contiguously; the L partial dot
+// products are combined by an xor tree (fixed order).  Used whenever h x sizeof(T) / 16 is a
+// power of two <= 32 (GPT-2: h = 64 bf16 -> L = 8); otherwise the thread-per-row kernel above.
+template <typename T, int L>
+__global__ void __launch_bounds__(kThreads) attn_rowdot_lanes_kernel(const T* __restrict__ dO,
+                                                                     const T* __restrict__ O, int64_t B, int64_t S,
+                                                                     int64_t H, float* __restrict__ D) {
+  NNT_PDL_ENTRY();
+  constexpr int V = 16 / sizeof(T);
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t idx = t / L;  // ((b*S + s)*H + n); rows are h = L*V elements, contiguous
+  const int part = (int)(t % L);
+  float acc = 0.f;
+  if (idx < B * S * H) {
+    const uint4 ua = __ldg(reinterpret_cast<const uint4*>(dO) + t), uo = __ldg(reinterpret_cast<const uint4*>(O) + t);
+    const T* ea = reinterpret_cast<const T*>(&ua);
+    const T* eo = reinterpret_cast<const T*>(&uo);
+#pragma unroll
+    for (int j = 0; j < V; ++j) acc = fmaf(to_f32(ea[j]), to_f32(eo[j]), acc);
+  }
+#pragma unroll
+  for (int o = L / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (part == 0 && idx < B * S * H) {
+    const int64_t n = idx % H, bs = idx / H, b = bs / S, s = bs % S;
+    D[(b * H + n) * S + s] = acc;
+  }
+}
+
 // ------------------------------------------------------------------ subroutine 2
 template <typename TO>
 __global__ void __launch_bounds__(kThreads) softmax_kernel(const float* __restrict__ x, int64_t rows, int64_t cols,
@@ -322,6 +351,22 @@ nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, 
   NNT_REQUIRE(aligned16(dO) && aligned16(O), NNT_ERR_ALIGN, "nnt_attn_rowdot: pointers must be 16-byte aligned");
   const int64_t n = B * S * H;
   LaunchScope sc(NNT_K_MISC, stream, 2.0 * dtype_size(dtype) * n * h + 4.0 * n, 2.0 * n * h);
+  const int64_t lanes = (h * (int64_t)dtype_size(dtype)) % 16 == 0 ? h * (int64_t)dtype_size(dtype) / 16 : 0;
+  if (lanes == 2 || lanes == 4 || lanes == 8 || lanes == 16 || lanes == 32) {
+    const unsigned g = (unsigned)((n * lanes + kThreads - 1) / kThreads);
+#define NNT_RDL(T, LN)                                                                                         \
+  case LN:                                                                                                     \
+    ::nnt::launch(attn_rowdot_lanes_kernel<T, LN>, g, kThreads, 0, stream, (const T*)dO, (const T*)O, B, S, H, D); \
+    break;
+    if (dtype == NNT_BF16) {
+      switch (lanes) { NNT_RDL(__nv_bfloat16, 2) NNT_RDL(__nv_bfloat16, 4) NNT_RDL(__nv_bfloat16, 8)
+                       NNT_RDL(__nv_bfloat16, 16) NNT_RDL(__nv_bfloat16, 32) }
+    } else {
+      switch (lanes) { NNT_RDL(float, 2) NNT_RDL(float, 4) NNT_RDL(float, 8) NNT_RDL(float, 16) NNT_RDL(float, 32) }
+    }
+#undef NNT_RDL
+    return check_launch("attn_rowdot");
+  }
   const unsigned grid = (unsigned)((n + kThreads - 1) / kThreads);
   if (dtype == NNT_BF16)
     ::nnt::launch(attn_rowdot_kernel<__nv_bfloat16>, grid, kThreads, 0, stream, (const __nv_bfloat16*)dO,

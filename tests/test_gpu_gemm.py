@@ -325,6 +325,23 @@ def test_fused_softmax_bwd_gemm_and_rowdot():
     assert rel(np.where(mask, got, 0.0), want) < 2e-2
 
 
+@pytest.mark.parametrize("dt,h", [("bf16", 64), ("bf16", 8), ("bf16", 16), ("bf16", 256), ("bf16", 24),
+                                  ("f32", 64), ("f32", 12), ("f32", 128)])
+def test_attn_rowdot_head_dims(dt, h):
+    """D[b, n, s] = sum_i dO[b, s, n, i] O[b, s, n, i] (R18's row-dot identity) for head dims that
+    take the lane-cooperative kernel (h x 2 B / 16 a power of two) and the thread-per-row one."""
+    B, S, H = 2, 77, 5
+    rng = np.random.default_rng(72 + h)
+    do = bf16_round(rng.standard_normal((B, S, H, h)))
+    o = bf16_round(rng.standard_normal((B, S, H, h)))
+    tdt, code = DT[dt]
+    D = torch.full((B * H * S,), float("nan"), device="cuda")
+    nnt.nnt_attn_rowdot(dev(do, tdt), dev(o, tdt), code, B, S, H, h, D)
+    torch.cuda.synchronize()
+    want = (do * o).sum(-1).transpose(0, 2, 1)  # [B, H, S]
+    assert rel(host(D).reshape(B, H, S), want) < 1e-6
+
+
 def test_gemm_rejects_bad_arguments():
     A = torch.zeros(64, 64, device="cuda", dtype=torch.bfloat16)
     with pytest.raises(nnt.NNTError) as e:  # misaligned leading dimension for TMA
