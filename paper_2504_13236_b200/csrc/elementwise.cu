@@ -277,13 +277,15 @@ __global__ void __launch_bounds__(kThreads) dot_partial_kernel(const float* __re
   }
 }
 
+// one warp: lane l sums partials l, l + 32, ... in order, then a fixed xor tree (was one thread
+// walking all 2 x 148 partials: a dependent chain of loads and fp64 adds, ~15 us)
 __global__ void dot_merge_kernel(const double* __restrict__ partial, int n, float scale, float* out) {
   NNT_PDL_ENTRY();
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < n; ++i) t += partial[i];
-    out[0] = (float)(t * (double)scale);
-  }
+  double t = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) t += partial[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) out[0] = (float)(t * (double)scale);
 }
 
 }  // namespace

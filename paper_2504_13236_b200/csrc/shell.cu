@@ -392,9 +392,11 @@ __global__ void __launch_bounds__(kCeT, 2)
     float f[8];
     load8<T>(row + 8 * j, f);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) f[k] = ex2f(fmaf(f[k], kLog2e, -ML)) * inv - (8 * j + k == c ? scale : 0.f);
+    for (int k = 0; k < 8; ++k) f[k] = ex2f(fmaf(f[k], kLog2e, -ML)) * inv;
     store8<T>(d + 8 * (int64_t)j, f);
   }
+  if (c < 8 * (int64_t)nv && threadIdx.x == (int)((c >> 3) % kCeT))  // - onehot(label), same thread
+    d[c] = from_f32<T>(ex2f(fmaf(xlabel, kLog2e, -ML)) * inv - scale);
   if (threadIdx.x < ntail) {
     const int64_t k = 8 * (int64_t)nv + threadIdx.x;
     d[k] = from_f32<T>(ex2f(fmaf(tail[threadIdx.x], kLog2e, -ML)) * inv - (k == c ? scale : 0.f));
@@ -502,9 +504,12 @@ __global__ void __launch_bounds__(kCePT, 1)
         float f[8];
         load8<T>(row + 8 * j, f);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) f[q] = ex2f(fmaf(f[q], kLog2e, -ML)) * inv - (8 * j + q == c ? scale : 0.f);
+        for (int q = 0; q < 8; ++q) f[q] = ex2f(fmaf(f[q], kLog2e, -ML)) * inv;
         store8<T>(d + 8 * (int64_t)j, f);
       }
+      // - onehot(label): the thread that stored the label's vector rewrites that one element
+      if (c < 8 * (int64_t)nv && threadIdx.x == (int)((c >> 3) % kCePT))
+        d[c] = from_f32<T>(ex2f(fmaf(xc, kLog2e, -ML)) * inv - scale);
       if (threadIdx.x < ntail) {
         const int64_t q = 8 * (int64_t)nv + threadIdx.x;
         d[q] = from_f32<T>(ex2f(fmaf(xt, kLog2e, -ML)) * inv - (q == c ? scale : 0.f));
