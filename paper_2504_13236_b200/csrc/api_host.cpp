@@ -35,8 +35,10 @@ int num_sms() {
 
 bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = getenv("NNT_PDL");  // off by default: measured slower on the GPT-2 step
-    return e && e[0] == '1';
+    // on by default since the early trigger moved to the GEMM's last operand load (interleaved
+    // A/B: 11.71 -> 11.64 ms/step); NNT_PDL=0 launches without the attribute
+    const char* e = getenv("NNT_PDL");
+    return !(e && e[0] == '0');
   }();
   return on;
 }

@@ -868,6 +868,10 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           }
         }
       }
+      // every operand load of this CTA is issued: with PDL the next kernel on the stream may be
+      // scheduled now (its CTAs wait in griddepcontrol.wait until this grid completes), hiding its
+      // launch behind this CTA's last MMAs and epilogue
+      pdl_trigger();
     }
   } else if (warp == 1) {
     // ===================== MMA issuer (CTA pair: the leader only)

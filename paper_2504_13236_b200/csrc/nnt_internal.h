@@ -78,7 +78,7 @@ int num_sms();
 // (smem carve-up, barrier init, TMEM allocation) and then block in griddepcontrol.wait until
 // the previous grid has completed and its writes are visible (NNT_PDL_ENTRY at the top of
 // every kernel).  Inside a CUDA graph this becomes a programmatic edge, hiding the per-kernel
-// launch gap of the ~450-launch training step.  Enabled by NNT_PDL=1 in the environment.
+// launch gap of the ~430-launch training step.  On by default; NNT_PDL=0 disables it.
 bool pdl_enabled();
 
 #if defined(__CUDACC__)
@@ -103,12 +103,12 @@ inline cudaError_t launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_
 // ---------------------------------------------------------------- PDL (see launch())
 // Wait until the previous grid on the stream has completed (its memory visible), then allow
 // the next grid to be scheduled.  A no-op when the kernel was launched without PDL.
-__device__ __forceinline__ void pdl_entry() {
-  asm volatile("griddepcontrol.wait;" ::: "memory");
-#ifndef NNT_PDL_NO_TRIGGER
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
-}
+// The early trigger is issued only where a kernel knows its remaining work is a tail (the
+// persistent GEMM once its last operand load is issued, pdl_trigger); elsewhere the dependents
+// are released as the CTAs exit.  (Triggering at every kernel's entry let dependent CTAs take
+// SM slots from the still-running grid: measured slower.)
+__device__ __forceinline__ void pdl_entry() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 #define NNT_PDL_ENTRY() ::nnt::pdl_entry()
 
 // ---------------------------------------------------------------- device math
