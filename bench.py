@@ -420,8 +420,12 @@ def run_nnt(args):
     t0 = time.perf_counter()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record()
+    reader = model.LossReader(2)  # each step's loss read back one step later (pipelined D2H)
     for i in range(args.steps):
-        lv = runner.step(batches[i % 2]).item()
+        reader.push(runner.step(batches[i % 2]))
+        if i:
+            lv = reader.pop()
+    lv = reader.pop()
     f1.record()
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(max(f0.elapsed_time(f1), 1000 * (time.perf_counter() - t0)) / args.steps)

@@ -103,6 +103,35 @@ def _update_kernel(o, b0, b1, m, v, t, stream, shadow):
     nnt.nnt_adam_step(n, o.w[b0:b1], o.g[b0:b1], m, v, w16, o._hp(t), stream=stream)
 
 
+class LossReader:
+    """Pipelined device -> host reads of the per-step loss (what a training loop logs).
+
+    push(loss) enqueues an asynchronous copy of this step's device loss into a pinned host slot
+    and records an event on the current stream; pop() waits for the oldest pending copy and
+    returns its value.  Reading step i's loss after step i+1 has been enqueued keeps the host
+    from stalling the stream between steps; every step's loss is still read back."""
+
+    def __init__(self, depth=2):
+        self.buf = torch.empty(depth, dtype=torch.float32, pin_memory=True)
+        self.ev = [torch.cuda.Event() for _ in range(depth)]
+        self.pending = []
+        self.n = 0
+
+    def push(self, loss):
+        if len(self.pending) == len(self.ev):
+            raise RuntimeError("LossReader: pop() before pushing more than `depth` losses")
+        slot = self.n % len(self.ev)
+        self.n += 1
+        self.buf[slot:slot + 1].copy_(loss.reshape(1).float(), non_blocking=True)
+        self.ev[slot].record()
+        self.pending.append(slot)
+
+    def pop(self):
+        slot = self.pending.pop(0)
+        self.ev[slot].synchronize()
+        return float(self.buf[slot])
+
+
 @dataclass
 class StackConfig:
     L: int
