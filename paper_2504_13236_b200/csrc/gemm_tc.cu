@@ -1381,6 +1381,45 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const float* __restr
       rowsum[i] = beta != 0.f ? fmaf(beta, rowsum[i], s) : s;
     }
   }
+  if (ldc == N && (!residual || ld_res == N) && !bias) {
+    // dense C (the dW GEMMs): flat float4 index, two independent elements per thread in flight
+    const float4* w4 = reinterpret_cast<const float4*>(ws);
+    float4* c4 = reinterpret_cast<float4*>(C);
+    const float4* r4 = reinterpret_cast<const float4*>(residual);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += 2 * stride) {
+      const int64_t j = i + stride;
+      const bool two = j < total;
+      float4 s0 = __ldcg(w4 + i), s1 = two ? __ldcg(w4 + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int64_t k = 1; k < splits; ++k) {
+        const float4 t0 = __ldcg(w4 + k * total + i);
+        s0.x += t0.x; s0.y += t0.y; s0.z += t0.z; s0.w += t0.w;
+        if (two) {
+          const float4 t1 = __ldcg(w4 + k * total + j);
+          s1.x += t1.x; s1.y += t1.y; s1.z += t1.z; s1.w += t1.w;
+        }
+      }
+      if (beta != 0.f) {
+        const float4 o0 = c4[i];
+        s0.x += beta * o0.x; s0.y += beta * o0.y; s0.z += beta * o0.z; s0.w += beta * o0.w;
+        if (two) {
+          const float4 o1 = c4[j];
+          s1.x += beta * o1.x; s1.y += beta * o1.y; s1.z += beta * o1.z; s1.w += beta * o1.w;
+        }
+      }
+      if (residual) {
+        const float4 o0 = r4[i];
+        s0.x += o0.x; s0.y += o0.y; s0.z += o0.z; s0.w += o0.w;
+        if (two) {
+          const float4 o1 = r4[j];
+          s1.x += o1.x; s1.y += o1.y; s1.z += o1.z; s1.w += o1.w;
+        }
+      }
+      c4[i] = s0;
+      if (two) c4[j] = s1;
+    }
+    return;
+  }
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / nq, c = (i % nq) * 4;
     float4 s = __ldcg(reinterpret_cast<const float4*>(ws + r * N + c));
