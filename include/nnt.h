@@ -360,13 +360,15 @@ nnt_status nnt_embedding_fwd(const int32_t* ids, int64_t T, int64_t S, const flo
 size_t nnt_embedding_bwd_scratch_bytes(int64_t T, int64_t V);
 
 /* Adjoint of nnt_embedding_fwd: dwte[v] (+)= sum over tokens t with ids[t] == v of dx[t]
- * (added in ascending t), dwpe[s] (+)= sum_b dx[b*S + s] (ascending b); accumulate != 0 adds
- * into dwte / dwpe (rows of dwte whose id does not occur are then untouched), 0 overwrites.
+ * (added in ascending t), dwpe[s] (+)= sum_b dx[b*S + s] (ascending b).  accumulate_wte != 0
+ * adds into dwte (rows of dwte whose id does not occur are then untouched; the tied LM head
+ * writes its half of the gradient there first), 0 overwrites; accumulate_wpe likewise for dwpe
+ * (separate flags: the two tables have separate producers).
  * Deterministic (integer counting sort, no floating-point atomics).  dx: device fp32 [T][E];
  * dwte: [V][E]; dwpe: [>= S][E] (rows >= S untouched). */
 nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const float* dx, int64_t E,
-                             float* dwte, int64_t V, float* dwpe, int accumulate, void* scratch,
-                             size_t scratch_bytes, nnt_stream_t stream);
+                             float* dwte, int64_t V, float* dwpe, int accumulate_wte, int accumulate_wpe,
+                             void* scratch, size_t scratch_bytes, nnt_stream_t stream);
 
 /* Cross-entropy through the two SoftMax subroutines (R13): per row r of
  * the logits x (device fp32/bf16 [rows][ld], V classes), subroutine 1 gives (M_r, S_r) =

@@ -417,8 +417,3 @@ def sgd_step(w, g, buf, lr=1e-2, momentum=0.9, weight_decay=0.0):
 def block_param_count(e):
     """12 E^2 + 13 E parameters per block (4 linears + 2 LayerNorms)."""
     return 12 * e * e + 13 * e
-
-
-def model_flops_per_token_layer(e, s):
-    """72 E^2 + 12 S E: fwd+bwd model FLOPs per token per layer (full-attention convention)."""
-    return 72 * e * e + 12 * s * e

@@ -7,6 +7,8 @@
 #include <cstdarg>
 #include <cstdio>
 #include <mutex>
+#include <set>
+#include <tuple>
 #include <vector>
 
 #include "nnt_internal.h"
@@ -31,6 +33,21 @@ int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+cudaError_t set_max_dyn_smem(const void* fn, int bytes) {
+  // cudaFuncSetAttribute acts on the current device's context: cache per (function, device)
+  static std::mutex mu;
+  static std::set<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  auto key = std::make_tuple(fn, dev, bytes);
+  if (done.count(key)) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert(key);
+  return e;
 }
 
 bool pdl_enabled() {

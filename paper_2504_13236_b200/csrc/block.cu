@@ -498,10 +498,19 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
                                op == NNT_OP_OUT_DB || op == NNT_OP_OUT_DW || op == NNT_OP_QKV_DB ||
                                op == NNT_OP_QKV_DW);
   };
-  static thread_local cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  if (side && !ev_fork) {
-    NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+  // fork / join events, one pair per device (events belong to the device current at creation)
+  static thread_local cudaEvent_t ev_pool[kMaxDevices][2] = {};
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  if (side) {
+    int dev = 0;
+    NNT_CUDA_TRY(cudaGetDevice(&dev));
+    NNT_REQUIRE(dev >= 0 && dev < kMaxDevices, NNT_ERR_UNSUPPORTED, "nnt_block_bwd_streams: device %d", dev);
+    if (!ev_pool[dev][0]) {
+      NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_pool[dev][0], cudaEventDisableTiming));
+      NNT_CUDA_TRY(cudaEventCreateWithFlags(&ev_pool[dev][1], cudaEventDisableTiming));
+    }
+    ev_fork = ev_pool[dev][0];
+    ev_join = ev_pool[dev][1];
   }
   Ctx cs = c;
   cs.st = side;
@@ -527,19 +536,29 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
       NNT_TRY(run_bwd_op(c, gr.op, p, x, dy, dx, g, accumulate_grads));
       main_advanced = true;
     }
-    if (grad_ready && !side) {
-      for (int k = 0; k < 4; ++k)
-        for (int j = 0; j < 4; ++j)
-          if (sets[k][j] == gr.op && --remaining[k] == 0 && grad_ready[k])
-            NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
-    }
+    if (!grad_ready) continue;
+    for (int k = 0; k < 4; ++k)
+      for (int j = 0; j < 4; ++j) {
+        if (sets[k][j] != gr.op || --remaining[k] != 0 || !grad_ready[k]) continue;
+        if (!side) {
+          NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
+          continue;
+        }
+        // the set's ops are split over both streams: bring the side stream past the main
+        // stream's work so far (side ops enqueued later would fork from a later point anyway),
+        // then the event on the side stream covers both -- each bucket fires as soon as its own
+        // set is done, not at the end of the layer
+        if (main_advanced) {
+          NNT_CUDA_TRY(cudaEventRecord(ev_fork, stream));
+          NNT_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));
+          main_advanced = false;
+        }
+        NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], side));
+      }
   }
   if (side) {  // join: the main stream continues only after the side stream's work
     NNT_CUDA_TRY(cudaEventRecord(ev_join, side));
     NNT_CUDA_TRY(cudaStreamWaitEvent(stream, ev_join, 0));
-    if (grad_ready)
-      for (int k = 0; k < 4; ++k)
-        if (grad_ready[k]) NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], stream));
   }
   return NNT_OK;
 }

@@ -1523,7 +1523,7 @@ int64_t pair_units() {
     using Cq = Cfg<256, 2>;
     auto kern = gemm_tc_kernel<256, float, EPI_GENERIC, 2>;
     int n = 0;
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cq::SMEM_BYTES) == cudaSuccess) {
+    if (set_max_dyn_smem(kern, (int)Cq::SMEM_BYTES) == cudaSuccess) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3((unsigned)(num_sms() / 2 * 2));
       q.blockDim = dim3(kThreads);
@@ -1547,12 +1547,7 @@ int64_t pair_units() {
 template <int BN, typename TC, int EPI, int CG = 1>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   using C = Cfg<BN, CG, EPI>;
-  static std::once_flag once;
-  static cudaError_t attr_err = cudaSuccess;
-  std::call_once(once, [] {
-    attr_err = cudaFuncSetAttribute(gemm_tc_kernel<BN, TC, EPI, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    C::SMEM_BYTES);
-  });
+  const cudaError_t attr_err = set_max_dyn_smem(gemm_tc_kernel<BN, TC, EPI, CG>, (int)C::SMEM_BYTES);
   NNT_REQUIRE(attr_err == cudaSuccess, NNT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
   NNT_TRY(get_encoder());
   TcParams P;

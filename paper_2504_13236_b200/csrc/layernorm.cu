@@ -439,7 +439,7 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
     const size_t smem_red = (size_t)kRowsWarps * (sum ? 3 : 2) * E * sizeof(float);  // <= 72 KB (E <= 1024)
     auto run = [&](auto kern) -> nnt_status {
       if (smem_red > 48 * 1024)
-        NNT_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_red));
+        NNT_CUDA_TRY(set_max_dyn_smem(kern, (int)smem_red));
       NNT_CUDA_TRY(::nnt::launch(kern, dim3((unsigned)chunks), dim3(32 * kRowsWarps), smem_red, stream, dy, lddy, x,
                                  ldx, mean, rstd, gamma, T, (int)E, rows_per_cta, dres, dx, lddx, d16, pg, pb, ps));
       return NNT_OK;

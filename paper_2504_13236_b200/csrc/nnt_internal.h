@@ -72,6 +72,16 @@ struct LaunchScope {
 
 int num_sms();
 
+// Per-process state is kept per device where CUDA ties it to one (events, function attributes):
+// one process may drive several GPUs.
+constexpr int kMaxDevices = 64;
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device, bytes).
+cudaError_t set_max_dyn_smem(const void* fn, int bytes);
+template <typename F>
+inline cudaError_t set_max_dyn_smem(F* fn, int bytes) {
+  return set_max_dyn_smem(reinterpret_cast<const void*>(fn), bytes);
+}
+
 // ---------------------------------------------------------------- launches
 // Every libnnt kernel is launched with programmatic dependent launch (PDL) allowed: the next
 // kernel on the stream may be scheduled while this one drains, its CTAs run their prologue

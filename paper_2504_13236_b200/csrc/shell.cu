@@ -552,8 +552,8 @@ size_t nnt_embedding_bwd_scratch_bytes(int64_t T, int64_t V) {
 }
 
 nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const float* dx, int64_t E, float* dwte,
-                             int64_t V, float* dwpe, int accumulate, void* scratch, size_t scratch_bytes,
-                             nnt_stream_t stream) {
+                             int64_t V, float* dwpe, int accumulate_wte, int accumulate_wpe, void* scratch,
+                             size_t scratch_bytes, nnt_stream_t stream) {
   NNT_REQUIRE(ids && dx && dwte && dwpe && scratch, NNT_ERR_NULL, "nnt_embedding_bwd: NULL pointer");
   NNT_REQUIRE(T > 0 && S > 0 && T % S == 0 && V > 0 && E > 0 && T < (1ll << 31) && V < (1ll << 30), NNT_ERR_SHAPE,
               "nnt_embedding_bwd: T=%lld S=%lld V=%lld E=%lld", (long long)T, (long long)S, (long long)V, (long long)E);
@@ -567,27 +567,22 @@ nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const flo
   int* offs = rank + T;
   int* order = offs + (V + 1);
   LaunchScope sc(NNT_K_MISC, s, 8.0 * T * E + 8.0 * V * 4 + 4.0 * V * E, 0, 7);
-  static const size_t scan_smem = [] {
-    cudaFuncSetAttribute(embed_scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(kScanMax * sizeof(int)));
-    return (size_t)kScanMax * sizeof(int);
-  }();
+  NNT_CUDA_TRY(set_max_dyn_smem(embed_scan_kernel, (int)(kScanMax * sizeof(int))));
   NNT_REQUIRE(V + 1 <= kScanMax, NNT_ERR_UNSUPPORTED, "nnt_embedding_bwd: V=%lld > %d", (long long)V,
               kScanMax - 1);
   NNT_CUDA_TRY(::nnt::launch(zero_ints_kernel, dim3(grid_cap(V + 1 + T, kT)), dim3(kT), 0, s, hist, V + 1 + T));
   NNT_CUDA_TRY(::nnt::launch(embed_hist_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V, hist));
   NNT_CUDA_TRY(::nnt::launch(embed_scan_kernel, dim3(1), dim3(1024), (size_t)(V + 1) * sizeof(int), s,
                              (const int*)hist, V + 1, offs));
-  (void)scan_smem;
   NNT_CUDA_TRY(::nnt::launch(embed_rank_kernel,
                              dim3((unsigned)((T + kT - 1) / kT), (unsigned)((T + kRankChunk - 1) / kRankChunk)),
                              dim3(kT), 0, s, ids, T, V, rank));
   NNT_CUDA_TRY(::nnt::launch(embed_place_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V,
                              (const int*)offs, (const int*)rank, order));
   NNT_CUDA_TRY(::nnt::launch(embed_bucket_kernel, dim3((unsigned)((V + kT / 32 - 1) / (kT / 32))), dim3(kT), 0, s,
-                             (const int*)offs, (const int*)order, dx, (int)E, V, dwte, accumulate));
+                             (const int*)offs, (const int*)order, dx, (int)E, V, dwte, accumulate_wte));
   NNT_CUDA_TRY(::nnt::launch(embed_pos_kernel, dim3(grid_cap(S * E / 4, kT)), dim3(kT), 0, s, dx, T / S, S, (int)E,
-                             dwpe, accumulate));
+                             dwpe, accumulate_wpe));
   return NNT_OK;
 }
 
@@ -610,12 +605,7 @@ nnt_status nnt_cross_entropy(const void* logits, int dtype, int64_t rows, int64_
     return e && e[0] == '1';
   }();
   if (2 * row_bytes <= kCeSmemMax + 8192 && dtype == NNT_BF16 && !restream) {
-    static const bool attr = [] {
-      cudaFuncSetAttribute(cross_entropy_pipe_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)(kCeSmemMax + 8192));
-      return true;
-    }();
-    (void)attr;
+    NNT_CUDA_TRY(set_max_dyn_smem(cross_entropy_pipe_kernel<__nv_bfloat16>, (int)(kCeSmemMax + 8192)));
     const int64_t grid = rows < num_sms() ? rows : num_sms();
     NNT_CUDA_TRY(::nnt::launch(cross_entropy_pipe_kernel<__nv_bfloat16>, dim3((unsigned)grid), dim3(kCePT),
                                2 * row_bytes, s, (const __nv_bfloat16*)logits, rows, V, ld, labels, scale, loss_rows,
@@ -624,22 +614,12 @@ nnt_status nnt_cross_entropy(const void* logits, int dtype, int64_t rows, int64_
   }
   if (row_bytes <= kCeSmemMax && !restream) {
     if (dtype == NNT_BF16) {
-      static const bool attr = [] {
-        cudaFuncSetAttribute(cross_entropy_staged_kernel<__nv_bfloat16>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCeSmemMax);
-        return true;
-      }();
-      (void)attr;
+      NNT_CUDA_TRY(set_max_dyn_smem(cross_entropy_staged_kernel<__nv_bfloat16>, (int)kCeSmemMax));
       NNT_CUDA_TRY(::nnt::launch(cross_entropy_staged_kernel<__nv_bfloat16>, dim3((unsigned)rows), dim3(kCeT),
                                  row_bytes, s, (const __nv_bfloat16*)logits, rows, V, ld, labels, scale, loss_rows,
                                  stats, (__nv_bfloat16*)dlogits, ld_d));
     } else {
-      static const bool attr = [] {
-        cudaFuncSetAttribute(cross_entropy_staged_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)kCeSmemMax);
-        return true;
-      }();
-      (void)attr;
+      NNT_CUDA_TRY(set_max_dyn_smem(cross_entropy_staged_kernel<float>, (int)kCeSmemMax));
       NNT_CUDA_TRY(::nnt::launch(cross_entropy_staged_kernel<float>, dim3((unsigned)rows), dim3(kCeT), row_bytes, s,
                                  (const float*)logits, rows, V, ld, labels, scale, loss_rows, stats, (float*)dlogits,
                                  ld_d));

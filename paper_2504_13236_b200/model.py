@@ -580,7 +580,9 @@ class GPT2Model:
                               st.view(st.g, c.L - 1, "b_pr") if top else None, 0,
                               self.lnf_scr, self.lnf_scr.numel())
         dx0 = st.backward(top_done=top)
-        nnt.nnt_embedding_bwd(self.ids, T, c.S, dx0, E, self.view(self.g, "wte"), V, self.view(self.g, "wpe"), 1,
+        # dwte accumulates onto the LM head's half (written with beta = 0 above); dwpe has no other
+        # producer and is overwritten
+        nnt.nnt_embedding_bwd(self.ids, T, c.S, dx0, E, self.view(self.g, "wte"), V, self.view(self.g, "wpe"), 1, 0,
                               self.emb_scr, self.emb_scr.numel())
         if st.dp:  # the shell bucket: all-reduce + Adam on the comm stream
             self.ev_shell.record()

@@ -140,7 +140,7 @@ _sig = {
     "nnt_dot": (_i32, [_vp, _vp, _i64, _f32, _vp, _vp, _sz, _vp]),
     "nnt_embedding_fwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _vp]),
     "nnt_embedding_bwd_scratch_bytes": (_sz, [_i64, _i64]),
-    "nnt_embedding_bwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _vp, _sz, _vp]),
+    "nnt_embedding_bwd": (_i32, [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i32, _i32, _vp, _sz, _vp]),
     "nnt_cross_entropy": (_i32, [_vp, _i32, _i64, _i64, _i64, _vp, _f32, _vp, _vp, _vp, _i64, _vp]),
     "nnt_block_workspace_size": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(_sz), C.POINTER(_sz)]),
     "nnt_block_fwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_params), _vp, _vp, _vp, _vp, _vp]),
@@ -353,9 +353,10 @@ def nnt_embedding_bwd_scratch_bytes(T, V):
     return lib.nnt_embedding_bwd_scratch_bytes(T, V)
 
 
-def nnt_embedding_bwd(ids, T, S, dx, E, dwte, V, dwpe, accumulate, scratch, scratch_bytes, stream=None):
-    return check(lib.nnt_embedding_bwd(ptr(ids), T, S, ptr(dx), E, ptr(dwte), V, ptr(dwpe), accumulate, ptr(scratch),
-                                       scratch_bytes, _stream(stream)))
+def nnt_embedding_bwd(ids, T, S, dx, E, dwte, V, dwpe, accumulate_wte, accumulate_wpe, scratch, scratch_bytes,
+                      stream=None):
+    return check(lib.nnt_embedding_bwd(ptr(ids), T, S, ptr(dx), E, ptr(dwte), V, ptr(dwpe), accumulate_wte,
+                                       accumulate_wpe, ptr(scratch), scratch_bytes, _stream(stream)))
 
 
 def nnt_cross_entropy(logits, dtype, rows, V, ld, labels, scale, loss_rows, stats, dlogits, ld_d, stream=None):

@@ -1,4 +1,7 @@
 """Helpers for the -m gpu parity tests (test infrastructure)."""
+import json
+import os
+
 import numpy as np
 import torch
 
@@ -7,6 +10,43 @@ def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def rel_max(a, b):
+    """max_i |a_i - b_i| / max_i |b_i| (SURVEY §8(c)'s element-wise parity metric)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def close(got, want, tol, what="", max_tol=None):
+    """Parity assertion used by every block / shape / GPT-2 / kernel test (reading R32):
+    the norm-wise error ||got - want||_2 / ||want||_2 < tol AND the element-wise error
+    max|got - want| / max|want| < max_tol (default: the same bound).  The norm alone would let one
+    wrong row, head or boundary tile of a large tensor pass; the element-wise bound does not.
+
+    With NNT_PARITY_LOG=<file> every comparison is appended there as one JSON line (the evidence
+    the bounds were chosen from)."""
+    got = np.asarray(got, np.float64)
+    want = np.asarray(want, np.float64)
+    assert got.shape == want.shape or got.size == want.size, (what, got.shape, want.shape)
+    got = got.reshape(want.shape)
+    assert np.all(np.isfinite(got)), f"{what}: non-finite values"
+    r, m = rel(got, want), rel_max(got, want)
+    max_tol = tol if max_tol is None else max_tol
+    log = os.environ.get("NNT_PARITY_LOG")
+    if log:
+        import inspect
+        test = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+        caller = inspect.stack()[1]
+        with open(log, "a") as f:
+            f.write(json.dumps({"test": test, "line": caller.lineno, "what": str(what), "n": int(want.size),
+                                "rel": r, "rel_max": m, "tol": tol, "max_tol": max_tol}) + "\n")
+    assert r < tol, f"{what}: norm-wise rel {r:.3e} >= {tol:.1e}"
+    assert m < max_tol, f"{what}: element-wise max rel {m:.3e} >= {max_tol:.1e}"
+    return r, m
 
 
 def dev(a, dtype=torch.float32):

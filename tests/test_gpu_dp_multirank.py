@@ -1,0 +1,211 @@
+"""The data-parallel product path with R = 2 and 3 ranks (VERDICT r1 "next" #2, §8(a) A16).
+
+NCCL cannot put two ranks on one GPU, so the ranks here are R processes sharing cuda:0 with a
+gloo process group (gloo all-reduces CUDA tensors through host staging).  Everything else is the
+product path: BlockStack / GPT2Model built with process_group=WORLD run train_step eagerly, so
+nnt_block_bwd's per-bucket grad_ready events, BlockStack._reduce_bucket on the communication
+stream, the per-bucket Adam (or ZeRO-1's reduce-scatter / owned-slice update / all-gather), and
+the shell bucket all execute with real cross-rank sums.  Rank r holds the batch tiles
+nnt_partition(NB, R, r) of the global batch (reading R14).
+
+Checks: (1) every rank's parameters after 2 steps are bitwise identical (a checksum all-gather
+across ranks, and the full parameter vectors compared on the host -- reading R17); (2) rank 0's
+parameter change equals the oracle's full-batch 2-step Adam trajectory (fp32 path, rel 1e-4,
+norm-wise and element-wise); (3) on the bf16 full model, the all-reduced gradients of step 2 equal
+the oracle's full-batch gradients at the parameters the ranks held before that step (2e-2).
+"""
+import os
+import socket
+import traceback
+
+import numpy as np
+import pytest
+import torch
+
+import nnt_inputs
+from oracle import dense
+from gpu_util import bf16_round, close
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _checksum_allgather(dist, *bufs):
+    """float64 sum and an integer hash of the raw bits of every buffer, gathered from all ranks."""
+    parts = []
+    for b in bufs:
+        bits = b.detach().contiguous().view(torch.int32).to(torch.int64)
+        parts += [float(b.double().sum()), float((bits * (torch.arange(bits.numel(), device=bits.device) % 1009 + 1))
+                                                  .sum())]
+    mine = torch.tensor(parts, dtype=torch.float64)
+    allv = [torch.zeros_like(mine) for _ in range(dist.get_world_size())]
+    dist.all_gather(allv, mine)
+    return [a.tolist() for a in allv]
+
+
+def _stack_worker(rank, world, port, nb, zero, q):
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2504_13236_b200 import model, nnt
+        c = nnt_inputs.CONFIGS["tiny"]
+        b0, b1 = nnt.nnt_partition(nb, world, rank)
+        sc = model.StackConfig(L=2, E=c.E, H=c.H, S=c.S, B=b1 - b0, tile_e=c.tile, tile_f=c.tile, tile_s=c.tile,
+                               tile_t=c.tile, dtype="f32", zero=zero)
+        layers = [nnt_inputs.make_params(c.E, seed=21, layer=l, n_layers=2) for l in range(2)]
+        st = model.BlockStack(sc, layers, process_group=dist.group.WORLD, global_tokens=nb * c.S)
+        losses = []
+        for t in range(1, 3):
+            x = torch.as_tensor(nnt_inputs.make_x(c.E, c.S, b0, b1, seed=500 + t)).cuda()
+            r = torch.as_tensor(nnt_inputs.make_r(c.E, c.S, b0, b1, seed=500 + t)).cuda()
+            losses.append(st.train_step(x, r).item())
+        torch.cuda.synchronize()
+        sums = _checksum_allgather(dist, st.w.cpu())
+        q.put((rank, (b0, b1), losses, st.w.cpu().numpy(), sums, None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, None, None, None, None, traceback.format_exc()))
+
+
+def _spawn(fn, world, *args):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=fn, args=(r, world, port) + args + (q,)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=120)
+    errs = [o[-1] for o in out if o[-1]]
+    assert not errs, "\n".join(errs)
+    return sorted(out, key=lambda o: o[0])
+
+
+def _oracle_stack_trajectory(nb):
+    from paper_2504_13236_b200 import model
+    c = nnt_inputs.CONFIGS["tiny"]
+    layers = [nnt_inputs.make_params(c.E, seed=21, layer=l, n_layers=2) for l in range(2)]
+    P = [{k: v.astype(np.float64) for k, v in p.items()} for p in layers]
+    m = [{k: np.zeros_like(v) for k, v in p.items()} for p in P]
+    v_ = [{k: np.zeros_like(v) for k, v in p.items()} for p in P]
+    losses = []
+    for t in range(1, 3):
+        x = nnt_inputs.make_x(c.E, c.S, 0, nb, seed=500 + t)
+        r = nnt_inputs.make_r(c.E, c.S, 0, nb, seed=500 + t)
+        y, caches = dense.stack_fwd(P, x, c.H)
+        losses.append(dense.probe_loss(y, r, nb * c.S))
+        _, g = dense.stack_bwd(P, caches, dense.probe_loss_grad(r, nb * c.S))
+        for l in range(2):
+            for k in P[l]:
+                P[l][k], m[l][k], v_[l][k] = dense.adam_step(P[l][k], g[l][k], m[l][k], v_[l][k], t)
+    offsets, _, numel = model.flat_layout(2, c.E)
+    return layers, P, offsets, losses
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world,zero", [(2, False), (3, False), (2, True)], ids=["R2", "R3", "R2-zero1"])
+def test_dp_stack_multirank_vs_full_batch_oracle(world, zero):
+    nb = 6
+    out = _spawn(_stack_worker, world, nb, zero)
+    # the batch-tile partition covers the global batch
+    assert [o[1] for o in out] == [(nb * r // world, nb * (r + 1) // world) for r in range(world)]
+    # replicas bitwise identical: all-gathered checksums, and the vectors themselves
+    sums = out[0][4]
+    assert all(s == sums[0] for s in sums)
+    for o in out[1:]:
+        assert np.array_equal(o[3], out[0][3])
+    layers, P, offsets, losses = _oracle_stack_trajectory(nb)
+    # every rank's probe loss is its share of the global loss (1/T_global scaling, reading R13/R14)
+    for t in range(2):
+        assert abs(sum(o[2][t] for o in out) - losses[t]) <= 1e-4 * abs(losses[t])
+    w = out[0][3]
+    E = nnt_inputs.CONFIGS["tiny"].E
+    for l in range(2):
+        for k, (o, n) in offsets[l].items():
+            got = w[o:o + n].astype(np.float64) - layers[l][k].ravel()
+            want = P[l][k].ravel() - layers[l][k].ravel()
+            if k == "b_qkv":  # key-bias gradient is exactly zero (R22): Adam amplifies its fp32 noise
+                got, want = np.delete(got, np.s_[E:2 * E]), np.delete(want, np.s_[E:2 * E])
+            close(got, want, 1e-4, f"R{world} L{l} {k}")
+
+
+def _gpt2_worker(rank, world, port, nb, q):
+    try:
+        import torch.distributed as dist
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        from paper_2504_13236_b200 import model, nnt
+        V, E, H, S, L = 1000, 768, 12, 128, 2
+        b0, b1 = nnt.nnt_partition(nb, world, rank)
+        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=b1 - b0, dtype="bf16")
+        layers = [nnt_inputs.make_params(E, seed=31, layer=l, init="parity", n_layers=L) for l in range(L)]
+        shell = nnt_inputs.make_shell_params(V, S, E, seed=32, init="parity")
+        gm = model.GPT2Model(sc, V, layers, shell, process_group=dist.group.WORLD, global_tokens=nb * S)
+        before = None
+        for t in range(1, 3):
+            if t == 2:  # the parameters step 2's gradients are taken at
+                before = (gm.w.cpu().numpy(), gm.stack.w.cpu().numpy())
+            tok = torch.as_tensor(nnt_inputs.make_ids(V, S, b0, b1, seed=600 + t)).cuda()
+            gm.train_step(tok[:, :S].contiguous(), tok[:, 1:].contiguous())
+        torch.cuda.synchronize()
+        sums = _checksum_allgather(dist, gm.w.cpu(), gm.stack.w.cpu(), gm.g.cpu(), gm.stack.g.cpu())
+        q.put((rank, before, (gm.g.cpu().numpy(), gm.stack.g.cpu().numpy(), gm.w.cpu().numpy(),
+                              gm.stack.w.cpu().numpy()), sums, None))
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        q.put((rank, None, None, None, traceback.format_exc()))
+
+
+@pytest.mark.timeout(900)
+def test_dp_gpt2_multirank_gradients_vs_full_batch_oracle():
+    from paper_2504_13236_b200 import model
+    world, nb = 2, 4
+    V, E, H, S, L = 1000, 768, 12, 128, 2
+    out = _spawn(_gpt2_worker, world, nb)
+    sums = out[0][3]
+    assert all(s == sums[0] for s in sums)
+    for o in out[1:]:
+        for a, b in zip(o[2], out[0][2]):
+            assert np.array_equal(a, b)
+    w_shell, w_stack = out[0][1]
+    g_shell, g_stack = out[0][2][0], out[0][2][1]
+    soff, _, _ = model.shell_layout(V, S, E)
+    offsets, _, _ = model.flat_layout(L, E)
+    shapes = model.param_shapes(E)
+    om = {k: w_shell[o:o + n].astype(np.float64) for k, (o, n) in soff.items()}
+    om["wte"] = bf16_round(om["wte"]).reshape(V, E)
+    om["wpe"] = om["wpe"].reshape(S, E)
+    om["blocks"] = []
+    for l in range(L):
+        p = {}
+        for k, (o, n) in offsets[l].items():
+            a = w_stack[o:o + n].astype(np.float64).reshape(shapes[k])
+            p[k] = bf16_round(a) if k.startswith("w_") else a
+        om["blocks"].append(p)
+    tok = nnt_inputs.make_ids(V, S, 0, nb, seed=602)
+    _, cache = dense.gpt2_fwd(om, tok[:, :S], tok[:, 1:], H)
+    g = dense.gpt2_bwd(om, cache)
+    for k, (o, n) in soff.items():
+        close(g_shell[o:o + n], g[k].ravel(), 2e-2, f"dp {k}")
+    for l in range(L):
+        for k, (o, n) in offsets[l].items():
+            got, want = g_stack[o:o + n], g["blocks"][l][k].ravel()
+            if k == "b_qkv":
+                got, want = np.delete(got, np.s_[E:2 * E]), np.delete(want, np.s_[E:2 * E])
+            close(got, want, 2e-2, f"dp L{l} {k}")

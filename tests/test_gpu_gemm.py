@@ -14,7 +14,7 @@ import torch
 
 import nnt_inputs
 from oracle import dense, tiled
-from gpu_util import bf16_round, dev, host, rel
+from gpu_util import close, bf16_round, dev, host, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -85,15 +85,15 @@ def test_gemm_epilogues(dtype, M):
     bias_d, res_d = dev(bias), dev(res)
     epi = nnt.make_epilogue(bias=bias_d, residual=res_d, ld_residual=N)
     got = _run(dtype, 0, 1, M, N, K, a, b, beta=0.5, c0=c0, epi=epi, alpha=0.75)
-    assert rel(host(got), 0.75 * base + bias + 0.5 * c0 + res) < tol
+    close(host(got), 0.75 * base + bias + 0.5 * c0 + res, tol)
     # GELU forward: aux <- pre, C <- gelu(pre)
     aux = torch.zeros(M, N, device="cuda", dtype=DT[dtype][0])
     epi = nnt.make_epilogue(bias=bias_d, act=nnt.NNT_ACT_GELU, aux=aux, ld_aux=N)
     got = _run(dtype, 0, 1, M, N, K, a, b, c_dtype=dtype, epi=epi)
     pre = base + bias
     t2 = 1e-6 if dtype == "f32" else 1e-2
-    assert rel(host(aux), pre) < t2
-    assert rel(host(got), dense.gelu(pre)) < t2
+    close(host(aux), pre, t2)
+    close(host(got), dense.gelu(pre), t2)
     # GELU backward: C <- pre * gelu'(aux)
     u = rng.standard_normal((M, N)).astype(np.float32)
     if dtype == "bf16":
@@ -101,7 +101,7 @@ def test_gemm_epilogues(dtype, M):
     auxu = dev(u, DT[dtype][0])
     epi = nnt.make_epilogue(act=nnt.NNT_ACT_GELU_BWD, aux=auxu, ld_aux=N)
     got = _run(dtype, 0, 1, M, N, K, a, b, c_dtype=dtype, epi=epi)
-    assert rel(host(got), base * dense.gelu_grad(u)) < t2
+    close(host(got), base * dense.gelu_grad(u), t2)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
@@ -249,7 +249,7 @@ def test_scores_gemm_fused_maxsumexp_partials(causal):
     m_ref, s_ref = dense.maxsumexp(a, mask)
     got = host(stats).reshape(B, H, S, 2)
     np.testing.assert_allclose(got[..., 0], m_ref, rtol=1e-5, atol=1e-5)
-    assert rel(got[..., 1], s_ref) < 1e-5
+    close(got[..., 1], s_ref, 1e-5)
 
 
 @pytest.mark.parametrize("causal", [0, 1])
@@ -281,7 +281,7 @@ def test_rowstats_then_softmax_gemms(causal, S):
     m_ref, s_ref = dense.maxsumexp(a, mask)
     got = host(stats).reshape(B, H, S, 2)
     np.testing.assert_allclose(got[..., 0], m_ref, rtol=1e-5, atol=1e-5)
-    assert rel(got[..., 1], s_ref) < 1e-5
+    close(got[..., 1], s_ref, 1e-5)
     p = host(P)
     p_ref = dense.softmax(a, mask)
     r, c = np.arange(S)[:, None], np.arange(S)[None, :]
@@ -289,7 +289,7 @@ def test_rowstats_then_softmax_gemms(causal, S):
     assert not np.isnan(p[..., written]).any() and np.isnan(p[..., ~written]).all()
     if causal:
         assert np.all(p[..., written & (c > r)] == 0.0)
-    assert rel(np.where(written, p, 0.0), p_ref) < 4e-3  # bf16 rounding of P
+    close(np.where(written, p, 0.0), p_ref, 4e-3)  # bf16 rounding of P
     np.testing.assert_allclose(np.where(written, p, 0.0).sum(-1), 1.0, atol=2e-2)
 
 
@@ -316,13 +316,13 @@ def test_fused_softmax_bwd_gemm_and_rowdot():
     torch.cuda.synchronize()
     dob = do.reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
     ob = O16.reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
-    assert rel(host(D).reshape(B, H, S), (dob * ob).sum(-1)) < 1e-5
+    close(host(D).reshape(B, H, S), (dob * ob).sum(-1), 1e-5)
     v = qkv[:, :, 2 * E:].reshape(B, S, H, Dh).transpose(0, 2, 1, 3)
     want = scale * dense.softmax_bwd(P16, dob @ v.transpose(0, 1, 3, 2))
     got = host(dA)
     mask = np.tril(np.ones((S, S), bool))
     assert np.all(got[..., ~mask & (np.arange(S)[None, :] < ((np.arange(S)[:, None] // 128 + 1) * 128))] == 0.0)
-    assert rel(np.where(mask, got, 0.0), want) < 2e-2
+    close(np.where(mask, got, 0.0), want, 2e-2)
 
 
 @pytest.mark.parametrize("dt,h", [("bf16", 64), ("bf16", 8), ("bf16", 16), ("bf16", 256), ("bf16", 24),
@@ -339,7 +339,7 @@ def test_attn_rowdot_head_dims(dt, h):
     nnt.nnt_attn_rowdot(dev(do, tdt), dev(o, tdt), code, B, S, H, h, D)
     torch.cuda.synchronize()
     want = (do * o).sum(-1).transpose(0, 2, 1)  # [B, H, S]
-    assert rel(host(D).reshape(B, H, S), want) < 1e-6
+    close(host(D).reshape(B, H, S), want, 1e-6)
 
 
 def test_gemm_rejects_bad_arguments():

@@ -12,7 +12,7 @@ import torch
 
 import nnt_inputs
 from oracle import dense, tiled
-from gpu_util import bf16_round, dev, host, rel
+from gpu_util import close, bf16_round, dev, host, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -45,7 +45,7 @@ def test_maxsumexp_and_softmax(causal, cols, tile_k):
     m_ref, s_ref = dense.maxsumexp(x.astype(np.float64), mask)
     got = host(st)
     assert np.array_equal(got[:, 0], m_ref.astype(np.float32))  # the max is exact
-    assert rel(got[:, 1], s_ref) < 1e-5
+    close(got[:, 1], s_ref, 1e-5)
     for ydt in ("f32", "bf16"):
         Y = torch.full((rows, cols), float("nan"), device="cuda",
                        dtype=torch.float32 if ydt == "f32" else torch.bfloat16)
@@ -61,7 +61,7 @@ def test_maxsumexp_and_softmax(causal, cols, tile_k):
             assert np.all(y[written & ~mask] == 0.0)
             y = np.where(written, y, 0.0)
         tol = 1e-5 if ydt == "f32" else 4e-3
-        assert rel(y, p_ref) < tol
+        close(y, p_ref, tol)
         if ydt == "f32":
             np.testing.assert_allclose(y.sum(-1), 1.0, atol=1e-5)
 
@@ -79,7 +79,7 @@ def test_maxsumexp_accumulate_per_key_tile_equals_single_call():
     torch.cuda.synchronize()
     a, b = host(st1), host(st2)
     assert np.array_equal(a[:, 0], b[:, 0])
-    assert rel(b[:, 1], a[:, 1]) < 1e-6
+    close(b[:, 1], a[:, 1], 1e-6)
 
 
 def test_softmax_large_logits_no_nan():
@@ -122,7 +122,7 @@ def test_softmax_bwd(causal, pdt):
         written = np.arange(cols)[None, :] < extent[:, None]
         assert np.all(got[written & ~mask] == 0.0)
         got = np.where(written, got, 0.0)
-    assert rel(got, want) < (1e-5 if pdt == "f32" else 4e-3)
+    close(got, want, (1e-5 if pdt == "f32" else 4e-3))
 
 
 @pytest.mark.parametrize("E", [64, 768, 1600, 8192])
@@ -139,9 +139,9 @@ def test_layernorm_fwd(E, ydt):
     nnt.nnt_layernorm_fwd(dev(x), T, E, E, 1024, dev(g), dev(b), 1e-5, Y, 0 if ydt == "f32" else 1, E, mean, rstd)
     torch.cuda.synchronize()
     y_ref, m_ref, r_ref = dense.layernorm_fwd(x, g, b, 1e-5)
-    assert rel(host(Y), y_ref) < (2e-5 if ydt == "f32" else 4e-3)
-    assert rel(host(mean), m_ref) < 1e-6
-    assert rel(host(rstd), r_ref) < 1e-4
+    close(host(Y), y_ref, (2e-5 if ydt == "f32" else 4e-3))
+    close(host(mean), m_ref, 1e-6)
+    close(host(rstd), r_ref, 1e-4)
 
 
 def test_layernorm_closed_forms():
@@ -183,12 +183,12 @@ def test_layernorm_bwd(E):
     nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)), dev(r_ref.astype(np.float32)),
                           dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, DS, 1, scr, nb)
     torch.cuda.synchronize()
-    assert rel(host(DX), dx_ref + dres) < 1e-5
-    assert rel(host(DX16), dx_ref + dres) < 4e-3
-    assert rel(host(DG), dg_ref + 1.0) < 1e-5
-    assert rel(host(DB), db_ref + 1.0) < 1e-5
+    close(host(DX), dx_ref + dres, 1e-5)
+    close(host(DX16), dx_ref + dres, 4e-3)
+    close(host(DG), dg_ref + 1.0, 1e-5)
+    close(host(DB), db_ref + 1.0, 1e-5)
     if DS is not None:
-        assert rel(host(DS), (dx_ref + dres).sum(axis=0) + 2.0) < 1e-5
+        close(host(DS), (dx_ref + dres).sum(axis=0) + 2.0, 1e-5)
     else:  # E > 1024: the CTA-per-row kernel has no fused column sum
         with pytest.raises(nnt.NNTError):
             nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)),
@@ -211,8 +211,8 @@ def test_gelu(dt):
     nnt.nnt_gelu_bwd(X, DY, DX, code, n)
     torch.cuda.synchronize()
     tol = 1e-6 if dt == "f32" else 4e-3
-    assert rel(host(Y), dense.gelu(x)) < tol
-    assert rel(host(DX), dense.gelu_bwd(x, dy)) < tol
+    close(host(Y), dense.gelu(x), tol)
+    close(host(DX), dense.gelu_bwd(x, dy), tol)
     assert host(Y)[n // 2] == 0.0  # gelu(0) = 0
 
 
@@ -227,7 +227,7 @@ def test_bias_grad(T, N):
     C16 = torch.zeros(T, N, device="cuda", dtype=torch.bfloat16)
     nnt.nnt_bias_grad(dev(dy), 0, T, N, N, DB, 1, C16, scr, nb)
     torch.cuda.synchronize()
-    assert rel(host(DB), dy.astype(np.float64).sum(0) + db0) < 1e-5
+    close(host(DB), dy.astype(np.float64).sum(0) + db0, 1e-5)
     assert np.array_equal(host(C16), bf16_round(dy))
     # deterministic: bitwise identical on repeat
     DB2 = dev(db0)
@@ -253,9 +253,10 @@ def test_adam_matches_oracle_and_step1_closed_form():
         torch.cuda.synchronize()
         # compare the update, not w; fp32 storage of w ~ N(0,1) bounds the update's rel error
         # near 2^-24 / lr ~ 6e-5 (worst element), hence the fp32-path tolerance
-        assert rel(host(W) - w, wr - w) < 1e-4
+        close(host(W) - w, wr - w, 1e-4)
         # fp32 beta2 = 0.999f makes (1 - beta2) off by 1.3e-5 relative: v inherits it
-        assert rel(host(M), mr) < 1e-6 and rel(host(V), vr) < 3e-5
+        close(host(M), mr, 1e-6, "m")
+        close(host(V), vr, 3e-5, "v")
         assert np.array_equal(host(W16), bf16_round(host(W)))
 
 
@@ -273,7 +274,7 @@ def test_adamw_decoupled_decay_matches_oracle():
         nnt.nnt_adam_step(n, W, dev(g), M, V, None, hp)
         wr, mr, vr = dense.adam_step(wr, g, mr, vr, t, lr=1e-2, weight_decay=0.1)
         torch.cuda.synchronize()
-        assert rel(host(W) - w, wr - w) < 1e-4
+        close(host(W) - w, wr - w, 1e-4)
 
 
 def test_sgd_momentum_matches_oracle():
@@ -288,7 +289,8 @@ def test_sgd_momentum_matches_oracle():
         nnt.nnt_sgd_step(n, W, dev(g), BUF, W16, 1e-2, 0.9, 0.01)
         wr, br = dense.sgd_step(wr, g, br, lr=1e-2, momentum=0.9, weight_decay=0.01)
         torch.cuda.synchronize()
-        assert rel(host(W) - w, wr - w) < 1e-5 and rel(host(BUF), br) < 1e-6
+        close(host(W) - w, wr - w, 1e-5, "dw")
+        close(host(BUF), br, 1e-6, "buf")
         assert np.array_equal(host(W16), bf16_round(host(W)))
 
 

@@ -15,7 +15,7 @@ import torch
 
 import nnt_inputs
 from oracle import dense
-from gpu_util import bf16_round, dev, host, rel
+from gpu_util import close, bf16_round, dev, host, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -93,11 +93,11 @@ def _run_shards(E, H, S, B, R, dtype, tile, seed=11):
 def test_tp_shards_match_oracle(E, H, S, B, R, dtype, tile, tol):
     shards, y, dx, y_ref, dx_ref, g_ref = _run_shards(E, H, S, B, R, dtype, tile)
     for r in range(R):
-        assert rel(host(y[r]), y_ref) < tol, r
-        assert rel(host(dx[r]), dx_ref) < tol, r
+        close(host(y[r]), y_ref, tol, r)
+        close(host(dx[r]), dx_ref, tol, r)
         want = tp.tp_shard(g_ref, H, R, r)
         for n, gv in shards[r].g.items():
-            assert rel(host(gv), want[n]) < tol, (r, n)
+            close(host(gv), want[n], tol, (r, n))
     if R > 1:  # replicated parameters' gradients are bitwise equal on every shard
         for n in ("ln1_g", "ln1_b", "b_o", "ln2_g", "ln2_b", "b_pr"):
             for r in range(1, R):
@@ -162,7 +162,7 @@ def test_tp_stack_nccl_world1_two_adam_steps():
                     assert np.abs(got[E:2 * E] - want[E:2 * E]).max() <= 4 * 1e-2 * 1.01, l
                     keep = np.r_[0:E, 2 * E:3 * E]
                     got, want, w0 = got[keep], want[keep], w0[keep]
-                assert rel(got - w0, want - w0) < 1e-3, (l, n)
+                close(got - w0, want - w0, 1e-3, (l, n))
     finally:
         if own:
             dist.destroy_process_group()
