@@ -160,7 +160,12 @@ typedef struct {
 /* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would
  * not split).  Splitting applies to fp32 C without activation or causal mode (the dW GEMMs):
  * split s writes alpha * (its K-range partial) to workspace slice s and an ordered reduce
- * forms C = beta*C + sum_s partial_s (+bias, +residual), splits added in ascending order. */
+ * forms C = beta*C + sum_s partial_s (+bias, +residual), splits added in ascending order (R25).
+ * The reduce runs inside the GEMM: the last split to finish each output region adds the
+ * partials; the arrival counters it uses sit at the end of this workspace.
+ * CONTRACT: a workspace of this size must be ZERO-FILLED before its first use (e.g.
+ * torch.zeros); every call leaves the counters zero again.  A smaller workspace that still holds
+ * the partials is accepted and reduces with a separate kernel launch instead. */
 size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int c_dtype, int act, int causal,
                                      int64_t batch_items);
 
@@ -314,6 +319,9 @@ typedef struct {
   /* device fp32 [2] = {bias_corr1, bias_corr2}, read by the kernel instead of the two
    * scalars above when non-NULL (lets a captured CUDA graph advance the step count) */
   const float* bias_corr_dev;
+  /* 1 - beta1 and 1 - beta2 rounded to fp32 from the caller's fp64 values (R23: 1.0f - 0.999f is
+   * off by 1.3e-5 relative from fp32(1 - 0.999)); 0 = derive them in fp32 from beta1 / beta2 */
+  float one_minus_beta1, one_minus_beta2;
 } nnt_adam_hparams;
 
 /* m = b1 m + (1-b1) g; v = b2 v + (1-b2) g^2; w -= lr (m/bc1) / (sqrt(v/bc2) + eps).
@@ -413,7 +421,9 @@ typedef struct {
 } nnt_block_grads;
 
 /* Bytes of the per-block `saved` activation workspace (kept from fwd to bwd, one per
- * layer) and of the shared `scratch` workspace (reusable across layers). */
+ * layer) and of the shared `scratch` workspace (reusable across layers).  `scratch` holds the
+ * dW GEMMs' split-K workspace: ZERO-FILL it before its first use (see
+ * nnt_tile_gemm_workspace_bytes); the block calls leave that part zero again. */
 nnt_status nnt_block_workspace_size(const nnt_block_cfg* cfg, size_t* saved_bytes,
                                     size_t* scratch_bytes);
 

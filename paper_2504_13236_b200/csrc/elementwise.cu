@@ -56,7 +56,9 @@ __global__ void __launch_bounds__(kThreads) adam_kernel(int64_t n, float* __rest
                                                         float* __restrict__ v, __nv_bfloat16* __restrict__ w16,
                                                         nnt_adam_hparams hp, bool vec_ok) {
   NNT_PDL_ENTRY();
-  const float b1 = hp.beta1, b2 = hp.beta2, c1 = 1.f - hp.beta1, c2 = 1.f - hp.beta2;
+  const float b1 = hp.beta1, b2 = hp.beta2;
+  const float c1 = hp.one_minus_beta1 != 0.f ? hp.one_minus_beta1 : 1.f - hp.beta1;
+  const float c2 = hp.one_minus_beta2 != 0.f ? hp.one_minus_beta2 : 1.f - hp.beta2;
   const float bc1 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev) : hp.bias_corr1;
   const float bc2 = hp.bias_corr_dev ? __ldg(hp.bias_corr_dev + 1) : hp.bias_corr2;
   const float inv_bc1 = 1.f / bc1, inv_bc2 = 1.f / bc2;

@@ -17,9 +17,8 @@ extern "C" size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K,
   g.causal = causal;
   g.batch0 = batch_items > 0 ? batch_items : 1;
   g.batch1 = 1;
-  const int64_t s = gemm_tc_splits(g);
-  // split partials of C, then of the a_rowsum row sums (R27)
-  return s > 1 ? (size_t)s * ((size_t)M * (size_t)N + (size_t)M) * sizeof(float) : 0;
+  // split partials of C, of the a_rowsum row sums (R27), then the in-kernel reduce's counters
+  return splitk_workspace_bytes(g, gemm_tc_splits(g));
 }
 
 extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const int64_t* batch,

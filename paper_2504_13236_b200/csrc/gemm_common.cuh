@@ -38,6 +38,9 @@ nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);
 // *kernels (optional) receives the number of kernels launched (2 with a split-K reduce).
 nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels = nullptr);
 int64_t gemm_tc_splits(const GemmArgs& a);  // split-K factor the tcgen05 path would use
+// split-K workspace bytes for `splits` (partials + a_rowsum partials + the in-kernel reduce's
+// arrival counters; 0 when splits == 1)
+size_t splitk_workspace_bytes(const GemmArgs& a, int64_t splits);
 
 // Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.
 template <typename TC>

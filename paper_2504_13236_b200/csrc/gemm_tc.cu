@@ -122,6 +122,11 @@ struct TcParams {
   int order;      // TileOrder
   int ws_mode;    // split partials go to the workspace map; bias/beta/residual applied by the reduce
   int in_kind;    // InKind: the epilogue input prefetched a chunk ahead (generic epilogue)
+  // ws_mode with the in-kernel ordered reduce: per (tile, CTA of the pair, epilogue warp) an
+  // arrival counter in the workspace; the last split to arrive adds all partials of its region
+  // in split order and stores C (no reduce kernel)
+  int fused_reduce;
+  uint32_t* counters;
 };
 
 // ------------------------------------------------------------------ PTX helpers
@@ -567,9 +572,9 @@ __device__ __forceinline__ void unstage_row(Raw8& r, const uint8_t* buf, int lan
 template <typename TC, int W>
 __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const TC* auxb, int64_t row, int64_t col0,
                                          bool extras, bool vec, float dval, int in_kind, const Raw8& raw,
-                                         float (&v)[W]) {
+                                         float (&v)[W], bool with_alpha = true) {
   constexpr bool kFast = sizeof(TC) == 2;
-  if (g.alpha != 1.f) {
+  if (with_alpha && g.alpha != 1.f) {
 #pragma unroll
     for (int j = 0; j < W; j += 2) {
       const float2 x = __fmul2_rn(make_float2(v[j], v[j + 1]), f2(g.alpha));
@@ -1342,6 +1347,66 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         acc = 0;
         acc_phase ^= 1;
       }
+      if (P.fused_reduce) {
+        // Ordered split-K reduction in the kernel (R25): this warp's region of the tile (its
+        // lane quadrant's 32 rows x its column chunks) gets one arrival per split; the split that
+        // arrives last adds the partials of all splits in ascending split order -- the same fixed
+        // association whichever CTA that is -- applies beta*C / bias / residual and stores C.
+        uint32_t* cnt = P.counters + ((uint32_t)ti.tile * CG + rank) * kEpiWarps + (uint32_t)(warp - 2);
+        int last = 0;
+        if (lane == 0) {
+          bulk_wait0();  // this warp's partial stores (async proxy) have completed
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          __threadfence();
+          last = atomicAdd(cnt, 1u) == (uint32_t)(P.splits - 1) ? 1 : 0;
+          if (last) {
+            *cnt = 0u;  // every launch leaves its counters zero (the workspace contract)
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+#pragma unroll 1
+          for (int c = half * W; c < BN; c += 2 * W) {
+            if (ti.n0 + c >= g.N) break;  // warp-uniform
+            const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
+            // partial s of this chunk -> staging buffer s & 1 (TMA, 32 rows x 128 B), one ahead
+            auto ld_part = [&](int64_t sp) {
+              const int b = (int)(sp & 1);
+              const uint32_t bar = smem_u32(&inbar[(warp - 2) * kStageBufs + b]);
+              mbar_expect_tx(bar, kStageBytesPerWarp);
+              tma_load_4d(smem_u32(stage_base + b * kStageBytesPerWarp), &tmAux, bar, cx, cy, (int)sp, 0);
+            };
+            if (lane == 0) {
+              bulk_wait_read0();  // earlier stores have read the staging buffers
+              ld_part(0);
+            }
+            __syncwarp();
+            float v[W];
+            Raw8 raw;
+#pragma unroll 1
+            for (int64_t sp = 0; sp < P.splits; ++sp) {
+              const int b = (int)(sp & 1);
+              if (lane == 0 && sp + 1 < P.splits) ld_part(sp + 1);
+              mbar_wait(smem_u32(&inbar[(warp - 2) * kStageBufs + b]), (in_phase >> b) & 1u);
+              in_phase ^= 1u << b;
+              unstage_row(raw, stage_base + b * kStageBytesPerWarp, lane);
+              __syncwarp();  // every lane has read buffer b before it is refilled
+              float t[8];
+#pragma unroll
+              for (int j = 0; j < W; j += 8) {
+                unpack8<float>(raw, j, t);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[j + i] = sp == 0 ? t[i] : v[j + i] + t[i];
+              }
+            }
+            epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, 0.f, IN_NONE, raw, v, false);
+            ring = 0;
+            stage_and_store(&tmC, v, false, cx, cy, (int)q, (int)p);
+          }
+        }
+      }
     }
     if (lane == 0) bulk_wait0();
   }
@@ -1544,6 +1609,30 @@ int64_t pair_units() {
   return units;
 }
 
+}  // namespace
+
+// Split-K workspace: partials [splits][M][N], a_rowsum partials [splits][M], then the arrival
+// counters of the in-kernel reduce (one per tile, CTA of a pair and epilogue warp; bounded by the
+// narrowest tile grid), 16-byte aligned.
+size_t splitk_counter_offset(const GemmArgs& a, int64_t splits) {
+  const size_t b = (size_t)splits * ((size_t)a.M * (size_t)a.N + (size_t)a.M) * sizeof(float);
+  return (b + 15) / 16 * 16;
+}
+size_t splitk_counter_bytes(const GemmArgs& a) {
+  return (size_t)cdiv(a.M, BM) * (size_t)cdiv(a.N, 64) * kEpiWarps * sizeof(uint32_t);
+}
+size_t splitk_workspace_bytes(const GemmArgs& a, int64_t splits) {
+  return splits > 1 ? splitk_counter_offset(a, splits) + splitk_counter_bytes(a) : 0;
+}
+// The reduce runs in the GEMM when the workspace holds the counters, C is TMA-storable and no
+// a_rowsum is requested (that keeps the separate ordered reduce kernel).
+bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
+  return splits > 1 && !a.a_rowsum && a.workspace_bytes >= splitk_workspace_bytes(a, splits) &&
+         c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
+}
+
+namespace {
+
 template <int BN, typename TC, int EPI, int CG = 1>
 nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   using C = Cfg<BN, CG, EPI>;
@@ -1582,6 +1671,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.f_level.init(P.num_tiles / P.mt);
   P.f_b1.init(a.batch1);
   P.ws_mode = splits > 1 ? 1 : 0;
+  P.fused_reduce = splits > 1 && fused_reduce_ok(a, splits) ? 1 : 0;
+  P.counters = P.fused_reduce ? (uint32_t*)((char*)a.workspace + splitk_counter_offset(a, splits)) : nullptr;
   // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
   if (P.ws_mode || !generic_epi(EPI))
     P.in_kind = IN_NONE;
@@ -1623,6 +1714,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     P.tma_store = 1;
     NNT_TRY(make_map(&tmAux, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.workspace, a.N, a.M, a.N, splits, a.M * a.N, 1, 0,
                      32, 32));
+    if (P.fused_reduce)  // C (fp32) stored by the last split of each region
+      NNT_TRY(make_map(&tmC, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.C, a.N, a.M, a.ldc, 1, 0, 1, 0, 32, 32));
   } else if (EPI == EPI_ROWSTATS) {
     P.tma_store = 0;  // no C
   } else {
@@ -1662,7 +1755,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     NNT_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, TC, EPI, CG>, P, tmA, tmB, tmC, tmAux));
   }
   NNT_TRY(check_launch("gemm_tc"));
-  if (P.ws_mode) {
+  if (P.ws_mode && !P.fused_reduce) {
     const int64_t total = a.M * (a.N / 4);
     int64_t blocks = cdiv(total, 256);
     if (blocks > 8 * num_sms()) blocks = 8 * num_sms();
@@ -1852,7 +1945,7 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
                      (!a.residual || ((reinterpret_cast<uintptr_t>(a.residual) & 15u) == 0 && a.ld_res % 4 == 0)) &&
                      (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);
   if (!ws_ok) splits = 1;
-  if (kernels) *kernels = splits > 1 ? 2 : 1;
+  if (kernels) *kernels = splits > 1 && !fused_reduce_ok(a, splits) ? 2 : 1;
   if (a.act == NNT_ACT_ROWSTATS) return launch_bn<128, float, EPI_ROWSTATS>(a, s, 1);
   if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits);
   return launch_tc<__nv_bfloat16>(a, s, splits);

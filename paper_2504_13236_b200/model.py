@@ -220,7 +220,7 @@ class BlockStack:
             self._grads.append(self._make_grads(l))
         saved_b, scratch_b = nnt.nnt_block_workspace_size(self.bcfg)
         self.saved = [torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for _ in range(cfg.L)]
-        self.scratch = torch.empty(scratch_b, device=self.dev, dtype=torch.uint8)
+        self.scratch = torch.zeros(scratch_b, device=self.dev, dtype=torch.uint8)  # zero: split-K counters
         act = dict(device=self.dev, dtype=torch.float32)
         self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
         self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
@@ -343,8 +343,7 @@ class BlockStack:
 
     def _hparams(self, t):
         c = self.cfg
-        return nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0 - c.beta1 ** t,
-                                    1.0 - c.beta2 ** t, 1.0)
+        return nnt.adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, t)
 
     def _adam_range(self, b0, b1, t, stream=None):
         self._update(b0, b1, b0, t, stream, shadow=True)
@@ -417,7 +416,7 @@ class BlockStack:
             self.t_dev = torch.tensor([self.step_count], device=dev, dtype=torch.int64)
             self.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
         c = self.cfg
-        hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
+        hp = nnt.adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay)
         hp.bias_corr_dev = self.bc_dev.data_ptr()
         if self.dp:  # the communicator must exist before capture: one eager collective on the comm stream
             with torch.cuda.stream(self.comm):
@@ -516,7 +515,7 @@ class GPT2Model:
         # split-K workspace of dh_f = dlogits wte (K = V: the library splits K when the tile grid
         # fills its last round badly); None when the library would not split
         wsb = nnt.nnt_tile_gemm_workspace_bytes(T, E, V, nnt.NNT_F32) if self.bf16 else 0
-        self.dh_ws = torch.empty(wsb, device=self.dev, dtype=torch.uint8) if wsb else None
+        self.dh_ws = torch.zeros(wsb, device=self.dev, dtype=torch.uint8) if wsb else None  # zero: counters
         self.dh_epi = nnt.make_epilogue(workspace=self.dh_ws) if wsb else None
         self.lnf_scr = torch.empty(nnt.nnt_layernorm_bwd_scratch_bytes(T, E), device=self.dev, dtype=torch.uint8)
         self.emb_scr = torch.empty(nnt.nnt_embedding_bwd_scratch_bytes(T, V), device=self.dev, dtype=torch.uint8)
@@ -641,7 +640,7 @@ class GPT2Model:
         if not hasattr(st, "t_dev"):
             st.t_dev = torch.tensor([st.step_count], device=dev, dtype=torch.int64)
             st.bc_dev = torch.zeros(2, device=dev, dtype=torch.float32)
-        hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0, 1.0, 1.0)
+        hp = nnt.adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay)
         hp.bias_corr_dev = st.bc_dev.data_ptr()
         if st.dp:
             with torch.cuda.stream(st.comm):

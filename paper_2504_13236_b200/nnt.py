@@ -68,7 +68,19 @@ class nnt_epilogue(C.Structure):
 
 class nnt_adam_hparams(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("lr", "beta1", "beta2", "eps", "weight_decay", "bias_corr1",
-                                          "bias_corr2", "grad_scale")] + [("bias_corr_dev", C.c_void_p)]
+                                          "bias_corr2", "grad_scale")] + [("bias_corr_dev", C.c_void_p),
+                                                                          ("one_minus_beta1", C.c_float),
+                                                                          ("one_minus_beta2", C.c_float)]
+
+
+def adam_hparams(lr, beta1, beta2, eps, weight_decay=0.0, t=None, grad_scale=1.0):
+    """nnt_adam_hparams with the caller-side fp64 terms (R12, R23): bias corrections 1 - beta^t
+    (1.0 when t is None: the device-side corrections of a captured graph are used) and 1 - beta."""
+    bc1, bc2 = (1.0, 1.0) if t is None else (1.0 - beta1 ** t, 1.0 - beta2 ** t)
+    hp = nnt_adam_hparams(lr, beta1, beta2, eps, weight_decay, bc1, bc2, grad_scale)
+    hp.one_minus_beta1 = 1.0 - beta1
+    hp.one_minus_beta2 = 1.0 - beta2
+    return hp
 
 
 class nnt_block_cfg(C.Structure):

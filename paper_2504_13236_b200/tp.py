@@ -111,7 +111,7 @@ class TPBlockStack:
         self._grads = [self._make_grads(l) for l in range(cfg.L)]
         saved_b, scratch_b = nnt.nnt_block_tp_workspace_size(self.bcfg, self.tp)
         self.saved = [torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for _ in range(cfg.L)]
-        self.scratch = torch.empty(scratch_b, device=self.dev, dtype=torch.uint8)
+        self.scratch = torch.zeros(scratch_b, device=self.dev, dtype=torch.uint8)  # zero: split-K counters
         act = dict(device=self.dev, dtype=torch.float32)
         self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
         self.x1 = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L)]
@@ -190,8 +190,7 @@ class TPBlockStack:
         if c.optimizer == "sgd":
             nnt.nnt_sgd_step(self.numel, self.w, self.g, self.m, self.w16, c.lr, c.momentum, c.weight_decay)
             return
-        hp = nnt.nnt_adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, 1.0 - c.beta1 ** t,
-                                  1.0 - c.beta2 ** t, 1.0)
+        hp = nnt.adam_hparams(c.lr, c.beta1, c.beta2, c.eps, c.weight_decay, t)
         nnt.nnt_adam_step(self.numel, self.w, self.g, self.m, self.v, self.w16, hp)
 
     def train_step(self, x=None, r=None):

@@ -49,6 +49,27 @@ def close(got, want, tol, what="", max_tol=None):
     return r, m
 
 
+def close_update(got_delta, want_delta, w_ref, rms_g, tol, what=""):
+    """Parity of an Adam parameter update Δw = w_new - w_old (reading R32).
+
+    Norm-wise over every element: ||Δ - Δref|| / ||Δref|| < tol.  Element-wise only where the
+    update is well conditioned, i.e. where the gradient history is not tiny: Adam's step
+    lr*m̂/(sqrt(v̂)+eps) has sensitivity ~ lr*eps*δg/|g|^2 to a gradient error δg, unbounded as
+    |g| -> 0 (at step 1 an element with |g| ~ 1e-7 turns a 1e-9 gradient rounding into a 1e-3 change
+    of its update), so elements whose RMS gradient rms_g (= sqrt(v) of the oracle's Adam state,
+    or |g| for one step) is below 1e-3 of the tensor's largest are left to the norm-wise bound;
+    the element-wise bound adds the fp32 storage rounding of w_new, 2^-23 * max|w| / max|Δref|."""
+    got = np.asarray(got_delta, np.float64).ravel()
+    want = np.asarray(want_delta, np.float64).ravel()
+    rms = np.abs(np.asarray(rms_g, np.float64)).ravel()
+    close(got, want, tol, what, max_tol=np.inf)
+    keep = rms >= 1e-3 * rms.max() if rms.size else rms.astype(bool)
+    if not keep.any():
+        return
+    storage = 2.0 ** -23 * np.abs(np.asarray(w_ref, np.float64)).max() / max(np.abs(want).max(), 1e-300)
+    close(got[keep], want[keep], np.inf, f"{what} (well-conditioned elements)", max_tol=tol + storage)
+
+
 def dev(a, dtype=torch.float32):
     return torch.as_tensor(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
 

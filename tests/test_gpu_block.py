@@ -11,7 +11,7 @@ import torch
 
 import nnt_inputs
 from oracle import dense
-from gpu_util import close, bf16_round, dev, host, rel
+from gpu_util import close, close_update, bf16_round, dev, host, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -32,14 +32,15 @@ def _stack(cfg_name, L=1, B=None, S=None, dtype=None, tile=None, init="parity", 
     return sc, layers, model.BlockStack(sc, layers)
 
 
-def _update_close(got_delta, want_delta, g_ref, tol, what=""):
-    """close() on an Adam update, skipping elements whose exact gradient is zero.
+def _update_close(got_delta, want_delta, g_ref, w_ref, rms_g, tol, what=""):
+    """close_update on an Adam update, skipping elements whose exact gradient is zero.
 
     The key-bias gradient is exactly zero in exact arithmetic (softmax is invariant to a
     per-query constant shift of the scores; tests/test_oracle_pins.py pins it), so Adam's
     g/(|g|+eps) turns fp32 noise there into O(lr) updates in either implementation."""
     keep = np.abs(g_ref) > 1e-9 * max(np.abs(g_ref).max(), 1e-300)
-    return close(np.asarray(got_delta)[keep], np.asarray(want_delta)[keep], tol, what)
+    return close_update(np.asarray(got_delta)[keep], np.asarray(want_delta)[keep], np.asarray(w_ref)[keep],
+                        np.asarray(rms_g)[keep], tol, what)
 
 
 def _oracle_step(layers, x, r, H, T):
@@ -72,7 +73,7 @@ def test_tiny_fp32_fwd_bwd_adam(tile):
     torch.cuda.synchronize()
     for n, wv in st.params_of(0).items():
         w1, _, _ = dense.adam_step(w0[n], g_ref[0][n], np.zeros_like(w0[n]), np.zeros_like(w0[n]), 1)
-        _update_close(host(wv) - w0[n], w1 - w0[n], g_ref[0][n], 1e-4, n)
+        _update_close(host(wv) - w0[n], w1 - w0[n], g_ref[0][n], w0[n], g_ref[0][n], 1e-4, n)
     kb = host(st.grads_of(0)["b_qkv"])[c.E:2 * c.E]
     assert np.abs(kb).max() <= 1e-5 * np.abs(host(st.grads_of(0)["b_qkv"])).max()
 
@@ -95,7 +96,7 @@ def test_tiny_fp32_three_training_steps():
             P[0][k], m[k], v_[k] = dense.adam_step(P[0][k], g[0][k], m[k], v_[k], t)
     w_init = layers[0]
     for n, wv in st.params_of(0).items():
-        _update_close(host(wv) - w_init[n], P[0][n] - w_init[n], m[n], 1e-4, n)
+        _update_close(host(wv) - w_init[n], P[0][n] - w_init[n], m[n], P[0][n], np.sqrt(v_[n]), 1e-4, n)
 
 
 @pytest.mark.parametrize("S,B", [(256, 2), (1024, 1)])

@@ -159,18 +159,49 @@ def test_gemm_split_k_workspace_bit_exact(M, N):
     c0 = nnt_inputs.make_matrix((M, N), seed=5, kind="int")
     nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
     assert nb > 0  # the library splits these shapes
-    ws = torch.empty(nb, device="cuda", dtype=torch.uint8)
-    epi = nnt.make_epilogue(workspace=ws)
+    # full size, zero-filled: the in-kernel ordered reduce (arrival counters at the end); run
+    # three times -- every launch must leave its counters zero for the next
+    ws = torch.zeros(nb, device="cuda", dtype=torch.uint8)
     A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
     want = tiled.gemm_tiled(a.T, b, 256, 256, 1024) + c0
-    outs = []
-    for _ in range(2):
+    # the partials alone (no counter space): the separate reduce kernel
+    nparts = nb - ((-(-M // 128)) * (-(-N // 64)) * 8 * 4)
+    ws_small = torch.empty(nparts, device="cuda", dtype=torch.uint8)
+    for w in (ws, ws_small):
+        epi = nnt.make_epilogue(workspace=w)
+        for _ in range(3):
+            Cm = dev(c0)
+            nnt.nnt_tile_gemm(1, 0, M, N, K, None, 1.0, A, 1, M, None, B, 1, N, None, 1.0, Cm, 0, N, None, None, epi)
+            torch.cuda.synchronize()
+            assert np.array_equal(host(Cm), want)
+    assert int(ws[-(-(-M // 128)) * (-(-N // 64)) * 8 * 4:].count_nonzero()) == 0  # counters back to zero
+
+
+@pytest.mark.parametrize("M,N", [(768, 768), (2304, 768)])
+def test_gemm_split_k_real_data_extras(M, N):
+    """Split-K with real-valued data and every extra the ordered reduce applies (alpha, beta*C, bias,
+    fp32 residual): in-kernel reduce vs separate reduce kernel vs the fp64 product."""
+    K = 8192
+    rng = np.random.default_rng(M + N)
+    a = bf16_round(rng.standard_normal((K, M)))
+    b = bf16_round(rng.standard_normal((K, N)))
+    c0 = rng.standard_normal((M, N)).astype(np.float32)
+    bias = rng.standard_normal(N).astype(np.float32)
+    res = rng.standard_normal((M, N)).astype(np.float32)
+    nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
+    nparts = nb - ((-(-M // 128)) * (-(-N // 64)) * 8 * 4)
+    A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
+    want = 0.5 * (a.T @ b) + bias + 0.75 * c0 + res
+    got = []
+    Bias, Res = dev(bias), dev(res)  # alive until the launches have run
+    for w in (torch.zeros(nb, device="cuda", dtype=torch.uint8), torch.empty(nparts, device="cuda", dtype=torch.uint8)):
+        epi = nnt.make_epilogue(workspace=w, bias=Bias, residual=Res, ld_residual=N)
         Cm = dev(c0)
-        nnt.nnt_tile_gemm(1, 0, M, N, K, None, 1.0, A, 1, M, None, B, 1, N, None, 1.0, Cm, 0, N, None, None, epi)
+        nnt.nnt_tile_gemm(1, 0, M, N, K, None, 0.5, A, 1, M, None, B, 1, N, None, 0.75, Cm, 0, N, None, None, epi)
         torch.cuda.synchronize()
-        outs.append(host(Cm))
-    assert np.array_equal(outs[0], want)
-    assert np.array_equal(outs[0], outs[1])
+        got.append(host(Cm))
+        close(got[-1], want, 1e-5)
+    close(got[0], got[1], 1e-6)
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0), (1, 1)])
@@ -201,7 +232,7 @@ def test_gemm_a_rowsum_bias_grad_bit_exact(M, N, K, ta, beta):
     c0 = nnt_inputs.make_matrix((M, N), seed=7, kind="int")
     r0 = nnt_inputs.make_matrix((M,), seed=8, kind="int")
     nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
-    ws = torch.empty(max(nb, 16), device="cuda", dtype=torch.uint8)
+    ws = torch.zeros(max(nb, 16), device="cuda", dtype=torch.uint8)
     rs = dev(r0)
     epi = nnt.make_epilogue(workspace=ws if nb else None, a_rowsum=rs)
     A, B, Cm = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(c0)

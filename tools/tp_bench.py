@@ -48,7 +48,7 @@ def main():
             setattr(G, n, g[n].data_ptr())
         sb, kb = nnt.nnt_block_tp_workspace_size(cfg, t)
         saved = torch.empty(sb, device="cuda", dtype=torch.uint8)
-        scratch = torch.empty(kb, device="cuda", dtype=torch.uint8)
+        scratch = torch.zeros(kb, device="cuda", dtype=torch.uint8)
         x = torch.randn(B, S, E, device="cuda")
         dy = torch.randn(B, S, E, device="cuda") / T
         x1, y, dh, dx = (torch.empty_like(x) for _ in range(4))
