@@ -162,10 +162,12 @@ typedef struct {
  * split s writes alpha * (its K-range partial) to workspace slice s and an ordered reduce
  * forms C = beta*C + sum_s partial_s (+bias, +residual), splits added in ascending order (R25).
  * The reduce runs inside the GEMM: the last split to finish each output region adds the
- * partials; the arrival counters it uses sit at the end of this workspace.
- * CONTRACT: a workspace of this size must be ZERO-FILLED before its first use (e.g.
- * torch.zeros); every call leaves the counters zero again.  A smaller workspace that still holds
- * the partials is accepted and reduces with a separate kernel launch instead. */
+ * partials; the arrival counters it uses sit in the last 16 KB of the workspace (as sized by the
+ * caller's workspace_bytes, which must stay the same for a buffer; GEMMs of different shapes may
+ * share one workspace sized for the largest).
+ * CONTRACT: that zone must be ZERO before the first use (e.g. torch.zeros for the whole buffer);
+ * every call leaves it zero again.  A smaller workspace that still holds the partials is accepted
+ * and reduces with a separate kernel launch instead. */
 size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K, int c_dtype, int act, int causal,
                                      int64_t batch_items);
 
@@ -278,8 +280,8 @@ size_t nnt_layernorm_bwd_scratch_bytes(int64_t T, int64_t E);
  * fp32 [T][lddx] or NULL (residual-stream gradient added to dx; may alias dx);
  * dx: device fp32 [T][lddx]; dx_bf16: device bf16 [T][lddx] copy of dx or NULL;
  * dgamma, dbeta: device fp32 [E]; dx_colsum: NULL or device fp32 [E] (+)= sum_t dx, the
- * bias gradient of the linear layer that produced this LayerNorm's input (E <= 1024 only,
- * else NNT_ERR_UNSUPPORTED); accumulate_params != 0 adds into dgamma / dbeta / dx_colsum.
+ * bias gradient of the linear layer that produced this LayerNorm's input; accumulate_params
+ * != 0 adds into dgamma / dbeta / dx_colsum.  E <= 8192.
  */
 nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int64_t ldx,
                              const float* mean, const float* rstd, const float* gamma,
@@ -454,7 +456,7 @@ typedef struct {
   const void* dy_bf16;  /* bf16 copy of dy made by the caller (the layer above's dx_bf16), or NULL */
   int dy_colsum_done;   /* != 0: g->b_pr already holds (+)= sum_t dy (the layer above's dx_colsum) */
   float* dx_colsum;     /* NULL or [E]: (+)= sum_t dx, the output-projection bias gradient of the
-                           layer below (follows accumulate_grads; E <= 1024) */
+                           layer below (follows accumulate_grads) */
   void* dx_bf16;        /* NULL or bf16 [T][E]: copy of dx for the layer below (bf16 path) */
 } nnt_block_bwd_links;
 nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,

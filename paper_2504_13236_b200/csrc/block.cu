@@ -113,7 +113,7 @@ struct Ctx {
   cudaStream_t st;
   cudaStream_t side;  // nnt_block_bwd_streams: weight/bias-gradient ops run here (or NULL)
   const nnt_block_bwd_links* links;  // nnt_block_bwd_streams: fused cross-layer bias sums (or NULL)
-  bool ln_rows;                      // E <= 1024: the LayerNorm row kernel (column sums of dx fusable)
+  bool ln_rows;                      // the LayerNorm backward fuses the column sums of dx (every E)
   template <typename P>
   P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
   template <typename P>
@@ -250,7 +250,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
                   nullptr, 0.f, x.dh, NNT_F32, E, nullptr, nullptr);
     case NNT_OP_LN2_BWD:
-      // b_o's gradient sum_t dx1 is the column sum of this LayerNorm's output: fused (E <= 1024)
+      // b_o's gradient sum_t dx1 is the column sum of this LayerNorm's output: fused
       return nnt_layernorm_bwd(x.dh, E, x.x1, E, x.s<float>(x.L.mean2),
                                x.s<float>(x.L.rstd2), p->ln2_g, T, E, dy, x.k<float>(x.L.dx1), E,
                                bf ? x.k<void>(x.L.dx116) : nullptr, g->ln2_g, g->ln2_b, x.ln_rows ? g->b_o : nullptr,
@@ -345,7 +345,7 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.st = st;
   x.side = nullptr;
   x.links = nullptr;
-  x.ln_rows = c.E <= 1024;
+  x.ln_rows = true;
   return x;
 }
 
@@ -482,8 +482,6 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
   NNT_REQUIRE(plan != nullptr, NNT_ERR_SHAPE, "nnt_block_bwd: %s", nnt_last_error());
   NNT_TRY(check_plan(plan));
   Ctx c = make_ctx(*cfg, const_cast<void*>(saved), scratch, stream);
-  NNT_REQUIRE(!links || !links->dx_colsum || c.ln_rows, NNT_ERR_UNSUPPORTED,
-              "nnt_block_bwd_streams: links.dx_colsum needs E <= 1024");
   NNT_REQUIRE(!links || !links->dx_bf16 || cfg->dtype == NNT_BF16, NNT_ERR_DTYPE,
               "nnt_block_bwd_streams: links.dx_bf16 is for the bf16 path");
   c.links = links;

@@ -57,11 +57,15 @@ constexpr int kBarBytes = kOnesOff + kOnesBytes;
 //   EPI_ROWSTATS per-row (max, sumexp) over all key tiles of a row block (ORDER_ROWS tasks),
 //                no C (softmax subroutine 1 with on-chip aggregation, R26)
 //   EPI_SOFTMAX  bf16 C = e^{alpha*acc - M} / S from the row's stats (subroutine 2, R26)
-enum EpiMode { EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4, EPI_GENERIC_RS = 5 };
+enum EpiMode {
+  EPI_GENERIC = 0, EPI_SCORES = 1, EPI_DA = 2, EPI_ROWSTATS = 3, EPI_SOFTMAX = 4, EPI_GENERIC_RS = 5, EPI_SPLITK = 6
+};
+// EPI_SPLITK: the generic epilogue of a split-K GEMM (fp32 C) with the in-kernel ordered reduce;
+// its own instantiation, so the reduce's registers do not weigh on the unsplit GEMMs.
 // EPI_GENERIC_RS: the generic epilogue plus the a_rowsum ones-vector MMAs (R27).  A separate
 // instantiation: even predicated off, the extra tcgen05.mma issue sequences in the MMA loop cost
 // ~30% of the single-thread issue rate (measured 422 -> 286 ns per K-block of a lone tile).
-constexpr bool generic_epi(int e) { return e == EPI_GENERIC || e == EPI_GENERIC_RS; }
+constexpr bool generic_epi(int e) { return e == EPI_GENERIC || e == EPI_GENERIC_RS || e == EPI_SPLITK; }
 
 // CG = CTAs per MMA (tcgen05 cta_group): 1, or 2 = an SM pair computing a 256 x BN tile
 // (each CTA stages its 128 A rows and half of the BN B rows; the leader issues M=256 MMAs).
@@ -1266,8 +1270,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           }
         }
         const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
-        if (P.ws_mode) {
-          // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce kernel
+        if (EPI == EPI_SPLITK || P.ws_mode) {
+          // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce
           epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, 0.f, IN_NONE, raw, v);
           stage_and_store(&tmAux, v, true, cx, cy, (int)ti.split, 0);
           continue;
@@ -1347,6 +1351,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         acc = 0;
         acc_phase ^= 1;
       }
+      if constexpr (EPI == EPI_SPLITK) {
       if (P.fused_reduce) {
         // Ordered split-K reduction in the kernel (R25): this warp's region of the tile (its
         // lane quadrant's 32 rows x its column chunks) gets one arrival per split; the split that
@@ -1406,6 +1411,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             stage_and_store(&tmC, v, false, cx, cy, (int)q, (int)p);
           }
         }
+      }
       }
     }
     if (lane == 0) bulk_wait0();
@@ -1611,24 +1617,30 @@ int64_t pair_units() {
 
 }  // namespace
 
-// Split-K workspace: partials [splits][M][N], a_rowsum partials [splits][M], then the arrival
-// counters of the in-kernel reduce (one per tile, CTA of a pair and epilogue warp; bounded by the
-// narrowest tile grid), 16-byte aligned.
-size_t splitk_counter_offset(const GemmArgs& a, int64_t splits) {
+// Split-K workspace: partials [splits][M][N] and a_rowsum partials [splits][M] from the start;
+// the arrival counters of the in-kernel reduce in a fixed zone of kSplitCounters words at the END
+// of the workspace as the caller sizes it (16-byte aligned down), so GEMMs of different shapes
+// sharing one workspace (the block's four dW GEMMs) all find their counters in the same zone,
+// never under another shape's partials.  One counter per (tile, CTA of a pair, epilogue warp).
+constexpr int64_t kSplitCounters = 4096;
+size_t splitk_partial_bytes(const GemmArgs& a, int64_t splits) {
   const size_t b = (size_t)splits * ((size_t)a.M * (size_t)a.N + (size_t)a.M) * sizeof(float);
   return (b + 15) / 16 * 16;
 }
-size_t splitk_counter_bytes(const GemmArgs& a) {
-  return (size_t)cdiv(a.M, BM) * (size_t)cdiv(a.N, 64) * kEpiWarps * sizeof(uint32_t);
-}
 size_t splitk_workspace_bytes(const GemmArgs& a, int64_t splits) {
-  return splits > 1 ? splitk_counter_offset(a, splits) + splitk_counter_bytes(a) : 0;
+  return splits > 1 ? splitk_partial_bytes(a, splits) + (size_t)kSplitCounters * sizeof(uint32_t) : 0;
 }
-// The reduce runs in the GEMM when the workspace holds the counters, C is TMA-storable and no
-// a_rowsum is requested (that keeps the separate ordered reduce kernel).
+uint32_t* splitk_counters(const GemmArgs& a) {
+  const uintptr_t end = (reinterpret_cast<uintptr_t>(a.workspace) + a.workspace_bytes) & ~uintptr_t(15);
+  return reinterpret_cast<uint32_t*>(end - (size_t)kSplitCounters * sizeof(uint32_t));
+}
+// The reduce runs in the GEMM when the workspace holds partials + counter zone, the tile grid's
+// counters fit the zone (split GEMMs use 256-wide tiles), C is TMA-storable and no a_rowsum is
+// requested (that keeps the separate ordered reduce kernel).
 bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
+  const int64_t regions = (cdiv(a.M, BM) + 1) * cdiv(a.N, 256) * kEpiWarps;
   return splits > 1 && !a.a_rowsum && a.workspace_bytes >= splitk_workspace_bytes(a, splits) &&
-         c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
+         regions <= kSplitCounters && c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
 }
 
 namespace {
@@ -1661,6 +1673,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.splits = splits;
   P.kb_per_split = cdiv(nkb, P.splits);
   P.num_tasks = P.num_tiles * P.splits;
+  NNT_REQUIRE(!P.fused_reduce || P.num_tiles * CG * kEpiWarps <= kSplitCounters, NNT_ERR_UNSUPPORTED,
+              "gemm(bf16): split-K counters");
   NNT_REQUIRE(P.num_tasks < (1ll << 31), NNT_ERR_UNSUPPORTED, "gemm(bf16): %lld tile tasks (> 2^31)",
               (long long)P.num_tasks);
   P.f_splits.init(P.splits);
@@ -1671,8 +1685,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.f_level.init(P.num_tiles / P.mt);
   P.f_b1.init(a.batch1);
   P.ws_mode = splits > 1 ? 1 : 0;
-  P.fused_reduce = splits > 1 && fused_reduce_ok(a, splits) ? 1 : 0;
-  P.counters = P.fused_reduce ? (uint32_t*)((char*)a.workspace + splitk_counter_offset(a, splits)) : nullptr;
+  P.fused_reduce = EPI == EPI_SPLITK ? 1 : 0;
+  P.counters = P.fused_reduce ? splitk_counters(a) : nullptr;
   // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
   if (P.ws_mode || !generic_epi(EPI))
     P.in_kind = IN_NONE;
@@ -1907,9 +1921,15 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     if (getenv("NNT_DEBUG_GEMM"))
       fprintf(stderr, "gemm_tc %lldx%lldx%lld: pair BN %d cost %.0f, single BN %d cost %.0f\n", (long long)a.M,
               (long long)a.N, (long long)a.K, bnp, cost_pair, bns, cost_single);
+    if constexpr (sizeof(TC) == 4) {
+      if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 2>(a, s, splits);
+    }
     if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single)  // ties go to pairs
       return bnp == 256 || splits > 1 ? launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits)
                                       : launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+  }
+  if constexpr (sizeof(TC) == 4) {
+    if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 1>(a, s, splits);
   }
   switch (splits > 1 ? 256 : choose_bn(a, sizeof(TC))) {
     case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);

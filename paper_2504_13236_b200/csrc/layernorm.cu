@@ -2,7 +2,8 @@
 //   E <= 1024: one WARP per token row (row in registers as float4, reductions by
 //              warp shuffle only); forward warps stride over rows with the next row
 //              prefetched, backward CTAs own a block of rows (single pass);
-//   E  > 1024: one 128-thread CTA per row (shuffle + 4-entry shared array).
+//   E  > 1024: forward one 128-thread CTA per row (shuffle + 4-entry shared array);
+//              backward a group of 4 or 8 warps per row, persistent CTAs (ln_bwd_groups).
 // The backward's dgamma/dbeta are per-CTA column partials (rows of a CTA are
 // accumulated in a fixed order) merged by the deterministic column merge
 // (reduce.cuh): bitwise reproducible, no atomics.
@@ -13,7 +14,7 @@ namespace {
 
 constexpr int kWarpRowsPerCta = 8;   // warp kernels: 8 warps
 constexpr int kT = 128;              // CTA-per-row kernels: threads
-constexpr int kCtaBwdRows = 16;      // CTA-per-row bwd kernel: rows per partial
+constexpr int kCtaBwdRows = 16;      // backward kernels: at least this many rows per partial
 
 template <typename T>
 __device__ __forceinline__ void store4(T* p, float4 v);
@@ -265,72 +266,162 @@ __global__ void __launch_bounds__(32 * kRowsWarps, 2)
   }
 }
 
-// ------------------------------------------------------------------ backward, CTA per row
-template <int NV>
-__global__ void __launch_bounds__(kT) ln_bwd_cta(const float* __restrict__ dy, int64_t lddy,
-                                                 const float* __restrict__ x, int64_t ldx,
-                                                 const float* __restrict__ mean, const float* __restrict__ rstd,
-                                                 const float* __restrict__ gamma, int64_t T, int64_t E,
-                                                 const float* dres, float* dx, int64_t lddx,
-                                                 __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg,
-                                                 float* __restrict__ pb) {
+// ------------------------------------------------------------------ backward, warp groups per row
+// E > 1024: a row is split over a group of G warps (float4 column i4 = lane + 32 (k + G j) for
+// warp k of the group, so each warp streams contiguous 512-byte pieces); the CTA's 8 warps form
+// 8 / G groups that stride over the CTA's rows.  The next row's x / dy / residual-gradient loads
+// are issued before the current row's reductions (double-buffered registers), the per-row sums
+// sa, sb cross the group's warps through double-buffered shared slots with one named barrier per
+// row, and dgamma / dbeta (/ sum_t dx) accumulate in registers over the group's rows; the groups
+// are combined in fixed order at the end into one partial row per CTA (deterministic, merged by
+// the column merge like the row kernel).  One CTA per SM, persistent over rows.
+constexpr int kGrpWarps = 8;
+
+template <int NV, int G, bool SUM>
+__global__ void __launch_bounds__(32 * kGrpWarps, 1)
+    ln_bwd_groups(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
+                  const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
+                  int64_t T, int E, int64_t rows_per_cta, const float* __restrict__ dres, float* __restrict__ dx,
+                  int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb,
+                  float* __restrict__ ps) {
   NNT_PDL_ENTRY();
-  __shared__ float sh[kT / 32];
-  float4 accg[NV], accb[NV], g4[NV];
+  constexpr int NG = kGrpWarps / G;  // row groups per CTA
+  constexpr int NP = SUM ? 3 : 2;
+  extern __shared__ float4 red[];    // [NG][NP][E/4] at the end
+  __shared__ float2 xs[2][NG][G];    // per-row (sa, sb) of each warp, double-buffered
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = w / G, k = w % G;
+  const int E4 = E / 4;
+  const float inv_e = 1.0f / (float)E;
+  // NV <= 4: the next row prefetched and gamma held in registers; NV > 4 (E > 4096): neither
+  // (register budget of one 256-thread CTA per SM)
+  constexpr bool PREF = NV <= 4;
+  float4 ag[NV], ab[NV], as[SUM ? NV : 1], gm[PREF ? NV : 1];
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    accg[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    accb[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-    int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-    if (col < E) g4[j] = ldg4(gamma + col);
+    ag[j] = ab[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (SUM) as[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int i4 = lane + 32 * (k + G * j);
+    if constexpr (PREF) gm[j] = i4 < E4 ? ldg4(gamma + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const int64_t r0 = (int64_t)blockIdx.x * kCtaBwdRows;
-  const int64_t r1 = min(r0 + kCtaBwdRows, T);
-  const float inv_e = 1.0f / (float)E;
-  for (int64_t row = r0; row < r1; ++row) {
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(r0 + rows_per_cta, T);
+  float4 xv[NV], dv[NV], rv[NV];
+  auto load = [&](int64_t row, float4 (&a)[NV], float4 (&b)[NV], float4 (&c)[NV]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * (k + G * j);
+      if (i4 < E4) {
+        a[j] = ldg4(x + row * ldx + 4 * i4);
+        b[j] = ldg4(dy + row * lddy + 4 * i4);
+        c[j] = dres ? ldg4(dres + row * lddx + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  };
+  int64_t row = r0 + grp;
+  if (row < r1) load(row, xv, dv, rv);
+  int buf = 0;
+  for (; row < r1; row += NG, buf ^= 1) {
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
-    RowGrad rg[NV];
+    float4 xn[PREF ? NV : 1], dn[PREF ? NV : 1], rn[PREF ? NV : 1];
+    const int64_t nrow = row + NG;
+    if constexpr (PREF) {
+      if (nrow < r1) load(nrow, xn, dn, rn);  // next row in flight during this one's reductions
+    }
     float sa = 0.f, sb = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-      if (col < E) {
-        float4 xv = ldg4(x + row * ldx + col);
-        float4 d = ldg4(dy + row * lddy + col);
-        rg[j].xh = make_float4((xv.x - mu) * rs, (xv.y - mu) * rs, (xv.z - mu) * rs, (xv.w - mu) * rs);
-        rg[j].dxh = make_float4(d.x * g4[j].x, d.y * g4[j].y, d.z * g4[j].z, d.w * g4[j].w);
-        sa += (rg[j].dxh.x + rg[j].dxh.y) + (rg[j].dxh.z + rg[j].dxh.w);
-        sb += (rg[j].dxh.x * rg[j].xh.x + rg[j].dxh.y * rg[j].xh.y) +
-              (rg[j].dxh.z * rg[j].xh.z + rg[j].dxh.w * rg[j].xh.w);
-        accg[j].x += d.x * rg[j].xh.x; accg[j].y += d.y * rg[j].xh.y;
-        accg[j].z += d.z * rg[j].xh.z; accg[j].w += d.w * rg[j].xh.w;
-        accb[j].x += d.x; accb[j].y += d.y; accb[j].z += d.z; accb[j].w += d.w;
+      const int i4 = lane + 32 * (k + G * j);
+      if (i4 < E4) {
+        const float4 d = dv[j];
+        float4& h = xv[j];
+        h = make_float4((h.x - mu) * rs, (h.y - mu) * rs, (h.z - mu) * rs, (h.w - mu) * rs);
+        ag[j].x += d.x * h.x; ag[j].y += d.y * h.y; ag[j].z += d.z * h.z; ag[j].w += d.w * h.w;
+        ab[j].x += d.x; ab[j].y += d.y; ab[j].z += d.z; ab[j].w += d.w;
+        float4 gj;
+        if constexpr (PREF)
+          gj = gm[j];
+        else
+          gj = ldg4(gamma + 4 * i4);
+        const float4 e = make_float4(d.x * gj.x, d.y * gj.y, d.z * gj.z, d.w * gj.w);  // dxhat
+        dv[j] = e;
+        sa += (e.x + e.y) + (e.z + e.w);
+        sb += (e.x * h.x + e.y * h.y) + (e.z * h.z + e.w * h.w);
       }
     }
-    sa = block_sum(sa, sh) * inv_e;
-    sb = block_sum(sb, sh) * inv_e;
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) xs[buf][grp][k] = make_float2(sa, sb);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * G) : "memory");
+    sa = 0.f;
+    sb = 0.f;
+#pragma unroll
+    for (int i = 0; i < G; ++i) {  // fixed warp order
+      const float2 t = xs[buf][grp][i];
+      sa += t.x;
+      sb += t.y;
+    }
+    sa *= inv_e;
+    sb *= inv_e;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
-      int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-      if (col < E) {
-        float4 o = dx_of(rg[j], rs, sa, sb);
-        if (dres) {
-          float4 r = *reinterpret_cast<const float4*>(dres + row * lddx + col);
-          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+      const int i4 = lane + 32 * (k + G * j);
+      if (i4 < E4) {
+        RowGrad rg{xv[j], dv[j]};
+        float4 o = dx_of(rg, rs, sa, sb);
+        o.x += rv[j].x; o.y += rv[j].y; o.z += rv[j].z; o.w += rv[j].w;
+        *reinterpret_cast<float4*>(dx + row * lddx + 4 * i4) = o;
+        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + 4 * i4, o);
+        if constexpr (SUM) {
+          as[j].x += o.x; as[j].y += o.y; as[j].z += o.z; as[j].w += o.w;
         }
-        *reinterpret_cast<float4*>(dx + row * lddx + col) = o;
-        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + col, o);
       }
+    }
+    if constexpr (PREF) {
+#pragma unroll
+      for (int j = 0; j < NV; ++j) {
+        xv[j] = xn[j];
+        dv[j] = dn[j];
+        rv[j] = rn[j];
+      }
+    } else if (nrow < r1) {
+      load(nrow, xv, dv, rv);
     }
   }
 #pragma unroll
   for (int j = 0; j < NV; ++j) {
-    int64_t col = 4 * ((int64_t)threadIdx.x + j * kT);
-    if (col < E) {
-      *reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E + col) = accg[j];
-      *reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E + col) = accb[j];
+    const int i4 = lane + 32 * (k + G * j);
+    if (i4 < E4) {
+      red[(size_t)(NP * grp) * E4 + i4] = ag[j];
+      red[(size_t)(NP * grp + 1) * E4 + i4] = ab[j];
+      if constexpr (SUM) red[(size_t)(NP * grp + 2) * E4 + i4] = as[j];
     }
   }
+  __syncthreads();
+  for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kGrpWarps) {
+    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f),
+           ss = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {  // fixed group order
+      const float4 a = red[(size_t)(NP * q) * E4 + i4], b = red[(size_t)(NP * q + 1) * E4 + i4];
+      sg.x += a.x; sg.y += a.y; sg.z += a.z; sg.w += a.w;
+      s4.x += b.x; s4.y += b.y; s4.z += b.z; s4.w += b.w;
+      if constexpr (SUM) {
+        const float4 c = red[(size_t)(NP * q + 2) * E4 + i4];
+        ss.x += c.x; ss.y += c.y; ss.z += c.z; ss.w += c.w;
+      }
+    }
+    reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E)[i4] = sg;
+    reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = s4;
+    if constexpr (SUM) reinterpret_cast<float4*>(ps + (int64_t)blockIdx.x * E)[i4] = ss;
+  }
+}
+
+// warps per row and float4s per lane of the group kernel (E > 1024): G = 4 up to E = 2048, 8 above
+void pick_groups(int64_t E, int* G, int* NV) {
+  const int64_t E4 = E / 4;
+  *G = E4 <= 4 * 32 * 4 ? 4 : 8;
+  *NV = (int)((E4 + 32 * *G - 1) / (32 * *G));
 }
 
 int pick_nv_cta(int64_t E) {
@@ -421,13 +512,13 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
               "nnt_layernorm_bwd: scratch %zu < %zu", scratch_bytes, nnt_layernorm_bwd_scratch_bytes(T, E));
   NNT_REQUIRE(pick_nv_cta(E) > 0, NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: E=%lld > 8192", (long long)E);
   const int nvw = pick_nv_warp(E);
-  NNT_REQUIRE(dx_colsum == nullptr || nvw > 0, NNT_ERR_UNSUPPORTED,
-              "nnt_layernorm_bwd: dx_colsum needs E <= 1024 (the row kernel), E=%lld", (long long)E);
-  // single-pass row kernel: rows per CTA so that two CTAs per SM cover T in one wave (>= 16
-  // rows, so the partial count stays within nnt_layernorm_bwd_scratch_bytes)
-  int64_t rows_per_cta = (T + 2 * num_sms() - 1) / (2 * num_sms());
+  // single-pass kernels: rows per CTA so that the resident CTAs (two per SM for the row kernel,
+  // one for the group kernel) cover T in one wave (>= 16 rows, so the partial count stays within
+  // nnt_layernorm_bwd_scratch_bytes)
+  const int64_t resident = (nvw > 0 ? 2 : 1) * (int64_t)num_sms();
+  int64_t rows_per_cta = (T + resident - 1) / resident;
   if (rows_per_cta < kCtaBwdRows) rows_per_cta = kCtaBwdRows;
-  const int64_t chunks = nvw > 0 ? (T + rows_per_cta - 1) / rows_per_cta : (T + kCtaBwdRows - 1) / kCtaBwdRows;
+  const int64_t chunks = (T + rows_per_cta - 1) / rows_per_cta;
   float* pg = (float*)scratch;
   float* pb = pg + chunks * E;
   float* ps = pb + chunks * E;
@@ -449,13 +540,23 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
     switch (nvw) { NNT_LNBR(1) NNT_LNBR(2) NNT_LNBR(4) NNT_LNBR(6) NNT_LNBR(8) }
 #undef NNT_LNBR
   } else {
-#define NNT_LNB(N)                                                                                               \
-  case N:                                                                                                        \
-    ::nnt::launch(ln_bwd_cta<N>, (unsigned)chunks, kT, 0, stream, dy, lddy, x, ldx, mean, rstd, gamma, T, E, dres, dx, lddx, \
-                                                       d16, pg, pb);                                             \
-    break;
-    switch (pick_nv_cta(E)) { NNT_LNB(1) NNT_LNB(2) NNT_LNB(3) NNT_LNB(4) NNT_LNB(6) NNT_LNB(8) NNT_LNB(12) NNT_LNB(16) }
-#undef NNT_LNB
+    int G = 0, NV = 0;
+    pick_groups(E, &G, &NV);
+    const size_t smem_red = (size_t)(kGrpWarps / G) * (sum ? 3 : 2) * E * sizeof(float);  // <= 64 KB
+    auto run = [&](auto kern) -> nnt_status {
+      NNT_CUDA_TRY(set_max_dyn_smem(kern, (int)smem_red));
+      NNT_CUDA_TRY(::nnt::launch(kern, dim3((unsigned)chunks), dim3(32 * kGrpWarps), smem_red, stream, dy, lddy, x,
+                                 ldx, mean, rstd, gamma, T, (int)E, rows_per_cta, dres, dx, lddx, d16, pg, pb, ps));
+      return NNT_OK;
+    };
+#define NNT_LNBG(GG, N)                                                                              \
+  if (G == GG && NV == N) {                                                                          \
+    NNT_TRY(sum ? run(ln_bwd_groups<N, GG, true>) : run(ln_bwd_groups<N, GG, false>));               \
+  } else
+    NNT_LNBG(4, 3) NNT_LNBG(4, 4) NNT_LNBG(8, 3) NNT_LNBG(8, 4) NNT_LNBG(8, 5) NNT_LNBG(8, 6) NNT_LNBG(8, 7)
+    NNT_LNBG(8, 8)
+    return fail(NNT_ERR_UNSUPPORTED, "nnt_layernorm_bwd: unsupported E");
+#undef NNT_LNBG
   }
   NNT_TRY(check_launch("layernorm_bwd"));
   if (sum)

@@ -103,6 +103,16 @@ def _update_kernel(o, b0, b1, m, v, t, stream, shadow):
     nnt.nnt_adam_step(n, o.w[b0:b1], o.g[b0:b1], m, v, w16, o._hp(t), stream=stream)
 
 
+def _distinct_stream(dev, avoid):
+    """A torch stream that is none of `avoid` (torch's stream pool recycles its streams)."""
+    taken = {s.cuda_stream for s in avoid if s is not None}
+    for _ in range(128):
+        s = torch.cuda.Stream(device=dev)
+        if s.cuda_stream not in taken:
+            return s
+    raise RuntimeError("no distinct CUDA stream available")
+
+
 class LossReader:
     """Pipelined device -> host reads of the per-step loss (what a training loop logs).
 
@@ -224,16 +234,20 @@ class BlockStack:
         act = dict(device=self.dev, dtype=torch.float32)
         self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
         self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
-        # links between consecutive blocks' backward passes (E <= 1024, the LayerNorm row kernel):
+        # links between consecutive blocks' backward passes (the LayerNorm backward kernels):
         # layer l's LayerNorm-1 backward also makes sum_t dx (layer l-1's projection-bias gradient)
         # and, on the bf16 path, the bf16 copy of dx that layer l-1's projection GEMMs read
-        self.chain = E <= 1024
+        self.chain = True
         self.dy16 = ([torch.empty(cfg.B, cfg.S, E, device=self.dev, dtype=torch.bfloat16) for _ in range(2)]
                      if self.chain and cfg.dtype == "bf16" else None)
         self.loss = torch.zeros(1, **act)
         self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
-        self.comm = torch.cuda.Stream(device=self.dev) if self.dp else None
-        self.side = torch.cuda.Stream(device=self.dev) if cfg.side_stream else None
+        # every stream of this model distinct (torch's round-robin stream pool recycles streams);
+        # cap_stream: graphs are captured on it (torch.cuda.graph would take one from the pool)
+        used = [] if self.host_state is None else [self.host_state.h2d, self.host_state.d2h]
+        self.comm = _distinct_stream(self.dev, used) if self.dp else None
+        self.side = _distinct_stream(self.dev, used + [self.comm]) if cfg.side_stream else None
+        self.cap_stream = _distinct_stream(self.dev, used + [self.comm, self.side])
         self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.dp else None
         if self.dp:  # torch creates the CUDA event handles lazily, at the first record()
             for evs in self.events:
@@ -425,7 +439,7 @@ class BlockStack:
         g = torch.cuda.CUDAGraph()
         self._graph_hp = hp
         try:
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=self.cap_stream):
                 nnt.nnt_adam_tick(c.beta1, c.beta2, self.t_dev, self.bc_dev)
                 self.forward()
                 self.probe_loss(self.r_buf)
@@ -649,7 +663,7 @@ class GPT2Model:
         g = torch.cuda.CUDAGraph()
         st._graph_hp = hp
         try:
-            with torch.cuda.graph(g):
+            with torch.cuda.graph(g, stream=st.cap_stream):
                 nnt.nnt_adam_tick(c.beta1, c.beta2, st.t_dev, st.bc_dev)
                 self.forward()
                 if st.dp:

@@ -18,6 +18,8 @@ from gpu_util import close, bf16_round, dev, host, rel
 
 pytestmark = pytest.mark.gpu
 
+SPLIT_COUNTER_BYTES = 4096 * 4  # the in-kernel split-K reduce's counter zone (gemm_tc.cu kSplitCounters)
+
 if torch.cuda.is_available():
     from paper_2504_13236_b200 import nnt
 
@@ -165,7 +167,7 @@ def test_gemm_split_k_workspace_bit_exact(M, N):
     A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
     want = tiled.gemm_tiled(a.T, b, 256, 256, 1024) + c0
     # the partials alone (no counter space): the separate reduce kernel
-    nparts = nb - ((-(-M // 128)) * (-(-N // 64)) * 8 * 4)
+    nparts = nb - SPLIT_COUNTER_BYTES
     ws_small = torch.empty(nparts, device="cuda", dtype=torch.uint8)
     for w in (ws, ws_small):
         epi = nnt.make_epilogue(workspace=w)
@@ -174,7 +176,31 @@ def test_gemm_split_k_workspace_bit_exact(M, N):
             nnt.nnt_tile_gemm(1, 0, M, N, K, None, 1.0, A, 1, M, None, B, 1, N, None, 1.0, Cm, 0, N, None, None, epi)
             torch.cuda.synchronize()
             assert np.array_equal(host(Cm), want)
-    assert int(ws[-(-(-M // 128)) * (-(-N // 64)) * 8 * 4:].count_nonzero()) == 0  # counters back to zero
+    assert int(ws[-SPLIT_COUNTER_BYTES:].count_nonzero()) == 0  # counters back to zero
+
+
+def test_gemm_split_k_shared_workspace_shapes():
+    """The block's four dW GEMMs share one split-K workspace sized for the largest: the in-kernel
+    reduce's counter zone (last 16 KB of the workspace) must never lie under another shape's
+    partials.  Alternate shapes and K (1024: 2 splits of 8 K-blocks; 8192) on one zero-filled
+    workspace, twice round, integer data (exact)."""
+    shapes = [(2304, 768), (768, 768), (3072, 768), (768, 3072)]
+    Ks = (1024, 8192)
+    nb = max(nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0) for M, N in shapes for K in Ks)
+    ws = torch.zeros(nb, device="cuda", dtype=torch.uint8)
+    epi = nnt.make_epilogue(workspace=ws)
+    for _ in range(2):
+        for K in Ks:
+            for M, N in shapes:
+                a = nnt_inputs.make_matrix((K, M), seed=M + 3 * N + K, kind="int")
+                b = nnt_inputs.make_matrix((K, N), seed=M + N + 7 * K, kind="int")
+                A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
+                Cm = torch.zeros(M, N, device="cuda")
+                nnt.nnt_tile_gemm(1, 0, M, N, K, None, 1.0, A, 1, M, None, B, 1, N, None, 0.0, Cm, 0, N, None, None,
+                                  epi)
+                torch.cuda.synchronize()
+                assert np.array_equal(host(Cm), a.T.astype(np.float64) @ b.astype(np.float64)), (M, N, K)
+    assert int(ws[-SPLIT_COUNTER_BYTES:].count_nonzero()) == 0
 
 
 @pytest.mark.parametrize("M,N", [(768, 768), (2304, 768)])
@@ -189,7 +215,7 @@ def test_gemm_split_k_real_data_extras(M, N):
     bias = rng.standard_normal(N).astype(np.float32)
     res = rng.standard_normal((M, N)).astype(np.float32)
     nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
-    nparts = nb - ((-(-M // 128)) * (-(-N // 64)) * 8 * 4)
+    nparts = nb - SPLIT_COUNTER_BYTES
     A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
     want = 0.5 * (a.T @ b) + bias + 0.75 * c0 + res
     got = []

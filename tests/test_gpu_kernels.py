@@ -161,9 +161,11 @@ def test_layernorm_closed_forms():
     np.testing.assert_allclose(y[1] - b, np.where(np.arange(E) % 2 == 0, -v, v), rtol=1e-6)
 
 
-@pytest.mark.parametrize("E", [64, 768, 1600])
-def test_layernorm_bwd(E):
-    T = 200
+# E <= 1024: the warp-per-row kernel; E > 1024: warp groups per row (G = 4 warps up to E = 2048,
+# 8 above; the next row prefetched up to E = 4096), T = 8192 gives several rows per group
+@pytest.mark.parametrize("E,T", [(64, 200), (768, 200), (1280, 200), (1600, 200), (1600, 8192), (2052, 300),
+                                 (4096, 200), (8192, 100)])
+def test_layernorm_bwd(E, T):
     rng = np.random.default_rng(E + 1)
     x = (1.0 + 2.0 * rng.standard_normal((T, E))).astype(np.float32)
     g = (1 + 0.1 * rng.standard_normal(E)).astype(np.float32)
@@ -178,8 +180,8 @@ def test_layernorm_bwd(E):
     DB = dev(np.ones(E, np.float32))
     nb = nnt.nnt_layernorm_bwd_scratch_bytes(T, E)
     scr = torch.empty(nb, device="cuda", dtype=torch.uint8)
-    # the fused column sum of the output dx (the row kernel, E <= 1024)
-    DS = dev(np.full(E, 2.0, np.float32)) if E <= 1024 else None
+    # the fused column sum of the output dx (every E)
+    DS = dev(np.full(E, 2.0, np.float32))
     nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)), dev(r_ref.astype(np.float32)),
                           dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, DS, 1, scr, nb)
     torch.cuda.synchronize()
@@ -187,13 +189,7 @@ def test_layernorm_bwd(E):
     close(host(DX16), dx_ref + dres, 4e-3)
     close(host(DG), dg_ref + 1.0, 1e-5)
     close(host(DB), db_ref + 1.0, 1e-5)
-    if DS is not None:
-        close(host(DS), (dx_ref + dres).sum(axis=0) + 2.0, 1e-5)
-    else:  # E > 1024: the CTA-per-row kernel has no fused column sum
-        with pytest.raises(nnt.NNTError):
-            nnt.nnt_layernorm_bwd(dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)),
-                                  dev(r_ref.astype(np.float32)), dev(g), T, E, dev(dres), DX, E, DX16, DG, DB, DG, 1,
-                                  scr, nb)
+    close(host(DS), (dx_ref + dres).sum(axis=0) + 2.0, 1e-5)
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
