@@ -253,6 +253,45 @@ nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, 
                            int64_t h, float* D, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
+/* Fused attention tiles (bf16 path, readings R20, R26, R33)       */
+/* ------------------------------------------------------------------------- */
+/* 1 when the fused attention kernels below cover (S, h): head size 64 and S % 128 == 0. */
+int nnt_attention_fused_supported(int64_t S, int64_t h);
+
+/*
+ * Softmax subroutine 2 and the value product of B = V SoftMax(K^T Q / sqrt(h)),
+ * per (batch b, head n), 128 x 128 tile by tile:
+ *   P[b][n][q][k] = e^{scale * q_q . k_k - M} / S_sum   (k <= q when causal, else 0 in the
+ *                   diagonal tile; tiles above the diagonal are not written)
+ *   O[b][q][n*h + i] = sum_k P[b][n][q][k] V[b][k][n*h + i]
+ * with (M, S_sum) the row statistics of softmax subroutine 1 (the ROWSTATS score GEMM, R26).
+ * Each P tile is staged in shared memory once: stored to HBM (the backward reads it) and fed to
+ * the P V tensor-core product from there.
+ * qkv: device bf16 [B][S][3][H][h] (Q | K | V thirds, row pitch 3*H*h); stats: device fp32
+ * [B*H*S][2] = (M in scaled-score units, S_sum); P: device bf16 [B][H][S][S]; O: device bf16
+ * [B][S][H*h].  h == 64, S % 128 == 0 (else NNT_ERR_UNSUPPORTED); 16-byte aligned.
+ */
+nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t h, float scale,
+                                int causal, const float* stats, void* P, void* O, nnt_stream_t stream);
+
+/*
+ * Softmax backward with the dK / dV products (R18, R20), per (b, n) and 128-key block kb over the
+ * query blocks qb (>= kb when causal):
+ *   dA^T[b][n][k][q] = scale * P[q][k] * (sum_i dO[q][i] V[k][i] - D[q])     (stored keys-major)
+ *   dK[k][n*h + i] = sum_q dA^T[k][q] Q[q][i]            dV[k][n*h + i] = sum_q P[q][k] dO[q][i]
+ * D = rowdot(dO, O) (nnt_attn_rowdot).  Each P tile is read once and each dA tile written once;
+ * dK and dV accumulate on chip over the query blocks.  dQ = dA K is the GEMM
+ * nnt_tile_gemm(NNT_TRANS, NNT_NOTRANS, S, h, S, {B, H}, 1, dAT, S, {H*S*S, S*S}, K, ...,
+ * causal NNT_CAUSAL_A_LOWER) on the keys-major dA^T (entries with k > q are zero; blocks with
+ * kb > qb are not written and not read).
+ * qkv, P, D as above; dO: device bf16 [B][S][H*h]; dAT: device bf16 [B][H][S][S]; dqkv: device
+ * bf16 [B][S][3][H][h] -- its K and V thirds are written, the Q third untouched.
+ */
+nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, const float* D, int64_t B,
+                                int64_t S, int64_t H, int64_t h, float scale, int causal, void* dAT,
+                                void* dqkv, nnt_stream_t stream);
+
+/* ------------------------------------------------------------------------- */
 /* LayerNorm in three steps                                       */
 /* ------------------------------------------------------------------------- */
 /*

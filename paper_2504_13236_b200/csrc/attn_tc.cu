@@ -1,0 +1,613 @@
+// Fused attention tile kernels of the bf16 path (readings R20, R26, R33).
+//
+// The paper's attention is B = V SoftMax(K^T Q / sqrt(h)) per (batch, head) with the
+// softmax built from the maxsumexp subroutine and a normalise subroutine.  The bf16
+// path runs subroutine 1 (the row statistics) in the score GEMM's epilogue (R26); these two
+// kernels then run every remaining attention product tile by tile, each key / query tile pair
+// touched once:
+//
+//   nnt_attention_fwd_pv  (subroutine 2 + the value product) -- task = (b, h, query block):
+//       for each key block kb <= qb:  S = Q K_kb^T (tcgen05, TMEM)  ->  P = e^{S - M} / S_sum
+//       (epilogue, from the row statistics)  ->  P stored to HBM (the backward reads it) AND
+//       staged in shared memory as the A operand of  O += P V_kb  (tcgen05, TMEM);  O stored once.
+//       P is read back from HBM zero times (the unfused path re-read it for P V).
+//   nnt_attention_bwd_kv  (softmax backward + dV + dK) -- task = (b, h, key block):
+//       for each query block qb >= kb:  dP^T = V_kb dO_qb^T (tcgen05)  ->
+//       dA^T = P^T (dP^T - D) / sqrt(h) (epilogue, P from the TMA-loaded tile)  ->  dA^T stored
+//       (keys-major, for dQ = dA K) and staged as the A operand of  dK += dA^T Q_qb;  and
+//       dV += P^T dO_qb  straight from the same P tile.  dK, dV accumulate in TMEM over the
+//       query blocks and are stored once.  Each P tile is read once, each dA tile written once
+//       (the unfused path read P three times and dA twice).
+//
+// Warp roles as in the GEMM (gemm_tc.cu): warp 0 TMA producer, warp 1 TMEM allocator + MMA
+// issuer, warps 2..9 epilogue (TMEM lane quadrant = warp % 4; the two warps of a quadrant take
+// the two 64-column halves of a 128 x 128 tile).  Persistent CTAs, static heaviest-first task
+// order with a boustrophedon assignment.  Head size h = 64 and S % 128 == 0 (the configurations
+// of BASELINE.json); the block falls back to the unfused GEMM sequence otherwise.
+#include <cuda.h>
+
+#include "gemm_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace nnt {
+namespace {
+
+constexpr int kAThreads = 64 + 32 * 8;
+constexpr int TB = 128;     // query / key block
+constexpr int HD = 64;      // head size
+constexpr int TILE16 = 16384;  // one 128-row x 128-byte SW128 tile (64 bf16 per row)
+constexpr int PIECE = 4096;    // one epilogue warp's 32-row x 128-byte staging piece
+
+struct AttnParams {
+  int B, H, S, nblk, num_tasks, causal;
+  float scale;          // 1 / sqrt(h)
+  const float* stats;   // fwd: (M, S_sum) per (b, h, query) as float2, M in scaled-score units
+  const float* D;       // bwd: D = rowdot(dO, O) per (b, h, query)
+};
+
+// idesc: fp32 accumulate, bf16 A / B, the operands' majors, N, M = 128
+__host__ __device__ constexpr uint32_t idesc_of(bool a_mn, bool b_mn, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TB >> 4) << 24);
+}
+
+__device__ __forceinline__ int64_t task_at(int64_t c, int64_t G, int64_t k) {
+  return k * G + ((k & 1) ? (G - 1 - c) : c);
+}
+
+__device__ __forceinline__ void tmem_alloc512(uint32_t slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(slot) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_free512(uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
+}
+
+// ============================================================================ forward
+// smem: Q[2] (task parity) | 3 stages of {K_kb, V_kb} | P staging[2] (32 KB: half h at +16 KB,
+// quadrant rows at +4 KB) | barriers.  TMEM: S[2] at columns 0 / 128, O[2] at 256 / 320.
+constexpr int F_STAGES = 3;
+constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_BAR = F_P + 2 * 2 * TILE16;
+constexpr int F_SMEM = F_BAR + 256 + 1024;
+
+__global__ void __launch_bounds__(kAThreads, 1)
+    attn_fwd_pv_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mQ,
+                       const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
+                       const __grid_constant__ CUtensorMap mPst, const __grid_constant__ CUtensorMap mO) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + F_BAR);
+  uint64_t* full = bars;                  // [3] stage K, V landed
+  uint64_t* empty = bars + 3;             // [3] stage consumed (MMA S and MMA O)
+  uint64_t* qfull = bars + 6;             // [2] Q of a task landed
+  uint64_t* qempty = bars + 8;            // [2] the task's last S MMA done
+  uint64_t* sfull = bars + 10;            // [2] S accumulator ready
+  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (8 warps)
+  uint64_t* pfull = bars + 14;            // [2] P staging written (8 warps)
+  uint64_t* pempty = bars + 16;           // [2] P staging consumed by MMA O
+  uint64_t* ofull = bars + 18;            // [2] O accumulator of a task complete
+  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int BH = P.B * P.H;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&qfull[i]), 1);
+      mbar_init(smem_u32(&qempty[i]), 1);
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), 8);
+      mbar_init(smem_u32(&pfull[i]), 8);
+      mbar_init(smem_u32(&pempty[i]), 1);
+      mbar_init(smem_u32(&ofull[i]), 1);
+      mbar_init(smem_u32(&oempty[i]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc512(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  NNT_PDL_ENTRY();
+  // task t (heaviest first): level = t / BH -> query block qb = nblk - 1 - level; bh = t % BH
+  auto decode = [&](int64_t t, int& qb, int& b, int& h) {
+    const int level = (int)(t / BH), bh = (int)(t % BH);
+    qb = P.nblk - 1 - level;
+    b = bh / P.H;
+    h = bh % P.H;
+  };
+  const int64_t c0 = blockIdx.x, G = gridDim.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    int tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int qs = tl & 1;
+      mbar_wait(smem_u32(&qempty[qs]), ((tl >> 1) & 1) ^ 1);
+      mbar_expect_tx_w(smem_u32(&qfull[qs]), TILE16);
+      tma_load_4d_w(smem_u32(smem + F_Q + qs * TILE16), &mQ, smem_u32(&qfull[qs]), 0, qb * TB, h, b);
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        const uint32_t st = smem_u32(smem + F_ST + stage * 2 * TILE16);
+        mbar_expect_tx_w(smem_u32(&full[stage]), 2 * TILE16);
+        tma_load_4d_w(st, &mK, smem_u32(&full[stage]), 0, kb * TB, h, b);
+        tma_load_4d_w(st + TILE16, &mV, smem_u32(&full[stage]), 0, kb * TB, h, b);
+        if (++stage == F_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    pdl_trigger();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    const uint32_t id_s = idesc_of(false, false, TB);  // S = Q K^T: both K-major, N = 128
+    const uint32_t id_o = idesc_of(false, true, HD);   // O += P V: P K-major, V MN-major, N = 64
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;  // iterations over all tasks (S / P buffer parity)
+    int tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int qs = tl & 1, os = tl & 1;
+      mbar_wait(smem_u32(&qfull[qs]), (tl >> 1) & 1);
+      mbar_wait(smem_u32(&oempty[os]), ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t sq = smem_u32(smem + F_Q + qs * TILE16);
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      // software pipeline: S MMA of iteration i+1 is issued before the O MMA of iteration i
+      // (which waits for the epilogue's P), so the tensor core works while the epilogue runs
+      auto issue_s = [&](int i, int stg) {
+        const int sb = (it + i) & 1;
+        mbar_wait(smem_u32(&sempty[sb]), (((it + i) >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&full[stg]), (uint32_t)((phase + ((stage + i) / F_STAGES)) & 1));
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + F_ST + stg * 2 * TILE16);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
+                     kk > 0 ? 1u : 0u);
+        mma_commit_w(smem_u32(&sfull[sb]));
+      };
+      issue_s(0, stage);
+      for (int i = 0; i < nk; ++i) {
+        const int stg = (stage + i) % F_STAGES;
+        if (i + 1 < nk) issue_s(i + 1, (stage + i + 1) % F_STAGES);
+        else mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
+        const int pb = (it + i) & 1;
+        mbar_wait(smem_u32(&pfull[pb]), ((it + i) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
+        const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)  // K = 128 keys: P chunk kk/4 (+16 KB), V rows +2 KB
+          mma_bf16_w(tmem + 256 + os * HD, make_sdesc(sp + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
+                     make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(smem_u32(&pempty[pb]));
+        mma_commit_w(smem_u32(&empty[stg]));
+      }
+      mma_commit_w(smem_u32(&ofull[os]));
+      // advance the stage ring and iteration counter by this task's nk iterations
+      phase ^= (uint32_t)(((stage + nk) / F_STAGES) & 1);
+      stage = (stage + nk) % F_STAGES;
+      it += nk;
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..9
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    const float L2E = 1.4426950408889634f;
+    const float sc = P.scale * L2E;
+    int it = 0, tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int q = qb * TB + quad * 32 + lane;  // this lane's query row
+      const float2 st = __ldg(reinterpret_cast<const float2*>(P.stats) + ((int64_t)(b * P.H + h) * P.S + q));
+      const float ml = st.x * L2E, inv = 1.f / st.y;
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      for (int i = 0; i < nk; ++i, ++it) {
+        const int sb = it & 1;
+        mbar_wait(smem_u32(&sfull[sb]), (it >> 1) & 1);
+        tc_fence_after();
+        float v[64];
+        tmem_ld_cols<2>(tmem + sb * TB + half * 64 + ((uint32_t)(quad * 32) << 16), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sempty[sb]));
+        const int key0 = i * TB + half * 64;
+        int lim = 64;  // causal: keys <= q
+        if (P.causal && key0 + 63 > q) lim = q - key0 + 1;
+        if (lim >= 64) {
+#pragma unroll
+          for (int j = 0; j < 64; j += 2) {
+            const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc, sc), make_float2(-ml, -ml));
+            const float2 y = __fmul2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(inv, inv));
+            v[j] = y.x;
+            v[j + 1] = y.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 64; ++j) v[j] = j < lim ? ex2_approx(fmaf(v[j], sc, -ml)) * inv : 0.f;
+        }
+        // P piece -> staging buffer pb (after MMA O of iteration it-2 and this warp's store of it)
+        const int pb = it & 1;
+        mbar_wait(smem_u32(&pempty[pb]), ((it >> 1) & 1) ^ 1);
+        uint8_t* piece = smem + F_P + pb * 2 * TILE16 + half * TILE16 + quad * PIECE;
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(&pfull[pb]));
+          tma_store_4d(&mPst, smem_u32(piece), key0, qb * TB + quad * 32, h, b);
+          bulk_commit();
+        }
+      }
+      // O = P V of the task (4 warps: half 0) -> bf16 -> TMA store
+      if (half == 0) {
+        const int os = tl & 1;
+        mbar_wait(smem_u32(&ofull[os]), (tl >> 1) & 1);
+        tc_fence_after();
+        float v[64];
+        tmem_ld_cols<2>(tmem + 256 + os * HD + ((uint32_t)(quad * 32) << 16), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
+        // staging: this warp's piece of the P buffer that MMA O has finished with (ofull covers it)
+        uint8_t* piece = smem + F_P + ((it - 1) & 1) * 2 * TILE16 + quad * PIECE;
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_4d(&mO, smem_u32(piece), 0, qb * TB + quad * 32, h, b);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free512(tmem);
+  }
+}
+
+// ============================================================================ backward
+// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | dA^T staging (32 KB:
+// query half h at +16 KB, quadrant rows at +4 KB) | barriers.  TMEM: dP^T[2] at columns 0 / 128,
+// {dV, dK}[2] at 256 / 384 (+64 for dK).
+constexpr int B_STAGES = 2;
+constexpr int B_STAGE_BYTES = 4 * TILE16;
+constexpr int B_V = 0, B_ST = 2 * TILE16, B_DA = B_ST + B_STAGES * B_STAGE_BYTES, B_BAR = B_DA + 2 * TILE16;
+constexpr int B_SMEM = B_BAR + 256 + 1024;
+
+__global__ void __launch_bounds__(kAThreads, 1)
+    attn_bwd_kv_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mV,
+                       const __grid_constant__ CUtensorMap mdO, const __grid_constant__ CUtensorMap mQ,
+                       const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mdAT,
+                       const __grid_constant__ CUtensorMap mdK, const __grid_constant__ CUtensorMap mdV) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
+  uint64_t* full = bars;          // [2] stage dO, Q, P landed
+  uint64_t* empty = bars + 2;     // [2] stage consumed: MMA commit + 8 epilogue warps (P reads)
+  uint64_t* vfull = bars + 4;     // [2]
+  uint64_t* vempty = bars + 6;    // [2] the task's last dP MMA done
+  uint64_t* tfull = bars + 8;     // [2] dP^T accumulator ready
+  uint64_t* tempty = bars + 10;   // [2] drained (8 warps)
+  uint64_t* dafull = bars + 12;   // dA^T staging written (8 warps)
+  uint64_t* daempty = bars + 13;  // dA^T staging consumed by MMA dK
+  uint64_t* afull = bars + 14;    // [2] dV, dK of a task complete
+  uint64_t* aempty = bars + 16;   // [2] drained (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int BH = P.B * P.H;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1 + 8);
+      mbar_init(smem_u32(&vfull[i]), 1);
+      mbar_init(smem_u32(&vempty[i]), 1);
+      mbar_init(smem_u32(&tfull[i]), 1);
+      mbar_init(smem_u32(&tempty[i]), 8);
+      mbar_init(smem_u32(&afull[i]), 1);
+      mbar_init(smem_u32(&aempty[i]), 8);
+    }
+    mbar_init(smem_u32(dafull), 8);
+    mbar_init(smem_u32(daempty), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc512(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  NNT_PDL_ENTRY();
+  // task t (heaviest first): level = t / BH -> key block kb = level (causal: nblk - kb query blocks)
+  auto decode = [&](int64_t t, int& kb, int& b, int& h) {
+    const int level = (int)(t / BH), bh = (int)(t % BH);
+    kb = level;
+    b = bh / P.H;
+    h = bh % P.H;
+  };
+  auto q_first = [&](int kb) { return P.causal ? kb : 0; };
+  const int64_t c0 = blockIdx.x, G = gridDim.x;
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer
+    int stage = 0;
+    uint32_t phase = 0;
+    int tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int kb, b, h;
+      decode(t, kb, b, h);
+      const int vs = tl & 1;
+      mbar_wait(smem_u32(&vempty[vs]), ((tl >> 1) & 1) ^ 1);
+      mbar_expect_tx_w(smem_u32(&vfull[vs]), TILE16);
+      tma_load_4d_w(smem_u32(smem + B_V + vs * TILE16), &mV, smem_u32(&vfull[vs]), 0, kb * TB, h, b);
+      for (int qb = q_first(kb); qb < P.nblk; ++qb) {
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        const uint32_t st = smem_u32(smem + B_ST + stage * B_STAGE_BYTES);
+        const uint32_t fb = smem_u32(&full[stage]);
+        mbar_expect_tx_w(fb, B_STAGE_BYTES);
+        tma_load_4d_w(st, &mdO, fb, 0, qb * TB, h, b);
+        tma_load_4d_w(st + TILE16, &mQ, fb, 0, qb * TB, h, b);
+        tma_load_4d_w(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b);       // keys kb*128 + 0..63
+        tma_load_4d_w(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b);  // keys + 64..127
+        if (++stage == B_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    pdl_trigger();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer
+    const uint32_t id_dp = idesc_of(false, false, TB);  // dP^T = V dO^T: both K-major, N = 128
+    const uint32_t id_dv = idesc_of(true, true, HD);    // dV += P^T dO: P MN-major, dO MN-major
+    const uint32_t id_dk = idesc_of(false, true, HD);   // dK += dA^T Q: dA^T K-major, Q MN-major
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int kb, b, h;
+      decode(t, kb, b, h);
+      const int vs = tl & 1, as = tl & 1;
+      mbar_wait(smem_u32(&vfull[vs]), (tl >> 1) & 1);
+      mbar_wait(smem_u32(&aempty[as]), ((tl >> 1) & 1) ^ 1);
+      tc_fence_after();
+      const uint32_t sv = smem_u32(smem + B_V + vs * TILE16);
+      const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
+      const int q0 = q_first(kb), nq = P.nblk - q0;
+      auto stg_of = [&](int i) { return (stage + i) % B_STAGES; };
+      auto ph_of = [&](int i) { return (uint32_t)((phase + ((stage + i) / B_STAGES)) & 1); };
+      auto issue_dp = [&](int i) {
+        const int tb = (it + i) & 1;
+        mbar_wait(smem_u32(&tempty[tb]), (((it + i) >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&full[stg_of(i)]), ph_of(i));
+        tc_fence_after();
+        const uint32_t sdo = smem_u32(smem + B_ST + stg_of(i) * B_STAGE_BYTES);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_w(tmem + tb * TB, make_sdesc(sv + kk * 32, 16, 1024), make_sdesc(sdo + kk * 32, 16, 1024), id_dp,
+                     kk > 0 ? 1u : 0u);
+        mma_commit_w(smem_u32(&tfull[tb]));
+      };
+      issue_dp(0);
+      for (int i = 0; i < nq; ++i) {
+        const uint32_t st = smem_u32(smem + B_ST + stg_of(i) * B_STAGE_BYTES);
+        // dV += P^T dO (both operands already in the stage): K = 128 queries
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)
+          mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
+                     id_dv, (i > 0 || kk > 0) ? 1u : 0u);
+        if (i + 1 < nq) issue_dp(i + 1);
+        else mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
+        // dK += dA^T Q once the epilogue has staged dA^T of iteration i
+        mbar_wait(smem_u32(dafull), (it + i) & 1);
+        tc_fence_after();
+        const uint32_t sda = smem_u32(smem + B_DA);
+#pragma unroll
+        for (int kk = 0; kk < TB / 16; ++kk)
+          mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
+                     make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (i > 0 || kk > 0) ? 1u : 0u);
+        mma_commit_w(smem_u32(daempty));
+        mma_commit_w(smem_u32(&empty[stg_of(i)]));
+      }
+      mma_commit_w(smem_u32(&afull[as]));
+      phase ^= (uint32_t)(((stage + nq) / B_STAGES) & 1);
+      stage = (stage + nq) % B_STAGES;
+      it += nq;
+    }
+  } else {
+    // ------------------------------------------------ epilogue warps 2..9
+    const int quad = warp & 3, half = (warp - 2) >> 2;
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0, tl = 0;
+    // P element (query r of the tile, this lane's key): tile box quad >> 1, 16-byte chunk
+    // (quad & 1) * 4 + lane / 8 swizzled by r % 8 (SW128), element lane % 8
+    const int pbox = (quad >> 1) * TILE16, pchunk = (quad & 1) * 4 + (lane >> 3), pel = (lane & 7) * 2;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int kb, b, h;
+      decode(t, kb, b, h);
+      const float* Dbh = P.D + (int64_t)(b * P.H + h) * P.S;
+      for (int qb = q_first(kb); qb < P.nblk; ++qb, ++it) {
+        const int tb = it & 1;
+        mbar_wait(smem_u32(&tfull[tb]), (it >> 1) & 1);
+        tc_fence_after();
+        float v[64];  // dP^T[key = lane row][query = half * 64 + j]
+        tmem_ld_cols<2>(tmem + tb * TB + half * 64 + ((uint32_t)(quad * 32) << 16), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&tempty[tb]));
+        mbar_wait(smem_u32(&full[stage]), phase);  // the P tile of this stage has landed
+        const uint8_t* ptile = smem + B_ST + stage * B_STAGE_BYTES + 2 * TILE16 + pbox;
+        const float* Dq = Dbh + qb * TB + half * 64;
+#pragma unroll
+        for (int j = 0; j < 64; j += 4) {
+          const float4 d = __ldg(reinterpret_cast<const float4*>(Dq + j));
+          const float dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int r = half * 64 + j + u;  // query row of the P tile
+            const uint16_t pr = *reinterpret_cast<const uint16_t*>(ptile + r * 128 + ((pchunk ^ (r & 7)) << 4) + pel);
+            const float p = __uint_as_float((uint32_t)pr << 16);
+            v[j + u] = (p * P.scale) * (v[j + u] - dd[u]);  // dA = P (dP - D) / sqrt(h)  (R20)
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // this warp's P reads are done
+        // dA^T piece -> staging (after MMA dK of the previous iteration and this warp's store)
+        mbar_wait(smem_u32(daempty), (it & 1) ^ 1);
+        uint8_t* piece = smem + B_DA + half * TILE16 + quad * PIECE;
+        if (lane == 0) bulk_wait_read0();
+        __syncwarp();
+        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(smem_u32(dafull));
+          tma_store_4d(&mdAT, smem_u32(piece), qb * TB + half * 64, kb * TB + quad * 32, h, b);
+          bulk_commit();
+        }
+        if (++stage == B_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      // dK (half 0) / dV (half 1) of the key block -> bf16 -> TMA store
+      const int as = tl & 1;
+      mbar_wait(smem_u32(&afull[as]), (tl >> 1) & 1);
+      tc_fence_after();
+      float v[64];
+      tmem_ld_cols<2>(tmem + 256 + as * 128 + (half == 0 ? HD : 0) + ((uint32_t)(quad * 32) << 16), v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&aempty[as]));
+      uint8_t* piece = smem + B_DA + half * TILE16 + quad * PIECE;  // MMA dK finished with it (afull)
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      stage_row<__nv_bfloat16, 64>(piece, lane, v);
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(half == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free512(tmem);
+  }
+}
+
+int64_t persistent_grid(int64_t tasks) { return tasks < num_sms() ? tasks : num_sms(); }
+
+nnt_status check_attn(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, const char* what) {
+  NNT_REQUIRE(qkv, NNT_ERR_NULL, "%s: NULL pointer", what);
+  NNT_REQUIRE(B > 0 && H > 0 && S > 0 && B * H * S < (1ll << 31), NNT_ERR_SHAPE, "%s: B=%lld S=%lld H=%lld", what,
+              (long long)B, (long long)S, (long long)H);
+  NNT_REQUIRE(Dh == HD && S % TB == 0, NNT_ERR_UNSUPPORTED, "%s: needs head size 64 and S %% 128 == 0 (Dh=%lld S=%lld)",
+              what, (long long)Dh, (long long)S);
+  NNT_REQUIRE(aligned16(qkv), NNT_ERR_ALIGN, "%s: 16-byte alignment", what);
+  return NNT_OK;
+}
+
+}  // namespace
+}  // namespace nnt
+
+using namespace nnt;
+
+extern "C" {
+
+int nnt_attention_fused_supported(int64_t S, int64_t Dh) { return Dh == HD && S > 0 && S % TB == 0 ? 1 : 0; }
+
+nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, float scale,
+                                int causal, const float* stats, void* P, void* O, nnt_stream_t stream) {
+  NNT_TRY(check_attn(qkv, B, S, H, Dh, "nnt_attention_fwd_pv"));
+  NNT_REQUIRE(stats && P && O, NNT_ERR_NULL, "nnt_attention_fwd_pv: NULL pointer");
+  NNT_REQUIRE(aligned16(P) && aligned16(O) && aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_fwd_pv: alignment");
+  const int64_t Ea = H * Dh, nblk = S / TB;
+  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr};
+  CUtensorMap mQ, mK, mV, mPst, mO;
+  const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
+  NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mK, bf, 2, q + Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mV, bf, 2, q + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mPst, bf, 2, P, S, S, S, H, S * S, B, H * S * S, 64, 32));
+  NNT_TRY(make_tma_map_4d(&mO, bf, 2, O, Dh, S, Ea, H, Dh, B, S * Ea, 64, 32));
+  // algorithmic bytes: P written once (causal: the lower-triangular 128 x 128 tiles), O written,
+  // Q / K / V read once each
+  const double ptiles = (double)B * H * (causal ? nblk * (nblk + 1) / 2 : nblk * nblk);
+  LaunchScope sc(NNT_K_GEMM_TC_ATTN, stream, ptiles * TB * TB * 2 + 4.0 * B * S * Ea * 2,
+                 ptiles * 4.0 * TB * TB * HD);
+  NNT_CUDA_TRY(set_max_dyn_smem(attn_fwd_pv_kernel, F_SMEM));
+  NNT_CUDA_TRY(::nnt::launch(attn_fwd_pv_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreads),
+                             (size_t)F_SMEM, (cudaStream_t)stream, prm, mQ, mK, mV, mPst, mO));
+  return check_launch("attn_fwd_pv");
+}
+
+nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, const float* D, int64_t B, int64_t S,
+                                int64_t H, int64_t Dh, float scale, int causal, void* dAT, void* dqkv,
+                                nnt_stream_t stream) {
+  NNT_TRY(check_attn(qkv, B, S, H, Dh, "nnt_attention_bwd_kv"));
+  NNT_REQUIRE(dO && P && D && dAT && dqkv, NNT_ERR_NULL, "nnt_attention_bwd_kv: NULL pointer");
+  NNT_REQUIRE(aligned16(dO) && aligned16(P) && aligned16(D) && aligned16(dAT) && aligned16(dqkv), NNT_ERR_ALIGN,
+              "nnt_attention_bwd_kv: alignment");
+  const int64_t Ea = H * Dh, nblk = S / TB;
+  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D};
+  CUtensorMap mV, mdO, mQ, mP, mdAT, mdK, mdV;
+  const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
+  __nv_bfloat16* dq = (__nv_bfloat16*)dqkv;
+  NNT_TRY(make_tma_map_4d(&mV, bf, 2, q + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mdO, bf, 2, dO, Dh, S, Ea, H, Dh, B, S * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mP, bf, 2, P, S, S, S, H, S * S, B, H * S * S, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mdAT, bf, 2, dAT, S, S, S, H, S * S, B, H * S * S, 64, 32));
+  NNT_TRY(make_tma_map_4d(&mdK, bf, 2, dq + Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));
+  NNT_TRY(make_tma_map_4d(&mdV, bf, 2, dq + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));
+  // algorithmic bytes: P read once, dA written once, Q / V / dO read, dK / dV written
+  const double ptiles = (double)B * H * (causal ? nblk * (nblk + 1) / 2 : nblk * nblk);
+  LaunchScope sc(NNT_K_GEMM_TC_ATTN, stream, ptiles * TB * TB * 2 * 2 + 5.0 * B * S * Ea * 2,
+                 ptiles * 6.0 * TB * TB * HD);
+  NNT_CUDA_TRY(set_max_dyn_smem(attn_bwd_kv_kernel, B_SMEM));
+  NNT_CUDA_TRY(::nnt::launch(attn_bwd_kv_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreads),
+                             (size_t)B_SMEM, (cudaStream_t)stream, prm, mV, mdO, mQ, mP, mdAT, mdK, mdV));
+  return check_launch("attn_bwd_kv");
+}
+
+}  // extern "C"

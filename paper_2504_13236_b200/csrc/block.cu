@@ -114,6 +114,7 @@ struct Ctx {
   cudaStream_t side;  // nnt_block_bwd_streams: weight/bias-gradient ops run here (or NULL)
   const nnt_block_bwd_links* links;  // nnt_block_bwd_streams: fused cross-layer bias sums (or NULL)
   bool ln_rows;                      // the LayerNorm backward fuses the column sums of dx (every E)
+  bool fused_attn;                   // bf16, h = 64, S % 128 == 0: the fused attention tile kernels (R33)
   template <typename P>
   P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
   template <typename P>
@@ -160,6 +161,9 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return nnt_maxsumexp(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S,
                            x.s<float>(x.L.stats), 0, x.st);
     case NNT_OP_SOFTMAX:
+      if (x.fused_attn)  // R33: subroutine 2 and P V in one tile pass; P stored once, never re-read
+        return nnt_attention_fwd_pv(x.s<void>(x.L.qkv), B, S, H, Dh, x.inv_sqrt_dh, x.c.causal, x.s<float>(x.L.stats),
+                                    x.s<void>(x.L.P), x.s<void>(x.L.O), x.st);
       if (dt == NNT_BF16) {
         // R26: subroutine 2 on recomputed score tiles (same MMA order as the stats pass), P in bf16
         const int64_t sq[2] = {S * 3 * Ea, Dh}, sp[2] = {H * S * S, S * S};
@@ -173,6 +177,7 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return nnt_softmax(x.k<float>(x.L.scores), B * H * S, S, S, x.c.tile_s, x.c.causal, S, x.s<float>(x.L.stats),
                          x.s<void>(x.L.P), dt, S, x.st);
     case NNT_OP_PV: {
+      if (x.fused_attn) return NNT_OK;  // formed with P in NNT_OP_SOFTMAX
       const size_t es = dt == NNT_BF16 ? 2 : 4;
       const int64_t sp[2] = {H * S * S, S * S}, sv[2] = {S * 3 * Ea, Dh}, so[2] = {S * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
@@ -266,6 +271,10 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, Ea, E, nullptr, 1.f, dx1A, E, nullptr, p->w_o, Ea, nullptr, 0.f,
                   x.k<void>(x.L.dO), dt, Ea, nullptr, nullptr);
     case NNT_OP_ATT_DP: {
+      if (x.fused_attn)  // R33: dA (keys-major), dK and dV in one pass over the P tiles
+        return nnt_attention_bwd_kv(x.s<void>(x.L.qkv), x.k<void>(x.L.dO), x.s<void>(x.L.P), x.k<float>(x.L.dvec),
+                                    B, S, H, Dh, x.inv_sqrt_dh, x.c.causal, x.k<void>(x.L.dA), x.k<void>(x.L.dqkv),
+                                    x.st);
       const int64_t so[2] = {S * Ea, Dh}, sv[2] = {S * 3 * Ea, Dh}, sp[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
       if (bf) {  // softmax backward in the epilogue: dA = P * (dO V^T - D) / sqrt(h), straight to bf16
@@ -281,6 +290,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
                   x.s<uint8_t>(x.L.qkv) + es * 2 * Ea, 3 * Ea, sv, 0.f, x.k<float>(x.L.scores), NNT_F32, S, sp, &e);
     }
     case NNT_OP_ATT_DV: {
+      if (x.fused_attn) return NNT_OK;  // formed in NNT_OP_ATT_DP
       const int64_t sp[2] = {H * S * S, S * S}, so[2] = {S * Ea, Dh}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
       return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.s<void>(x.L.P), S, sp, x.k<void>(x.L.dO), Ea, so,
@@ -294,10 +304,14 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
     case NNT_OP_ATT_DQ: {
       const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
+      if (x.fused_attn)  // dQ = dA K with dA stored keys-major (op(A) = (dA^T)^T)
+        return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
+                    x.s<uint8_t>(x.L.qkv) + es * Ea, 3 * Ea, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * Ea, sq, &e);
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
                   x.s<uint8_t>(x.L.qkv) + es * Ea, 3 * Ea, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * Ea, sq, &e);
     }
     case NNT_OP_ATT_DK: {
+      if (x.fused_attn) return NNT_OK;  // formed in NNT_OP_ATT_DP
       const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_UPPER : NNT_CAUSAL_NONE;
       return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp, x.s<void>(x.L.qkv),
@@ -346,6 +360,11 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.side = nullptr;
   x.links = nullptr;
   x.ln_rows = true;
+  static const bool attn_env = [] {  // NNT_ATTN_FUSED=0: the unfused GEMM sequence (A/B runs)
+    const char* e = getenv("NNT_ATTN_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  x.fused_attn = attn_env && c.dtype == NNT_BF16 && nnt_attention_fused_supported(c.S, x.Dh);
   return x;
 }
 

@@ -1,5 +1,7 @@
 // Shared GEMM argument block and epilogue (SIMT fp32 path and tcgen05 bf16 path).
 #pragma once
+#include <cuda.h>
+
 #include "nnt_internal.h"
 
 namespace nnt {
@@ -41,6 +43,11 @@ int64_t gemm_tc_splits(const GemmArgs& a);  // split-K factor the tcgen05 path w
 // split-K workspace bytes for `splits` (partials + a_rowsum partials + the in-kernel reduce's
 // arrival counters; 0 when splits == 1)
 size_t splitk_workspace_bytes(const GemmArgs& a, int64_t splits);
+// 4-D TMA tensor map (dims {inner, outer, batch1, batch0}, SWIZZLE_128B, box {box_inner, box_outer,
+// 1, 1}; es = element bytes, ld / s1 / s0 in elements)
+nnt_status make_tma_map_4d(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t inner,
+                           int64_t outer, int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_inner,
+                           int box_outer);
 
 // Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.
 template <typename TC>

@@ -29,6 +29,7 @@
 #include <mutex>
 
 #include "gemm_common.cuh"
+#include "tc_ptx.cuh"
 
 namespace nnt {
 namespace {
@@ -133,237 +134,7 @@ struct TcParams {
   uint32_t* counters;
 };
 
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  uint32_t ok = 0;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(ok)
-        : "r"(bar), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-
-__device__ __forceinline__ void tma_load_4d(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
-                                            int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
-      "[%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, uint32_t src, int c0, int c1, int c2, int c3) {
-  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
-                   reinterpret_cast<uint64_t>(map)),
-               "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-               : "memory");
-}
-// CTA-pair (cta_group::2) variants: the TMA completes bytes on the leader CTA's mbarrier
-// (shared::cluster address), MMA completion is multicast to the same barrier of both CTAs.
-__device__ __forceinline__ void tma_load_4d_pair(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                                 int c1, int c2, int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-      "%5, %6}], [%2];" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Arrive on a (possibly remote) barrier of the cluster.  Default .release.cta semantics: the
-// only thing the waiter (the leader's MMA issuer) relies on is that this warp's tcgen05.ld of
-// the accumulator completed, which tcgen05.wait::ld + tcgen05.fence::before_thread_sync order
-// before the arrive; a .release.cluster arrive costs a GPU-scope MEMBAR per warp and tile.
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
-__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
-__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
-
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit(uint32_t bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                              uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
-      "h"((uint16_t)3)
-      : "memory");
-}
-
-
-// ---- warp-wide issue: the producer and MMA loops run on all 32 lanes of their warp (uniform
-// control flow, operands in uniform registers); each issuing instruction is guarded by an
-// elect.sync inside its asm, so exactly one lane issues it.  (A single-lane loop made the
-// compiler wrap every tcgen05.mma in an R2UR/ELECT waterfall: ~140 cycles per MMA issue.)
-#define NNT_ELECT "elect.sync _|e, 0xffffffff;\n\t"
-__device__ __forceinline__ void mbar_expect_tx_w(uint32_t bar, uint32_t bytes) {
-  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(bar),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_load_4d_w(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1, int c2,
-                                              int c3) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t" NNT_ELECT
-      "@e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
-      "[%2];\n\t}" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_4d_pair_w(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
-                                                   int c1, int c2, int c3) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t" NNT_ELECT
-      "@e cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
-      "%5, %6}], [%2];\n\t}" ::"r"(dst),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
-__device__ __forceinline__ void mma_bf16_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                           uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t" NNT_ELECT
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void mma_bf16_pair_w(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                                uint32_t accum) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t" NNT_ELECT
-      "@e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-      : "memory");
-}
-__device__ __forceinline__ void mma_commit_w(uint32_t bar) {
-  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
-               "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
-               : "memory");
-}
-__device__ __forceinline__ void mma_commit_pair_w(uint32_t bar) {
-  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
-               "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(
-                   bar),
-               "h"((uint16_t)3)
-               : "memory");
-}
-
-// 32 consecutive fp32 columns of this warp's TMEM lane quadrant, no wait
-__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t* r) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-}
-// n x 32 columns (n loads in flight, one wait)
-template <int n>
-__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, float* v) {
-  uint32_t r[32 * n];
-#pragma unroll
-  for (int h = 0; h < n; ++h) tmem_ld32_nowait(taddr + 32 * h, r + 32 * h);
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 32 * n; ++j) v[j] = __uint_as_float(r[j]);
-}
-
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
-      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-}
-
-// No-swizzle K-major descriptor (core matrices of 8 rows x 16 B; lbo / sbo between core matrices
-// along K / along M-N).  Only the all-ones a_rowsum tile uses it, whose bytes are all equal.
-__device__ __forceinline__ uint64_t make_sdesc_noswz(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell); layout type 0 = SWIZZLE_NONE
-  return d;
-}
-__device__ __forceinline__ float tmem_ld1(uint32_t taddr) {
-  uint32_t r;
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-  return __uint_as_float(r);
-}
-
-// SW128 shared-memory matrix descriptor (sm_100 "version 1" format).
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
-  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
-  return d;
-}
+// PTX helpers (mbarrier, TMA, tcgen05 MMA / TMEM, smem descriptors): tc_ptx.cuh
 
 // Output tiles per task: 1, or (ORDER_ROWS) the key tiles of the task's row block.
 __device__ __forceinline__ int64_t task_subtiles(const TcParams& P, int64_t t, int bn) {
@@ -451,14 +222,6 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
 }
 
 // ------------------------------------------------------------------ epilogue math
-// 2^x as one MUFU.EX2 (results below 2^-126 flush to 0: immaterial for softmax weights <= 1;
-// exp2f's IEEE path adds a denormal-range rescale around every MUFU op)
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 template <bool kFast>
 __device__ __forceinline__ float tanh_f(float x) {
   if (kFast) {  // bf16 outputs: tanh.approx (rel err ~2^-11) is below bf16 rounding
@@ -529,46 +292,10 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o, bool cg) {
   }
 }
 
-// One 128-byte row chunk of an epilogue input (W elements of TI) loaded through the
-// read-only path (the two 16-byte halves of a 32-byte sector share one L1 fill) one chunk
-// ahead of its use, unpacked 8 values at a time.
-struct Raw8 {
-  uint4 u[8];
-};
-__device__ __forceinline__ void raw_load(Raw8& r, const void* p) {
-  const uint4* src = reinterpret_cast<const uint4*>(p);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) r.u[i] = __ldg(src + i);
-}
-template <typename TI>
-__device__ __forceinline__ void unpack8(const Raw8& r, int j, float* t) {
-  if (sizeof(TI) == 4) {
-    const uint4 a = r.u[j / 4], b = r.u[j / 4 + 1];
-    t[0] = __uint_as_float(a.x); t[1] = __uint_as_float(a.y); t[2] = __uint_as_float(a.z); t[3] = __uint_as_float(a.w);
-    t[4] = __uint_as_float(b.x); t[5] = __uint_as_float(b.y); t[6] = __uint_as_float(b.z); t[7] = __uint_as_float(b.w);
-  } else {
-    const uint4 a = r.u[j / 8];
-    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&a);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      float2 f = __bfloat1622float2(h[i]);
-      t[2 * i] = f.x;
-      t[2 * i + 1] = f.y;
-    }
-  }
-}
 // The streamed (prefetched) epilogue input of a GEMM: at most one, element type = C's.
 // IN_AUX_SMEM: the aux chunk is TMA-loaded into the chunk's staging buffer at tile start
 // (before the accumulator wait) and read from shared memory; the output overwrites it in place.
 enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3, IN_AUX_SMEM = 4 };
-
-// Reads back one 128-byte row chunk from SW128 staging (the layout stage_row writes and a
-// 32-row TMA box of the same map loads).
-__device__ __forceinline__ void unstage_row(Raw8& r, const uint8_t* buf, int lane) {
-  const uint8_t* rowp = buf + lane * 128;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) r.u[j] = *reinterpret_cast<const uint4*>(rowp + ((j ^ (lane & 7)) << 4));
-}
 
 // The W pre-activation outputs of one row chunk (GELU is applied by the caller after
 // staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
@@ -689,32 +416,6 @@ __device__ __forceinline__ void epi_math(const GemmArgs& g, const TC* Cb, const 
       for (int j = 0; j < W; ++j)
         if (full || col0 + j < g.N) v[j] *= gelu_grad_e<kFast>(ld_elem(ar + j));
     }
-  }
-}
-
-// Writes a 128-byte row chunk to SW128-swizzled staging (row = lane, 8 x 16 B pieces).
-template <typename TS, int W>
-__device__ __forceinline__ void stage_row(uint8_t* buf, int lane, const float (&v)[W]) {
-  uint8_t* rowp = buf + lane * 128;
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint4 u;
-    if (sizeof(TS) == 4) {
-      u.x = __float_as_uint(v[4 * j]);
-      u.y = __float_as_uint(v[4 * j + 1]);
-      u.z = __float_as_uint(v[4 * j + 2]);
-      u.w = __float_as_uint(v[4 * j + 3]);
-    } else {
-      __nv_bfloat162 t0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
-      __nv_bfloat162 t1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
-      __nv_bfloat162 t2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
-      __nv_bfloat162 t3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
-      u.x = *reinterpret_cast<uint32_t*>(&t0);
-      u.y = *reinterpret_cast<uint32_t*>(&t1);
-      u.z = *reinterpret_cast<uint32_t*>(&t2);
-      u.w = *reinterpret_cast<uint32_t*>(&t3);
-    }
-    *reinterpret_cast<uint4*>(rowp + ((j ^ (lane & 7)) << 4)) = u;
   }
 }
 
@@ -1554,6 +1255,13 @@ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace
 
+nnt_status make_tma_map_4d(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t inner,
+                           int64_t outer, int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_inner,
+                           int box_outer) {
+  NNT_TRY(get_encoder());
+  return make_map(map, dt, es, base, inner, outer, ld, b1, s1, b0, s0, box_inner, box_outer);
+}
+
 // Split-K factor for a GEMM: fp32 C, no activation, unbatched, non-causal, an output grid
 // that leaves SMs idle and a K long enough to cut (>= 8 K-blocks per split).
 namespace {
@@ -1637,7 +1345,15 @@ uint32_t* splitk_counters(const GemmArgs& a) {
 // The reduce runs in the GEMM when the workspace holds partials + counter zone, the tile grid's
 // counters fit the zone (split GEMMs use 256-wide tiles), C is TMA-storable and no a_rowsum is
 // requested (that keeps the separate ordered reduce kernel).
+bool fused_reduce_on() {  // NNT_SPLITK_FUSED=0: the separate ordered reduce kernel (A/B runs)
+  static const bool on = [] {
+    const char* e = getenv("NNT_SPLITK_FUSED");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
+  if (!fused_reduce_on()) return false;
   const int64_t regions = (cdiv(a.M, BM) + 1) * cdiv(a.N, 256) * kEpiWarps;
   return splits > 1 && !a.a_rowsum && a.workspace_bytes >= splitk_workspace_bytes(a, splits) &&
          regions <= kSplitCounters && c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;

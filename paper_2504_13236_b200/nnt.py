@@ -49,7 +49,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_block_tp_workspace_size", "nnt_block_tp_fwd", "nnt_block_tp_bwd",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
-           "nnt_cross_entropy")
+           "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv")
 
 
 class NNTError(RuntimeError):
@@ -133,6 +133,9 @@ _sig = {
     "nnt_maxsumexp": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _i32, _vp]),
     "nnt_maxsumexp_merge": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp]),
     "nnt_attn_rowdot": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
+    "nnt_attention_fused_supported": (_i32, [_i64, _i64]),
+    "nnt_attention_fwd_pv": (_i32, [_vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp, _vp]),
+    "nnt_attention_bwd_kv": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
     "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
     "nnt_layernorm_fwd": (_i32, [_vp, _i64, _i64, _i64, _i64, _vp, _vp, _f32, _vp, _i32, _i64, _vp, _vp, _vp]),
@@ -282,6 +285,20 @@ def nnt_maxsumexp_merge(part, rows, nparts, ld_parts, part_cols, causal, seq_q, 
 
 def nnt_attn_rowdot(dO, O, dtype, B, S, H, h, D, stream=None):
     return check(lib.nnt_attn_rowdot(ptr(dO), ptr(O), dtype, B, S, H, h, ptr(D), _stream(stream)))
+
+
+def nnt_attention_fused_supported(S, h):
+    return bool(lib.nnt_attention_fused_supported(S, h))
+
+
+def nnt_attention_fwd_pv(qkv, B, S, H, h, scale, causal, stats, P, O, stream=None):
+    return check(lib.nnt_attention_fwd_pv(ptr(qkv), B, S, H, h, scale, causal, ptr(stats), ptr(P), ptr(O),
+                                          _stream(stream)))
+
+
+def nnt_attention_bwd_kv(qkv, dO, P, D, B, S, H, h, scale, causal, dAT, dqkv, stream=None):
+    return check(lib.nnt_attention_bwd_kv(ptr(qkv), ptr(dO), ptr(P), ptr(D), B, S, H, h, scale, causal, ptr(dAT),
+                                          ptr(dqkv), _stream(stream)))
 
 
 def nnt_softmax(x, rows, cols, ldx, tile_k, causal, seq_q, stats, y, y_dtype, ldy, stream=None):

@@ -99,7 +99,8 @@ def test_tiny_fp32_three_training_steps():
         _update_close(host(wv) - w_init[n], P[0][n] - w_init[n], m[n], P[0][n], np.sqrt(v_[n]), 1e-4, n)
 
 
-@pytest.mark.parametrize("S,B", [(256, 2), (1024, 1)])
+# S = 192: not a multiple of 128 -> the unfused attention GEMM sequence (nnt_attention_fused_supported)
+@pytest.mark.parametrize("S,B", [(256, 2), (1024, 1), (192, 2)])
 def test_bf16_gpt2_small_block(S, B):
     """GPT-2-small-shaped block (E=768, H=12) on the tcgen05 path vs the fp64 oracle, rel <= 2e-2.
 
