@@ -590,6 +590,18 @@ nnt_status nnt_block_dag_describe(const nnt_block_cfg* cfg, int pass,
                                   nnt_task* tasks, int64_t task_cap, int64_t* n_tasks,
                                   nnt_launch_group* groups, int64_t group_cap, int64_t* n_groups);
 
+/* The STF graph builder the block plans use ("inserts tasks into the graph one by one";
+ * dependency rules S:46: R->R none, R->W/RW edge, W/RW->anything edge, Reduce->Reduce none,
+ * Reduce<->R/W/RW edge), on an arbitrary program: n_tasks tasks submitted in order over handles
+ * 0..n_handles-1; task t has n_acc[t] accesses, taken in order from acc_handle / acc_mode
+ * (nnt_access_mode: 0 R, 1 W, 2 RW, 3 Reduce; a handle at most once per task).  Outputs (host
+ * arrays): level[n_tasks] (longest dependency chain), dep_offsets[n_tasks + 1] and the
+ * predecessor lists dep_ids[dep_offsets[t] .. dep_offsets[t+1]) (at most dep_cap entries;
+ * NNT_ERR_WORKSPACE with dep_offsets filled when dep_cap is too small).  Host-only, for tests. */
+nnt_status nnt_stf_build(int64_t n_handles, int64_t n_tasks, const int32_t* n_acc, const int64_t* acc_handle,
+                         const int32_t* acc_mode, int32_t* level, int64_t* dep_offsets, int32_t* dep_ids,
+                         int64_t dep_cap);
+
 /* ------------------------------------------------------------------------- */
 /* Kernel timing (bench.py roofline): CUDA events around every launch.         */
 /* ------------------------------------------------------------------------- */

@@ -1,8 +1,9 @@
 // STF tile-task DAG of the GPT-2 block ("nodes correspond to tasks and
 // directed edges correspond to tiles", P:80-84 sequential task flow), with the
 // access-mode dependency rules of S:46 and the lowering used by nnt_block_fwd /
-// nnt_block_bwd.  Host-only integer code; bit-exact tests compare it with a
-// Python reference (tests/test_dag.py).
+// nnt_block_bwd.  Host-only integer code: the block plans' task counts / levels are
+// tested bit-exactly (tests/test_abi.py), the graph builder itself by a serializability
+// fuzz against a sequential Python executor through nnt_stf_build (tests/test_dag.py).
 #include "dag.h"
 
 #include <algorithm>
@@ -584,6 +585,49 @@ const char* nnt_op_name(int op) {
       "att_dq",   "att_dk",   "qkv_db",   "qkv_dw",    "qkv_dx",      "ln1_bwd"};
   if (op < 0 || op >= NNT_OP_COUNT) return "?";
   return names[op];
+}
+
+nnt_status nnt_stf_build(int64_t n_handles, int64_t n_tasks, const int32_t* n_acc, const int64_t* acc_handle,
+                         const int32_t* acc_mode, int32_t* level, int64_t* dep_offsets, int32_t* dep_ids,
+                         int64_t dep_cap) {
+  NNT_REQUIRE(n_handles > 0 && n_tasks >= 0 && n_handles < (1ll << 31) && n_tasks < (1ll << 31), NNT_ERR_SHAPE,
+              "nnt_stf_build: n_handles=%lld n_tasks=%lld", (long long)n_handles, (long long)n_tasks);
+  NNT_REQUIRE(n_tasks == 0 || (n_acc && acc_handle && acc_mode && level && dep_offsets), NNT_ERR_NULL,
+              "nnt_stf_build: NULL argument");
+  StfGraph g;
+  const int tensor = g.new_tensor(n_handles);
+  int64_t a = 0;
+  const int64_t zero[3] = {0, 0, 0};
+  for (int64_t t = 0; t < n_tasks; ++t) {
+    NNT_REQUIRE(n_acc[t] > 0, NNT_ERR_ARG, "nnt_stf_build: task %lld has no access", (long long)t);
+    std::vector<std::pair<int64_t, int>> hm;
+    for (int32_t i = 0; i < n_acc[t]; ++i, ++a) {
+      const int64_t h = acc_handle[a];
+      const int m = acc_mode[a];
+      NNT_REQUIRE(h >= 0 && h < n_handles && m >= ACC_R && m <= ACC_REDUCE, NNT_ERR_ARG,
+                  "nnt_stf_build: access (%lld, %d)", (long long)h, m);
+      for (auto& e : hm)
+        NNT_REQUIRE(e.first != g.handle(tensor, h), NNT_ERR_ARG, "nnt_stf_build: handle %lld twice in task %lld",
+                    (long long)h, (long long)t);
+      hm.emplace_back(g.handle(tensor, h), m);
+    }
+    g.submit((int)(t % NNT_OP_COUNT), zero, hm);
+  }
+  int64_t n = 0;
+  dep_offsets[0] = 0;
+  for (int64_t t = 0; t < n_tasks; ++t) {
+    level[t] = g.tasks[t].level;
+    n += (int64_t)g.tasks[t].deps.size();
+    dep_offsets[t + 1] = n;
+  }
+  NNT_REQUIRE(n <= dep_cap && (n == 0 || dep_ids), NNT_ERR_WORKSPACE, "nnt_stf_build: %lld dependencies > cap %lld",
+              (long long)n, (long long)dep_cap);
+  for (int64_t t = 0; t < n_tasks; ++t) {
+    std::vector<int> d = g.tasks[t].deps;
+    std::sort(d.begin(), d.end());
+    for (size_t i = 0; i < d.size(); ++i) dep_ids[dep_offsets[t] + (int64_t)i] = d[i];
+  }
+  return NNT_OK;
 }
 
 nnt_status nnt_block_dag_describe(const nnt_block_cfg* cfg, int pass, nnt_task* tasks, int64_t task_cap,

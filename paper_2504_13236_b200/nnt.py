@@ -49,7 +49,8 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_block_tp_workspace_size", "nnt_block_tp_fwd", "nnt_block_tp_bwd",
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
-           "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv")
+           "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv",
+           "nnt_stf_build")
 
 
 class NNTError(RuntimeError):
@@ -134,6 +135,7 @@ _sig = {
     "nnt_maxsumexp_merge": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp]),
     "nnt_attn_rowdot": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
     "nnt_attention_fused_supported": (_i32, [_i64, _i64]),
+    "nnt_stf_build": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
     "nnt_attention_fwd_pv": (_i32, [_vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp, _vp]),
     "nnt_attention_bwd_kv": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
@@ -285,6 +287,24 @@ def nnt_maxsumexp_merge(part, rows, nparts, ld_parts, part_cols, causal, seq_q, 
 
 def nnt_attn_rowdot(dO, O, dtype, B, S, H, h, D, stream=None):
     return check(lib.nnt_attn_rowdot(ptr(dO), ptr(O), dtype, B, S, H, h, ptr(D), _stream(stream)))
+
+
+def nnt_stf_build(n_handles, tasks):
+    """tasks: list of [(handle, mode), ...] in submission order (modes 0 R, 1 W, 2 RW, 3 Reduce).
+    Returns (levels, deps) with deps[t] the sorted predecessor list of task t."""
+    import numpy as np
+    n = len(tasks)
+    n_acc = np.array([len(t) for t in tasks], np.int32)
+    hs = np.array([h for t in tasks for h, _ in t], np.int64)
+    ms = np.array([m for t in tasks for _, m in t], np.int32)
+    level = np.zeros(max(n, 1), np.int32)
+    offs = np.zeros(n + 1, np.int64)
+    cap = max(1, n * n)
+    ids = np.zeros(cap, np.int32)
+    p = lambda a: a.ctypes.data if a.size else None  # noqa: E731
+    check(lib.nnt_stf_build(n_handles, n, p(n_acc), p(hs), p(ms), level.ctypes.data, offs.ctypes.data,
+                            ids.ctypes.data, cap))
+    return level[:n].tolist(), [ids[offs[t]:offs[t + 1]].tolist() for t in range(n)]
 
 
 def nnt_attention_fused_supported(S, h):
