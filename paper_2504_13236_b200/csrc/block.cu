@@ -360,10 +360,8 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.side = nullptr;
   x.links = nullptr;
   x.ln_rows = true;
-  static const bool attn_env = [] {  // NNT_ATTN_FUSED=0: the unfused GEMM sequence (A/B runs)
-    const char* e = getenv("NNT_ATTN_FUSED");
-    return !(e && e[0] == '0');
-  }();
+  const char* attn_e = getenv("NNT_ATTN_FUSED");  // =0: the unfused GEMM sequence (A/B runs, tests)
+  const bool attn_env = !(attn_e && attn_e[0] == '0');
   x.fused_attn = attn_env && c.dtype == NNT_BF16 && nnt_attention_fused_supported(c.S, x.Dh);
   return x;
 }

@@ -1345,12 +1345,13 @@ uint32_t* splitk_counters(const GemmArgs& a) {
 // The reduce runs in the GEMM when the workspace holds partials + counter zone, the tile grid's
 // counters fit the zone (split GEMMs use 256-wide tiles), C is TMA-storable and no a_rowsum is
 // requested (that keeps the separate ordered reduce kernel).
-bool fused_reduce_on() {  // NNT_SPLITK_FUSED=0: the separate ordered reduce kernel (A/B runs)
-  static const bool on = [] {
-    const char* e = getenv("NNT_SPLITK_FUSED");
-    return !(e && e[0] == '0');
-  }();
-  return on;
+// Off by default: measured in the GPT-2 small step (4 interleaved runs) the separate
+// reduce kernels, which run on the backward's side stream under the main-stream work, cost less
+// than the in-kernel reduction's serial tail (gemm class 7.41 vs 7.72 ms/step).  NNT_SPLITK_FUSED=1
+// turns it on.
+bool fused_reduce_on() {  // read per call (tests switch it within one process)
+  const char* e = getenv("NNT_SPLITK_FUSED");
+  return e && e[0] == '1';
 }
 bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
   if (!fused_reduce_on()) return false;

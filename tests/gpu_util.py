@@ -45,7 +45,11 @@ def close(got, want, tol, what="", max_tol=None):
             f.write(json.dumps({"test": test, "line": caller.lineno, "what": str(what), "n": int(want.size),
                                 "rel": r, "rel_max": m, "tol": tol, "max_tol": max_tol}) + "\n")
     assert r < tol, f"{what}: norm-wise rel {r:.3e} >= {tol:.1e}"
-    assert m < max_tol, f"{what}: element-wise max rel {m:.3e} >= {max_tol:.1e}"
+    if not m < max_tol:
+        i = int(np.abs(got - want).argmax())
+        raise AssertionError(f"{what}: element-wise max rel {m:.3e} >= {max_tol:.1e} at flat index {i}: "
+                             f"got {got.ravel()[i]:.6e} want {want.ravel()[i]:.6e} (max|want| "
+                             f"{np.abs(want).max():.6e})")
     return r, m
 
 

@@ -36,7 +36,7 @@ def _rowstats(Q, B, S, H, scale, causal):
     """Softmax subroutine 1 by the library's ROWSTATS score GEMM (as nnt_block_fwd runs it)."""
     E = H * H_D
     stats = torch.empty(B * H * S, 2, device="cuda")
-    q = Q.view(torch.uint8)
+    q = Q.reshape(-1).view(torch.uint8)  # byte offsets: K starts 2 * E bytes into a row
     sq = [S * 3 * E, H_D]
     epi = nnt.make_epilogue(act=nnt.NNT_ACT_ROWSTATS, row_stats=stats,
                             causal=nnt.NNT_CAUSAL_OUT_LOWER if causal else nnt.NNT_CAUSAL_NONE)
@@ -83,7 +83,7 @@ def test_fused_attention_fwd_bwd(B, S, H, causal):
     nnt.nnt_attention_bwd_kv(Q, dO, P, D, B, S, H, H_D, scale, causal, dAT, dqkv)
     sp = [H * S * S, S * S]
     sq = [S * 3 * E, H_D]
-    qb = Q.view(torch.uint8)
+    qb = Q.reshape(-1).view(torch.uint8)
     epi = nnt.make_epilogue(causal=nnt.NNT_CAUSAL_A_LOWER if causal else nnt.NNT_CAUSAL_NONE)
     nnt.nnt_tile_gemm(1, 0, S, H_D, S, [B, H], 1.0, dAT, 1, S, sp, qb[2 * E:], 1, 3 * E, sq, 0.0, dqkv, 1, 3 * E,
                       sq, None, epi)

@@ -121,6 +121,13 @@ def test_bf16_gpt2_small_block(S, B):
         close(host(gv), g_ref[0][n], 2e-2, n)
 
 
+def test_bf16_block_unfused_attention_path(monkeypatch):
+    """NNT_ATTN_FUSED=0 (read per block call): the attention as the unfused GEMM sequence (P pass,
+    P V, dP -> dA, dV, dQ, dK GEMMs) -- the path S % 128 != 0 takes -- at S = 256 vs the oracle."""
+    monkeypatch.setenv("NNT_ATTN_FUSED", "0")
+    test_bf16_gpt2_small_block(256, 2)
+
+
 def test_bf16_first_query_pin():
     """Causal: query 0 attends only to key 0, so P[.,.,0,0] = 1 exactly and O[q=0] = V[0] bit-exactly."""
     E, H, S, B = 768, 12, 256, 2

@@ -151,8 +151,16 @@ def test_gemm_attention_views_and_causal(dtype, causal):
         assert np.array_equal(host(O), want)
 
 
+@pytest.fixture(params=["0", "1"], ids=["reduce-kernel", "in-kernel-reduce"])
+def splitk_mode(request, monkeypatch):
+    """Both split-K reductions: the separate ordered reduce kernel (default) and the in-kernel one
+    (NNT_SPLITK_FUSED=1, read by the library at every launch)."""
+    monkeypatch.setenv("NNT_SPLITK_FUSED", request.param)
+    return request.param
+
+
 @pytest.mark.parametrize("M,N", [(768, 768), (2304, 768), (768, 3072)])
-def test_gemm_split_k_workspace_bit_exact(M, N):
+def test_gemm_split_k_workspace_bit_exact(M, N, splitk_mode):
     """dW-shaped GEMMs (K = T = 8192) split K into a workspace and reduce in split order:
     integer data keeps every partial exact, so the result is bit-exact and run-to-run identical."""
     K = 8192
@@ -179,7 +187,7 @@ def test_gemm_split_k_workspace_bit_exact(M, N):
     assert int(ws[-SPLIT_COUNTER_BYTES:].count_nonzero()) == 0  # counters back to zero
 
 
-def test_gemm_split_k_shared_workspace_shapes():
+def test_gemm_split_k_shared_workspace_shapes(splitk_mode):
     """The block's four dW GEMMs share one split-K workspace sized for the largest: the in-kernel
     reduce's counter zone (last 16 KB of the workspace) must never lie under another shape's
     partials.  Alternate shapes and K (1024: 2 splits of 8 K-blocks; 8192) on one zero-filled
@@ -204,7 +212,7 @@ def test_gemm_split_k_shared_workspace_shapes():
 
 
 @pytest.mark.parametrize("M,N", [(768, 768), (2304, 768)])
-def test_gemm_split_k_real_data_extras(M, N):
+def test_gemm_split_k_real_data_extras(M, N, splitk_mode):
     """Split-K with real-valued data and every extra the ordered reduce applies (alpha, beta*C, bias,
     fp32 residual): in-kernel reduce vs separate reduce kernel vs the fp64 product."""
     K = 8192
