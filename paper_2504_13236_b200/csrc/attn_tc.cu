@@ -51,6 +51,19 @@ __host__ __device__ constexpr uint32_t idesc_of(bool a_mn, bool b_mn, int n) {
          ((uint32_t)(n >> 3) << 17) | ((uint32_t)(TB >> 4) << 24);
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 1-D bulk copy global -> shared, completing `bytes` on the mbarrier (one elected lane)
+__device__ __forceinline__ void bulk_load_w(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("{\n\t.reg .pred e;\n\t" NNT_ELECT
+               "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
 __device__ __forceinline__ int64_t task_at(int64_t c, int64_t G, int64_t k) {
   return k * G + ((k & 1) ? (G - 1 - c) : c);
 }
@@ -152,44 +165,57 @@ __global__ void __launch_bounds__(kAThreads, 1)
     pdl_trigger();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // A flat stream of iterations g over this CTA's tasks (S / P buffer g & 1, stage g % 3): the S
+    // MMA of iteration g + 1 -- also the first one of the next task -- is issued before the O MMA
+    // of iteration g, which waits for the epilogue's P, so the tensor core runs ahead of the
+    // epilogue across task boundaries too.
     const uint32_t id_s = idesc_of(false, false, TB);  // S = Q K^T: both K-major, N = 128
     const uint32_t id_o = idesc_of(false, true, HD);   // O += P V: P K-major, V MN-major, N = 64
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0;  // iterations over all tasks (S / P buffer parity)
-    int tl = 0;
-    for (int64_t k = 0;; ++k, ++tl) {
-      const int64_t t = task_at(c0, G, k);
-      if (t >= P.num_tasks) break;
-      int qb, b, h;
-      decode(t, qb, b, h);
-      const int qs = tl & 1, os = tl & 1;
-      mbar_wait(smem_u32(&qfull[qs]), (tl >> 1) & 1);
-      mbar_wait(smem_u32(&oempty[os]), ((tl >> 1) & 1) ^ 1);
+    auto nk_of = [&](int qb) { return P.causal ? qb + 1 : P.nblk; };
+    auto issue_s = [&](int64_t g, int tl, int i, int nk) {
+      const int sb = (int)(g & 1), stg = (int)(g % F_STAGES);
+      const int qs = tl & 1;
+      if (i == 0) mbar_wait(smem_u32(&qfull[qs]), (tl >> 1) & 1);
+      mbar_wait(smem_u32(&sempty[sb]), (uint32_t)(((g >> 1) & 1) ^ 1));
+      mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / F_STAGES) & 1));
       tc_fence_after();
       const uint32_t sq = smem_u32(smem + F_Q + qs * TILE16);
-      const int nk = P.causal ? qb + 1 : P.nblk;
-      // software pipeline: S MMA of iteration i+1 is issued before the O MMA of iteration i
-      // (which waits for the epilogue's P), so the tensor core works while the epilogue runs
-      auto issue_s = [&](int i, int stg) {
-        const int sb = (it + i) & 1;
-        mbar_wait(smem_u32(&sempty[sb]), (((it + i) >> 1) & 1) ^ 1);
-        mbar_wait(smem_u32(&full[stg]), (uint32_t)((phase + ((stage + i) / F_STAGES)) & 1));
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + F_ST + stg * 2 * TILE16);
+      const uint32_t sk = smem_u32(smem + F_ST + stg * 2 * TILE16);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
-                     kk > 0 ? 1u : 0u);
-        mma_commit_w(smem_u32(&sfull[sb]));
-      };
-      issue_s(0, stage);
-      for (int i = 0; i < nk; ++i) {
-        const int stg = (stage + i) % F_STAGES;
-        if (i + 1 < nk) issue_s(i + 1, (stage + i + 1) % F_STAGES);
-        else mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
-        const int pb = (it + i) & 1;
-        mbar_wait(smem_u32(&pfull[pb]), ((it + i) >> 1) & 1);
+      for (int kk = 0; kk < HD / 16; ++kk)
+        mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
+                   kk > 0 ? 1u : 0u);
+      mma_commit_w(smem_u32(&sfull[sb]));
+      if (i == nk - 1) mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
+    };
+    int64_t k = 0;
+    int64_t t = task_at(c0, G, 0);
+    if (t < P.num_tasks) {
+      int qb, b, h;
+      decode(t, qb, b, h);
+      int tl = 0, i = 0, nk = nk_of(qb);
+      int64_t g = 0;
+      issue_s(0, 0, 0, nk);
+      for (;;) {
+        // the next iteration: (tl, i + 1) or the first of the next task
+        int tl2 = tl, i2 = i + 1, nk2 = nk;
+        bool more = true;
+        if (i2 == nk) {
+          const int64_t t2 = task_at(c0, G, k + 1);
+          more = t2 < P.num_tasks;
+          if (more) {
+            int qb2, b2, h2;
+            decode(t2, qb2, b2, h2);
+            tl2 = tl + 1;
+            i2 = 0;
+            nk2 = nk_of(qb2);
+          }
+        }
+        if (more) issue_s(g + 1, tl2, i2, nk2);
+        // O += P V for iteration g
+        const int os = tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
+        if (i == 0) mbar_wait(smem_u32(&oempty[os]), ((tl >> 1) & 1) ^ 1);
+        mbar_wait(smem_u32(&pfull[pb]), (uint32_t)((g >> 1) & 1));
         tc_fence_after();
         const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
         const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
@@ -199,12 +225,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
                      make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(smem_u32(&pempty[pb]));
         mma_commit_w(smem_u32(&empty[stg]));
+        if (i == nk - 1) mma_commit_w(smem_u32(&ofull[os]));
+        if (!more) break;
+        if (tl2 != tl) ++k;
+        tl = tl2;
+        i = i2;
+        nk = nk2;
+        ++g;
       }
-      mma_commit_w(smem_u32(&ofull[os]));
-      // advance the stage ring and iteration counter by this task's nk iterations
-      phase ^= (uint32_t)(((stage + nk) / F_STAGES) & 1);
-      stage = (stage + nk) % F_STAGES;
-      it += nk;
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..9
@@ -212,14 +240,24 @@ __global__ void __launch_bounds__(kAThreads, 1)
     const float L2E = 1.4426950408889634f;
     const float sc = P.scale * L2E;
     int it = 0, tl = 0;
+    // the row statistics of this lane's query row, loaded one task ahead
+    auto stats_of = [&](int64_t tt) {
+      if (tt >= P.num_tasks) return make_float2(0.f, 1.f);
+      int qb_, b_, h_;
+      decode(tt, qb_, b_, h_);
+      return __ldg(reinterpret_cast<const float2*>(P.stats) +
+                   ((int64_t)(b_ * P.H + h_) * P.S + qb_ * TB + quad * 32 + lane));
+    };
+    float2 st_next = stats_of(task_at(c0, G, 0));
     for (int64_t k = 0;; ++k, ++tl) {
       const int64_t t = task_at(c0, G, k);
       if (t >= P.num_tasks) break;
       int qb, b, h;
       decode(t, qb, b, h);
       const int q = qb * TB + quad * 32 + lane;  // this lane's query row
-      const float2 st = __ldg(reinterpret_cast<const float2*>(P.stats) + ((int64_t)(b * P.H + h) * P.S + q));
-      const float ml = st.x * L2E, inv = 1.f / st.y;
+      const float2 st = st_next;
+      st_next = stats_of(task_at(c0, G, k + 1));
+      const float ml = st.x * L2E, inv = rcp_approx(st.y);
       const int nk = P.causal ? qb + 1 : P.nblk;
       for (int i = 0; i < nk; ++i, ++it) {
         const int sb = it & 1;
@@ -241,9 +279,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
             v[j] = y.x;
             v[j + 1] = y.y;
           }
-        } else {
+        } else {  // diagonal tile: keys > q masked (-> 0); no exponentials for whole masked halves
+          if (lim > 0) {
 #pragma unroll
-          for (int j = 0; j < 64; ++j) v[j] = j < lim ? ex2_approx(fmaf(v[j], sc, -ml)) * inv : 0.f;
+            for (int j = 0; j < 64; ++j) v[j] = ex2_approx(j < lim ? fmaf(v[j], sc, -ml) : -INFINITY) * inv;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 64; ++j) v[j] = 0.f;
+          }
         }
         // P piece -> staging buffer pb (after MMA O of iteration it-2 and this warp's store of it)
         const int pb = it & 1;
@@ -294,11 +337,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
 }
 
 // ============================================================================ backward
-// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | dA^T staging (32 KB:
+// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB), D_qb} | dA^T staging (32 KB:
 // query half h at +16 KB, quadrant rows at +4 KB) | barriers.  TMEM: dP^T[2] at columns 0 / 128,
 // {dV, dK}[2] at 256 / 384 (+64 for dK).
 constexpr int B_STAGES = 2;
-constexpr int B_STAGE_BYTES = 4 * TILE16;
+constexpr int B_D_BYTES = TB * 4;                    // D of the stage's query block (bulk copy)
+constexpr int B_STAGE_TX = 4 * TILE16 + B_D_BYTES;   // bytes landing per stage
+constexpr int B_STAGE_BYTES = 4 * TILE16 + 1024;     // (1024-aligned stages)
 constexpr int B_V = 0, B_ST = 2 * TILE16, B_DA = B_ST + B_STAGES * B_STAGE_BYTES, B_BAR = B_DA + 2 * TILE16;
 constexpr int B_SMEM = B_BAR + 256 + 1024;
 
@@ -372,7 +417,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         const uint32_t st = smem_u32(smem + B_ST + stage * B_STAGE_BYTES);
         const uint32_t fb = smem_u32(&full[stage]);
-        mbar_expect_tx_w(fb, B_STAGE_BYTES);
+        mbar_expect_tx_w(fb, B_STAGE_TX);
+        bulk_load_w(st + 4 * TILE16, P.D + ((int64_t)(b * P.H + h) * P.S + qb * TB), B_D_BYTES, fb);
         tma_load_4d_w(st, &mdO, fb, 0, qb * TB, h, b);
         tma_load_4d_w(st + TILE16, &mQ, fb, 0, qb * TB, h, b);
         tma_load_4d_w(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b);       // keys kb*128 + 0..63
@@ -386,50 +432,66 @@ __global__ void __launch_bounds__(kAThreads, 1)
     pdl_trigger();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
+    // A flat stream of iterations g over this CTA's tasks (dP^T buffer g & 1, stage g % 2): the dP
+    // MMA of iteration g + 1 (also the next task's first) is issued before the dK MMA of iteration
+    // g, which waits for the epilogue's dA^T.
     const uint32_t id_dp = idesc_of(false, false, TB);  // dP^T = V dO^T: both K-major, N = 128
     const uint32_t id_dv = idesc_of(true, true, HD);    // dV += P^T dO: P MN-major, dO MN-major
     const uint32_t id_dk = idesc_of(false, true, HD);   // dK += dA^T Q: dA^T K-major, Q MN-major
-    int stage = 0;
-    uint32_t phase = 0;
-    int it = 0, tl = 0;
-    for (int64_t k = 0;; ++k, ++tl) {
-      const int64_t t = task_at(c0, G, k);
-      if (t >= P.num_tasks) break;
-      int kb, b, h;
-      decode(t, kb, b, h);
-      const int vs = tl & 1, as = tl & 1;
-      mbar_wait(smem_u32(&vfull[vs]), (tl >> 1) & 1);
-      mbar_wait(smem_u32(&aempty[as]), ((tl >> 1) & 1) ^ 1);
+    auto nq_of = [&](int kb) { return P.nblk - q_first(kb); };
+    auto issue_dp = [&](int64_t g, int tl, int i, int nq) {
+      const int tb = (int)(g & 1), stg = (int)(g % B_STAGES), vs = tl & 1;
+      if (i == 0) mbar_wait(smem_u32(&vfull[vs]), (tl >> 1) & 1);
+      mbar_wait(smem_u32(&tempty[tb]), (uint32_t)(((g >> 1) & 1) ^ 1));
+      mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / B_STAGES) & 1));
       tc_fence_after();
       const uint32_t sv = smem_u32(smem + B_V + vs * TILE16);
-      const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
-      const int q0 = q_first(kb), nq = P.nblk - q0;
-      auto stg_of = [&](int i) { return (stage + i) % B_STAGES; };
-      auto ph_of = [&](int i) { return (uint32_t)((phase + ((stage + i) / B_STAGES)) & 1); };
-      auto issue_dp = [&](int i) {
-        const int tb = (it + i) & 1;
-        mbar_wait(smem_u32(&tempty[tb]), (((it + i) >> 1) & 1) ^ 1);
-        mbar_wait(smem_u32(&full[stg_of(i)]), ph_of(i));
-        tc_fence_after();
-        const uint32_t sdo = smem_u32(smem + B_ST + stg_of(i) * B_STAGE_BYTES);
+      const uint32_t sdo = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
 #pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk)
-          mma_bf16_w(tmem + tb * TB, make_sdesc(sv + kk * 32, 16, 1024), make_sdesc(sdo + kk * 32, 16, 1024), id_dp,
-                     kk > 0 ? 1u : 0u);
-        mma_commit_w(smem_u32(&tfull[tb]));
-      };
-      issue_dp(0);
-      for (int i = 0; i < nq; ++i) {
-        const uint32_t st = smem_u32(smem + B_ST + stg_of(i) * B_STAGE_BYTES);
+      for (int kk = 0; kk < HD / 16; ++kk)
+        mma_bf16_w(tmem + tb * TB, make_sdesc(sv + kk * 32, 16, 1024), make_sdesc(sdo + kk * 32, 16, 1024), id_dp,
+                   kk > 0 ? 1u : 0u);
+      mma_commit_w(smem_u32(&tfull[tb]));
+      if (i == nq - 1) mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
+    };
+    int64_t k = 0;
+    const int64_t t0 = task_at(c0, G, 0);
+    if (t0 < P.num_tasks) {
+      int kb, b, h;
+      decode(t0, kb, b, h);
+      int tl = 0, i = 0, nq = nq_of(kb);
+      int64_t g = 0;
+      issue_dp(0, 0, 0, nq);
+      for (;;) {
+        const int as = tl & 1, stg = (int)(g % B_STAGES);
+        const uint32_t st = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
+        const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
+        if (i == 0) {
+          mbar_wait(smem_u32(&aempty[as]), ((tl >> 1) & 1) ^ 1);
+          tc_fence_after();
+        }
         // dV += P^T dO (both operands already in the stage): K = 128 queries
 #pragma unroll
         for (int kk = 0; kk < TB / 16; ++kk)
           mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
                      id_dv, (i > 0 || kk > 0) ? 1u : 0u);
-        if (i + 1 < nq) issue_dp(i + 1);
-        else mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
-        // dK += dA^T Q once the epilogue has staged dA^T of iteration i
-        mbar_wait(smem_u32(dafull), (it + i) & 1);
+        // the next iteration: (tl, i + 1) or the first of the next task
+        int tl2 = tl, i2 = i + 1, nq2 = nq;
+        bool more = true;
+        if (i2 == nq) {
+          const int64_t t2 = task_at(c0, G, k + 1);
+          more = t2 < P.num_tasks;
+          if (more) {
+            int kb2, b2, h2;
+            decode(t2, kb2, b2, h2);
+            tl2 = tl + 1;
+            i2 = 0;
+            nq2 = nq_of(kb2);
+          }
+        }
+        if (more) issue_dp(g + 1, tl2, i2, nq2);
+        // dK += dA^T Q once the epilogue has staged dA^T of iteration g
+        mbar_wait(smem_u32(dafull), (uint32_t)(g & 1));
         tc_fence_after();
         const uint32_t sda = smem_u32(smem + B_DA);
 #pragma unroll
@@ -437,12 +499,15 @@ __global__ void __launch_bounds__(kAThreads, 1)
           mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
                      make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(smem_u32(daempty));
-        mma_commit_w(smem_u32(&empty[stg_of(i)]));
+        mma_commit_w(smem_u32(&empty[stg]));
+        if (i == nq - 1) mma_commit_w(smem_u32(&afull[as]));
+        if (!more) break;
+        if (tl2 != tl) ++k;
+        tl = tl2;
+        i = i2;
+        nq = nq2;
+        ++g;
       }
-      mma_commit_w(smem_u32(&afull[as]));
-      phase ^= (uint32_t)(((stage + nq) / B_STAGES) & 1);
-      stage = (stage + nq) % B_STAGES;
-      it += nq;
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..9
@@ -458,7 +523,6 @@ __global__ void __launch_bounds__(kAThreads, 1)
       if (t >= P.num_tasks) break;
       int kb, b, h;
       decode(t, kb, b, h);
-      const float* Dbh = P.D + (int64_t)(b * P.H + h) * P.S;
       for (int qb = q_first(kb); qb < P.nblk; ++qb, ++it) {
         const int tb = it & 1;
         mbar_wait(smem_u32(&tfull[tb]), (it >> 1) & 1);
@@ -470,10 +534,10 @@ __global__ void __launch_bounds__(kAThreads, 1)
         if (lane == 0) mbar_arrive(smem_u32(&tempty[tb]));
         mbar_wait(smem_u32(&full[stage]), phase);  // the P tile of this stage has landed
         const uint8_t* ptile = smem + B_ST + stage * B_STAGE_BYTES + 2 * TILE16 + pbox;
-        const float* Dq = Dbh + qb * TB + half * 64;
+        const float* Dq = reinterpret_cast<const float*>(smem + B_ST + stage * B_STAGE_BYTES + 4 * TILE16) + half * 64;
 #pragma unroll
         for (int j = 0; j < 64; j += 4) {
-          const float4 d = __ldg(reinterpret_cast<const float4*>(Dq + j));
+          const float4 d = *reinterpret_cast<const float4*>(Dq + j);  // (broadcast)
           const float dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {

@@ -79,7 +79,11 @@ struct Cfg {
   static constexpr int BUFS = CTAS == 2 ? 1 : kStageBufs;  // staging buffers per epilogue warp
   static constexpr int SMEM_LIMIT = CTAS == 2 ? 113 * 1024 : kMaxSmem;
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = (BN / CG) * BK * 2;
+  static constexpr int B_ROWS = BN / CG;             // B rows (N) this CTA stages
+  static constexpr int B_BLKS = (B_ROWS + 63) / 64;  // MN-major B: whole 64-element blocks (a
+  // 96-row pair half loads two; the MMA reads the first 96 columns)
+  static constexpr int B_BYTES_K = B_ROWS * BK * 2;  // K-major B bytes per stage
+  static constexpr int B_BYTES = B_BLKS * 64 * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // ROWSTATS: no C staging, only the half-merge exchange slots (2 x BM float2)
   static constexpr int EPI_BYTES = EPI == EPI_ROWSTATS ? 2 * BM * 8 : kEpiWarps * BUFS * kStageBytesPerWarp;
@@ -458,7 +462,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     gemm_tc_kernel(const __grid_constant__ TcParams P, const __grid_constant__ CUtensorMap tmA,
                    const __grid_constant__ CUtensorMap tmB, const __grid_constant__ CUtensorMap tmC,
                    const __grid_constant__ CUtensorMap tmAux) {
-  static_assert(CG == 1 || (CG == 2 && generic_epi(EPI) && (BN / 2) % 64 == 0), "CTA-pair configuration");
+  static_assert(CG == 1 || (CG == 2 && generic_epi(EPI) && (BN / 2) % 32 == 0), "CTA-pair configuration");
   using C = Cfg<BN, CG, EPI>;
   static_assert(EPI != EPI_DA || C::BUFS == 2, "EPI_DA double-buffers P");
   constexpr int W = 128 / (int)sizeof(TC);  // columns per 128-byte staging row
@@ -539,9 +543,10 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
           const uint32_t sb = sa + C::A_BYTES;
           const int k0 = (int)(kb * BK);
+          const uint32_t stage_tx = C::A_BYTES + (P.b_kmajor ? C::B_BYTES_K : C::B_BYTES);
           if constexpr (CG == 2) {
             const uint32_t fb_local = smem_u32(&full[stage]);
-            if (rank == 0) mbar_expect_tx_w(fb_local, CG * C::STAGE_BYTES);
+            if (rank == 0) mbar_expect_tx_w(fb_local, CG * stage_tx);
             const uint32_t fb = map_to_rank(fb_local, 0);
             if (P.a_kmajor) {
               tma_load_4d_pair_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
@@ -554,11 +559,11 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
               tma_load_4d_pair_w(sb, &tmB, fb, k0, nb0, q, p);
             } else {
 #pragma unroll
-              for (int j = 0; j < BN / CG / 64; ++j) tma_load_4d_pair_w(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
+              for (int j = 0; j < C::B_BLKS; ++j) tma_load_4d_pair_w(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
             }
           } else {
             const uint32_t fb = smem_u32(&full[stage]);
-            mbar_expect_tx_w(fb, C::STAGE_BYTES);
+            mbar_expect_tx_w(fb, stage_tx);
             if (P.a_kmajor) {
               tma_load_4d_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
             } else {
@@ -1574,10 +1579,13 @@ bool use_pair(const GemmArgs& a) {
 
 // Pair widths whose half is a whole 64-column MN-major block.
 int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
-  const int cands[2] = {256, 128};
+  // 192: N = 1600 (GPT-2 XL) tiles as 9 x 192 (8 % over) instead of 7 x 256 (12 % over and a
+  // nearly empty last round of the persistent schedule)
+  const int cands[3] = {256, 192, 128};
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
+    if (bn == 192 && forced_cg() != 2 && getenv("NNT_GEMM_NO192")) continue;
     const double cost = tile_cost(a, bn, 2, pair_units(), es_c);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
@@ -1641,9 +1649,11 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     if constexpr (sizeof(TC) == 4) {
       if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 2>(a, s, splits);
     }
-    if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single)  // ties go to pairs
-      return bnp == 256 || splits > 1 ? launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits)
-                                      : launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+    if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single) {  // ties go to pairs
+      if (bnp == 256 || splits > 1) return launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits);
+      if (bnp == 192) return launch_bn<192, TC, EPI_GENERIC, 2>(a, s, splits);
+      return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+    }
   }
   if constexpr (sizeof(TC) == 4) {
     if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 1>(a, s, splits);

@@ -148,6 +148,11 @@ def test_tp_stack_nccl_world1_two_adam_steps():
             want = dense.probe_loss(y, r, B * S)
             _, g = dense.stack_bwd(P, caches, dense.probe_loss_grad(r, B * S))
             assert abs(loss - want) <= 1e-4 * abs(want), t
+            torch.cuda.synchronize()
+            for l in range(L):  # this step's gradients (taken at the GPU's parameters) vs the oracle's
+                for n, gv in st.grads_of(l).items():
+                    if n != "b_qkv":
+                        close(host(gv), g[l][n], 1e-4, (t, l, n))
             for l in range(L):
                 for n in P[l]:
                     P[l][n], m1, v1 = dense.adam_step(P[l][n], g[l][n], *mv[l][n], t, lr=1e-2)
