@@ -1579,13 +1579,13 @@ bool use_pair(const GemmArgs& a) {
 
 // Pair widths whose half is a whole 64-column MN-major block.
 int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
-  // 192: N = 1600 (GPT-2 XL) tiles as 9 x 192 (8 % over) instead of 7 x 256 (12 % over and a
-  // nearly empty last round of the persistent schedule)
-  const int cands[3] = {256, 192, 128};
+  // (192-wide pair tiles -- N = 1600 as 9 x 192 instead of 7 x 256 with a nearly empty last round
+  // -- ran 2-4 % slower on every GPT-2 XL shape: these GEMMs are bound by the L2 -> SM operand
+  // stream, which narrower tiles increase per FLOP; DESIGN §7.1.  NNT_GEMM_192=1 re-enables them.)
+  const int cands[3] = {256, 128, getenv("NNT_GEMM_192") ? 192 : 128};
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
-    if (bn == 192 && forced_cg() != 2 && getenv("NNT_GEMM_NO192")) continue;
     const double cost = tile_cost(a, bn, 2, pair_units(), es_c);
     if (cost < best_cost * 0.999) {
       best_cost = cost;

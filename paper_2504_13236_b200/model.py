@@ -169,6 +169,9 @@ class StackConfig:
     # optimizer state (Adam m, v / SGD momentum) in pinned host memory, streamed through device
     # staging slots by the copy engines around each update (offload.py)
     offload: bool = False
+    # saved activations of the lowest `act_offload` layers in pinned host memory, moved by the copy
+    # engines out after each forward and back before each backward (offload.HostActivations)
+    act_offload: int = 0
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
 
@@ -229,7 +232,10 @@ class BlockStack:
             self._params.append(self._make_params(l))
             self._grads.append(self._make_grads(l))
         saved_b, scratch_b = nnt.nnt_block_workspace_size(self.bcfg)
-        self.saved = [torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for _ in range(cfg.L)]
+        self.n_off = max(0, min(cfg.act_offload, cfg.L))
+        self.act_host = offload.HostActivations(self.n_off, saved_b, self.dev) if self.n_off else None
+        self.saved = [self.act_host.slot(l) if l < self.n_off else
+                      torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for l in range(cfg.L)]
         self.scratch = torch.zeros(scratch_b, device=self.dev, dtype=torch.uint8)  # zero: split-K counters
         act = dict(device=self.dev, dtype=torch.float32)
         self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
@@ -245,6 +251,8 @@ class BlockStack:
         # every stream of this model distinct (torch's round-robin stream pool recycles streams);
         # cap_stream: graphs are captured on it (torch.cuda.graph would take one from the pool)
         used = [] if self.host_state is None else [self.host_state.h2d, self.host_state.d2h]
+        if self.act_host is not None:
+            used += [self.act_host.h2d, self.act_host.d2h]
         self.comm = _distinct_stream(self.dev, used) if self.dp else None
         self.side = _distinct_stream(self.dev, used + [self.comm]) if cfg.side_stream else None
         self.cap_stream = _distinct_stream(self.dev, used + [self.comm, self.side])
@@ -288,8 +296,14 @@ class BlockStack:
     def forward(self, x=None):
         if x is not None:
             self.xs[0].copy_(x)
+        ah = self.act_host
+        compute = torch.cuda.current_stream()
         for l in range(self.cfg.L):
+            if ah is not None and l < self.n_off:
+                ah.before_fwd(l, compute)
             nnt.nnt_block_fwd(self.bcfg, self._params[l], self.xs[l], self.xs[l + 1], self.saved[l], self.scratch)
+            if ah is not None and l < self.n_off:
+                ah.after_fwd(l, compute)
         return self.xs[-1]
 
     def probe_loss(self, r):
@@ -308,7 +322,10 @@ class BlockStack:
         cur = 0
         compute = torch.cuda.current_stream()
         dp = self.dp
+        ah = self.act_host
         for l in range(self.cfg.L - 1, -1, -1):
+            if ah is not None and l < self.n_off:
+                ah.before_bwd(l, compute)
             ev = self.events[l] if dp else None
             links = None
             if self.chain:
@@ -322,10 +339,15 @@ class BlockStack:
             nnt.nnt_block_bwd_streams(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch,
                                       self.dy[cur], self.dy[1 - cur], self._grads[l], 0, ev,
                                       side_stream=self.side, links=links)
+            if ah is not None and l < self.n_off:
+                ah.after_bwd(l, compute)
+                ah.prefetch(l - 2, after_bwd_of=l)  # slot l % 2 is free: bring back layer l - 2
             if dp:
                 for si in range(4):
                     self._reduce_bucket(l, si, ev[si], overlap_optimizer)
             cur = 1 - cur
+        if ah is not None:
+            ah.join(compute)
         if dp:
             compute.wait_stream(self.comm)
         return self.dy[cur]

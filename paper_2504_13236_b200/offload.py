@@ -69,3 +69,70 @@ class HostOptimizerState:
         stream.wait_stream(self.d2h)
         stream.wait_stream(self.h2d)
         self.bytes_moved = moved
+
+
+class HostActivations:
+    """The saved-activation workspaces of the first `n_layers` blocks in pinned host memory
+    (tiles that do not fit the GPU live in host RAM).
+
+    Such a layer's forward writes its `saved` workspace (LayerNorm statistics, h1, qkv, P, O, x1,
+    h2, u, g: the tensors its backward reads) into one of two device slots; the copy engine then
+    moves it to host RAM (device-to-host stream) while the next layers compute.  The backward
+    brings it back (host-to-device stream) into the same slot, issued as soon as the slot's
+    previous user (the layer two above) is done, so the transfer overlaps the backward of the
+    layer in between.  The two highest offloaded layers skip the round trip: their slots still
+    hold their data when the backward reaches them.  Every byte moves by cudaMemcpyAsync; the blocks'
+    arithmetic is unchanged, so results are bitwise those of the resident path."""
+
+    def __init__(self, n_layers, saved_bytes, device):
+        self.n, self.dev = n_layers, torch.device(device)
+        self.host = [torch.empty(saved_bytes, dtype=torch.uint8).pin_memory() for _ in range(n_layers)]
+        self.slots = [torch.empty(saved_bytes, device=self.dev, dtype=torch.uint8) for _ in range(min(2, n_layers))]
+        self.h2d = torch.cuda.Stream(device=self.dev)
+        self.d2h = torch.cuda.Stream(device=self.dev)
+        self.ev_fwd = [torch.cuda.Event() for _ in range(n_layers)]      # layer's forward done
+        self.ev_bwd = [torch.cuda.Event() for _ in range(n_layers)]      # layer's backward done
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]             # slot's D2H copy done
+        self.ev_in = [torch.cuda.Event() for _ in range(n_layers)]       # layer's H2D copy done
+        self.bytes_per_layer = saved_bytes
+
+    def slot(self, l):
+        return self.slots[l % 2]
+
+    # ---------------------------------------------------------------- forward
+    def before_fwd(self, l, stream):
+        """The compute stream may overwrite slot l % 2 once its previous layer's copy-out is done."""
+        if l >= 2:
+            stream.wait_event(self.ev_out[l % 2])
+
+    def after_fwd(self, l, stream):
+        """Copy layer l's saved workspace to host RAM (overlaps the next layers' forward)."""
+        self.ev_fwd[l].record(stream)
+        self.d2h.wait_event(self.ev_fwd[l])
+        with torch.cuda.stream(self.d2h):
+            self.host[l].copy_(self.slot(l), non_blocking=True)
+            self.ev_out[l % 2].record(self.d2h)
+
+    # ---------------------------------------------------------------- backward
+    def prefetch(self, l, after_bwd_of=None):
+        """Bring layer l's saved workspace back into slot l % 2 once the slot's current user (the
+        backward of layer `after_bwd_of`, or the copy-out of the forward) is done."""
+        if l < 0 or l >= self.n - 2:
+            return  # the top two offloaded layers' slots still hold their data
+        if after_bwd_of is not None:
+            self.h2d.wait_event(self.ev_bwd[after_bwd_of])
+        self.h2d.wait_event(self.ev_out[l % 2])
+        with torch.cuda.stream(self.h2d):
+            self.slot(l).copy_(self.host[l], non_blocking=True)
+            self.ev_in[l].record(self.h2d)
+
+    def before_bwd(self, l, stream):
+        if l < self.n - 2:
+            stream.wait_event(self.ev_in[l])
+
+    def after_bwd(self, l, stream):
+        self.ev_bwd[l].record(stream)
+
+    def join(self, stream):
+        stream.wait_stream(self.h2d)
+        stream.wait_stream(self.d2h)

@@ -32,7 +32,7 @@ def _stack(cfg_name, L=1, B=None, S=None, dtype=None, tile=None, init="parity", 
     return sc, layers, model.BlockStack(sc, layers)
 
 
-def _update_close(got_delta, want_delta, g_ref, w_ref, rms_g, tol, what=""):
+def _update_close(got_delta, want_delta, g_ref, w_ref, rms_g, tol, what="", elementwise=True):
     """close_update on an Adam update, skipping elements whose exact gradient is zero.
 
     The key-bias gradient is exactly zero in exact arithmetic (softmax is invariant to a
@@ -40,7 +40,7 @@ def _update_close(got_delta, want_delta, g_ref, w_ref, rms_g, tol, what=""):
     g/(|g|+eps) turns fp32 noise there into O(lr) updates in either implementation."""
     keep = np.abs(g_ref) > 1e-9 * max(np.abs(g_ref).max(), 1e-300)
     return close_update(np.asarray(got_delta)[keep], np.asarray(want_delta)[keep], np.asarray(w_ref)[keep],
-                        np.asarray(rms_g)[keep], tol, what)
+                        np.asarray(rms_g)[keep], tol, what, elementwise)
 
 
 def _oracle_step(layers, x, r, H, T):
@@ -96,7 +96,8 @@ def test_tiny_fp32_three_training_steps():
             P[0][k], m[k], v_[k] = dense.adam_step(P[0][k], g[0][k], m[k], v_[k], t)
     w_init = layers[0]
     for n, wv in st.params_of(0).items():
-        _update_close(host(wv) - w_init[n], P[0][n] - w_init[n], m[n], P[0][n], np.sqrt(v_[n]), 1e-4, n)
+        _update_close(host(wv) - w_init[n], P[0][n] - w_init[n], m[n], P[0][n], np.sqrt(v_[n]), 1e-4, n,
+                      elementwise=False)
 
 
 # S = 192: not a multiple of 128 -> the unfused attention GEMM sequence (nnt_attention_fused_supported)

@@ -141,7 +141,7 @@ def test_dp_stack_multirank_vs_full_batch_oracle(world, zero):
             w1, rms = P[l][k].ravel(), np.sqrt(v_[l][k]).ravel()
             if k == "b_qkv":  # key-bias gradient is exactly zero (R22): Adam amplifies its fp32 noise
                 got, want, w1, rms = (np.delete(a, np.s_[E:2 * E]) for a in (got, want, w1, rms))
-            close_update(got, want, w1, rms, 1e-4, f"R{world} L{l} {k}")
+            close_update(got, want, w1, rms, 1e-4, f"R{world} L{l} {k}", elementwise=False)
 
 
 def _gpt2_worker(rank, world, port, nb, q):

@@ -165,11 +165,11 @@ def test_gpt2_multistep_gradients_vs_oracle(cfg, graph):
     if not bf16:  # the trajectory: parameter change over 3 steps vs the oracle's, key bias excluded (R22)
         for k, v in gm.params().items():
             close_update(host(v) - shell[k], traj[k] - shell[k], traj[k], np.sqrt(mom["shell"][k][1]), 1e-4,
-                         f"traj {k}")
+                         f"traj {k}", elementwise=False)
         for l in range(L):
             for k, v in gm.stack.params_of(l).items():
                 got, want = host(v) - layers[l][k], traj["blocks"][l][k] - layers[l][k]
                 w1, rms = traj["blocks"][l][k], np.sqrt(mom["blocks"][l][k][1])
                 if k == "b_qkv":
                     got, want, w1, rms = (np.delete(a, np.s_[E:2 * E]) for a in (got, want, w1, rms))
-                close_update(got, want, w1, rms, 1e-4, f"traj L{l} {k}")
+                close_update(got, want, w1, rms, 1e-4, f"traj L{l} {k}", elementwise=False)
