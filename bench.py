@@ -294,7 +294,8 @@ def run_nnt(args):
     dtype = "f32" if args.config == "tiny" else "bf16"
     tile = 16 if args.config == "tiny" else 1024
     sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile, dtype=dtype,
-                           optimizer=args.optimizer, zero=args.zero, offload=args.offload)
+                           optimizer=args.optimizer, zero=args.zero, offload=args.offload,
+                           act_offload=args.act_offload)
     layers = [nnt_inputs.make_params(E, seed=1234, layer=l, init="gpt2", n_layers=L) for l in range(L)]
     b0, b1 = nnt.nnt_partition(B * world, world, rank)  # rank r's batch tiles of the global batch
     batches = []
@@ -488,6 +489,7 @@ def run_nnt(args):
                       "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}" + ("-zero1" if args.zero and world > 1 else ""),
                       "optimizer": args.optimizer + (" (state offloaded to pinned host memory)" if args.offload
                                                      else ""),
+                      "activation_offload_layers": args.act_offload,
                       "launch": "one CUDA graph per step" if use_graph else "eager launches",
                       "l2": "per-step working set (GBs of activations) >> 126 MB L2; no explicit flush"},
            "model_tflops": model_tflops, "model_tflops_frac_of_bf16": model_tflops / peaks["bf16"],
@@ -535,6 +537,8 @@ def main():
                     "owned-slice update, all-gather) instead of all-reduce + replicated update")
     ap.add_argument("--offload", action="store_true", help="optimizer state in pinned host memory, streamed "
                     "through device staging slots around each update (SURVEY f4)")
+    ap.add_argument("--act-offload", type=int, default=0, help="saved activations of the lowest K layers in "
+                    "pinned host memory, copied out after their forward and back before their backward (SURVEY f4)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3:

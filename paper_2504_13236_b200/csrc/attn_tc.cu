@@ -20,8 +20,9 @@
 //       (the unfused path read P three times and dA twice).
 //
 // Warp roles as in the GEMM (gemm_tc.cu): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2..9 epilogue (TMEM lane quadrant = warp % 4; the two warps of a quadrant take
-// the two 64-column halves of a 128 x 128 tile).  Persistent CTAs, static heaviest-first task
+// issuer, warps 2..17 epilogue (TMEM lane quadrant = warp % 4; the four warps of a quadrant take
+// the four 32-column groups of a 128 x 128 tile: the epilogues are latency- and MUFU-bound, so
+// they get more warps than the GEMM's).  Persistent CTAs, static heaviest-first task
 // order with a boustrophedon assignment.  Head size h = 64 and S % 128 == 0 (the configurations
 // of BASELINE.json); the block falls back to the unfused GEMM sequence otherwise.
 #include <cuda.h>
@@ -32,7 +33,8 @@
 namespace nnt {
 namespace {
 
-constexpr int kAThreads = 64 + 32 * 8;
+constexpr int kEW = 16;                      // epilogue warps: 4 per TMEM lane quadrant
+constexpr int kAThreads = 64 + 32 * kEW;
 constexpr int TB = 128;     // query / key block
 constexpr int HD = 64;      // head size
 constexpr int TILE16 = 16384;  // one 128-row x 128-byte SW128 tile (64 bf16 per row)
@@ -62,6 +64,29 @@ __device__ __forceinline__ void bulk_load_w(uint32_t dst, const void* src, uint3
                "@e cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n\t}" ::"r"(dst),
                "l"(src), "r"(bytes), "r"(bar)
                : "memory");
+}
+
+// 32 values (bf16) -> one half (16-byte chunks 4 sub .. 4 sub + 3) of this lane's 128-byte row of
+// an SW128 staging piece; the other half is written by the partner warp
+__device__ __forceinline__ void stage_half_row(uint8_t* piece, int lane, int sub, const float (&v)[32]) {
+  uint8_t* rowp = piece + lane * 128;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    uint4 u;
+    __nv_bfloat162 t0 = __floats2bfloat162_rn(v[8 * j], v[8 * j + 1]);
+    __nv_bfloat162 t1 = __floats2bfloat162_rn(v[8 * j + 2], v[8 * j + 3]);
+    __nv_bfloat162 t2 = __floats2bfloat162_rn(v[8 * j + 4], v[8 * j + 5]);
+    __nv_bfloat162 t3 = __floats2bfloat162_rn(v[8 * j + 6], v[8 * j + 7]);
+    u.x = *reinterpret_cast<uint32_t*>(&t0);
+    u.y = *reinterpret_cast<uint32_t*>(&t1);
+    u.z = *reinterpret_cast<uint32_t*>(&t2);
+    u.w = *reinterpret_cast<uint32_t*>(&t3);
+    *reinterpret_cast<uint4*>(rowp + (((sub * 4 + j) ^ (lane & 7)) << 4)) = u;
+  }
+}
+// the two warps of a (quadrant, 64-column chunk) pair: named barrier 1 + pair (64 threads)
+__device__ __forceinline__ void pair_sync(int pair) {
+  asm volatile("bar.sync %0, 64;" ::"r"(1 + pair) : "memory");
 }
 
 __device__ __forceinline__ int64_t task_at(int64_t c, int64_t G, int64_t k) {
@@ -95,11 +120,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint64_t* qfull = bars + 6;             // [2] Q of a task landed
   uint64_t* qempty = bars + 8;            // [2] the task's last S MMA done
   uint64_t* sfull = bars + 10;            // [2] S accumulator ready
-  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (8 warps)
-  uint64_t* pfull = bars + 14;            // [2] P staging written (8 warps)
+  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (16 warps)
+  uint64_t* pfull = bars + 14;            // [2] P staging written (16 warps)
   uint64_t* pempty = bars + 16;           // [2] P staging consumed by MMA O
   uint64_t* ofull = bars + 18;            // [2] O accumulator of a task complete
-  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (4 warps)
+  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
@@ -112,11 +137,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_init(smem_u32(&qfull[i]), 1);
       mbar_init(smem_u32(&qempty[i]), 1);
       mbar_init(smem_u32(&sfull[i]), 1);
-      mbar_init(smem_u32(&sempty[i]), 8);
-      mbar_init(smem_u32(&pfull[i]), 8);
+      mbar_init(smem_u32(&sempty[i]), kEW);
+      mbar_init(smem_u32(&pfull[i]), kEW);
       mbar_init(smem_u32(&pempty[i]), 1);
       mbar_init(smem_u32(&ofull[i]), 1);
-      mbar_init(smem_u32(&oempty[i]), 4);
+      mbar_init(smem_u32(&oempty[i]), kEW / 2);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -235,8 +260,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..9
-    const int quad = warp & 3, half = (warp - 2) >> 2;
+    // ------------------------------------------------ epilogue warps 2..17
+    // warp: TMEM lane quadrant quad (rows), 32-column group cg of the 128-wide tile; the pair of
+    // warps sharing a 64-column chunk h = cg / 2 writes the two halves (sub) of its staging rows
+    // and the first of them (sub == 0) issues the chunk's TMA store
+    const int quad = warp & 3, cg = (warp - 2) >> 2, hc = cg >> 1, sub = cg & 1, pair = quad * 2 + hc;
+    const bool leader = sub == 0;
     const float L2E = 1.4426950408889634f;
     const float sc = P.scale * L2E;
     int it = 0, tl = 0;
@@ -263,64 +292,64 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const int sb = it & 1;
         mbar_wait(smem_u32(&sfull[sb]), (it >> 1) & 1);
         tc_fence_after();
-        float v[64];
-        tmem_ld_cols<2>(tmem + sb * TB + half * 64 + ((uint32_t)(quad * 32) << 16), v);
+        float v[32];
+        tmem_ld32(tmem + sb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&sempty[sb]));
-        const int key0 = i * TB + half * 64;
-        int lim = 64;  // causal: keys <= q
-        if (P.causal && key0 + 63 > q) lim = q - key0 + 1;
-        if (lim >= 64) {
+        const int key0 = i * TB + cg * 32;
+        int lim = 32;  // causal: keys <= q
+        if (P.causal && key0 + 31 > q) lim = q - key0 + 1;
+        if (lim >= 32) {
 #pragma unroll
-          for (int j = 0; j < 64; j += 2) {
+          for (int j = 0; j < 32; j += 2) {
             const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc, sc), make_float2(-ml, -ml));
             const float2 y = __fmul2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(inv, inv));
             v[j] = y.x;
             v[j + 1] = y.y;
           }
-        } else {  // diagonal tile: keys > q masked (-> 0); no exponentials for whole masked halves
-          if (lim > 0) {
+        } else if (lim > 0) {  // diagonal tile: keys > q masked (-> 0)
 #pragma unroll
-            for (int j = 0; j < 64; ++j) v[j] = ex2_approx(j < lim ? fmaf(v[j], sc, -ml) : -INFINITY) * inv;
-          } else {
+          for (int j = 0; j < 32; ++j) v[j] = ex2_approx(j < lim ? fmaf(v[j], sc, -ml) : -INFINITY) * inv;
+        } else {
 #pragma unroll
-            for (int j = 0; j < 64; ++j) v[j] = 0.f;
-          }
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
-        // P piece -> staging buffer pb (after MMA O of iteration it-2 and this warp's store of it)
+        // P -> staging buffer pb (after MMA O of iteration it-2 and the pair's store from it)
         const int pb = it & 1;
         mbar_wait(smem_u32(&pempty[pb]), ((it >> 1) & 1) ^ 1);
-        uint8_t* piece = smem + F_P + pb * 2 * TILE16 + half * TILE16 + quad * PIECE;
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
-        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        uint8_t* piece = smem + F_P + pb * 2 * TILE16 + hc * TILE16 + quad * PIECE;
+        if (leader && lane == 0) bulk_wait_read0();
+        pair_sync(pair);
+        stage_half_row(piece, lane, sub, v);
         fence_async_smem();
-        __syncwarp();
+        pair_sync(pair);
         if (lane == 0) {
           mbar_arrive(smem_u32(&pfull[pb]));
-          tma_store_4d(&mPst, smem_u32(piece), key0, qb * TB + quad * 32, h, b);
-          bulk_commit();
+          if (leader) {
+            tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
+            bulk_commit();
+          }
         }
       }
-      // O = P V of the task (4 warps: half 0) -> bf16 -> TMA store
-      if (half == 0) {
+      // O = P V of the task (8 warps: chunk 0) -> bf16 -> TMA store
+      if (hc == 0) {
         const int os = tl & 1;
         mbar_wait(smem_u32(&ofull[os]), (tl >> 1) & 1);
         tc_fence_after();
-        float v[64];
-        tmem_ld_cols<2>(tmem + 256 + os * HD + ((uint32_t)(quad * 32) << 16), v);
+        float v[32];
+        tmem_ld32(tmem + 256 + os * HD + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
-        // staging: this warp's piece of the P buffer that MMA O has finished with (ofull covers it)
+        // staging: the pair's piece of the P buffer MMA O has finished with (ofull covers it)
         uint8_t* piece = smem + F_P + ((it - 1) & 1) * 2 * TILE16 + quad * PIECE;
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
-        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        if (leader && lane == 0) bulk_wait_read0();
+        pair_sync(pair);
+        stage_half_row(piece, lane, sub, v);
         fence_async_smem();
-        __syncwarp();
-        if (lane == 0) {
+        pair_sync(pair);
+        if (leader && lane == 0) {
           tma_store_4d(&mO, smem_u32(piece), 0, qb * TB + quad * 32, h, b);
           bulk_commit();
         }
@@ -356,30 +385,30 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
   uint64_t* full = bars;          // [2] stage dO, Q, P landed
-  uint64_t* empty = bars + 2;     // [2] stage consumed: MMA commit + 8 epilogue warps (P reads)
+  uint64_t* empty = bars + 2;     // [2] stage consumed: MMA commit + 16 epilogue warps (P reads)
   uint64_t* vfull = bars + 4;     // [2]
   uint64_t* vempty = bars + 6;    // [2] the task's last dP MMA done
   uint64_t* tfull = bars + 8;     // [2] dP^T accumulator ready
-  uint64_t* tempty = bars + 10;   // [2] drained (8 warps)
-  uint64_t* dafull = bars + 12;   // dA^T staging written (8 warps)
+  uint64_t* tempty = bars + 10;   // [2] drained (16 warps)
+  uint64_t* dafull = bars + 12;   // dA^T staging written (16 warps)
   uint64_t* daempty = bars + 13;  // dA^T staging consumed by MMA dK
   uint64_t* afull = bars + 14;    // [2] dV, dK of a task complete
-  uint64_t* aempty = bars + 16;   // [2] drained (8 warps)
+  uint64_t* aempty = bars + 16;   // [2] drained (16 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
-      mbar_init(smem_u32(&empty[i]), 1 + 8);
+      mbar_init(smem_u32(&empty[i]), 1 + kEW);
       mbar_init(smem_u32(&vfull[i]), 1);
       mbar_init(smem_u32(&vempty[i]), 1);
       mbar_init(smem_u32(&tfull[i]), 1);
-      mbar_init(smem_u32(&tempty[i]), 8);
+      mbar_init(smem_u32(&tempty[i]), kEW);
       mbar_init(smem_u32(&afull[i]), 1);
-      mbar_init(smem_u32(&aempty[i]), 8);
+      mbar_init(smem_u32(&aempty[i]), kEW);
     }
-    mbar_init(smem_u32(dafull), 8);
+    mbar_init(smem_u32(dafull), kEW);
     mbar_init(smem_u32(daempty), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -510,8 +539,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..9
-    const int quad = warp & 3, half = (warp - 2) >> 2;
+    // ------------------------------------------------ epilogue warps 2..17
+    // warp: TMEM lane quadrant quad (keys), 32-query group cg of the tile; the pair sharing the
+    // 64-query chunk hc = cg / 2 writes the two halves of its dA^T staging rows, the first of the
+    // pair (sub == 0) issues the TMA store
+    const int quad = warp & 3, cg = (warp - 2) >> 2, hc = cg >> 1, sub = cg & 1, pair = quad * 2 + hc;
+    const bool leader = sub == 0;
     int stage = 0;
     uint32_t phase = 0;
     int it = 0, tl = 0;
@@ -527,63 +560,65 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const int tb = it & 1;
         mbar_wait(smem_u32(&tfull[tb]), (it >> 1) & 1);
         tc_fence_after();
-        float v[64];  // dP^T[key = lane row][query = half * 64 + j]
-        tmem_ld_cols<2>(tmem + tb * TB + half * 64 + ((uint32_t)(quad * 32) << 16), v);
+        float v[32];  // dP^T[key = lane row][query = cg * 32 + j]
+        tmem_ld32(tmem + tb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(smem_u32(&tempty[tb]));
-        mbar_wait(smem_u32(&full[stage]), phase);  // the P tile of this stage has landed
+        mbar_wait(smem_u32(&full[stage]), phase);  // the P tile and D of this stage have landed
         const uint8_t* ptile = smem + B_ST + stage * B_STAGE_BYTES + 2 * TILE16 + pbox;
-        const float* Dq = reinterpret_cast<const float*>(smem + B_ST + stage * B_STAGE_BYTES + 4 * TILE16) + half * 64;
+        const float* Dq = reinterpret_cast<const float*>(smem + B_ST + stage * B_STAGE_BYTES + 4 * TILE16) + cg * 32;
 #pragma unroll
-        for (int j = 0; j < 64; j += 4) {
+        for (int j = 0; j < 32; j += 4) {
           const float4 d = *reinterpret_cast<const float4*>(Dq + j);  // (broadcast)
           const float dd[4] = {d.x, d.y, d.z, d.w};
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
-            const int r = half * 64 + j + u;  // query row of the P tile
+            const int r = cg * 32 + j + u;  // query row of the P tile
             const uint16_t pr = *reinterpret_cast<const uint16_t*>(ptile + r * 128 + ((pchunk ^ (r & 7)) << 4) + pel);
             const float p = __uint_as_float((uint32_t)pr << 16);
             v[j + u] = (p * P.scale) * (v[j + u] - dd[u]);  // dA = P (dP - D) / sqrt(h)  (R20)
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // this warp's P reads are done
-        // dA^T piece -> staging (after MMA dK of the previous iteration and this warp's store)
+        if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // this warp's P / D reads are done
+        // dA^T -> staging (after MMA dK of the previous iteration and the pair's store from it)
         mbar_wait(smem_u32(daempty), (it & 1) ^ 1);
-        uint8_t* piece = smem + B_DA + half * TILE16 + quad * PIECE;
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
-        stage_row<__nv_bfloat16, 64>(piece, lane, v);
+        uint8_t* piece = smem + B_DA + hc * TILE16 + quad * PIECE;
+        if (leader && lane == 0) bulk_wait_read0();
+        pair_sync(pair);
+        stage_half_row(piece, lane, sub, v);
         fence_async_smem();
-        __syncwarp();
+        pair_sync(pair);
         if (lane == 0) {
           mbar_arrive(smem_u32(dafull));
-          tma_store_4d(&mdAT, smem_u32(piece), qb * TB + half * 64, kb * TB + quad * 32, h, b);
-          bulk_commit();
+          if (leader) {
+            tma_store_4d(&mdAT, smem_u32(piece), qb * TB + hc * 64, kb * TB + quad * 32, h, b);
+            bulk_commit();
+          }
         }
         if (++stage == B_STAGES) {
           stage = 0;
           phase ^= 1;
         }
       }
-      // dK (half 0) / dV (half 1) of the key block -> bf16 -> TMA store
+      // dK (chunk 0 pairs) / dV (chunk 1 pairs) of the key block -> bf16 -> TMA store
       const int as = tl & 1;
       mbar_wait(smem_u32(&afull[as]), (tl >> 1) & 1);
       tc_fence_after();
-      float v[64];
-      tmem_ld_cols<2>(tmem + 256 + as * 128 + (half == 0 ? HD : 0) + ((uint32_t)(quad * 32) << 16), v);
+      float v[32];
+      tmem_ld32(tmem + 256 + as * 128 + (hc == 0 ? HD : 0) + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&aempty[as]));
-      uint8_t* piece = smem + B_DA + half * TILE16 + quad * PIECE;  // MMA dK finished with it (afull)
-      if (lane == 0) bulk_wait_read0();
-      __syncwarp();
-      stage_row<__nv_bfloat16, 64>(piece, lane, v);
+      uint8_t* piece = smem + B_DA + hc * TILE16 + quad * PIECE;  // MMA dK finished with it (afull)
+      if (leader && lane == 0) bulk_wait_read0();
+      pair_sync(pair);
+      stage_half_row(piece, lane, sub, v);
       fence_async_smem();
-      __syncwarp();
-      if (lane == 0) {
-        tma_store_4d(half == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
+      pair_sync(pair);
+      if (leader && lane == 0) {
+        tma_store_4d(hc == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
         bulk_commit();
       }
     }

@@ -110,3 +110,54 @@ def test_offload_dp_world1_bitwise():
     finally:
         if own:
             dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ saved activations in host RAM
+def _stack_act(n_off, graph, L_=4, steps=2):
+    sc = model.StackConfig(L=L_, E=E, H=H, S=S, B=B, dtype="bf16", act_offload=n_off)
+    layers = [nnt_inputs.make_params(E, seed=19, layer=l, init="gpt2", n_layers=L_) for l in range(L_)]
+    st = model.BlockStack(sc, layers)
+    if n_off:
+        assert all(t.device.type == "cpu" and t.is_pinned() for t in st.act_host.host)
+        assert len(st.act_host.slots) == min(2, n_off)
+    if graph:
+        st.enable_graph()
+    losses = []
+    for t in range(steps):
+        x = dev(nnt_inputs.make_x(E, S, 0, B, seed=90 + t))
+        r = dev(nnt_inputs.make_r(E, S, 0, B, seed=90 + t))
+        losses.append(st.train_step(x, r).item())
+    torch.cuda.synchronize()
+    return [losses, st.w.clone(), st.w16.clone(), st.m.clone(), st.v.clone()]
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("n_off", [1, 2, 3, 4])
+def test_activation_offload_stack_bitwise(n_off):
+    """StackConfig.act_offload (offload.HostActivations): the saved workspaces of
+    the lowest n_off of 4 layers go to pinned host RAM after their forward and come back before
+    their backward (n_off >= 3 exercises the prefetch into a reused slot).  Bitwise equal to the
+    resident run, eager and graph-captured."""
+    ref = _stack_act(0, False)
+    _same(_stack_act(n_off, False), ref)
+    _same(_stack_act(n_off, True), ref)
+
+
+@pytest.mark.timeout(300)
+def test_activation_offload_gpt2_bitwise():
+    def run(n_off, graph):
+        sc = model.StackConfig(L=3, E=E, H=H, S=S, B=B, dtype="bf16", act_offload=n_off, offload=n_off > 0)
+        layers = [nnt_inputs.make_params(E, seed=29, layer=l, init="gpt2", n_layers=3) for l in range(3)]
+        shell = nnt_inputs.make_shell_params(V, S, E, seed=30, init="gpt2")
+        gm = model.GPT2Model(sc, V, layers, shell)
+        if graph:
+            gm.enable_graph()
+        losses = []
+        for t in range(2):
+            tok = torch.as_tensor(nnt_inputs.make_ids(V, S, 0, B, seed=95 + t)).cuda()
+            losses.append(gm.train_step(tok[:, :S].contiguous(), tok[:, 1:].contiguous()).item())
+        torch.cuda.synchronize()
+        return [losses, gm.w.clone(), gm.stack.w.clone(), gm.stack.w16.clone()]
+    ref = run(0, False)
+    _same(run(3, False), ref)
+    _same(run(3, True), ref)
