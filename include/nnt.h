@@ -255,6 +255,13 @@ nnt_status nnt_attn_rowdot(const void* dO, const void* O, int dtype, int64_t B, 
 /* ------------------------------------------------------------------------- */
 /* Fused attention tiles (bf16 path, readings R20, R26, R33)       */
 /* ------------------------------------------------------------------------- */
+/* Pipeline trace of the fused attention kernels (tools/attn_trace.py): enable != 0 makes CTA 0
+ * of the following launches record %globaltimer at 6 events of each of its first 256 iterations
+ * (fwd: K/V loads issued, S MMA issued, S ready in the epilogue, P staged, P seen by the MMA
+ * issuer, O MMA issued); host_out (nullable, up to cap entries of [2][6][256] uint64) receives the
+ * last recorded values (index 0 forward, 1 backward).  Debug only; off by default. */
+nnt_status nnt_attention_trace(int enable, uint64_t* host_out, int64_t cap);
+
 /* 1 when the fused attention kernels below cover (S, h): head size 64 and S % 128 == 0. */
 int nnt_attention_fused_supported(int64_t S, int64_t h);
 

@@ -45,7 +45,20 @@ struct AttnParams {
   float scale;          // 1 / sqrt(h)
   const float* stats;   // fwd: (M, S_sum) per (b, h, query) as float2, M in scaled-score units
   const float* D;       // bwd: D = rowdot(dO, O) per (b, h, query)
+  unsigned long long* trace;  // nnt_attention_trace: CTA 0's per-iteration event times, or NULL
 };
+
+// Pipeline trace (nnt_attention_trace, tools): CTA 0 records %globaltimer at kTraceEv events of
+// each of its first kTraceIt iterations.
+constexpr int kTraceIt = 256, kTraceEv = 6;
+__device__ unsigned long long g_attn_trace[2][kTraceEv][kTraceIt];
+__device__ __forceinline__ void trace_ev(const AttnParams& P, int ev, int64_t g) {
+  if (P.trace && blockIdx.x == 0 && g < kTraceIt) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    P.trace[ev * kTraceIt + g] = t;
+  }
+}
 
 // idesc: fp32 accumulate, bf16 A / B, the operands' majors, N, M = 128
 __host__ __device__ constexpr uint32_t idesc_of(bool a_mn, bool b_mn, int n) {
@@ -165,6 +178,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tl = 0;
+    int64_t it_p = 0;
     for (int64_t k = 0;; ++k, ++tl) {
       const int64_t t = task_at(c0, G, k);
       if (t >= P.num_tasks) break;
@@ -181,6 +195,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
         mbar_expect_tx_w(smem_u32(&full[stage]), 2 * TILE16);
         tma_load_4d_w(st, &mK, smem_u32(&full[stage]), 0, kb * TB, h, b);
         tma_load_4d_w(st + TILE16, &mV, smem_u32(&full[stage]), 0, kb * TB, h, b);
+        if (lane == 0) trace_ev(P, 0, it_p);
+        ++it_p;
         if (++stage == F_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -211,6 +227,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
       mma_commit_w(smem_u32(&sfull[sb]));
+      if (lane == 0) trace_ev(P, 1, g);
       if (i == nk - 1) mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
     };
     int64_t k = 0;
@@ -241,6 +258,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const int os = tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
         if (i == 0) mbar_wait(smem_u32(&oempty[os]), ((tl >> 1) & 1) ^ 1);
         mbar_wait(smem_u32(&pfull[pb]), (uint32_t)((g >> 1) & 1));
+        if (lane == 0) trace_ev(P, 4, g);
         tc_fence_after();
         const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
         const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
@@ -250,6 +268,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
                      make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(smem_u32(&pempty[pb]));
         mma_commit_w(smem_u32(&empty[stg]));
+        if (lane == 0) trace_ev(P, 5, g);
         if (i == nk - 1) mma_commit_w(smem_u32(&ofull[os]));
         if (!more) break;
         if (tl2 != tl) ++k;
@@ -291,6 +310,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       for (int i = 0; i < nk; ++i, ++it) {
         const int sb = it & 1;
         mbar_wait(smem_u32(&sfull[sb]), (it >> 1) & 1);
+        if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
         float v[32];
         tmem_ld32(tmem + sb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
@@ -326,6 +346,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         pair_sync(pair);
         if (lane == 0) {
           mbar_arrive(smem_u32(&pfull[pb]));
+          if (warp == 2) trace_ev(P, 3, it);
           if (leader) {
             tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
             bulk_commit();
@@ -634,6 +655,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
 
 int64_t persistent_grid(int64_t tasks) { return tasks < num_sms() ? tasks : num_sms(); }
 
+bool g_trace_on = false;
+unsigned long long* trace_ptr(int which) {
+  if (!g_trace_on) return nullptr;
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, g_attn_trace) != cudaSuccess) return nullptr;
+  return reinterpret_cast<unsigned long long*>(p) + (size_t)which * kTraceEv * kTraceIt;
+}
+
 nnt_status check_attn(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, const char* what) {
   NNT_REQUIRE(qkv, NNT_ERR_NULL, "%s: NULL pointer", what);
   NNT_REQUIRE(B > 0 && H > 0 && S > 0 && B * H * S < (1ll << 31), NNT_ERR_SHAPE, "%s: B=%lld S=%lld H=%lld", what,
@@ -651,6 +680,15 @@ using namespace nnt;
 
 extern "C" {
 
+nnt_status nnt_attention_trace(int enable, uint64_t* host_out, int64_t cap) {
+  g_trace_on = enable != 0;
+  if (host_out && cap > 0) {
+    const int64_t n = cap < 2 * kTraceEv * kTraceIt ? cap : 2 * kTraceEv * kTraceIt;
+    NNT_CUDA_TRY(cudaMemcpyFromSymbol(host_out, g_attn_trace, (size_t)n * sizeof(uint64_t)));
+  }
+  return NNT_OK;
+}
+
 int nnt_attention_fused_supported(int64_t S, int64_t Dh) { return Dh == HD && S > 0 && S % TB == 0 ? 1 : 0; }
 
 nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, float scale,
@@ -659,7 +697,8 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
   NNT_REQUIRE(stats && P && O, NNT_ERR_NULL, "nnt_attention_fwd_pv: NULL pointer");
   NNT_REQUIRE(aligned16(P) && aligned16(O) && aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_fwd_pv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
-  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr};
+  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr,
+                 trace_ptr(0)};
   CUtensorMap mQ, mK, mV, mPst, mO;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -687,7 +726,8 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
   NNT_REQUIRE(aligned16(dO) && aligned16(P) && aligned16(D) && aligned16(dAT) && aligned16(dqkv), NNT_ERR_ALIGN,
               "nnt_attention_bwd_kv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
-  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D};
+  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D,
+                 trace_ptr(1)};
   CUtensorMap mV, mdO, mQ, mP, mdAT, mdK, mdV;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;

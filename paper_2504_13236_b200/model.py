@@ -298,6 +298,8 @@ class BlockStack:
             self.xs[0].copy_(x)
         ah = self.act_host
         compute = torch.cuda.current_stream()
+        if ah is not None:
+            ah.begin(compute)
         for l in range(self.cfg.L):
             if ah is not None and l < self.n_off:
                 ah.before_fwd(l, compute)

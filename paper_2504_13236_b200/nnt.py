@@ -50,7 +50,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
            "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv",
-           "nnt_stf_build")
+           "nnt_stf_build", "nnt_attention_trace")
 
 
 class NNTError(RuntimeError):
@@ -136,6 +136,7 @@ _sig = {
     "nnt_attn_rowdot": (_i32, [_vp, _vp, _i32, _i64, _i64, _i64, _i64, _vp, _vp]),
     "nnt_attention_fused_supported": (_i32, [_i64, _i64]),
     "nnt_stf_build": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
+    "nnt_attention_trace": (_i32, [_i32, _vp, _i64]),
     "nnt_attention_fwd_pv": (_i32, [_vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp, _vp]),
     "nnt_attention_bwd_kv": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
@@ -305,6 +306,12 @@ def nnt_stf_build(n_handles, tasks):
     check(lib.nnt_stf_build(n_handles, n, p(n_acc), p(hs), p(ms), level.ctypes.data, offs.ctypes.data,
                             ids.ctypes.data, cap))
     return level[:n].tolist(), [ids[offs[t]:offs[t + 1]].tolist() for t in range(n)]
+
+
+def nnt_attention_trace(enable, out=None):
+    """out: a numpy uint64 array (filled with the last trace) or None."""
+    return check(lib.nnt_attention_trace(enable, out.ctypes.data if out is not None else None,
+                                         out.size if out is not None else 0))
 
 
 def nnt_attention_fused_supported(S, h):

@@ -100,6 +100,11 @@ class HostActivations:
         return self.slots[l % 2]
 
     # ---------------------------------------------------------------- forward
+    def begin(self, stream):
+        """Join the copy streams to the caller's work (and to a CUDA-graph capture in progress)."""
+        self.h2d.wait_stream(stream)
+        self.d2h.wait_stream(stream)
+
     def before_fwd(self, l, stream):
         """The compute stream may overwrite slot l % 2 once its previous layer's copy-out is done."""
         if l >= 2:
