@@ -116,9 +116,11 @@ __device__ __forceinline__ void tmem_free512(uint32_t base) {
 
 // ============================================================================ forward
 // smem: Q[2] (task parity) | 3 stages of {K_kb, V_kb} | P staging[2] (32 KB: half h at +16 KB,
-// quadrant rows at +4 KB) | barriers.  TMEM: S[2] at columns 0 / 128, O[2] at 256 / 320.
+// quadrant rows at +4 KB) | O staging (16 KB) | barriers.  TMEM: S[2] at columns 0 / 128, O[2] at
+// 256 / 320.
 constexpr int F_STAGES = 3;
-constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_BAR = F_P + 2 * 2 * TILE16;
+constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_O = F_P + 2 * 2 * TILE16;
+constexpr int F_BAR = F_O + TILE16;
 constexpr int F_SMEM = F_BAR + 256 + 1024;
 
 __global__ void __launch_bounds__(kAThreads, 1)
@@ -297,6 +299,32 @@ __global__ void __launch_bounds__(kAThreads, 1)
                    ((int64_t)(b_ * P.H + h_) * P.S + qb_ * TB + quad * 32 + lane));
     };
     float2 st_next = stats_of(task_at(c0, G, 0));
+    // O = P V of a finished task -> bf16 -> TMA store (the 8 warps of chunk 0; the second warp of
+    // each pair issues the store, so the P stores' bulk groups stay apart).  Run after the NEXT
+    // task's first P tile, so the O MMA's completion and the store overlap P work (O is
+    // double-buffered in TMEM).
+    auto o_epilogue = [&](int tlo, int qbo, int bo, int ho) {
+      if (hc != 0) return;
+      const int os = tlo & 1;
+      mbar_wait(smem_u32(&ofull[os]), (tlo >> 1) & 1);
+      tc_fence_after();
+      float v[32];
+      tmem_ld32(tmem + 256 + os * HD + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
+      uint8_t* piece = smem + F_O + quad * PIECE;
+      if (!leader && lane == 0) bulk_wait_read0();  // this pair's previous O store
+      pair_sync(pair);
+      stage_half_row(piece, lane, sub, v);
+      fence_async_smem();
+      pair_sync(pair);
+      if (!leader && lane == 0) {
+        tma_store_4d(&mO, smem_u32(piece), 0, qbo * TB + quad * 32, ho, bo);
+        bulk_commit();
+      }
+    };
+    int pq = -1, pb_ = 0, ph = 0;  // the task whose O epilogue is pending
     for (int64_t k = 0;; ++k, ++tl) {
       const int64_t t = task_at(c0, G, k);
       if (t >= P.num_tasks) break;
@@ -335,11 +363,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) v[j] = 0.f;
         }
-        // P -> staging buffer pb (after MMA O of iteration it-2 and the pair's store from it)
+        // P -> staging buffer pb (after MMA O of iteration it-2 and the pair's store from it: the
+        // leader's only more recent bulk group is the store of iteration it-1)
         const int pb = it & 1;
         mbar_wait(smem_u32(&pempty[pb]), ((it >> 1) & 1) ^ 1);
         uint8_t* piece = smem + F_P + pb * 2 * TILE16 + hc * TILE16 + quad * PIECE;
-        if (leader && lane == 0) bulk_wait_read0();
+        if (leader && lane == 0) bulk_wait_read1();
         pair_sync(pair);
         stage_half_row(piece, lane, sub, v);
         fence_async_smem();
@@ -352,30 +381,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
             bulk_commit();
           }
         }
+        if (i == 0 && pq >= 0) o_epilogue(tl - 1, pq, pb_, ph);  // the previous task's O
       }
-      // O = P V of the task (8 warps: chunk 0) -> bf16 -> TMA store
-      if (hc == 0) {
-        const int os = tl & 1;
-        mbar_wait(smem_u32(&ofull[os]), (tl >> 1) & 1);
-        tc_fence_after();
-        float v[32];
-        tmem_ld32(tmem + 256 + os * HD + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
-        // staging: the pair's piece of the P buffer MMA O has finished with (ofull covers it)
-        uint8_t* piece = smem + F_P + ((it - 1) & 1) * 2 * TILE16 + quad * PIECE;
-        if (leader && lane == 0) bulk_wait_read0();
-        pair_sync(pair);
-        stage_half_row(piece, lane, sub, v);
-        fence_async_smem();
-        pair_sync(pair);
-        if (leader && lane == 0) {
-          tma_store_4d(&mO, smem_u32(piece), 0, qb * TB + quad * 32, h, b);
-          bulk_commit();
-        }
-      }
+      pq = qb;
+      pb_ = b;
+      ph = h;
     }
+    if (pq >= 0) o_epilogue(tl - 1, pq, pb_, ph);
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
