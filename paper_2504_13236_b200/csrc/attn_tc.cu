@@ -116,11 +116,11 @@ __device__ __forceinline__ void tmem_free512(uint32_t base) {
 
 // ============================================================================ forward
 // smem: Q[2] (task parity) | 3 stages of {K_kb, V_kb} | P staging[2] (32 KB: half h at +16 KB,
-// quadrant rows at +4 KB) | O staging (16 KB) | barriers.  TMEM: S[2] at columns 0 / 128, O[2] at
-// 256 / 320.
+// quadrant rows at +4 KB) | O staging[2] (16 KB each) | barriers.  TMEM: S[2] at columns 0 / 128,
+// O[2] at 256 / 320.
 constexpr int F_STAGES = 3;
 constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_O = F_P + 2 * 2 * TILE16;
-constexpr int F_BAR = F_O + TILE16;
+constexpr int F_BAR = F_O + 2 * TILE16;
 constexpr int F_SMEM = F_BAR + 256 + 1024;
 
 __global__ void __launch_bounds__(kAThreads, 1)
@@ -135,11 +135,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint64_t* qfull = bars + 6;             // [2] Q of a task landed
   uint64_t* qempty = bars + 8;            // [2] the task's last S MMA done
   uint64_t* sfull = bars + 10;            // [2] S accumulator ready
-  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (16 warps)
-  uint64_t* pfull = bars + 14;            // [2] P staging written (16 warps)
+  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (8 warps)
+  uint64_t* pfull = bars + 14;            // [2] P staging written (8 warps)
   uint64_t* pempty = bars + 16;           // [2] P staging consumed by MMA O
   uint64_t* ofull = bars + 18;            // [2] O accumulator of a task complete
-  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (8 warps)
+  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (4 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
@@ -152,11 +152,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_init(smem_u32(&qfull[i]), 1);
       mbar_init(smem_u32(&qempty[i]), 1);
       mbar_init(smem_u32(&sfull[i]), 1);
-      mbar_init(smem_u32(&sempty[i]), kEW);
-      mbar_init(smem_u32(&pfull[i]), kEW);
+      mbar_init(smem_u32(&sempty[i]), kEW / 2);  // one ping-pong group per buffer
+      mbar_init(smem_u32(&pfull[i]), kEW / 2);
       mbar_init(smem_u32(&pempty[i]), 1);
       mbar_init(smem_u32(&ofull[i]), 1);
-      mbar_init(smem_u32(&oempty[i]), kEW / 2);
+      mbar_init(smem_u32(&oempty[i]), 4);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -281,12 +281,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
       }
     }
   } else {
-    // ------------------------------------------------ epilogue warps 2..17
-    // warp: TMEM lane quadrant quad (rows), 32-column group cg of the 128-wide tile; the pair of
-    // warps sharing a 64-column chunk h = cg / 2 writes the two halves (sub) of its staging rows
-    // and the first of them (sub == 0) issues the chunk's TMA store
-    const int quad = warp & 3, cg = (warp - 2) >> 2, hc = cg >> 1, sub = cg & 1, pair = quad * 2 + hc;
-    const bool leader = sub == 0;
+    // ------------------------------------------------ epilogue warps 2..17: two ping-pong groups
+    // Group grp = (warp - 2) / 8 takes the iterations g with g % 2 == grp (S buffer, P staging
+    // buffer grp), so each group has two iterations' time for its P tile: the epilogue's per-tile
+    // latency chain (TMEM load, exponentials, staging, proxy fence, barrier, store) overlaps the
+    // other group's.  Inside a group: TMEM lane quadrant quad (rows), 64-column chunk hc (two
+    // 32-column halves in turn); each warp writes whole 128-byte staging rows and stores its piece.
+    const int grp = (warp - 2) >> 3, quad = warp & 3, hc = ((warp - 2) >> 2) & 1;
     const float L2E = 1.4426950408889634f;
     const float sc = P.scale * L2E;
     int it = 0, tl = 0;
@@ -299,27 +300,26 @@ __global__ void __launch_bounds__(kAThreads, 1)
                    ((int64_t)(b_ * P.H + h_) * P.S + qb_ * TB + quad * 32 + lane));
     };
     float2 st_next = stats_of(task_at(c0, G, 0));
-    // O = P V of a finished task -> bf16 -> TMA store (the 8 warps of chunk 0; the second warp of
-    // each pair issues the store, so the P stores' bulk groups stay apart).  Run after the NEXT
-    // task's first P tile, so the O MMA's completion and the store overlap P work (O is
-    // double-buffered in TMEM).
+    // O = P V of a finished task -> bf16 -> TMA store, by the 4 chunk-0 warps of the group that
+    // owns the NEXT task's first iteration, after that iteration's P tile (O is double-buffered
+    // in TMEM, so its completion and store overlap P work); O staging buffer grp
     auto o_epilogue = [&](int tlo, int qbo, int bo, int ho) {
       if (hc != 0) return;
       const int os = tlo & 1;
       mbar_wait(smem_u32(&ofull[os]), (tlo >> 1) & 1);
       tc_fence_after();
-      float v[32];
-      tmem_ld32(tmem + 256 + os * HD + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+      float v[64];
+      tmem_ld_cols<2>(tmem + 256 + os * HD + ((uint32_t)(quad * 32) << 16), v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
-      uint8_t* piece = smem + F_O + quad * PIECE;
-      if (!leader && lane == 0) bulk_wait_read0();  // this pair's previous O store
-      pair_sync(pair);
-      stage_half_row(piece, lane, sub, v);
+      uint8_t* piece = smem + F_O + grp * TILE16 + quad * PIECE;
+      if (lane == 0) bulk_wait_read0();
+      __syncwarp();
+      stage_row<__nv_bfloat16, 64>(piece, lane, v);
       fence_async_smem();
-      pair_sync(pair);
-      if (!leader && lane == 0) {
+      __syncwarp();
+      if (lane == 0) {
         tma_store_4d(&mO, smem_u32(piece), 0, qbo * TB + quad * 32, ho, bo);
         bulk_commit();
       }
@@ -336,50 +336,50 @@ __global__ void __launch_bounds__(kAThreads, 1)
       const float ml = st.x * L2E, inv = rcp_approx(st.y);
       const int nk = P.causal ? qb + 1 : P.nblk;
       for (int i = 0; i < nk; ++i, ++it) {
-        const int sb = it & 1;
+        if ((it & 1) != grp) continue;
+        const int sb = it & 1;  // == grp
         mbar_wait(smem_u32(&sfull[sb]), (it >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
-        float v[32];
-        tmem_ld32(tmem + sb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
-        tc_fence_before();
+        // P staging buffer grp: free once MMA O of iteration it-2 (pempty) and this warp's store
+        // of it (its most recent bulk group) are done
+        mbar_wait(smem_u32(&pempty[sb]), ((it >> 1) & 1) ^ 1);
+        uint8_t* piece = smem + F_P + sb * 2 * TILE16 + hc * TILE16 + quad * PIECE;
+        if (lane == 0) bulk_wait_read0();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&sempty[sb]));
-        const int key0 = i * TB + cg * 32;
-        int lim = 32;  // causal: keys <= q
-        if (P.causal && key0 + 31 > q) lim = q - key0 + 1;
-        if (lim >= 32) {
 #pragma unroll
-          for (int j = 0; j < 32; j += 2) {
-            const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc, sc), make_float2(-ml, -ml));
-            const float2 y = __fmul2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(inv, inv));
-            v[j] = y.x;
-            v[j + 1] = y.y;
+        for (int sub = 0; sub < 2; ++sub) {
+          float v[32];
+          tmem_ld32(tmem + sb * TB + hc * 64 + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+          const int key0 = i * TB + hc * 64 + sub * 32;
+          int lim = 32;  // causal: keys <= q
+          if (P.causal && key0 + 31 > q) lim = q - key0 + 1;
+          if (lim >= 32) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 2) {
+              const float2 x = __ffma2_rn(make_float2(v[j], v[j + 1]), make_float2(sc, sc), make_float2(-ml, -ml));
+              const float2 y = __fmul2_rn(make_float2(ex2_approx(x.x), ex2_approx(x.y)), make_float2(inv, inv));
+              v[j] = y.x;
+              v[j + 1] = y.y;
+            }
+          } else if (lim > 0) {  // diagonal tile: keys > q masked (-> 0)
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = ex2_approx(j < lim ? fmaf(v[j], sc, -ml) : -INFINITY) * inv;
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
           }
-        } else if (lim > 0) {  // diagonal tile: keys > q masked (-> 0)
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = ex2_approx(j < lim ? fmaf(v[j], sc, -ml) : -INFINITY) * inv;
-        } else {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          stage_half_row(piece, lane, sub, v);
         }
-        // P -> staging buffer pb (after MMA O of iteration it-2 and the pair's store from it: the
-        // leader's only more recent bulk group is the store of iteration it-1)
-        const int pb = it & 1;
-        mbar_wait(smem_u32(&pempty[pb]), ((it >> 1) & 1) ^ 1);
-        uint8_t* piece = smem + F_P + pb * 2 * TILE16 + hc * TILE16 + quad * PIECE;
-        if (leader && lane == 0) bulk_wait_read1();
-        pair_sync(pair);
-        stage_half_row(piece, lane, sub, v);
+        tc_fence_before();
         fence_async_smem();
-        pair_sync(pair);
+        __syncwarp();
         if (lane == 0) {
-          mbar_arrive(smem_u32(&pfull[pb]));
+          mbar_arrive(smem_u32(&sempty[sb]));
+          mbar_arrive(smem_u32(&pfull[sb]));
           if (warp == 2) trace_ev(P, 3, it);
-          if (leader) {
-            tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
-            bulk_commit();
-          }
+          tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
+          bulk_commit();
         }
         if (i == 0 && pq >= 0) o_epilogue(tl - 1, pq, pb_, ph);  // the previous task's O
       }
@@ -387,7 +387,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       pb_ = b;
       ph = h;
     }
-    if (pq >= 0) o_epilogue(tl - 1, pq, pb_, ph);
+    if (pq >= 0 && (it & 1) == grp) o_epilogue(tl - 1, pq, pb_, ph);
     if (lane == 0) bulk_wait0();
   }
   tc_fence_before();
