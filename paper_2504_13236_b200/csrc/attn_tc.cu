@@ -116,8 +116,8 @@ __device__ __forceinline__ void tmem_free512(uint32_t base) {
 
 // ============================================================================ forward
 // smem: Q[2] (task parity) | 3 stages of {K_kb, V_kb} | P staging[2] (32 KB: half h at +16 KB,
-// quadrant rows at +4 KB) | O staging[2] (16 KB each) | barriers.  TMEM: S[2] at columns 0 / 128,
-// O[2] at 256 / 320.
+// quadrant rows at +4 KB) | O staging[2] (16 KB each) | barriers.  TMEM: S[3] at columns 0 / 128 /
+// 256, O[2] at 384 / 448.
 constexpr int F_STAGES = 3;
 constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_O = F_P + 2 * 2 * TILE16;
 constexpr int F_BAR = F_O + 2 * TILE16;
@@ -134,25 +134,25 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint64_t* empty = bars + 3;             // [3] stage consumed (MMA S and MMA O)
   uint64_t* qfull = bars + 6;             // [2] Q of a task landed
   uint64_t* qempty = bars + 8;            // [2] the task's last S MMA done
-  uint64_t* sfull = bars + 10;            // [2] S accumulator ready
-  uint64_t* sempty = bars + 12;           // [2] S accumulator drained (8 warps)
-  uint64_t* pfull = bars + 14;            // [2] P staging written (8 warps)
-  uint64_t* pempty = bars + 16;           // [2] P staging consumed by MMA O
-  uint64_t* ofull = bars + 18;            // [2] O accumulator of a task complete
-  uint64_t* oempty = bars + 20;           // [2] O accumulator drained (4 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 22);
+  uint64_t* sfull = bars + 10;            // [3] S accumulator ready
+  uint64_t* sempty = bars + 13;           // [3] S accumulator drained (8 warps)
+  uint64_t* pfull = bars + 16;            // [2] P staging written (8 warps)
+  uint64_t* pempty = bars + 18;           // [2] P staging consumed by MMA O
+  uint64_t* ofull = bars + 20;            // [2] O accumulator of a task complete
+  uint64_t* oempty = bars + 22;           // [2] O accumulator drained (4 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 3; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
       mbar_init(smem_u32(&empty[i]), 1);
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), kEW / 2);  // one ping-pong group per use
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&qfull[i]), 1);
       mbar_init(smem_u32(&qempty[i]), 1);
-      mbar_init(smem_u32(&sfull[i]), 1);
-      mbar_init(smem_u32(&sempty[i]), kEW / 2);  // one ping-pong group per buffer
       mbar_init(smem_u32(&pfull[i]), kEW / 2);
       mbar_init(smem_u32(&pempty[i]), 1);
       mbar_init(smem_u32(&ofull[i]), 1);
@@ -208,18 +208,47 @@ __global__ void __launch_bounds__(kAThreads, 1)
     pdl_trigger();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // A flat stream of iterations g over this CTA's tasks (S / P buffer g & 1, stage g % 3): the S
-    // MMA of iteration g + 1 -- also the first one of the next task -- is issued before the O MMA
-    // of iteration g, which waits for the epilogue's P, so the tensor core runs ahead of the
-    // epilogue across task boundaries too.
+    // A flat stream of iterations g over this CTA's tasks (S buffer g % 3, P buffer g % 2, stage
+    // g % 3): the S MMAs run two iterations ahead of the O MMA of iteration g (which waits for the
+    // epilogue's P), across task boundaries too, so each ping-pong epilogue group finds its next
+    // S tile ready when it finishes a P tile.
     const uint32_t id_s = idesc_of(false, false, TB);  // S = Q K^T: both K-major, N = 128
     const uint32_t id_o = idesc_of(false, true, HD);   // O += P V: P K-major, V MN-major, N = 64
-    auto nk_of = [&](int qb) { return P.causal ? qb + 1 : P.nblk; };
-    auto issue_s = [&](int64_t g, int tl, int i, int nk) {
-      const int sb = (int)(g & 1), stg = (int)(g % F_STAGES);
-      const int qs = tl & 1;
-      if (i == 0) mbar_wait(smem_u32(&qfull[qs]), (tl >> 1) & 1);
-      mbar_wait(smem_u32(&sempty[sb]), (uint32_t)(((g >> 1) & 1) ^ 1));
+    struct Cur {
+      int64_t k;  // task index in this CTA's schedule
+      int tl, i, nk;
+      bool ok;
+    };
+    auto first = [&]() {
+      Cur c{0, 0, 0, 0, false};
+      const int64_t t = task_at(c0, G, 0);
+      if (t < P.num_tasks) {
+        int qb, b, h;
+        decode(t, qb, b, h);
+        c.nk = P.causal ? qb + 1 : P.nblk;
+        c.ok = true;
+      }
+      return c;
+    };
+    auto next = [&](Cur c) {
+      if (++c.i < c.nk) return c;
+      const int64_t t = task_at(c0, G, c.k + 1);
+      if (t >= P.num_tasks) {
+        c.ok = false;
+        return c;
+      }
+      int qb, b, h;
+      decode(t, qb, b, h);
+      ++c.k;
+      ++c.tl;
+      c.i = 0;
+      c.nk = P.causal ? qb + 1 : P.nblk;
+      return c;
+    };
+    auto issue_s = [&](int64_t g, const Cur& c) {
+      const int sb = (int)(g % 3), stg = (int)(g % F_STAGES), qs = c.tl & 1;
+      if (c.i == 0) mbar_wait(smem_u32(&qfull[qs]), (c.tl >> 1) & 1);
+      mbar_wait(smem_u32(&sempty[sb]), (uint32_t)(((g / 3) & 1) ^ 1));
       mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / F_STAGES) & 1));
       tc_fence_after();
       const uint32_t sq = smem_u32(smem + F_Q + qs * TILE16);
@@ -230,55 +259,36 @@ __global__ void __launch_bounds__(kAThreads, 1)
                    kk > 0 ? 1u : 0u);
       mma_commit_w(smem_u32(&sfull[sb]));
       if (lane == 0) trace_ev(P, 1, g);
-      if (i == nk - 1) mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
+      if (c.i == c.nk - 1) mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
     };
-    int64_t k = 0;
-    int64_t t = task_at(c0, G, 0);
-    if (t < P.num_tasks) {
-      int qb, b, h;
-      decode(t, qb, b, h);
-      int tl = 0, i = 0, nk = nk_of(qb);
-      int64_t g = 0;
-      issue_s(0, 0, 0, nk);
-      for (;;) {
-        // the next iteration: (tl, i + 1) or the first of the next task
-        int tl2 = tl, i2 = i + 1, nk2 = nk;
-        bool more = true;
-        if (i2 == nk) {
-          const int64_t t2 = task_at(c0, G, k + 1);
-          more = t2 < P.num_tasks;
-          if (more) {
-            int qb2, b2, h2;
-            decode(t2, qb2, b2, h2);
-            tl2 = tl + 1;
-            i2 = 0;
-            nk2 = nk_of(qb2);
-          }
-        }
-        if (more) issue_s(g + 1, tl2, i2, nk2);
-        // O += P V for iteration g
-        const int os = tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
-        if (i == 0) mbar_wait(smem_u32(&oempty[os]), ((tl >> 1) & 1) ^ 1);
-        mbar_wait(smem_u32(&pfull[pb]), (uint32_t)((g >> 1) & 1));
-        if (lane == 0) trace_ev(P, 4, g);
-        tc_fence_after();
-        const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
-        const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
+    Cur cur = first(), ahead1 = cur, ahead2 = cur;
+    if (cur.ok) {
+      issue_s(0, cur);
+      ahead1 = next(cur);
+      if (ahead1.ok) issue_s(1, ahead1);
+      ahead2 = ahead1.ok ? next(ahead1) : ahead1;
+    }
+    for (int64_t g = 0; cur.ok; ++g) {
+      if (ahead2.ok) issue_s(g + 2, ahead2);
+      // O += P V for iteration g
+      const int os = cur.tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
+      if (cur.i == 0) mbar_wait(smem_u32(&oempty[os]), ((cur.tl >> 1) & 1) ^ 1);
+      mbar_wait(smem_u32(&pfull[pb]), (uint32_t)((g >> 1) & 1));
+      if (lane == 0) trace_ev(P, 4, g);
+      tc_fence_after();
+      const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
+      const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
 #pragma unroll
-        for (int kk = 0; kk < TB / 16; ++kk)  // K = 128 keys: P chunk kk/4 (+16 KB), V rows +2 KB
-          mma_bf16_w(tmem + 256 + os * HD, make_sdesc(sp + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
-                     make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(smem_u32(&pempty[pb]));
-        mma_commit_w(smem_u32(&empty[stg]));
-        if (lane == 0) trace_ev(P, 5, g);
-        if (i == nk - 1) mma_commit_w(smem_u32(&ofull[os]));
-        if (!more) break;
-        if (tl2 != tl) ++k;
-        tl = tl2;
-        i = i2;
-        nk = nk2;
-        ++g;
-      }
+      for (int kk = 0; kk < TB / 16; ++kk)  // K = 128 keys: P chunk kk/4 (+16 KB), V rows +2 KB
+        mma_bf16_w(tmem + 384 + os * HD, make_sdesc(sp + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
+                   make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (cur.i > 0 || kk > 0) ? 1u : 0u);
+      mma_commit_w(smem_u32(&pempty[pb]));
+      mma_commit_w(smem_u32(&empty[stg]));
+      if (lane == 0) trace_ev(P, 5, g);
+      if (cur.i == cur.nk - 1) mma_commit_w(smem_u32(&ofull[os]));
+      cur = ahead1;
+      ahead1 = ahead2;
+      if (ahead2.ok) ahead2 = next(ahead2);
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..17: two ping-pong groups
@@ -309,7 +319,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_wait(smem_u32(&ofull[os]), (tlo >> 1) & 1);
       tc_fence_after();
       float v[64];
-      tmem_ld_cols<2>(tmem + 256 + os * HD + ((uint32_t)(quad * 32) << 16), v);
+      tmem_ld_cols<2>(tmem + 384 + os * HD + ((uint32_t)(quad * 32) << 16), v);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(&oempty[os]));
@@ -337,14 +347,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
       const int nk = P.causal ? qb + 1 : P.nblk;
       for (int i = 0; i < nk; ++i, ++it) {
         if ((it & 1) != grp) continue;
-        const int sb = it & 1;  // == grp
-        mbar_wait(smem_u32(&sfull[sb]), (it >> 1) & 1);
+        const int sb = it % 3, pbuf = it & 1;  // S buffer, P staging buffer (== grp)
+        mbar_wait(smem_u32(&sfull[sb]), (uint32_t)((it / 3) & 1));
         if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
         // P staging buffer grp: free once MMA O of iteration it-2 (pempty) and this warp's store
         // of it (its most recent bulk group) are done
-        mbar_wait(smem_u32(&pempty[sb]), ((it >> 1) & 1) ^ 1);
-        uint8_t* piece = smem + F_P + sb * 2 * TILE16 + hc * TILE16 + quad * PIECE;
+        mbar_wait(smem_u32(&pempty[pbuf]), ((it >> 1) & 1) ^ 1);
+        uint8_t* piece = smem + F_P + pbuf * 2 * TILE16 + hc * TILE16 + quad * PIECE;
         if (lane == 0) bulk_wait_read0();
         __syncwarp();
 #pragma unroll
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(smem_u32(&sempty[sb]));
-          mbar_arrive(smem_u32(&pfull[sb]));
+          mbar_arrive(smem_u32(&pfull[pbuf]));
           if (warp == 2) trace_ev(P, 3, it);
           tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
           bulk_commit();
