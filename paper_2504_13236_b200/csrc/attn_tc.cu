@@ -245,6 +245,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
       c.nk = P.causal ? qb + 1 : P.nblk;
       return c;
     };
+    // S(g) can be issued without blocking: its Q, S buffer and K tile are there
+    auto s_ready = [&](int64_t g, const Cur& c) {
+      const int sb = (int)(g % 3), stg = (int)(g % F_STAGES), qs = c.tl & 1;
+      return (c.i != 0 || mbar_test(smem_u32(&qfull[qs]), (c.tl >> 1) & 1)) &&
+             mbar_test(smem_u32(&sempty[sb]), (uint32_t)(((g / 3) & 1) ^ 1)) &&
+             mbar_test(smem_u32(&full[stg]), (uint32_t)((g / F_STAGES) & 1));
+    };
     auto issue_s = [&](int64_t g, const Cur& c) {
       const int sb = (int)(g % 3), stg = (int)(g % F_STAGES), qs = c.tl & 1;
       if (c.i == 0) mbar_wait(smem_u32(&qfull[qs]), (c.tl >> 1) & 1);
@@ -269,7 +276,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
       ahead2 = ahead1.ok ? next(ahead1) : ahead1;
     }
     for (int64_t g = 0; cur.ok; ++g) {
-      if (ahead2.ok) issue_s(g + 2, ahead2);
+      // S(g + 2) now if nothing blocks it, else after O(g): O(g) never waits behind a K load
+      bool s_pending = ahead2.ok;
+      if (s_pending && s_ready(g + 2, ahead2)) {
+        issue_s(g + 2, ahead2);
+        s_pending = false;
+      }
       // O += P V for iteration g
       const int os = cur.tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
       if (cur.i == 0) mbar_wait(smem_u32(&oempty[os]), ((cur.tl >> 1) & 1) ^ 1);
@@ -286,6 +298,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mma_commit_w(smem_u32(&empty[stg]));
       if (lane == 0) trace_ev(P, 5, g);
       if (cur.i == cur.nk - 1) mma_commit_w(smem_u32(&ofull[os]));
+      if (s_pending) issue_s(g + 2, ahead2);
       cur = ahead1;
       ahead1 = ahead2;
       if (ahead2.ok) ahead2 = next(ahead2);
@@ -361,6 +374,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
         for (int sub = 0; sub < 2; ++sub) {
           float v[32];
           tmem_ld32(tmem + sb * TB + hc * 64 + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+          if (sub == 1) {  // the S buffer is free once both halves are in registers
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&sempty[sb]));
+          }
           const int key0 = i * TB + hc * 64 + sub * 32;
           int lim = 32;  // causal: keys <= q
           if (P.causal && key0 + 31 > q) lim = q - key0 + 1;
@@ -381,11 +399,9 @@ __global__ void __launch_bounds__(kAThreads, 1)
           }
           stage_half_row(piece, lane, sub, v);
         }
-        tc_fence_before();
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(smem_u32(&sempty[sb]));
           mbar_arrive(smem_u32(&pfull[pbuf]));
           if (warp == 2) trace_ev(P, 3, it);
           tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
