@@ -115,23 +115,25 @@ __device__ __forceinline__ void tmem_free512(uint32_t base) {
 }
 
 // ============================================================================ forward
-// smem: Q[2] (task parity) | 3 stages of {K_kb, V_kb} | P staging[2] (32 KB: half h at +16 KB,
+// smem: Q[2] (task parity) | K ring[3] | V ring[3] | P staging[2] (32 KB: half h at +16 KB,
 // quadrant rows at +4 KB) | O staging[2] (16 KB each) | barriers.  TMEM: S[3] at columns 0 / 128 /
 // 256, O[2] at 384 / 448.
-constexpr int F_STAGES = 3;
-constexpr int F_Q = 0, F_ST = 2 * TILE16, F_P = F_ST + F_STAGES * 2 * TILE16, F_O = F_P + 2 * 2 * TILE16;
+constexpr int F_STAGES = 3;  // K ring and V ring, 3 tiles each
+constexpr int F_Q = 0, F_K = 2 * TILE16, F_V = F_K + F_STAGES * TILE16, F_P = F_V + F_STAGES * TILE16;
+constexpr int F_O = F_P + 2 * 2 * TILE16;
+constexpr int kAThreadsF = kAThreads + 32;  // + the V producer warp (warp 18)
 constexpr int F_BAR = F_O + 2 * TILE16;
 constexpr int F_SMEM = F_BAR + 256 + 1024;
 
-__global__ void __launch_bounds__(kAThreads, 1)
+__global__ void __launch_bounds__(kAThreadsF, 1)
     attn_fwd_pv_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mQ,
                        const __grid_constant__ CUtensorMap mK, const __grid_constant__ CUtensorMap mV,
                        const __grid_constant__ CUtensorMap mPst, const __grid_constant__ CUtensorMap mO) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + F_BAR);
-  uint64_t* full = bars;                  // [3] stage K, V landed
-  uint64_t* empty = bars + 3;             // [3] stage consumed (MMA S and MMA O)
+  uint64_t* full = bars;                  // [3] K tile landed
+  uint64_t* empty = bars + 3;             // [3] K tile consumed (its S MMA done)
   uint64_t* qfull = bars + 6;             // [2] Q of a task landed
   uint64_t* qempty = bars + 8;            // [2] the task's last S MMA done
   uint64_t* sfull = bars + 10;            // [3] S accumulator ready
@@ -140,7 +142,9 @@ __global__ void __launch_bounds__(kAThreads, 1)
   uint64_t* pempty = bars + 18;           // [2] P staging consumed by MMA O
   uint64_t* ofull = bars + 20;            // [2] O accumulator of a task complete
   uint64_t* oempty = bars + 22;           // [2] O accumulator drained (4 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
+  uint64_t* vfull = bars + 24;            // [3] V tile landed
+  uint64_t* vempty = bars + 27;           // [3] V tile consumed (its O MMA done)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 30);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
   if (warp == 0 && lane == 0) {
@@ -149,6 +153,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_init(smem_u32(&empty[i]), 1);
       mbar_init(smem_u32(&sfull[i]), 1);
       mbar_init(smem_u32(&sempty[i]), kEW / 2);  // one ping-pong group per use
+      mbar_init(smem_u32(&vfull[i]), 1);
+      mbar_init(smem_u32(&vempty[i]), 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&qfull[i]), 1);
@@ -176,7 +182,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
   const int64_t c0 = blockIdx.x, G = gridDim.x;
 
   if (warp == 0) {
-    // ------------------------------------------------ TMA producer
+    // ------------------------------------------------ TMA producer: Q and the K ring
     int stage = 0;
     uint32_t phase = 0;
     int tl = 0;
@@ -193,10 +199,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
       const int nk = P.causal ? qb + 1 : P.nblk;
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
-        const uint32_t st = smem_u32(smem + F_ST + stage * 2 * TILE16);
-        mbar_expect_tx_w(smem_u32(&full[stage]), 2 * TILE16);
-        tma_load_4d_w(st, &mK, smem_u32(&full[stage]), 0, kb * TB, h, b);
-        tma_load_4d_w(st + TILE16, &mV, smem_u32(&full[stage]), 0, kb * TB, h, b);
+        mbar_expect_tx_w(smem_u32(&full[stage]), TILE16);
+        tma_load_4d_w(smem_u32(smem + F_K + stage * TILE16), &mK, smem_u32(&full[stage]), 0, kb * TB, h, b);
         if (lane == 0) trace_ev(P, 0, it_p);
         ++it_p;
         if (++stage == F_STAGES) {
@@ -206,6 +210,28 @@ __global__ void __launch_bounds__(kAThreads, 1)
       }
     }
     pdl_trigger();
+  } else if (warp == 2 + kEW) {
+    // ------------------------------------------------ TMA producer: the V ring (its tiles are
+    // released by the O MMAs, later than the K tiles by the S MMAs: separate rings and producers
+    // let the K loads run ahead)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t k = 0;; ++k) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(&vempty[stage]), phase ^ 1);
+        mbar_expect_tx_w(smem_u32(&vfull[stage]), TILE16);
+        tma_load_4d_w(smem_u32(smem + F_V + stage * TILE16), &mV, smem_u32(&vfull[stage]), 0, kb * TB, h, b);
+        if (++stage == F_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
     // A flat stream of iterations g over this CTA's tasks (S buffer g % 3, P buffer g % 2, stage
@@ -259,12 +285,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
       mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / F_STAGES) & 1));
       tc_fence_after();
       const uint32_t sq = smem_u32(smem + F_Q + qs * TILE16);
-      const uint32_t sk = smem_u32(smem + F_ST + stg * 2 * TILE16);
+      const uint32_t sk = smem_u32(smem + F_K + stg * TILE16);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk)
         mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
                    kk > 0 ? 1u : 0u);
       mma_commit_w(smem_u32(&sfull[sb]));
+      mma_commit_w(smem_u32(&empty[stg]));  // the K tile is free
       if (lane == 0) trace_ev(P, 1, g);
       if (c.i == c.nk - 1) mma_commit_w(smem_u32(&qempty[qs]));  // the task's last S MMA: Q may be reloaded
     };
@@ -285,17 +312,18 @@ __global__ void __launch_bounds__(kAThreads, 1)
       // O += P V for iteration g
       const int os = cur.tl & 1, pb = (int)(g & 1), stg = (int)(g % F_STAGES);
       if (cur.i == 0) mbar_wait(smem_u32(&oempty[os]), ((cur.tl >> 1) & 1) ^ 1);
+      mbar_wait(smem_u32(&vfull[stg]), (uint32_t)((g / F_STAGES) & 1));
       mbar_wait(smem_u32(&pfull[pb]), (uint32_t)((g >> 1) & 1));
       if (lane == 0) trace_ev(P, 4, g);
       tc_fence_after();
       const uint32_t sp = smem_u32(smem + F_P + pb * 2 * TILE16);
-      const uint32_t sv = smem_u32(smem + F_ST + stg * 2 * TILE16 + TILE16);
+      const uint32_t sv = smem_u32(smem + F_V + stg * TILE16);
 #pragma unroll
       for (int kk = 0; kk < TB / 16; ++kk)  // K = 128 keys: P chunk kk/4 (+16 KB), V rows +2 KB
         mma_bf16_w(tmem + 384 + os * HD, make_sdesc(sp + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
                    make_sdesc(sv + kk * 2048, 8192, 1024), id_o, (cur.i > 0 || kk > 0) ? 1u : 0u);
       mma_commit_w(smem_u32(&pempty[pb]));
-      mma_commit_w(smem_u32(&empty[stg]));
+      mma_commit_w(smem_u32(&vempty[stg]));
       if (lane == 0) trace_ev(P, 5, g);
       if (cur.i == cur.nk - 1) mma_commit_w(smem_u32(&ofull[os]));
       if (s_pending) issue_s(g + 2, ahead2);
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       ahead1 = ahead2;
       if (ahead2.ok) ahead2 = next(ahead2);
     }
-  } else {
+  } else if (warp < 2 + kEW) {
     // ------------------------------------------------ epilogue warps 2..17: two ping-pong groups
     // Group grp = (warp - 2) / 8 takes the iterations g with g % 2 == grp (S buffer, P staging
     // buffer grp), so each group has two iterations' time for its P tile: the epilogue's per-tile
@@ -751,7 +779,7 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
   LaunchScope sc(NNT_K_GEMM_TC_ATTN, stream, ptiles * TB * TB * 2 + 4.0 * B * S * Ea * 2,
                  ptiles * 4.0 * TB * TB * HD);
   NNT_CUDA_TRY(set_max_dyn_smem(attn_fwd_pv_kernel, F_SMEM));
-  NNT_CUDA_TRY(::nnt::launch(attn_fwd_pv_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreads),
+  NNT_CUDA_TRY(::nnt::launch(attn_fwd_pv_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreadsF),
                              (size_t)F_SMEM, (cudaStream_t)stream, prm, mQ, mK, mV, mPst, mO));
   return check_launch("attn_fwd_pv");
 }
