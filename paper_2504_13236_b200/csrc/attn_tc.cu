@@ -520,6 +520,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
     int stage = 0;
     uint32_t phase = 0;
     int tl = 0;
+    int64_t it_p = 0;
     for (int64_t k = 0;; ++k, ++tl) {
       const int64_t t = task_at(c0, G, k);
       if (t >= P.num_tasks) break;
@@ -539,6 +540,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
         tma_load_4d_w(st + TILE16, &mQ, fb, 0, qb * TB, h, b);
         tma_load_4d_w(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b);       // keys kb*128 + 0..63
         tma_load_4d_w(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b);  // keys + 64..127
+        if (lane == 0) trace_ev(P, 0, it_p);
+        ++it_p;
         if (++stage == B_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -568,6 +571,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         mma_bf16_w(tmem + tb * TB, make_sdesc(sv + kk * 32, 16, 1024), make_sdesc(sdo + kk * 32, 16, 1024), id_dp,
                    kk > 0 ? 1u : 0u);
       mma_commit_w(smem_u32(&tfull[tb]));
+      if (lane == 0) trace_ev(P, 1, g);
       if (i == nq - 1) mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
     };
     int64_t k = 0;
@@ -608,6 +612,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         if (more) issue_dp(g + 1, tl2, i2, nq2);
         // dK += dA^T Q once the epilogue has staged dA^T of iteration g
         mbar_wait(smem_u32(dafull), (uint32_t)(g & 1));
+        if (lane == 0) trace_ev(P, 4, g);
         tc_fence_after();
         const uint32_t sda = smem_u32(smem + B_DA);
 #pragma unroll
@@ -615,6 +620,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
           mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
                      make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (i > 0 || kk > 0) ? 1u : 0u);
         mma_commit_w(smem_u32(daempty));
+        if (lane == 0) trace_ev(P, 5, g);
         mma_commit_w(smem_u32(&empty[stg]));
         if (i == nq - 1) mma_commit_w(smem_u32(&afull[as]));
         if (!more) break;
@@ -646,6 +652,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
       for (int qb = q_first(kb); qb < P.nblk; ++qb, ++it) {
         const int tb = it & 1;
         mbar_wait(smem_u32(&tfull[tb]), (it >> 1) & 1);
+        if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
         float v[32];  // dP^T[key = lane row][query = cg * 32 + j]
         tmem_ld32(tmem + tb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
@@ -679,6 +686,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         pair_sync(pair);
         if (lane == 0) {
           mbar_arrive(smem_u32(dafull));
+          if (warp == 2) trace_ev(P, 3, it);
           if (leader) {
             tma_store_4d(&mdAT, smem_u32(piece), qb * TB + hc * 64, kb * TB + quad * 32, h, b);
             bulk_commit();
