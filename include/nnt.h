@@ -570,6 +570,9 @@ typedef struct {
   int32_t op;
   int32_t level;
   int64_t n_tasks;
+  int32_t side_stream_ok;  /* 1: no task of another op depends on this op and it writes only
+                              parameter gradients (a sink of the pass): nnt_block_bwd_streams runs
+                              it on the side stream */
 } nnt_launch_group;
 
 /* Ops of the block DAG, in submission (program) order. */

@@ -508,11 +508,9 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
   // fork event per batch of side ops), and the main stream joins the side stream at the end.
   // They write disjoint gradients and read buffers the main stream does not overwrite within
   // this call (the side column sums use their own scratch), so results are bitwise unchanged.
-  auto on_side = [&](int op) {
-    return side != nullptr && (op == NNT_OP_PROJ_DW || op == NNT_OP_FC_DB || op == NNT_OP_FC_DW ||
-                               op == NNT_OP_OUT_DB || op == NNT_OP_OUT_DW || op == NNT_OP_QKV_DB ||
-                               op == NNT_OP_QKV_DW);
-  };
+  // Which ops: the DAG's sinks that write only parameter gradients (LaunchGroup::side_ok, dag.cpp):
+  // the dW GEMMs and the bias column sums that make no copy for a later op.
+  auto on_side = [&](const LaunchGroup& gr) { return side != nullptr && gr.side_ok; };
   // fork / join events, one pair per device (events belong to the device current at creation)
   static thread_local cudaEvent_t ev_pool[kMaxDevices][2] = {};
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -540,7 +538,7 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
   int remaining[4];
   for (int k = 0; k < 4; ++k) remaining[k] = sets[k][3] < 0 ? 3 : 4;
   for (const auto& gr : plan->groups) {
-    if (on_side(gr.op)) {
+    if (on_side(gr)) {
       if (main_advanced) {
         NNT_CUDA_TRY(cudaEventRecord(ev_fork, stream));
         NNT_CUDA_TRY(cudaStreamWaitEvent(side, ev_fork, 0));

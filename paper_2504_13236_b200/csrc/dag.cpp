@@ -19,8 +19,15 @@ int StfGraph::new_tensor(int64_t n_tiles) {
   int id = (int)base_.size();
   int64_t b = hs_.size();
   base_.push_back(b);
+  param_grad_.push_back(0);
   hs_.resize(b + n_tiles);
   return id;
+}
+
+void StfGraph::mark_param_grad(int tensor) { param_grad_[tensor] = 1; }
+
+int StfGraph::tensor_of(int64_t handle) const {
+  return (int)(std::upper_bound(base_.begin(), base_.end(), handle) - base_.begin()) - 1;
 }
 
 static void add_unique(std::vector<int>& v, int x) {
@@ -38,6 +45,9 @@ int StfGraph::submit(int op, const int64_t tile[3], const std::vector<std::pair<
   t.tile[2] = tile[2];
   t.level = 0;
   t.group = -1;
+  t.writes_only_grads = true;
+  for (auto& [h, mode] : hm)
+    if (mode != ACC_R && !param_grad_[tensor_of(h)]) t.writes_only_grads = false;
   const int id = (int)tasks.size();
   for (auto& [h, mode] : hm) {
     HState& s = hs_[h];
@@ -108,12 +118,17 @@ bool StfGraph::lower(BlockPlan* plan) {
   plan->groups.clear();
   for (auto& [lv, first, op] : order) {
     group_of[op] = (int)plan->groups.size();
-    plan->groups.push_back({op, lv, 0});
+    plan->groups.push_back({op, lv, 0, true});
   }
   for (auto& t : tasks) {
     t.group = group_of[t.op];
-    plan->groups[t.group].n_tasks++;
+    LaunchGroup& gr = plan->groups[t.group];
+    gr.n_tasks++;
+    if (!t.writes_only_grads) gr.side_ok = false;
   }
+  for (const Task& t : tasks)  // an op with a dependent in another op stays on the critical chain
+    for (int d : t.deps)
+      if (tasks[d].op != t.op) plan->groups[group_of[tasks[d].op]].side_ok = false;
   plan->tasks = tasks;
   return true;
 }
@@ -251,6 +266,8 @@ void make_bwd_tensors(StfGraph& g, const Shapes& s, BlockTensors& t) {
   t.gbfc.make(g, 1, F, 1, s.tf);
   t.gwpr.make(g, E, F, s.te, s.tf);
   t.gbpr.make(g, 1, E, 1, s.te);
+  for (const T2* pg : {&t.gln1, &t.gln2, &t.gwqkv, &t.gbqkv, &t.gwo, &t.gbo, &t.gwfc, &t.gbfc, &t.gwpr, &t.gbpr})
+    g.mark_param_grad(pg->id);
   t.dP.make(g, s);
   t.dA.make(g, s);
   t.Dv.make(g, s);
@@ -654,6 +671,7 @@ nnt_status nnt_block_dag_describe(const nnt_block_cfg* cfg, int pass, nnt_task* 
       groups[i].op = p->groups[i].op;
       groups[i].level = p->groups[i].level;
       groups[i].n_tasks = p->groups[i].n_tasks;
+      groups[i].side_stream_ok = p->groups[i].side_ok ? 1 : 0;
     }
   return NNT_OK;
 }

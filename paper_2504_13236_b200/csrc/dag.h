@@ -20,12 +20,16 @@ struct Task {
   int level;
   int group;
   std::vector<int> deps;
+  bool writes_only_grads;  // every handle it writes belongs to a parameter-gradient tensor
 };
 
 struct LaunchGroup {
   int op;
   int level;
   int64_t n_tasks;
+  // no task of another op depends on this op's tasks and all it writes are parameter gradients:
+  // it may run on a second stream beside the critical chain (nnt_block_bwd_streams)
+  bool side_ok;
 };
 
 struct BlockPlan {
@@ -37,6 +41,7 @@ struct BlockPlan {
 class StfGraph {
  public:
   int new_tensor(int64_t n_tiles);
+  void mark_param_grad(int tensor);  // the tensor's tiles are parameter gradients (pass outputs)
   // Submit a task; accesses are (tensor, tile index, mode).
   int submit(int op, const int64_t tile[3], const std::vector<std::pair<int64_t, int>>& handle_modes);
   int64_t handle(int tensor, int64_t tile) const { return base_[tensor] + tile; }
@@ -49,6 +54,8 @@ class StfGraph {
   };
   std::vector<int64_t> base_;
   std::vector<HState> hs_;
+  std::vector<char> param_grad_;  // per tensor
+  int tensor_of(int64_t handle) const;
 };
 
 // Cached plan for (cfg, pass).  Returns nullptr and sets the error on failure.

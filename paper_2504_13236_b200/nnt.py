@@ -115,7 +115,7 @@ class nnt_task(C.Structure):
 
 
 class nnt_launch_group(C.Structure):
-    _fields_ = [("op", C.c_int32), ("level", C.c_int32), ("n_tasks", C.c_int64)]
+    _fields_ = [("op", C.c_int32), ("level", C.c_int32), ("n_tasks", C.c_int64), ("side_stream_ok", C.c_int32)]
 
 
 # ---------------------------------------------------------------- signatures

@@ -185,6 +185,13 @@ def test_dag_task_counts_and_levels(nnt, name, tile):
     assert len(groups) == len(bwd_n)                         # one launch group per op
     for t in tasks:
         assert groups[t.group].op == t.op and t.level <= groups[t.group].level
+    # the ops the backward may run on a side stream (weak r1 #11): exactly the DAG's sinks that write
+    # only parameter gradients -- the dW GEMMs and the bias column sums that copy nothing for a later
+    # op (on the bf16 path proj_db also writes dy's bf16 copy, read by proj_dw / proj_dx)
+    side = {nnt.OP_NAMES[g.op] for g in groups if g.side_stream_ok}
+    want = {"proj_dw", "fc_db", "fc_dw", "out_db", "out_dw", "qkv_db", "qkv_dw"} | ({"proj_db"} if not bf else set())
+    assert side == want
+    assert not any(g.side_stream_ok for g in nnt.nnt_block_dag_describe(cfg, 0)[1])  # forward: a chain
 
 
 def test_dag_reduce_tasks_are_independent(nnt):
