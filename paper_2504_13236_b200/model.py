@@ -174,6 +174,10 @@ class StackConfig:
     act_offload: int = 0
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
+    # train_step without DP: each bucket's optimizer update runs on an update stream as soon as the
+    # backward has finished with the bucket (its grad_ready event), overlapping the rest of the
+    # backward -- the DP path's schedule without the all-reduce (NNT_OVERLAP_UPDATE=0 disables)
+    overlap_update: bool = os.environ.get("NNT_OVERLAP_UPDATE", "1") != "0"
 
     def block_cfg(self):
         return nnt.nnt_block_cfg(self.E, self.H, self.S, self.B, self.tile_e, self.tile_f, self.tile_s, self.tile_t,
@@ -253,11 +257,13 @@ class BlockStack:
         used = [] if self.host_state is None else [self.host_state.h2d, self.host_state.d2h]
         if self.act_host is not None:
             used += [self.act_host.h2d, self.act_host.d2h]
-        self.comm = _distinct_stream(self.dev, used) if self.dp else None
+        # bucketed: gradient buckets handed to the comm / update stream on their grad_ready events
+        self.bucketed = self.dp or cfg.overlap_update
+        self.comm = _distinct_stream(self.dev, used) if self.bucketed else None
         self.side = _distinct_stream(self.dev, used + [self.comm]) if cfg.side_stream else None
         self.cap_stream = _distinct_stream(self.dev, used + [self.comm, self.side])
-        self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.dp else None
-        if self.dp:  # torch creates the CUDA event handles lazily, at the first record()
+        self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.bucketed else None
+        if self.bucketed:  # torch creates the CUDA event handles lazily, at the first record()
             for evs in self.events:
                 for e in evs:
                     e.record()
@@ -316,14 +322,20 @@ class BlockStack:
         nnt.nnt_scale(r, inv, self.dy[0], n)
         return self.loss
 
-    def backward(self, overlap_optimizer=True, top_done=False):
-        """Backward through the stack; with DP, bucket all-reduce (+ Adam) overlapped on the comm stream.
+    def backward(self, overlap_optimizer=None, top_done=False):
+        """Backward through the stack.  With DP every gradient bucket is SUM-all-reduced on the comm
+        stream as soon as it is complete; with overlap_optimizer (default: with DP) the bucket's
+        optimizer update follows it there, overlapping the rest of the backward.  Without DP,
+        overlap_optimizer=True runs the per-bucket updates the same way (no all-reduce).
 
         top_done: the caller already wrote sum_t dy into the top layer's b_pr gradient and (bf16)
         the bf16 copy of dy into self.dy16[0] (GPT2Model's final-LayerNorm backward does)."""
         cur = 0
         compute = torch.cuda.current_stream()
-        dp = self.dp
+        if overlap_optimizer is None:
+            overlap_optimizer = self.dp
+        dp = self.dp or bool(overlap_optimizer)
+        assert not dp or self.events is not None, "per-bucket updates need StackConfig.overlap_update or DP"
         ah = self.act_host
         for l in range(self.cfg.L - 1, -1, -1):
             if ah is not None and l < self.n_off:
@@ -368,7 +380,8 @@ class BlockStack:
                 assert with_adam, "ZeRO-1 updates inside the bucket step"
                 self._zero_bucket(b0, b1, self.step_count + 1)
                 return
-            torch.distributed.all_reduce(self.g[b0:b1], group=self.pg)
+            if self.dp:
+                torch.distributed.all_reduce(self.g[b0:b1], group=self.pg)
             if with_adam:
                 self._adam_range(b0, b1, self.step_count + 1, stream=self.comm)
 
@@ -421,7 +434,7 @@ class BlockStack:
             r = self.r_buf
         self.forward(x)
         self.probe_loss(r)
-        if self.dp:
+        if self.bucketed:  # per-bucket all-reduce (DP) and update on the comm / update stream
             self.backward(overlap_optimizer=True)
             self.step_count += 1
         else:
@@ -467,7 +480,7 @@ class BlockStack:
                 nnt.nnt_adam_tick(c.beta1, c.beta2, self.t_dev, self.bc_dev)
                 self.forward()
                 self.probe_loss(self.r_buf)
-                if self.dp:
+                if self.bucketed:
                     self.backward(overlap_optimizer=True)
                 else:
                     self.backward()
@@ -561,7 +574,7 @@ class GPT2Model:
         self.loss = torch.zeros(1, **f32)
         self.step_count = 0
         self.ev_shell = torch.cuda.Event()
-        if st.dp:
+        if st.bucketed:
             self.ev_shell.record()
         self.graph = None
 
@@ -599,8 +612,13 @@ class GPT2Model:
         nnt.nnt_dot(self.loss_rows, self.ones, T, inv, self.loss, self.dot_scr, self.dot_scr.numel())
         return self.loss
 
-    def backward(self):
+    def backward(self, overlap_optimizer=None):
+        """Backward through the whole model.  overlap_optimizer (default: with DP): every bucket's
+        update -- the blocks' and, after the embedding backward, the shell's -- runs on the comm /
+        update stream as soon as its gradients are complete (after their all-reduce with DP)."""
         c, st = self.cfg, self.stack
+        if overlap_optimizer is None:
+            overlap_optimizer = st.dp
         T, E, V = c.T, c.E, self.V
         wsrc = self.w16 if self.bf16 else self.w
         tiles = (c.tile_t, c.tile_e, c.tile_e)
@@ -616,16 +634,18 @@ class GPT2Model:
                               self.view(self.g, "lnf_g"), self.view(self.g, "lnf_b"),
                               st.view(st.g, c.L - 1, "b_pr") if top else None, 0,
                               self.lnf_scr, self.lnf_scr.numel())
-        dx0 = st.backward(top_done=top)
+        dx0 = st.backward(overlap_optimizer=overlap_optimizer, top_done=top)
         # dwte accumulates onto the LM head's half (written with beta = 0 above); dwpe has no other
         # producer and is overwritten
         nnt.nnt_embedding_bwd(self.ids, T, c.S, dx0, E, self.view(self.g, "wte"), V, self.view(self.g, "wpe"), 1, 0,
                               self.emb_scr, self.emb_scr.numel())
-        if st.dp:  # the shell bucket: all-reduce + Adam on the comm stream
+        if st.dp or overlap_optimizer:  # the shell bucket: all-reduce (DP) + update on the comm stream
             self.ev_shell.record()
             with torch.cuda.stream(st.comm):
                 st.comm.wait_event(self.ev_shell)
-                if st.zero:
+                if not st.dp:
+                    self._adam(st.step_count + 1, stream=st.comm)
+                elif st.zero:
                     s0, s1, _ = self.shard
                     zero1_bucket(self.g, self.w, 0, self.numel, s0, s1, st.pg,
                                  lambda a, b: self._update(a, b, 0, st.step_count + 1, st.comm, shadow=False))
@@ -662,8 +682,8 @@ class GPT2Model:
             self.step_count = self.stack.step_count
             return self.loss
         self.forward(ids, labels)
-        if self.stack.dp:
-            self.backward()
+        if self.stack.bucketed:
+            self.backward(overlap_optimizer=True)
             self.stack.step_count += 1
             self.step_count = self.stack.step_count
         else:
@@ -690,8 +710,8 @@ class GPT2Model:
             with torch.cuda.graph(g, stream=st.cap_stream):
                 nnt.nnt_adam_tick(c.beta1, c.beta2, st.t_dev, st.bc_dev)
                 self.forward()
-                if st.dp:
-                    self.backward()
+                if st.bucketed:
+                    self.backward(overlap_optimizer=True)
                 else:
                     self.backward()
                     st._adam_range(0, st.numel, 0)
