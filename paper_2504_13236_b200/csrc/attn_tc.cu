@@ -453,15 +453,19 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
 }
 
 // ============================================================================ backward
-// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB), D_qb} | dA^T staging (32 KB:
-// query half h at +16 KB, quadrant rows at +4 KB) | barriers.  TMEM: dP^T[2] at columns 0 / 128,
-// {dV, dK}[2] at 256 / 384 (+64 for dK).
+// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | D slots [2] | dA^T
+// staging[2] (one per ping-pong group, 32 KB: query chunk h at +16 KB, quadrant rows at +4 KB) |
+// barriers.  TMEM: dP^T[2] at columns 0 / 128, {dV, dK}[2] at 256 / 384 (+64 for dK).
+// Iteration g (a query block of a task) uses stage g % 2, dP^T buffer g % 2, and is processed by
+// epilogue group g % 2 with its own dA^T staging buffer.
 constexpr int B_STAGES = 2;
 constexpr int B_D_BYTES = TB * 4;                    // D of the stage's query block (bulk copy)
 constexpr int B_STAGE_TX = 4 * TILE16 + B_D_BYTES;   // bytes landing per stage
-constexpr int B_STAGE_BYTES = 4 * TILE16 + 1024;     // (1024-aligned stages)
-constexpr int B_V = 0, B_ST = 2 * TILE16, B_DA = B_ST + B_STAGES * B_STAGE_BYTES, B_BAR = B_DA + 2 * TILE16;
+constexpr int B_STAGE_BYTES = 4 * TILE16;
+constexpr int B_V = 0, B_ST = 2 * TILE16, B_D = B_ST + B_STAGES * B_STAGE_BYTES, B_DA = B_D + 1024;
+constexpr int B_BAR = B_DA + 2 * 2 * TILE16;
 constexpr int B_SMEM = B_BAR + 256 + 1024;
+static_assert(B_DA % 1024 == 0, "SW128 staging alignment");
 
 __global__ void __launch_bounds__(kAThreads, 1)
     attn_bwd_kv_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mV,
@@ -471,32 +475,32 @@ __global__ void __launch_bounds__(kAThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
-  uint64_t* full = bars;          // [2] stage dO, Q, P landed
-  uint64_t* empty = bars + 2;     // [2] stage consumed: MMA commit + 16 epilogue warps (P reads)
-  uint64_t* vfull = bars + 4;     // [2]
-  uint64_t* vempty = bars + 6;    // [2] the task's last dP MMA done
-  uint64_t* tfull = bars + 8;     // [2] dP^T accumulator ready
-  uint64_t* tempty = bars + 10;   // [2] drained (16 warps)
-  uint64_t* dafull = bars + 12;   // dA^T staging written (16 warps)
-  uint64_t* daempty = bars + 13;  // dA^T staging consumed by MMA dK
-  uint64_t* afull = bars + 14;    // [2] dV, dK of a task complete
-  uint64_t* aempty = bars + 16;   // [2] drained (16 warps)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 18);
+  uint64_t* full = bars;           // [2] stage dO, Q, P, D landed
+  uint64_t* empty = bars + 2;      // [2] stage consumed: MMA commit + the 8 warps of its group (P / D reads)
+  uint64_t* vfull = bars + 4;      // [2]
+  uint64_t* vempty = bars + 6;     // [2] the task's last dP MMA done
+  uint64_t* tfull = bars + 8;      // [2] dP^T accumulator ready
+  uint64_t* tempty = bars + 10;    // [2] drained (8 warps)
+  uint64_t* dafull = bars + 12;    // [2] dA^T staging of group g written (8 warps)
+  uint64_t* daempty = bars + 14;   // [2] dA^T staging of group g consumed by MMA dK
+  uint64_t* afull = bars + 16;     // [2] dV, dK of a task complete
+  uint64_t* aempty = bars + 18;    // [2] drained (8 warps)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
   if (warp == 0 && lane == 0) {
     for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
-      mbar_init(smem_u32(&empty[i]), 1 + kEW);
+      mbar_init(smem_u32(&empty[i]), 1 + kEW / 2);
       mbar_init(smem_u32(&vfull[i]), 1);
       mbar_init(smem_u32(&vempty[i]), 1);
       mbar_init(smem_u32(&tfull[i]), 1);
-      mbar_init(smem_u32(&tempty[i]), kEW);
+      mbar_init(smem_u32(&tempty[i]), kEW / 2);
+      mbar_init(smem_u32(&dafull[i]), kEW / 2);
+      mbar_init(smem_u32(&daempty[i]), 1);
       mbar_init(smem_u32(&afull[i]), 1);
-      mbar_init(smem_u32(&aempty[i]), kEW);
+      mbar_init(smem_u32(&aempty[i]), kEW / 2);
     }
-    mbar_init(smem_u32(dafull), kEW);
-    mbar_init(smem_u32(daempty), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) tmem_alloc512(smem_u32(tmem_slot));
@@ -535,7 +539,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
         const uint32_t st = smem_u32(smem + B_ST + stage * B_STAGE_BYTES);
         const uint32_t fb = smem_u32(&full[stage]);
         mbar_expect_tx_w(fb, B_STAGE_TX);
-        bulk_load_w(st + 4 * TILE16, P.D + ((int64_t)(b * P.H + h) * P.S + qb * TB), B_D_BYTES, fb);
+        bulk_load_w(smem_u32(smem + B_D + stage * B_D_BYTES), P.D + ((int64_t)(b * P.H + h) * P.S + qb * TB),
+                    B_D_BYTES, fb);
         tma_load_4d_w(st, &mdO, fb, 0, qb * TB, h, b);
         tma_load_4d_w(st + TILE16, &mQ, fb, 0, qb * TB, h, b);
         tma_load_4d_w(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b);       // keys kb*128 + 0..63
@@ -551,16 +556,43 @@ __global__ void __launch_bounds__(kAThreads, 1)
     pdl_trigger();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // A flat stream of iterations g over this CTA's tasks (dP^T buffer g & 1, stage g % 2): the dP
-    // MMA of iteration g + 1 (also the next task's first) is issued before the dK MMA of iteration
-    // g, which waits for the epilogue's dA^T.
+    // A flat stream of iterations g over this CTA's tasks: the dP MMA of iteration g + 1 (also the
+    // next task's first) is issued as soon as nothing blocks it -- before the dK MMA of iteration
+    // g if possible, which waits for the epilogue's dA^T, else right after it.
     const uint32_t id_dp = idesc_of(false, false, TB);  // dP^T = V dO^T: both K-major, N = 128
     const uint32_t id_dv = idesc_of(true, true, HD);    // dV += P^T dO: P MN-major, dO MN-major
     const uint32_t id_dk = idesc_of(false, true, HD);   // dK += dA^T Q: dA^T K-major, Q MN-major
-    auto nq_of = [&](int kb) { return P.nblk - q_first(kb); };
-    auto issue_dp = [&](int64_t g, int tl, int i, int nq) {
-      const int tb = (int)(g & 1), stg = (int)(g % B_STAGES), vs = tl & 1;
-      if (i == 0) mbar_wait(smem_u32(&vfull[vs]), (tl >> 1) & 1);
+    struct Cur {
+      int64_t k;
+      int tl, i, nq;
+      bool ok;
+    };
+    auto nq_of = [&](int64_t t) {
+      int kb, b, h;
+      decode(t, kb, b, h);
+      return P.nblk - q_first(kb);
+    };
+    auto next = [&](Cur c) {
+      if (++c.i < c.nq) return c;
+      const int64_t t = task_at(c0, G, c.k + 1);
+      if (t >= P.num_tasks) {
+        c.ok = false;
+        return c;
+      }
+      ++c.k;
+      ++c.tl;
+      c.i = 0;
+      c.nq = nq_of(t);
+      return c;
+    };
+    auto dp_ready = [&](int64_t g, const Cur& c) {
+      return (c.i != 0 || mbar_test(smem_u32(&vfull[c.tl & 1]), (c.tl >> 1) & 1)) &&
+             mbar_test(smem_u32(&tempty[g & 1]), (uint32_t)(((g >> 1) & 1) ^ 1)) &&
+             mbar_test(smem_u32(&full[g % B_STAGES]), (uint32_t)((g / B_STAGES) & 1));
+    };
+    auto issue_dp = [&](int64_t g, const Cur& c) {
+      const int tb = (int)(g & 1), stg = (int)(g % B_STAGES), vs = c.tl & 1;
+      if (c.i == 0) mbar_wait(smem_u32(&vfull[vs]), (c.tl >> 1) & 1);
       mbar_wait(smem_u32(&tempty[tb]), (uint32_t)(((g >> 1) & 1) ^ 1));
       mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / B_STAGES) & 1));
       tc_fence_after();
@@ -572,74 +604,59 @@ __global__ void __launch_bounds__(kAThreads, 1)
                    kk > 0 ? 1u : 0u);
       mma_commit_w(smem_u32(&tfull[tb]));
       if (lane == 0) trace_ev(P, 1, g);
-      if (i == nq - 1) mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
+      if (c.i == c.nq - 1) mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
     };
-    int64_t k = 0;
-    const int64_t t0 = task_at(c0, G, 0);
-    if (t0 < P.num_tasks) {
-      int kb, b, h;
-      decode(t0, kb, b, h);
-      int tl = 0, i = 0, nq = nq_of(kb);
-      int64_t g = 0;
-      issue_dp(0, 0, 0, nq);
-      for (;;) {
-        const int as = tl & 1, stg = (int)(g % B_STAGES);
-        const uint32_t st = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
-        const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
-        if (i == 0) {
-          mbar_wait(smem_u32(&aempty[as]), ((tl >> 1) & 1) ^ 1);
-          tc_fence_after();
-        }
-        // dV += P^T dO (both operands already in the stage): K = 128 queries
-#pragma unroll
-        for (int kk = 0; kk < TB / 16; ++kk)
-          mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
-                     id_dv, (i > 0 || kk > 0) ? 1u : 0u);
-        // the next iteration: (tl, i + 1) or the first of the next task
-        int tl2 = tl, i2 = i + 1, nq2 = nq;
-        bool more = true;
-        if (i2 == nq) {
-          const int64_t t2 = task_at(c0, G, k + 1);
-          more = t2 < P.num_tasks;
-          if (more) {
-            int kb2, b2, h2;
-            decode(t2, kb2, b2, h2);
-            tl2 = tl + 1;
-            i2 = 0;
-            nq2 = nq_of(kb2);
-          }
-        }
-        if (more) issue_dp(g + 1, tl2, i2, nq2);
-        // dK += dA^T Q once the epilogue has staged dA^T of iteration g
-        mbar_wait(smem_u32(dafull), (uint32_t)(g & 1));
-        if (lane == 0) trace_ev(P, 4, g);
-        tc_fence_after();
-        const uint32_t sda = smem_u32(smem + B_DA);
-#pragma unroll
-        for (int kk = 0; kk < TB / 16; ++kk)
-          mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
-                     make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (i > 0 || kk > 0) ? 1u : 0u);
-        mma_commit_w(smem_u32(daempty));
-        if (lane == 0) trace_ev(P, 5, g);
-        mma_commit_w(smem_u32(&empty[stg]));
-        if (i == nq - 1) mma_commit_w(smem_u32(&afull[as]));
-        if (!more) break;
-        if (tl2 != tl) ++k;
-        tl = tl2;
-        i = i2;
-        nq = nq2;
-        ++g;
+    Cur cur{0, 0, 0, 0, false};
+    {
+      const int64_t t0 = task_at(c0, G, 0);
+      if (t0 < P.num_tasks) {
+        cur.nq = nq_of(t0);
+        cur.ok = true;
       }
     }
+    if (cur.ok) issue_dp(0, cur);
+    for (int64_t g = 0; cur.ok; ++g) {
+      const int as = cur.tl & 1, stg = (int)(g % B_STAGES), db = (int)(g & 1);
+      const uint32_t st = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
+      const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
+      if (cur.i == 0) {
+        mbar_wait(smem_u32(&aempty[as]), ((cur.tl >> 1) & 1) ^ 1);
+        tc_fence_after();
+      }
+      // dV += P^T dO (both operands already in the stage): K = 128 queries
+#pragma unroll
+      for (int kk = 0; kk < TB / 16; ++kk)
+        mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
+                   id_dv, (cur.i > 0 || kk > 0) ? 1u : 0u);
+      const Cur nxt = next(cur);
+      bool pending = nxt.ok;
+      if (pending && dp_ready(g + 1, nxt)) {
+        issue_dp(g + 1, nxt);
+        pending = false;
+      }
+      // dK += dA^T Q once group g % 2 has staged dA^T of iteration g
+      mbar_wait(smem_u32(&dafull[db]), (uint32_t)((g >> 1) & 1));
+      if (lane == 0) trace_ev(P, 4, g);
+      tc_fence_after();
+      const uint32_t sda = smem_u32(smem + B_DA + db * 2 * TILE16);
+#pragma unroll
+      for (int kk = 0; kk < TB / 16; ++kk)
+        mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
+                   make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (cur.i > 0 || kk > 0) ? 1u : 0u);
+      mma_commit_w(smem_u32(&daempty[db]));
+      if (lane == 0) trace_ev(P, 5, g);
+      mma_commit_w(smem_u32(&empty[stg]));
+      if (cur.i == cur.nq - 1) mma_commit_w(smem_u32(&afull[as]));
+      if (pending) issue_dp(g + 1, nxt);
+      cur = nxt;
+    }
   } else {
-    // ------------------------------------------------ epilogue warps 2..17
-    // warp: TMEM lane quadrant quad (keys), 32-query group cg of the tile; the pair sharing the
-    // 64-query chunk hc = cg / 2 writes the two halves of its dA^T staging rows, the first of the
-    // pair (sub == 0) issues the TMA store
-    const int quad = warp & 3, cg = (warp - 2) >> 2, hc = cg >> 1, sub = cg & 1, pair = quad * 2 + hc;
-    const bool leader = sub == 0;
-    int stage = 0;
-    uint32_t phase = 0;
+    // ------------------------------------------------ epilogue warps 2..17: two ping-pong groups
+    // Group grp = (warp - 2) / 8 takes the iterations g with g % 2 == grp (stage, dP^T buffer and
+    // dA^T staging buffer grp).  Inside a group: TMEM lane quadrant quad (keys), 64-query chunk hc
+    // (two 32-query halves in turn); each warp writes whole 128-byte staging rows and stores them.
+    // The group that ran a task's last iteration then drains its dK (hc 0) / dV (hc 1).
+    const int grp = (warp - 2) >> 3, quad = warp & 3, hc = ((warp - 2) >> 2) & 1;
     int it = 0, tl = 0;
     // P element (query r of the tile, this lane's key): tile box quad >> 1, 16-byte chunk
     // (quad & 1) * 4 + lane / 8 swizzled by r % 8 (SW128), element lane % 8
@@ -649,72 +666,76 @@ __global__ void __launch_bounds__(kAThreads, 1)
       if (t >= P.num_tasks) break;
       int kb, b, h;
       decode(t, kb, b, h);
-      for (int qb = q_first(kb); qb < P.nblk; ++qb, ++it) {
-        const int tb = it & 1;
-        mbar_wait(smem_u32(&tfull[tb]), (it >> 1) & 1);
+      const int q0 = q_first(kb);
+      for (int qb = q0; qb < P.nblk; ++qb, ++it) {
+        if ((it & 1) != grp) continue;
+        mbar_wait(smem_u32(&tfull[grp]), (it >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
-        float v[32];  // dP^T[key = lane row][query = cg * 32 + j]
-        tmem_ld32(tmem + tb * TB + cg * 32 + ((uint32_t)(quad * 32) << 16), v);
-        tc_fence_before();
+        mbar_wait(smem_u32(&full[grp]), (uint32_t)((it / B_STAGES) & 1));  // P and D of this stage
+        const uint8_t* ptile = smem + B_ST + grp * B_STAGE_BYTES + 2 * TILE16 + pbox;
+        const float* Dq = reinterpret_cast<const float*>(smem + B_D + grp * B_D_BYTES) + hc * 64;
+        // dA^T staging buffer grp: free once MMA dK of iteration it-2 and this warp's stores are done
+        mbar_wait(smem_u32(&daempty[grp]), ((it >> 1) & 1) ^ 1);
+        uint8_t* piece = smem + B_DA + grp * 2 * TILE16 + hc * TILE16 + quad * PIECE;
+        if (lane == 0) bulk_wait_read0();
         __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&tempty[tb]));
-        mbar_wait(smem_u32(&full[stage]), phase);  // the P tile and D of this stage have landed
-        const uint8_t* ptile = smem + B_ST + stage * B_STAGE_BYTES + 2 * TILE16 + pbox;
-        const float* Dq = reinterpret_cast<const float*>(smem + B_ST + stage * B_STAGE_BYTES + 4 * TILE16) + cg * 32;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          const float4 d = *reinterpret_cast<const float4*>(Dq + j);  // (broadcast)
-          const float dd[4] = {d.x, d.y, d.z, d.w};
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int r = cg * 32 + j + u;  // query row of the P tile
-            const uint16_t pr = *reinterpret_cast<const uint16_t*>(ptile + r * 128 + ((pchunk ^ (r & 7)) << 4) + pel);
-            const float p = __uint_as_float((uint32_t)pr << 16);
-            v[j + u] = (p * P.scale) * (v[j + u] - dd[u]);  // dA = P (dP - D) / sqrt(h)  (R20)
+#pragma unroll 1
+        for (int sub = 0; sub < 2; ++sub) {
+          float v[32];  // dP^T[key = lane row][query = hc * 64 + sub * 32 + j]
+          tmem_ld32(tmem + grp * TB + hc * 64 + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+          if (sub == 1) {  // the dP^T buffer is free once both halves are in registers
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(smem_u32(&tempty[grp]));
           }
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const float4 d = *reinterpret_cast<const float4*>(Dq + sub * 32 + j);  // (broadcast)
+            const float dd[4] = {d.x, d.y, d.z, d.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const int r = hc * 64 + sub * 32 + j + u;  // query row of the P tile
+              const uint16_t pr =
+                  *reinterpret_cast<const uint16_t*>(ptile + r * 128 + ((pchunk ^ (r & 7)) << 4) + pel);
+              const float p = __uint_as_float((uint32_t)pr << 16);
+              v[j + u] = (p * P.scale) * (v[j + u] - dd[u]);  // dA = P (dP - D) / sqrt(h)  (R20)
+            }
+          }
+          stage_half_row(piece, lane, sub, v);
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(smem_u32(&empty[stage]));  // this warp's P / D reads are done
-        // dA^T -> staging (after MMA dK of the previous iteration and the pair's store from it)
-        mbar_wait(smem_u32(daempty), (it & 1) ^ 1);
-        uint8_t* piece = smem + B_DA + hc * TILE16 + quad * PIECE;
-        if (leader && lane == 0) bulk_wait_read0();
-        pair_sync(pair);
-        stage_half_row(piece, lane, sub, v);
         fence_async_smem();
-        pair_sync(pair);
+        __syncwarp();
         if (lane == 0) {
-          mbar_arrive(smem_u32(dafull));
+          mbar_arrive(smem_u32(&empty[grp]));  // this warp's P / D reads are done
+          mbar_arrive(smem_u32(&dafull[grp]));
           if (warp == 2) trace_ev(P, 3, it);
-          if (leader) {
-            tma_store_4d(&mdAT, smem_u32(piece), qb * TB + hc * 64, kb * TB + quad * 32, h, b);
+          tma_store_4d(&mdAT, smem_u32(piece), qb * TB + hc * 64, kb * TB + quad * 32, h, b);
+          bulk_commit();
+        }
+        if (qb == P.nblk - 1) {
+          // dK (hc 0) / dV (hc 1) of the key block -> bf16 -> TMA store, from this group's staging
+          // buffer (afull: MMA dK has finished with it; own stores finished reading first)
+          const int as = tl & 1;
+          mbar_wait(smem_u32(&afull[as]), (tl >> 1) & 1);
+          tc_fence_after();
+          if (lane == 0) bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int sub = 0; sub < 2; ++sub) {
+            float v[32];
+            tmem_ld32(tmem + 256 + as * 128 + (hc == 0 ? HD : 0) + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
+            stage_half_row(piece, lane, sub, v);
+          }
+          tc_fence_before();
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(smem_u32(&aempty[as]));
+            tma_store_4d(hc == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
             bulk_commit();
           }
         }
-        if (++stage == B_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-      // dK (chunk 0 pairs) / dV (chunk 1 pairs) of the key block -> bf16 -> TMA store
-      const int as = tl & 1;
-      mbar_wait(smem_u32(&afull[as]), (tl >> 1) & 1);
-      tc_fence_after();
-      float v[32];
-      tmem_ld32(tmem + 256 + as * 128 + (hc == 0 ? HD : 0) + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(&aempty[as]));
-      uint8_t* piece = smem + B_DA + hc * TILE16 + quad * PIECE;  // MMA dK finished with it (afull)
-      if (leader && lane == 0) bulk_wait_read0();
-      pair_sync(pair);
-      stage_half_row(piece, lane, sub, v);
-      fence_async_smem();
-      pair_sync(pair);
-      if (leader && lane == 0) {
-        tma_store_4d(hc == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
-        bulk_commit();
       }
     }
     if (lane == 0) bulk_wait0();
