@@ -519,10 +519,12 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     }
   }
   tc_fence_before();
-  if constexpr (CG == 2)
+  if constexpr (CG == 2) {
     cluster_sync_all();  // both CTAs' barriers initialised before any cross-CTA arrive / complete_tx
-  else
+    __syncthreads();     // (also a CTA barrier for the TMEM-address slot: racecheck does not model the cluster one)
+  } else {
     __syncthreads();
+  }
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
   // PDL: everything above (barrier init, TMEM allocation, tensor-map prefetch) overlapped the
