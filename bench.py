@@ -290,6 +290,8 @@ def run_nnt(args):
         pg = dist.group.WORLD
     nnt.nnt_device_check(local)
     L, E, H, S, B = CONFIGS[args.config]
+    if args.layers:  # capacity runs (f4): the config's layer shape, a different depth
+        L = args.layers
     mdl = args.model or default_model(args.config)
     dtype = "f32" if args.config == "tiny" else "bf16"
     tile = 16 if args.config == "tiny" else 1024
@@ -484,7 +486,8 @@ def run_nnt(args):
                                    if mdl == "gpt2" else
                                    f"gpt2-{args.config}: {L} pre-LN GPT-2 blocks fwd+bwd+Adam (block stack, "
                                    f"linear-probe loss)"),
-                      "model": f"gpt2-{args.config}" + ("" if mdl == "gpt2" else "-blocks"), "layers": L,
+                      "model": f"gpt2-{args.config}" + (f"-L{L}" if args.layers else "") +
+                               ("" if mdl == "gpt2" else "-blocks"), "layers": L,
                       "d_model": E, "heads": H, "vocab": VOCAB if mdl == "gpt2" else None,
                       "global_batch": B * world, "seq_len": S, "tile": tile, "parallelism": f"dp{world}" + ("-zero1" if args.zero and world > 1 else ""),
                       "optimizer": args.optimizer + (" (state offloaded to pinned host memory)" if args.offload
@@ -539,6 +542,8 @@ def main():
                     "through device staging slots around each update (SURVEY f4)")
     ap.add_argument("--act-offload", type=int, default=0, help="saved activations of the lowest K layers in "
                     "pinned host memory, copied out after their forward and back before their backward (SURVEY f4)")
+    ap.add_argument("--layers", type=int, default=0, help="override the config's layer count (capacity runs with "
+                    "--act-offload / --offload; not a BASELINE configuration)")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel eagerly (no CUDA graph)")
     args = ap.parse_args()
     if args.warmup < 3:

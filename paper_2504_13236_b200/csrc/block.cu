@@ -15,8 +15,8 @@ struct Layout {
   // saved (per layer)
   size_t mean1, rstd1, h1, qkv, P, stats, O, x1, mean2, rstd2, h2, u, g, saved_bytes;
   // scratch
-  size_t scores, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, colsum2, lnscr, gemm_ws, scratch_bytes;
-  size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes;
+  size_t scores, dvec, dy16, du, dh, dx1, dx116, dO, dA, dqkv, colsum, colsum2, lnscr, gemm_ws, sk_ws, scratch_bytes;
+  size_t colsum_bytes, lnscr_bytes, gemm_ws_bytes, sk_ws_bytes;
 };
 
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -79,6 +79,12 @@ Layout make_layout(const nnt_block_cfg& c, int64_t H_l, int64_t F_l) {
     }
   }
   L.gemm_ws = take(L.gemm_ws_bytes);
+  // the main stream's projection GEMMs (forward and dX): stream-K partial slots and flags (the dW
+  // GEMMs, which may run concurrently on the side stream, keep gemm_ws)
+  L.sk_ws_bytes = c.dtype == NNT_BF16 ? nnt_tile_gemm_workspace_bytes((int64_t)T, (int64_t)E, (int64_t)E, NNT_BF16,
+                                                                      NNT_ACT_NONE, NNT_CAUSAL_NONE, 1)
+                                      : 0;
+  L.sk_ws = take(L.sk_ws_bytes);
   L.scratch_bytes = o;
   return L;
 }
@@ -124,6 +130,13 @@ struct Ctx {
 nnt_status gemm(const Ctx& x, int ta, int tb, int64_t M, int64_t N, int64_t K, const int64_t* batch, float alpha,
                 const void* A, int64_t lda, const int64_t* sa, const void* B, int64_t ldb, const int64_t* sb,
                 float beta, void* C, int cdt, int64_t ldc, const int64_t* sc, const nnt_epilogue* epi) {
+  nnt_epilogue e{};
+  if (!batch && x.L.sk_ws_bytes && !(epi && epi->workspace)) {  // unbatched main-stream GEMM: stream-K slots
+    if (epi) e = *epi;
+    e.workspace = x.k<void>(x.L.sk_ws);
+    e.workspace_bytes = x.L.sk_ws_bytes;
+    epi = &e;
+  }
   return nnt_tile_gemm(ta, tb, M, N, K, batch, alpha, A, x.dt, lda, sa, B, x.dt, ldb, sb, beta, C, cdt, ldc, sc,
                        x.tile_lin, epi, x.st);
 }

@@ -17,8 +17,13 @@ extern "C" size_t nnt_tile_gemm_workspace_bytes(int64_t M, int64_t N, int64_t K,
   g.causal = causal;
   g.batch0 = batch_items > 0 ? batch_items : 1;
   g.batch1 = 1;
-  // split partials of C, of the a_rowsum row sums (R27), then the in-kernel reduce's counters
-  return splitk_workspace_bytes(g, gemm_tc_splits(g));
+  // split partials of C, of the a_rowsum row sums (R27), then the in-kernel reduce's counters;
+  // or, for a GEMM the stream-K schedule can take, its partial slots and flags (the larger)
+  const size_t split = splitk_workspace_bytes(g, gemm_tc_splits(g));
+  const bool sk = sk_on() && g.batch0 == 1 && causal == NNT_CAUSAL_NONE &&
+                  (act == NNT_ACT_NONE || act == NNT_ACT_GELU || act == NNT_ACT_GELU_BWD);
+  const size_t skb = sk ? sk_workspace_bytes() : 0;
+  return split > skb ? split : skb;
 }
 
 extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const int64_t* batch,

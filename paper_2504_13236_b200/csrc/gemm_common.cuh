@@ -43,6 +43,10 @@ int64_t gemm_tc_splits(const GemmArgs& a);  // split-K factor the tcgen05 path w
 // split-K workspace bytes for `splits` (partials + a_rowsum partials + the in-kernel reduce's
 // arrival counters; 0 when splits == 1)
 size_t splitk_workspace_bytes(const GemmArgs& a, int64_t splits);
+// stream-K workspace bytes (partial slots + flag zone; shape independent) and whether the
+// stream-K schedule is enabled (NNT_GEMM_SK != 0)
+size_t sk_workspace_bytes();
+bool sk_on();
 // 4-D TMA tensor map (dims {inner, outer, batch1, batch0}, SWIZZLE_128B, box {box_inner, box_outer,
 // 1, 1}; es = element bytes, ld / s1 / s0 in elements)
 nnt_status make_tma_map_4d(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t inner,

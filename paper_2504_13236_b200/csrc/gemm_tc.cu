@@ -136,7 +136,19 @@ struct TcParams {
   // in split order and stores C (no reduce kernel)
   int fused_reduce;
   uint32_t* counters;
+  // Stream-K (sk = 1; generic epilogue, unbatched, non-causal, splits == 1): tiles [0, sk_dp_tiles)
+  // run whole (tile k*G + unit), the remaining tiles' K-block iterations (sk_iters in all) are
+  // cut into G equal contiguous ranges, one per unit, so the last wave is not quantised.  A tile
+  // covered by several units is finished by the unit holding its last K-block: it adds the other
+  // units' fp32 partials (sk_part slots, one per unit and CTA) in a fixed order, behind per-warp
+  // flags in the counter zone.
+  int sk;
+  int64_t sk_dp_tiles, sk_iters, nkb;
+  float* sk_part;
 };
+
+// Stream-K roles of a unit's work item
+enum SkRole { SK_FULL = 0, SK_WRITER = 1, SK_FINISHER = 2 };
 
 // PTX helpers (mbarrier, TMA, tcgen05 MMA / TMEM, smem descriptors): tc_ptx.cuh
 
@@ -223,6 +235,92 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
   ti.kb_begin = min(kb1, kb0 + ti.split * P.kb_per_split);
   ti.kb_end = min(kb1, ti.kb_begin + P.kb_per_split);
   return ti;
+}
+
+// A unit's (CTA or CTA pair's) work list, walked identically by the producer, MMA and epilogue
+// roles: the static task schedule (TaskIter), or with P.sk the stream-K list
+//   [writer segment] [whole data-parallel tiles] [whole stream-K tiles] [finisher segment]
+// Unit c owns iterations [s0, s1) = [c I / G, (c+1) I / G) of the stream-K tiles' (tile-major,
+// K-block-minor) iteration space.  Its segment in the tile holding s1 - 1 ends before that tile's
+// last K-block when s1 is not a tile boundary: a WRITER segment, processed first (its partial is
+// stored early).  Its segment in the tile holding s0 starts after that tile's first K-block when s0
+// is not a boundary: a FINISHER segment (it holds the tile's last K-block), processed last; the
+// units it waits for are lower-numbered and wrote their partial as their first item, so the waits
+// always point at work that never waits (no deadlock; launched in index order).
+struct Walk {
+  TaskIter it;
+  int64_t j, n, s0, s1, n_dp, tf0, tf1;
+  int has_w, has_f;
+  __device__ __forceinline__ Walk(const TcParams& P, int64_t c, int64_t G) : it(c, G), j(0), n(0) {
+    if (!P.sk) return;
+    const int64_t I = P.sk_iters, nkb = P.nkb;
+    s0 = c * I / G;
+    s1 = (c + 1) * I / G;
+    n_dp = P.sk_dp_tiles > c ? (P.sk_dp_tiles - c + G - 1) / G : 0;
+    has_w = has_f = 0;
+    tf0 = tf1 = 0;
+    if (s1 > s0) {
+      has_w = (s1 % nkb) != 0;
+      has_f = (s0 % nkb) != 0 && !(s0 / nkb == (s1 - 1) / nkb && has_w);
+      tf0 = (s0 + nkb - 1) / nkb;
+      tf1 = s1 / nkb;
+      if (tf1 < tf0) tf1 = tf0;
+    }
+    n = has_w + n_dp + (tf1 - tf0) + has_f;
+  }
+  __device__ __forceinline__ bool ok(const TcParams& P) const { return P.sk ? j < n : it.t < P.num_tasks; }
+  __device__ __forceinline__ void next(const TcParams& P, int bn) {
+    if (P.sk)
+      ++j;
+    else
+      it.next(P, bn);
+  }
+  __device__ __forceinline__ TileInfo info(const TcParams& P, int bn, int bm_tile, int row_off, int& role) const {
+    if (!P.sk) {
+      role = SK_FULL;
+      return decode_task(P, it.t, bn, bm_tile, row_off, it.sub);
+    }
+    const int64_t nkb = P.nkb, dp = P.sk_dp_tiles;
+    int64_t jj = j, tile, kb0 = 0, kb1 = nkb;
+    role = SK_FULL;
+    if (jj < has_w) {
+      const int64_t t1 = (s1 - 1) / nkb;
+      tile = dp + t1;
+      kb0 = (s0 > t1 * nkb ? s0 : t1 * nkb) - t1 * nkb;
+      kb1 = s1 - t1 * nkb;
+      role = SK_WRITER;
+    } else if ((jj -= has_w) < n_dp) {
+      tile = jj * it.G + it.c;
+    } else if ((jj -= n_dp) < tf1 - tf0) {
+      tile = dp + tf0 + jj;
+    } else {
+      const int64_t t0 = s0 / nkb;
+      tile = dp + t0;
+      kb0 = s0 - t0 * nkb;
+      role = SK_FINISHER;
+    }
+    TileInfo ti = decode_task(P, tile, bn, bm_tile, row_off, 0);
+    ti.kb_begin = kb0;
+    ti.kb_end = kb1;
+    return ti;
+  }
+};
+
+// Stream-K partial slot of (unit, CTA rank): [BN/4][BM][4] fp32 -- a warp's float4 accesses for
+// one column quad cover 32 consecutive rows (512 contiguous bytes)
+__device__ __forceinline__ float* sk_slot(const TcParams& P, int64_t unit, uint32_t rank, int cg, int bn) {
+  return P.sk_part + ((size_t)unit * cg + rank) * (size_t)BM * bn;
+}
+__device__ __forceinline__ uint32_t* sk_flag(const TcParams& P, int64_t unit, uint32_t rank, int cg, int epi_warp) {
+  return P.counters + ((size_t)unit * cg + rank) * kEpiWarps + epi_warp;
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // ------------------------------------------------------------------ epilogue math
@@ -536,8 +634,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     {
       int stage = 0;
       uint32_t phase = 0;
-      for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
+      for (Walk wk(P, task0, task_step); wk.ok(P); wk.next(P, BN)) {
+        int role;
+        TileInfo ti = wk.info(P, BN, BM * CG, row_off, role);
         const int p = ti.p, q = ti.q;
         const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
@@ -602,8 +701,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       // apart; +2 KB per UMMA_K=16.
       const uint32_t a_lbo = P.a_kmajor ? 16u : 8192u, b_lbo = P.b_kmajor ? 16u : 8192u;
       const uint32_t a_step = P.a_kmajor ? 32u : 2048u, b_step = P.b_kmajor ? 32u : 2048u;
-      for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-        TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off, it.sub);
+      for (Walk wk(P, task0, task_step); wk.ok(P); wk.next(P, BN)) {
+        int role;
+        TileInfo ti = wk.info(P, BN, BM * CG, row_off, role);
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
@@ -923,8 +1023,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
     int acc = 0;
     uint32_t acc_phase = 0;
     uint32_t in_phase = 0;  // IN_AUX_SMEM: bit i = phase of this warp's input barrier i
-    for (TaskIter it(task0, task_step); it.t < P.num_tasks; it.next(P, BN)) {
-      TileInfo ti = decode_task(P, it.t, BN, BM * CG, row_off);
+    for (Walk wk(P, task0, task_step); wk.ok(P); wk.next(P, BN)) {
+      int role;
+      TileInfo ti = wk.info(P, BN, BM * CG, row_off, role);
       const int64_t p = ti.p, q = ti.q;
       TC* Cb = (TC*)g.C + p * g.sc0 + q * g.sc1;
       TC* auxb = g.aux ? (TC*)g.aux + p * g.sc0 + q * g.sc1 : nullptr;
@@ -938,11 +1039,12 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       };
       // (fp32 C only: a bf16 chunk already holds 64 live values, a prefetch buffer would spill)
       auto can_stream = [&](int c) {
-        return sizeof(TC) == 4 && P.in_kind != IN_NONE && vec && row < g.M && c < BN && ti.n0 + c + W <= g.N;
+        return sizeof(TC) == 4 && P.in_kind != IN_NONE && vec && row < g.M && c < BN && ti.n0 + c + W <= g.N &&
+               role != SK_WRITER;
       };
       Raw8 raw;
       if (can_stream(half * W)) raw_load(raw, in_ptr(half * W));  // overlaps the wait for the MMAs
-      if (P.in_kind == IN_AUX_SMEM) {
+      if (P.in_kind == IN_AUX_SMEM && role != SK_WRITER) {
         // TMA-load this warp's aux chunks of the tile into its staging buffers (chunk i ->
         // buffer i) before the accumulator wait, so the loads overlap the MMAs
         if (lane == 0) {
@@ -963,6 +1065,24 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       const bool has_k = ti.kb_end > ti.kb_begin;
       const float dval =
           (g.act == NNT_ACT_SOFTMAX_BWD && row < g.M) ? __ldg(g.rowvec + ti.bz * g.M + row) : 0.f;
+      // stream-K: this warp's partial slot region (writer), or the first / last unit whose partial
+      // of this tile the finisher adds (units w_lo..w_hi, all below this one)
+      const int rrow = quad * 32 + lane;  // row within this CTA's 128
+      int64_t w_lo = 0, w_hi = -1;
+      if (role == SK_FINISHER) {
+        const int64_t t_start = (ti.tile - P.sk_dp_tiles) * P.nkb;  // the tile's first iteration
+        w_hi = wk.it.c - 1;
+        w_lo = w_hi;
+        while (w_lo > 0 && (w_lo * P.sk_iters) / wk.it.G > t_start) --w_lo;  // unit w_lo starts at or before
+        if (lane == 0) {
+          for (int64_t w = w_lo; w <= w_hi; ++w) {
+            uint32_t* f = sk_flag(P, w, rank, CG, warp - 2);
+            while (ld_acquire_u32(f) == 0u) __nanosleep(64);
+            *f = 0u;  // consumed: every launch leaves the flags zero (the workspace contract)
+          }
+        }
+        __syncwarp();
+      }
       int ci = 0;  // chunk index within the tile (IN_AUX_SMEM: its staging buffer)
 #pragma unroll 1
       for (int c = half * W; c < BN; c += 2 * W, ++ci) {
@@ -978,6 +1098,28 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           }
         }
         const int cx = (int)(ti.n0 + c), cy = (int)(ti.m0 + quad * 32);
+        if (role == SK_WRITER) {  // raw fp32 partial -> this unit's slot (alpha and extras at the finisher)
+          float4* sl = reinterpret_cast<float4*>(sk_slot(P, wk.it.c, rank, CG, BN)) + (size_t)(c / 4) * BM + rrow;
+#pragma unroll
+          for (int j = 0; j < W / 4; ++j)
+            __stcg(sl + (size_t)j * BM, make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]));
+          continue;
+        }
+        if (role == SK_FINISHER) {  // own partial + the lower units' partials, in descending unit order
+#pragma unroll 1
+          for (int64_t w = w_hi; w >= w_lo; --w) {
+            const float4* sl =
+                reinterpret_cast<const float4*>(sk_slot(P, w, rank, CG, BN)) + (size_t)(c / 4) * BM + rrow;
+#pragma unroll
+            for (int j = 0; j < W / 4; ++j) {
+              const float4 t = __ldcg(sl + (size_t)j * BM);
+              v[4 * j] += t.x;
+              v[4 * j + 1] += t.y;
+              v[4 * j + 2] += t.z;
+              v[4 * j + 3] += t.w;
+            }
+          }
+        }
         if (EPI == EPI_SPLITK || P.ws_mode) {
           // split-K partial (fp32) -> workspace slice ti.split; C is formed by the reduce
           epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, false, vec, 0.f, IN_NONE, raw, v);
@@ -1048,12 +1190,14 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         }
       }
       tc_fence_before();
+      if (role == SK_WRITER) __threadfence();  // this lane's partial stores before the flag
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 2)
           mbar_arrive_cluster(map_to_rank(smem_u32(&tempty[acc]), 0));  // the leader's MMA waits on it
         else
           mbar_arrive(smem_u32(&tempty[acc]));
+        if (role == SK_WRITER) st_release_u32(sk_flag(P, wk.it.c, rank, CG, warp - 2), 1u);
       }
       if (++acc == 2) {
         acc = 0;
@@ -1367,10 +1511,48 @@ bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
          regions <= kSplitCounters && c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
 }
 
+// Stream-K (P.sk): off by default, NNT_GEMM_SK=1 enables it; NNT_GEMM_SK_EFF sets the wave
+// efficiency (tiles / (waves x units)) below which a GEMM is scheduled stream-K (default 0.82).
+// Measured on the GPT-2 XL step (4 interleaved runs): the GEMM class 77.0 -> 75.5 ms
+// but the step 106.1 -> 106.9 ms (lower SM clock under the power cap, side-stream overlap).
+bool sk_on() {  // read per call (tests switch it within one process)
+  const char* e = getenv("NNT_GEMM_SK");
+  return e && e[0] == '1';
+}
+double sk_eff() {
+  const char* e = getenv("NNT_GEMM_SK_EFF");
+  return e ? atof(e) : 0.82;
+}
+// Partial slots: one BM x 256 fp32 region per CTA of the widest grid, then the flag zone (the
+// split-K counter zone at the workspace end: one flag per CTA and epilogue warp).
+size_t sk_workspace_bytes() {
+  return (size_t)num_sms() * BM * 256 * sizeof(float) + 16 + (size_t)kSplitCounters * sizeof(uint32_t);
+}
+// A GEMM the stream-K schedule can take: generic epilogue, unbatched, non-causal, no a_rowsum,
+// and a workspace holding the slots and flags.
+bool sk_possible(const GemmArgs& a) {
+  const bool generic = a.act == NNT_ACT_NONE || a.act == NNT_ACT_GELU || a.act == NNT_ACT_GELU_BWD;
+  return sk_on() && generic && !a.row_stats && !a.a_rowsum && a.batch0 * a.batch1 == 1 &&
+         a.causal == NNT_CAUSAL_NONE && a.workspace && (reinterpret_cast<uintptr_t>(a.workspace) & 15u) == 0 &&
+         a.workspace_bytes >= sk_workspace_bytes() && num_sms() * kEpiWarps <= kSplitCounters;
+}
+// Worth it (measured on the GPT-2 XL shapes, tools/gemm_bench.py): the last
+// data-parallel wave is at most ~80 % full, K is long (>= 64 K-blocks: the fp32 partial written and
+// read back is small against a tile's main loop) and at least two whole waves stay data-parallel.
+// With fewer whole waves, or short K, the units' desynchronised K offsets cost more L2 operand
+// traffic than the balanced last wave saves (XL QKV-dW 131 -> 143 us, QKV 93 -> 100 us, small
+// FC+GELU 52 -> 65 us).  Every unit then also gets >= 1 tile of K-blocks (no empty unit range,
+// whose finisher would wait for a flag nobody sets).
+bool sk_pays(int64_t tiles, int64_t nkb, int64_t units) {
+  const int64_t waves = (tiles + units - 1) / units;
+  const double eff = (double)tiles / (double)(waves * units);
+  return eff < sk_eff() && nkb >= 64 && tiles / units >= 2;
+}
+
 namespace {
 
 template <int BN, typename TC, int EPI, int CG = 1>
-nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
+nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_allowed = false) {
   using C = Cfg<BN, CG, EPI>;
   const cudaError_t attr_err = set_max_dyn_smem(gemm_tc_kernel<BN, TC, EPI, CG>, (int)C::SMEM_BYTES);
   NNT_REQUIRE(attr_err == cudaSuccess, NNT_ERR_CUDA, "cudaFuncSetAttribute: %s", cudaGetErrorString(attr_err));
@@ -1411,6 +1593,25 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   P.ws_mode = splits > 1 ? 1 : 0;
   P.fused_reduce = EPI == EPI_SPLITK ? 1 : 0;
   P.counters = P.fused_reduce ? splitk_counters(a) : nullptr;
+  // stream-K when the data-parallel waves would leave a partly empty last wave
+  const int64_t G_units = CG == 1 ? num_sms() * C::CTAS : pair_units();
+  P.sk = 0;
+  P.sk_dp_tiles = P.sk_iters = 0;
+  P.nkb = nkb;
+  P.sk_part = nullptr;
+  if (sk_allowed && EPI == EPI_GENERIC && splits == 1 && P.order == ORDER_N_OUTER && !a.a_rowsum &&
+      sk_pays(P.num_tiles, nkb, G_units)) {
+    const int64_t full_waves = P.num_tiles / G_units;
+    P.sk = 1;
+    P.sk_dp_tiles = full_waves >= 1 ? (full_waves - 1) * G_units : 0;
+    P.sk_iters = (P.num_tiles - P.sk_dp_tiles) * nkb;
+    P.sk_part = reinterpret_cast<float*>(a.workspace);
+    P.counters = splitk_counters(a);
+    if (getenv("NNT_DEBUG_GEMM"))
+      fprintf(stderr, "gemm_tc stream-K %lldx%lldx%lld: BN %d CG %d tiles %lld units %lld dp %lld iters %lld\n",
+              (long long)a.M, (long long)a.N, (long long)a.K, BN, CG, (long long)P.num_tiles, (long long)G_units,
+              (long long)P.sk_dp_tiles, (long long)P.sk_iters);
+  }
   // the one epilogue input streamed (prefetched) per chunk; element size must equal C's
   if (P.ws_mode || !generic_epi(EPI))
     P.in_kind = IN_NONE;
@@ -1469,7 +1670,7 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   }
   if constexpr (CG == 1) {
     const int64_t units = num_sms() * C::CTAS;  // persistent: C::CTAS CTAs per SM
-    int64_t grid = P.num_tasks < units ? P.num_tasks : units;
+    int64_t grid = P.sk ? units : (P.num_tasks < units ? P.num_tasks : units);
     if (grid < 1) grid = 1;
     ::nnt::launch(gemm_tc_kernel<BN, TC, EPI, 1>, (unsigned)grid, kThreads, C::SMEM_BYTES, s, P, tmA, tmB, tmC, tmAux);
   } else {
@@ -1487,12 +1688,16 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits) {
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 2 : 1;
     const int64_t max_clusters = pair_units();
-    int64_t grid = P.num_tasks < max_clusters ? P.num_tasks : max_clusters;
+    int64_t grid = P.sk ? max_clusters : (P.num_tasks < max_clusters ? P.num_tasks : max_clusters);
     if (grid < 1) grid = 1;
     cfg.gridDim = dim3((unsigned)(grid * CG));
     NNT_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, TC, EPI, CG>, P, tmA, tmB, tmC, tmAux));
   }
   NNT_TRY(check_launch("gemm_tc"));
+  if (getenv("NNT_DEBUG_GEMM"))
+    fprintf(stderr, "gemm_tc launch %lldx%lldx%lld batch %lld: BN %d CG %d EPI %d splits %lld sk %d tiles %lld\n",
+            (long long)a.M, (long long)a.N, (long long)a.K, (long long)(a.batch0 * a.batch1), BN, CG, EPI,
+            (long long)splits, P.sk, (long long)P.num_tiles);
   if (P.ws_mode && !P.fused_reduce) {
     const int64_t total = a.M * (a.N / 4);
     int64_t blocks = cdiv(total, 256);
@@ -1522,7 +1727,7 @@ double l2_bytes_per_cycle() {
   return v;
 }
 
-double tile_cost(const GemmArgs& a, int bn, int cg, int64_t units, size_t es_c) {
+double tile_cost(const GemmArgs& a, int bn, int cg, int64_t units, size_t es_c, bool sk = false) {
   const int64_t nb = a.batch0 * a.batch1;
   const int64_t tiles = cdiv(a.M, (int64_t)BM * cg) * cdiv(a.N, bn) * nb;
   const double kp = (double)(cdiv(a.K, BK) * BK);
@@ -1537,12 +1742,17 @@ double tile_cost(const GemmArgs& a, int bn, int cg, int64_t units, size_t es_c) 
   // SW128 staging -> TMA store); it overlaps the next tile's MMAs, the last tile's is exposed
   const double t_epi = (double)BM * bn * epi / 12.0;
   const int64_t full = tiles / units, rem = tiles % units;
+  if (sk && rem && sk_pays(tiles, (int64_t)(kp / BK), units)) {
+    // stream-K: fractional waves, plus a partial tile written and read back (fp32) per unit
+    const double wave = fmax(fmax(mma, (double)units * cg * bytes_sm / l2), t_epi);
+    return (double)tiles / (double)units * wave + t_epi + 2.0 * BM * bn * 4.0 / 12.0;
+  }
   double cost = (double)full * fmax(fmax(mma, (double)units * cg * bytes_sm / l2), t_epi);
   if (rem) cost += fmax(fmax(mma, (double)rem * cg * bytes_sm / l2), t_epi);
   return cost + t_epi;
 }
 
-int choose_bn(const GemmArgs& a, size_t es_c, double* cost_out = nullptr) {
+int choose_bn(const GemmArgs& a, size_t es_c, double* cost_out = nullptr, bool sk = false) {
   if (cost_out) *cost_out = 1e300;
   if (a.N <= 64) return 64;
   if (a.causal == NNT_CAUSAL_OUT_LOWER) return 128;
@@ -1550,7 +1760,7 @@ int choose_bn(const GemmArgs& a, size_t es_c, double* cost_out = nullptr) {
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
-    const double cost = tile_cost(a, bn, 1, num_sms(), es_c);
+    const double cost = tile_cost(a, bn, 1, num_sms(), es_c, sk);
     if (cost < best_cost * 0.97) {  // near-ties (within the model's error) go to the wider tile
       best_cost = cost;
       best = bn;
@@ -1580,15 +1790,19 @@ bool use_pair(const GemmArgs& a) {
 }
 
 // Pair widths whose half is a whole 64-column MN-major block.
-int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out) {
+int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out, bool sk = false) {
   // (192-wide pair tiles -- N = 1600 as 9 x 192 instead of 7 x 256 with a nearly empty last round
   // -- ran 2-4 % slower on every GPT-2 XL shape: these GEMMs are bound by the L2 -> SM operand
   // stream, which narrower tiles increase per FLOP; DESIGN §7.1.  NNT_GEMM_192=1 re-enables them.)
   const int cands[3] = {256, 128, getenv("NNT_GEMM_192") ? 192 : 128};
+  if (const char* f = getenv("NNT_GEMM_BN")) {  // A/B override of the tile model
+    *cost_out = 0;
+    return atoi(f);
+  }
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {
-    const double cost = tile_cost(a, bn, 2, pair_units(), es_c);
+    const double cost = tile_cost(a, bn, 2, pair_units(), es_c, sk);
     if (cost < best_cost * 0.999) {
       best_cost = cost;
       best = bn;
@@ -1622,7 +1836,7 @@ int64_t long_k_splits(const GemmArgs& a) {
 }
 
 template <typename TC>
-nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
+nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk = false) {
   const bool tma_ok = splits == 1 && c_tma_ok(a, sizeof(TC));
   if constexpr (sizeof(TC) == 2) {
     if (tma_ok && a.act == NNT_ACT_SOFTMAX_BWD && aligned16(a.aux) && (a.ld_aux * 2) % 16 == 0)
@@ -1643,8 +1857,8 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
   }
   if (use_pair(a)) {
     double cost_pair = 0, cost_single = 0;
-    const int bnp = choose_bn_pair(a, sizeof(TC), &cost_pair);
-    const int bns = choose_bn(a, sizeof(TC), &cost_single);
+    const int bnp = choose_bn_pair(a, sizeof(TC), &cost_pair, sk);
+    const int bns = choose_bn(a, sizeof(TC), &cost_single, sk);
     if (getenv("NNT_DEBUG_GEMM"))
       fprintf(stderr, "gemm_tc %lldx%lldx%lld: pair BN %d cost %.0f, single BN %d cost %.0f\n", (long long)a.M,
               (long long)a.N, (long long)a.K, bnp, cost_pair, bns, cost_single);
@@ -1652,19 +1866,19 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits) {
       if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 2>(a, s, splits);
     }
     if (splits > 1 || forced_cg() == 2 || cost_pair <= cost_single) {  // ties go to pairs
-      if (bnp == 256 || splits > 1) return launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits);
-      if (bnp == 192) return launch_bn<192, TC, EPI_GENERIC, 2>(a, s, splits);
-      return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits);
+      if (bnp == 256 || splits > 1) return launch_bn<256, TC, EPI_GENERIC, 2>(a, s, splits, sk);
+      if (bnp == 192) return launch_bn<192, TC, EPI_GENERIC, 2>(a, s, splits, sk);
+      return launch_bn<128, TC, EPI_GENERIC, 2>(a, s, splits, sk);
     }
   }
   if constexpr (sizeof(TC) == 4) {
     if (splits > 1 && fused_reduce_ok(a, splits)) return launch_bn<256, TC, EPI_SPLITK, 1>(a, s, splits);
   }
-  switch (splits > 1 ? 256 : choose_bn(a, sizeof(TC))) {
-    case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits);
-    case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits);
-    case 192: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits);
-    default: return launch_bn<256, TC, EPI_GENERIC>(a, s, splits);
+  switch (splits > 1 ? 256 : choose_bn(a, sizeof(TC), nullptr, sk)) {
+    case 64: return launch_bn<64, TC, EPI_GENERIC>(a, s, splits, sk);
+    case 128: return launch_bn<128, TC, EPI_GENERIC>(a, s, splits, sk);
+    case 192: return launch_bn<192, TC, EPI_GENERIC>(a, s, splits, sk);
+    default: return launch_bn<256, TC, EPI_GENERIC>(a, s, splits, sk);
   }
 }
 
@@ -1694,10 +1908,14 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
                      (!a.residual || ((reinterpret_cast<uintptr_t>(a.residual) & 15u) == 0 && a.ld_res % 4 == 0)) &&
                      (!a.bias || (reinterpret_cast<uintptr_t>(a.bias) & 15u) == 0);
   if (!ws_ok) splits = 1;
+  // stream-K (a workspace big enough for its slots) replaces split-K: no partial round trip
+  // through HBM for the whole tile grid and no reduce launch
+  const bool sk = sk_possible(a);
+  if (sk) splits = 1;
   if (kernels) *kernels = splits > 1 && !fused_reduce_ok(a, splits) ? 2 : 1;
   if (a.act == NNT_ACT_ROWSTATS) return launch_bn<128, float, EPI_ROWSTATS>(a, s, 1);
-  if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits);
-  return launch_tc<__nv_bfloat16>(a, s, splits);
+  if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits, sk);
+  return launch_tc<__nv_bfloat16>(a, s, splits, sk);
 }
 
 }  // namespace nnt

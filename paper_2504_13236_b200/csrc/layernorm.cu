@@ -2,11 +2,15 @@
 //   E <= 1024: one WARP per token row (row in registers as float4, reductions by
 //              warp shuffle only); forward warps stride over rows with the next row
 //              prefetched, backward CTAs own a block of rows (single pass);
-//   E  > 1024: forward one 128-thread CTA per row (shuffle + 4-entry shared array);
+//   E  > 1024: forward one 128-thread CTA per row (shuffle + 4-entry shared array; a variant with
+//              4-warp groups striding over rows, the next row prefetched, measured slower at
+//              E = 1600: 16.1 vs 11.4 us);
 //              backward a group of 4 or 8 warps per row, persistent CTAs (ln_bwd_groups).
 // The backward's dgamma/dbeta are per-CTA column partials (rows of a CTA are
 // accumulated in a fixed order) merged by the deterministic column merge
 // (reduce.cuh): bitwise reproducible, no atomics.
+#include <cstdlib>
+
 #include "reduce.cuh"
 
 namespace nnt {
@@ -319,14 +323,21 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1)
     }
   };
   int64_t row = r0 + grp;
-  if (row < r1) load(row, xv, dv, rv);
+  float mu = 0.f, rs = 0.f;  // this row's statistics, loaded with its data (a late load stalls every use)
+  if (row < r1) {
+    load(row, xv, dv, rv);
+    mu = __ldg(mean + row);
+    rs = __ldg(rstd + row);
+  }
   int buf = 0;
   for (; row < r1; row += NG, buf ^= 1) {
-    const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
     float4 xn[PREF ? NV : 1], dn[PREF ? NV : 1], rn[PREF ? NV : 1];
+    float mun = 0.f, rsn = 0.f;
     const int64_t nrow = row + NG;
-    if constexpr (PREF) {
-      if (nrow < r1) load(nrow, xn, dn, rn);  // next row in flight during this one's reductions
+    if (nrow < r1) {
+      mun = __ldg(mean + nrow);
+      rsn = __ldg(rstd + nrow);
+      if constexpr (PREF) load(nrow, xn, dn, rn);  // next row in flight during this one's reductions
     }
     float sa = 0.f, sb = 0.f;
 #pragma unroll
@@ -387,6 +398,8 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1)
     } else if (nrow < r1) {
       load(nrow, xv, dv, rv);
     }
+    mu = mun;
+    rs = rsn;
   }
 #pragma unroll
   for (int j = 0; j < NV; ++j) {

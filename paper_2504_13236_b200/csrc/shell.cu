@@ -6,8 +6,8 @@
 //   nnt_embedding_bwd  dwte[v] (+)= sum of dx over the tokens with id v, in token order;
 //                      dwpe[s] (+)= sum_b dx[b, s]
 //                      deterministic without atomics on floats: a counting sort of the token
-//                      positions by id (integer histogram, one-CTA exclusive scan, stable rank
-//                      = number of earlier tokens with the same id), then one warp per
+//                      positions by id (integer histogram, one-CTA exclusive scan; the bucket
+//                      order from a sort of the unique (id, t) keys), then one warp per
 //                      vocabulary row sums its bucket in token order
 //   nnt_cross_entropy  per row: subroutine 1 (the row's (max, sumexp), R10) then loss =
 //                      log S + M - x[label] and, fused with subroutine 2, the gradient
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kT) embed_fwd_kernel(const int32_t* __restrict
 }
 
 // ------------------------------------------------------------------ embedding backward
-// scratch layout (ints): hist[V + 1] | rank[T] | offs[V + 1] | order[T]
+// scratch layout: hist[V + 1] | offs[V + 1] | order[T] (ints) | keys[2][T] (uint64, 8-byte aligned)
 __global__ void __launch_bounds__(kT) embed_hist_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
                                                         int* __restrict__ hist) {
   NNT_PDL_ENTRY();
@@ -96,43 +96,70 @@ __global__ void __launch_bounds__(1024) embed_scan_kernel(const int* __restrict_
   for (int64_t i = threadIdx.x; i < n; i += 1024) offs[i] = buf[i];
 }
 
-// rank[t] = #{t' < t : ids[t'] == ids[t]} (stable position inside the id's bucket).  CTA (x, y)
-// compares its kT tokens with the earlier tokens of chunk y (kRankChunk ids staged in shared
-// memory) and adds its counts with integer atomics (order-independent, exact).
-constexpr int kRankChunk = 1024;
-__global__ void __launch_bounds__(kT) embed_rank_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
-                                                        int* __restrict__ rank) {
-  NNT_PDL_ENTRY();
-  __shared__ int tile[kRankChunk];
-  const int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x;
-  const int64_t c0 = (int64_t)blockIdx.y * kRankChunk;
-  if (c0 >= (int64_t)blockIdx.x * kT + kT || c0 >= T) return;  // chunk entirely after this CTA's tokens
-  for (int i = threadIdx.x; i < kRankChunk; i += kT) {
-    const int64_t j = c0 + i;
-    int64_t v = j < T ? ids[j] : -2;
-    if (j < T) v = v < 0 ? 0 : (v >= V ? V - 1 : v);
-    tile[i] = (int)v;
-  }
-  __syncthreads();
-  if (t >= T) return;
-  int64_t my = ids[t];
-  my = my < 0 ? 0 : (my >= V ? V - 1 : my);
-  const int64_t lim64 = t - c0 < kRankChunk ? t - c0 : kRankChunk;
-  const int lim = lim64 > 0 ? (int)lim64 : 0;
-  int r = 0;
-  for (int k = 0; k < lim; ++k) r += tile[k] == (int)my;
-  if (r) atomicAdd(rank + t, r);
+// The bucket order: the token positions sorted by the key (id, t) -- keys are unique, so ANY sort
+// yields the one order "by id, then ascending t" (the stable counting sort's order) and
+// order[p] = t of the p-th smallest key lands each token at offs[id] + (number of earlier tokens
+// with its id).  A chunk of kSortChunk keys is bitonic-sorted in shared memory per CTA, then
+// merge passes double the sorted run length (merge path: a key's output position is its index
+// in its own run plus the number of smaller keys in the partner run, by binary search).
+// O(T log^2 kSortChunk + T log T) work over all SMs.
+constexpr int kSortChunk = 2048;
+__device__ __forceinline__ uint64_t embed_key(const int32_t* ids, int64_t t, int64_t V) {
+  int64_t v = ids[t];
+  v = v < 0 ? 0 : (v >= V ? V - 1 : v);
+  return ((uint64_t)v << 32) | (uint64_t)t;
 }
-
-__global__ void __launch_bounds__(kT) embed_place_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
-                                                         const int* __restrict__ offs, const int* __restrict__ rank,
+__global__ void __launch_bounds__(1024) embed_sort_chunk_kernel(const int32_t* __restrict__ ids, int64_t T, int64_t V,
+                                                                uint64_t* __restrict__ keys) {
+  NNT_PDL_ENTRY();
+  __shared__ uint64_t k[kSortChunk];
+  const int64_t c0 = (int64_t)blockIdx.x * kSortChunk;
+  for (int i = threadIdx.x; i < kSortChunk; i += 1024)
+    k[i] = c0 + i < T ? embed_key(ids, c0 + i, V) : ~0ull;  // padding sorts last
+  __syncthreads();
+  for (int size = 2; size <= kSortChunk; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < kSortChunk / 2; i += 1024) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;  // the pair (lo, hi) of this step
+        const bool up = (lo & size) == 0;
+        const uint64_t a = k[lo], b = k[hi];
+        if ((a > b) == up) {
+          k[lo] = b;
+          k[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < kSortChunk; i += 1024)
+    if (c0 + i < T) keys[c0 + i] = k[i];
+}
+// Merge the sorted runs [2jL, 2jL + L) and [2jL + L, 2(j+1)L) of src into dst (runs cut at T).
+__global__ void __launch_bounds__(kT) embed_merge_kernel(const uint64_t* __restrict__ src, int64_t T, int64_t L,
+                                                         uint64_t* __restrict__ dst) {
+  NNT_PDL_ENTRY();
+  for (int64_t i = (int64_t)blockIdx.x * kT + threadIdx.x; i < T; i += (int64_t)gridDim.x * kT) {
+    const int64_t base = i / (2 * L) * (2 * L);
+    const bool first = i - base < L;
+    const int64_t own0 = first ? base : base + L;
+    const int64_t o0 = min(T, first ? base + L : base), o1 = min(T, o0 + L);  // the partner run (may be empty)
+    const uint64_t key = src[i];
+    int64_t lo = o0, hi = o1;  // count the partner's smaller keys (keys are unique)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (src[mid] < key)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    dst[base + (i - own0) + (lo - o0)] = key;
+  }
+}
+__global__ void __launch_bounds__(kT) embed_order_kernel(const uint64_t* __restrict__ keys, int64_t T,
                                                          int* __restrict__ order) {
   NNT_PDL_ENTRY();
-  for (int64_t t = (int64_t)blockIdx.x * kT + threadIdx.x; t < T; t += (int64_t)gridDim.x * kT) {
-    int64_t my = ids[t];
-    my = my < 0 ? 0 : (my >= V ? V - 1 : my);
-    order[offs[my] + rank[t]] = (int)t;
-  }
+  for (int64_t p = (int64_t)blockIdx.x * kT + threadIdx.x; p < T; p += (int64_t)gridDim.x * kT)
+    order[p] = (int)(keys[p] & 0xffffffffu);
 }
 
 // dwte[v] (+)= sum over the bucket of v in token order; one warp per vocabulary row
@@ -548,7 +575,8 @@ nnt_status nnt_embedding_fwd(const int32_t* ids, int64_t T, int64_t S, const flo
 
 size_t nnt_embedding_bwd_scratch_bytes(int64_t T, int64_t V) {
   if (T <= 0 || V <= 0) return 0;
-  return (size_t)(2 * (V + 1) + 2 * T) * sizeof(int);
+  const size_t ints = (size_t)(2 * (V + 1) + T);
+  return (ints * sizeof(int) + 7) / 8 * 8 + (size_t)2 * T * sizeof(uint64_t);
 }
 
 nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const float* dx, int64_t E, float* dwte,
@@ -562,23 +590,32 @@ nnt_status nnt_embedding_bwd(const int32_t* ids, int64_t T, int64_t S, const flo
   NNT_REQUIRE(scratch_bytes >= nnt_embedding_bwd_scratch_bytes(T, V), NNT_ERR_WORKSPACE,
               "nnt_embedding_bwd: scratch %zu < %zu", scratch_bytes, nnt_embedding_bwd_scratch_bytes(T, V));
   cudaStream_t s = (cudaStream_t)stream;
-  int* hist = (int*)scratch;  // hist[V + 1] then rank[T] (zeroed together)
-  int* rank = hist + (V + 1);
-  int* offs = rank + T;
+  int* hist = (int*)scratch;
+  int* offs = hist + (V + 1);
   int* order = offs + (V + 1);
+  uint64_t* keys = reinterpret_cast<uint64_t*>(scratch) + ((2 * (V + 1) + T) * sizeof(int) + 7) / 8;
+  uint64_t* keys2 = keys + T;
   LaunchScope sc(NNT_K_MISC, s, 8.0 * T * E + 8.0 * V * 4 + 4.0 * V * E, 0, 7);
   NNT_CUDA_TRY(set_max_dyn_smem(embed_scan_kernel, (int)(kScanMax * sizeof(int))));
   NNT_REQUIRE(V + 1 <= kScanMax, NNT_ERR_UNSUPPORTED, "nnt_embedding_bwd: V=%lld > %d", (long long)V,
               kScanMax - 1);
-  NNT_CUDA_TRY(::nnt::launch(zero_ints_kernel, dim3(grid_cap(V + 1 + T, kT)), dim3(kT), 0, s, hist, V + 1 + T));
+  NNT_REQUIRE(aligned16(scratch), NNT_ERR_ALIGN, "nnt_embedding_bwd: scratch must be 16-byte aligned");
+  NNT_CUDA_TRY(::nnt::launch(zero_ints_kernel, dim3(grid_cap(V + 1, kT)), dim3(kT), 0, s, hist, V + 1));
   NNT_CUDA_TRY(::nnt::launch(embed_hist_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V, hist));
   NNT_CUDA_TRY(::nnt::launch(embed_scan_kernel, dim3(1), dim3(1024), (size_t)(V + 1) * sizeof(int), s,
                              (const int*)hist, V + 1, offs));
-  NNT_CUDA_TRY(::nnt::launch(embed_rank_kernel,
-                             dim3((unsigned)((T + kT - 1) / kT), (unsigned)((T + kRankChunk - 1) / kRankChunk)),
-                             dim3(kT), 0, s, ids, T, V, rank));
-  NNT_CUDA_TRY(::nnt::launch(embed_place_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, ids, T, V,
-                             (const int*)offs, (const int*)rank, order));
+  NNT_CUDA_TRY(::nnt::launch(embed_sort_chunk_kernel, dim3((unsigned)((T + kSortChunk - 1) / kSortChunk)), dim3(1024),
+                             0, s, ids, T, V, keys));
+  for (int64_t L = kSortChunk; L < T; L *= 2) {
+    NNT_CUDA_TRY(::nnt::launch(embed_merge_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, (const uint64_t*)keys, T, L,
+                               keys2));
+    uint64_t* tmp = keys;
+    keys = keys2;
+    keys2 = tmp;
+    sc.add_kernels(1);
+  }
+  NNT_CUDA_TRY(::nnt::launch(embed_order_kernel, dim3(grid_cap(T, kT)), dim3(kT), 0, s, (const uint64_t*)keys, T,
+                             order));
   NNT_CUDA_TRY(::nnt::launch(embed_bucket_kernel, dim3((unsigned)((V + kT / 32 - 1) / (kT / 32))), dim3(kT), 0, s,
                              (const int*)offs, (const int*)order, dx, (int)E, V, dwte, accumulate_wte));
   NNT_CUDA_TRY(::nnt::launch(embed_pos_kernel, dim3(grid_cap(S * E / 4, kT)), dim3(kT), 0, s, dx, T / S, S, (int)E,

@@ -156,6 +156,7 @@ def splitk_mode(request, monkeypatch):
     """Both split-K reductions: the separate ordered reduce kernel (default) and the in-kernel one
     (NNT_SPLITK_FUSED=1, read by the library at every launch)."""
     monkeypatch.setenv("NNT_SPLITK_FUSED", request.param)
+    monkeypatch.setenv("NNT_GEMM_SK", "0")  # split-K itself (stream-K would take these workspaces)
     return request.param
 
 
@@ -236,6 +237,88 @@ def test_gemm_split_k_real_data_extras(M, N, splitk_mode):
         got.append(host(Cm))
         close(got[-1], want, 1e-5)
     close(got[0], got[1], 1e-6)
+
+
+# Stream-K shapes: (M, N, K, ta, tb, residual) -- the GPT-2 XL projections the schedule takes
+# (long K, >= 2 whole data-parallel waves, a last wave <= 82 % full): 8192 x 1600 with K = 6400 /
+# 4800 (224 pair tiles on 74 pairs: 2 data-parallel waves + 76 tiles over 74 units), the dW-shaped
+# 1600 x 6400 x 8192 (175 tiles, beta = 2 here), and a ragged M / N residual GEMM.
+SK_SHAPES = [(8192, 1600, 6400, 0, 1, False), (8192, 1600, 4800, 0, 0, False), (1600, 6400, 8192, 1, 0, False),
+             (8000, 1560, 6400, 0, 1, True)]
+
+
+@pytest.mark.parametrize("shape", SK_SHAPES, ids=lambda s: "x".join(map(str, s[:3])) + ("r" if s[5] else ""))
+def test_gemm_stream_k_bit_exact(shape, capfd, monkeypatch):
+    """Stream-K schedule (the last wave's K-block iterations spread over all units; a tile shared by
+    several units finished by the one holding its last K-block, which adds the others' fp32
+    partials): integer data keeps every partial exact, so C must equal the exact product with beta*C,
+    bias and residual; three launches on one zero-filled workspace (the flags must come back to 0)."""
+    monkeypatch.setenv("NNT_DEBUG_GEMM", "1")
+    monkeypatch.setenv("NNT_GEMM_SK", "1")  # opt-in schedule (DESIGN §7.1)
+    M, N, K, ta, tb, with_res = shape
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + N + K, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=3 * M + N + 5 * K, kind="int")
+    c0 = nnt_inputs.make_matrix((M, N), seed=9, kind="int")
+    bias = nnt_inputs.make_matrix((1, N), seed=10, kind="int")[0]
+    res = nnt_inputs.make_matrix((M, N), seed=11, kind="int")
+    nb = nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0)
+    ws = torch.zeros(nb, device="cuda", dtype=torch.uint8)
+    A, B = dev(a, torch.bfloat16), dev(b, torch.bfloat16)
+    Bias, Res = dev(bias), dev(res)
+    epi = (nnt.make_epilogue(workspace=ws, bias=Bias, residual=Res, ld_residual=N) if with_res
+           else nnt.make_epilogue(workspace=ws, bias=Bias))
+    want = _op(a, ta).astype(np.float64) @ _op(b, tb).astype(np.float64) + bias + 2.0 * c0 + (res if with_res else 0)
+    lda, ldb = a.shape[1], b.shape[1]
+    for _ in range(3):
+        Cm = dev(c0)
+        nnt.nnt_tile_gemm(ta, tb, M, N, K, None, 1.0, A, 1, lda, None, B, 1, ldb, None, 2.0, Cm, 0, N, None, None, epi)
+        torch.cuda.synchronize()
+        got = host(Cm)
+        assert np.array_equal(got, want), f"max |diff| {np.abs(got - want).max()}"
+    assert "stream-K" in capfd.readouterr().err  # the schedule really ran
+    assert int(ws[-SPLIT_COUNTER_BYTES:].count_nonzero()) == 0  # flags consumed
+
+
+@pytest.mark.parametrize("act", ["gelu", "gelu_bwd", "plain"])
+def test_gemm_stream_k_bf16_epilogues_vs_data_parallel(act, monkeypatch):
+    """bf16-output stream-K GEMMs with the fused epilogues (bias + GELU storing the pre-activation,
+    GELU' with the aux input) on real data: against the fp64 product (bf16 tolerance) and against
+    the data-parallel schedule (NNT_GEMM_SK=0; only the K association of the shared tiles differs),
+    and bitwise reproducible run to run."""
+    M, N, K = 8192, 1600, 6400
+    rng = np.random.default_rng(17)
+    a = bf16_round(rng.standard_normal((M, K)) / 16)
+    b = bf16_round(rng.standard_normal((N, K)) / 16)
+    bias = rng.standard_normal(N).astype(np.float32) / 4
+    u = bf16_round(rng.standard_normal((M, N)))
+    A, B, Bias, U = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(bias), dev(u, torch.bfloat16)
+    monkeypatch.setenv("NNT_GEMM_SK", "1")  # (the workspace size includes the stream-K slots)
+    ws = torch.zeros(nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 1, 1), device="cuda", dtype=torch.uint8)
+    base = a.astype(np.float64) @ b.astype(np.float64).T
+    outs = []
+    for sk in ("1", "1", "0"):
+        monkeypatch.setenv("NNT_GEMM_SK", sk)
+        Cm = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        aux = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        if act == "gelu":
+            epi = nnt.make_epilogue(workspace=ws, bias=Bias, act=nnt.NNT_ACT_GELU, aux=aux, ld_aux=N)
+        elif act == "gelu_bwd":
+            epi = nnt.make_epilogue(workspace=ws, act=nnt.NNT_ACT_GELU_BWD, aux=U, ld_aux=N)
+        else:
+            epi = nnt.make_epilogue(workspace=ws)
+        nnt.nnt_tile_gemm(0, 1, M, N, K, None, 1.0, A, 1, K, None, B, 1, K, None, 0.0, Cm, 1, N, None, None, epi)
+        torch.cuda.synchronize()
+        outs.append((host(Cm), host(aux)))
+    if act == "gelu":
+        close(outs[0][1], base + bias, 1e-2)
+        close(outs[0][0], dense.gelu(base + bias), 1e-2)
+    elif act == "gelu_bwd":
+        close(outs[0][0], base * dense.gelu_grad(u), 1e-2)
+    else:
+        close(outs[0][0], base, 1e-2)
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])  # reproducible
+    close(outs[0][0], outs[2][0], 1e-2)  # vs the data-parallel schedule
+    assert int(ws[-SPLIT_COUNTER_BYTES:].count_nonzero()) == 0
 
 
 @pytest.mark.parametrize("ta,tb", [(0, 1), (1, 0), (0, 0), (1, 1)])

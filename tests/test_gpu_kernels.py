@@ -125,10 +125,12 @@ def test_softmax_bwd(causal, pdt):
     close(got, want, (1e-5 if pdt == "f32" else 4e-3))
 
 
-@pytest.mark.parametrize("E", [64, 768, 1600, 8192])
+# E <= 1024: warp per row; 1024 < E <= 2048: 4-warp groups striding over rows with the next row
+# prefetched (T = 5000: several rows per group, ragged last stride); above: one CTA per row
+@pytest.mark.parametrize("E,T", [(64, 96), (768, 96), (1028, 5000), (1600, 96), (1600, 5000), (2048, 5000),
+                                 (2052, 96), (8192, 96)])
 @pytest.mark.parametrize("ydt", ["f32", "bf16"])
-def test_layernorm_fwd(E, ydt):
-    T = 96
+def test_layernorm_fwd(E, T, ydt):
     rng = np.random.default_rng(E)
     x = (50.0 + 3.0 * rng.standard_normal((T, E))).astype(np.float32)  # |mean| >> std
     g = (1 + 0.1 * rng.standard_normal(E)).astype(np.float32)

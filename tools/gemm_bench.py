@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--config", default="small")
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--only", default=None, help="comma-separated GEMM names")
+    ap.add_argument("--no-ws", action="store_true", help="no workspace for the unbatched GEMMs (no stream-K)")
     a = ap.parse_args()
     L, E, H, S, B = bench.CONFIGS[a.config]
     T, F, Dh = B * S, 4 * E, E // H
@@ -94,7 +95,7 @@ def main():
         ("square8192", 0, 1, 8192, 8192, 8192, None, big, 8192, None, big, 8192, None, outb, 1, 8192, None,
          None, 1.0),
     ]
-    ws = torch.empty(64 << 20, device="cuda", dtype=torch.uint8)  # split-K workspace for the dW GEMMs
+    ws = torch.zeros(64 << 20, device="cuda", dtype=torch.uint8)  # split-K / stream-K workspace (zero: flags)
     total = 0.0
     print(f"{'gemm':14s} {'M':>6s} {'N':>6s} {'K':>6s} {'batch':>8s} {'us':>8s} {'TFLOP/s':>8s}")
     for (name, ta, tb, M, N, K, batch, A, lda, sa, Bm, ldb, sb, Cm, cdt, ldc, sc, epi, frac) in cases:
@@ -106,6 +107,11 @@ def main():
         if name.endswith("_dw+db"):
             beta = 1.0
             epi = nnt.make_epilogue(workspace=ws, a_rowsum=rowsum)
+        if batch is None and not a.no_ws:  # unbatched: the workspace a block passes (stream-K slots)
+            if epi is None:
+                epi = nnt.make_epilogue(workspace=ws)
+            else:
+                epi.workspace, epi.workspace_bytes = ws.data_ptr(), ws.numel()
         if name == "square8192" and T * F < 8192 * 8192:
             outb = torch.empty(8192 * 8192, **bf)
             Cm = outb
