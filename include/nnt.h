@@ -284,18 +284,18 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
 /*
  * Softmax backward with the dK / dV products (R18, R20), per (b, n) and 128-key block kb over the
  * query blocks qb (>= kb when causal):
- *   dA^T[b][n][k][q] = scale * P[q][k] * (sum_i dO[q][i] V[k][i] - D[q])     (stored keys-major)
- *   dK[k][n*h + i] = sum_q dA^T[k][q] Q[q][i]            dV[k][n*h + i] = sum_q P[q][k] dO[q][i]
- * D = rowdot(dO, O) (nnt_attn_rowdot).  Each P tile is read once and each dA tile written once;
- * dK and dV accumulate on chip over the query blocks.  dQ = dA K is the GEMM
- * nnt_tile_gemm(NNT_TRANS, NNT_NOTRANS, S, h, S, {B, H}, 1, dAT, S, {H*S*S, S*S}, K, ...,
- * causal NNT_CAUSAL_A_LOWER) on the keys-major dA^T (entries with k > q are zero; blocks with
+ *   dA[b][n][q][k] = scale * P[q][k] * (sum_i dO[q][i] V[k][i] - D[q])      (stored query-major)
+ *   dK[k][n*h + i] = sum_q dA[q][k] Q[q][i]              dV[k][n*h + i] = sum_q P[q][k] dO[q][i]
+ * D = rowdot(dO, O) (nnt_attn_rowdot).  Each P tile is read once and each dA tile written once
+ * (formed over the P tile in shared memory); dK and dV accumulate on chip over the query blocks.
+ * dQ = dA K is the GEMM nnt_tile_gemm(NNT_NOTRANS, NNT_NOTRANS, S, h, S, {B, H}, 1, dA, S,
+ * {H*S*S, S*S}, K, ..., causal NNT_CAUSAL_A_LOWER) (entries with k > q are zero; blocks with
  * kb > qb are not written and not read).
- * qkv, P, D as above; dO: device bf16 [B][S][H*h]; dAT: device bf16 [B][H][S][S]; dqkv: device
+ * qkv, P, D as above; dO: device bf16 [B][S][H*h]; dA: device bf16 [B][H][S][S]; dqkv: device
  * bf16 [B][S][3][H][h] -- its K and V thirds are written, the Q third untouched.
  */
 nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, const float* D, int64_t B,
-                                int64_t S, int64_t H, int64_t h, float scale, int causal, void* dAT,
+                                int64_t S, int64_t H, int64_t h, float scale, int causal, void* dA,
                                 void* dqkv, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */

@@ -12,12 +12,12 @@
 //       staged in shared memory as the A operand of  O += P V_kb  (tcgen05, TMEM);  O stored once.
 //       P is read back from HBM zero times (the unfused path re-read it for P V).
 //   nnt_attention_bwd_kv  (softmax backward + dV + dK) -- task = (b, h, key block):
-//       for each query block qb >= kb:  dP^T = V_kb dO_qb^T (tcgen05)  ->
-//       dA^T = P^T (dP^T - D) / sqrt(h) (epilogue, P from the TMA-loaded tile)  ->  dA^T stored
-//       (keys-major, for dQ = dA K) and staged as the A operand of  dK += dA^T Q_qb;  and
-//       dV += P^T dO_qb  straight from the same P tile.  dK, dV accumulate in TMEM over the
-//       query blocks and are stored once.  Each P tile is read once, each dA tile written once
-//       (the unfused path read P three times and dA twice).
+//       for each query block qb >= kb:  dP = dO_qb V_kb^T (tcgen05) and dV += P^T dO_qb straight
+//       from the TMA-loaded P tile  ->  dA = P (dP - D) / sqrt(h) (epilogue, written over the P
+//       tile in shared memory)  ->  dA stored (for dQ = dA K) and used in place as the A operand
+//       of  dK += dA^T Q_qb.  dK, dV accumulate in TMEM over the query blocks and are stored
+//       once.  Each P tile is read once, each dA tile written once (the unfused path read P three
+//       times and dA twice).
 //
 // Warp roles as in the GEMM (gemm_tc.cu): warp 0 TMA producer, warp 1 TMEM allocator + MMA
 // issuer, warps 2..17 epilogue (TMEM lane quadrant = warp % 4; the four warps of a quadrant take
@@ -453,51 +453,55 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
 }
 
 // ============================================================================ backward
-// smem: V[2] (task parity) | 2 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | D slots [2] | dA^T
-// staging[2] (one per ping-pong group, 32 KB: query chunk h at +16 KB, quadrant rows at +4 KB) |
-// barriers.  TMEM: dP^T[2] at columns 0 / 128, {dV, dK}[2] at 256 / 384 (+64 for dK).
-// Iteration g (a query block of a task) uses stage g % 2, dP^T buffer g % 2, and is processed by
-// epilogue group g % 2 with its own dA^T staging buffer.
-constexpr int B_STAGES = 2;
+// smem: V[2] (task parity) | 3 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | D slots [3] | barriers.
+// TMEM: dP[2] at columns 0 / 128, {dV, dK}[2] at 256 / 384 (+64 for dK).
+// Iteration g (a query block of a task) uses stage g % 3 and dP buffer g % 2, and is processed by
+// epilogue group g % 2.  dP = dO V^T puts the tile's queries on the TMEM lanes, so an epilogue lane
+// owns one query row: it reads that row of P as 16-byte chunks, forms dA = P (dP - D) / sqrt(h)
+// and writes it back IN PLACE over P (the dV MMA that read P is committed with dP, so it has
+// completed when the epilogue sees dP); the tile then serves as the A operand of dK += dA^T Q (the
+// same MN-major view dV uses for P^T) and is stored by TMA (query-major dA, for dQ = dA K).  No
+// separate dA staging: the freed 64 KB hold a third operand stage.
+constexpr int B_STAGES = 3;
 constexpr int B_D_BYTES = TB * 4;                    // D of the stage's query block (bulk copy)
 constexpr int B_STAGE_TX = 4 * TILE16 + B_D_BYTES;   // bytes landing per stage
 constexpr int B_STAGE_BYTES = 4 * TILE16;
-constexpr int B_V = 0, B_ST = 2 * TILE16, B_D = B_ST + B_STAGES * B_STAGE_BYTES, B_DA = B_D + 1024;
-constexpr int B_BAR = B_DA + 2 * 2 * TILE16;
+constexpr int B_V = 0, B_ST = 2 * TILE16, B_D = B_ST + B_STAGES * B_STAGE_BYTES;
+constexpr int B_BAR = B_D + B_STAGES * B_D_BYTES;
 constexpr int B_SMEM = B_BAR + 256 + 1024;
-static_assert(B_DA % 1024 == 0, "SW128 staging alignment");
+static_assert(B_SMEM <= 232448, "backward shared memory budget");
 
 __global__ void __launch_bounds__(kAThreads, 1)
     attn_bwd_kv_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mV,
                        const __grid_constant__ CUtensorMap mdO, const __grid_constant__ CUtensorMap mQ,
-                       const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mdAT,
+                       const __grid_constant__ CUtensorMap mP, const __grid_constant__ CUtensorMap mdA,
                        const __grid_constant__ CUtensorMap mdK, const __grid_constant__ CUtensorMap mdV) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + B_BAR);
-  uint64_t* full = bars;           // [2] stage dO, Q, P, D landed
-  uint64_t* empty = bars + 2;      // [2] stage consumed: MMA commit + the 8 warps of its group (P / D reads)
-  uint64_t* vfull = bars + 4;      // [2]
-  uint64_t* vempty = bars + 6;     // [2] the task's last dP MMA done
-  uint64_t* tfull = bars + 8;      // [2] dP^T accumulator ready
-  uint64_t* tempty = bars + 10;    // [2] drained (8 warps)
-  uint64_t* dafull = bars + 12;    // [2] dA^T staging of group g written (8 warps)
-  uint64_t* daempty = bars + 14;   // [2] dA^T staging of group g consumed by MMA dK
+  uint64_t* full = bars;           // [3] stage dO, Q, P, D landed
+  uint64_t* empty = bars + 3;      // [3] stage released: MMA dK committed + the 8 warps of its group (dA stored)
+  uint64_t* vfull = bars + 6;      // [2]
+  uint64_t* vempty = bars + 8;     // [2] the task's last dP MMA done
+  uint64_t* tfull = bars + 10;     // [2] dP accumulator ready (and the iteration's dV MMA done)
+  uint64_t* tempty = bars + 12;    // [2] drained (8 warps)
+  uint64_t* dafull = bars + 14;    // [2] dA of group g written over P (8 warps)
   uint64_t* afull = bars + 16;     // [2] dV, dK of a task complete
   uint64_t* aempty = bars + 18;    // [2] drained (8 warps)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int BH = P.B * P.H;
   if (warp == 0 && lane == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < B_STAGES; ++i) {
       mbar_init(smem_u32(&full[i]), 1);
       mbar_init(smem_u32(&empty[i]), 1 + kEW / 2);
+    }
+    for (int i = 0; i < 2; ++i) {
       mbar_init(smem_u32(&vfull[i]), 1);
       mbar_init(smem_u32(&vempty[i]), 1);
       mbar_init(smem_u32(&tfull[i]), 1);
       mbar_init(smem_u32(&tempty[i]), kEW / 2);
       mbar_init(smem_u32(&dafull[i]), kEW / 2);
-      mbar_init(smem_u32(&daempty[i]), 1);
       mbar_init(smem_u32(&afull[i]), 1);
       mbar_init(smem_u32(&aempty[i]), kEW / 2);
     }
@@ -556,12 +560,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
     pdl_trigger();
   } else if (warp == 1) {
     // ------------------------------------------------ MMA issuer
-    // A flat stream of iterations g over this CTA's tasks: the dP MMA of iteration g + 1 (also the
-    // next task's first) is issued as soon as nothing blocks it -- before the dK MMA of iteration
-    // g if possible, which waits for the epilogue's dA^T, else right after it.
-    const uint32_t id_dp = idesc_of(false, false, TB);  // dP^T = V dO^T: both K-major, N = 128
-    const uint32_t id_dv = idesc_of(true, true, HD);    // dV += P^T dO: P MN-major, dO MN-major
-    const uint32_t id_dk = idesc_of(false, true, HD);   // dK += dA^T Q: dA^T K-major, Q MN-major
+    // A flat stream of iterations g over this CTA's tasks.  issue_dp(g) = dP of g (dO V^T) then dV
+    // += P^T dO of g, one commit: the epilogue may overwrite P once dP is visible.  The dP / dV of
+    // iteration g + 1 is issued as soon as nothing blocks it -- before the dK MMA of iteration g if
+    // possible (which waits for the epilogue's dA), else right after it.
+    const uint32_t id_dp = idesc_of(false, false, TB);  // dP = dO V^T: both K-major, N = 128 keys
+    const uint32_t id_pt = idesc_of(true, true, HD);    // dV += P^T dO, dK += dA^T Q: both MN-major
     struct Cur {
       int64_t k;
       int tl, i, nq;
@@ -586,22 +590,32 @@ __global__ void __launch_bounds__(kAThreads, 1)
       return c;
     };
     auto dp_ready = [&](int64_t g, const Cur& c) {
-      return (c.i != 0 || mbar_test(smem_u32(&vfull[c.tl & 1]), (c.tl >> 1) & 1)) &&
+      const uint32_t tp = (uint32_t)((c.tl >> 1) & 1);
+      return (c.i != 0 || (mbar_test(smem_u32(&vfull[c.tl & 1]), tp) && mbar_test(smem_u32(&aempty[c.tl & 1]), tp ^ 1))) &&
              mbar_test(smem_u32(&tempty[g & 1]), (uint32_t)(((g >> 1) & 1) ^ 1)) &&
              mbar_test(smem_u32(&full[g % B_STAGES]), (uint32_t)((g / B_STAGES) & 1));
     };
     auto issue_dp = [&](int64_t g, const Cur& c) {
       const int tb = (int)(g & 1), stg = (int)(g % B_STAGES), vs = c.tl & 1;
-      if (c.i == 0) mbar_wait(smem_u32(&vfull[vs]), (c.tl >> 1) & 1);
+      if (c.i == 0) {
+        mbar_wait(smem_u32(&vfull[vs]), (c.tl >> 1) & 1);
+        mbar_wait(smem_u32(&aempty[vs]), ((c.tl >> 1) & 1) ^ 1);  // the task's dV / dK buffer drained
+      }
       mbar_wait(smem_u32(&tempty[tb]), (uint32_t)(((g >> 1) & 1) ^ 1));
       mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / B_STAGES) & 1));
       tc_fence_after();
       const uint32_t sv = smem_u32(smem + B_V + vs * TILE16);
-      const uint32_t sdo = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
+      const uint32_t st = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
 #pragma unroll
       for (int kk = 0; kk < HD / 16; ++kk)
-        mma_bf16_w(tmem + tb * TB, make_sdesc(sv + kk * 32, 16, 1024), make_sdesc(sdo + kk * 32, 16, 1024), id_dp,
+        mma_bf16_w(tmem + tb * TB, make_sdesc(st + kk * 32, 16, 1024), make_sdesc(sv + kk * 32, 16, 1024), id_dp,
                    kk > 0 ? 1u : 0u);
+      // dV += P^T dO (both operands in the stage): K = 128 queries
+      const uint32_t tdv = tmem + 256 + vs * 128;
+#pragma unroll
+      for (int kk = 0; kk < TB / 16; ++kk)
+        mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
+                   id_pt, (c.i > 0 || kk > 0) ? 1u : 0u);
       mma_commit_w(smem_u32(&tfull[tb]));
       if (lane == 0) trace_ev(P, 1, g);
       if (c.i == c.nq - 1) mma_commit_w(smem_u32(&vempty[vs]));  // the task's last dP MMA: V may be reloaded
@@ -618,32 +632,21 @@ __global__ void __launch_bounds__(kAThreads, 1)
     for (int64_t g = 0; cur.ok; ++g) {
       const int as = cur.tl & 1, stg = (int)(g % B_STAGES), db = (int)(g & 1);
       const uint32_t st = smem_u32(smem + B_ST + stg * B_STAGE_BYTES);
-      const uint32_t tdv = tmem + 256 + as * 128, tdk = tdv + HD;
-      if (cur.i == 0) {
-        mbar_wait(smem_u32(&aempty[as]), ((cur.tl >> 1) & 1) ^ 1);
-        tc_fence_after();
-      }
-      // dV += P^T dO (both operands already in the stage): K = 128 queries
-#pragma unroll
-      for (int kk = 0; kk < TB / 16; ++kk)
-        mma_bf16_w(tdv, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024), make_sdesc(st + kk * 2048, 8192, 1024),
-                   id_dv, (cur.i > 0 || kk > 0) ? 1u : 0u);
+      const uint32_t tdk = tmem + 256 + as * 128 + HD;
       const Cur nxt = next(cur);
       bool pending = nxt.ok;
       if (pending && dp_ready(g + 1, nxt)) {
         issue_dp(g + 1, nxt);
         pending = false;
       }
-      // dK += dA^T Q once group g % 2 has staged dA^T of iteration g
+      // dK += dA^T Q once group g % 2 has written dA over the stage's P tile
       mbar_wait(smem_u32(&dafull[db]), (uint32_t)((g >> 1) & 1));
       if (lane == 0) trace_ev(P, 4, g);
       tc_fence_after();
-      const uint32_t sda = smem_u32(smem + B_DA + db * 2 * TILE16);
 #pragma unroll
       for (int kk = 0; kk < TB / 16; ++kk)
-        mma_bf16_w(tdk, make_sdesc(sda + (kk >> 2) * TILE16 + (kk & 3) * 32, 16, 1024),
-                   make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_dk, (cur.i > 0 || kk > 0) ? 1u : 0u);
-      mma_commit_w(smem_u32(&daempty[db]));
+        mma_bf16_w(tdk, make_sdesc(st + 2 * TILE16 + kk * 2048, TILE16, 1024),
+                   make_sdesc(st + TILE16 + kk * 2048, 8192, 1024), id_pt, (cur.i > 0 || kk > 0) ? 1u : 0u);
       if (lane == 0) trace_ev(P, 5, g);
       mma_commit_w(smem_u32(&empty[stg]));
       if (cur.i == cur.nq - 1) mma_commit_w(smem_u32(&afull[as]));
@@ -652,15 +655,13 @@ __global__ void __launch_bounds__(kAThreads, 1)
     }
   } else {
     // ------------------------------------------------ epilogue warps 2..17: two ping-pong groups
-    // Group grp = (warp - 2) / 8 takes the iterations g with g % 2 == grp (stage, dP^T buffer and
-    // dA^T staging buffer grp).  Inside a group: TMEM lane quadrant quad (keys), 64-query chunk hc
-    // (two 32-query halves in turn); each warp writes whole 128-byte staging rows and stores them.
-    // The group that ran a task's last iteration then drains its dK (hc 0) / dV (hc 1).
+    // Group grp = (warp - 2) / 8 takes the iterations g with g % 2 == grp.  Inside a group: TMEM
+    // lane quadrant quad (query rows quad*32 ..), key half hc (P box hc: keys hc*64 .. +63, the
+    // lane's 128-byte row of it).  The group that ran a task's last iteration then drains its dK
+    // (hc 0) / dV (hc 1) through its own dA piece of the stage.
     const int grp = (warp - 2) >> 3, quad = warp & 3, hc = ((warp - 2) >> 2) & 1;
+    const int qrow = quad * 32 + lane;  // this lane's query row of the tile
     int it = 0, tl = 0;
-    // P element (query r of the tile, this lane's key): tile box quad >> 1, 16-byte chunk
-    // (quad & 1) * 4 + lane / 8 swizzled by r % 8 (SW128), element lane % 8
-    const int pbox = (quad >> 1) * TILE16, pchunk = (quad & 1) * 4 + (lane >> 3), pel = (lane & 7) * 2;
     for (int64_t k = 0;; ++k, ++tl) {
       const int64_t t = task_at(c0, G, k);
       if (t >= P.num_tasks) break;
@@ -669,53 +670,52 @@ __global__ void __launch_bounds__(kAThreads, 1)
       const int q0 = q_first(kb);
       for (int qb = q0; qb < P.nblk; ++qb, ++it) {
         if ((it & 1) != grp) continue;
+        const int stg = it % B_STAGES;
         mbar_wait(smem_u32(&tfull[grp]), (it >> 1) & 1);
         if (warp == 2 && lane == 0) trace_ev(P, 2, it);
         tc_fence_after();
-        mbar_wait(smem_u32(&full[grp]), (uint32_t)((it / B_STAGES) & 1));  // P and D of this stage
-        const uint8_t* ptile = smem + B_ST + grp * B_STAGE_BYTES + 2 * TILE16 + pbox;
-        const float* Dq = reinterpret_cast<const float*>(smem + B_D + grp * B_D_BYTES) + hc * 64;
-        // dA^T staging buffer grp: free once MMA dK of iteration it-2 and this warp's stores are done
-        mbar_wait(smem_u32(&daempty[grp]), ((it >> 1) & 1) ^ 1);
-        uint8_t* piece = smem + B_DA + grp * 2 * TILE16 + hc * TILE16 + quad * PIECE;
-        if (lane == 0) bulk_wait_read0();
-        __syncwarp();
+        mbar_wait(smem_u32(&full[stg]), (uint32_t)((it / B_STAGES) & 1));  // P and D of this stage
+        uint8_t* const box = smem + B_ST + stg * B_STAGE_BYTES + 2 * TILE16 + hc * TILE16;
+        uint8_t* const prow = box + qrow * 128;
+        uint8_t* const piece = box + quad * PIECE;  // this warp's 32 rows of the box
+        const float dq = reinterpret_cast<const float*>(smem + B_D + stg * B_D_BYTES)[qrow];
 #pragma unroll 1
         for (int sub = 0; sub < 2; ++sub) {
-          float v[32];  // dP^T[key = lane row][query = hc * 64 + sub * 32 + j]
+          float v[32];  // dP[query = qrow][key = hc * 64 + sub * 32 + j]
           tmem_ld32(tmem + grp * TB + hc * 64 + sub * 32 + ((uint32_t)(quad * 32) << 16), v);
-          if (sub == 1) {  // the dP^T buffer is free once both halves are in registers
+          if (sub == 1) {  // the dP buffer is free once both halves are in registers
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(smem_u32(&tempty[grp]));
           }
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const float4 d = *reinterpret_cast<const float4*>(Dq + sub * 32 + j);  // (broadcast)
-            const float dd[4] = {d.x, d.y, d.z, d.w};
+          for (int c = 0; c < 4; ++c) {  // 16-byte chunk sub * 4 + c of the row: keys 8 (sub*4+c) ..
+            uint4* ptr = reinterpret_cast<uint4*>(prow + (((sub * 4 + c) ^ (qrow & 7)) << 4));
+            uint4 u = *ptr;
+            uint32_t* wd = reinterpret_cast<uint32_t*>(&u);
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const int r = hc * 64 + sub * 32 + j + u;  // query row of the P tile
-              const uint16_t pr =
-                  *reinterpret_cast<const uint16_t*>(ptile + r * 128 + ((pchunk ^ (r & 7)) << 4) + pel);
-              const float p = __uint_as_float((uint32_t)pr << 16);
-              v[j + u] = (p * P.scale) * (v[j + u] - dd[u]);  // dA = P (dP - D) / sqrt(h)  (R20)
+            for (int e = 0; e < 4; ++e) {
+              const float2 pp = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wd[e]));
+              const float a0 = (pp.x * P.scale) * (v[8 * c + 2 * e] - dq);  // dA = P (dP - D) / sqrt(h)  (R20)
+              const float a1 = (pp.y * P.scale) * (v[8 * c + 2 * e + 1] - dq);
+              __nv_bfloat162 r = __floats2bfloat162_rn(a0, a1);
+              wd[e] = *reinterpret_cast<uint32_t*>(&r);
             }
+            *ptr = u;
           }
-          stage_half_row(piece, lane, sub, v);
         }
         fence_async_smem();
         __syncwarp();
         if (lane == 0) {
-          mbar_arrive(smem_u32(&empty[grp]));  // this warp's P / D reads are done
           mbar_arrive(smem_u32(&dafull[grp]));
           if (warp == 2) trace_ev(P, 3, it);
-          tma_store_4d(&mdAT, smem_u32(piece), qb * TB + hc * 64, kb * TB + quad * 32, h, b);
+          tma_store_4d(&mdA, smem_u32(piece), kb * TB + hc * 64, qb * TB + quad * 32, h, b);
           bulk_commit();
         }
         if (qb == P.nblk - 1) {
-          // dK (hc 0) / dV (hc 1) of the key block -> bf16 -> TMA store, from this group's staging
-          // buffer (afull: MMA dK has finished with it; own stores finished reading first)
+          // dK (hc 0) / dV (hc 1) of the key block -> bf16 -> TMA store, staged in this warp's dA
+          // piece (afull: the task's dK MMAs, the last readers of the stage, are done; the dA
+          // store has read the piece)
           const int as = tl & 1;
           mbar_wait(smem_u32(&afull[as]), (tl >> 1) & 1);
           tc_fence_after();
@@ -735,6 +735,10 @@ __global__ void __launch_bounds__(kAThreads, 1)
             tma_store_4d(hc == 0 ? &mdK : &mdV, smem_u32(piece), 0, kb * TB + quad * 32, h, b);
             bulk_commit();
           }
+        }
+        if (lane == 0) {  // the stage may be refilled once this warp's stores have read it
+          bulk_wait_read0();
+          mbar_arrive(smem_u32(&empty[stg]));
         }
       }
     }
@@ -814,16 +818,16 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
 }
 
 nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, const float* D, int64_t B, int64_t S,
-                                int64_t H, int64_t Dh, float scale, int causal, void* dAT, void* dqkv,
+                                int64_t H, int64_t Dh, float scale, int causal, void* dA, void* dqkv,
                                 nnt_stream_t stream) {
   NNT_TRY(check_attn(qkv, B, S, H, Dh, "nnt_attention_bwd_kv"));
-  NNT_REQUIRE(dO && P && D && dAT && dqkv, NNT_ERR_NULL, "nnt_attention_bwd_kv: NULL pointer");
-  NNT_REQUIRE(aligned16(dO) && aligned16(P) && aligned16(D) && aligned16(dAT) && aligned16(dqkv), NNT_ERR_ALIGN,
+  NNT_REQUIRE(dO && P && D && dA && dqkv, NNT_ERR_NULL, "nnt_attention_bwd_kv: NULL pointer");
+  NNT_REQUIRE(aligned16(dO) && aligned16(P) && aligned16(D) && aligned16(dA) && aligned16(dqkv), NNT_ERR_ALIGN,
               "nnt_attention_bwd_kv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D,
                  trace_ptr(1)};
-  CUtensorMap mV, mdO, mQ, mP, mdAT, mdK, mdV;
+  CUtensorMap mV, mdO, mQ, mP, mdA, mdK, mdV;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
   __nv_bfloat16* dq = (__nv_bfloat16*)dqkv;
@@ -831,7 +835,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
   NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mdO, bf, 2, dO, Dh, S, Ea, H, Dh, B, S * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mP, bf, 2, P, S, S, S, H, S * S, B, H * S * S, 64, TB));
-  NNT_TRY(make_tma_map_4d(&mdAT, bf, 2, dAT, S, S, S, H, S * S, B, H * S * S, 64, 32));
+  NNT_TRY(make_tma_map_4d(&mdA, bf, 2, dA, S, S, S, H, S * S, B, H * S * S, 64, 32));
   NNT_TRY(make_tma_map_4d(&mdK, bf, 2, dq + Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));
   NNT_TRY(make_tma_map_4d(&mdV, bf, 2, dq + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));
   // algorithmic bytes: P read once, dA written once, Q / V / dO read, dK / dV written
@@ -840,7 +844,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
                  ptiles * 6.0 * TB * TB * HD);
   NNT_CUDA_TRY(set_max_dyn_smem(attn_bwd_kv_kernel, B_SMEM));
   NNT_CUDA_TRY(::nnt::launch(attn_bwd_kv_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreads),
-                             (size_t)B_SMEM, (cudaStream_t)stream, prm, mV, mdO, mQ, mP, mdAT, mdK, mdV));
+                             (size_t)B_SMEM, (cudaStream_t)stream, prm, mV, mdO, mQ, mP, mdA, mdK, mdV));
   return check_launch("attn_bwd_kv");
 }
 

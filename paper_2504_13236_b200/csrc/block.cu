@@ -317,9 +317,7 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
     case NNT_OP_ATT_DQ: {
       const int64_t sp[2] = {H * S * S, S * S}, sq[2] = {S * 3 * Ea, Dh};
       e.causal = x.c.causal ? NNT_CAUSAL_A_LOWER : NNT_CAUSAL_NONE;
-      if (x.fused_attn)  // dQ = dA K with dA stored keys-major (op(A) = (dA^T)^T)
-        return gemm(x, NNT_TRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
-                    x.s<uint8_t>(x.L.qkv) + es * Ea, 3 * Ea, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * Ea, sq, &e);
+      // dQ = dA K (dA query-major, from nnt_attention_bwd_kv or the dP GEMM's softmax-backward epilogue)
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, S, Dh, S, batch, 1.f, x.k<void>(x.L.dA), S, sp,
                   x.s<uint8_t>(x.L.qkv) + es * Ea, 3 * Ea, sq, 0.f, x.k<void>(x.L.dqkv), dt, 3 * Ea, sq, &e);
     }

@@ -12,6 +12,7 @@
 #include <cstdlib>
 
 #include "reduce.cuh"
+#include "tc_ptx.cuh"
 
 namespace nnt {
 namespace {
@@ -430,6 +431,173 @@ __global__ void __launch_bounds__(32 * kGrpWarps, 1)
   }
 }
 
+// ------------------------------------------------------------------ backward, row ring (1024 < E <= 2048)
+// The group kernel above keeps one row in flight per group beyond the one being reduced (register
+// prefetch: 220 registers, 8 warps per SM), so each group waits about one DRAM latency per row
+// (ncu: 47 % of DRAM bandwidth at E = 1600, long-scoreboard stalls).  Here each group of 4 warps
+// owns a ring of kRing shared-memory slots; one elected thread streams the group's rows into it
+// with 1-D bulk copies (x, dy and the residual gradient of a row: 3 E floats, completing on the
+// slot's mbarrier), kRing rows ahead of the row being reduced.  The arithmetic, the per-row
+// cross-warp sums and the fixed-order column partials are those of ln_bwd_groups.
+constexpr int kRing = 4, kRingGroups = 2, kRingG = 4;
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int NV, bool SUM>
+__global__ void __launch_bounds__(32 * kRingG * kRingGroups, 1)
+    ln_bwd_ring(const float* __restrict__ dy, int64_t lddy, const float* __restrict__ x, int64_t ldx,
+                const float* __restrict__ mean, const float* __restrict__ rstd, const float* __restrict__ gamma,
+                int64_t T, int E, int64_t rows_per_cta, const float* __restrict__ dres, float* __restrict__ dx,
+                int64_t lddx, __nv_bfloat16* __restrict__ dx16, float* __restrict__ pg, float* __restrict__ pb,
+                float* __restrict__ ps) {
+  NNT_PDL_ENTRY();
+  constexpr int NP = SUM ? 3 : 2;
+  extern __shared__ __align__(1024) uint8_t ring_smem[];  // [kRingGroups][kRing] slots of {x, dy, dres} rows
+  __shared__ float2 xs[2][kRingGroups][kRingG];
+  __shared__ __align__(8) uint64_t fullb[kRingGroups][kRing];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = w / kRingG, k = w % kRingG;
+  const int E4 = E / 4;
+  const float inv_e = 1.0f / (float)E;
+  const int nin = dres ? 3 : 2;
+  const uint32_t row_bytes = (uint32_t)E * 4u;
+  float4* const slots = reinterpret_cast<float4*>(ring_smem) + (size_t)grp * kRing * 3 * E4;
+  if (k == 0 && lane == 0)
+    for (int i = 0; i < kRing; ++i) mbar_init(smem_u32(&fullb[grp][i]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(r0 + rows_per_cta, T);
+  // the group's rows: r0 + grp, r0 + grp + kRingGroups, ...; row index n of the group -> slot n % kRing
+  auto issue = [&](int64_t n) {  // elected thread: bulk copies of the group's n-th row
+    const int64_t row = r0 + grp + n * kRingGroups;
+    if (row >= r1) return;
+    const int sl = (int)(n % kRing);
+    const uint32_t bar = smem_u32(&fullb[grp][sl]);
+    const uint32_t dst = smem_u32(slots + (size_t)sl * 3 * E4);
+    mbar_expect_tx(bar, row_bytes * (uint32_t)nin);
+    bulk_g2s(dst, x + row * ldx, row_bytes, bar);
+    bulk_g2s(dst + row_bytes, dy + row * lddy, row_bytes, bar);
+    if (dres) bulk_g2s(dst + 2 * row_bytes, dres + row * lddx, row_bytes, bar);
+  };
+  if (k == 0 && lane == 0)
+    for (int n = 0; n < kRing; ++n) issue(n);
+  float4 ag[NV], ab[NV], as[SUM ? NV : 1], gm[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    ag[j] = ab[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (SUM) as[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int i4 = lane + 32 * (k + kRingG * j);
+    gm[j] = i4 < E4 ? ldg4(gamma + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  int64_t row = r0 + grp;
+  float mu = 0.f, rs = 0.f;
+  if (row < r1) {
+    mu = __ldg(mean + row);
+    rs = __ldg(rstd + row);
+  }
+  int buf = 0;
+  for (int64_t n = 0; row < r1; ++n, row += kRingGroups, buf ^= 1) {
+    const int sl = (int)(n % kRing);
+    float mun = 0.f, rsn = 0.f;
+    if (row + kRingGroups < r1) {
+      mun = __ldg(mean + row + kRingGroups);
+      rsn = __ldg(rstd + row + kRingGroups);
+    }
+    mbar_wait(smem_u32(&fullb[grp][sl]), (uint32_t)((n / kRing) & 1));
+    const float4* xr = slots + (size_t)sl * 3 * E4;
+    float4 xv[NV], dv[NV], rv[NV];
+    float sa = 0.f, sb = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * (k + kRingG * j);
+      if (i4 < E4) {
+        float4 h = xr[i4];
+        const float4 d = xr[E4 + i4];
+        rv[j] = dres ? xr[2 * E4 + i4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        h = make_float4((h.x - mu) * rs, (h.y - mu) * rs, (h.z - mu) * rs, (h.w - mu) * rs);
+        xv[j] = h;
+        ag[j].x += d.x * h.x; ag[j].y += d.y * h.y; ag[j].z += d.z * h.z; ag[j].w += d.w * h.w;
+        ab[j].x += d.x; ab[j].y += d.y; ab[j].z += d.z; ab[j].w += d.w;
+        const float4 gj = gm[j];
+        const float4 e = make_float4(d.x * gj.x, d.y * gj.y, d.z * gj.z, d.w * gj.w);  // dxhat
+        dv[j] = e;
+        sa += (e.x + e.y) + (e.z + e.w);
+        sb += (e.x * h.x + e.y * h.y) + (e.z * h.z + e.w * h.w);
+      }
+    }
+    sa = warp_sum(sa);
+    sb = warp_sum(sb);
+    if (lane == 0) xs[buf][grp][k] = make_float2(sa, sb);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * kRingG) : "memory");  // also: the slot is read
+    if (k == 0 && lane == 0) issue(n + kRing);  // refill the slot kRing rows ahead
+    sa = 0.f;
+    sb = 0.f;
+#pragma unroll
+    for (int i = 0; i < kRingG; ++i) {  // fixed warp order
+      const float2 t = xs[buf][grp][i];
+      sa += t.x;
+      sb += t.y;
+    }
+    sa *= inv_e;
+    sb *= inv_e;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * (k + kRingG * j);
+      if (i4 < E4) {
+        RowGrad rg{xv[j], dv[j]};
+        float4 o = dx_of(rg, rs, sa, sb);
+        o.x += rv[j].x; o.y += rv[j].y; o.z += rv[j].z; o.w += rv[j].w;
+        *reinterpret_cast<float4*>(dx + row * lddx + 4 * i4) = o;
+        if (dx16) store4<__nv_bfloat16>(dx16 + row * lddx + 4 * i4, o);
+        if constexpr (SUM) {
+          as[j].x += o.x; as[j].y += o.y; as[j].z += o.z; as[j].w += o.w;
+        }
+      }
+    }
+    mu = mun;
+    rs = rsn;
+  }
+  __syncthreads();  // the ring is free: reuse it for the group partials
+  float4* red = reinterpret_cast<float4*>(ring_smem);  // [kRingGroups][NP][E/4]
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i4 = lane + 32 * (k + kRingG * j);
+    if (i4 < E4) {
+      red[(size_t)(NP * grp) * E4 + i4] = ag[j];
+      red[(size_t)(NP * grp + 1) * E4 + i4] = ab[j];
+      if constexpr (SUM) red[(size_t)(NP * grp + 2) * E4 + i4] = as[j];
+    }
+  }
+  __syncthreads();
+  for (int i4 = threadIdx.x; i4 < E4; i4 += 32 * kRingG * kRingGroups) {
+    float4 sg = make_float4(0.f, 0.f, 0.f, 0.f), s4 = make_float4(0.f, 0.f, 0.f, 0.f),
+           ss = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int q = 0; q < kRingGroups; ++q) {  // fixed group order
+      const float4 a = red[(size_t)(NP * q) * E4 + i4], b = red[(size_t)(NP * q + 1) * E4 + i4];
+      sg.x += a.x; sg.y += a.y; sg.z += a.z; sg.w += a.w;
+      s4.x += b.x; s4.y += b.y; s4.z += b.z; s4.w += b.w;
+      if constexpr (SUM) {
+        const float4 c = red[(size_t)(NP * q + 2) * E4 + i4];
+        ss.x += c.x; ss.y += c.y; ss.z += c.z; ss.w += c.w;
+      }
+    }
+    reinterpret_cast<float4*>(pg + (int64_t)blockIdx.x * E)[i4] = sg;
+    reinterpret_cast<float4*>(pb + (int64_t)blockIdx.x * E)[i4] = s4;
+    if constexpr (SUM) reinterpret_cast<float4*>(ps + (int64_t)blockIdx.x * E)[i4] = ss;
+  }
+}
+
+// NNT_LN_BWD_RING=0: the register-prefetch group kernel for 1024 < E <= 2048 too (A/B runs)
+bool ln_bwd_ring_on() {
+  const char* e = getenv("NNT_LN_BWD_RING");
+  return !(e && e[0] == '0');
+}
+
 // warps per row and float4s per lane of the group kernel (E > 1024): G = 4 up to E = 2048, 8 above
 void pick_groups(int64_t E, int* G, int* NV) {
   const int64_t E4 = E / 4;
@@ -552,6 +720,22 @@ nnt_status nnt_layernorm_bwd(const float* dy, int64_t lddy, const float* x, int6
   case N: NNT_TRY(sum ? run(ln_bwd_rows<N, true>) : run(ln_bwd_rows<N, false>)); break;
     switch (nvw) { NNT_LNBR(1) NNT_LNBR(2) NNT_LNBR(4) NNT_LNBR(6) NNT_LNBR(8) }
 #undef NNT_LNBR
+  } else if (E <= 2048 && ln_bwd_ring_on() && (ldx * 4) % 16 == 0 && (lddy * 4) % 16 == 0 && aligned16(x) &&
+             aligned16(dy)) {
+    // rows streamed into shared-memory rings by bulk copies (16-byte aligned rows)
+    const int NV = (int)((E / 4 + 32 * kRingG - 1) / (32 * kRingG));
+    const size_t smem_ring = (size_t)kRingGroups * kRing * 3 * E * sizeof(float);  // <= 192 KB
+    auto run = [&](auto kern) -> nnt_status {
+      NNT_CUDA_TRY(set_max_dyn_smem(kern, (int)smem_ring));
+      NNT_CUDA_TRY(::nnt::launch(kern, dim3((unsigned)chunks), dim3(32 * kRingG * kRingGroups), smem_ring, stream, dy,
+                                 lddy, x, ldx, mean, rstd, gamma, T, (int)E, rows_per_cta, dres, dx, lddx, d16, pg, pb,
+                                 ps));
+      return NNT_OK;
+    };
+    if (NV == 3)
+      NNT_TRY(sum ? run(ln_bwd_ring<3, true>) : run(ln_bwd_ring<3, false>));
+    else
+      NNT_TRY(sum ? run(ln_bwd_ring<4, true>) : run(ln_bwd_ring<4, false>));
   } else {
     int G = 0, NV = 0;
     pick_groups(E, &G, &NV);

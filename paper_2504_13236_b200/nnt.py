@@ -323,8 +323,8 @@ def nnt_attention_fwd_pv(qkv, B, S, H, h, scale, causal, stats, P, O, stream=Non
                                           _stream(stream)))
 
 
-def nnt_attention_bwd_kv(qkv, dO, P, D, B, S, H, h, scale, causal, dAT, dqkv, stream=None):
-    return check(lib.nnt_attention_bwd_kv(ptr(qkv), ptr(dO), ptr(P), ptr(D), B, S, H, h, scale, causal, ptr(dAT),
+def nnt_attention_bwd_kv(qkv, dO, P, D, B, S, H, h, scale, causal, dA, dqkv, stream=None):
+    return check(lib.nnt_attention_bwd_kv(ptr(qkv), ptr(dO), ptr(P), ptr(D), B, S, H, h, scale, causal, ptr(dA),
                                           ptr(dqkv), _stream(stream)))
 
 

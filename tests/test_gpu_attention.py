@@ -1,8 +1,9 @@
 """The fused attention tile kernels (R33) against the fp64 oracle, through the C-ABI.
 
 nnt_attention_fwd_pv: softmax subroutine 2 from the row statistics (the ROWSTATS score GEMM, R26)
-and O = P V, P staged once; nnt_attention_bwd_kv: dA = P (dP - D) / sqrt(h) stored keys-major,
-dK = dA^T Q and dV = P^T dO accumulated on chip; dQ = dA K by nnt_tile_gemm on the keys-major dA.
+and O = P V, P staged once; nnt_attention_bwd_kv: dA = P (dP - D) / sqrt(h) written over the P tile
+in shared memory and stored (query-major), dK = dA^T Q and dV = P^T dO accumulated on chip; dQ = dA K
+by nnt_tile_gemm on the stored dA.
 Shapes span several 128-row tiles (S = 256, 384), causal and not, B * H > 1; bf16 tolerance 2e-2
 norm-wise and element-wise (gpu_util.close).  The block tests (test_gpu_block / test_gpu_shapes /
 test_gpu_parity_full) run the same kernels inside nnt_block_fwd / _bwd.
@@ -78,14 +79,14 @@ def test_fused_attention_fwd_bwd(B, S, H, causal):
     dO = dev(do, torch.bfloat16)
     D = torch.empty(B * H * S, device="cuda")
     nnt.nnt_attn_rowdot(dO, O, nnt.NNT_BF16, B, S, H, H_D, D)
-    dAT = torch.full((B, H, S, S), float("nan"), device="cuda", dtype=torch.bfloat16)
+    dA = torch.full((B, H, S, S), float("nan"), device="cuda", dtype=torch.bfloat16)
     dqkv = torch.zeros(B, S, 3 * E, device="cuda", dtype=torch.bfloat16)
-    nnt.nnt_attention_bwd_kv(Q, dO, P, D, B, S, H, H_D, scale, causal, dAT, dqkv)
+    nnt.nnt_attention_bwd_kv(Q, dO, P, D, B, S, H, H_D, scale, causal, dA, dqkv)
     sp = [H * S * S, S * S]
     sq = [S * 3 * E, H_D]
     qb = Q.reshape(-1).view(torch.uint8)
     epi = nnt.make_epilogue(causal=nnt.NNT_CAUSAL_A_LOWER if causal else nnt.NNT_CAUSAL_NONE)
-    nnt.nnt_tile_gemm(1, 0, S, H_D, S, [B, H], 1.0, dAT, 1, S, sp, qb[2 * E:], 1, 3 * E, sq, 0.0, dqkv, 1, 3 * E,
+    nnt.nnt_tile_gemm(0, 0, S, H_D, S, [B, H], 1.0, dA, 1, S, sp, qb[2 * E:], 1, 3 * E, sq, 0.0, dqkv, 1, 3 * E,
                       sq, None, epi)
     torch.cuda.synchronize()
     # oracle backward from the P the GPU produced (isolates the backward kernels)
@@ -94,11 +95,11 @@ def test_fused_attention_fwd_bwd(B, S, H, causal):
     got = host(dqkv)
     for j, name in enumerate(("dQ", "dK", "dV")):
         close(got[..., j * E:(j + 1) * E], want[..., j * E:(j + 1) * E], 2e-2, name)
-    # dA (keys-major) on the written tiles: the oracle's dA / sqrt(h), transposed
+    # dA (query-major) on the written tiles: the oracle's dA / sqrt(h)
     q_, k_, v_ = dense.split_heads(qkv, H)
     do_h = do.reshape(B, S, H, H_D).transpose(0, 2, 1, 3)
     da_ref = dense.softmax_bwd(p_used, do_h @ v_.transpose(0, 1, 3, 2)) * scale
-    da = host(dAT).transpose(0, 1, 3, 2)
+    da = host(dA)
     close(da[:, :, w], da_ref[:, :, w], 2e-2, "dA")
 
 

@@ -163,10 +163,11 @@ def test_layernorm_closed_forms():
     np.testing.assert_allclose(y[1] - b, np.where(np.arange(E) % 2 == 0, -v, v), rtol=1e-6)
 
 
-# E <= 1024: the warp-per-row kernel; E > 1024: warp groups per row (G = 4 warps up to E = 2048,
-# 8 above; the next row prefetched up to E = 4096), T = 8192 gives several rows per group
-@pytest.mark.parametrize("E,T", [(64, 200), (768, 200), (1280, 200), (1600, 200), (1600, 8192), (2052, 300),
-                                 (4096, 200), (8192, 100)])
+# E <= 1024: the warp-per-row kernel; 1024 < E <= 2048: 4-warp groups fed by shared-memory row rings
+# (bulk copies, 4 rows ahead); above: warp groups (8 warps), the next row prefetched in registers up
+# to E = 4096.  T = 8192 gives several rows per group.
+@pytest.mark.parametrize("E,T", [(64, 200), (768, 200), (1028, 3000), (1280, 200), (1600, 200), (1600, 8192),
+                                 (2048, 2000), (2052, 300), (4096, 200), (8192, 100)])
 def test_layernorm_bwd(E, T):
     rng = np.random.default_rng(E + 1)
     x = (1.0 + 2.0 * rng.standard_normal((T, E))).astype(np.float32)
@@ -192,6 +193,39 @@ def test_layernorm_bwd(E, T):
     close(host(DG), dg_ref + 1.0, 1e-5)
     close(host(DB), db_ref + 1.0, 1e-5)
     close(host(DS), (dx_ref + dres).sum(axis=0) + 2.0, 1e-5)
+
+
+@pytest.mark.parametrize("E,extras", [(1600, True), (1600, False), (1028, False), (2048, True)])
+def test_layernorm_bwd_ring_equals_group_kernel(E, extras, monkeypatch):
+    """1024 < E <= 2048: the ring kernel (rows streamed into shared memory) keeps the group kernel's
+    arithmetic -- same row-to-group assignment, column mapping, per-row sum order and column
+    partials -- so every output is bitwise equal to NNT_LN_BWD_RING=0's; with and without the
+    residual gradient, the bf16 copy and the fused column sum."""
+    T = 5000
+    rng = np.random.default_rng(E + 7)
+    x = (1.0 + 2.0 * rng.standard_normal((T, E))).astype(np.float32)
+    g = (1 + 0.1 * rng.standard_normal(E)).astype(np.float32)
+    dy = rng.standard_normal((T, E)).astype(np.float32)
+    dres = rng.standard_normal((T, E)).astype(np.float32)
+    _, m_ref, r_ref = dense.layernorm_fwd(x, g, np.zeros(E, np.float32), 1e-5)
+    nb = nnt.nnt_layernorm_bwd_scratch_bytes(T, E)
+    args = (dev(dy), E, dev(x), E, dev(m_ref.astype(np.float32)), dev(r_ref.astype(np.float32)), dev(g), T, E)
+    R = dev(dres)
+    outs = []
+    for ring in ("1", "0"):
+        monkeypatch.setenv("NNT_LN_BWD_RING", ring)
+        DX = torch.zeros(T, E, device="cuda")
+        DX16 = torch.zeros(T, E, device="cuda", dtype=torch.bfloat16) if extras else None
+        DG, DB = torch.zeros(E, device="cuda"), torch.zeros(E, device="cuda")
+        DS = torch.zeros(E, device="cuda") if extras else None
+        scr = torch.empty(nb, device="cuda", dtype=torch.uint8)
+        nnt.nnt_layernorm_bwd(*args, R if extras else None, DX, E, DX16, DG, DB, DS, 0, scr, nb)
+        torch.cuda.synchronize()
+        outs.append([host(t) for t in (DX, DX16, DG, DB, DS) if t is not None])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    dx_ref, dg_ref, db_ref = dense.layernorm_bwd(dy, x, g, m_ref, r_ref)
+    close(outs[0][0], dx_ref + (dres if extras else 0), 1e-5)
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
