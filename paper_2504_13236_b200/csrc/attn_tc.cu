@@ -27,6 +27,8 @@
 // of BASELINE.json); the block falls back to the unfused GEMM sequence otherwise.
 #include <cuda.h>
 
+#include <cstdlib>
+
 #include "gemm_common.cuh"
 #include "tc_ptx.cuh"
 
@@ -46,6 +48,8 @@ struct AttnParams {
   const float* stats;   // fwd: (M, S_sum) per (b, h, query) as float2, M in scaled-score units
   const float* D;       // bwd: D = rowdot(dO, O) per (b, h, query)
   unsigned long long* trace;  // nnt_attention_trace: CTA 0's per-iteration event times, or NULL
+  int l2hints;                // L2 policies on the TMA traffic: 0 none, 1 evict_last on the re-read tiles and
+                              // evict_first on the P / dA streams, 2 (default) evict_first on the streams only
 };
 
 // Pipeline trace (nnt_attention_trace, tools): CTA 0 records %globaltimer at kTraceEv events of
@@ -180,6 +184,8 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
     h = bh % P.H;
   };
   const int64_t c0 = blockIdx.x, G = gridDim.x;
+  const uint64_t pol_keep = P.l2hints == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+  const uint64_t pol_stream = P.l2hints ? l2_policy_evict_first() : l2_policy_evict_normal();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer: Q and the K ring
@@ -200,7 +206,8 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
         mbar_expect_tx_w(smem_u32(&full[stage]), TILE16);
-        tma_load_4d_w(smem_u32(smem + F_K + stage * TILE16), &mK, smem_u32(&full[stage]), 0, kb * TB, h, b);
+        tma_load_4d_w_hint(smem_u32(smem + F_K + stage * TILE16), &mK, smem_u32(&full[stage]), 0, kb * TB, h, b,
+                           pol_keep);  // K_kb: re-read by the (b, h)'s other query-block tasks
         if (lane == 0) trace_ev(P, 0, it_p);
         ++it_p;
         if (++stage == F_STAGES) {
@@ -225,7 +232,8 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(smem_u32(&vempty[stage]), phase ^ 1);
         mbar_expect_tx_w(smem_u32(&vfull[stage]), TILE16);
-        tma_load_4d_w(smem_u32(smem + F_V + stage * TILE16), &mV, smem_u32(&vfull[stage]), 0, kb * TB, h, b);
+        tma_load_4d_w_hint(smem_u32(smem + F_V + stage * TILE16), &mV, smem_u32(&vfull[stage]), 0, kb * TB, h, b,
+                           pol_keep);
         if (++stage == F_STAGES) {
           stage = 0;
           phase ^= 1;
@@ -432,7 +440,7 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
         if (lane == 0) {
           mbar_arrive(smem_u32(&pfull[pbuf]));
           if (warp == 2) trace_ev(P, 3, it);
-          tma_store_4d(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b);
+          tma_store_4d_hint(&mPst, smem_u32(piece), i * TB + hc * 64, qb * TB + quad * 32, h, b, pol_stream);
           bulk_commit();
         }
         if (i == 0 && pq >= 0) o_epilogue(tl - 1, pq, pb_, ph);  // the previous task's O
@@ -522,6 +530,8 @@ __global__ void __launch_bounds__(kAThreads, 1)
   };
   auto q_first = [&](int kb) { return P.causal ? kb : 0; };
   const int64_t c0 = blockIdx.x, G = gridDim.x;
+  const uint64_t pol_keep = P.l2hints == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+  const uint64_t pol_stream = P.l2hints ? l2_policy_evict_first() : l2_policy_evict_normal();
 
   if (warp == 0) {
     // ------------------------------------------------ TMA producer
@@ -545,10 +555,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
         mbar_expect_tx_w(fb, B_STAGE_TX);
         bulk_load_w(smem_u32(smem + B_D + stage * B_D_BYTES), P.D + ((int64_t)(b * P.H + h) * P.S + qb * TB),
                     B_D_BYTES, fb);
-        tma_load_4d_w(st, &mdO, fb, 0, qb * TB, h, b);
-        tma_load_4d_w(st + TILE16, &mQ, fb, 0, qb * TB, h, b);
-        tma_load_4d_w(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b);       // keys kb*128 + 0..63
-        tma_load_4d_w(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b);  // keys + 64..127
+        // dO_qb / Q_qb are re-read by the (b, h)'s other key-block tasks (kept in L2); P is read once
+        tma_load_4d_w_hint(st, &mdO, fb, 0, qb * TB, h, b, pol_keep);
+        tma_load_4d_w_hint(st + TILE16, &mQ, fb, 0, qb * TB, h, b, pol_keep);
+        tma_load_4d_w_hint(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b, pol_stream);       // keys kb*128 + 0..63
+        tma_load_4d_w_hint(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b, pol_stream);  // keys + 64..127
         if (lane == 0) trace_ev(P, 0, it_p);
         ++it_p;
         if (++stage == B_STAGES) {
@@ -709,7 +720,7 @@ __global__ void __launch_bounds__(kAThreads, 1)
         if (lane == 0) {
           mbar_arrive(smem_u32(&dafull[grp]));
           if (warp == 2) trace_ev(P, 3, it);
-          tma_store_4d(&mdA, smem_u32(piece), kb * TB + hc * 64, qb * TB + quad * 32, h, b);
+          tma_store_4d_hint(&mdA, smem_u32(piece), kb * TB + hc * 64, qb * TB + quad * 32, h, b, pol_stream);
           bulk_commit();
         }
         if (qb == P.nblk - 1) {
@@ -755,6 +766,10 @@ __global__ void __launch_bounds__(kAThreads, 1)
 int64_t persistent_grid(int64_t tasks) { return tasks < num_sms() ? tasks : num_sms(); }
 
 bool g_trace_on = false;
+int l2hints_on() {  // read per call (A/B runs switch it within one process)
+  const char* e = getenv("NNT_ATTN_L2HINT");
+  return e ? atoi(e) : 2;
+}
 unsigned long long* trace_ptr(int which) {
   if (!g_trace_on) return nullptr;
   void* p = nullptr;
@@ -797,7 +812,7 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
   NNT_REQUIRE(aligned16(P) && aligned16(O) && aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_fwd_pv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr,
-                 trace_ptr(0)};
+                 trace_ptr(0), l2hints_on()};
   CUtensorMap mQ, mK, mV, mPst, mO;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -826,7 +841,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
               "nnt_attention_bwd_kv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D,
-                 trace_ptr(1)};
+                 trace_ptr(1), l2hints_on()};
   CUtensorMap mV, mdO, mQ, mP, mdA, mdK, mdV;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
