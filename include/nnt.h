@@ -123,6 +123,26 @@ typedef enum {
   NNT_ACT_SOFTMAX = 5
 } nnt_act;
 
+/* Tensor-parallel reduction over peer memory (reading R35).
+ * A group of R ranks SUMs an fp32 [rows][cols] tensor of which each rank holds a partial.  Rows
+ * are owned in blocks of rows_per = ceil(rows / R): owner o holds rows [o rows_per, (o+1) rows_per).
+ * All pointers are device addresses usable by this rank's kernels: its own buffers and the
+ * peers' buffers mapped into its address space (symmetric memory over NVLink; on one GPU, plain
+ * allocations standing for the ranks).  Ownership stays with the caller.
+ *   recv[o]:  owner o's receive buffer, [R][rows_per][cols] fp32: slot w holds writer w's partial
+ *             of o's rows.  A GEMM with nnt_epilogue.scatter = comm writes its output rows
+ *             straight into these slots (the reduce-scatter's send, fused into the epilogue).
+ *   flags[q]: rank q's flag words, [2][NNT_TP_MAX] uint32, zero-initialised once; a reduction
+ *             is identified by a caller-chosen epoch (increasing, never 0). */
+#define NNT_TP_MAX 8
+typedef struct {
+  int R;                           /* group size, 1..NNT_TP_MAX */
+  int rank;                        /* this rank, 0..R-1         */
+  int64_t rows, cols;              /* the reduced tensor: rows x cols fp32 (row-major, ld = cols) */
+  float* recv[NNT_TP_MAX];
+  uint32_t* flags[NNT_TP_MAX];
+} nnt_tp_comm;
+
 typedef struct {
   const float* bias;      /* device fp32 [N] added to every row, or NULL          */
   const float* residual;  /* device fp32 [M][ld_residual] added, or NULL (may alias C
@@ -155,6 +175,10 @@ typedef struct {
    * stages.  bf16 operands, unbatched, non-causal, no activation; it uses the GEMM's split-K
    * workspace when the GEMM splits K (nnt_tile_gemm_workspace_bytes includes its slices). */
   float* a_rowsum;
+  /* Tensor-parallel row scatter (R35), or NULL: output row i is stored to
+   * scatter->recv[i / rows_per] slot scatter->rank instead of C (C is not written).  fp32 C,
+   * unbatched, M == scatter->rows, N == ldc == scatter->cols; no split-K / stream-K. */
+  const nnt_tp_comm* scatter;
 } nnt_epilogue;
 
 /* Workspace bytes that let nnt_tile_gemm split K for this shape (bf16 path; 0 when it would
@@ -527,6 +551,11 @@ typedef struct {
   int64_t heads;  /* attention heads of this shard (1..H); heads * h a multiple of 8 */
   int64_t ffn;    /* MLP hidden units of this shard (1..4E), a multiple of 8           */
   int add_bias;   /* 1 on exactly one shard of the group: it adds b_o, b_pr and the residuals */
+  const nnt_tp_comm* comm;  /* NULL: the stages write their partial sums locally (x1 / y / dh) and
+                               the caller reduces them (e.g. NCCL); else the partial-producing
+                               GEMM of each stage scatters its rows into comm->recv (R35) and the
+                               caller completes the SUM with nnt_tp_signal / nnt_tp_reduce_gather /
+                               nnt_tp_wait, which write x1 / y / dh on every rank */
 } nnt_block_tp;
 
 /* Workspace bytes of one shard (as nnt_block_workspace_size). */
@@ -554,6 +583,22 @@ nnt_status nnt_block_tp_bwd(const nnt_block_cfg* cfg, const nnt_block_tp* tp, co
                             int stage, const float* x, const float* x1, const void* saved, void* scratch,
                             const float* dy, float* dh, float* dx, const nnt_block_grads* g,
                             int accumulate_grads, nnt_stream_t stream);
+
+/* The rest of a tensor-parallel SUM after the GEMMs have scattered their partials (R35).  A rank
+ * calls, on its stream, in this order:
+ *   nnt_tp_signal(comm, epoch, 0)        tell every owner this rank's partials are in place;
+ *   nnt_tp_reduce_gather(comm, out, epoch) wait for the R writers of this rank's rows, sum the R
+ *                                        partials of each row in rank order (the same fixed
+ *                                        association on every rank: replicas stay bitwise
+ *                                        identical), write the sums into every rank's out[q]
+ *                                        (out[q]: rank q's [rows][cols] destination);
+ *   nnt_tp_signal(comm, epoch, 1)        tell every rank this rank's rows are gathered;
+ *   nnt_tp_wait(comm, epoch)             wait until every owner's rows have arrived here.
+ * After nnt_tp_wait the rank may read its out and reuse the recv buffers.  (On one GPU, ranks
+ * standing in one process may issue all signals before the reduce-gathers.) */
+nnt_status nnt_tp_signal(const nnt_tp_comm* comm, uint32_t epoch, int which, nnt_stream_t stream);
+nnt_status nnt_tp_reduce_gather(const nnt_tp_comm* comm, float* const* out, uint32_t epoch, nnt_stream_t stream);
+nnt_status nnt_tp_wait(const nnt_tp_comm* comm, uint32_t epoch, nnt_stream_t stream);
 
 /* ------------------------------------------------------------------------- */
 /* Tile-task DAG (STF rules S:46)                               */

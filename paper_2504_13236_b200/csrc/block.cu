@@ -121,6 +121,7 @@ struct Ctx {
   const nnt_block_bwd_links* links;  // nnt_block_bwd_streams: fused cross-layer bias sums (or NULL)
   bool ln_rows;                      // the LayerNorm backward fuses the column sums of dx (every E)
   bool fused_attn;                   // bf16, h = 64, S % 128 == 0: the fused attention tile kernels (R33)
+  const nnt_tp_comm* comm;           // nnt_block_tp with a comm: the partial-producing GEMMs scatter (R35)
   template <typename P>
   P* s(size_t off) const { return reinterpret_cast<P*>(sv + off); }
   template <typename P>
@@ -203,6 +204,7 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
         e.residual = xin;
         e.ld_residual = E;
       }
+      e.scatter = x.comm;  // tensor-parallel partial x1 -> its owners' receive slots (R35)
       return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, Ea, nullptr, 1.f, x.s<void>(x.L.O), Ea, nullptr, p->w_o, Ea,
                   nullptr, 0.f, x.x1, NNT_F32, E, nullptr, &e);
     case NNT_OP_LN2:
@@ -221,6 +223,7 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
         e.residual = x.x1;
         e.ld_residual = E;
       }
+      e.scatter = x.comm;
       return gemm(x, NNT_NOTRANS, NNT_TRANS, T, E, F, nullptr, 1.f, x.s<void>(x.L.g), F, nullptr, p->w_pr, F,
                   nullptr, 0.f, y, NNT_F32, E, nullptr, &e);
   }
@@ -265,8 +268,9 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_TRANS, NNT_NOTRANS, F, E, T, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr,
                   x.s<void>(x.L.h2), E, nullptr, beta, g->w_fc, NNT_F32, E, nullptr, &ws);
     case NNT_OP_FC_DX:
+      e.scatter = x.comm;  // tensor-parallel partial dL/dh2 (R35)
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, F, nullptr, 1.f, x.k<void>(x.L.du), F, nullptr, p->w_fc, E,
-                  nullptr, 0.f, x.dh, NNT_F32, E, nullptr, nullptr);
+                  nullptr, 0.f, x.dh, NNT_F32, E, nullptr, x.comm ? &e : nullptr);
     case NNT_OP_LN2_BWD:
       // b_o's gradient sum_t dx1 is the column sum of this LayerNorm's output: fused
       return nnt_layernorm_bwd(x.dh, E, x.x1, E, x.s<float>(x.L.mean2),
@@ -335,8 +339,9 @@ nnt_status run_bwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       return gemm(x, NNT_TRANS, NNT_NOTRANS, 3 * Ea, E, T, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * Ea, nullptr,
                   x.s<void>(x.L.h1), E, nullptr, beta, g->w_qkv, NNT_F32, E, nullptr, &ws);
     case NNT_OP_QKV_DX:
+      e.scatter = x.comm;  // tensor-parallel partial dL/dh1 (R35)
       return gemm(x, NNT_NOTRANS, NNT_NOTRANS, T, E, 3 * Ea, nullptr, 1.f, x.k<void>(x.L.dqkv), 3 * Ea, nullptr,
-                  p->w_qkv, E, nullptr, 0.f, x.dh, NNT_F32, E, nullptr, nullptr);
+                  p->w_qkv, E, nullptr, 0.f, x.dh, NNT_F32, E, nullptr, x.comm ? &e : nullptr);
     case NNT_OP_LN1_BWD:
       return nnt_layernorm_bwd(x.dh, E, xin, E, x.s<float>(x.L.mean1), x.s<float>(x.L.rstd1), p->ln1_g,
                                T, E, x.k<float>(x.L.dx1), dx, E, x.links ? x.links->dx_bf16 : nullptr, g->ln1_g,
@@ -364,6 +369,7 @@ Ctx make_ctx(const nnt_block_cfg& c, void* saved, void* scratch, cudaStream_t st
   x.sc = (uint8_t*)scratch;
   x.Ea = x.H * x.Dh;
   x.add_bias = tp ? tp->add_bias != 0 : true;
+  x.comm = tp ? tp->comm : nullptr;
   x.L = make_layout(c, x.H, x.F);
   x.x1 = reinterpret_cast<float*>(x.sv + x.L.x1);
   x.dh = reinterpret_cast<float*>(x.sc + x.L.dh);
@@ -395,6 +401,10 @@ nnt_status check_tp(const nnt_block_cfg* c, const nnt_block_tp* tp) {
               (long long)tp->ffn, (long long)(4 * c->E));
   NNT_REQUIRE(tp->ffn % 8 == 0, NNT_ERR_ALIGN, "nnt_block_tp: shard ffn width must be a multiple of 8");
   NNT_REQUIRE(tp->add_bias == 0 || tp->add_bias == 1, NNT_ERR_ARG, "nnt_block_tp: add_bias must be 0 or 1");
+  NNT_REQUIRE(!tp->comm || (tp->comm->rows == c->B * c->S && tp->comm->cols == c->E), NNT_ERR_SHAPE,
+              "nnt_block_tp: comm reduces %lld x %lld, the block's activations are %lld x %lld",
+              (long long)(tp->comm ? tp->comm->rows : 0), (long long)(tp->comm ? tp->comm->cols : 0),
+              (long long)(c->B * c->S), (long long)c->E);
   return NNT_OK;
 }
 

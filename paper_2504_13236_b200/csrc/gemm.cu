@@ -109,6 +109,24 @@ extern "C" nnt_status nnt_tile_gemm(int trans_a, int trans_b, int64_t M, int64_t
     g.rowvec = epi->rowvec;
     g.rowscale = epi->rowscale;
     g.a_rowsum = epi->a_rowsum;
+    if (epi->scatter) {  // R35 tensor-parallel row scatter
+      const nnt_tp_comm* cm = epi->scatter;
+      NNT_REQUIRE(cm->R >= 1 && cm->R <= NNT_TP_MAX && cm->rank >= 0 && cm->rank < cm->R, NNT_ERR_ARG,
+                  "nnt_tile_gemm: scatter R=%d rank=%d", cm->R, cm->rank);
+      NNT_REQUIRE(c_dtype == NNT_F32 && b0 == 1 && b1 == 1 && M == cm->rows && N == cm->cols && ldc == N &&
+                      beta == 0.f && epi->act == NNT_ACT_NONE && !epi->a_rowsum && !epi->row_stats,
+                  NNT_ERR_UNSUPPORTED,
+                  "nnt_tile_gemm: scatter needs fp32 C, unbatched, M == rows, N == ldc == cols, beta 0, no activation");
+      g.scat_R = cm->R;
+      g.scat_rank = cm->rank;
+      g.scat_rows = (cm->rows + cm->R - 1) / cm->R;
+      for (int o = 0; o < cm->R; ++o) {
+        NNT_REQUIRE(cm->recv[o], NNT_ERR_NULL, "nnt_tile_gemm: scatter recv[%d] NULL", o);
+        g.scat[o] = cm->recv[o];
+      }
+      g.workspace = nullptr;  // no split-K / stream-K partials
+      g.workspace_bytes = 0;
+    }
     NNT_REQUIRE(!epi->a_rowsum || (a_dtype == NNT_BF16 && b0 == 1 && b1 == 1 && epi->causal == NNT_CAUSAL_NONE &&
                                    epi->act == NNT_ACT_NONE && !epi->row_stats),
                 NNT_ERR_UNSUPPORTED,

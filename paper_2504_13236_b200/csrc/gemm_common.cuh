@@ -34,7 +34,19 @@ struct GemmArgs {
   const float* rowvec;  // NNT_ACT_SOFTMAX_BWD: D per row
   float rowscale;
   float* a_rowsum;  // R27: beta * a_rowsum + alpha * sum_k op(A)[i][k] (bias gradient of dW GEMMs)
+  // R35 tensor-parallel row scatter: row i -> scat[i / scat_rows] + (scat_rank * scat_rows + i % scat_rows) * ldc
+  int scat_R, scat_rank;
+  int64_t scat_rows;
+  float* scat[NNT_TP_MAX];
 };
+
+// Base pointer for row i of C under the R35 row scatter (row i's address = base + i * ldc), or Cb.
+template <typename TC>
+__device__ __forceinline__ TC* scatter_row_base(const GemmArgs& g, TC* Cb, int64_t i) {
+  if (!g.scat_R) return Cb;
+  const int64_t o = i / g.scat_rows;
+  return reinterpret_cast<TC*>(g.scat[o]) + ((int64_t)g.scat_rank - o) * g.scat_rows * g.ldc;
+}
 
 nnt_status gemm_simt_launch(const GemmArgs& a, cudaStream_t s);
 // *kernels (optional) receives the number of kernels launched (2 with a split-K reduce).
@@ -68,7 +80,7 @@ __device__ __forceinline__ void epilogue_store(const GemmArgs& g, TC* __restrict
   } else if (g.act == NNT_ACT_GELU_BWD) {
     out = pre * gelu_grad_f(to_f32(auxb[i * g.ld_aux + j]));
   }
-  Cb[i * g.ldc + j] = from_f32<TC>(out);
+  scatter_row_base(g, Cb, i)[i * g.ldc + j] = from_f32<TC>(out);
 }
 
 }  // namespace nnt

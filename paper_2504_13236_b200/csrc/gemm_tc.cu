@@ -1174,7 +1174,7 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         if (P.tma_store)
           stage_store(&tmC);
         else
-          direct_store<TC, W>(g.M, g.N, g.ldc, Cb, row, ti.n0 + c, v);
+          direct_store<TC, W>(g.M, g.N, g.ldc, scatter_row_base(g, Cb, row), row, ti.n0 + c, v);
       }
       if constexpr (C::ROWSUM) {
         // R27: this row's sum of op(A) over the task's K range (one warp per lane quadrant)
@@ -1438,7 +1438,7 @@ namespace {
 // C (and the GELU aux) can be written by TMA tensor stores
 bool c_tma_ok(const GemmArgs& a, size_t es) {
   auto ok16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; };
-  return ok16(a.C) && (a.ldc * es) % 16 == 0 && (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
+  return !a.scat_R && ok16(a.C) && (a.ldc * es) % 16 == 0 && (a.batch1 <= 1 || (a.sc1 > 0 && (a.sc1 * es) % 16 == 0)) &&
          (a.batch0 <= 1 || (a.sc0 > 0 && (a.sc0 * es) % 16 == 0)) &&
          (a.act != NNT_ACT_GELU || (ok16(a.aux) && (a.ld_aux * es) % 16 == 0));
 }
@@ -1910,8 +1910,8 @@ nnt_status gemm_tc_launch(const GemmArgs& a, cudaStream_t s, int* kernels) {
   if (!ws_ok) splits = 1;
   // stream-K (a workspace big enough for its slots) replaces split-K: no partial round trip
   // through HBM for the whole tile grid and no reduce launch
-  const bool sk = sk_possible(a);
-  if (sk) splits = 1;
+  const bool sk = sk_possible(a) && !a.scat_R;
+  if (sk || a.scat_R) splits = 1;
   if (kernels) *kernels = splits > 1 && !fused_reduce_ok(a, splits) ? 2 : 1;
   if (a.act == NNT_ACT_ROWSTATS) return launch_bn<128, float, EPI_ROWSTATS>(a, s, 1);
   if (a.c_dtype == NNT_F32) return launch_tc<float>(a, s, splits, sk);

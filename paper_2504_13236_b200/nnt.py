@@ -50,7 +50,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
            "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv",
-           "nnt_stf_build", "nnt_attention_trace")
+           "nnt_stf_build", "nnt_attention_trace", "nnt_tp_signal", "nnt_tp_reduce_gather", "nnt_tp_wait")
 
 
 class NNTError(RuntimeError):
@@ -60,11 +60,20 @@ class NNTError(RuntimeError):
 
 
 # ---------------------------------------------------------------- structs
+NNT_TP_MAX = 8
+
+
+class nnt_tp_comm(C.Structure):
+    _fields_ = [("R", C.c_int), ("rank", C.c_int), ("rows", C.c_int64), ("cols", C.c_int64),
+                ("recv", C.c_void_p * NNT_TP_MAX), ("flags", C.c_void_p * NNT_TP_MAX)]
+
+
 class nnt_epilogue(C.Structure):
     _fields_ = [("bias", C.c_void_p), ("residual", C.c_void_p), ("ld_residual", C.c_int64), ("act", C.c_int),
                 ("aux", C.c_void_p), ("ld_aux", C.c_int64), ("causal", C.c_int), ("workspace", C.c_void_p),
                 ("workspace_bytes", C.c_size_t), ("row_stats", C.c_void_p), ("ld_row_stats", C.c_int64),
-                ("rowvec", C.c_void_p), ("rowscale", C.c_float), ("a_rowsum", C.c_void_p)]
+                ("rowvec", C.c_void_p), ("rowscale", C.c_float), ("a_rowsum", C.c_void_p),
+                ("scatter", C.POINTER(nnt_tp_comm))]
 
 
 class nnt_adam_hparams(C.Structure):
@@ -106,7 +115,7 @@ class nnt_block_bwd_links(C.Structure):
 
 
 class nnt_block_tp(C.Structure):
-    _fields_ = [("heads", C.c_int64), ("ffn", C.c_int64), ("add_bias", C.c_int)]
+    _fields_ = [("heads", C.c_int64), ("ffn", C.c_int64), ("add_bias", C.c_int), ("comm", C.POINTER(nnt_tp_comm))]
 
 
 class nnt_task(C.Structure):
@@ -173,6 +182,9 @@ _sig = {
                                 _vp, _vp, _vp, _vp, _vp, _vp]),
     "nnt_block_tp_bwd": (_i32, [C.POINTER(nnt_block_cfg), C.POINTER(nnt_block_tp), C.POINTER(nnt_block_params), _i32,
                                 _vp, _vp, _vp, _vp, _vp, _vp, _vp, C.POINTER(nnt_block_grads), _i32, _vp]),
+    "nnt_tp_signal": (_i32, [C.POINTER(nnt_tp_comm), C.c_uint32, _i32, _vp]),
+    "nnt_tp_reduce_gather": (_i32, [C.POINTER(nnt_tp_comm), C.POINTER(_vp), C.c_uint32, _vp]),
+    "nnt_tp_wait": (_i32, [C.POINTER(nnt_tp_comm), C.c_uint32, _vp]),
     "nnt_op_name": (C.c_char_p, [_i32]),
     "nnt_block_dag_describe": (_i32, [C.POINTER(nnt_block_cfg), _i32, C.POINTER(nnt_task), _i64, _P64,
                                       C.POINTER(nnt_launch_group), _i64, _P64]),
@@ -256,12 +268,38 @@ def nnt_partition(n_units, n_ranks, rank):
 
 def make_epilogue(bias=None, residual=None, ld_residual=0, act=NNT_ACT_NONE, aux=None, ld_aux=0,
                   causal=NNT_CAUSAL_NONE, workspace=None, workspace_bytes=0, row_stats=None, ld_row_stats=0,
-                  rowvec=None, rowscale=1.0, a_rowsum=None):
-    """The caller keeps every tensor passed here alive until the launch has run."""
+                  rowvec=None, rowscale=1.0, a_rowsum=None, scatter=None):
+    """The caller keeps every tensor passed here alive until the launch has run (scatter: an
+    nnt_tp_comm, kept alive too)."""
     if workspace is not None and not workspace_bytes and hasattr(workspace, "numel"):
         workspace_bytes = workspace.numel() * workspace.element_size()
     return nnt_epilogue(ptr(bias), ptr(residual), ld_residual, act, ptr(aux), ld_aux, causal, ptr(workspace),
-                        workspace_bytes, ptr(row_stats), ld_row_stats, ptr(rowvec), rowscale, ptr(a_rowsum))
+                        workspace_bytes, ptr(row_stats), ld_row_stats, ptr(rowvec), rowscale, ptr(a_rowsum),
+                        C.pointer(scatter) if scatter is not None else None)
+
+
+def make_tp_comm(R, rank, rows, cols, recv, flags):
+    """nnt_tp_comm for rank `rank` of R: recv[o] / flags[o] are device tensors or raw device addresses
+    (rank o's buffers as mapped into this process).  Keep the buffers alive while it is used."""
+    c = nnt_tp_comm()
+    c.R, c.rank, c.rows, c.cols = R, rank, rows, cols
+    for o in range(R):
+        c.recv[o] = recv[o] if isinstance(recv[o], int) else ptr(recv[o])
+        c.flags[o] = flags[o] if isinstance(flags[o], int) else ptr(flags[o])
+    return c
+
+
+def nnt_tp_signal(comm, epoch, which, stream=None):
+    return check(lib.nnt_tp_signal(C.byref(comm), epoch, which, _stream(stream)))
+
+
+def nnt_tp_reduce_gather(comm, out, epoch, stream=None):
+    arr = (_vp * len(out))(*[o if isinstance(o, int) else ptr(o) for o in out])
+    return check(lib.nnt_tp_reduce_gather(C.byref(comm), arr, epoch, _stream(stream)))
+
+
+def nnt_tp_wait(comm, epoch, stream=None):
+    return check(lib.nnt_tp_wait(C.byref(comm), epoch, _stream(stream)))
 
 
 def nnt_tile_gemm_workspace_bytes(M, N, K, c_dtype, act=NNT_ACT_NONE, causal=NNT_CAUSAL_NONE, batch_items=1):

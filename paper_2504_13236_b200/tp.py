@@ -77,7 +77,12 @@ class TPBlockStack:
     may be world size 1).  forward / probe_loss / backward / adam / train_step like
     model.BlockStack; params_of / grads_of give this rank's shard."""
 
-    def __init__(self, cfg: StackConfig, layer_params, process_group, device="cuda"):
+    def __init__(self, cfg: StackConfig, layer_params, process_group, device="cuda", fused=False):
+        """fused: the four SUMs per block run over peer memory (R35): the partial-producing GEMMs
+        scatter their rows into the owners' receive slots, the owners reduce in rank order and
+        gather the sums to every rank (libnnt nnt_tp_*); x1 / y / dh and the receive and flag
+        buffers are then symmetric allocations (torch symmetric memory when R > 1, so every
+        rank can address every other rank's copy).  Else NCCL all-reduces between the stages."""
         assert len(layer_params) == cfg.L and process_group is not None
         self.cfg, self.pg = cfg, process_group
         self.dev = torch.device(device)
@@ -113,10 +118,25 @@ class TPBlockStack:
         self.saved = [torch.empty(saved_b, device=self.dev, dtype=torch.uint8) for _ in range(cfg.L)]
         self.scratch = torch.zeros(scratch_b, device=self.dev, dtype=torch.uint8)  # zero: split-K counters
         act = dict(device=self.dev, dtype=torch.float32)
-        self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
-        self.x1 = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L)]
+        self.fused = fused
+        self.peer = {}  # data_ptr of a symmetric buffer -> [rank q's address of it]
+        if fused:
+            T = cfg.B * cfg.S
+            shape = (cfg.B, cfg.S, E)
+            self.xs = [torch.empty(*shape, **act)] + [self._sym(shape, torch.float32) for _ in range(cfg.L)]
+            self.x1 = [self._sym(shape, torch.float32) for _ in range(cfg.L)]
+            self.dh = self._sym(shape, torch.float32)
+            self.recv = self._sym((self.R, -(-T // self.R), E), torch.float32)
+            self.flags = self._sym((2 * nnt.NNT_TP_MAX,), torch.int32)
+            self.comm = nnt.make_tp_comm(self.R, self.rank, T, E, self.peer[self.recv.data_ptr()],
+                                         self.peer[self.flags.data_ptr()])
+            self.tp.comm = nnt.C.pointer(self.comm)
+            self.epoch = 0
+        else:
+            self.xs = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L + 1)]
+            self.x1 = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(cfg.L)]
+            self.dh = torch.empty(cfg.B, cfg.S, E, **act)
         self.dy = [torch.empty(cfg.B, cfg.S, E, **act) for _ in range(2)]
-        self.dh = torch.empty(cfg.B, cfg.S, E, **act)
         self.loss = torch.zeros(1, **act)
         self.dot_scratch = torch.empty(nnt.nnt_dot_scratch_bytes(cfg.T * E), device=self.dev, dtype=torch.uint8)
         self.step_count = 0
@@ -147,8 +167,31 @@ class TPBlockStack:
     def grads_of(self, l):
         return self.params_of(l, self.g)
 
+    def _sym(self, shape, dtype):
+        """A zeroed buffer that every rank of the group can address (self.peer[ptr][q] = rank q's
+        copy as mapped here): a plain allocation when R == 1, torch symmetric memory otherwise."""
+        if self.R == 1:
+            t = torch.zeros(shape, device=self.dev, dtype=dtype)
+            self.peer[t.data_ptr()] = [t.data_ptr()]
+            return t
+        import torch.distributed._symmetric_memory as symm_mem
+        t = symm_mem.empty(shape, device=self.dev, dtype=dtype)
+        t.zero_()
+        h = symm_mem.rendezvous(t, self.pg)
+        self.peer[t.data_ptr()] = [int(p) for p in h.buffer_ptrs]
+        torch.distributed.barrier(group=self.pg)  # every rank's copy zeroed before any peer writes
+        return t
+
     def _sum(self, t):
-        torch.distributed.all_reduce(t, group=self.pg)
+        if not self.fused:
+            torch.distributed.all_reduce(t, group=self.pg)
+            return
+        # R35: the GEMMs have scattered this rank's partials; complete the SUM into every rank's t
+        self.epoch += 1
+        nnt.nnt_tp_signal(self.comm, self.epoch, 0)
+        nnt.nnt_tp_reduce_gather(self.comm, self.peer[t.data_ptr()], self.epoch)
+        nnt.nnt_tp_signal(self.comm, self.epoch, 1)
+        nnt.nnt_tp_wait(self.comm, self.epoch)
 
     def forward(self, x=None):
         if x is not None:

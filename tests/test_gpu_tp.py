@@ -45,7 +45,11 @@ class _Shard:
         self.scratch = torch.zeros(kb, device="cuda", dtype=torch.uint8)
 
 
-def _run_shards(E, H, S, B, R, dtype, tile, seed=11):
+def _run_shards(E, H, S, B, R, dtype, tile, seed=11, fused=False):
+    """fused: the partial-producing GEMMs scatter their rows into the owners' receive slots and the
+    SUM is completed by nnt_tp_signal / nnt_tp_reduce_gather / nnt_tp_wait (R35), with the R ranks
+    standing in this process (their buffers plain allocations); else the test sums the partials.
+    Both sum in rank order (p0 + p1 + ...), so the two runs must agree bitwise."""
     bf = dtype == "bf16"
     sc = model.StackConfig(L=1, E=E, H=H, S=S, B=B, tile_e=tile, tile_f=tile, tile_s=tile, tile_t=tile,
                            dtype=dtype)
@@ -55,13 +59,35 @@ def _run_shards(E, H, S, B, R, dtype, tile, seed=11):
     x = nnt_inputs.make_x(E, S, 0, B, seed=seed + 1)
     dy = nnt_inputs.make_r(E, S, 0, B, seed=seed + 1) / (B * S)
     X, DY = dev(x), dev(dy)
-    x1 = [torch.empty_like(X) for _ in range(R)]
-    y = [torch.empty_like(X) for _ in range(R)]
-    dh = [torch.empty_like(X) for _ in range(R)]
+    x1 = [torch.full_like(X, float("nan")) for _ in range(R)]
+    y = [torch.full_like(X, float("nan")) for _ in range(R)]
+    dh = [torch.full_like(X, float("nan")) for _ in range(R)]
     dx = [torch.empty_like(X) for _ in range(R)]
+    T = B * S
+    if fused:
+        rows_per = -(-T // R)
+        recv = [torch.full((R, rows_per, E), float("nan"), device="cuda") for _ in range(R)]
+        flags = [torch.zeros(2 * nnt.NNT_TP_MAX, device="cuda", dtype=torch.int32) for _ in range(R)]
+        comms = [nnt.make_tp_comm(R, r, T, E, recv, flags) for r in range(R)]
+        for r, sh in enumerate(shards):
+            sh.tp.comm = nnt.C.pointer(comms[r])
+        epoch = [0]
 
     def allsum(bufs):
-        s = torch.stack(bufs).sum(0)
+        if fused:  # every rank's GEMMs have scattered; the ranks complete the SUM in phases
+            epoch[0] += 1
+            for r in range(R):
+                nnt.nnt_tp_signal(comms[r], epoch[0], 0)
+            for r in range(R):
+                nnt.nnt_tp_reduce_gather(comms[r], bufs, epoch[0])
+            for r in range(R):
+                nnt.nnt_tp_signal(comms[r], epoch[0], 1)
+            for r in range(R):
+                nnt.nnt_tp_wait(comms[r], epoch[0])
+            return
+        s = bufs[0].clone()
+        for b in bufs[1:]:
+            s += b
         for b in bufs:
             b.copy_(s)
 
@@ -104,6 +130,27 @@ def test_tp_shards_match_oracle(E, H, S, B, R, dtype, tile, tol):
                 assert torch.equal(shards[r].g[n], shards[0].g[n]), (n, r)
 
 
+@pytest.mark.parametrize("E,H,S,B,R,dtype,tile", [
+    (64, 4, 32, 2, 1, "f32", 16), (64, 4, 32, 2, 4, "f32", 16), (96, 6, 32, 2, 3, "f32", 16),
+    (256, 4, 256, 2, 2, "bf16", 1024), (768, 12, 128, 2, 3, "bf16", 1024),
+], ids=["f32-R1", "f32-R4", "f32-R3-ragged", "bf16-R2", "bf16-E768-R3-ragged"])
+def test_tp_fused_reduction_equals_summed_partials(E, H, S, B, R, dtype, tile):
+    """R35: the partial-producing GEMMs (out-projection, projection, FC-dX, QKV-dX) write their
+    rows straight into the owners' receive slots and the owners sum them in rank order and
+    gather the sums to every rank: y, dx and every gradient bitwise equal to the run whose
+    partials the test sums in the same order (T = 64 / 256 rows over 3 ranks: a short last
+    owner), and within tolerance of the oracle."""
+    a = _run_shards(E, H, S, B, R, dtype, tile, fused=True)
+    b = _run_shards(E, H, S, B, R, dtype, tile, fused=False)
+    for r in range(R):
+        assert torch.equal(a[1][r], b[1][r]) and torch.equal(a[2][r], b[2][r]), r
+        for n in a[0][r].g:
+            assert torch.equal(a[0][r].g[n], b[0][r].g[n]), (r, n)
+    tol = 1e-4 if dtype == "f32" else 2e-2
+    close(host(a[1][0]), a[3], tol, "y")
+    close(host(a[2][0]), a[4], tol, "dx")
+
+
 def test_tp_argument_errors():
     sc = model.StackConfig(L=1, E=64, H=4, S=32, B=2, tile_e=16, tile_f=16, tile_s=16, tile_t=16, dtype="f32")
     cfg = sc.block_cfg()
@@ -121,6 +168,35 @@ def _free_port():
     p = s.getsockname()[1]
     s.close()
     return p
+
+
+@pytest.mark.timeout(300)
+def test_tp_stack_fused_world1_equals_nccl():
+    """TPBlockStack with the fused peer-memory SUMs (R35) on a group of one rank: two training
+    steps bitwise equal to the NCCL-reduced stack (bf16, 2 layers)."""
+    import torch.distributed as dist
+    own = not dist.is_initialized()
+    if own:
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", 0))
+    try:
+        E, H, S, B, L = 256, 4, 256, 2, 2
+        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", lr=1e-3)
+        layers = [nnt_inputs.make_params(E, seed=23, layer=l, n_layers=L) for l in range(L)]
+        runs = []
+        for fused in (True, False):
+            st = tp.TPBlockStack(sc, layers, dist.group.WORLD, fused=fused)
+            for t in (1, 2):
+                x = dev(nnt_inputs.make_x(E, S, 0, B, seed=40 + t))
+                r = dev(nnt_inputs.make_r(E, S, 0, B, seed=40 + t))
+                st.train_step(x, r)
+            torch.cuda.synchronize()
+            runs.append((st.w.clone(), st.g.clone(), st.xs[-1].clone(), st.loss.clone()))
+        for a, b in zip(*runs):
+            assert torch.equal(a, b)
+    finally:
+        if own:
+            dist.destroy_process_group()
 
 
 @pytest.mark.timeout(300)
