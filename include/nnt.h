@@ -302,6 +302,17 @@ int nnt_attention_fused_supported(int64_t S, int64_t h);
  * [B*H*S][2] = (M in scaled-score units, S_sum); P: device bf16 [B][H][S][S]; O: device bf16
  * [B][S][H*h].  h == 64, S % 128 == 0 (else NNT_ERR_UNSUPPORTED); 16-byte aligned.
  */
+/* Softmax subroutine 1 of the bf16 attention, per (b, n, query q): the score row
+ * x[k] = scale * sum_i Q[q][i] K[k][i] over keys k (k <= q when causal) is formed tile by tile on
+ * the tensor cores and reduced on chip -- never stored (R26) -- to stats[(b*H + n)*S + q] =
+ * (M, S) = (max_k x[k], sum_k e^{x[k] - M}) as two floats (the input nnt_attention_fwd_pv reads).
+ * qkv as above; stats: device fp32 [B][H][S][2].  Same conditions (h = 64, S % 128 == 0). */
+nnt_status nnt_attention_stats(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t h, float scale, int causal,
+                               float* stats, nnt_stream_t stream);
+/* 1 unless NNT_ATTN_STATS=0 in the environment: the block uses nnt_attention_stats for the row
+ * statistics (else the NNT_ACT_ROWSTATS score GEMM). */
+int nnt_attention_stats_enabled(void);
+
 nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t h, float scale,
                                 int causal, const float* stats, void* P, void* O, nnt_stream_t stream);
 

@@ -460,6 +460,226 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
   }
 }
 
+// ============================================================================ row statistics
+// Softmax subroutine 1 on the score tiles of one (b, h, query block) task, formed on
+// the tensor cores and never stored (R26): per query row the running (max, sumexp) over the key
+// tiles, merged with the rule of R10.  The pipeline of the forward kernel without the value
+// product: warp 0 streams Q (per task) and the K tiles (3-stage ring), warp 1 issues S = Q K^T
+// into three TMEM buffers, two ping-pong groups of 8 epilogue warps (iterations g % 2) reduce a
+// tile's 32-key halves into per-lane running pairs, and at the end of a task each epilogue warp
+// deposits its pair in a shared-memory slot; warp 18 merges the 4 pairs of each row (group 0 /
+// 1 x key half 0 / 1, fixed order) and writes (M, S) -- M in scaled-score units, S = sum
+// e^{scale x - M} -- the format of the NNT_ACT_ROWSTATS GEMM epilogue.
+constexpr int R_STAGES = 3;
+constexpr int R_Q = 0, R_K = 2 * TILE16, R_X = R_K + R_STAGES * TILE16;  // X: [2][4 quad][4][32] float2
+constexpr int R_BAR = R_X + 2 * 4 * 4 * 32 * 8;
+constexpr int R_SMEM = R_BAR + 256 + 1024;
+constexpr int kAThreadsR = kAThreads + 32;  // + the merge warp (warp 18)
+
+__global__ void __launch_bounds__(kAThreadsR, 1)
+    attn_stats_kernel(const __grid_constant__ AttnParams P, const __grid_constant__ CUtensorMap mQ,
+                      const __grid_constant__ CUtensorMap mK, float* __restrict__ stats) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + R_BAR);
+  uint64_t* full = bars;        // [3] K tile landed
+  uint64_t* empty = bars + 3;   // [3] K tile consumed (its S MMA done)
+  uint64_t* qfull = bars + 6;   // [2]
+  uint64_t* qempty = bars + 8;  // [2] the task's last S MMA done
+  uint64_t* sfull = bars + 10;  // [3] S accumulator ready
+  uint64_t* sempty = bars + 13; // [3] drained (8 warps)
+  uint64_t* xfull = bars + 16;  // [2] a task's 16 per-warp pairs deposited (16 warps)
+  uint64_t* xempty = bars + 18; // [2] merged (warp 18)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  float2* xs = reinterpret_cast<float2*>(smem + R_X);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int BH = P.B * P.H;
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < 3; ++i) {
+      mbar_init(smem_u32(&full[i]), 1);
+      mbar_init(smem_u32(&empty[i]), 1);
+      mbar_init(smem_u32(&sfull[i]), 1);
+      mbar_init(smem_u32(&sempty[i]), kEW / 2);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(smem_u32(&qfull[i]), 1);
+      mbar_init(smem_u32(&qempty[i]), 1);
+      mbar_init(smem_u32(&xfull[i]), kEW);
+      mbar_init(smem_u32(&xempty[i]), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) tmem_alloc512(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  NNT_PDL_ENTRY();
+  auto decode = [&](int64_t t, int& qb, int& b, int& h) {  // heaviest first, as the forward
+    const int level = (int)(t / BH), bh = (int)(t % BH);
+    qb = P.nblk - 1 - level;
+    b = bh / P.H;
+    h = bh % P.H;
+  };
+  const int64_t c0 = blockIdx.x, G = gridDim.x;
+  const uint64_t pol_keep = P.l2hints == 1 ? l2_policy_evict_last() : l2_policy_evict_normal();
+
+  if (warp == 0) {
+    // ------------------------------------------------ TMA producer: Q and the K ring
+    int stage = 0;
+    uint32_t phase = 0;
+    int tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int qs = tl & 1;
+      mbar_wait(smem_u32(&qempty[qs]), ((tl >> 1) & 1) ^ 1);
+      mbar_expect_tx_w(smem_u32(&qfull[qs]), TILE16);
+      tma_load_4d_w(smem_u32(smem + R_Q + qs * TILE16), &mQ, smem_u32(&qfull[qs]), 0, qb * TB, h, b);
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
+        mbar_expect_tx_w(smem_u32(&full[stage]), TILE16);
+        tma_load_4d_w_hint(smem_u32(smem + R_K + stage * TILE16), &mK, smem_u32(&full[stage]), 0, kb * TB, h, b,
+                           pol_keep);
+        if (++stage == R_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    pdl_trigger();
+  } else if (warp == 1) {
+    // ------------------------------------------------ MMA issuer: S(g) = Q K_kb^T into buffer g % 3
+    const uint32_t id_s = idesc_of(false, false, TB);
+    int tl = 0;
+    int64_t g = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int qs = tl & 1, nk = P.causal ? qb + 1 : P.nblk;
+      mbar_wait(smem_u32(&qfull[qs]), (tl >> 1) & 1);
+      for (int i = 0; i < nk; ++i, ++g) {
+        const int sb = (int)(g % 3), stg = (int)(g % R_STAGES);
+        mbar_wait(smem_u32(&sempty[sb]), (uint32_t)(((g / 3) & 1) ^ 1));
+        mbar_wait(smem_u32(&full[stg]), (uint32_t)((g / R_STAGES) & 1));
+        tc_fence_after();
+        const uint32_t sq = smem_u32(smem + R_Q + qs * TILE16), sk = smem_u32(smem + R_K + stg * TILE16);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk)
+          mma_bf16_w(tmem + sb * TB, make_sdesc(sq + kk * 32, 16, 1024), make_sdesc(sk + kk * 32, 16, 1024), id_s,
+                     kk > 0 ? 1u : 0u);
+        mma_commit_w(smem_u32(&sfull[sb]));
+        mma_commit_w(smem_u32(&empty[stg]));
+        if (i == nk - 1) mma_commit_w(smem_u32(&qempty[qs]));
+      }
+    }
+  } else if (warp < 2 + kEW) {
+    // ------------------------------------------------ epilogue warps 2..17
+    const int grp = (warp - 2) >> 3, quad = warp & 3, hc = ((warp - 2) >> 2) & 1;
+    const float sc = P.scale * 1.4426950408889634f;  // log2-scaled scores: y = x * scale * log2(e)
+    int it = 0, tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int q = qb * TB + quad * 32 + lane;  // this lane's query row
+      const int nk = P.causal ? qb + 1 : P.nblk;
+      float m = -INFINITY, l = 0.f;  // running (max, sumexp) in log2 units over this warp's keys
+      for (int i = 0; i < nk; ++i, ++it) {
+        if ((it & 1) != grp) continue;
+        const int sb = it % 3;
+        mbar_wait(smem_u32(&sfull[sb]), (uint32_t)((it / 3) & 1));
+        tc_fence_after();
+        float v[64];
+        tmem_ld_cols<2>(tmem + sb * TB + hc * 64 + ((uint32_t)(quad * 32) << 16), v);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sempty[sb]));
+        const int key0 = i * TB + hc * 64;
+        int lim = 64;  // causal: keys <= q
+        if (P.causal && key0 + 63 > q) lim = q - key0 + 1;
+        if (lim >= 64) {
+          float m0 = fmaxf(v[0], v[1]), m1 = fmaxf(v[2], v[3]);
+#pragma unroll
+          for (int j = 4; j < 64; j += 4) {
+            m0 = fmaxf(m0, fmaxf(v[j], v[j + 1]));
+            m1 = fmaxf(m1, fmaxf(v[j + 2], v[j + 3]));
+          }
+          const float mn = fmaxf(m, fmaxf(m0, m1) * sc);
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 64; j += 4) {
+            s0 += ex2_approx(fmaf(v[j], sc, -mn));
+            s1 += ex2_approx(fmaf(v[j + 1], sc, -mn));
+            s2 += ex2_approx(fmaf(v[j + 2], sc, -mn));
+            s3 += ex2_approx(fmaf(v[j + 3], sc, -mn));
+          }
+          l = l * ex2_approx(m - mn) + ((s0 + s1) + (s2 + s3));
+          m = mn;
+        } else if (lim > 0) {  // diagonal tile: keys > q masked
+          float mx = -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < lim) mx = fmaxf(mx, v[j]);
+          const float mn = fmaxf(m, mx * sc);
+          float s = 0.f;
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j < lim) s += ex2_approx(fmaf(v[j], sc, -mn));
+          l = (m == -INFINITY ? 0.f : l * ex2_approx(m - mn)) + s;
+          m = mn;
+        }
+      }
+      // this warp's pair for the task -> slot (task parity, quad, grp * 2 + hc, lane)
+      const int xs_ = tl & 1;
+      mbar_wait(smem_u32(&xempty[xs_]), ((tl >> 1) & 1) ^ 1);
+      xs[((xs_ * 4 + quad) * 4 + grp * 2 + hc) * 32 + lane] = make_float2(m, l);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&xfull[xs_]));
+    }
+  } else {
+    // ------------------------------------------------ warp 18: merge the 4 pairs of each row
+    int tl = 0;
+    for (int64_t k = 0;; ++k, ++tl) {
+      const int64_t t = task_at(c0, G, k);
+      if (t >= P.num_tasks) break;
+      int qb, b, h;
+      decode(t, qb, b, h);
+      const int xs_ = tl & 1;
+      mbar_wait(smem_u32(&xfull[xs_]), (tl >> 1) & 1);
+      float2* out = reinterpret_cast<float2*>(stats) + ((int64_t)(b * P.H + h) * P.S + qb * TB);
+#pragma unroll 1
+      for (int quad = 0; quad < 4; ++quad) {
+        float2 pr[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) pr[w] = xs[((xs_ * 4 + quad) * 4 + w) * 32 + lane];
+        float M = fmaxf(fmaxf(pr[0].x, pr[1].x), fmaxf(pr[2].x, pr[3].x));
+        float S = 0.f;
+        if (M != -INFINITY) {
+#pragma unroll
+          for (int w = 0; w < 4; ++w)  // fixed order: (group 0, half 0), (0, 1), (1, 0), (1, 1)
+            if (pr[w].x != -INFINITY) S += pr[w].y * ex2_approx(pr[w].x - M);
+        }
+        out[quad * 32 + lane] = make_float2(M * 0.6931471805599453f, S);  // (scaled-score max, sumexp)
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&xempty[xs_]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_free512(tmem);
+  }
+}
+
 // ============================================================================ backward
 // smem: V[2] (task parity) | 3 stages of {dO_qb, Q_qb, P tile (2 x 16 KB)} | D slots [3] | barriers.
 // TMEM: dP[2] at columns 0 / 128, {dV, dK}[2] at 256 / 384 (+64 for dK).
@@ -804,6 +1024,34 @@ nnt_status nnt_attention_trace(int enable, uint64_t* host_out, int64_t cap) {
 }
 
 int nnt_attention_fused_supported(int64_t S, int64_t Dh) { return Dh == HD && S > 0 && S % TB == 0 ? 1 : 0; }
+
+// NNT_ATTN_STATS=0: the row statistics by the NNT_ACT_ROWSTATS score GEMM (A/B runs)
+int nnt_attention_stats_enabled() {
+  const char* e = getenv("NNT_ATTN_STATS");
+  return e && e[0] == '0' ? 0 : 1;
+}
+
+nnt_status nnt_attention_stats(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, float scale, int causal,
+                               float* stats, nnt_stream_t stream) {
+  NNT_TRY(check_attn(qkv, B, S, H, Dh, "nnt_attention_stats"));
+  NNT_REQUIRE(stats, NNT_ERR_NULL, "nnt_attention_stats: NULL stats");
+  NNT_REQUIRE(aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_stats: alignment");
+  const int64_t Ea = H * Dh, nblk = S / TB;
+  AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, nullptr,
+                 nullptr, l2hints_on()};
+  CUtensorMap mQ, mK;
+  const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
+  NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  NNT_TRY(make_tma_map_4d(&mK, bf, 2, q + Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
+  // algorithmic bytes: Q and K read once, the (max, sumexp) pairs written
+  const double ptiles = (double)B * H * (causal ? nblk * (nblk + 1) / 2 : nblk * nblk);
+  LaunchScope sc(NNT_K_GEMM_TC_ATTN, stream, 2.0 * B * S * Ea * 2 + 8.0 * B * H * S, ptiles * 2.0 * TB * TB * HD);
+  NNT_CUDA_TRY(set_max_dyn_smem(attn_stats_kernel, R_SMEM));
+  NNT_CUDA_TRY(::nnt::launch(attn_stats_kernel, dim3((unsigned)persistent_grid(prm.num_tasks)), dim3(kAThreadsR),
+                             (size_t)R_SMEM, (cudaStream_t)stream, prm, mQ, mK, stats));
+  return check_launch("attn_stats");
+}
 
 nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H, int64_t Dh, float scale,
                                 int causal, const float* stats, void* P, void* O, nnt_stream_t stream) {

@@ -160,6 +160,9 @@ nnt_status run_fwd_op(const Ctx& x, int op, const nnt_block_params* p, const flo
       const int64_t sq[2] = {S * 3 * Ea, Dh}, ssc[2] = {H * S * S, S * S};
       e.causal = x.c.causal ? NNT_CAUSAL_OUT_LOWER : NNT_CAUSAL_NONE;
       uint8_t* q = x.s<uint8_t>(x.L.qkv);
+      if (x.fused_attn && nnt_attention_stats_enabled())  // R26 in the fused attention pipeline
+        return nnt_attention_stats(x.s<void>(x.L.qkv), B, S, H, Dh, x.inv_sqrt_dh, x.c.causal, x.s<float>(x.L.stats),
+                                   x.st);
       if (dt == NNT_BF16) {
         // R26: the score tiles stay on chip; subroutine 1 and its aggregation over all key tiles
         // of a row run in the GEMM epilogue, producing the slice stats directly

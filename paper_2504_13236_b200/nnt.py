@@ -50,6 +50,7 @@ EXPORTS = ("nnt_abi_version", "nnt_last_error", "nnt_device_check", "nnt_tile_gr
            "nnt_op_name", "nnt_block_dag_describe", "nnt_timing_enable", "nnt_timing_read", "nnt_timing_trace",
            "nnt_launch_count", "nnt_embedding_fwd", "nnt_embedding_bwd_scratch_bytes", "nnt_embedding_bwd",
            "nnt_cross_entropy", "nnt_attention_fused_supported", "nnt_attention_fwd_pv", "nnt_attention_bwd_kv",
+           "nnt_attention_stats", "nnt_attention_stats_enabled",
            "nnt_stf_build", "nnt_attention_trace", "nnt_tp_signal", "nnt_tp_reduce_gather", "nnt_tp_wait")
 
 
@@ -147,6 +148,8 @@ _sig = {
     "nnt_stf_build": (_i32, [_i64, _i64, _vp, _vp, _vp, _vp, _vp, _vp, _i64]),
     "nnt_attention_trace": (_i32, [_i32, _vp, _i64]),
     "nnt_attention_fwd_pv": (_i32, [_vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp, _vp]),
+    "nnt_attention_stats": (_i32, [_vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp]),
+    "nnt_attention_stats_enabled": (_i32, []),
     "nnt_attention_bwd_kv": (_i32, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, C.c_float, _i32, _vp, _vp, _vp]),
     "nnt_softmax": (_i32, [_vp, _i64, _i64, _i64, _i64, _i32, _i64, _vp, _vp, _i32, _i64, _vp]),
     "nnt_softmax_bwd": (_i32, [_vp, _i32, _i64, _vp, _i64, _i64, _i64, _i32, _i64, _f32, _vp, _i32, _i64, _vp]),
@@ -354,6 +357,14 @@ def nnt_attention_trace(enable, out=None):
 
 def nnt_attention_fused_supported(S, h):
     return bool(lib.nnt_attention_fused_supported(S, h))
+
+
+def nnt_attention_stats(qkv, B, S, H, h, scale, causal, stats, stream=None):
+    return check(lib.nnt_attention_stats(ptr(qkv), B, S, H, h, scale, causal, ptr(stats), _stream(stream)))
+
+
+def nnt_attention_stats_enabled():
+    return lib.nnt_attention_stats_enabled()
 
 
 def nnt_attention_fwd_pv(qkv, B, S, H, h, scale, causal, stats, P, O, stream=None):

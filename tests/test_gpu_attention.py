@@ -46,6 +46,30 @@ def _rowstats(Q, B, S, H, scale, causal):
     return stats
 
 
+@pytest.mark.parametrize("causal", [1, 0])
+@pytest.mark.parametrize("B,S,H", [(2, 256, 3), (1, 384, 2), (2, 1024, 4)])
+def test_attention_stats_kernel(B, S, H, causal):
+    """nnt_attention_stats (softmax subroutine 1 on recomputed score tiles, R26) vs the oracle's
+    maxsumexp of the scaled scores, and vs the ROWSTATS score GEMM (both up to fp32 rounding)."""
+    E = H * H_D
+    scale = 1.0 / np.sqrt(H_D)
+    qkv, _ = _inputs(B, S, H, seed=S + H + 7 * causal)
+    Q = dev(qkv, torch.bfloat16)
+    st = torch.full((B * H * S, 2), float("nan"), device="cuda")
+    nnt.nnt_attention_stats(Q, B, S, H, H_D, scale, causal, st)
+    ref_gemm = _rowstats(Q, B, S, H, scale, causal)
+    torch.cuda.synchronize()
+    q_, k_, _ = dense.split_heads(qkv, H)
+    x = (q_ @ k_.transpose(0, 1, 3, 2)) * scale
+    if causal:
+        x = np.where(dense.causal_mask(S), x, -np.inf)
+    want_m, want_s = dense.maxsumexp(x.reshape(-1, S))  # (max, sumexp) per row
+    got = host(st)
+    close(got[:, 0], want_m, 1e-5, "max")
+    close(got[:, 1], want_s, 1e-5, "sumexp")
+    close(got, host(ref_gemm), 1e-5, "vs ROWSTATS GEMM")
+
+
 def _written(S, causal):
     """Mask of the 128 x 128 (query, key) tiles the kernels write: all, or kb <= qb."""
     t = np.arange(S) // 128
