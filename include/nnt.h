@@ -539,6 +539,15 @@ typedef struct {
   float* dx_colsum;     /* NULL or [E]: (+)= sum_t dx, the output-projection bias gradient of the
                            layer below (follows accumulate_grads) */
   void* dx_bf16;        /* NULL or bf16 [T][E]: copy of dx for the layer below (bf16 path) */
+  /* Lagged join of the side stream (with a side stream only): the side stream's ops of one layer
+   * may still run while the main stream does the layer below, when the caller alternates two
+   * scratch workspaces between layers and gives these events (NULL: join at the end of the call).
+   *   side_done:      recorded on the side stream after this call's side ops (no join);
+   *   wait_before_dx: the main stream waits on it before the LayerNorm-1 backward writes dx and
+   *                   dx_bf16 -- the previous call's side_done (its side ops read the dy and the
+   *                   bf16 copy of dy that this call's dx overwrites). */
+  nnt_event_t side_done;
+  nnt_event_t wait_before_dx;
 } nnt_block_bwd_links;
 nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_params* p, const float* x,
                                  const void* saved, void* scratch, const float* dy, float* dx,

@@ -561,7 +561,10 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
                                  {NNT_OP_QKV_DB, NNT_OP_QKV_DW, NNT_OP_QKV_DX, NNT_OP_LN1_BWD}};
   int remaining[4];
   for (int k = 0; k < 4; ++k) remaining[k] = sets[k][3] < 0 ? 3 : 4;
+  const bool lagged = side && links && links->side_done;
   for (const auto& gr : plan->groups) {
+    if (gr.op == NNT_OP_LN1_BWD && side && links && links->wait_before_dx)  // the layer above's side ops
+      NNT_CUDA_TRY(cudaStreamWaitEvent(stream, (cudaEvent_t)links->wait_before_dx, 0));  // read dy
     if (on_side(gr)) {
       if (main_advanced) {
         NNT_CUDA_TRY(cudaEventRecord(ev_fork, stream));
@@ -593,7 +596,9 @@ nnt_status nnt_block_bwd_streams(const nnt_block_cfg* cfg, const nnt_block_param
         NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)grad_ready[k], side));
       }
   }
-  if (side) {  // join: the main stream continues only after the side stream's work
+  if (lagged) {  // the caller joins later (links.side_done); its next call alternates scratch
+    NNT_CUDA_TRY(cudaEventRecord((cudaEvent_t)links->side_done, side));
+  } else if (side) {  // join: the main stream continues only after the side stream's work
     NNT_CUDA_TRY(cudaEventRecord(ev_join, side));
     NNT_CUDA_TRY(cudaStreamWaitEvent(stream, ev_join, 0));
   }

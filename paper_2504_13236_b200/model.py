@@ -174,6 +174,10 @@ class StackConfig:
     act_offload: int = 0
     # weight/bias-gradient ops of the backward on a second stream (NNT_SIDE_STREAM=0 disables)
     side_stream: bool = os.environ.get("NNT_SIDE_STREAM", "1") != "0"
+    # the side stream's join lagged by one layer (two scratch workspaces alternate between layers;
+    # NNT_SIDE_LAG=1).  Off by default: measured no gain on the GPT-2 small / XL steps;
+    # not combined with activation offload (a layer's saved slot is refilled right after its call)
+    side_lag: bool = os.environ.get("NNT_SIDE_LAG", "0") == "1"
     # train_step without DP: each bucket's optimizer update runs on an update stream as soon as the
     # backward has finished with the bucket (its grad_ready event), overlapping the rest of the
     # backward -- the DP path's schedule without the all-reduce (NNT_OVERLAP_UPDATE=0 disables)
@@ -263,8 +267,15 @@ class BlockStack:
         self.side = _distinct_stream(self.dev, used + [self.comm]) if cfg.side_stream else None
         self.cap_stream = _distinct_stream(self.dev, used + [self.comm, self.side])
         self.events = [[torch.cuda.Event() for _ in range(4)] for _ in range(cfg.L)] if self.bucketed else None
-        if self.bucketed:  # torch creates the CUDA event handles lazily, at the first record()
-            for evs in self.events:
+        # lagged side-stream join: layer l uses scratch l % 2 and records its side ops' completion in
+        # ev_side[l % 2]; the main stream waits on it before layer l - 2 reuses that scratch, and
+        # the layer below waits on it before overwriting the dy its side ops read
+        self.lag = self.side is not None and cfg.side_lag and cfg.L > 1 and not self.n_off
+        self.scratch2 = torch.zeros_like(self.scratch) if self.lag else None  # zero: split-K counters
+        self.ev_side = [torch.cuda.Event(), torch.cuda.Event()] if self.lag else None
+        created = (self.events or []) + ([self.ev_side] if self.lag else [])
+        if created:  # torch creates the CUDA event handles lazily, at the first record()
+            for evs in created:
                 for e in evs:
                     e.record()
             torch.cuda.synchronize(self.dev)
@@ -337,20 +348,30 @@ class BlockStack:
         dp = self.dp or bool(overlap_optimizer)
         assert not dp or self.events is not None, "per-bucket updates need StackConfig.overlap_update or DP"
         ah = self.act_host
+        lag = self.lag
         for l in range(self.cfg.L - 1, -1, -1):
             if ah is not None and l < self.n_off:
                 ah.before_bwd(l, compute)
             ev = self.events[l] if dp else None
             links = None
-            if self.chain:
+            scratch = self.scratch
+            if lag:
+                scratch = self.scratch if l % 2 == 0 else self.scratch2
+                if l <= self.cfg.L - 3:  # layer l + 2's side ops (same scratch) are done
+                    compute.wait_event(self.ev_side[l % 2])
+            if self.chain or lag:
                 links = nnt.nnt_block_bwd_links()
+            if lag:
+                links.side_done = self.ev_side[l % 2].cuda_event
+                links.wait_before_dx = self.ev_side[(l + 1) % 2].cuda_event if l < self.cfg.L - 1 else None
+            if self.chain:
                 done = l < self.cfg.L - 1 or top_done
                 links.dy_colsum_done = 1 if done else 0
                 links.dy_bf16 = self.dy16[cur].data_ptr() if (done and self.dy16 is not None) else None
                 if l > 0:
                     links.dx_colsum = self.view(self.g, l - 1, "b_pr").data_ptr()
                     links.dx_bf16 = self.dy16[1 - cur].data_ptr() if self.dy16 is not None else None
-            nnt.nnt_block_bwd_streams(self.bcfg, self._params[l], self.xs[l], self.saved[l], self.scratch,
+            nnt.nnt_block_bwd_streams(self.bcfg, self._params[l], self.xs[l], self.saved[l], scratch,
                                       self.dy[cur], self.dy[1 - cur], self._grads[l], 0, ev,
                                       side_stream=self.side, links=links)
             if ah is not None and l < self.n_off:
@@ -360,6 +381,8 @@ class BlockStack:
                 for si in range(4):
                     self._reduce_bucket(l, si, ev[si], overlap_optimizer)
             cur = 1 - cur
+        if lag:  # the bottom layer's side ops (the last lagged ones) before anything that follows
+            compute.wait_event(self.ev_side[0])
         if ah is not None:
             ah.join(compute)
         if dp:

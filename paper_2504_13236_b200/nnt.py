@@ -112,7 +112,7 @@ class nnt_block_grads(C.Structure):
 
 class nnt_block_bwd_links(C.Structure):
     _fields_ = [("dy_bf16", C.c_void_p), ("dy_colsum_done", C.c_int), ("dx_colsum", C.c_void_p),
-                ("dx_bf16", C.c_void_p)]
+                ("dx_bf16", C.c_void_p), ("side_done", C.c_void_p), ("wait_before_dx", C.c_void_p)]
 
 
 class nnt_block_tp(C.Structure):

@@ -194,12 +194,14 @@ def test_block_determinism_bitwise():
 
 @pytest.mark.parametrize("graph", [False, True])
 def test_side_stream_backward_bitwise(graph):
-    """nnt_block_bwd_streams: the weight/bias-gradient ops on a second stream (forked and joined
-    inside each call) give results bitwise equal to the single-stream backward."""
-    E, H, S, B, L = 768, 12, 256, 2, 2
+    """nnt_block_bwd_streams: the weight/bias-gradient ops on a second stream -- joined inside each
+    call, or (side_lag) joined one layer later with two scratch workspaces alternating between
+    layers -- give results bitwise equal to the single-stream backward (4 layers: the lagged
+    scratch reuse and the dy / dx waits all occur)."""
+    E, H, S, B, L = 768, 12, 256, 2, 4
     outs = []
-    for side in (False, True):
-        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", side_stream=side)
+    for side, lag in ((False, False), (True, False), (True, True)):
+        sc = model.StackConfig(L=L, E=E, H=H, S=S, B=B, dtype="bf16", side_stream=side, side_lag=lag)
         layers = [nnt_inputs.make_params(E, seed=11, layer=l, init="parity", n_layers=L) for l in range(L)]
         st = model.BlockStack(sc, layers)
         if graph:
@@ -210,10 +212,12 @@ def test_side_stream_backward_bitwise(graph):
             r = dev(nnt_inputs.make_r(E, S, 0, B, seed=90 + t))
             losses.append(st.train_step(x, r).item())
         torch.cuda.synchronize()
+        assert st.lag == lag
         outs.append((losses, st.g.clone(), st.w.clone(), st.dy[L % 2].clone()))
-    assert outs[0][0] == outs[1][0]
-    for a, b in zip(outs[0][1:], outs[1][1:]):
-        assert torch.equal(a, b)
+    for o in outs[1:]:
+        assert outs[0][0] == o[0]
+        for a, b in zip(outs[0][1:], o[1:]):
+            assert torch.equal(a, b)
 
 
 @pytest.mark.parametrize("dtype", ["f32", "bf16"])
