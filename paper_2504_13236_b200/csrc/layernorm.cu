@@ -2,9 +2,8 @@
 //   E <= 1024: one WARP per token row (row in registers as float4, reductions by
 //              warp shuffle only); forward warps stride over rows with the next row
 //              prefetched, backward CTAs own a block of rows (single pass);
-//   E  > 1024: forward one 128-thread CTA per row (shuffle + 4-entry shared array; a variant with
-//              4-warp groups striding over rows, the next row prefetched, measured slower at
-//              E = 1600: 16.1 vs 11.4 us);
+//   E  > 1024: forward one 128-thread CTA per row (shuffle + 4-entry shared array; the ring-fed
+//              4-warp-group variant, NNT_LN_FWD_RING=1, measured slower);
 //              backward a group of 4 or 8 warps per row, persistent CTAs (ln_bwd_groups).
 // The backward's dgamma/dbeta are per-CTA column partials (rows of a CTA are
 // accumulated in a fixed order) merged by the deterministic column merge
@@ -621,6 +620,104 @@ int pick_nv_warp(int64_t E) {
   return -1;
 }
 
+// ------------------------------------------------------------------ forward, row ring (1024 < E <= 2048)
+// The forward counterpart of ln_bwd_ring: groups of 4 warps, each with a ring of kRing x rows
+// streamed by bulk copies (kRing rows ahead), CTAs persistent over a block of rows; the row's
+// shifted sums (c = x[row][0], R9) cross the group's warps through double-buffered shared slots
+// (fixed warp order).  Same arithmetic as ln_fwd_cta up to the order of the shifted sums.
+template <typename TO, int NV>
+__global__ void __launch_bounds__(32 * kRingG * kRingGroups)
+    ln_fwd_ring(const float* __restrict__ x, int64_t T, int E, int64_t ldx, int64_t rows_per_cta,
+                const float* __restrict__ gamma, const float* __restrict__ beta, float eps, TO* __restrict__ y,
+                int64_t ldy, float* __restrict__ mean_out, float* __restrict__ rstd_out) {
+  NNT_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t ring_smem[];  // [kRingGroups][kRing] x rows
+  __shared__ float2 xs[2][kRingGroups][kRingG];
+  __shared__ __align__(8) uint64_t fullb[kRingGroups][kRing];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int grp = w / kRingG, k = w % kRingG;
+  const int E4 = E / 4;
+  const float inv_e = 1.0f / (float)E;
+  const uint32_t row_bytes = (uint32_t)E * 4u;
+  float4* const slots = reinterpret_cast<float4*>(ring_smem) + (size_t)grp * kRing * E4;
+  if (k == 0 && lane == 0)
+    for (int i = 0; i < kRing; ++i) mbar_init(smem_u32(&fullb[grp][i]), 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta;
+  const int64_t r1 = min(r0 + rows_per_cta, T);
+  auto issue = [&](int64_t n) {  // elected thread: the group's n-th row into slot n % kRing
+    const int64_t row = r0 + grp + n * kRingGroups;
+    if (row >= r1) return;
+    const int sl = (int)(n % kRing);
+    const uint32_t bar = smem_u32(&fullb[grp][sl]);
+    mbar_expect_tx(bar, row_bytes);
+    bulk_g2s(smem_u32(slots + (size_t)sl * E4), x + row * ldx, row_bytes, bar);
+  };
+  if (k == 0 && lane == 0)
+    for (int n = 0; n < kRing; ++n) issue(n);
+  float4 gm[NV], bt[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int i4 = lane + 32 * (k + kRingG * j);
+    gm[j] = i4 < E4 ? ldg4(gamma + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    bt[j] = i4 < E4 ? ldg4(beta + 4 * i4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  int buf = 0;
+  int64_t row = r0 + grp;
+  for (int64_t n = 0; row < r1; ++n, row += kRingGroups, buf ^= 1) {
+    const int sl = (int)(n % kRing);
+    mbar_wait(smem_u32(&fullb[grp][sl]), (uint32_t)((n / kRing) & 1));
+    const float4* xr = slots + (size_t)sl * E4;
+    const float c = reinterpret_cast<const float*>(xr)[0];
+    float4 v[NV];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * (k + kRingG * j);
+      if (i4 < E4) {
+        v[j] = xr[i4];
+        const float d0 = v[j].x - c, d1 = v[j].y - c, d2 = v[j].z - c, d3 = v[j].w - c;
+        s1 += (d0 + d1) + (d2 + d3);
+        s2 += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+      }
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) xs[buf][grp][k] = make_float2(s1, s2);
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(32 * kRingG) : "memory");  // also: the slot is read
+    if (k == 0 && lane == 0) issue(n + kRing);
+    s1 = 0.f;
+    s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < kRingG; ++i) {  // fixed warp order
+      const float2 t = xs[buf][grp][i];
+      s1 += t.x;
+      s2 += t.y;
+    }
+    const float ms = s1 * inv_e;
+    const float var = fmaxf(s2 * inv_e - ms * ms, 0.f);
+    const float mu = c + ms, rs = rsqrtf(var + eps);
+    if (k == 0 && lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+    TO* yr = y + row * ldy;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+      const int i4 = lane + 32 * (k + kRingG * j);
+      if (i4 < E4) store4<TO>(yr + 4 * i4, affine(v[j], gm[j], bt[j], mu, rs));
+    }
+  }
+}
+
+// NNT_LN_FWD_RING=1 selects the ring forward for 1024 < E <= 2048; off by default: measured slower
+// than the one-CTA-per-row kernel (E = 1600: 14.1 vs 11.5 us, E = 1280: 9.6 vs 9.3 us)
+bool ln_fwd_ring_on() {
+  const char* e = getenv("NNT_LN_FWD_RING");
+  return e && e[0] == '1';
+}
+
 template <typename TO>
 nnt_status launch_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, const float* g, const float* b, float eps,
                       TO* y, int64_t ldy, float* mean, float* rstd, cudaStream_t s) {
@@ -633,6 +730,26 @@ nnt_status launch_fwd(const float* x, int64_t T, int64_t E, int64_t ldx, const f
   case N: ::nnt::launch(ln_fwd_warp<TO, N>, grid, 32 * kWarpRowsPerCta, 0, s, x, T, (int)E, ldx, g, b, eps, y, ldy, mean, rstd); break;
     switch (nvw) { NNT_LNFW(1) NNT_LNFW(2) NNT_LNFW(4) NNT_LNFW(6) NNT_LNFW(8) }
 #undef NNT_LNFW
+    return check_launch("layernorm_fwd");
+  }
+  if (E <= 2048 && ln_fwd_ring_on() && (ldx * 4) % 16 == 0 && aligned16(x)) {
+    // rows streamed into shared-memory rings; persistent CTAs, 4 per SM
+    const int nvr = (int)((E / 4 + 32 * kRingG - 1) / (32 * kRingG));
+    const int64_t resident = 4 * (int64_t)num_sms();
+    int64_t rows_per = (T + resident - 1) / resident;
+    if (rows_per < kRingGroups) rows_per = kRingGroups;
+    const int64_t grid = (T + rows_per - 1) / rows_per;
+    const size_t smem_ring = (size_t)kRingGroups * kRing * E * sizeof(float);  // <= 64 KB
+    auto run = [&](auto kern) -> nnt_status {
+      NNT_CUDA_TRY(set_max_dyn_smem(kern, (int)smem_ring));
+      NNT_CUDA_TRY(::nnt::launch(kern, dim3((unsigned)grid), dim3(32 * kRingG * kRingGroups), smem_ring, s, x, T,
+                                 (int)E, ldx, rows_per, g, b, eps, y, ldy, mean, rstd));
+      return NNT_OK;
+    };
+    if (nvr == 3)
+      NNT_TRY(run(ln_fwd_ring<TO, 3>));
+    else
+      NNT_TRY(run(ln_fwd_ring<TO, 4>));
     return check_launch("layernorm_fwd");
   }
   int nv = pick_nv_cta(E);

@@ -130,7 +130,9 @@ def test_softmax_bwd(causal, pdt):
 @pytest.mark.parametrize("E,T", [(64, 96), (768, 96), (1028, 5000), (1600, 96), (1600, 5000), (2048, 5000),
                                  (2052, 96), (8192, 96)])
 @pytest.mark.parametrize("ydt", ["f32", "bf16"])
-def test_layernorm_fwd(E, T, ydt):
+@pytest.mark.parametrize("ring", ["0", "1"])
+def test_layernorm_fwd(E, T, ydt, ring, monkeypatch):
+    monkeypatch.setenv("NNT_LN_FWD_RING", ring)  # 1024 < E <= 2048: also the (opt-in) ring kernel
     rng = np.random.default_rng(E)
     x = (50.0 + 3.0 * rng.standard_normal((T, E))).astype(np.float32)  # |mean| >> std
     g = (1 + 0.1 * rng.standard_normal(E)).astype(np.float32)
