@@ -100,7 +100,12 @@ struct Cfg {
   static_assert(CTAS * TMEM_COLS <= 512, "TMEM columns per SM");
 };
 
-enum TileOrder { ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3, ORDER_ROWS = 4 };
+// ORDER_N_OUTER: consecutive tiles walk down M for one N column (B tile shared, A streamed);
+// ORDER_M_OUTER: consecutive tiles walk along N for one M row block (A shared, B streamed) -- the
+// concurrent wave then reads each block of the larger operand once instead of once per wave
+enum TileOrder {
+  ORDER_N_OUTER = 0, ORDER_TRI = 1, ORDER_HEAVY_LOW_M = 2, ORDER_HEAVY_HIGH_M = 3, ORDER_ROWS = 4, ORDER_M_OUTER = 5
+};
 
 // n / d and n % d for a runtime divisor d >= 1 and n < 2^31 with a multiply-high and a shift
 // (round-up multiplier method).  The single-thread TMA producer and MMA issuer decode a tile per
@@ -216,6 +221,11 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
     const uint32_t r = P.f_tpb.mod(tile, bz);
     nb = P.f_mt.div(r);
     mb = P.f_mt.mod(r, nb);
+  } else if (P.order == ORDER_M_OUTER) {
+    bz = P.f_tpb.div(tile);
+    const uint32_t r = P.f_tpb.mod(tile, bz);
+    mb = P.f_nt.div(r);
+    nb = P.f_nt.mod(r, mb);
   } else {
     // heaviest K-range first: the m-block level is outermost, (batch, n) inner
     const uint32_t level = P.f_level.div(tile), r = P.f_level.mod(tile, level);
@@ -1511,6 +1521,12 @@ bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
          regions <= kSplitCounters && c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
 }
 
+// Tile raster (NNT_GEMM_ORDER=0: always N-outer, the round-1 order; A/B runs)
+bool m_outer_on() {  // read per call
+  const char* e = getenv("NNT_GEMM_ORDER");
+  return !(e && e[0] == '0');
+}
+
 // Stream-K (P.sk): off by default, NNT_GEMM_SK=1 enables it; NNT_GEMM_SK_EFF sets the wave
 // efficiency (tiles / (waves x units)) below which a GEMM is scheduled stream-K (default 0.82).
 // Measured on the GPT-2 XL step (4 interleaved runs): the GEMM class 77.0 -> 75.5 ms
@@ -1572,6 +1588,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
   } else {
     P.order = a.causal == NNT_CAUSAL_A_LOWER ? ORDER_HEAVY_HIGH_M
                                              : (a.causal == NNT_CAUSAL_A_UPPER ? ORDER_HEAVY_LOW_M : ORDER_N_OUTER);
+    // non-causal: keep the LARGER operand's blocks shared by the concurrently running tiles
+    if (P.order == ORDER_N_OUTER && m_outer_on() && a.M > a.N) P.order = ORDER_M_OUTER;
     P.tiles_per_batch = P.mt * P.nt;
   }
   P.num_tiles = P.tiles_per_batch * a.batch0 * a.batch1;
@@ -1599,7 +1617,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
   P.sk_dp_tiles = P.sk_iters = 0;
   P.nkb = nkb;
   P.sk_part = nullptr;
-  if (sk_allowed && EPI == EPI_GENERIC && splits == 1 && P.order == ORDER_N_OUTER && !a.a_rowsum &&
+  if (sk_allowed && EPI == EPI_GENERIC && splits == 1 && (P.order == ORDER_N_OUTER || P.order == ORDER_M_OUTER) &&
+      !a.a_rowsum &&
       sk_pays(P.num_tiles, nkb, G_units)) {
     const int64_t full_waves = P.num_tiles / G_units;
     P.sk = 1;
