@@ -128,6 +128,11 @@ struct TcParams {
   int64_t mt, nt, tiles_per_batch, num_tiles, num_tasks;
   int64_t splits, kb_per_split;
   FastDiv f_splits, f_tpb, f_mt, f_nt, f_nbat, f_level, f_b1;  // divisors of the task decode
+  // split-K tasks split-major (task = split * num_tiles + tile): a wave runs many tiles of ONE K
+  // range, so it shares that range of both operands, instead of every K range of a few tiles
+  // (which streamed all of the narrow operand once per wave); tile-major with NNT_GEMM_SPLITMAJOR=0
+  int split_major;
+  FastDiv f_tiles;
   uint32_t idesc;
   uint32_t idesc_ones;  // a_rowsum MMA: N = 16, B (ones) K-major
   int rowsum;           // a_rowsum requested (R27)
@@ -198,8 +203,14 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
                                                 int row_off = 0, int64_t j = 0) {
   TileInfo ti;
   const uint32_t tt = (uint32_t)t;
-  const uint32_t tile = P.f_splits.div(tt);
-  ti.split = P.f_splits.mod(tt, tile);
+  uint32_t tile;
+  if (P.split_major) {
+    ti.split = P.f_tiles.div(tt);
+    tile = P.f_tiles.mod(tt, (uint32_t)ti.split);
+  } else {
+    tile = P.f_splits.div(tt);
+    ti.split = P.f_splits.mod(tt, tile);
+  }
   ti.tile = tile;
   uint32_t mb, nb, bz;
   if (P.order == ORDER_ROWS) {
@@ -1521,6 +1532,11 @@ bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
          regions <= kSplitCounters && c_tma_ok(a, sizeof(float)) && a.batch0 * a.batch1 == 1;
 }
 
+bool split_major_on() {  // NNT_GEMM_SPLITMAJOR=0: split-K tasks tile-major (A/B runs)
+  const char* e = getenv("NNT_GEMM_SPLITMAJOR");
+  return !(e && e[0] == '0');
+}
+
 // Tile raster (NNT_GEMM_ORDER=0: always N-outer, the round-1 order; A/B runs)
 bool m_outer_on() {  // read per call
   const char* e = getenv("NNT_GEMM_ORDER");
@@ -1602,6 +1618,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
   NNT_REQUIRE(P.num_tasks < (1ll << 31), NNT_ERR_UNSUPPORTED, "gemm(bf16): %lld tile tasks (> 2^31)",
               (long long)P.num_tasks);
   P.f_splits.init(P.splits);
+  P.split_major = P.splits > 1 && split_major_on() ? 1 : 0;
+  P.f_tiles.init(P.num_tiles);
   P.f_tpb.init(P.tiles_per_batch);
   P.f_mt.init(P.mt);
   P.f_nt.init(P.nt);
