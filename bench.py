@@ -506,7 +506,8 @@ def run_nnt(args):
            "loss": loss, "gpu_launches": int(launches),
            "comm": ({"backend": dist.get_backend(pg), "world_size": dist.get_world_size(pg),
                      "collective": "bucketed SUM all-reduce of the fp32 gradients on a comm stream" +
-                                   (" (ZeRO-1: reduce-scatter + all-gather)" if args.zero else "")}
+                                   (" (ZeRO-1: reduce-scatter, all-gather of bf16 weight shadows + fp32 small "
+                                    "parameters)" if args.zero else "")}
                     if world > 1 else None),
            "clocks": clocks, "roofline": roof, "kernels": kernels,
            "e2e": {"value": tokens / (e2e_ms / 1e3), "unit": "tokens/s", "h2d_bytes_per_step": h2d,
@@ -544,7 +545,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--optimizer", default="adam", choices=["adam", "sgd"], help="adam (P:194) or sgd (momentum)")
     ap.add_argument("--zero", action="store_true", help="N>1: ZeRO-1 optimizer-state sharding (reduce-scatter, "
-                    "owned-slice update, all-gather) instead of all-reduce + replicated update")
+                    "owned-slice update, all-gather of the bf16 weight shadows + fp32 small parameters) instead of "
+                    "all-reduce + replicated update")
     ap.add_argument("--offload", action="store_true", help="optimizer state in pinned host memory, streamed "
                     "through device staging slots around each update (SURVEY f4)")
     ap.add_argument("--act-offload", type=int, default=0, help="saved activations of the lowest K layers in "

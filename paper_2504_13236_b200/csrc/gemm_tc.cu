@@ -137,6 +137,9 @@ struct TcParams {
   uint32_t idesc_ones;  // a_rowsum MMA: N = 16, B (ones) K-major
   int rowsum;           // a_rowsum requested (R27)
   int a_kmajor, b_kmajor;
+  // MN-major operand through a 5-D map (make_map_blocked): all its 64-element blocks of a stage in
+  // one TMA request instead of one request per block
+  int a_blk, b_blk;
   int tma_store;  // epilogue stores through TMA (C / aux / workspace maps valid)
   int order;      // TileOrder
   int ws_mode;    // split partials go to the workspace map; bias/beta/residual applied by the reduce
@@ -155,6 +158,15 @@ struct TcParams {
   int sk;
   int64_t sk_dp_tiles, sk_iters, nkb;
   float* sk_part;
+  // Narrow tail tiles (generic epilogues, N % BN != 0): the last N column of tiles (n0 == tail_n0)
+  // runs its MMAs with N = tail_n (the column remainder rounded up to 32) instead of BN, the CTAs
+  // of a pair staging tail_n / 2 B rows each, so no tensor-core cycles go to the zero-filled
+  // columns; with tail_last (ORDER_M_OUTER) those cheap tiles are enumerated after every full
+  // tile, so they fill the persistent schedule's last round.  tail_n0 = -1: off.
+  int64_t tail_n0;
+  int tail_n, tail_last;
+  uint32_t idesc_tail;
+  FastDiv f_ntf;  // nt - 1 (tail_last)
 };
 
 // Stream-K roles of a unit's work item
@@ -235,8 +247,18 @@ __device__ __forceinline__ TileInfo decode_task(const TcParams& P, int64_t t, in
   } else if (P.order == ORDER_M_OUTER) {
     bz = P.f_tpb.div(tile);
     const uint32_t r = P.f_tpb.mod(tile, bz);
-    mb = P.f_nt.div(r);
-    nb = P.f_nt.mod(r, mb);
+    const uint32_t full = P.tail_last ? (uint32_t)(P.mt * (P.nt - 1)) : 0xffffffffu;
+    if (r >= full) {  // the narrow tail column, after every full tile; the last row blocks first
+      // (their A blocks are the ones the concurrent full tiles are streaming / most recently used)
+      mb = (uint32_t)P.mt - 1 - (r - full);
+      nb = (uint32_t)P.nt - 1;
+    } else if (P.tail_last) {
+      mb = P.f_ntf.div(r);
+      nb = P.f_ntf.mod(r, mb);
+    } else {
+      mb = P.f_nt.div(r);
+      nb = P.f_nt.mod(r, mb);
+    }
   } else {
     // heaviest K-range first: the m-block level is outermost, (batch, n) inner
     const uint32_t level = P.f_level.div(tile), r = P.f_level.mod(tile, level);
@@ -659,7 +681,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         int role;
         TileInfo ti = wk.info(P, BN, BM * CG, row_off, role);
         const int p = ti.p, q = ti.q;
-        const int nb0 = (int)ti.n0 + (int)rank * (BN / CG);  // this CTA's B rows
+        // this CTA's B rows (a narrow tail tile: tail_n / CG rows per CTA, the MMA's N / 2 each)
+        const int nb0 = (int)ti.n0 + (int)rank * ((ti.n0 == P.tail_n0 ? P.tail_n : BN) / CG);
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&empty[stage]), phase ^ 1);
           const uint32_t sa = smem_u32(smem + stage * C::STAGE_BYTES);
@@ -672,6 +695,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             const uint32_t fb = map_to_rank(fb_local, 0);
             if (P.a_kmajor) {
               tma_load_4d_pair_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+            } else if (P.a_blk) {
+              tma_load_5d_pair_w(sa, &tmA, fb, 0, k0, (int)ti.m0 / 64, q, p);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j)
@@ -679,6 +704,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             }
             if (P.b_kmajor) {
               tma_load_4d_pair_w(sb, &tmB, fb, k0, nb0, q, p);
+            } else if (P.b_blk) {
+              tma_load_5d_pair_w(sb, &tmB, fb, 0, k0, nb0 / 64, q, p);
             } else {
 #pragma unroll
               for (int j = 0; j < C::B_BLKS; ++j) tma_load_4d_pair_w(sb + j * 8192, &tmB, fb, nb0 + 64 * j, k0, q, p);
@@ -688,12 +715,16 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             mbar_expect_tx_w(fb, stage_tx);
             if (P.a_kmajor) {
               tma_load_4d_w(sa, &tmA, fb, k0, (int)ti.m0, q, p);
+            } else if (P.a_blk) {
+              tma_load_5d_w(sa, &tmA, fb, 0, k0, (int)ti.m0 / 64, q, p);
             } else {
 #pragma unroll
               for (int j = 0; j < BM / 64; ++j) tma_load_4d_w(sa + j * 8192, &tmA, fb, (int)ti.m0 + 64 * j, k0, q, p);
             }
             if (P.b_kmajor) {
               tma_load_4d_w(sb, &tmB, fb, k0, (int)ti.n0, q, p);
+            } else if (P.b_blk) {
+              tma_load_5d_w(sb, &tmB, fb, 0, k0, (int)ti.n0 / 64, q, p);
             } else {
 #pragma unroll
               for (int j = 0; j < BN / 64; ++j) tma_load_4d_w(sb + j * 8192, &tmB, fb, (int)ti.n0 + 64 * j, k0, q, p);
@@ -728,6 +759,8 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
         mbar_wait(smem_u32(&tempty[acc]), acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        // narrow tail tile: N = tail_n (the epilogue reads past it only into clipped columns >= N)
+        const uint32_t idesc = ti.n0 == P.tail_n0 ? P.idesc_tail : P.idesc;
         for (int64_t kb = ti.kb_begin; kb < ti.kb_end; ++kb) {
           mbar_wait(smem_u32(&full[stage]), phase);
           tc_fence_after();
@@ -738,9 +771,9 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
             uint64_t ad = make_sdesc(sa + kk * a_step, a_lbo, 1024u);
             uint64_t bd = make_sdesc(sb + kk * b_step, b_lbo, 1024u);
             if constexpr (CG == 2)
-              mma_bf16_pair_w(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+              mma_bf16_pair_w(tmem_d, ad, bd, idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
             else
-              mma_bf16_w(tmem_d, ad, bd, P.idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
+              mma_bf16_w(tmem_d, ad, bd, idesc, (kb > ti.kb_begin || kk > 0) ? 1u : 0u);
             if constexpr (C::ROWSUM) {
               // R27: sum_k op(A)[i][k] = op(A) x ones, into 16 columns past the two accumulators
               // (the first N tile of each row block only)
@@ -1423,6 +1456,34 @@ nnt_status make_map(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const v
   return NNT_OK;
 }
 
+// One TMA request per MN-major operand stage (make_map_blocked; NNT_GEMM_BLOCKED=0: one per
+// 64-element block, A/B runs)
+bool blocked_off() {
+  const char* e = getenv("NNT_GEMM_BLOCKED");
+  return e && e[0] == '0';
+}
+
+// MN-major operand [K][MN] (row stride ld) as {64, K, MN / 64, b1, b0}: dim 2 steps 64 elements
+// (128 B) along MN, so one box {64, box_k, nblk} stages nblk consecutive 64-element MN blocks of a
+// SW128 operand, blocks 64 * box_k * es bytes apart in shared memory.  MN % 64 == 0 only (dim 0 is
+// never clipped: a ragged MN edge could not be zero-filled).  Returns false if the driver rejects
+// the map (the caller keeps the one-request-per-block 4-D map).
+bool make_map_blocked(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t mn, int64_t k,
+                      int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_k, int nblk) {
+  if (mn % 64 != 0 || nblk < 1 || nblk > 256 || blocked_off()) return false;
+  cuuint64_t dims[5] = {64, (cuuint64_t)k, (cuuint64_t)(mn / 64), (cuuint64_t)b1, (cuuint64_t)b0};
+  int64_t st1 = b1 > 1 ? s1 : ld * k;
+  int64_t st0 = b0 > 1 ? s0 : st1 * b1;
+  cuuint64_t strides[4] = {(cuuint64_t)(ld * es), (cuuint64_t)(64 * es), (cuuint64_t)(st1 * es),
+                           (cuuint64_t)(st0 * es)};
+  cuuint32_t box[5] = {64, (cuuint32_t)box_k, (cuuint32_t)nblk, 1, 1};
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(map, dt, 5, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace
@@ -1534,6 +1595,12 @@ bool fused_reduce_ok(const GemmArgs& a, int64_t splits) {
 
 bool split_major_on() {  // NNT_GEMM_SPLITMAJOR=0: split-K tasks tile-major (A/B runs)
   const char* e = getenv("NNT_GEMM_SPLITMAJOR");
+  return !(e && e[0] == '0');
+}
+
+// Narrow tail tiles (P.tail_n0; NNT_GEMM_TAIL=0: full-width MMAs on the last N column, A/B runs)
+bool tail_on() {  // read per call
+  const char* e = getenv("NNT_GEMM_TAIL");
   return !(e && e[0] == '0');
 }
 
@@ -1667,16 +1734,44 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)((BM * CG) >> 4) << 24);
   P.idesc_ones = (1u << 4) | (1u << 7) | (1u << 10) | ((P.a_kmajor ? 0u : 1u) << 15) | ((uint32_t)(16 >> 3) << 17) |
                  ((uint32_t)((BM * CG) >> 4) << 24);
+  P.tail_n0 = -1;
+  P.tail_n = BN;
+  P.tail_last = 0;
+  P.idesc_tail = P.idesc;
+  if (generic_epi(EPI) && tail_on() && a.N % BN != 0) {
+    // K-major B: the remainder rounded up to 32 (a CTA pair stages tn / 2 rows per CTA, a multiple
+    // of 16); MN-major B: to 64 per CTA, so the pair's second half starts on a 64-element (128-byte)
+    // block of the TMA box (measured: 32-element offsets split every box row over two lines)
+    const int gran = P.b_kmajor ? 32 : 64 * CG;
+    const int tn = (int)(((a.N % BN) + gran - 1) / gran * gran);
+    if (tn < BN) {
+      P.tail_n0 = (P.nt - 1) * BN;
+      P.tail_n = tn;
+      P.idesc_tail = (P.idesc & ~(0x3Fu << 17)) | ((uint32_t)(tn >> 3) << 17);
+      // tail tiles last only with a K-major A: the dW GEMMs' (MN-major A) tail tiles re-read their
+      // A blocks from DRAM when they run apart from their row block (measured slower)
+      P.tail_last = (P.order == ORDER_M_OUTER && !P.sk && P.nt > 1 && P.a_kmajor) ? 1 : 0;
+    }
+  }
+  P.f_ntf.init(P.nt > 1 ? P.nt - 1 : 1);
   P.rowsum = a.a_rowsum != nullptr ? 1 : 0;
   NNT_REQUIRE(!P.rowsum || C::ROWSUM, NNT_ERR_UNSUPPORTED, "gemm(bf16): a_rowsum needs a tile width <= 192");
   CUtensorMap tmA, tmB, tmC, tmAux;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  P.a_blk = P.b_blk = 0;
   if (P.a_kmajor)
     NNT_TRY(make_map(&tmA, bf, 2, a.A, a.K, a.M, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, BK, BM));
+  else if (make_map_blocked(&tmA, bf, 2, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, BK, BM / 64))
+    P.a_blk = 1;
   else
     NNT_TRY(make_map(&tmA, bf, 2, a.A, a.M, a.K, a.lda, a.batch1, a.sa1, a.batch0, a.sa0, 64, BK));
+  // (MN-major B blocked only when every CTA's first B row is 64-aligned: pair halves and the
+  // narrow tail's halves are multiples of 64 then)
   if (P.b_kmajor)
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.K, a.N, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, BN / CG));
+  else if ((BN / CG) % 64 == 0 && (P.tail_n0 < 0 || (P.tail_n / CG) % 64 == 0) &&
+           make_map_blocked(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, BK, C::B_BLKS))
+    P.b_blk = 1;
   else
     NNT_TRY(make_map(&tmB, bf, 2, a.B, a.N, a.K, a.ldb, a.batch1, a.sb1, a.batch0, a.sb0, 64, BK));
   const size_t es = sizeof(TC);
@@ -1732,9 +1827,9 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
   }
   NNT_TRY(check_launch("gemm_tc"));
   if (getenv("NNT_DEBUG_GEMM"))
-    fprintf(stderr, "gemm_tc launch %lldx%lldx%lld batch %lld: BN %d CG %d EPI %d splits %lld sk %d tiles %lld\n",
+    fprintf(stderr, "gemm_tc launch %lldx%lldx%lld batch %lld: BN %d CG %d EPI %d splits %lld sk %d tiles %lld tail %d%s\n",
             (long long)a.M, (long long)a.N, (long long)a.K, (long long)(a.batch0 * a.batch1), BN, CG, EPI,
-            (long long)splits, P.sk, (long long)P.num_tiles);
+            (long long)splits, P.sk, (long long)P.num_tiles, P.tail_n0 >= 0 ? P.tail_n : 0, P.tail_last ? " last" : "");
   if (P.ws_mode && !P.fused_reduce) {
     const int64_t total = a.M * (a.N / 4);
     int64_t blocks = cdiv(total, 256);

@@ -44,25 +44,42 @@ def flat_layout(L, E, shards=1):
     [(layer, set index, begin, end)] in backward-completion order (layer L-1 first; inside a
     layer the SETS order), each bucket a contiguous slice; every tensor starts on an ALIGN
     boundary.  These buckets are the units of the DP all-reduce.
-    shards > 1 (ZeRO-1): every bucket is padded to a multiple of
-    shards * ALIGN elements, so it splits into `shards` equal ALIGN-aligned owner slices."""
+    shards > 1 (ZeRO-1): every bucket is two regions (`bucket_regions`), the
+    set's GEMM weight and then its small parameters (biases, LayerNorm), each padded to a multiple
+    of shards * ALIGN elements, so each splits into `shards` equal ALIGN-aligned owner slices:
+    the weight region is all-gathered as bf16 shadows, the small one in fp32."""
     shapes = param_shapes(E)
     offsets = [None] * L
     buckets = []
     off = 0
+    q = ALIGN * shards
     for l in range(L - 1, -1, -1):
         d = {}
         for si, names in enumerate(SETS):
             b0 = off
-            for n in names:
+            for i, n in enumerate(names):
                 numel = math.prod(shapes[n])
                 d[n] = (off, numel)
                 off += -(-numel // ALIGN) * ALIGN
-            q = ALIGN * shards
+                if shards > 1 and i == 0:  # end of the weight region
+                    off = b0 + -(-(off - b0) // q) * q
             off = b0 + -(-(off - b0) // q) * q
             buckets.append((l, si, b0, off))
         offsets[l] = d
     return offsets, buckets, off
+
+
+def bucket_regions(offsets, bucket, shards):
+    """The ZeRO-1 gather regions of a flat_layout bucket (l, si, b0, b1): [(b0, mid, True), (mid,
+    b1, False)] with [b0, mid) the set's GEMM weight (read by the kernels as a bf16 shadow on the
+    bf16 path) and [mid, b1) its biases / LayerNorm parameters (read in fp32).  Unsharded, one
+    region (b0, b1, True): its only owner updates the fp32 values of the whole bucket in place, so
+    the bf16 shadows it writes are all the (identity) gather has to move."""
+    l, si, b0, b1 = bucket
+    if shards <= 1:
+        return [(b0, b1, True)]
+    mid = offsets[l][SETS[si][1]][0]
+    return [(b0, mid, True), (mid, b1, False)]
 
 
 def zero_shards(buckets, world, rank):
@@ -81,15 +98,21 @@ def zero_shards(buckets, world, rank):
     return out, c
 
 
-def zero1_bucket(g, w, b0, b1, s0, s1, group, update):
-    """One bucket of the ZeRO-1 step: reduce-scatter the gradient slice so
-    this rank holds the SUM over ranks of its owned part (in place: the owned part of g is the
+def zero1_bucket(g, w, b0, b1, s0, s1, group, update, w16=None):
+    """One bucket (region) of the ZeRO-1 step: reduce-scatter the gradient slice
+    so this rank holds the SUM over ranks of its owned part (in place: the owned part of g is the
     NCCL in-place receive position), update the owned parameters (update(s0, s1): Adam / SGD on
-    the owned slice with the rank's compact state), all-gather the updated slices of w back
-    into every rank's replica (in place again).  The caller's current stream orders it."""
+    the owned slice with the rank's compact state), all-gather the updated slices back into every
+    rank's replica (in place again): the fp32 parameters w, or -- w16 given, a GEMM-weight region
+    on the bf16 path -- only their bf16 shadows, which the update wrote for the owned slice (half
+    the bytes; the fp32 master of a slice then lives on its owner alone, `BlockStack.gather_master`
+    rebuilds the full vector off the step).  The caller's current stream orders it."""
     torch.distributed.reduce_scatter_tensor(g[s0:s1], g[b0:b1], group=group)
     update(s0, s1)
-    torch.distributed.all_gather_into_tensor(w[b0:b1], w[s0:s1], group=group)
+    if w16 is None:
+        torch.distributed.all_gather_into_tensor(w[b0:b1], w[s0:s1], group=group)
+    else:
+        torch.distributed.all_gather_into_tensor(w16[b0:b1], w16[s0:s1], group=group)
 
 
 def _update_kernel(o, b0, b1, m, v, t, stream, shadow):
@@ -216,7 +239,9 @@ class BlockStack:
         self.g = torch.zeros(off, **f32)
         nstate = off
         if self.zero:
-            self.shards, nstate = zero_shards(self.buckets, self.world, torch.distributed.get_rank(process_group))
+            self.regions = {b[2]: bucket_regions(self.offsets, b, self.world) for b in self.buckets}
+            self.shards, nstate = zero_shards([r[:2] for b in self.buckets for r in self.regions[b[2]]], self.world,
+                                              torch.distributed.get_rank(process_group))
         self.host_state = None
         if cfg.offload:
             self.host_state = offload.HostOptimizerState(nstate, self.dev, two_moments=cfg.optimizer != "sgd")
@@ -409,11 +434,28 @@ class BlockStack:
                 self._adam_range(b0, b1, self.step_count + 1, stream=self.comm)
 
     def _zero_bucket(self, b0, b1, t):
-        s0, s1, c = self.shards[b0]
-        zero1_bucket(self.g, self.w, b0, b1, s0, s1, self.pg,
-                     lambda a, b: self._update(a, b, c, t, self.comm, shadow=False))
-        if self.bf16:  # the replicas' bf16 shadows, from the gathered fp32 parameters
-            nnt.nnt_convert(self.w[b0:b1], nnt.NNT_F32, self.w16[b0:b1], nnt.NNT_BF16, b1 - b0, stream=self.comm)
+        for r0, r1, is_w in self.regions[b0]:
+            s0, s1, c = self.shards[r0]
+            # bf16 path: the weight region's owner writes the bf16 shadows of its slice and only they
+            # are gathered; the small parameters (read in fp32) are gathered in fp32
+            shadow = self.bf16 and is_w
+            zero1_bucket(self.g, self.w, r0, r1, s0, s1, self.pg,
+                         lambda a, b, c=c, shadow=shadow: self._update(a, b, c, t, self.comm, shadow=shadow),
+                         w16=self.w16 if shadow else None)
+
+    def gather_master(self):
+        """ZeRO-1 on the bf16 path keeps the fp32 master of each weight slice on its owner only
+        (the step gathers the bf16 shadows): all-gather the fp32 weight regions so every replica's
+        `w` is the full current parameter vector again (checkpoints, tests).  Off the step path;
+        a no-op without ZeRO-1 or on the fp32 path."""
+        if not (self.zero and self.bf16):
+            return
+        torch.cuda.current_stream().wait_stream(self.comm)
+        for b in self.buckets:
+            for r0, r1, is_w in self.regions[b[2]]:
+                if is_w:
+                    s0, s1, _ = self.shards[r0]
+                    torch.distributed.all_gather_into_tensor(self.w[r0:r1], self.w[s0:s1], group=self.pg)
 
     def _hparams(self, t):
         c = self.cfg
@@ -692,6 +734,11 @@ class GPT2Model:
         self.stack.adam()
         self.step_count = self.stack.step_count
         self._adam(self.step_count)
+
+    def gather_master(self):
+        """The block stack's fp32 masters after ZeRO-1 bf16 steps (BlockStack.gather_master); the
+        shell bucket is gathered in fp32 every step (the embedding forward reads fp32 tables)."""
+        self.stack.gather_master()
 
     def train_step(self, ids=None, labels=None):
         """forward -> cross-entropy -> backward (+ DP all-reduce) -> Adam; returns the device loss."""

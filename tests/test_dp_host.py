@@ -145,6 +145,23 @@ def test_zero_shards_partition():
             cover = sorted((owned[r][0][b0][0], owned[r][0][b0][1]) for r in range(R))
             assert cover[0][0] == b0 and cover[-1][1] == b1
             assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+        # the gather regions (bf16 shadows of the GEMM weight, fp32 small parameters): each a
+        # multiple of R * ALIGN, the weight alone in the first, the rest in the second
+        for b in buckets:
+            l, si, b0, b1 = b
+            (r0, mid, w0), (m1, r1, w1) = model.bucket_regions(offsets, b, R)
+            assert (r0, r1, m1, w0, w1) == (b0, b1, mid, True, False)
+            assert (mid - b0) % (R * model.ALIGN) == 0 and (b1 - mid) % (R * model.ALIGN) == 0
+            o, k = offsets[l][model.SETS[si][0]]
+            assert o == b0 and o + k <= mid
+            assert all(mid <= offsets[l][n][0] for n in model.SETS[si][1:])
+        regions = [r[:2] for b in buckets for r in model.bucket_regions(offsets, b, R)]
+        for r in range(R):
+            sh, nst = model.zero_shards(regions, R, r)
+            assert nst * R == numel and all(s1 - s0 == (e - a) // R for (a, e), (s0, s1, _) in
+                                             zip(regions, [sh[a] for a, _ in regions]))
+    offsets1, buckets1, _ = model.flat_layout(2, 16)
+    assert model.bucket_regions(offsets1, buckets1[0], 1) == [(buckets1[0][2], buckets1[0][3], True)]
 
 
 def _zero_worker(rank, world, port, out):

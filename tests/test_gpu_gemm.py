@@ -498,3 +498,71 @@ def test_gemm_rejects_bad_arguments():
     with pytest.raises(nnt.NNTError) as e:  # mixed operand dtypes
         nnt.nnt_tile_gemm(0, 1, 64, 64, 64, None, 1.0, A, 1, 64, None, A, 0, 64, None, 0.0, A, 1, 64, None)
     assert e.value.status == nnt.NNT_ERR_DTYPE
+
+
+# Narrow tail tiles: (M, N, K, ta, tb) with N % BN != 0 -- the GPT-2 XL N = 1600 shapes (7th pair
+# tile column 64 wide), a remainder that is not a multiple of 32 (1616: 80 -> 96 / 128-wide MMAs), a
+# split-K dW shape (1600 x 1600 x 8192, MN-major operands), single-CTA tiles (M < 256)
+TAIL_SHAPES = [(8192, 1600, 1600, 0, 1), (8192, 1600, 640, 0, 0), (1024, 1616, 256, 1, 0), (640, 1560, 192, 1, 1),
+               (1600, 1600, 8192, 1, 0), (200, 1600, 128, 0, 1)]
+
+
+@pytest.mark.parametrize("shape", TAIL_SHAPES, ids=lambda s: "x".join(map(str, s)))
+def test_gemm_narrow_tail_bit_exact(shape, capfd, monkeypatch):
+    """The last N column of tiles runs N = tail_n MMAs (the remainder rounded up to 32; a CTA pair
+    stages tail_n / 2 B rows per CTA) and, M-outer, after every full tile: on integer data C must
+    equal the exact product plus bias and 2*C0 (fp32 out) / its bf16 rounding (bf16 out), exactly
+    as with full-width tail MMAs (NNT_GEMM_TAIL=0)."""
+    monkeypatch.setenv("NNT_DEBUG_GEMM", "1")
+    M, N, K, ta, tb = shape
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + N + K, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=3 * M + N + 5 * K, kind="int")
+    c0 = nnt_inputs.make_matrix((M, N), seed=9, kind="int")
+    bias = nnt_inputs.make_matrix((1, N), seed=10, kind="int")[0]
+    ws = torch.zeros(nnt.nnt_tile_gemm_workspace_bytes(M, N, K, 0), device="cuda", dtype=torch.uint8)
+    A, B, Bias = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(bias)
+    want = _op(a, ta).astype(np.float64) @ _op(b, tb).astype(np.float64)
+    lda, ldb = a.shape[1], b.shape[1]
+    for tail in ("1", "0"):
+        monkeypatch.setenv("NNT_GEMM_TAIL", tail)
+        Cm = dev(c0)
+        epi = nnt.make_epilogue(workspace=ws, bias=Bias)
+        nnt.nnt_tile_gemm(ta, tb, M, N, K, None, 1.0, A, 1, lda, None, B, 1, ldb, None, 2.0, Cm, 0, N, None, None, epi)
+        Cb = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+        nnt.nnt_tile_gemm(ta, tb, M, N, K, None, 1.0, A, 1, lda, None, B, 1, ldb, None, 0.0, Cb, 1, N, None, None,
+                          nnt.make_epilogue(workspace=ws))
+        torch.cuda.synchronize()
+        got = host(Cm)
+        assert np.array_equal(got, want + bias + 2.0 * c0), f"tail={tail} max |diff| {np.abs(got - want).max()}"
+        assert np.array_equal(host(Cb), bf16_round(want)), f"tail={tail} bf16"
+        err = capfd.readouterr().err
+        launches = [l for l in err.splitlines() if l.startswith("gemm_tc launch")]
+        assert launches, err
+        import re
+        for l in launches:
+            bn, cg = int(re.search(r" BN (\d+)", l).group(1)), int(re.search(r" CG (\d+)", l).group(1))
+            gran = 32 if tb else 64 * cg  # MN-major B: 64-element halves per CTA
+            tn = -(-(N % bn) // gran) * gran
+            if tail == "1" and N % bn and tn < bn:
+                assert f" tail {tn}" in l, l  # the narrow MMAs really ran
+            else:
+                assert " tail 0" in l, l
+
+
+@pytest.mark.parametrize("ta,tb", [(1, 0), (0, 0), (1, 1)])
+@pytest.mark.parametrize("shape", [(1600, 1600, 1024), (512, 1536, 320), (8192, 1600, 192)])
+def test_gemm_blocked_mn_major_maps_bit_exact(ta, tb, shape, monkeypatch):
+    """MN-major operands with MN % 64 == 0 are staged by ONE 5-D TMA request per stage (dims {64, K,
+    MN / 64, ...}; all the stage's 64-element blocks) instead of one request per block: on integer
+    data the product is exact either way (NNT_GEMM_BLOCKED=0 restores the 4-D maps), with the M / N
+    tails past the last whole block zero-filled by the block dimension's bound."""
+    M, N, K = shape
+    a = nnt_inputs.make_matrix((K, M) if ta else (M, K), seed=M + 7 * N + K, kind="int")
+    b = nnt_inputs.make_matrix((N, K) if tb else (K, N), seed=5 * M + N + 3 * K, kind="int")
+    want = _op(a, ta).astype(np.float64) @ _op(b, tb).astype(np.float64)
+    for blk in ("1", "0"):
+        monkeypatch.setenv("NNT_GEMM_BLOCKED", blk)
+        got = host(_run("bf16", ta, tb, M, N, K, a, b))
+        assert np.array_equal(got, want), f"blocked={blk} max |diff| {np.abs(got - want).max()}"
+        gotb = host(_run("bf16", ta, tb, M, N, K, a, b, c_dtype="bf16"))
+        assert np.array_equal(gotb, bf16_round(want)), f"blocked={blk} bf16"
