@@ -50,6 +50,8 @@ struct AttnParams {
   unsigned long long* trace;  // nnt_attention_trace: CTA 0's per-iteration event times, or NULL
   int l2hints;                // L2 policies on the TMA traffic: 0 none, 1 evict_last on the re-read tiles and
                               // evict_first on the P / dA streams, 2 (default) evict_first on the streams only
+  int p_blk;                  // backward: the P map is blocked (make_tma_map_blocked): a 128 x 128 P tile's two
+                              // 64-key halves in one TMA request
 };
 
 // Pipeline trace (nnt_attention_trace, tools): CTA 0 records %globaltimer at kTraceEv events of
@@ -778,8 +780,12 @@ __global__ void __launch_bounds__(kAThreads, 1)
         // dO_qb / Q_qb are re-read by the (b, h)'s other key-block tasks (kept in L2); P is read once
         tma_load_4d_w_hint(st, &mdO, fb, 0, qb * TB, h, b, pol_keep);
         tma_load_4d_w_hint(st + TILE16, &mQ, fb, 0, qb * TB, h, b, pol_keep);
-        tma_load_4d_w_hint(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b, pol_stream);       // keys kb*128 + 0..63
-        tma_load_4d_w_hint(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b, pol_stream);  // keys + 64..127
+        if (P.p_blk) {  // both 64-key halves of the P tile in one request
+          tma_load_5d_w_hint(st + 2 * TILE16, &mP, fb, 0, qb * TB, kb * (TB / 64), h, b, pol_stream);
+        } else {
+          tma_load_4d_w_hint(st + 2 * TILE16, &mP, fb, kb * TB, qb * TB, h, b, pol_stream);       // keys kb*128 + 0..63
+          tma_load_4d_w_hint(st + 3 * TILE16, &mP, fb, kb * TB + 64, qb * TB, h, b, pol_stream);  // keys + 64..127
+        }
         if (lane == 0) trace_ev(P, 0, it_p);
         ++it_p;
         if (++stage == B_STAGES) {
@@ -1038,7 +1044,7 @@ nnt_status nnt_attention_stats(const void* qkv, int64_t B, int64_t S, int64_t H,
   NNT_REQUIRE(aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_stats: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, nullptr,
-                 nullptr, l2hints_on()};
+                 nullptr, l2hints_on(), 0};
   CUtensorMap mQ, mK;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1060,7 +1066,7 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
   NNT_REQUIRE(aligned16(P) && aligned16(O) && aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_fwd_pv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr,
-                 trace_ptr(0), l2hints_on()};
+                 trace_ptr(0), l2hints_on(), 0};
   CUtensorMap mQ, mK, mV, mPst, mO;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1089,7 +1095,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
               "nnt_attention_bwd_kv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D,
-                 trace_ptr(1), l2hints_on()};
+                 trace_ptr(1), l2hints_on(), 0};
   CUtensorMap mV, mdO, mQ, mP, mdA, mdK, mdV;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1097,7 +1103,13 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
   NNT_TRY(make_tma_map_4d(&mV, bf, 2, q + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mdO, bf, 2, dO, Dh, S, Ea, H, Dh, B, S * Ea, 64, TB));
-  NNT_TRY(make_tma_map_4d(&mP, bf, 2, P, S, S, S, H, S * S, B, H * S * S, 64, TB));
+  // NNT_ATTN_PBLK=1: one blocked request per P tile instead of two 4-D ones (measured neutral: the
+  // kernel is DRAM-bound; off by default)
+  const char* pb = getenv("NNT_ATTN_PBLK");
+  if ((pb && pb[0] == '1') && make_tma_map_blocked(&mP, bf, 2, P, S, S, S, H, S * S, B, H * S * S, TB, TB / 64))
+    prm.p_blk = 1;
+  else
+    NNT_TRY(make_tma_map_4d(&mP, bf, 2, P, S, S, S, H, S * S, B, H * S * S, 64, TB));
   NNT_TRY(make_tma_map_4d(&mdA, bf, 2, dA, S, S, S, H, S * S, B, H * S * S, 64, 32));
   NNT_TRY(make_tma_map_4d(&mdK, bf, 2, dq + Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));
   NNT_TRY(make_tma_map_4d(&mdV, bf, 2, dq + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, 32));

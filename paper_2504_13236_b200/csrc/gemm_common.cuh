@@ -65,6 +65,14 @@ nnt_status make_tma_map_4d(CUtensorMap* map, CUtensorMapDataType dt, size_t es, 
                            int64_t outer, int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_inner,
                            int box_outer);
 
+// 5-D "blocked" TMA map of an [outer][mn] operand (row stride ld) as {64, outer, mn / 64, b1, b0}:
+// one box {64, box_outer, nblk} stages nblk consecutive 64-element blocks of a row range, blocks
+// 64 * box_outer * es bytes apart in shared memory (the SW128 layout of nblk separate 2-D boxes).
+// mn % 64 == 0 only.  Returns false when not applicable or rejected (NNT_GEMM_BLOCKED=0: always).
+bool make_tma_map_blocked(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t mn,
+                          int64_t outer, int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_outer,
+                          int nblk);
+
 // Epilogue for one element: acc is sum_k op(A) op(B) of batch item (p,q), row i, col j.
 template <typename TC>
 __device__ __forceinline__ void epilogue_store(const GemmArgs& g, TC* __restrict__ Cb, TC* __restrict__ auxb,

@@ -1495,6 +1495,13 @@ nnt_status make_tma_map_4d(CUtensorMap* map, CUtensorMapDataType dt, size_t es, 
   return make_map(map, dt, es, base, inner, outer, ld, b1, s1, b0, s0, box_inner, box_outer);
 }
 
+bool make_tma_map_blocked(CUtensorMap* map, CUtensorMapDataType dt, size_t es, const void* base, int64_t mn,
+                          int64_t outer, int64_t ld, int64_t b1, int64_t s1, int64_t b0, int64_t s0, int box_outer,
+                          int nblk) {
+  if (get_encoder() != NNT_OK) return false;
+  return make_map_blocked(map, dt, es, base, mn, outer, ld, b1, s1, b0, s0, box_outer, nblk);
+}
+
 // Split-K factor for a GEMM: fp32 C, no activation, unbatched, non-causal, an output grid
 // that leaves SMs idle and a K long enough to cut (>= 8 K-blocks per split).
 namespace {

@@ -200,6 +200,15 @@ __device__ __forceinline__ void tma_load_5d_w(uint32_t dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d_w_hint(uint32_t dst, const CUtensorMap* map, uint32_t bar, int c0, int c1,
+                                                   int c2, int c3, int c4, uint64_t policy) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t" NNT_ELECT
+      "@e cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
+      "%4, %5, %6, %7}], [%2], %8;\n\t}" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_5d_pair_w(uint32_t dst, const CUtensorMap* map, uint32_t bar_cluster, int c0,
                                                    int c1, int c2, int c3, int c4) {
   asm volatile(
