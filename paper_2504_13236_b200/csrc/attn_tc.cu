@@ -52,6 +52,7 @@ struct AttnParams {
                               // evict_first on the P / dA streams, 2 (default) evict_first on the streams only
   int p_blk;                  // backward: the P map is blocked (make_tma_map_blocked): a 128 x 128 P tile's two
                               // 64-key halves in one TMA request
+  int bgroup;                 // backward: key-block levels interleaved per (b, h) in groups of bgroup (1: level-major)
 };
 
 // Pipeline trace (nnt_attention_trace, tools): CTA 0 records %globaltimer at kTraceEv events of
@@ -179,8 +180,9 @@ __global__ void __launch_bounds__(kAThreadsF, 1)
   const uint32_t tmem = *tmem_slot;
   NNT_PDL_ENTRY();
   // task t (heaviest first): level = t / BH -> query block qb = nblk - 1 - level; bh = t % BH
-  auto decode = [&](int64_t t, int& qb, int& b, int& h) {
-    const int level = (int)(t / BH), bh = (int)(t % BH);
+  auto decode = [&](int64_t t, int& qb, int& b, int& h) {  // (bgroup: levels interleaved per (b, h))
+    const int g = P.bgroup;
+    const int level = (int)(t / ((int64_t)g * BH)) * g + (int)(t % g), bh = (int)((t / g) % BH);
     qb = P.nblk - 1 - level;
     b = bh / P.H;
     h = bh % P.H;
@@ -518,7 +520,8 @@ __global__ void __launch_bounds__(kAThreadsR, 1)
   const uint32_t tmem = *tmem_slot;
   NNT_PDL_ENTRY();
   auto decode = [&](int64_t t, int& qb, int& b, int& h) {  // heaviest first, as the forward
-    const int level = (int)(t / BH), bh = (int)(t % BH);
+    const int g = P.bgroup;
+    const int level = (int)(t / ((int64_t)g * BH)) * g + (int)(t % g), bh = (int)((t / g) % BH);
     qb = P.nblk - 1 - level;
     b = bh / P.H;
     h = bh % P.H;
@@ -744,8 +747,11 @@ __global__ void __launch_bounds__(kAThreads, 1)
   const uint32_t tmem = *tmem_slot;
   NNT_PDL_ENTRY();
   // task t (heaviest first): level = t / BH -> key block kb = level (causal: nblk - kb query blocks)
+  // bgroup g > 1: levels [j g, (j+1) g) of one (b, h) are consecutive tasks, so they run at the same
+  // time and share their dO / Q tiles in L2 (level-major: a (b, h)'s next level runs ~1.4 rounds later)
   auto decode = [&](int64_t t, int& kb, int& b, int& h) {
-    const int level = (int)(t / BH), bh = (int)(t % BH);
+    const int g = P.bgroup;
+    const int level = (int)(t / ((int64_t)g * BH)) * g + (int)(t % g), bh = (int)((t / g) % BH);
     kb = level;
     b = bh / P.H;
     h = bh % P.H;
@@ -992,6 +998,14 @@ __global__ void __launch_bounds__(kAThreads, 1)
 int64_t persistent_grid(int64_t tasks) { return tasks < num_sms() ? tasks : num_sms(); }
 
 bool g_trace_on = false;
+// key / query-block levels interleaved per (b, h) in groups of g (attention kernels' task order;
+// NNT_ATTN_FGROUP: forward / statistics, NNT_ATTN_BGROUP: backward; 1 = level-major)
+int attn_group(const char* var, int64_t nblk) {
+  const char* e = getenv(var);
+  const int g = e ? atoi(e) : 1;
+  return (g > 1 && nblk % g == 0) ? g : 1;
+}
+
 int l2hints_on() {  // read per call (A/B runs switch it within one process)
   const char* e = getenv("NNT_ATTN_L2HINT");
   return e ? atoi(e) : 2;
@@ -1044,7 +1058,7 @@ nnt_status nnt_attention_stats(const void* qkv, int64_t B, int64_t S, int64_t H,
   NNT_REQUIRE(aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_stats: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, nullptr,
-                 nullptr, l2hints_on(), 0};
+                 nullptr, l2hints_on(), 0, attn_group("NNT_ATTN_FGROUP", nblk)};
   CUtensorMap mQ, mK;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1066,7 +1080,7 @@ nnt_status nnt_attention_fwd_pv(const void* qkv, int64_t B, int64_t S, int64_t H
   NNT_REQUIRE(aligned16(P) && aligned16(O) && aligned16(stats), NNT_ERR_ALIGN, "nnt_attention_fwd_pv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, stats, nullptr,
-                 trace_ptr(0), l2hints_on(), 0};
+                 trace_ptr(0), l2hints_on(), 0, attn_group("NNT_ATTN_FGROUP", nblk)};
   CUtensorMap mQ, mK, mV, mPst, mO;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1095,7 +1109,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
               "nnt_attention_bwd_kv: alignment");
   const int64_t Ea = H * Dh, nblk = S / TB;
   AttnParams prm{(int)B, (int)H, (int)S, (int)nblk, (int)(B * H * nblk), causal ? 1 : 0, scale, nullptr, D,
-                 trace_ptr(1), l2hints_on(), 0};
+                 trace_ptr(1), l2hints_on(), 0, 1};
   CUtensorMap mV, mdO, mQ, mP, mdA, mdK, mdV;
   const CUtensorMapDataType bf = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   const __nv_bfloat16* q = (const __nv_bfloat16*)qkv;
@@ -1103,6 +1117,7 @@ nnt_status nnt_attention_bwd_kv(const void* qkv, const void* dO, const void* P, 
   NNT_TRY(make_tma_map_4d(&mV, bf, 2, q + 2 * Ea, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mQ, bf, 2, q, Dh, S, 3 * Ea, H, Dh, B, S * 3 * Ea, 64, TB));
   NNT_TRY(make_tma_map_4d(&mdO, bf, 2, dO, Dh, S, Ea, H, Dh, B, S * Ea, 64, TB));
+  prm.bgroup = attn_group("NNT_ATTN_BGROUP", nblk);
   // NNT_ATTN_PBLK=1: one blocked request per P tile instead of two 4-D ones (measured neutral: the
   // kernel is DRAM-bound; off by default)
   const char* pb = getenv("NNT_ATTN_PBLK");

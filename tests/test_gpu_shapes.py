@@ -98,3 +98,51 @@ def test_bench_config_full_gpt2_sampled_sequences():
         _, cache = dense.gpt2_fwd(om, tok[j:j + 1, :S], tok[j:j + 1, 1:], H)
         want, _ = dense.cross_entropy(cache["logits"], tok[j, 1:])
         close(rows[j], want, 2e-2, j)
+
+
+@pytest.mark.timeout(1500)
+def test_xl_bench_shape_block_every_gradient():
+    """One GPT-2 XL block at the exact per-layer shapes the default bench times (E=1600, H=25, B=8,
+    S=1024: T = 8192 tokens, so the dW GEMMs run K = 8192, the N = 1600 GEMMs their narrow tail
+    tiles after the full ones, the MN-major operands the blocked TMA maps), GPT-2 init, one
+    CUDA-graph training step (forward, probe loss, backward, Adam): y, dx, every parameter
+    gradient and the Adam step against the fp64 oracle on the same batch, norm-wise and
+    element-wise (reading R32)."""
+    import bench
+    _, E, H, S, B = bench.CONFIGS["xl"]
+    assert (E, H, S, B) == (1600, 25, 1024, 8)
+    sc = model.StackConfig(L=1, E=E, H=H, S=S, B=B, dtype="bf16")
+    layers = [nnt_inputs.make_params(E, seed=2468, layer=0, init="gpt2", n_layers=48)]
+    st = model.BlockStack(sc, layers)
+    st.enable_graph()
+    x = nnt_inputs.make_x(E, S, 0, B, seed=1357)
+    r = nnt_inputs.make_r(E, S, 0, B, seed=1357)
+    w0 = {n: host(v).astype(np.float64) for n, v in st.params_of(0).items()}
+    st.train_step(dev(x), dev(r))
+    torch.cuda.synchronize()
+    got_y, got_dx = host(st.xs[-1]), host(st.dy[1])  # L = 1: backward's dx lands in dy[1]
+    got_g = {n: host(v) for n, v in st.grads_of(0).items()}
+    got_w = {n: host(v).astype(np.float64) for n, v in st.params_of(0).items()}
+    used = _used(layers[0])
+    del st, layers
+    torch.cuda.empty_cache()
+    y_ref, cache = dense.block_fwd(used, x, H)
+    close(got_y, y_ref, 2e-2, "y")
+    dx_ref, g_ref = dense.block_bwd(used, cache, dense.probe_loss_grad(r, B * S))
+    del cache
+    close(got_dx, dx_ref, 2e-2, "dx")
+    for n, gv in got_g.items():
+        if n == "b_qkv":  # the key-bias gradient is exactly zero in exact arithmetic (reading R22)
+            close(np.delete(gv, np.s_[E:2 * E]), np.delete(g_ref[n], np.s_[E:2 * E]), 2e-2, n)
+            assert np.abs(gv[E:2 * E]).max() <= 1e-3 * np.abs(g_ref[n]).max()
+        else:
+            close(gv, g_ref[n], 2e-2, n)
+    # Adam step 1 from zero moments: w1 - w0 = -lr * g / (|g| + eps) elementwise (sign step), so
+    # compare the update on the elements whose oracle gradient is clearly non-zero
+    for n in got_w:
+        w1, _, _ = dense.adam_step(w0[n], g_ref[n], np.zeros_like(w0[n]), np.zeros_like(w0[n]), 1)
+        keep = np.abs(g_ref[n]) > 5e-2 * np.abs(g_ref[n]).max()
+        if n == "b_qkv":
+            keep[E:2 * E] = False
+        d_got, d_want = (got_w[n] - w0[n])[keep], (w1 - w0[n])[keep]
+        close(d_got, d_want, 2e-2, f"adam {n}")
