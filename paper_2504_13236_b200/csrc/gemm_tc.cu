@@ -1938,6 +1938,20 @@ int choose_bn_pair(const GemmArgs& a, size_t es_c, double* cost_out, bool sk = f
     *cost_out = 0;
     return atoi(f);
   }
+  // Measured exception: a K-major B whose 256-wide pair tiles fill their rounds badly (< 70 %: GPT-2
+  // small's N = 768 projection, 96 tiles on 74 pairs) takes 192-wide pairs (128 tiles: 86 %): small
+  // proj 54 -> 47 us.  Not for MN-major B (a 96-row half over-fetches a 64-column block) nor for the
+  // milder XL case (N = 1600: 76 %, measured slower).  NNT_GEMM_192_EXC=0 disables it.
+  if (a.tb == NNT_TRANS && a.batch0 * a.batch1 == 1 && a.N % 192 == 0 && !getenv("NNT_GEMM_192")) {
+    const char* e = getenv("NNT_GEMM_192_EXC");
+    const int64_t units = pair_units(), t256 = cdiv(a.M, 2 * BM) * cdiv(a.N, 256), t192 = cdiv(a.M, 2 * BM) * (a.N / 192);
+    const double eff256 = (double)t256 / (double)(cdiv(t256, units) * units);
+    const double eff192 = (double)t192 / (double)(cdiv(t192, units) * units);
+    if (!(e && e[0] == '0') && eff256 < 0.7 && eff192 > 0.8) {
+      *cost_out = tile_cost(a, 192, 2, units, es_c, sk);
+      return 192;
+    }
+  }
   int best = 256;
   double best_cost = 1e300;
   for (int bn : cands) {

@@ -566,3 +566,35 @@ def test_gemm_blocked_mn_major_maps_bit_exact(ta, tb, shape, monkeypatch):
         assert np.array_equal(got, want), f"blocked={blk} max |diff| {np.abs(got - want).max()}"
         gotb = host(_run("bf16", ta, tb, M, N, K, a, b, c_dtype="bf16"))
         assert np.array_equal(gotb, bf16_round(want)), f"blocked={blk} bf16"
+
+
+@pytest.mark.parametrize("shape", [(8192, 768, 3072), (2048, 576, 320)], ids=lambda s: "x".join(map(str, s)))
+def test_gemm_pair192_exception_bit_exact(shape, capfd, monkeypatch):
+    """K-major-B GEMMs whose 256-wide CTA-pair tiles fill under 70 % of their rounds (GPT-2 small's
+    N = 768 projection: 96 tiles on 74 pairs) run on 192-wide pair tiles (96 B rows per CTA): on
+    integer data with bias, 2*C0 and an fp32 residual the product is exact with the exception on and
+    off (NNT_GEMM_192_EXC=0: 256-wide tiles)."""
+    monkeypatch.setenv("NNT_DEBUG_GEMM", "1")
+    M, N, K = shape
+    a = nnt_inputs.make_matrix((M, K), seed=M + N + 2 * K, kind="int")
+    b = nnt_inputs.make_matrix((N, K), seed=7 * M + N + K, kind="int")
+    c0 = nnt_inputs.make_matrix((M, N), seed=19, kind="int")
+    bias = nnt_inputs.make_matrix((1, N), seed=20, kind="int")[0]
+    res = nnt_inputs.make_matrix((M, N), seed=21, kind="int")
+    A, B, Bias, Res = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(bias), dev(res)
+    want = a.astype(np.float64) @ b.astype(np.float64).T + bias + 2.0 * c0 + res
+    import re
+    seen = {}
+    for exc in ("1", "0"):
+        monkeypatch.setenv("NNT_GEMM_192_EXC", exc)
+        Cm = dev(c0)
+        epi = nnt.make_epilogue(bias=Bias, residual=Res, ld_residual=N)
+        nnt.nnt_tile_gemm(0, 1, M, N, K, None, 1.0, A, 1, K, None, B, 1, K, None, 2.0, Cm, 0, N, None, None, epi)
+        torch.cuda.synchronize()
+        got = host(Cm)
+        assert np.array_equal(got, want), f"exc={exc} max |diff| {np.abs(got - want).max()}"
+        launches = [l for l in capfd.readouterr().err.splitlines() if l.startswith("gemm_tc launch")]
+        seen[exc] = [(int(re.search(r" BN (\d+)", l).group(1)), int(re.search(r" CG (\d+)", l).group(1)))
+                     for l in launches]
+    if M == 8192:  # the GPT-2 small projection shape takes the exception
+        assert seen["1"] == [(192, 2)] and seen["0"] != [(192, 2)], seen
