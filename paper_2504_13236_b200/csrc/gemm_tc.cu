@@ -440,7 +440,10 @@ __device__ __forceinline__ void ld8(const __nv_bfloat16* p, float* o, bool cg) {
 // The streamed (prefetched) epilogue input of a GEMM: at most one, element type = C's.
 // IN_AUX_SMEM: the aux chunk is TMA-loaded into the chunk's staging buffer at tile start
 // (before the accumulator wait) and read from shared memory; the output overwrites it in place.
-enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3, IN_AUX_SMEM = 4 };
+// IN_RES_SMEM: the same for an fp32 residual, with more chunks per warp and tile than staging
+// buffers: the first kStageBufs chunks load at tile start, chunk i + kStageBufs into buffer
+// i % kStageBufs once chunk i's store has read it.
+enum InKind { IN_NONE = 0, IN_AUX = 1, IN_RESIDUAL = 2, IN_COLD = 3, IN_AUX_SMEM = 4, IN_RES_SMEM = 5 };
 
 // The W pre-activation outputs of one row chunk (GELU is applied by the caller after
 // staging the pre-activation).  vec: operands 16-byte aligned with 16-byte pitches.
@@ -1093,11 +1096,29 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
       };
       // (fp32 C only: a bf16 chunk already holds 64 live values, a prefetch buffer would spill)
       auto can_stream = [&](int c) {
-        return sizeof(TC) == 4 && P.in_kind != IN_NONE && vec && row < g.M && c < BN && ti.n0 + c + W <= g.N &&
-               role != SK_WRITER;
+        return sizeof(TC) == 4 && P.in_kind != IN_NONE && P.in_kind != IN_RES_SMEM && vec && row < g.M && c < BN &&
+               ti.n0 + c + W <= g.N && role != SK_WRITER;
       };
       Raw8 raw;
       if (can_stream(half * W)) raw_load(raw, in_ptr(half * W));  // overlaps the wait for the MMAs
+      // IN_*_SMEM: this warp's input chunk c of the tile -> staging buffer b (TMA, inbar[b])
+      auto in_load = [&](int c, int b) {
+        const uint32_t bar = smem_u32(&inbar[(warp - 2) * kStageBufs + b]);
+        mbar_expect_tx(bar, kStageBytesPerWarp);
+        tma_load_4d(smem_u32(stage_base + b * kStageBytesPerWarp), &tmAux, bar, (int)(ti.n0 + c),
+                    (int)(ti.m0 + quad * 32), (int)q, (int)p);
+      };
+      const bool in_smem = (P.in_kind == IN_AUX_SMEM || P.in_kind == IN_RES_SMEM) && role != SK_WRITER;
+      if (P.in_kind == IN_RES_SMEM && role != SK_WRITER) {
+        // the first kStageBufs residual chunks of the tile, before the accumulator wait
+        if (lane == 0) {
+          bulk_wait_read0();  // earlier TMA stores have finished reading the buffers
+          int i = 0;
+          for (int c = half * W; c < BN && ti.n0 + c < g.N && i < kStageBufs; c += 2 * W, ++i) in_load(c, i);
+        }
+        __syncwarp();
+        ring = 0;
+      }
       if (P.in_kind == IN_AUX_SMEM && role != SK_WRITER) {
         // TMA-load this warp's aux chunks of the tile into its staging buffers (chunk i ->
         // buffer i) before the accumulator wait, so the loads overlap the MMAs
@@ -1181,11 +1202,12 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           continue;
         }
         int kind = can_stream(c) ? P.in_kind : IN_NONE;
-        if (P.in_kind == IN_AUX_SMEM) {  // the aux chunk landed in staging buffer ci (== ring)
-          mbar_wait(smem_u32(&inbar[(warp - 2) * kStageBufs + ci]), (in_phase >> ci) & 1u);
-          in_phase ^= 1u << ci;
-          unstage_row(raw, stage_base + ci * kStageBytesPerWarp, lane);
-          kind = IN_AUX;
+        const int ib = ci % kStageBufs;  // IN_*_SMEM: the chunk's staging buffer (== ring)
+        if (in_smem) {  // the input chunk landed in staging buffer ib
+          mbar_wait(smem_u32(&inbar[(warp - 2) * kStageBufs + ib]), (in_phase >> ib) & 1u);
+          in_phase ^= 1u << ib;
+          unstage_row(raw, stage_base + ib * kStageBytesPerWarp, lane);
+          kind = P.in_kind == IN_AUX_SMEM ? IN_AUX : IN_RESIDUAL;
         }
         epi_math<TC, W>(g, Cb, auxb, row, ti.n0 + c, true, vec, dval, kind, raw, v);
         if (can_stream(c + 2 * W)) raw_load(raw, in_ptr(c + 2 * W));  // next chunk's input, in flight meanwhile
@@ -1229,6 +1251,15 @@ __global__ void __launch_bounds__(kThreads, (Cfg<BN, CG, EPI>::CTAS))
           stage_store(&tmC);
         else
           direct_store<TC, W>(g.M, g.N, g.ldc, scatter_row_base(g, Cb, row), row, ti.n0 + c, v);
+        if (in_smem && P.in_kind == IN_RES_SMEM) {
+          // refill buffer ib with chunk ci + kStageBufs once this chunk's store has read it
+          const int cn = c + 2 * W * kStageBufs;
+          if (lane == 0 && cn < BN && ti.n0 + cn < g.N) {
+            bulk_wait_read0();
+            in_load(cn, ib);
+          }
+          __syncwarp();
+        }
       }
       if constexpr (C::ROWSUM) {
         // R27: this row's sum of op(A) over the task's K range (one warp per lane quadrant)
@@ -1605,6 +1636,12 @@ bool split_major_on() {  // NNT_GEMM_SPLITMAJOR=0: split-K tasks tile-major (A/B
   return !(e && e[0] == '0');
 }
 
+// fp32 residual chunks staged by TMA (IN_RES_SMEM; NNT_GEMM_RES_SMEM=0: register prefetch, A/B runs)
+bool res_smem_on() {
+  const char* e = getenv("NNT_GEMM_RES_SMEM");
+  return !(e && e[0] == '0');
+}
+
 // Narrow tail tiles (P.tail_n0; NNT_GEMM_TAIL=0: full-width MMAs on the last N column, A/B runs)
 bool tail_on() {  // read per call
   const char* e = getenv("NNT_GEMM_TAIL");
@@ -1732,7 +1769,10 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
                     ? IN_AUX_SMEM  // bf16: the register prefetch would spill; stage it through smem
                     : IN_AUX;
   else if (a.residual && sizeof(TC) == 4)
-    P.in_kind = IN_RESIDUAL;
+    P.in_kind = res_smem_on() && c_tma_ok(a, sizeof(TC)) && aligned16(a.residual) && a.ld_res % 4 == 0 &&
+                        a.batch0 * a.batch1 == 1
+                    ? IN_RES_SMEM  // TMA-staged residual chunks (NNT_GEMM_RES_SMEM=0: register prefetch)
+                    : IN_RESIDUAL;
   else if (a.beta != 0.f)
     P.in_kind = IN_COLD;
   else
@@ -1805,6 +1845,8 @@ nnt_status launch_bn(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk_
       NNT_TRY(make_map(&tmC, cdt, es, a.C, a.N, a.M, a.ldc, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
       if (a.act == NNT_ACT_GELU || P.in_kind == IN_AUX_SMEM || EPI == EPI_DA)  // GELU out / GELU', P in
         NNT_TRY(make_map(&tmAux, cdt, es, a.aux, a.N, a.M, a.ld_aux, a.batch1, a.sc1, a.batch0, a.sc0, W, 32));
+      if (P.in_kind == IN_RES_SMEM)  // the fp32 residual, staged chunk by chunk
+        NNT_TRY(make_map(&tmAux, cdt, es, a.residual, a.N, a.M, a.ld_res, 1, 0, 1, 0, W, 32));
     }
   }
   if constexpr (CG == 1) {

@@ -598,3 +598,30 @@ def test_gemm_pair192_exception_bit_exact(shape, capfd, monkeypatch):
                      for l in launches]
     if M == 8192:  # the GPT-2 small projection shape takes the exception
         assert seen["1"] == [(192, 2)] and seen["0"] != [(192, 2)], seen
+
+
+@pytest.mark.parametrize("shape", [(8192, 1600, 1600), (8192, 768, 3072), (1000, 1560, 256), (640, 320, 2048)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_gemm_residual_tma_staged_bit_exact(shape, monkeypatch):
+    """The fp32 residual of the out-projection / projection epilogues TMA-staged chunk by chunk through
+    the epilogue warps' staging buffers (IN_RES_SMEM: 3-4 chunks per warp and tile over 2 buffers,
+    each refilled once its chunk's store has read it): on integer data with bias, 2*C0 and the
+    residual, C is exact with the staged path and with the register prefetch (NNT_GEMM_RES_SMEM=0),
+    for CTA-pair and single-CTA tiles and ragged M / N edges."""
+    M, N, K = shape
+    a = nnt_inputs.make_matrix((M, K), seed=3 * M + N + K, kind="int")
+    b = nnt_inputs.make_matrix((N, K), seed=M + 5 * N + K, kind="int")
+    c0 = nnt_inputs.make_matrix((M, N), seed=29, kind="int")
+    bias = nnt_inputs.make_matrix((1, N), seed=30, kind="int")[0]
+    res = nnt_inputs.make_matrix((M, N), seed=31, kind="int")
+    A, B, Bias, Res = dev(a, torch.bfloat16), dev(b, torch.bfloat16), dev(bias), dev(res)
+    want = a.astype(np.float64) @ b.astype(np.float64).T + bias + 2.0 * c0 + res
+    for rs in ("1", "0"):
+        monkeypatch.setenv("NNT_GEMM_RES_SMEM", rs)
+        for _ in range(2):
+            Cm = dev(c0)
+            epi = nnt.make_epilogue(bias=Bias, residual=Res, ld_residual=N)
+            nnt.nnt_tile_gemm(0, 1, M, N, K, None, 1.0, A, 1, K, None, B, 1, K, None, 2.0, Cm, 0, N, None, None, epi)
+            torch.cuda.synchronize()
+            got = host(Cm)
+            assert np.array_equal(got, want), f"res_smem={rs} max |diff| {np.abs(got - want).max()}"
