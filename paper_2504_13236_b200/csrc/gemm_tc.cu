@@ -1961,6 +1961,18 @@ int forced_cg() {
   }();
   return forced;
 }
+// The out-projection-type GEMM (fp32 residual, K < 2048) with the TMA-staged residual and a narrow
+// last N column (N % 256 in (0, 128]: GPT-2 XL's N = 1600) runs fastest on 256-wide CTA pairs:
+// 47.5 us vs 52.6 (single-CTA 192) and 62 (the tile model's 128-wide pairs, which do not see the
+// narrow tail); with N a multiple of 256 (small N = 768) single-CTA tiles stay ahead (measured).
+bool out_proj_pair256(const GemmArgs& a) {
+  const char* e = getenv("NNT_GEMM_OUT_PAIR");  // NNT_GEMM_OUT_PAIR=0: the tile model's choice (A/B runs)
+  if (e && e[0] == '0') return false;
+  return forced_cg() != 1 && a.residual && a.K < 2048 && a.c_dtype == NNT_F32 && res_smem_on() && tail_on() &&
+         a.N % 256 != 0 && a.N % 256 <= 128 && a.act == NNT_ACT_NONE && a.batch0 * a.batch1 == 1 &&
+         a.causal == NNT_CAUSAL_NONE && a.M >= 2 * BM && !a.a_rowsum && c_tma_ok(a, sizeof(float)) &&
+         aligned16(a.residual) && a.ld_res % 4 == 0 && num_sms() >= 2;
+}
 bool use_pair(const GemmArgs& a) {
   if (forced_cg() == 1) return false;
   // measured exception to the model: a streamed fp32 residual with a short K (the attention
@@ -2050,6 +2062,8 @@ nnt_status launch_tc(const GemmArgs& a, cudaStream_t s, int64_t splits, bool sk 
       default: return launch_bn<192, TC, EPI_GENERIC_RS>(a, s, splits);
     }
   }
+  if (splits == 1 && !sk && !getenv("NNT_GEMM_BN") && out_proj_pair256(a))
+    return launch_bn<256, TC, EPI_GENERIC, 2>(a, s, 1, false);
   if (use_pair(a)) {
     double cost_pair = 0, cost_single = 0;
     const int bnp = choose_bn_pair(a, sizeof(TC), &cost_pair, sk);
